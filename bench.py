@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark of the per-iteration hot path (BASELINE.json metric: ADMM
+iterations/s and PSD-cone projections/s against the fp64 roofline).
+
+  python bench.py [--gpus N --steps K --warmup W] [--workload cfg2|cfg1|cfg3|cfg4]
+                  [--form primal|dual] [--impl ours|reference]
+
+A "step" is one ADMM iteration (Algorithm 1 or 2: KKT solve, all clique PSD
+projections, multiplier update, residuals) on the workload's synthetic seeded
+instance, or one full batch of PSD projections for cfg4.  Default workload:
+BASELINE configs[2] (block-arrow l=400, d=20, h=10, m=2000) -- see DESIGN.md
+"Measurement" for why this config carries the headline.  Inputs are resident
+in HBM; A (2.63 GB) is larger than L2 (126 MB), so no L2 flush is needed.
+
+Rank 0 prints ONE JSON line.  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ADMM iterations/sec and PSD cone projections/sec vs fp64 roofline"
+RHO = {("block_arrow", "primal"): 10.0, ("block_arrow", "dual"): 0.1,
+       ("maxcut", "primal"): 0.1, ("maxcut", "dual"): 10.0}   # DESIGN.md reading G11
+WL_INDEX = {"cfg0": 0, "cfg1": 1, "cfg2": 2, "cfg3": 3, "cfg4": 4}
+
+
+# ------------------------------------------------------------------ peaks
+def load_peaks():
+    p = {"hbm_gbs": 6650.0, "hbm_src": "fallback (B200_PROFILING.md)", "sm_max_mhz": 1965.0}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        p["hbm_gbs"] = float(mp["hbm_gbs"])
+        p["hbm_src"] = "measured (MEASURED_PEAKS.json copy bandwidth)"
+        p["sm_max_mhz"] = float(mp.get("sm_max_mhz", 1965.0))
+    except Exception:
+        pass
+    # FP64 (non-tensor and DMMA) peak: not in MEASURED_PEAKS.json; derived from
+    # the unit counts: 148 SMs x 64 FP64 FMA/clk x 2 flop x max SM clock.
+    p["fp64_tflops"] = 148 * 64 * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+    p["fp64_src"] = "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz"
+    return p
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.dev)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ roofline model
+def iteration_model(info, nnzA, m, s_diag):
+    """Algorithmic bytes and flops of one ADMM iteration."""
+    ks = info["_ks"]
+    N, stot = info["N"], info["stot"]
+    B = 16.0 * nnzA + (0 if s_diag else 8.0 * m * (m + 1)) + 32.0 * stot + 8.0 * stot + 48.0 * N
+    F = float(np.sum(10.0 * ks.astype(np.float64) ** 3)) + 4.0 * nnzA + (0 if s_diag else 2.0 * m * m)
+    return B, F
+
+
+def traffic_lookup(workload, kernel):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(workload, {}).get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ CPU oracle timing
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_admm_rate(prob, form, rho, iters, warm=1):
+    from oracle import admm
+    from oracle import decompose as dc
+    t0 = time.perf_counter()
+    dec = dc.decompose(prob)
+    setup = time.perf_counter() - t0
+    st = admm.step(dec, admm.zero_state(dec), rho, form, warm)
+    t0 = time.perf_counter()
+    st = admm.step(dec, st, rho, form, iters)
+    dt = time.perf_counter() - t0
+    return iters / dt, setup, dec.p
+
+
+def oracle_batch_rate(ks, vals, count):
+    from oracle import psd as opsd
+    nv = int(np.sum(ks[:count].astype(np.int64) * (ks[:count] + 1) // 2))
+    t0 = time.perf_counter()
+    opsd.project_psd_packed_batch(ks[:count], vals[:nv])
+    return count / (time.perf_counter() - t0)
+
+
+# ------------------------------------------------------------------ distributed helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def max_over_ranks(v, world, torch):
+    if world == 1:
+        return v
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, rank, world, local):
+    import torch
+    import paper_1609_06068_b200 as L
+    import sdp_inputs as gen
+
+    torch.cuda.set_device(local)
+    peaks = load_peaks()
+    stream = torch.cuda.current_stream()
+    wl = args.workload
+    idx = WL_INDEX[wl]
+    out = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (seeded generators, sdp_inputs/; DESIGN.md input recipe)"}
+    if idx == 4:
+        ks, vals = gen.config(4)
+        plan = L.PsdPlan(ks, device=local)
+        d_in = torch.from_numpy(vals).cuda()
+        d_out = torch.empty_like(d_in)
+        for _ in range(args.warmup):
+            plan.project(d_in, d_out, stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(args.steps):
+                plan.project(d_in, d_out, stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        barrier(world)
+        ms = e0.elapsed_time(e1) / args.steps
+        ms = max_over_ranks(ms, world, torch)
+        count = len(ks)
+        F = float(np.sum(10.0 * ks.astype(np.float64) ** 3))
+        B = 16.0 * vals.size
+        proj_s = world * count / (ms / 1e3)
+        achieved_tf = F / (ms / 1e3) / 1e12
+        out.update({"value": proj_s, "unit": "projections/s", "ms_per_step": ms,
+                    "config": {"workload": "cfg4_psd_batch_2e5", "count": count, "sizes": [8, 16, 32, 64],
+                               "seed": 1004, "l2": "inputs (1.1 GB in + out) larger than L2"},
+                    "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peaks["fp64_tflops"],
+                                 "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_tflops"],
+                                 "traffic": traffic_lookup(wl, "psd"), "algorithmic": "F = sum 10 k^3",
+                                 "peak_src": peaks["fp64_src"], "bytes_per_batch": B},
+                    "gpu_launches": sum(1 for _ in set(np.minimum(np.searchsorted([8, 16, 32, 64, 96], ks), 5)))
+                    * args.steps,
+                    "clocks": clk.summary()})
+        # e2e: host buffers through the C ABI, copies inside the timed region
+        h_out = np.empty_like(vals)
+        reps = max(1, min(3, args.steps))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            plan.project_host(vals, h_out)
+        e2e = world * count * reps / (time.perf_counter() - t0)
+        out["e2e"] = {"value": e2e, "unit": "projections/s", "h2d_bytes_per_step": int(vals.nbytes),
+                      "d2h_bytes_per_step": int(vals.nbytes)}
+        if rank == 0 and world == 1 and not args.no_cpu:
+            nsamp = 20000
+            r = oracle_batch_rate(ks, vals, nsamp)
+            out["cpu_baseline"] = {"value": r, "unit": "projections/s", "cores": cpu_cores(), "kind": "oracle",
+                                   "sample": f"first {nsamp} of the 2e5 matrices (numpy eigh per matrix)"}
+        return out
+
+    prob = gen.config(idx)
+    kind = prob.meta["kind"]
+    rho = args.rho if args.rho else RHO[(kind, args.form)]
+    t0 = time.perf_counter()
+    s = L.Solver(prob, form=args.form, rho=rho, device=local, stream=stream)
+    setup_wall = time.perf_counter() - t0
+    info = s.info()
+    ks = np.array([len(c) for c in s.cliques()], dtype=np.int64)
+    info["_ks"] = ks
+    s.step(args.warmup)
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        s.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(ms, world, torch)
+    it_s = world * 1e3 / ms
+    fin = s.info()
+    nnzA = prob.a_val.size if prob.a_fmt == "dense" else prob.a_val.size
+    B, F = iteration_model(info, nnzA, prob.m, info["s_diagonal"])
+    t_roof = max(B / (peaks["hbm_gbs"] * 1e9), F / (peaks["fp64_tflops"] * 1e12))
+    # per-phase device times (CUDA events on the launching stream), live
+    phases = s.profile_phases(min(args.steps, 50))
+    dom = max(phases, key=phases.get)
+    N, m, stot = info["N"], prob.m, info["stot"]
+    npat = prob.a_row.size
+    if dom in ("gemv", "gemvT") and prob.a_fmt == "dense":
+        # algorithmic bytes per launch: A once (8 m npat) + the N-vectors it touches
+        byts = 8.0 * m * npat + (8.0 * N if dom == "gemv" else 8.0 * 3 * N + 8.0 * m)
+        achieved = byts / (phases[dom] / 1e3) / 1e9
+        roof = {"bound": "hbm", "kernel": f"k_{dom}_dense", "achieved": achieved, "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic_lookup(wl, dom),
+                "algorithmic_bytes_per_launch": byts, "peak_src": peaks["hbm_src"]}
+    else:
+        fl = float(np.sum(10.0 * ks.astype(np.float64) ** 3))
+        achieved = fl / (phases[dom] / 1e3) / 1e12
+        roof = {"bound": "fp64", "kernel": f"phase:{dom}", "achieved": achieved, "peak": peaks["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"], "traffic": traffic_lookup(wl, dom),
+                "algorithmic_flops_per_launch": fl, "peak_src": peaks["fp64_src"]}
+    total_phase = sum(phases.values())
+    roof["share_of_step"] = phases[dom] / total_phase if total_phase > 0 else None
+    out.update({
+        "value": it_s, "unit": "iterations/s", "ms_per_step": ms,
+        "projections_per_s": it_s * info["p"],
+        "config": {"workload": prob.name, "form": args.form, "rho": rho, "n": prob.n, "m": prob.m,
+                   "N": N, "p": info["p"], "kmin": info["kmin"], "kmax": info["kmax"], "stot": stot,
+                   "seed": prob.meta.get("seed"),
+                   "l2": "inputs larger than L2 (A = %.2f GB vs 126 MB L2)" % (8.0 * nnzA / 1e9)
+                   if prob.a_fmt == "dense" else "working set (%.0f MB) re-read every step" % (B / 1e6),
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "roofline": roof,
+        "step_roofline": {"algorithmic_bytes": B, "algorithmic_flops": F, "t_roof_ms": t_roof * 1e3,
+                          "frac": t_roof * 1e3 / ms, "model": "SURVEY 8(d) / DESIGN.md Roofline"},
+        "phases_ms": phases,
+        "gpu_launches": int(fin["launches_per_iter"]) * args.steps,
+        "clocks": clk.summary(),
+        "setup_s": setup_wall,
+        "residuals_after": {"iters": fin["iters"], "eps_p": fin["eps_p"], "eps_d": fin["eps_d"],
+                            "objective": fin["objective"]},
+    })
+    # e2e through the public API: per step, sdp_step(1) + sdp_get_info (D2H of the
+    # step's result: eps_p, eps_d, objective, iteration count).
+    reps = max(5, min(args.steps, 200))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        s.step(1)
+        s.info()
+    e2e = world * reps / (time.perf_counter() - t0)
+    out["e2e"] = {"value": e2e, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 48,
+                  "note": "ADMM state is resident by design; per step the host reads the residuals"}
+    s.close()
+    if rank == 0 and world == 1 and not args.no_cpu:
+        iters = {1: 20, 2: 3, 3: 1}.get(idx, 3)
+        r, osetup, p = oracle_admm_rate(prob, args.form, rho, iters)
+        out["cpu_baseline"] = {"value": r, "unit": "iterations/s", "cores": cpu_cores(), "kind": "oracle",
+                               "sample": f"{iters} oracle iterations of the same instance after 1 warm-up "
+                                         f"(oracle setup {osetup:.1f} s not timed)"}
+    return out
+
+
+# ------------------------------------------------------------------ reference arm (the CPU oracle)
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    import sdp_inputs as gen
+    wl = args.workload
+    idx = WL_INDEX[wl]
+    steps = args.steps
+    if idx == 4:
+        ks, vals = gen.config(4)
+        per = 2000
+        t0 = time.perf_counter()
+        for _ in range(args.warmup):
+            oracle_batch_rate(ks, vals, 200)
+        t0 = time.perf_counter()
+        nsteps = max(1, min(steps, 5))
+        for _ in range(nsteps):
+            oracle_batch_rate(ks, vals, per)
+        dt = (time.perf_counter() - t0) / nsteps
+        v = per / dt
+        unit = "projections/s"
+        sample = f"each step = {per} of the 2e5 matrices; {nsteps} steps timed"
+        cfg = {"workload": "cfg4_psd_batch_2e5"}
+        ms = dt * 1e3
+    else:
+        prob = gen.config(idx)
+        kind = prob.meta["kind"]
+        rho = args.rho if args.rho else RHO[(kind, args.form)]
+        from oracle import admm
+        from oracle import decompose as dc
+        dec = dc.decompose(prob)
+        st = admm.step(dec, admm.zero_state(dec), rho, args.form, min(args.warmup, 3))
+        cap = {1: 200, 2: 20, 3: 3}.get(idx, 20)
+        nsteps = max(1, min(steps, cap))
+        t0 = time.perf_counter()
+        st = admm.step(dec, st, rho, args.form, nsteps)
+        dt = (time.perf_counter() - t0) / nsteps
+        v = 1.0 / dt
+        unit = "iterations/s"
+        sample = f"{nsteps} oracle ADMM iterations timed (of --steps {steps}; capped to bound the run)"
+        cfg = {"workload": prob.name, "form": args.form, "rho": rho, "n": prob.n, "m": prob.m}
+        ms = dt * 1e3
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": unit, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg,
+            "cpu_baseline": {"value": v, "unit": unit, "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WL_INDEX))
+    ap.add_argument("--form", default="primal", choices=["primal", "dual"])
+    ap.add_argument("--rho", type=float, default=None)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    res = run_ours(args, rank, world, local)
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,199 @@
+/*
+ * chordal_sdp.h -- C ABI of the B200-native per-iteration hot path of the
+ * chordally decomposed ADMM for sparse SDPs (arXiv 1609.06068).
+ *
+ * Citations: "P:L" = /root/reference/PAPER.md line L (LaTeX labels given too).
+ *
+ * Problem: given b in R^m, C in S^n and A_1..A_m in S^n,
+ *   primal  E:PrimalSDP  min <C,X>  s.t. A(X) = b, X PSD
+ *   dual    E:DualSDP    max <b,y>  s.t. A*(y) + Z = C, Z PSD.
+ * sdp_setup() finds the aggregate pattern, its chordal extension
+ * (exact minimum degree + symbolic elimination), the maximal cliques
+ * C_1..C_p, the entry selectors H_k, D = sum H_k^T H_k
+ * and the cached factor of S = A D^-1 A^T.  sdp_step()/sdp_solve()
+ * run Algorithm 1 (primal) or Algorithm 2 (dual) on the
+ * GPU.  sdp_project_psd_batch() exposes the clique projection P_k (E:XkUpdate,
+ * P:244-253) on its own.
+ *
+ * Conventions
+ *  - All indices are 0-based int32; matrix entries are given for the upper
+ *    triangle (row <= col) and are UNSCALED matrix values.  Internally the
+ *    library uses svec (off-diagonal x sqrt 2) over the extended pattern.
+ *  - "Host" pointers are ordinary CPU memory owned by the caller and only read
+ *    (or written, for getters) during the call.  "Device" pointers are CUDA
+ *    global memory on the handle's device, owned by the caller.
+ *  - Every call returns an int status: SDP_OK (0), SDP_MAX_ITER (1, not an
+ *    error) or a negative SDP_E_* code; sdp_last_error() gives a thread-local
+ *    message naming the offending argument.
+ *  - Handles are not thread-safe; distinct handles are independent.
+ *  - Pattern order ("canonical"): upper-triangle entries of the extended
+ *    pattern sorted by column, then row.  Clique order: cliques sorted
+ *    ascending inside, list sorted lexicographically.  Stacked clique vectors
+ *    concatenate each clique's svec in packed-upper column-major local order.
+ */
+#ifndef CHORDAL_SDP_H
+#define CHORDAL_SDP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define SDP_OK 0
+#define SDP_MAX_ITER 1             /* sdp_solve hit max_iters: not an error */
+#define SDP_E_INVALID_ARG (-1)     /* bad index, i > j, duplicate entry, n or m <= 0, ...   */
+#define SDP_E_RANK_DEFICIENT (-2)  /* S = A D^-1 A^T not positive definite          */
+#define SDP_E_CUDA (-3)            /* CUDA runtime error (message has the CUDA error string)*/
+#define SDP_E_NCCL (-4)            /* reserved: multi-GPU communication error               */
+#define SDP_E_OOM (-5)             /* device or host allocation failed                      */
+#define SDP_E_NUMERICAL (-6)       /* NaN/Inf in the iterates                       */
+#define SDP_E_STATE (-7)           /* call not valid in the handle's current state          */
+
+#define SDP_FORM_PRIMAL 0          /* Algorithm 1 */
+#define SDP_FORM_DUAL 1            /* Algorithm 2, Remark 2 ordering */
+
+#define SDP_A_COO 0                /* A given as (con, row, col, val) entries              */
+#define SDP_A_DENSE_ON_PATTERN 1   /* A given as one (row, col) list + m x npat values     */
+
+#define SDP_MAX_K 1024             /* largest clique / batch matrix order supported         */
+
+/* ---- problem data ------------------------------------------- */
+typedef struct {
+  int32_t n;                 /* order of C, A_i (cone S^n)                          */
+  int32_t m;                 /* number of equality constraints                      */
+  /* C: upper-triangle COO, c_nnz entries, (c_row[t] <= c_col[t]) */
+  int64_t c_nnz;
+  const int32_t* c_row;
+  const int32_t* c_col;
+  const double* c_val;
+  /* A_1..A_m */
+  int32_t a_fmt;             /* SDP_A_COO or SDP_A_DENSE_ON_PATTERN                  */
+  int64_t a_nnz;             /* COO: number of entries; DENSE: number of pattern entries npat */
+  const int32_t* a_con;      /* COO: constraint index in [0,m) per entry; DENSE: unused (NULL) */
+  const int32_t* a_row;      /* COO: per entry; DENSE: per pattern entry             */
+  const int32_t* a_col;
+  const double* a_val;       /* COO: a_nnz values; DENSE: m x npat row-major values  */
+  const double* b;           /* m values                                             */
+  /* optional user pattern E ("described by the graph G(V,E)"), may be NULL */
+  int64_t e_nnz;
+  const int32_t* e_row;
+  const int32_t* e_col;
+} sdp_problem;
+
+typedef struct {
+  int32_t form;              /* SDP_FORM_PRIMAL or SDP_FORM_DUAL                     */
+  double rho;                /* ADMM penalty rho > 0; default 1.0     */
+  int32_t device;            /* CUDA device ordinal; default 0                        */
+  void* stream;              /* cudaStream_t to enqueue on (NULL = library-owned)    */
+  int32_t check_every;       /* sdp_solve: host reads the stop flag every K iterations (default 10) */
+  int32_t use_graph;         /* 1 (default): replay one captured CUDA graph per iteration */
+  int32_t rank, world;       /* reserved for clique sharding; must be 0, 1           */
+} sdp_options;
+
+typedef struct {
+  int64_t iters;             /* iterations run since the last reset                 */
+  double eps_p, eps_d;       /* residuals of the last iteration (reading G9) */
+  double objective;          /* primal <c,x> / dual <b,y> of the last iteration (G17) */
+  double setup_s;            /* host wall time of sdp_setup                          */
+  int64_t n, m, N, p;        /* sizes: pattern coordinates N, cliques p              */
+  int64_t kmin, kmax, stot;  /* clique order range, stacked clique length sum k(k+1)/2 */
+  int32_t form;
+  int32_t s_diagonal;        /* 1 if S = A D^-1 A^T is diagonal (elementwise KKT)   */
+  int64_t jacobi_capped;     /* count of projections that hit the sweep cap          */
+  int32_t launches_per_iter; /* kernels launched per ADMM iteration                   */
+} sdp_info;
+
+typedef struct sdp_handle_s* sdp_handle;
+
+/* Fill *opt with the defaults listed above. */
+void sdp_default_options(sdp_options* opt);
+
+/* Build the decomposed problem and upload it (host setup, run once; timed
+ * separately, "Setup: Chordal decomposition, KKT factorization").
+ * prob, opt: host, read during the call.  out: receives the handle.
+ * Errors: SDP_E_INVALID_ARG (index out of range, row > col, duplicate entry,
+ * n <= 0, m <= 0, clique order > SDP_MAX_K), SDP_E_RANK_DEFICIENT, SDP_E_CUDA,
+ * SDP_E_OOM.  On error *out is NULL. */
+int sdp_setup(const sdp_problem* prob, const sdp_options* opt, sdp_handle* out);
+
+/* Run exactly `iters` ADMM iterations from the current state, no stopping test.
+ * Asynchronous on the handle's stream; returns after enqueueing. */
+int sdp_step(sdp_handle h, int32_t iters);
+
+/* Iterate until max(eps_p, eps_d) < tol (Algorithm 1/2 line 3) or until
+ * max_iters iterations have run since the last reset.  The stop is exact (the
+ * state is that of the first converged iteration).  Synchronises the stream.
+ * info (host, may be NULL) receives the final info.
+ * Returns SDP_OK, SDP_MAX_ITER, or SDP_E_NUMERICAL. */
+int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info);
+
+/* Zero the ADMM state (initial guesses = 0, reading G12). */
+int sdp_reset(sdp_handle h);
+
+/* Change rho between iterations; the cached factor is rho-independent. */
+int sdp_set_rho(sdp_handle h, double rho);
+
+/* Synchronise and report sizes, residuals and objective (host out). */
+int sdp_get_info(sdp_handle h, sdp_info* info);
+
+/* ---- getters: synchronise the stream, copy into host buffers ----------- */
+#define SDP_VEC_X 0        /* N: x (svec on the pattern, primal KKT x / dual KKT x)   */
+#define SDP_VEC_Y 1        /* m: KKT y                                               */
+#define SDP_VEC_XMAT 2     /* N: unscaled matrix entries of x on the pattern         */
+#define SDP_BLK_XK 0       /* stacked x_k (primal) or z_k (dual)                      */
+#define SDP_BLK_LAMBDA 1   /* stacked lambda_k                                       */
+#define SDP_BLK_VK 2       /* stacked v_k (dual only)                                */
+int sdp_get_vector(sdp_handle h, int32_t which, double* out);
+int sdp_get_blocks(sdp_handle h, int32_t which, double* out);   /* stot values */
+/* Pattern coordinates (row[N], col[N]) in canonical order. */
+int sdp_get_pattern(sdp_handle h, int32_t* row, int32_t* col);
+/* Clique sizes (p values) and the concatenated sorted vertex lists (sum of sizes). */
+int sdp_get_cliques(sdp_handle h, int32_t* sizes, int32_t* vertices);
+/* Per-iteration history since reset: rows of (eps_p, eps_d, objective); at most cap rows. */
+int sdp_get_history(sdp_handle h, double* out, int64_t cap, int64_t* rows);
+
+/* Per-phase timing: run `iters` iterations (no graph) with CUDA events recorded
+ * on the handle's stream around every phase; out_ms[ph] (host, capacity
+ * SDP_NUM_PHASES) receives the mean device time per iteration of phase ph:
+ * 0 gemv (A.v), 1 kkt-small (reduce + triangular solves), 2 gemvT (A^T.y + x),
+ * 3 projection (all tiers), 4 scatter, 5 dual update, 6 finalize.
+ * Advances the state like sdp_step.  Synchronises. */
+#define SDP_NUM_PHASES 7
+int sdp_profile_phases(sdp_handle h, int32_t iters, double* out_ms);
+
+/* Free all resources of the handle (synchronises). */
+int sdp_destroy(sdp_handle h);
+
+/* ---- chordal analysis only (host, no GPU) ------------------------------ */
+/* Chordal extension + maximal cliques of the pattern given by (row, col) upper
+ * entries (diagonal implicit).  sizes: host buffer of capacity n; vertices:
+ * capacity cap_vertices; *p receives the clique count, *nv the vertex count.
+ * Same rules as sdp_setup (exact minimum degree, lowest index on ties). */
+int sdp_chordal_cliques(int32_t n, int64_t nnz, const int32_t* row, const int32_t* col,
+                        int32_t* p, int32_t* sizes, int64_t cap_vertices, int32_t* vertices,
+                        int64_t* nv, int64_t* fill_edges);
+
+/* ---- batched PSD projection (E:XkUpdate) ---------------------- */
+typedef struct sdp_psd_plan_s* sdp_psd_plan;
+
+/* Plan for `count` matrices of orders h_sizes[i] (host, 1 <= k <= SDP_MAX_K).
+ * Matrix i occupies k(k+1)/2 doubles at offset sum_{j<i} k_j(k_j+1)/2 of the
+ * in/out arrays, packed upper column-major, UNSCALED entries. */
+int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, sdp_psd_plan* out);
+/* out_i = argmin_{P PSD} ||P - in_i||_F for every i.  d_in, d_out: device,
+ * may alias (in place).  Asynchronous on `stream` (cudaStream_t, NULL = default). */
+int sdp_project_psd_batch(sdp_psd_plan plan, const double* d_in, double* d_out, void* stream);
+/* Same, from/to HOST buffers (copies inside the call; synchronous). */
+int sdp_project_psd_batch_host(sdp_psd_plan plan, const double* h_in, double* h_out, void* stream);
+int64_t sdp_psd_plan_values(sdp_psd_plan plan);   /* total doubles of in/out */
+int sdp_psd_plan_destroy(sdp_psd_plan plan);
+
+const char* sdp_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CHORDAL_SDP_H */

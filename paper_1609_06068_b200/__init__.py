@@ -1,0 +1,10 @@
+"""B200-native hot path of the chordally decomposed ADMM for sparse SDPs
+(arXiv 1609.06068).  The compute lives in libchordal_sdp.so (C ABI declared in
+include/chordal_sdp.h); this package is its thin Python binding.
+
+    from paper_1609_06068_b200 import Solver, PsdPlan, chordal_cliques
+"""
+from ._lib import (EXPORTED, LIB_PATH, PsdPlan, SdpError, Solver, chordal_cliques,  # noqa: F401
+                   lib)
+
+__all__ = ["Solver", "PsdPlan", "chordal_cliques", "SdpError", "lib", "LIB_PATH", "EXPORTED"]

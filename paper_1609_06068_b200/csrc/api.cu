@@ -1,0 +1,1116 @@
+// C ABI (include/chordal_sdp.h): setup, the ADMM iteration pipeline captured in
+// a CUDA graph, getters, and the batched PSD projection plan.
+#include <omp.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels_vec.h"
+
+namespace sdp {
+
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+void psd_init_attributes();
+
+namespace {
+
+constexpr double kSqrt2 = 1.41421356237309504880;
+constexpr long long kHistCap = 1 << 20;
+
+struct Alloc {
+  std::vector<void*> ptrs;
+  template <class T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    SDP_CUDA_TRY(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    ptrs.push_back(p);
+    return (T*)p;
+  }
+  template <class T>
+  T* zeros(size_t n) {
+    T* p = get<T>(n);
+    SDP_CUDA_TRY(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+    return p;
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v, size_t n_alloc = 0) {
+    size_t n = std::max(v.size(), n_alloc);
+    T* p = zeros<T>(n);
+    if (!v.empty()) SDP_CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  }
+  void release(void* p) {
+    auto it = std::find(ptrs.begin(), ptrs.end(), p);
+    if (it != ptrs.end()) {
+      cudaFree(p);
+      ptrs.erase(it);
+    }
+  }
+  void free_all() {
+    for (void* p : ptrs) cudaFree(p);
+    ptrs.clear();
+  }
+};
+
+// Host Cholesky S = L L^T (row-major, lower).  Returns false if S is not
+// numerically positive definite (pivot <= 1e-12 * S_ii).
+bool cholesky_host(std::vector<double>& S, int m) {
+  for (int i = 0; i < m; ++i) {
+    double* Li = S.data() + (size_t)i * m;
+    for (int j = 0; j <= i; ++j) {
+      const double* Lj = S.data() + (size_t)j * m;
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      int k = 0;
+      for (; k + 4 <= j; k += 4) {
+        a0 += Li[k] * Lj[k];
+        a1 += Li[k + 1] * Lj[k + 1];
+        a2 += Li[k + 2] * Lj[k + 2];
+        a3 += Li[k + 3] * Lj[k + 3];
+      }
+      for (; k < j; ++k) a0 += Li[k] * Lj[k];
+      const double s = Li[j] - ((a0 + a1) + (a2 + a3));
+      if (i == j) {
+        if (!(s > 1e-12 * Li[i]) || !std::isfinite(s)) return false;
+        Li[i] = std::sqrt(s);
+      } else {
+        Li[j] = s / Lj[j];
+      }
+    }
+    for (int j = i + 1; j < m; ++j) Li[j] = 0.0;
+  }
+  return true;
+}
+
+// Wt = (L^-1)^T (row-major upper): row j of Wt is column j of L^-1.
+void tri_inverse_T(const std::vector<double>& L, int m, std::vector<double>& Wt) {
+  Wt.assign((size_t)m * m, 0.0);
+#pragma omp parallel for schedule(dynamic, 8)
+  for (int j = 0; j < m; ++j) {
+    double* w = Wt.data() + (size_t)j * m;
+    w[j] = 1.0 / L[(size_t)j * m + j];
+    for (int i = j + 1; i < m; ++i) {
+      const double* Li = L.data() + (size_t)i * m;
+      double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+      int k = j;
+      for (; k + 4 <= i; k += 4) {
+        a0 += Li[k] * w[k];
+        a1 += Li[k + 1] * w[k + 1];
+        a2 += Li[k + 2] * w[k + 2];
+        a3 += Li[k + 3] * w[k + 3];
+      }
+      for (; k < i; ++k) a0 += Li[k] * w[k];
+      w[i] = -((a0 + a1) + (a2 + a3)) / Li[i];
+    }
+  }
+}
+
+}  // namespace
+}  // namespace sdp
+
+using namespace sdp;
+
+struct sdp_handle_s {
+  int n = 0, m = 0;
+  int64_t N = 0, lda = 0, p = 0, stot = 0;
+  int form = 0;
+  double rho = 1.0;
+  int device = 0;
+  cudaStream_t stream = nullptr, cap_stream = nullptr;
+  bool own_stream = false;
+  int check_every = 10, use_graph = 1;
+  double setup_s = 0;
+  int64_t fill_edges = 0;
+  // host copies
+  std::vector<int32_t> coord_row, coord_col, clique_size, clique_vert;
+  std::vector<int64_t> clique_off;
+  int64_t kmin = 0, kmax = 0;
+  // device buffers
+  Alloc alloc;
+  double *x = nullptr, *rD = nullptr, *Dinv = nullptr, *c = nullptr, *sprev = nullptr, *y = nullptr, *u = nullptr,
+         *t = nullptr, *b = nullptr;
+  double *xk = nullptr, *lam = nullptr, *vk = nullptr;
+  int32_t *G = nullptr, *seg_ptr = nullptr, *seg_idx = nullptr, *longc = nullptr;
+  int n_long = 0;
+  int64_t* d_off = nullptr;
+  int32_t* d_ksz = nullptr;
+  int32_t* d_ids[B_NUM] = {};
+  int bcount[B_NUM] = {};
+  double* work = nullptr;
+  int work_slots = 0, ld_work = 0;
+  // A
+  int a_dense = 1;
+  double* A = nullptr;
+  int32_t *a_rp = nullptr, *a_ci = nullptr, *at_cp = nullptr, *at_ri = nullptr;
+  double *a_val = nullptr, *at_val = nullptr;
+  int s_diag = 0;
+  double* sdiag = nullptr;
+  double *W = nullptr, *WT = nullptr;
+  double* gemv_part = nullptr;
+  int chunk = 8192, nchunks = 0;
+  // residuals
+  double *proj_part = nullptr, *scat_part = nullptr, *gT_part = nullptr, *upd_part = nullptr;
+  int nb_scat = 0, nb_gT = 0, nb_upd = 0;
+  double *res = nullptr, *hist = nullptr, *tol = nullptr;
+  long long* iter = nullptr;
+  int *done = nullptr, *numerical = nullptr;
+  unsigned long long* capped = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+struct sdp_psd_plan_s {
+  int device = 0;
+  int64_t count = 0, values = 0;
+  Alloc alloc;
+  int64_t* d_off = nullptr;
+  int32_t* d_ksz = nullptr;
+  int32_t* d_ids[B_NUM] = {};
+  int bcount[B_NUM] = {};
+  double* work = nullptr;
+  int work_slots = 0, ld_work = 0;
+  unsigned long long* capped = nullptr;
+  double *h_in_dev = nullptr, *h_out_dev = nullptr;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) SDP_CUDA_TRY(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return SDP_E_OOM;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return SDP_E_INVALID_ARG;
+  }
+}
+
+void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_NUM], int bcount[B_NUM],
+                   double*& work, int& slots, int& ld_work) {
+  std::vector<std::vector<int32_t>> lists(B_NUM);
+  int kg = 0;
+  for (size_t i = 0; i < ksz.size(); ++i) {
+    const int b = bucket_of(ksz[i]);
+    lists[b].push_back((int32_t)i);
+    if (b == B_GLOBAL) kg = std::max(kg, (int)ksz[i]);
+  }
+  // GLOBAL tier: biggest first so the long projections start early
+  std::stable_sort(lists[B_GLOBAL].begin(), lists[B_GLOBAL].end(),
+                   [&](int32_t a, int32_t b) { return ksz[a] > ksz[b]; });
+  for (int b = 0; b < B_NUM; ++b) {
+    bcount[b] = (int)lists[b].size();
+    d_ids[b] = bcount[b] ? al.upload(lists[b]) : nullptr;
+  }
+  if (bcount[B_GLOBAL]) {
+    ld_work = kg + (kg & 1);
+    slots = std::min(bcount[B_GLOBAL], 148);
+    work = al.get<double>((size_t)slots * 2 * ld_work * ld_work);
+  }
+}
+
+void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
+  ProjArgs a{};
+  a.off = h->d_off;
+  a.ksz = h->d_ksz;
+  a.x = h->x;
+  a.G = h->G;
+  a.xk = h->xk;
+  a.lam = h->lam;
+  a.vk = h->vk;
+  a.rho = h->rho;
+  a.part = h->proj_part;
+  a.work = h->work;
+  a.work_slots = h->work_slots;
+  a.ld_work = h->ld_work;
+  a.capped = h->capped;
+  a.done = h->done;
+  // big tiers first: they are the long poles
+  for (int b = B_NUM - 1; b >= 0; --b) {
+    if (!h->bcount[b]) continue;
+    a.ids = h->d_ids[b];
+    a.count = h->bcount[b];
+    launch_projection(b, mode, a, s);
+  }
+}
+
+void enqueue_scatter(sdp_handle h, cudaStream_t s) {
+  ScatterArgs a{};
+  a.N = (int)h->N;
+  a.seg_ptr = h->seg_ptr;
+  a.seg_idx = h->seg_idx;
+  a.longc = h->longc;
+  a.n_long = h->n_long;
+  a.xk = h->xk;
+  a.lam = h->lam;
+  a.c = h->c;
+  a.Dinv = h->Dinv;
+  a.rho = h->rho;
+  a.rD = h->rD;
+  a.sprev = h->sprev;
+  a.part = h->scat_part;
+  a.done = h->done;
+  launch_scatter(h->form, a, s);
+}
+
+// Phase hook: records an event at a phase boundary when profiling.
+struct PhaseRec {
+  std::vector<cudaEvent_t>* ev = nullptr;
+  int* idx = nullptr;
+  void mark(int phase, cudaStream_t s) const {
+    if (!ev) return;
+    cudaEventRecord((*ev)[(*idx)++], s);
+    (void)phase;
+  }
+};
+thread_local PhaseRec g_phase;
+thread_local int g_phase_id[64];
+thread_local int g_phase_n = 0;
+inline void phase(int ph, cudaStream_t s) {
+  if (!g_phase.ev) return;
+  g_phase_id[g_phase_n++] = ph;
+  g_phase.mark(ph, s);
+}
+
+void enqueue_kkt(sdp_handle h, cudaStream_t s) {
+  const int f = h->form;
+  double* ydst = h->s_diag ? h->y : nullptr;
+  phase(0, s);
+  if (h->a_dense) {
+    launch_gemv_dense(h->A, h->lda, h->m, h->rD, h->chunk, h->gemv_part, h->done, s);
+    phase(1, s);
+    launch_reduce_u(f, h->gemv_part, h->nchunks, h->m, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr, ydst,
+                    h->done, s);
+  } else {
+    launch_gemv_csr(f, h->a_rp, h->a_ci, h->a_val, h->m, h->rD, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr,
+                    ydst, h->done, s);
+    phase(1, s);
+  }
+  if (!h->s_diag) {
+    launch_trmv(1, h->W, h->m, h->u, h->t, h->done, s);   // t = L^-1 u
+    launch_trmv(0, h->WT, h->m, h->t, h->y, h->done, s);  // y = L^-T t
+  }
+  phase(2, s);
+  if (h->a_dense)
+    launch_gemvT_dense(f, h->A, h->lda, h->m, (int)h->N, h->y, h->rD, h->Dinv, h->c, h->x, h->gT_part, h->done, s);
+  else
+    launch_gemvT_csc(f, h->at_cp, h->at_ri, h->at_val, (int)h->N, h->y, h->rD, h->Dinv, h->c, h->x, h->gT_part,
+                     h->done, s);
+}
+
+void enqueue_finalize(sdp_handle h, cudaStream_t s) {
+  FinalArgs a{};
+  a.proj_part = h->proj_part;
+  a.n_proj = (int)h->p;
+  a.upd_part = h->upd_part;
+  a.n_upd = h->nb_upd;
+  a.scat_part = h->scat_part;
+  a.n_scat = h->nb_scat;
+  a.gT_part = h->gT_part;
+  a.n_gT = h->nb_gT;
+  a.b = h->b;
+  a.y = h->y;
+  a.m = h->m;
+  a.rho = h->rho;
+  a.res = h->res;
+  a.hist = h->hist;
+  a.hist_cap = kHistCap;
+  a.iter = h->iter;
+  a.done = h->done;
+  a.numerical = h->numerical;
+  a.tol = h->tol;
+  launch_finalize(h->form, a, s);
+}
+
+// One ADMM iteration (Algorithm 1 lines 4-7 / Algorithm 2 lines 4-8).
+void enqueue_iteration(sdp_handle h, cudaStream_t s) {
+  if (h->form == SDP_FORM_PRIMAL) {
+    enqueue_kkt(h, s);                       // x   (E:OptCondMinYPrimal)
+    phase(3, s);
+    enqueue_projection(h, PM_PRIMAL, s);     // x_k (E:XkUpdate), lambda_k (E:LambdakUpdate)
+    phase(4, s);
+    enqueue_scatter(h, s);                   // rhs of the next KKT solve + eps_d partials
+  } else {
+    phase(3, s);
+    enqueue_projection(h, PM_DUAL, s);       // z_k (E:zkUpdate)
+    phase(4, s);
+    enqueue_scatter(h, s);                   // rhs of E:OptCondMinYDual
+    enqueue_kkt(h, s);                       // x, y
+    phase(5, s);
+    launch_update_dual(h->stot, h->G, h->x, h->xk, h->lam, h->vk, h->rho, h->upd_part, h->done, s);  // v_k, lambda_k
+  }
+  phase(6, s);
+  enqueue_finalize(h, s);
+  phase(7, s);
+}
+
+int launches_per_iter(sdp_handle h) {
+  int n = 0;
+  for (int b = 0; b < B_NUM; ++b) n += h->bcount[b] ? 1 : 0;
+  n += 1;                                       // scatter
+  n += h->a_dense ? 3 : 2;                      // gemv (+ reduce) + gemvT
+  n += h->s_diag ? 0 : 2;                       // triangular solves
+  n += (h->form == SDP_FORM_DUAL) ? 1 : 0;      // dual update
+  n += 1;                                       // finalize
+  return n;
+}
+
+void rebuild_graph(sdp_handle h) {
+  if (h->exec) {
+    cudaGraphExecDestroy(h->exec);
+    h->exec = nullptr;
+  }
+  if (h->graph) {
+    cudaGraphDestroy(h->graph);
+    h->graph = nullptr;
+  }
+  if (!h->use_graph) return;
+  SDP_CUDA_TRY(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+  enqueue_iteration(h, h->cap_stream);
+  SDP_CUDA_TRY(cudaStreamEndCapture(h->cap_stream, &h->graph));
+  SDP_CUDA_TRY(cudaGraphInstantiate(&h->exec, h->graph, 0));
+}
+
+void reset_state(sdp_handle h) {
+  cudaStream_t s = h->stream;
+  SDP_CUDA_TRY(cudaMemsetAsync(h->xk, 0, h->stot * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->lam, 0, h->stot * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->vk, 0, h->stot * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->x, 0, h->lda * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->rD, 0, h->lda * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->sprev, 0, h->lda * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->y, 0, h->m * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->res, 0, 4 * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->iter, 0, sizeof(long long), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->numerical, 0, sizeof(int), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->capped, 0, sizeof(unsigned long long), s));
+  const double neg = -1.0;
+  SDP_CUDA_TRY(cudaMemcpyAsync(h->tol, &neg, sizeof(double), cudaMemcpyHostToDevice, s));
+  if (h->form == SDP_FORM_PRIMAL) enqueue_scatter(h, s);  // r1 = -c/rho for iteration 1
+  SDP_CUDA_TRY(cudaGetLastError());
+  SDP_CUDA_TRY(cudaStreamSynchronize(s));
+}
+
+void check_indices(const char* what, int64_t nnz, const int32_t* r, const int32_t* c, int n) {
+  for (int64_t e = 0; e < nnz; ++e) {
+    if (r[e] < 0 || c[e] < 0 || r[e] >= n || c[e] >= n)
+      throw Error{SDP_E_INVALID_ARG, std::string(what) + " entry " + std::to_string(e) + " index out of range"};
+    if (r[e] > c[e])
+      throw Error{SDP_E_INVALID_ARG, std::string(what) + " entry " + std::to_string(e) + " has row > col"};
+  }
+}
+
+void destroy_handle(sdp_handle h) {
+  if (!h) return;
+  int cur = -1;
+  cudaGetDevice(&cur);
+  cudaSetDevice(h->device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  if (h->exec) cudaGraphExecDestroy(h->exec);
+  if (h->graph) cudaGraphDestroy(h->graph);
+  h->alloc.free_all();
+  if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  if (cur >= 0) cudaSetDevice(cur);
+  delete h;
+}
+
+int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out) {
+  auto t0 = std::chrono::steady_clock::now();
+  if (!out) throw Error{SDP_E_INVALID_ARG, "out is NULL"};
+  *out = nullptr;
+  if (!P) throw Error{SDP_E_INVALID_ARG, "problem is NULL"};
+  sdp_options opt;
+  sdp_default_options(&opt);
+  if (opt_in) opt = *opt_in;
+  const int n = P->n, m = P->m;
+  if (n <= 0) throw Error{SDP_E_INVALID_ARG, "n <= 0"};
+  if (m <= 0) throw Error{SDP_E_INVALID_ARG, "m <= 0"};
+  if (!(opt.rho > 0) || !std::isfinite(opt.rho)) throw Error{SDP_E_INVALID_ARG, "rho must be positive"};
+  if (opt.form != SDP_FORM_PRIMAL && opt.form != SDP_FORM_DUAL) throw Error{SDP_E_INVALID_ARG, "bad form"};
+  if (opt.world != 1 || opt.rank != 0)
+    throw Error{SDP_E_INVALID_ARG, "clique sharding across ranks is not available in this build (world must be 1)"};
+  if (!P->b) throw Error{SDP_E_INVALID_ARG, "b is NULL"};
+  if (P->c_nnz < 0 || (P->c_nnz > 0 && (!P->c_row || !P->c_col || !P->c_val)))
+    throw Error{SDP_E_INVALID_ARG, "C arrays missing"};
+  if (P->a_fmt != SDP_A_COO && P->a_fmt != SDP_A_DENSE_ON_PATTERN) throw Error{SDP_E_INVALID_ARG, "bad a_fmt"};
+  if (P->a_nnz < 0 || (P->a_nnz > 0 && (!P->a_row || !P->a_col || !P->a_val)))
+    throw Error{SDP_E_INVALID_ARG, "A arrays missing"};
+  if (P->a_fmt == SDP_A_COO && P->a_nnz > 0 && !P->a_con) throw Error{SDP_E_INVALID_ARG, "a_con missing"};
+  if (P->e_nnz < 0 || (P->e_nnz > 0 && (!P->e_row || !P->e_col))) throw Error{SDP_E_INVALID_ARG, "E arrays missing"};
+  check_indices("C", P->c_nnz, P->c_row, P->c_col, n);
+  check_indices("A", P->a_nnz, P->a_row, P->a_col, n);
+  check_indices("E", P->e_nnz, P->e_row, P->e_col, n);
+  for (int i = 0; i < m; ++i)
+    if (!std::isfinite(P->b[i])) throw Error{SDP_E_INVALID_ARG, "b[" + std::to_string(i) + "] not finite"};
+  for (int64_t e = 0; e < P->c_nnz; ++e)
+    if (!std::isfinite(P->c_val[e])) throw Error{SDP_E_INVALID_ARG, "C value " + std::to_string(e) + " not finite"};
+  if (P->a_fmt == SDP_A_COO)
+    for (int64_t e = 0; e < P->a_nnz; ++e)
+      if (P->a_con[e] < 0 || P->a_con[e] >= m)
+        throw Error{SDP_E_INVALID_ARG, "A entry " + std::to_string(e) + " constraint index out of range"};
+
+  int ndev = 0;
+  SDP_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (opt.device < 0 || opt.device >= ndev) throw Error{SDP_E_INVALID_ARG, "bad device ordinal"};
+  DeviceGuard dg(opt.device);
+
+  // ---- 1. aggregate pattern and chordal analysis
+  std::vector<std::pair<int32_t, int32_t>> edges;
+  edges.reserve((size_t)(P->c_nnz + P->a_nnz + P->e_nnz));
+  auto add = [&](int64_t nnz, const int32_t* r, const int32_t* c) {
+    for (int64_t e = 0; e < nnz; ++e)
+      if (r[e] != c[e]) edges.push_back({r[e], c[e]});
+  };
+  add(P->c_nnz, P->c_row, P->c_col);
+  add(P->a_nnz, P->a_row, P->a_col);
+  add(P->e_nnz, P->e_row, P->e_col);
+  ChordalResult cr = chordal_analysis(n, edges);
+  edges.clear();
+  edges.shrink_to_fit();
+
+  sdp_handle h = new sdp_handle_s();
+  *out = h;  // so the caller-side cleanup path below can destroy it
+  h->n = n;
+  h->m = m;
+  h->form = opt.form;
+  h->rho = opt.rho;
+  h->device = opt.device;
+  h->check_every = opt.check_every > 0 ? opt.check_every : 10;
+  h->use_graph = opt.use_graph;
+  h->fill_edges = cr.fill_edges;
+  if (opt.stream) {
+    h->stream = (cudaStream_t)opt.stream;
+  } else {
+    SDP_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+    h->own_stream = true;
+  }
+  SDP_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  const int64_t N = (int64_t)cr.coord_row.size();
+  h->N = N;
+  h->lda = (N + 31) / 32 * 32;
+  h->coord_row = cr.coord_row;
+  h->coord_col = cr.coord_col;
+  if (N >= (1ll << 31)) throw Error{SDP_E_INVALID_ARG, "pattern too large"};
+
+  // ---- 2. layout: clique offsets, H_k maps, D, inverse map
+  const int64_t p = (int64_t)cr.cliques.size();
+  h->p = p;
+  std::vector<int64_t> off(p + 1, 0);
+  std::vector<int32_t> ksz(p);
+  h->kmin = INT64_MAX;
+  h->kmax = 0;
+  for (int64_t k = 0; k < p; ++k) {
+    const int kk = (int)cr.cliques[k].size();
+    if (kk > SDP_MAX_K)
+      throw Error{SDP_E_INVALID_ARG, "clique of order " + std::to_string(kk) + " exceeds SDP_MAX_K"};
+    ksz[k] = kk;
+    off[k + 1] = off[k] + (int64_t)kk * (kk + 1) / 2;
+    h->kmin = std::min<int64_t>(h->kmin, kk);
+    h->kmax = std::max<int64_t>(h->kmax, kk);
+    h->clique_size.push_back(kk);
+    for (int v : cr.cliques[k]) h->clique_vert.push_back(v);
+  }
+  const int64_t stot = off[p];
+  h->stot = stot;
+  h->clique_off = off;
+  if (stot >= (1ll << 31)) throw Error{SDP_E_INVALID_ARG, "stacked clique vectors too large"};
+  std::vector<int32_t> Gmap(stot);
+  std::vector<int32_t> cnt(N + 1, 0);
+#pragma omp parallel for schedule(dynamic, 16)
+  for (int64_t k = 0; k < p; ++k) {
+    const auto& C = cr.cliques[k];
+    int64_t e = off[k];
+    for (size_t bcol = 0; bcol < C.size(); ++bcol)
+      for (size_t arow = 0; arow <= bcol; ++arow) Gmap[e++] = (int32_t)coord_index(cr, C[arow], C[bcol]);
+  }
+  for (int64_t s = 0; s < stot; ++s) cnt[Gmap[s] + 1]++;
+  std::vector<int32_t> seg_ptr(N + 1, 0);
+  for (int64_t t = 0; t < N; ++t) seg_ptr[t + 1] = seg_ptr[t] + cnt[t + 1];
+  std::vector<int32_t> seg_idx(stot), fillp(seg_ptr.begin(), seg_ptr.end() - 1);
+  for (int64_t s = 0; s < stot; ++s) seg_idx[fillp[Gmap[s]]++] = (int32_t)s;
+  std::vector<double> Dinv(h->lda, 0.0);
+  std::vector<int32_t> longc;
+  for (int64_t t = 0; t < N; ++t) {
+    const int d = seg_ptr[t + 1] - seg_ptr[t];
+    if (d <= 0) throw Error{SDP_E_INVALID_ARG, "internal: pattern coordinate covered by no clique"};
+    Dinv[t] = 1.0 / (double)d;
+    if (d > kLongSeg) longc.push_back((int32_t)t);
+  }
+  h->n_long = (int)longc.size();
+
+  // ---- 3. c = svec(C) on the pattern
+  std::vector<double> cvec(h->lda, 0.0);
+  {
+    std::vector<char> seen(N, 0);
+    for (int64_t e = 0; e < P->c_nnz; ++e) {
+      const int64_t t = coord_index(cr, P->c_row[e], P->c_col[e]);
+      if (seen[t]) throw Error{SDP_E_INVALID_ARG, "duplicate C entry " + std::to_string(e)};
+      seen[t] = 1;
+      cvec[t] = P->c_val[e] * (P->c_row[e] == P->c_col[e] ? 1.0 : kSqrt2);
+    }
+  }
+
+  // ---- 4. device uploads of the layout
+  Alloc& al = h->alloc;
+  h->G = al.upload(Gmap);
+  h->seg_ptr = al.upload(seg_ptr);
+  h->seg_idx = al.upload(seg_idx);
+  h->longc = al.upload(longc);
+  h->Dinv = al.upload(Dinv);
+  h->c = al.upload(cvec);
+  h->d_off = al.upload(off);
+  h->d_ksz = al.upload(ksz);
+  h->b = al.upload(std::vector<double>(P->b, P->b + m));
+  h->x = al.zeros<double>(h->lda);
+  h->rD = al.zeros<double>(h->lda);
+  h->sprev = al.zeros<double>(h->lda);
+  h->y = al.zeros<double>(m);
+  h->u = al.zeros<double>(m);
+  h->t = al.zeros<double>(m);
+  h->xk = al.zeros<double>(stot);
+  h->lam = al.zeros<double>(stot);
+  h->vk = al.zeros<double>(stot);
+  build_buckets(al, ksz, h->d_ids, h->bcount, h->work, h->work_slots, h->ld_work);
+
+  // ---- 5. A (svec rows) and S = A D^-1 A^T, factor cached once
+  std::vector<double> S;
+  if (P->a_fmt == SDP_A_DENSE_ON_PATTERN) {
+    h->a_dense = 1;
+    const int64_t npat = P->a_nnz;
+    std::vector<int64_t> map(npat);
+    std::vector<double> scale(npat);
+    std::vector<char> seen(N, 0);
+    for (int64_t e = 0; e < npat; ++e) {
+      const int64_t t = coord_index(cr, P->a_row[e], P->a_col[e]);
+      if (seen[t]) throw Error{SDP_E_INVALID_ARG, "duplicate A pattern entry " + std::to_string(e)};
+      seen[t] = 1;
+      map[e] = t;
+      scale[e] = (P->a_row[e] == P->a_col[e]) ? 1.0 : kSqrt2;
+    }
+    h->A = al.zeros<double>((size_t)m * h->lda);
+    if (npat > 0) {
+      // stream the raw values in row slabs of <= 256 MB through a staging buffer
+      const int64_t rows_per = std::max<int64_t>(1, (256ll << 20) / (8 * npat));
+      double* raw = al.get<double>((size_t)std::min<int64_t>(rows_per, m) * npat);
+      int64_t* dmap = al.upload(map);
+      double* dscale = al.upload(scale);
+      for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
+        const int64_t nr = std::min<int64_t>(rows_per, m - r0);
+        for (int64_t i = 0; i < nr * npat; ++i)
+          if (!std::isfinite(P->a_val[r0 * npat + i])) throw Error{SDP_E_INVALID_ARG, "A value not finite"};
+        SDP_CUDA_TRY(cudaMemcpy(raw, P->a_val + r0 * npat, nr * npat * sizeof(double), cudaMemcpyHostToDevice));
+        launch_place_dense(raw, npat, (int)nr, dmap, dscale, h->A + r0 * h->lda, h->lda, nullptr);
+        SDP_CUDA_TRY(cudaGetLastError());
+        SDP_CUDA_TRY(cudaDeviceSynchronize());
+      }
+      al.release(raw);
+      al.release(dmap);
+      al.release(dscale);
+    }
+    h->chunk = 8192;
+    h->nchunks = (int)((h->lda + h->chunk - 1) / h->chunk);
+    h->gemv_part = al.zeros<double>((size_t)h->nchunks * m);
+    double* dS = al.get<double>((size_t)m * m);
+    launch_syrk_dense(h->A, h->lda, m, h->Dinv, dS, nullptr);
+    SDP_CUDA_TRY(cudaGetLastError());
+    S.resize((size_t)m * m);
+    SDP_CUDA_TRY(cudaMemcpy(S.data(), dS, S.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    al.release(dS);
+  } else {
+    h->a_dense = 0;
+    struct Ent {
+      int32_t con;
+      int32_t t;
+      double v;
+    };
+    std::vector<Ent> ents((size_t)P->a_nnz);
+    for (int64_t e = 0; e < P->a_nnz; ++e) {
+      if (!std::isfinite(P->a_val[e])) throw Error{SDP_E_INVALID_ARG, "A value " + std::to_string(e) + " not finite"};
+      ents[e] = {P->a_con[e], (int32_t)coord_index(cr, P->a_row[e], P->a_col[e]),
+                 P->a_val[e] * (P->a_row[e] == P->a_col[e] ? 1.0 : kSqrt2)};
+    }
+    std::sort(ents.begin(), ents.end(),
+              [](const Ent& a, const Ent& b) { return a.con != b.con ? a.con < b.con : a.t < b.t; });
+    for (size_t e = 1; e < ents.size(); ++e)
+      if (ents[e].con == ents[e - 1].con && ents[e].t == ents[e - 1].t)
+        throw Error{SDP_E_INVALID_ARG, "duplicate A entry (constraint " + std::to_string(ents[e].con) + ")"};
+    std::vector<int32_t> rp(m + 1, 0), ci(ents.size());
+    std::vector<double> val(ents.size());
+    for (size_t e = 0; e < ents.size(); ++e) {
+      rp[ents[e].con + 1]++;
+      ci[e] = ents[e].t;
+      val[e] = ents[e].v;
+    }
+    for (int i = 0; i < m; ++i) rp[i + 1] += rp[i];
+    // CSC
+    std::vector<int32_t> cp(N + 1, 0), ri(ents.size());
+    std::vector<double> cval(ents.size());
+    for (auto& en : ents) cp[en.t + 1]++;
+    for (int64_t t = 0; t < N; ++t) cp[t + 1] += cp[t];
+    std::vector<int32_t> pos(cp.begin(), cp.end() - 1);
+    int maxcol = 0;
+    for (auto& en : ents) {  // ents sorted by (con, t): rows ascend inside each column
+      ri[pos[en.t]] = en.con;
+      cval[pos[en.t]++] = en.v;
+    }
+    for (int64_t t = 0; t < N; ++t) maxcol = std::max(maxcol, cp[t + 1] - cp[t]);
+    h->a_rp = al.upload(rp);
+    h->a_ci = al.upload(ci);
+    h->a_val = al.upload(val);
+    h->at_cp = al.upload(cp);
+    h->at_ri = al.upload(ri);
+    h->at_val = al.upload(cval);
+    if (maxcol <= 1) {
+      // rows of A have disjoint supports: S = A D^-1 A^T is diagonal
+      std::vector<double> sd(m, 0.0);
+      for (int i = 0; i < m; ++i)
+        for (int e = rp[i]; e < rp[i + 1]; ++e) sd[i] += val[e] * val[e] * Dinv[ci[e]];
+      for (int i = 0; i < m; ++i)
+        if (!(sd[i] > 0)) throw Error{SDP_E_RANK_DEFICIENT, "constraint " + std::to_string(i) + " is empty"};
+      h->s_diag = 1;
+      h->sdiag = al.upload(sd);
+    } else {
+      S.assign((size_t)m * m, 0.0);
+      for (int64_t t = 0; t < N; ++t)
+        for (int e1 = cp[t]; e1 < cp[t + 1]; ++e1)
+          for (int e2 = cp[t]; e2 < cp[t + 1]; ++e2) S[(size_t)ri[e1] * m + ri[e2]] += cval[e1] * cval[e2] * Dinv[t];
+    }
+  }
+  if (!h->s_diag) {
+    if (!cholesky_host(S, m)) throw Error{SDP_E_RANK_DEFICIENT, "S = A D^-1 A^T is not positive definite"};
+    std::vector<double> Wt;
+    tri_inverse_T(S, m, Wt);
+    std::vector<double> Wl((size_t)m * m);
+#pragma omp parallel for
+    for (int i = 0; i < m; ++i)
+      for (int j = 0; j < m; ++j) Wl[(size_t)i * m + j] = Wt[(size_t)j * m + i];
+    h->W = al.upload(Wl);
+    h->WT = al.upload(Wt);
+  }
+
+  // ---- 6. residual buffers, state, graph
+  h->nb_scat = scatter_blocks((int)N, h->n_long);
+  h->nb_gT = h->a_dense ? gemvT_blocks(h->lda) : gemvT_csc_blocks((int)N);
+  h->nb_upd = update_blocks(stot);
+  h->proj_part = al.zeros<double>(3 * (size_t)p);
+  h->scat_part = al.zeros<double>(2 * (size_t)h->nb_scat);
+  h->gT_part = al.zeros<double>(h->nb_gT);
+  h->upd_part = al.zeros<double>(3 * (size_t)h->nb_upd);
+  h->res = al.zeros<double>(4);
+  h->hist = al.zeros<double>(3 * (size_t)kHistCap);
+  h->tol = al.zeros<double>(1);
+  h->iter = al.zeros<long long>(1);
+  h->done = al.zeros<int>(1);
+  h->numerical = al.zeros<int>(1);
+  h->capped = al.zeros<unsigned long long>(1);
+  psd_init_attributes();
+  SDP_CUDA_TRY(cudaDeviceSynchronize());
+  reset_state(h);
+  rebuild_graph(h);
+  h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return SDP_OK;
+}
+
+void fill_info(sdp_handle h, sdp_info* info) {
+  double res[3];
+  long long it;
+  unsigned long long cap;
+  SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  SDP_CUDA_TRY(cudaMemcpy(res, h->res, 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(long long), cudaMemcpyDeviceToHost));
+  SDP_CUDA_TRY(cudaMemcpy(&cap, h->capped, sizeof(cap), cudaMemcpyDeviceToHost));
+  std::memset(info, 0, sizeof(*info));
+  info->iters = it;
+  info->eps_p = res[0];
+  info->eps_d = res[1];
+  info->objective = res[2];
+  info->setup_s = h->setup_s;
+  info->n = h->n;
+  info->m = h->m;
+  info->N = h->N;
+  info->p = h->p;
+  info->kmin = h->kmin;
+  info->kmax = h->kmax;
+  info->stot = h->stot;
+  info->form = h->form;
+  info->s_diagonal = h->s_diag;
+  info->jacobi_capped = (int64_t)cap;
+  info->launches_per_iter = launches_per_iter(h);
+}
+
+void launch_iterations(sdp_handle h, int32_t iters) {
+  for (int32_t i = 0; i < iters; ++i) {
+    if (h->exec)
+      SDP_CUDA_TRY(cudaGraphLaunch(h->exec, h->stream));
+    else
+      enqueue_iteration(h, h->stream);
+  }
+  SDP_CUDA_TRY(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+void sdp_default_options(sdp_options* opt) {
+  if (!opt) return;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->form = SDP_FORM_PRIMAL;
+  opt->rho = 1.0;
+  opt->device = 0;
+  opt->stream = nullptr;
+  opt->check_every = 10;
+  opt->use_graph = 1;
+  opt->rank = 0;
+  opt->world = 1;
+}
+
+int sdp_setup(const sdp_problem* prob, const sdp_options* opt, sdp_handle* out) {
+  int rc = guarded([&] { return setup_impl(prob, opt, out); });
+  if (rc != SDP_OK && out && *out) {
+    destroy_handle(*out);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+int sdp_step(sdp_handle h, int32_t iters) {
+  return guarded([&] {
+    if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
+    if (iters < 0) throw Error{SDP_E_INVALID_ARG, "iters < 0"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
+    launch_iterations(h, iters);
+    return SDP_OK;
+  });
+}
+
+int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info) {
+  return guarded([&] {
+    if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
+    if (!(tol > 0)) throw Error{SDP_E_INVALID_ARG, "tol must be positive"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SDP_CUDA_TRY(cudaMemcpy(h->tol, &tol, sizeof(double), cudaMemcpyHostToDevice));
+    SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
+    long long it = 0;
+    int done = 0, num = 0;
+    SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
+    while (it < max_iters) {
+      const int chunk = (int)std::min<long long>(h->check_every, max_iters - it);
+      launch_iterations(h, chunk);
+      SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+      SDP_CUDA_TRY(cudaMemcpy(&done, h->done, sizeof(int), cudaMemcpyDeviceToHost));
+      SDP_CUDA_TRY(cudaMemcpy(&num, h->numerical, sizeof(int), cudaMemcpyDeviceToHost));
+      SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
+      if (num || done) break;
+    }
+    const double neg = -1.0;
+    SDP_CUDA_TRY(cudaMemcpy(h->tol, &neg, sizeof(double), cudaMemcpyHostToDevice));
+    SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
+    if (info) fill_info(h, info);
+    if (num) throw Error{SDP_E_NUMERICAL, "non-finite residuals (NaN/Inf in the iterates)"};
+    return done ? SDP_OK : SDP_MAX_ITER;
+  });
+}
+
+int sdp_reset(sdp_handle h) {
+  return guarded([&] {
+    if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
+    DeviceGuard dg(h->device);
+    reset_state(h);
+    return SDP_OK;
+  });
+}
+
+int sdp_set_rho(sdp_handle h, double rho) {
+  return guarded([&] {
+    if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
+    if (!(rho > 0) || !std::isfinite(rho)) throw Error{SDP_E_INVALID_ARG, "rho must be positive"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    h->rho = rho;
+    if (h->form == SDP_FORM_PRIMAL) {
+      // r1 depends on rho: recompute it from the current x_k, lambda_k (sprev is unchanged)
+      SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
+      enqueue_scatter(h, h->stream);
+      SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    }
+    rebuild_graph(h);
+    return SDP_OK;
+  });
+}
+
+int sdp_get_info(sdp_handle h, sdp_info* info) {
+  return guarded([&] {
+    if (!h || !info) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    DeviceGuard dg(h->device);
+    fill_info(h, info);
+    int num = 0;
+    SDP_CUDA_TRY(cudaMemcpy(&num, h->numerical, sizeof(int), cudaMemcpyDeviceToHost));
+    if (num) throw Error{SDP_E_NUMERICAL, "non-finite residuals (NaN/Inf in the iterates)"};
+    return SDP_OK;
+  });
+}
+
+int sdp_get_vector(sdp_handle h, int32_t which, double* out) {
+  return guarded([&] {
+    if (!h || !out) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    if (which == SDP_VEC_X || which == SDP_VEC_XMAT) {
+      SDP_CUDA_TRY(cudaMemcpy(out, h->x, h->N * sizeof(double), cudaMemcpyDeviceToHost));
+      if (which == SDP_VEC_XMAT)
+        for (int64_t t = 0; t < h->N; ++t)
+          if (h->coord_row[t] != h->coord_col[t]) out[t] /= kSqrt2;
+    } else if (which == SDP_VEC_Y) {
+      SDP_CUDA_TRY(cudaMemcpy(out, h->y, h->m * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+      throw Error{SDP_E_INVALID_ARG, "unknown vector id"};
+    }
+    return SDP_OK;
+  });
+}
+
+int sdp_get_blocks(sdp_handle h, int32_t which, double* out) {
+  return guarded([&] {
+    if (!h || !out) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    const double* src = which == SDP_BLK_XK ? h->xk : which == SDP_BLK_LAMBDA ? h->lam : which == SDP_BLK_VK ? h->vk : nullptr;
+    if (!src) throw Error{SDP_E_INVALID_ARG, "unknown block id"};
+    SDP_CUDA_TRY(cudaMemcpy(out, src, h->stot * sizeof(double), cudaMemcpyDeviceToHost));
+    return SDP_OK;
+  });
+}
+
+int sdp_get_pattern(sdp_handle h, int32_t* row, int32_t* col) {
+  return guarded([&] {
+    if (!h || !row || !col) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    std::memcpy(row, h->coord_row.data(), h->N * sizeof(int32_t));
+    std::memcpy(col, h->coord_col.data(), h->N * sizeof(int32_t));
+    return SDP_OK;
+  });
+}
+
+int sdp_get_cliques(sdp_handle h, int32_t* sizes, int32_t* vertices) {
+  return guarded([&] {
+    if (!h || !sizes || !vertices) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    std::memcpy(sizes, h->clique_size.data(), h->clique_size.size() * sizeof(int32_t));
+    std::memcpy(vertices, h->clique_vert.data(), h->clique_vert.size() * sizeof(int32_t));
+    return SDP_OK;
+  });
+}
+
+int sdp_get_history(sdp_handle h, double* out, int64_t cap, int64_t* rows) {
+  return guarded([&] {
+    if (!h || !out || !rows) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    long long it = 0;
+    SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
+    const int64_t r = std::min<int64_t>(std::min<int64_t>(it, kHistCap), cap);
+    if (r > 0) SDP_CUDA_TRY(cudaMemcpy(out, h->hist, 3 * r * sizeof(double), cudaMemcpyDeviceToHost));
+    *rows = r;
+    return SDP_OK;
+  });
+}
+
+int sdp_profile_phases(sdp_handle h, int32_t iters, double* out_ms) {
+  return guarded([&] {
+    if (!h || !out_ms || iters <= 0) throw Error{SDP_E_INVALID_ARG, "bad argument"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
+    std::vector<cudaEvent_t> ev(16 * (size_t)iters);
+    for (auto& e : ev) SDP_CUDA_TRY(cudaEventCreate(&e));
+    std::vector<int> ids;
+    int idx = 0;
+    for (int it = 0; it < iters; ++it) {
+      g_phase.ev = &ev;
+      g_phase.idx = &idx;
+      g_phase_n = 0;
+      enqueue_iteration(h, h->stream);
+      for (int i = 0; i < g_phase_n; ++i) ids.push_back(g_phase_id[i]);
+    }
+    g_phase.ev = nullptr;
+    g_phase.idx = nullptr;
+    SDP_CUDA_TRY(cudaGetLastError());
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    for (int p = 0; p < SDP_NUM_PHASES; ++p) out_ms[p] = 0.0;
+    // consecutive marks (i, i+1) inside one iteration delimit phase ids[i]
+    const int per = (int)ids.size() / iters;
+    for (int it = 0; it < iters; ++it)
+      for (int i = 0; i + 1 < per; ++i) {
+        float ms = 0.f;
+        SDP_CUDA_TRY(cudaEventElapsedTime(&ms, ev[it * per + i], ev[it * per + i + 1]));
+        const int ph = ids[it * per + i];
+        if (ph < SDP_NUM_PHASES) out_ms[ph] += ms / iters;
+      }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return SDP_OK;
+  });
+}
+
+int sdp_destroy(sdp_handle h) {
+  return guarded([&] {
+    destroy_handle(h);
+    return SDP_OK;
+  });
+}
+
+int sdp_chordal_cliques(int32_t n, int64_t nnz, const int32_t* row, const int32_t* col, int32_t* p, int32_t* sizes,
+                        int64_t cap_vertices, int32_t* vertices, int64_t* nv, int64_t* fill_edges) {
+  return guarded([&] {
+    if (n <= 0) throw Error{SDP_E_INVALID_ARG, "n <= 0"};
+    if (nnz > 0 && (!row || !col)) throw Error{SDP_E_INVALID_ARG, "NULL pattern"};
+    if (!p || !sizes || !vertices || !nv) throw Error{SDP_E_INVALID_ARG, "NULL output"};
+    check_indices("pattern", nnz, row, col, n);
+    std::vector<std::pair<int32_t, int32_t>> edges;
+    for (int64_t e = 0; e < nnz; ++e)
+      if (row[e] != col[e]) edges.push_back({row[e], col[e]});
+    ChordalResult cr = chordal_analysis(n, edges);
+    int64_t tot = 0;
+    for (auto& c : cr.cliques) tot += (int64_t)c.size();
+    *p = (int32_t)cr.cliques.size();
+    *nv = tot;
+    if (fill_edges) *fill_edges = cr.fill_edges;
+    if (tot > cap_vertices) throw Error{SDP_E_INVALID_ARG, "vertices buffer too small"};
+    int64_t e = 0;
+    for (size_t k = 0; k < cr.cliques.size(); ++k) {
+      sizes[k] = (int32_t)cr.cliques[k].size();
+      for (int v : cr.cliques[k]) vertices[e++] = v;
+    }
+    return SDP_OK;
+  });
+}
+
+int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, sdp_psd_plan* out) {
+  sdp_psd_plan pl = nullptr;
+  int rc = guarded([&] {
+    if (!out) throw Error{SDP_E_INVALID_ARG, "out is NULL"};
+    *out = nullptr;
+    if (count < 0 || (count > 0 && !h_sizes)) throw Error{SDP_E_INVALID_ARG, "bad sizes"};
+    if (count >= (1ll << 31)) throw Error{SDP_E_INVALID_ARG, "count too large"};
+    int ndev = 0;
+    SDP_CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Error{SDP_E_INVALID_ARG, "bad device ordinal"};
+    DeviceGuard dg(device);
+    pl = new sdp_psd_plan_s();
+    pl->device = device;
+    pl->count = count;
+    std::vector<int64_t> off(count + 1, 0);
+    std::vector<int32_t> ksz(h_sizes, h_sizes + count);
+    for (int64_t i = 0; i < count; ++i) {
+      const int k = ksz[i];
+      if (k < 1 || k > SDP_MAX_K)
+        throw Error{SDP_E_INVALID_ARG, "matrix " + std::to_string(i) + " has order outside [1, SDP_MAX_K]"};
+      off[i + 1] = off[i] + (int64_t)k * (k + 1) / 2;
+    }
+    pl->values = off[count];
+    pl->d_off = pl->alloc.upload(off);
+    pl->d_ksz = pl->alloc.upload(ksz);
+    build_buckets(pl->alloc, ksz, pl->d_ids, pl->bcount, pl->work, pl->work_slots, pl->ld_work);
+    pl->capped = pl->alloc.zeros<unsigned long long>(1);
+    psd_init_attributes();
+    *out = pl;
+    return SDP_OK;
+  });
+  if (rc != SDP_OK && pl) {
+    pl->alloc.free_all();
+    delete pl;
+  }
+  return rc;
+}
+
+int sdp_project_psd_batch(sdp_psd_plan pl, const double* d_in, double* d_out, void* stream) {
+  return guarded([&] {
+    if (!pl) throw Error{SDP_E_INVALID_ARG, "plan is NULL"};
+    if (pl->values > 0 && (!d_in || !d_out)) throw Error{SDP_E_INVALID_ARG, "NULL data pointer"};
+    DeviceGuard dg(pl->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    ProjArgs a{};
+    a.off = pl->d_off;
+    a.ksz = pl->d_ksz;
+    a.in = d_in;
+    a.out = d_out;
+    a.work = pl->work;
+    a.work_slots = pl->work_slots;
+    a.ld_work = pl->ld_work;
+    a.capped = pl->capped;
+    a.done = nullptr;
+    for (int b = B_NUM - 1; b >= 0; --b) {
+      if (!pl->bcount[b]) continue;
+      a.ids = pl->d_ids[b];
+      a.count = pl->bcount[b];
+      launch_projection(b, PM_BATCH, a, s);
+    }
+    SDP_CUDA_TRY(cudaGetLastError());
+    return SDP_OK;
+  });
+}
+
+int sdp_project_psd_batch_host(sdp_psd_plan pl, const double* h_in, double* h_out, void* stream) {
+  return guarded([&] {
+    if (!pl) throw Error{SDP_E_INVALID_ARG, "plan is NULL"};
+    if (pl->values > 0 && (!h_in || !h_out)) throw Error{SDP_E_INVALID_ARG, "NULL data pointer"};
+    DeviceGuard dg(pl->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!pl->h_in_dev) {
+      pl->h_in_dev = pl->alloc.get<double>(pl->values);
+      pl->h_out_dev = pl->alloc.get<double>(pl->values);
+    }
+    SDP_CUDA_TRY(cudaMemcpyAsync(pl->h_in_dev, h_in, pl->values * sizeof(double), cudaMemcpyHostToDevice, s));
+    int rc = sdp_project_psd_batch(pl, pl->h_in_dev, pl->h_out_dev, stream);
+    if (rc != SDP_OK) return rc;
+    SDP_CUDA_TRY(cudaMemcpyAsync(h_out, pl->h_out_dev, pl->values * sizeof(double), cudaMemcpyDeviceToHost, s));
+    SDP_CUDA_TRY(cudaStreamSynchronize(s));
+    return SDP_OK;
+  });
+}
+
+int64_t sdp_psd_plan_values(sdp_psd_plan pl) { return pl ? pl->values : -1; }
+
+int sdp_psd_plan_destroy(sdp_psd_plan pl) {
+  return guarded([&] {
+    if (!pl) return SDP_OK;
+    int cur = -1;
+    cudaGetDevice(&cur);
+    cudaSetDevice(pl->device);
+    cudaDeviceSynchronize();
+    pl->alloc.free_all();
+    if (cur >= 0) cudaSetDevice(cur);
+    delete pl;
+    return SDP_OK;
+  });
+}
+
+const char* sdp_last_error(void) { return g_err.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// Internal declarations shared by the host setup, the kernels and the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/chordal_sdp.h"
+
+namespace sdp {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+#define SDP_CUDA_TRY(expr)                                                                   \
+  do {                                                                                       \
+    cudaError_t _e = (expr);                                                                 \
+    if (_e != cudaSuccess)                                                                   \
+      throw ::sdp::Error{_e == cudaErrorMemoryAllocation ? SDP_E_OOM : SDP_E_CUDA,           \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e)};                \
+  } while (0)
+
+// ---------------------------------------------------------------- host setup
+// Chordal analysis (setup_host.cpp).
+struct ChordalResult {
+  std::vector<std::vector<int32_t>> cliques;  // sorted inside, list sorted lexicographically
+  // extended pattern, canonical (column-major upper) order
+  std::vector<int32_t> coord_row, coord_col;
+  std::vector<int64_t> col_ptr;  // coordinates of column j are [col_ptr[j], col_ptr[j+1])
+  int64_t fill_edges = 0;
+};
+// edges: off-diagonal upper pairs (i<j), may contain duplicates
+ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges);
+int64_t coord_index(const ChordalResult& cr, int32_t i, int32_t j);  // -1 if absent
+
+// ---------------------------------------------------------------- projection buckets
+// Kernel tiers for the batched eigen-projection (kernels_psd.cu).
+enum BucketKind { B_G8 = 0, B_G16 = 1, B_G32 = 2, B_CTA64 = 3, B_CTA96 = 4, B_GLOBAL = 5, B_NUM = 6 };
+int bucket_of(int k);
+
+// Projection modes
+enum ProjMode { PM_BATCH = 0, PM_PRIMAL = 1, PM_DUAL = 2 };
+
+struct ProjArgs {
+  const int64_t* off;   // per task: offset of its packed values
+  const int32_t* ksz;   // per task: order k
+  const int32_t* ids;   // bucket list of task ids
+  int32_t count;        // tasks in this bucket
+  // batch mode
+  const double* in;
+  double* out;
+  // ADMM modes
+  const double* x;      // N, global iterate (primal gather source)
+  const int32_t* G;     // stacked -> coordinate map
+  double* xk;           // stacked x_k / z_k (output)
+  double* lam;          // stacked lambda_k (primal: updated in place)
+  const double* vk;     // dual: stacked v_k
+  double rho;
+  double* part;         // primal: per task 3 partials (|xk-hx|^2, |xk|^2, |hx|^2)
+  double* work;         // global workspace for B_GLOBAL (2 * kmax_even^2 doubles per slot)
+  int32_t work_slots;
+  int32_t ld_work;
+  unsigned long long* capped;  // count of sweep-capped projections
+  const int32_t* done;  // device stop flag (skip work when set)
+};
+
+void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
+
+}  // namespace sdp

@@ -1,0 +1,401 @@
+// Batched projection onto the PSD cone, P_k(X) = V max(Lambda, 0) V^T
+// (E:XkUpdate P:244-253, E:zkUpdate P:403-410), for every clique block or
+// every matrix of a batch.
+//
+// Eigendecomposition: two-sided cyclic Jacobi with the parallel round-robin
+// ("circle") ordering: every step applies kp/2 disjoint rotations at once, a
+// sweep is kp-1 steps and covers every pair once.  Rotations follow Golub &
+// Van Loan's sym.schur2; the sweep stops when off(A)_F <= 1e-15 ||A||_F
+// (reading G16) or after 30 sweeps (counted in `capped`).  Eigenvalues
+// are clipped at exactly 0 (reading G15) and the projection is rebuilt as
+// sum_t max(l_t,0) v_t v_t^T.
+//
+// Tiers (bucket_of): a group of G lanes owns one matrix held in shared memory
+//   G8  : 8 lanes,  k <= 8   (16 matrices per 128-thread CTA)
+//   G16 : 16 lanes, k <= 16  (8 per CTA)
+//   G32 : one warp, k <= 32  (4 per CTA)
+//   CTA64: 128 threads, k <= 64;  CTA96: 256 threads, k <= 96
+//   GLOBAL: 256 threads, k <= SDP_MAX_K, A and V in an L2-resident global workspace
+// Odd k is padded with one zero row/column (exact: P_+(diag(X,0)) = diag(P_+(X),0)).
+#include <cmath>
+
+#include "internal.h"
+
+namespace sdp {
+
+namespace {
+
+constexpr double kInvSqrt2 = 0.70710678118654752440;
+constexpr double kSqrt2 = 1.41421356237309504880;
+constexpr int kMaxSweeps = 30;
+constexpr double kJacTol = 1e-15;
+
+__device__ __forceinline__ void packed_rc(int e, int& r, int& c) {
+  int cc = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  while ((cc + 1) * (cc + 2) / 2 <= e) ++cc;
+  while (cc * (cc + 1) / 2 > e) --cc;
+  c = cc;
+  r = e - cc * (cc + 1) / 2;
+}
+
+template <int G>
+struct Group {
+  int tid;
+  unsigned mask;
+  double* red;  // CTA-level reduction scratch (G > 32), >= G/32 + 1 doubles
+  __device__ __forceinline__ void sync() const {
+    if constexpr (G <= 32)
+      __syncwarp(mask);
+    else
+      __syncthreads();
+  }
+  // Deterministic sum over the group; every member receives the same value.
+  __device__ __forceinline__ double sum(double v) const {
+    if constexpr (G <= 32) {
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o, G);
+      return v;
+    } else {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      const int w = tid >> 5;
+      __syncthreads();
+      if ((tid & 31) == 0) red[w] = v;
+      __syncthreads();
+      double s = 0.0;
+#pragma unroll 1
+      for (int i = 0; i < G / 32; ++i) s += red[i];
+      return s;
+    }
+  }
+};
+
+struct Rot {
+  int* p;
+  int* q;
+  double* c;
+  double* s;
+  double* t;
+};
+
+template <int G, int MODE>
+__device__ void project_matrix(const Group<G>& g, const int k, const int64_t off, const int task,
+                               double* __restrict__ A, double* __restrict__ V, const int ld, Rot rot,
+                               const ProjArgs& a) {
+  const int kp = k + (k & 1);
+  const int P = kp >> 1;
+  const int ns = k * (k + 1) / 2;
+  // ---- load (gather H_k x for the primal form) ----
+  for (int e = g.tid; e < ns; e += G) {
+    int r, c;
+    packed_rc(e, r, c);
+    double v;
+    if constexpr (MODE == PM_BATCH) {
+      v = a.in[off + e];
+    } else if constexpr (MODE == PM_PRIMAL) {
+      const double hx = __ldg(a.x + a.G[off + e]);
+      v = hx - a.lam[off + e] / a.rho;
+      if (r != c) v *= kInvSqrt2;
+    } else {
+      v = a.vk[off + e] - a.lam[off + e] / a.rho;
+      if (r != c) v *= kInvSqrt2;
+    }
+    A[r * ld + c] = v;
+    A[c * ld + r] = v;
+  }
+  if (k & 1) {
+    for (int e = g.tid; e < kp; e += G) {
+      A[k * ld + e] = 0.0;
+      A[e * ld + k] = 0.0;
+    }
+  }
+  for (int e = g.tid; e < kp * kp; e += G) {
+    const int r = e / kp, c = e - r * kp;
+    V[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  }
+  g.sync();
+  double fro2 = 0.0;
+  for (int e = g.tid; e < kp * kp; e += G) {
+    const int r = e / kp, c = e - r * kp;
+    const double v = A[r * ld + c];
+    fro2 += v * v;
+  }
+  fro2 = g.sum(fro2);
+  const double thr = kJacTol * kJacTol * fro2;
+  const int nblk = P * (P + 1) / 2;
+  int sweep = 0;
+  for (; sweep < kMaxSweeps; ++sweep) {
+    double off2 = 0.0;
+    for (int e = g.tid; e < kp * kp; e += G) {
+      const int r = e / kp, c = e - r * kp;
+      if (r != c) {
+        const double v = A[r * ld + c];
+        off2 += v * v;
+      }
+    }
+    off2 = g.sum(off2);
+    if (off2 <= thr) break;
+    for (int step = 0; step < kp - 1; ++step) {
+      // rotation parameters of the P disjoint pairs of this step
+      for (int i = g.tid; i < P; i += G) {
+        const int p = (i == 0) ? 0 : 1 + (i - 1 + step) % (kp - 1);
+        const int q = 1 + (kp - 2 - i + step) % (kp - 1);
+        const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
+        double cs = 1.0, sn = 0.0, t = 0.0;
+        if (apq != 0.0) {
+          const double tau = (aqq - app) / (2.0 * apq);
+          const double at = fabs(tau);
+          t = (at > 1e150) ? 0.5 / tau : copysign(1.0, tau) / (at + sqrt(1.0 + tau * tau));
+          cs = 1.0 / sqrt(1.0 + t * t);
+          sn = t * cs;
+        }
+        rot.p[i] = p;
+        rot.q[i] = q;
+        rot.c[i] = cs;
+        rot.s[i] = sn;
+        rot.t[i] = t;
+      }
+      g.sync();
+      // A <- J^T A J on the 2x2 blocks (i <= j) of the pair partition, mirrored
+      for (int b = g.tid; b < nblk; b += G) {
+        int i, j;
+        packed_rc(b, i, j);
+        const int p1 = rot.p[i], q1 = rot.q[i];
+        if (i == j) {
+          const double apq = A[p1 * ld + q1], t = rot.t[i];
+          A[p1 * ld + p1] -= t * apq;
+          A[q1 * ld + q1] += t * apq;
+          A[p1 * ld + q1] = 0.0;
+          A[q1 * ld + p1] = 0.0;
+        } else {
+          const int p2 = rot.p[j], q2 = rot.q[j];
+          const double c1 = rot.c[i], s1 = rot.s[i], c2 = rot.c[j], s2 = rot.s[j];
+          const double b00 = A[p1 * ld + p2], b01 = A[p1 * ld + q2];
+          const double b10 = A[q1 * ld + p2], b11 = A[q1 * ld + q2];
+          // rows: J_i^T B
+          const double r00 = c1 * b00 - s1 * b10, r01 = c1 * b01 - s1 * b11;
+          const double r10 = s1 * b00 + c1 * b10, r11 = s1 * b01 + c1 * b11;
+          // cols: (J_i^T B) J_j
+          const double n00 = c2 * r00 - s2 * r01, n01 = s2 * r00 + c2 * r01;
+          const double n10 = c2 * r10 - s2 * r11, n11 = s2 * r10 + c2 * r11;
+          A[p1 * ld + p2] = n00;
+          A[p2 * ld + p1] = n00;
+          A[p1 * ld + q2] = n01;
+          A[q2 * ld + p1] = n01;
+          A[q1 * ld + p2] = n10;
+          A[p2 * ld + q1] = n10;
+          A[q1 * ld + q2] = n11;
+          A[q2 * ld + q1] = n11;
+        }
+      }
+      // V <- V J
+      for (int e = g.tid; e < kp * P; e += G) {
+        const int r = e / P, i = e - r * P;
+        const int p = rot.p[i], q = rot.q[i];
+        const double cs = rot.c[i], sn = rot.s[i];
+        const double vp = V[r * ld + p], vq = V[r * ld + q];
+        V[r * ld + p] = cs * vp - sn * vq;
+        V[r * ld + q] = sn * vp + cs * vq;
+      }
+      g.sync();
+    }
+  }
+  if (sweep == kMaxSweeps && g.tid == 0 && a.capped) atomicAdd(a.capped, 1ull);
+  // ---- reconstruction sum_t max(l_t,0) v_t v_t^T, then the mode epilogue ----
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+  for (int e = g.tid; e < ns; e += G) {
+    int r, c;
+    packed_rc(e, r, c);
+    double acc = 0.0;
+    for (int t = 0; t < kp; ++t) {
+      const double l = A[t * ld + t];
+      if (l > 0.0) acc += l * V[r * ld + t] * V[c * ld + t];
+    }
+    if constexpr (MODE == PM_BATCH) {
+      a.out[off + e] = acc;
+    } else if constexpr (MODE == PM_PRIMAL) {
+      // E:LambdakUpdate: lambda_k += rho (x_k - H_k x)
+      const double xkv = (r == c) ? acc : acc * kSqrt2;
+      const double hx = __ldg(a.x + a.G[off + e]);
+      const double d = xkv - hx;
+      a.xk[off + e] = xkv;
+      a.lam[off + e] = a.lam[off + e] + a.rho * d;
+      p0 += d * d;
+      p1 += xkv * xkv;
+      p2 += hx * hx;
+    } else {
+      a.xk[off + e] = (r == c) ? acc : acc * kSqrt2;
+    }
+  }
+  if constexpr (MODE == PM_PRIMAL) {
+    p0 = g.sum(p0);
+    p1 = g.sum(p1);
+    p2 = g.sum(p2);
+    if (g.tid == 0) {
+      a.part[3 * (int64_t)task + 0] = p0;
+      a.part[3 * (int64_t)task + 1] = p1;
+      a.part[3 * (int64_t)task + 2] = p2;
+    }
+  }
+  g.sync();
+}
+
+// --- small tiers: G lanes per matrix, NG groups per 128-thread CTA ---------
+template <int G, int KMAX, int MODE>
+__global__ void __launch_bounds__(128) k_psd_small(ProjArgs a) {
+  if (a.done && *a.done) return;
+  constexpr int NG = 128 / G;
+  constexpr int LD = KMAX + 1;
+  constexpr int P = KMAX / 2;
+  extern __shared__ double smem[];
+  const int grp = threadIdx.x / G;
+  const int task_slot = blockIdx.x * NG + grp;
+  if (task_slot >= a.count) return;
+  double* base = smem + (size_t)grp * (2 * KMAX * LD + 3 * P + P);
+  double* A = base;
+  double* V = base + KMAX * LD;
+  double* rc = V + KMAX * LD;
+  double* rs = rc + P;
+  double* rt = rs + P;
+  int* rpq = (int*)(rt + P);
+  Rot rot{rpq, rpq + P, rc, rs, rt};
+  Group<G> g;
+  g.tid = threadIdx.x % G;
+  g.mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
+  g.red = nullptr;
+  const int task = a.ids ? a.ids[task_slot] : task_slot;
+  project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, LD, rot, a);
+}
+
+template <int G, int KMAX>
+constexpr size_t small_smem() {
+  return (size_t)(128 / G) * (2 * KMAX * (KMAX + 1) + 4 * (KMAX / 2)) * sizeof(double);
+}
+
+// --- CTA tiers: one CTA per matrix, A and V in shared memory ---------------
+template <int G, int KMAX, int MODE>
+__global__ void __launch_bounds__(G) k_psd_cta(ProjArgs a) {
+  if (a.done && *a.done) return;
+  constexpr int LD = KMAX + 1;
+  constexpr int P = KMAX / 2;
+  extern __shared__ double smem[];
+  double* A = smem;
+  double* V = A + KMAX * LD;
+  double* rc = V + KMAX * LD;
+  double* rs = rc + P;
+  double* rt = rs + P;
+  int* rpq = (int*)(rt + P);
+  double* red = (double*)(rpq + 2 * P);
+  Rot rot{rpq, rpq + P, rc, rs, rt};
+  Group<G> g;
+  g.tid = threadIdx.x;
+  g.mask = 0xffffffffu;
+  g.red = red;
+  for (int slot = blockIdx.x; slot < a.count; slot += gridDim.x) {
+    const int task = a.ids ? a.ids[slot] : slot;
+    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, LD, rot, a);
+  }
+}
+
+template <int G, int KMAX>
+constexpr size_t cta_smem() {
+  return (size_t)(2 * KMAX * (KMAX + 1) + 4 * (KMAX / 2) + G / 32 + 2) * sizeof(double);
+}
+
+// --- GLOBAL tier: A, V in a global (L2-resident) workspace slot per CTA -----
+template <int G, int MODE>
+__global__ void __launch_bounds__(G) k_psd_global(ProjArgs a) {
+  if (a.done && *a.done) return;
+  constexpr int PMAX = SDP_MAX_K / 2;
+  __shared__ double rc[PMAX], rs[PMAX], rt[PMAX];
+  __shared__ int rpq[2 * PMAX];
+  __shared__ double red[G / 32 + 2];
+  Rot rot{rpq, rpq + PMAX, rc, rs, rt};
+  Group<G> g;
+  g.tid = threadIdx.x;
+  g.mask = 0xffffffffu;
+  g.red = red;
+  const int ld = a.ld_work;
+  double* A = a.work + (size_t)blockIdx.x * 2 * ld * ld;
+  double* V = A + (size_t)ld * ld;
+  for (int slot = blockIdx.x; slot < a.count; slot += gridDim.x) {
+    const int task = a.ids ? a.ids[slot] : slot;
+    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, ld, rot, a);
+  }
+}
+
+template <int MODE>
+void launch_mode(int bucket, const ProjArgs& a, cudaStream_t s) {
+  if (a.count <= 0) return;
+  switch (bucket) {
+    case B_G8: {
+      constexpr size_t sm = small_smem<8, 8>();
+      k_psd_small<8, 8, MODE><<<(a.count + 15) / 16, 128, sm, s>>>(a);
+      break;
+    }
+    case B_G16: {
+      constexpr size_t sm = small_smem<16, 16>();
+      k_psd_small<16, 16, MODE><<<(a.count + 7) / 8, 128, sm, s>>>(a);
+      break;
+    }
+    case B_G32: {
+      constexpr size_t sm = small_smem<32, 32>();
+      k_psd_small<32, 32, MODE><<<(a.count + 3) / 4, 128, sm, s>>>(a);
+      break;
+    }
+    case B_CTA64: {
+      constexpr size_t sm = cta_smem<128, 64>();
+      k_psd_cta<128, 64, MODE><<<a.count, 128, sm, s>>>(a);
+      break;
+    }
+    case B_CTA96: {
+      constexpr size_t sm = cta_smem<256, 96>();
+      k_psd_cta<256, 96, MODE><<<a.count, 256, sm, s>>>(a);
+      break;
+    }
+    case B_GLOBAL: {
+      const int grid = a.count < a.work_slots ? a.count : a.work_slots;
+      k_psd_global<256, MODE><<<grid, 256, 0, s>>>(a);
+      break;
+    }
+  }
+}
+
+template <int MODE>
+void init_attrs_mode() {
+  cudaFuncSetAttribute(k_psd_small<32, 32, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)small_smem<32, 32>());
+  cudaFuncSetAttribute(k_psd_cta<128, 64, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)cta_smem<128, 64>());
+  cudaFuncSetAttribute(k_psd_cta<256, 96, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)cta_smem<256, 96>());
+}
+
+}  // namespace
+
+// Opt the large-shared-memory tiers into > 48 KB (per device; call before capture).
+void psd_init_attributes() {
+  init_attrs_mode<PM_BATCH>();
+  init_attrs_mode<PM_PRIMAL>();
+  init_attrs_mode<PM_DUAL>();
+}
+
+int bucket_of(int k) {
+  if (k <= 8) return B_G8;
+  if (k <= 16) return B_G16;
+  if (k <= 32) return B_G32;
+  if (k <= 64) return B_CTA64;
+  if (k <= 96) return B_CTA96;
+  return B_GLOBAL;
+}
+
+void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s) {
+  if (mode == PM_BATCH)
+    launch_mode<PM_BATCH>(bucket, a, s);
+  else if (mode == PM_PRIMAL)
+    launch_mode<PM_PRIMAL>(bucket, a, s);
+  else
+    launch_mode<PM_DUAL>(bucket, a, s);
+}
+
+}  // namespace sdp

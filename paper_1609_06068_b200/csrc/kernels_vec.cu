@@ -1,0 +1,536 @@
+// Per-iteration vector kernels of Algorithms 1 and 2 (everything except the
+// clique projection):
+//   scatter   r1 = sum_k H_k^T(.)  (E:OptCondMinYPrimal / E:OptCondMinYDual rhs)
+//   gemv      u  = A (D^-1 r1) - r2           (block elimination)
+//   trsv      y  = L^-T L^-1 u  with the cached inverse factor W = L^-1
+//   gemvT     x  = D^-1 (r1 - A^T y)
+//   update    v_k, lambda_k of the dual (E:vkEqn, E:MultUpdateDualSDP)
+//   finalize  eps_p, eps_d, objective, stop flag   (reading G9)
+// All reductions are deterministic (fixed assignment and fixed tree order; no
+// floating-point atomics), so two runs give bit-identical iterates.
+#include "kernels_vec.h"
+
+namespace sdp {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide deterministic sum of NV values per thread; result valid in thread 0.
+template <int NV, int NT>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* sm /* NV*NT/32 */) {
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) sm[j * (NT / 32) + w] = v[j];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double s = 0.0;
+#pragma unroll 1
+      for (int i = 0; i < NT / 32; ++i) s += sm[j * (NT / 32) + i];
+      v[j] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- scatter
+// Primal (E:OptCondMinYPrimal):  r1 = sum_k H_k^T (x_k + lam_k/rho) - c/rho
+// Dual   (E:OptCondMinYDual):    r1 = c - sum_k H_k^T (z_k + lam_k/rho)
+// Writes rD = r1 / D.  Residual partials: |sum H^T x_k - previous|^2 and
+// (primal) |sum H^T lam_k|^2; previous <- sum H^T x_k.
+// Coordinates with short segments: one thread each; long segments (listed
+// in `longc`): one warp each.
+template <int FORM>
+__global__ void __launch_bounds__(256) k_scatter(ScatterArgs a) {
+  if (a.done && *a.done) return;
+  __shared__ double sm[2 * 8];
+  double acc[2] = {0.0, 0.0};
+  const int nb_short = (a.N + 255) / 256;
+  if ((int)blockIdx.x < nb_short) {
+    const int t = blockIdx.x * 256 + threadIdx.x;
+    if (t < a.N) {
+      const int b = a.seg_ptr[t], e = a.seg_ptr[t + 1];
+      if (e - b <= kLongSeg) {
+        double sr = 0.0, sx = 0.0, sl = 0.0;
+        for (int i = b; i < e; ++i) {
+          const int s = a.seg_idx[i];
+          const double xv = a.xk[s], lv = a.lam[s];
+          sr += xv + lv / a.rho;
+          sx += xv;
+          sl += lv;
+        }
+        const double r1 = (FORM == 0) ? sr - a.c[t] / a.rho : a.c[t] - sr;
+        a.rD[t] = r1 * a.Dinv[t];
+        const double d = sx - a.sprev[t];
+        a.sprev[t] = sx;
+        acc[0] = d * d;
+        acc[1] = sl * sl;
+      }
+    }
+  } else {
+    const int warp = (blockIdx.x - nb_short) * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (warp < a.n_long) {
+      const int t = a.longc[warp];
+      const int b = a.seg_ptr[t], e = a.seg_ptr[t + 1];
+      double sr = 0.0, sx = 0.0, sl = 0.0;
+      for (int i = b + lane; i < e; i += 32) {
+        const int s = a.seg_idx[i];
+        const double xv = a.xk[s], lv = a.lam[s];
+        sr += xv + lv / a.rho;
+        sx += xv;
+        sl += lv;
+      }
+      sr = warp_sum(sr);
+      sx = warp_sum(sx);
+      sl = warp_sum(sl);
+      if (lane == 0) {
+        const double r1 = (FORM == 0) ? sr - a.c[t] / a.rho : a.c[t] - sr;
+        a.rD[t] = r1 * a.Dinv[t];
+        const double d = sx - a.sprev[t];
+        a.sprev[t] = sx;
+        acc[0] = d * d;
+        acc[1] = sl * sl;
+      }
+    }
+  }
+  block_sum<2, 256>(acc, sm);
+  if (threadIdx.x == 0) {
+    a.part[2 * blockIdx.x + 0] = acc[0];
+    a.part[2 * blockIdx.x + 1] = acc[1];
+  }
+}
+
+// ---------------------------------------------------------------- dense GEMV
+// part[chunk][i] = sum_{t in chunk} A[i][t] * v[t]; A row-major m x lda (lda
+// even, zero padded), v zero padded to lda.  Grid (m/RB, nchunks), 256 threads,
+// every thread streams RB rows with 16-byte evict-first loads.
+template <int RB>
+__global__ void __launch_bounds__(256) k_gemv_dense(const double* __restrict__ A, int64_t lda, int m,
+                                                     const double* __restrict__ v, int chunk,
+                                                     double* __restrict__ part, const int* done) {
+  if (done && *done) return;
+  __shared__ double sm[RB * 8];
+  const int row0 = blockIdx.x * RB;
+  const int64_t c0 = (int64_t)blockIdx.y * chunk;
+  const int64_t c1 = (c0 + chunk < lda) ? c0 + chunk : lda;
+  double acc[RB];
+  const double2* Ar[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    acc[r] = 0.0;
+    const int rr = (row0 + r < m) ? row0 + r : m - 1;
+    Ar[r] = reinterpret_cast<const double2*>(A + (int64_t)rr * lda);
+  }
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+#pragma unroll 4
+  for (int64_t t = c0 / 2 + threadIdx.x; t < c1 / 2; t += 256) {
+    const double2 vv = __ldg(v2 + t);
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const double2 aa = __ldcs(Ar[r] + t);
+      acc[r] = fma(aa.x, vv.x, acc[r]);
+      acc[r] = fma(aa.y, vv.y, acc[r]);
+    }
+  }
+  block_sum<RB, 256>(acc, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (row0 + r < m) part[(int64_t)blockIdx.y * m + row0 + r] = acc[r];
+  }
+}
+
+// u_i = sum_chunks part[.][i] - r2_i   (r2 = b primal, -b/rho dual);
+// with a diagonal S the KKT solve is elementwise: y_i = u_i / S_ii.
+template <int FORM>
+__global__ void k_reduce_u(const double* __restrict__ part, int nchunks, int m, const double* __restrict__ b,
+                           double rho, double* __restrict__ u, const double* __restrict__ sdiag,
+                           double* __restrict__ y, const int* done) {
+  if (done && *done) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += part[(int64_t)c * m + i];
+  const double ui = (FORM == 0) ? s - b[i] : s - (-b[i] / rho);
+  if (sdiag) {
+    y[i] = ui / sdiag[i];
+  } else {
+    u[i] = ui;
+  }
+}
+
+// Triangular matrix-vector product with the cached inverse factor:
+// out_i = sum_{j in [lo_i, hi_i)} M[i][j] in_j, lower (LOWER=1: j <= i) or upper
+// (j >= i).  One warp per row.
+template <int LOWER>
+__global__ void __launch_bounds__(256) k_trmv(const double* __restrict__ M, int m, const double* __restrict__ in,
+                                               double* __restrict__ out, const int* done) {
+  if (done && *done) return;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const int lo = LOWER ? 0 : row;
+  const int hi = LOWER ? row + 1 : m;
+  const double* Mr = M + (int64_t)row * m;
+  double s = 0.0;
+  for (int j = lo + lane; j < hi; j += 32) s = fma(Mr[j], in[j], s);
+  s = warp_sum(s);
+  if (lane == 0) out[row] = s;
+}
+
+// ---------------------------------------------------------------- dense GEMV^T
+// x_t = rD_t - Dinv_t * sum_i A[i][t] y_i    (x = D^-1 (r1 - A^T y))
+// CTA = 256 threads x 2 columns; y staged in shared memory in tiles.
+// Partials: primal <c, x>; dual |D x|^2 (= |sum_k H_k^T lambda_k|^2 / rho^2).
+template <int FORM>
+__global__ void __launch_bounds__(256) k_gemvT_dense(const double* __restrict__ A, int64_t lda, int m, int N,
+                                                      const double* __restrict__ y, const double* __restrict__ rD,
+                                                      const double* __restrict__ Dinv, const double* __restrict__ c,
+                                                      double* __restrict__ x, double* __restrict__ part,
+                                                      const int* done) {
+  if (done && *done) return;
+  constexpr int TILE = 4096;
+  __shared__ double ys[TILE];
+  __shared__ double sm[8];
+  const int64_t t2 = (int64_t)blockIdx.x * 256 + threadIdx.x;  // column pair index
+  const bool act = 2 * t2 < lda;
+  const double2* Ac = reinterpret_cast<const double2*>(A) + t2;
+  const int64_t ld2 = lda / 2;
+  double w0 = 0.0, w1 = 0.0;
+  for (int r0 = 0; r0 < m; r0 += TILE) {
+    const int nr = (m - r0 < TILE) ? m - r0 : TILE;
+    __syncthreads();
+    for (int i = threadIdx.x; i < nr; i += 256) ys[i] = y[r0 + i];
+    __syncthreads();
+    if (act) {
+      const double2* Ap = Ac + (int64_t)r0 * ld2;
+#pragma unroll 8
+      for (int i = 0; i < nr; ++i) {
+        const double2 aa = __ldcs(Ap + (int64_t)i * ld2);
+        const double yi = ys[i];
+        w0 = fma(aa.x, yi, w0);
+        w1 = fma(aa.y, yi, w1);
+      }
+    }
+  }
+  double acc[1] = {0.0};
+  if (act) {
+    const int64_t t = 2 * t2;
+    if (t < N) {
+      const double xv = rD[t] - Dinv[t] * w0;
+      x[t] = xv;
+      acc[0] += (FORM == 0) ? c[t] * xv : (xv / Dinv[t]) * (xv / Dinv[t]);
+    }
+    if (t + 1 < N) {
+      const double xv = rD[t + 1] - Dinv[t + 1] * w1;
+      x[t + 1] = xv;
+      acc[0] += (FORM == 0) ? c[t + 1] * xv : (xv / Dinv[t + 1]) * (xv / Dinv[t + 1]);
+    }
+  }
+  block_sum<1, 256>(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+}
+
+// ---------------------------------------------------------------- sparse A (CSR / CSC)
+template <int FORM>
+__global__ void __launch_bounds__(256) k_gemv_csr(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                   const double* __restrict__ val, int m, const double* __restrict__ v,
+                                                   const double* __restrict__ b, double rho, double* __restrict__ u,
+                                                   const double* __restrict__ sdiag, double* __restrict__ y,
+                                                   const int* done) {
+  if (done && *done) return;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  double s = 0.0;
+  for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) s = fma(val[e], v[ci[e]], s);
+  s = warp_sum(s);
+  if (lane == 0) {
+    const double ui = (FORM == 0) ? s - b[row] : s - (-b[row] / rho);
+    if (sdiag)
+      y[row] = ui / sdiag[row];
+    else
+      u[row] = ui;
+  }
+}
+
+template <int FORM>
+__global__ void __launch_bounds__(256) k_gemvT_csc(const int32_t* __restrict__ cp, const int32_t* __restrict__ ri,
+                                                    const double* __restrict__ val, int N, const double* __restrict__ y,
+                                                    const double* __restrict__ rD, const double* __restrict__ Dinv,
+                                                    const double* __restrict__ c, double* __restrict__ x,
+                                                    double* __restrict__ part, const int* done) {
+  if (done && *done) return;
+  __shared__ double sm[8];
+  const int t = blockIdx.x * 256 + threadIdx.x;
+  double acc[1] = {0.0};
+  if (t < N) {
+    double w = 0.0;
+    for (int e = cp[t]; e < cp[t + 1]; ++e) w = fma(val[e], y[ri[e]], w);
+    const double xv = rD[t] - Dinv[t] * w;
+    x[t] = xv;
+    acc[0] = (FORM == 0) ? c[t] * xv : (xv / Dinv[t]) * (xv / Dinv[t]);
+  }
+  block_sum<1, 256>(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+}
+
+// ---------------------------------------------------------------- dual update
+// v_k = z_k + lam_k/rho + H_k x  (E:vkEqn);  lam_k = -rho H_k x  (G7)
+__global__ void __launch_bounds__(256) k_update_dual(int64_t stot, const int32_t* __restrict__ G,
+                                                      const double* __restrict__ x, const double* __restrict__ z,
+                                                      double* __restrict__ lam, double* __restrict__ v, double rho,
+                                                      double* __restrict__ part, const int* done) {
+  if (done && *done) return;
+  __shared__ double sm[3 * 8];
+  const int64_t s = (int64_t)blockIdx.x * 256 + threadIdx.x;
+  double acc[3] = {0.0, 0.0, 0.0};
+  if (s < stot) {
+    const double hx = __ldg(x + G[s]);
+    const double zv = z[s];
+    const double vv = zv + lam[s] / rho + hx;
+    v[s] = vv;
+    lam[s] = -rho * hx;
+    const double d = zv - vv;
+    acc[0] = d * d;
+    acc[1] = zv * zv;
+    acc[2] = vv * vv;
+  }
+  block_sum<3, 256>(acc, sm);
+  if (threadIdx.x == 0) {
+    part[3 * blockIdx.x + 0] = acc[0];
+    part[3 * blockIdx.x + 1] = acc[1];
+    part[3 * blockIdx.x + 2] = acc[2];
+  }
+}
+
+// ---------------------------------------------------------------- finalize
+// Single CTA: fixed-order reduction of all partials, residuals (reading G9),
+// objective (G17), history, stop flag.
+template <int FORM>
+__global__ void __launch_bounds__(256) k_finalize(FinalArgs a) {
+  if (*a.done) return;
+  __shared__ double sm[8 * 8];
+  double v[6] = {0, 0, 0, 0, 0, 0};
+  if (FORM == 0) {
+    for (int i = threadIdx.x; i < a.n_proj; i += 256) {
+      v[0] += a.proj_part[3 * i + 0];
+      v[1] += a.proj_part[3 * i + 1];
+      v[2] += a.proj_part[3 * i + 2];
+    }
+  } else {
+    for (int i = threadIdx.x; i < a.n_upd; i += 256) {
+      v[0] += a.upd_part[3 * i + 0];
+      v[1] += a.upd_part[3 * i + 1];
+      v[2] += a.upd_part[3 * i + 2];
+    }
+  }
+  for (int i = threadIdx.x; i < a.n_scat; i += 256) {
+    v[3] += a.scat_part[2 * i + 0];
+    v[4] += a.scat_part[2 * i + 1];
+  }
+  for (int i = threadIdx.x; i < a.n_gT; i += 256) v[5] += a.gT_part[i];
+  double w[1] = {0.0};
+  if (FORM == 1)
+    for (int i = threadIdx.x; i < a.m; i += 256) w[0] += a.b[i] * a.y[i];
+  block_sum<6, 256>(v, sm);
+  __syncthreads();
+  block_sum<1, 256>(w, sm + 48);
+  if (threadIdx.x == 0) {
+    const double np = sqrt(v[0]);
+    const double den_p = fmax(fmax(sqrt(v[1]), sqrt(v[2])), 1.0);
+    const double eps_p = np / den_p;
+    double eps_d, obj;
+    if (FORM == 0) {
+      eps_d = a.rho * sqrt(v[3]) / fmax(sqrt(v[4]), 1.0);
+      obj = v[5];
+    } else {
+      // |sum_k H_k^T lam_k| = rho |D x|
+      eps_d = a.rho * sqrt(v[3]) / fmax(a.rho * sqrt(v[5]), 1.0);
+      obj = w[0];
+    }
+    const long long it = *a.iter;
+    a.res[0] = eps_p;
+    a.res[1] = eps_d;
+    a.res[2] = obj;
+    if (it < a.hist_cap) {
+      a.hist[3 * it + 0] = eps_p;
+      a.hist[3 * it + 1] = eps_d;
+      a.hist[3 * it + 2] = obj;
+    }
+    *a.iter = it + 1;
+    const bool bad = !(isfinite(eps_p) && isfinite(eps_d) && isfinite(obj));
+    if (bad) {
+      *a.numerical = 1;
+      *a.done = 1;
+    } else if (fmax(eps_p, eps_d) < *a.tol) {
+      *a.done = 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- setup kernels
+// S = A D^-1 A^T for dense A (m x lda): 64 x 64 output tiles (upper tiles only,
+// mirrored), 256 threads with 4 x 4 outputs each, K tiles of 16 columns.
+__global__ void __launch_bounds__(256) k_syrk_dense(const double* __restrict__ A, int64_t lda, int m,
+                                                     const double* __restrict__ Dinv, double* __restrict__ S) {
+  const int bi = blockIdx.y, bj = blockIdx.x;
+  if (bi > bj) return;
+  __shared__ double As[16][65];
+  __shared__ double Bs[16][65];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[4][4] = {};
+  const int i0 = bi * 64, j0 = bj * 64;
+  for (int64_t k0 = 0; k0 < lda; k0 += 16) {
+    for (int e = threadIdx.x; e < 64 * 16; e += 256) {
+      const int r = e >> 4, kk = e & 15;
+      const int64_t col = k0 + kk;
+      double av = 0.0, bv = 0.0;
+      if (col < lda) {
+        if (i0 + r < m) av = A[(int64_t)(i0 + r) * lda + col] * Dinv[col];
+        if (j0 + r < m) bv = A[(int64_t)(j0 + r) * lda + col];
+      }
+      As[kk][r] = av;
+      Bs[kk][r] = bv;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a4[4], b4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        a4[q] = As[kk][ty + 16 * q];
+        b4[q] = Bs[kk][tx + 16 * q];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(a4[p], b4[q], acc[p][q]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = i0 + ty + 16 * p, j = j0 + tx + 16 * q;
+      if (i < m && j < m) {
+        S[(int64_t)i * m + j] = acc[p][q];
+        S[(int64_t)j * m + i] = acc[p][q];
+      }
+    }
+}
+
+// Column permutation + svec scaling of the user's dense-on-pattern A.
+__global__ void k_place_dense(const double* __restrict__ raw, int64_t npat, int m, const int64_t* __restrict__ map,
+                              const double* __restrict__ scale, double* __restrict__ A, int64_t lda) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (e >= npat || i >= m) return;
+  A[(int64_t)i * lda + map[e]] = raw[(int64_t)i * npat + e] * scale[e];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+void launch_scatter(int form, const ScatterArgs& a, cudaStream_t s) {
+  const int grid = (a.N + 255) / 256 + (a.n_long + 7) / 8;
+  if (form == 0)
+    k_scatter<0><<<grid, 256, 0, s>>>(a);
+  else
+    k_scatter<1><<<grid, 256, 0, s>>>(a);
+}
+int scatter_blocks(int N, int n_long) { return (N + 255) / 256 + (n_long + 7) / 8; }
+
+void launch_gemv_dense(const double* A, int64_t lda, int m, const double* v, int chunk, double* part,
+                       const int* done, cudaStream_t s) {
+  const int nch = (int)((lda + chunk - 1) / chunk);
+  dim3 grid((m + 3) / 4, nch);
+  k_gemv_dense<4><<<grid, 256, 0, s>>>(A, lda, m, v, chunk, part, done);
+}
+
+void launch_reduce_u(int form, const double* part, int nchunks, int m, const double* b, double rho, double* u,
+                     const double* sdiag, double* y, const int* done, cudaStream_t s) {
+  if (form == 0)
+    k_reduce_u<0><<<(m + 255) / 256, 256, 0, s>>>(part, nchunks, m, b, rho, u, sdiag, y, done);
+  else
+    k_reduce_u<1><<<(m + 255) / 256, 256, 0, s>>>(part, nchunks, m, b, rho, u, sdiag, y, done);
+}
+
+void launch_trmv(int lower, const double* M, int m, const double* in, double* out, const int* done, cudaStream_t s) {
+  if (lower)
+    k_trmv<1><<<(m + 7) / 8, 256, 0, s>>>(M, m, in, out, done);
+  else
+    k_trmv<0><<<(m + 7) / 8, 256, 0, s>>>(M, m, in, out, done);
+}
+
+int gemvT_blocks(int64_t lda) { return (int)((lda / 2 + 255) / 256); }
+
+void launch_gemvT_dense(int form, const double* A, int64_t lda, int m, int N, const double* y, const double* rD,
+                        const double* Dinv, const double* c, double* x, double* part, const int* done,
+                        cudaStream_t s) {
+  const int grid = gemvT_blocks(lda);
+  if (form == 0)
+    k_gemvT_dense<0><<<grid, 256, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
+  else
+    k_gemvT_dense<1><<<grid, 256, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
+}
+
+void launch_gemv_csr(int form, const int32_t* rp, const int32_t* ci, const double* val, int m, const double* v,
+                     const double* b, double rho, double* u, const double* sdiag, double* y, const int* done,
+                     cudaStream_t s) {
+  if (form == 0)
+    k_gemv_csr<0><<<(m + 7) / 8, 256, 0, s>>>(rp, ci, val, m, v, b, rho, u, sdiag, y, done);
+  else
+    k_gemv_csr<1><<<(m + 7) / 8, 256, 0, s>>>(rp, ci, val, m, v, b, rho, u, sdiag, y, done);
+}
+
+int gemvT_csc_blocks(int N) { return (N + 255) / 256; }
+
+void launch_gemvT_csc(int form, const int32_t* cp, const int32_t* ri, const double* val, int N, const double* y,
+                      const double* rD, const double* Dinv, const double* c, double* x, double* part,
+                      const int* done, cudaStream_t s) {
+  const int grid = gemvT_csc_blocks(N);
+  if (form == 0)
+    k_gemvT_csc<0><<<grid, 256, 0, s>>>(cp, ri, val, N, y, rD, Dinv, c, x, part, done);
+  else
+    k_gemvT_csc<1><<<grid, 256, 0, s>>>(cp, ri, val, N, y, rD, Dinv, c, x, part, done);
+}
+
+int update_blocks(int64_t stot) { return (int)((stot + 255) / 256); }
+
+void launch_update_dual(int64_t stot, const int32_t* G, const double* x, const double* z, double* lam, double* v,
+                        double rho, double* part, const int* done, cudaStream_t s) {
+  if (stot <= 0) return;
+  k_update_dual<<<update_blocks(stot), 256, 0, s>>>(stot, G, x, z, lam, v, rho, part, done);
+}
+
+void launch_finalize(int form, const FinalArgs& a, cudaStream_t s) {
+  if (form == 0)
+    k_finalize<0><<<1, 256, 0, s>>>(a);
+  else
+    k_finalize<1><<<1, 256, 0, s>>>(a);
+}
+
+void launch_syrk_dense(const double* A, int64_t lda, int m, const double* Dinv, double* S, cudaStream_t s) {
+  const int nt = (m + 63) / 64;
+  dim3 grid(nt, nt);
+  k_syrk_dense<<<grid, 256, 0, s>>>(A, lda, m, Dinv, S);
+}
+
+void launch_place_dense(const double* raw, int64_t npat, int m, const int64_t* map, const double* scale, double* A,
+                        int64_t lda, cudaStream_t s) {
+  dim3 grid((unsigned)((npat + 255) / 256), m);
+  k_place_dense<<<grid, 256, 0, s>>>(raw, npat, m, map, scale, A, lda);
+}
+
+}  // namespace sdp

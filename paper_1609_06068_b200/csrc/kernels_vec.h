@@ -1,0 +1,73 @@
+#pragma once
+#include "internal.h"
+
+namespace sdp {
+
+constexpr int kLongSeg = 16;  // scatter: segments longer than this get a warp
+
+struct ScatterArgs {
+  int N;
+  const int32_t* seg_ptr;  // N+1
+  const int32_t* seg_idx;  // stot, stacked positions of each coordinate (ascending)
+  const int32_t* longc;    // coordinates with long segments
+  int n_long;
+  const double* xk;        // x_k (primal) / z_k (dual)
+  const double* lam;
+  const double* c;
+  const double* Dinv;
+  double rho;
+  double* rD;              // out: r1 / D
+  double* sprev;           // in/out: previous sum_k H_k^T x_k
+  double* part;            // out: 2 per block
+  const int* done;
+};
+
+struct FinalArgs {
+  const double* proj_part;
+  int n_proj;
+  const double* upd_part;
+  int n_upd;
+  const double* scat_part;
+  int n_scat;
+  const double* gT_part;
+  int n_gT;
+  const double* b;
+  const double* y;
+  int m;
+  double rho;
+  double* res;        // eps_p, eps_d, objective
+  double* hist;
+  long long hist_cap;
+  long long* iter;
+  int* done;
+  int* numerical;
+  const double* tol;
+};
+
+void launch_scatter(int form, const ScatterArgs& a, cudaStream_t s);
+int scatter_blocks(int N, int n_long);
+void launch_gemv_dense(const double* A, int64_t lda, int m, const double* v, int chunk, double* part,
+                       const int* done, cudaStream_t s);
+void launch_reduce_u(int form, const double* part, int nchunks, int m, const double* b, double rho, double* u,
+                     const double* sdiag, double* y, const int* done, cudaStream_t s);
+void launch_trmv(int lower, const double* M, int m, const double* in, double* out, const int* done, cudaStream_t s);
+int gemvT_blocks(int64_t lda);
+void launch_gemvT_dense(int form, const double* A, int64_t lda, int m, int N, const double* y, const double* rD,
+                        const double* Dinv, const double* c, double* x, double* part, const int* done,
+                        cudaStream_t s);
+void launch_gemv_csr(int form, const int32_t* rp, const int32_t* ci, const double* val, int m, const double* v,
+                     const double* b, double rho, double* u, const double* sdiag, double* y, const int* done,
+                     cudaStream_t s);
+int gemvT_csc_blocks(int N);
+void launch_gemvT_csc(int form, const int32_t* cp, const int32_t* ri, const double* val, int N, const double* y,
+                      const double* rD, const double* Dinv, const double* c, double* x, double* part,
+                      const int* done, cudaStream_t s);
+int update_blocks(int64_t stot);
+void launch_update_dual(int64_t stot, const int32_t* G, const double* x, const double* z, double* lam, double* v,
+                        double rho, double* part, const int* done, cudaStream_t s);
+void launch_finalize(int form, const FinalArgs& a, cudaStream_t s);
+void launch_syrk_dense(const double* A, int64_t lda, int m, const double* Dinv, double* S, cudaStream_t s);
+void launch_place_dense(const double* raw, int64_t npat, int m, const int64_t* map, const double* scale, double* A,
+                        int64_t lda, cudaStream_t s);
+
+}  // namespace sdp

@@ -1,0 +1,145 @@
+// Host-side chordal analysis, run once in sdp_setup ("Setup: Chordal
+// decomposition").  Independent of oracle/ (which is Python); the two are
+// checked against each other by tests/test_library_host.py.
+//
+//  * aggregate pattern arrives as off-diagonal upper edges;
+//  * chordal extension: exact minimum-degree symbolic elimination with
+//    lowest-index ties (reading G13) -- the fill edges are E' \ E;
+//  * maximal cliques from the elimination tree: the
+//    candidate K_v = {v} U adj+(v) is maximal iff no child w of v in the
+//    elimination tree has |K_w| = |K_v| + 1;
+//  * cliques sorted ascending inside and lexicographically as a list
+//    (reading G14); coordinates of E' in column-major upper order.
+//
+// Adjacency is a dense bitset (n^2/8 bytes): n <= 46340 in this build.
+#include <algorithm>
+#include <set>
+#include <stdexcept>
+
+#include "internal.h"
+
+namespace sdp {
+
+namespace {
+inline int popc(uint64_t x) { return __builtin_popcountll(x); }
+}  // namespace
+
+ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges) {
+  if (n > 46340) throw Error{SDP_E_INVALID_ARG, "n > 46340 not supported by the bitset chordal analysis"};
+  const int64_t W = (n + 63) / 64;
+  std::vector<uint64_t> adj((size_t)n * W, 0ull);
+  auto row = [&](int v) { return adj.data() + (size_t)v * W; };
+  int64_t e0 = 0;
+  for (auto& e : edges) {
+    int i = e.first, j = e.second;
+    if (i == j) continue;
+    uint64_t* ri = row(i);
+    if (!(ri[j >> 6] >> (j & 63) & 1ull)) {
+      ri[j >> 6] |= 1ull << (j & 63);
+      row(j)[i >> 6] |= 1ull << (i & 63);
+      ++e0;
+    }
+  }
+  std::vector<uint64_t> alive(W, ~0ull);
+  if (n % 64) alive[W - 1] = (1ull << (n % 64)) - 1ull;
+  std::vector<int32_t> deg(n), pos(n);
+  std::set<std::pair<int32_t, int32_t>> queue;
+  for (int v = 0; v < n; ++v) {
+    int d = 0;
+    const uint64_t* r = row(v);
+    for (int64_t w = 0; w < W; ++w) d += popc(r[w]);
+    deg[v] = d;
+    queue.insert({d, v});
+  }
+  std::vector<std::vector<int32_t>> later(n);
+  std::vector<uint64_t> nbmask(W);
+  for (int step = 0; step < n; ++step) {
+    auto it = queue.begin();  // smallest degree, then smallest index
+    const int v = it->second;
+    queue.erase(it);
+    pos[v] = step;
+    alive[v >> 6] &= ~(1ull << (v & 63));
+    const uint64_t* rv = row(v);
+    std::vector<int32_t>& nb = later[v];
+    for (int64_t w = 0; w < W; ++w) {
+      uint64_t m = rv[w] & alive[w];
+      nbmask[w] = m;
+      while (m) {
+        int b = __builtin_ctzll(m);
+        nb.push_back((int32_t)(w * 64 + b));
+        m &= m - 1;
+      }
+    }
+    // eliminate v: its remaining neighbourhood becomes a clique (fill edges)
+    for (int u : nb) {
+      uint64_t* ru = row(u);
+      for (int64_t w = 0; w < W; ++w) ru[w] |= nbmask[w];
+      ru[u >> 6] &= ~(1ull << (u & 63));
+    }
+    for (int u : nb) {
+      const uint64_t* ru = row(u);
+      int d = 0;
+      for (int64_t w = 0; w < W; ++w) d += popc(ru[w] & alive[w]);
+      if (d != deg[u]) {
+        queue.erase({deg[u], u});
+        deg[u] = d;
+        queue.insert({d, u});
+      }
+    }
+  }
+  ChordalResult cr;
+  // elimination tree: parent(v) = first-eliminated later neighbour
+  std::vector<int32_t> parent(n, -1);
+  for (int v = 0; v < n; ++v) {
+    int best = -1;
+    for (int u : later[v])
+      if (best < 0 || pos[u] < pos[best]) best = u;
+    parent[v] = best;
+  }
+  std::vector<char> maximal(n, 1);
+  for (int w = 0; w < n; ++w) {
+    int v = parent[w];
+    if (v >= 0 && later[w].size() == later[v].size() + 1) maximal[v] = 0;
+  }
+  for (int v = 0; v < n; ++v) {
+    if (!maximal[v]) continue;
+    std::vector<int32_t> K = later[v];
+    K.push_back(v);
+    std::sort(K.begin(), K.end());
+    cr.cliques.push_back(std::move(K));
+  }
+  std::sort(cr.cliques.begin(), cr.cliques.end());
+  // extended pattern E' (+ diagonal) in canonical order
+  int64_t e1 = 0;
+  cr.col_ptr.assign(n + 1, 0);
+  for (int j = 0; j < n; ++j) {
+    const uint64_t* rj = row(j);
+    for (int64_t w = 0; w <= (j >> 6); ++w) {
+      uint64_t m = rj[w];
+      if (w == (j >> 6)) m &= (j & 63) ? ((1ull << (j & 63)) - 1ull) : 0ull;
+      while (m) {
+        int b = __builtin_ctzll(m);
+        cr.coord_row.push_back((int32_t)(w * 64 + b));
+        cr.coord_col.push_back(j);
+        ++e1;
+        m &= m - 1;
+      }
+    }
+    cr.coord_row.push_back(j);
+    cr.coord_col.push_back(j);
+    cr.col_ptr[j + 1] = (int64_t)cr.coord_row.size();
+  }
+  cr.fill_edges = e1 - e0;
+  return cr;
+}
+
+int64_t coord_index(const ChordalResult& cr, int32_t i, int32_t j) {
+  if (i > j) std::swap(i, j);
+  const int32_t* b = cr.coord_row.data() + cr.col_ptr[j];
+  const int32_t* e = cr.coord_row.data() + cr.col_ptr[j + 1];
+  const int32_t* p = std::lower_bound(b, e, i);
+  if (p == e || *p != i) return -1;
+  return (int64_t)(p - cr.coord_row.data());
+}
+
+}  // namespace sdp
