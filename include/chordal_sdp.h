@@ -87,7 +87,7 @@ typedef struct {
   int32_t form;              /* SDP_FORM_PRIMAL or SDP_FORM_DUAL                     */
   double rho;                /* ADMM penalty rho > 0; default 1.0     */
   int32_t device;            /* CUDA device ordinal; default 0                        */
-  void* stream;              /* cudaStream_t to enqueue on (NULL = library-owned)    */
+  void* stream;              /* cudaStream_t to enqueue on (NULL = default stream)   */
   int32_t check_every;       /* sdp_solve: host reads the stop flag every K iterations (default 10) */
   int32_t use_graph;         /* 1 (default): replay one captured CUDA graph per iteration */
   int32_t rank, world;       /* reserved for clique sharding; must be 0, 1           */

@@ -213,9 +213,11 @@ int guarded(F&& f) {
 void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_NUM], int bcount[B_NUM],
                    double*& work, int& slots, int& ld_work) {
   std::vector<std::vector<int32_t>> lists(B_NUM);
+  int64_t in_range[6] = {0, 0, 0, 0, 0, 0};
+  for (size_t i = 0; i < ksz.size(); ++i) in_range[size_range(ksz[i])]++;
   int kg = 0;
   for (size_t i = 0; i < ksz.size(); ++i) {
-    const int b = bucket_of(ksz[i]);
+    const int b = bucket_of(ksz[i], in_range[size_range(ksz[i])]);
     lists[b].push_back((int32_t)i);
     if (b == B_GLOBAL) kg = std::max(kg, (int)ksz[i]);
   }
@@ -504,12 +506,8 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->check_every = opt.check_every > 0 ? opt.check_every : 10;
   h->use_graph = opt.use_graph;
   h->fill_edges = cr.fill_edges;
-  if (opt.stream) {
-    h->stream = (cudaStream_t)opt.stream;
-  } else {
-    SDP_CUDA_TRY(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-    h->own_stream = true;
-  }
+  h->stream = (cudaStream_t)opt.stream;  // NULL = the legacy default stream, as in the CUDA runtime
+  h->own_stream = false;
   SDP_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
   const int64_t N = (int64_t)cr.coord_row.size();
   h->N = N;

@@ -39,8 +39,12 @@ int64_t coord_index(const ChordalResult& cr, int32_t i, int32_t j);  // -1 if ab
 
 // ---------------------------------------------------------------- projection buckets
 // Kernel tiers for the batched eigen-projection (kernels_psd.cu).
-enum BucketKind { B_G8 = 0, B_G16 = 1, B_G32 = 2, B_CTA64 = 3, B_CTA96 = 4, B_GLOBAL = 5, B_NUM = 6 };
-int bucket_of(int k);
+enum BucketKind { B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_NUM };
+// Size ranges (k <= 8, 16, 32, 64, 96, larger) with fewer than kFewMatrices
+// members use one CTA per matrix so that a small batch still fills the GPU.
+constexpr int64_t kFewMatrices = 2048;
+int size_range(int k);
+int bucket_of(int k, int64_t count_in_range);
 
 // Projection modes
 enum ProjMode { PM_BATCH = 0, PM_PRIMAL = 1, PM_DUAL = 2 };

@@ -10,12 +10,13 @@
 // are clipped at exactly 0 (reading G15) and the projection is rebuilt as
 // sum_t max(l_t,0) v_t v_t^T.
 //
-// Tiers (bucket_of): a group of G lanes owns one matrix held in shared memory
-//   G8  : 8 lanes,  k <= 8   (16 matrices per 128-thread CTA)
-//   G16 : 16 lanes, k <= 16  (8 per CTA)
-//   G32 : one warp, k <= 32  (4 per CTA)
-//   CTA64: 128 threads, k <= 64;  CTA96: 256 threads, k <= 96
-//   GLOBAL: 256 threads, k <= SDP_MAX_K, A and V in an L2-resident global workspace
+// Tiers (chosen per bucket by order k and by how many matrices share it,
+// see bucket assignment in api.cu): a group of G threads owns one matrix whose
+// A and V live in shared memory (GLOBAL: in an L2-resident workspace).
+//   G8 / G16 / G32 : 8 / 16 / 32 lanes per matrix, k <= 8 / 16 / 32, many matrices
+//   CTA32          : 128 threads per matrix, k <= 32, few matrices (fills the GPU)
+//   CTA64          : 128 threads, k <= 64;  CTA96: 256 threads, k <= 96
+//   GLOBAL         : 256 threads, k <= SDP_MAX_K
 // Odd k is padded with one zero row/column (exact: P_+(diag(X,0)) = diag(P_+(X),0)).
 #include <cmath>
 
@@ -42,7 +43,7 @@ template <int G>
 struct Group {
   int tid;
   unsigned mask;
-  double* red;  // CTA-level reduction scratch (G > 32), >= G/32 + 1 doubles
+  double* red;  // CTA-level reduction scratch (G > 32), >= G/32 doubles
   __device__ __forceinline__ void sync() const {
     if constexpr (G <= 32)
       __syncwarp(mask);
@@ -63,7 +64,7 @@ struct Group {
       if ((tid & 31) == 0) red[w] = v;
       __syncthreads();
       double s = 0.0;
-#pragma unroll 1
+#pragma unroll
       for (int i = 0; i < G / 32; ++i) s += red[i];
       return s;
     }
@@ -76,6 +77,27 @@ struct Rot {
   double* c;
   double* s;
   double* t;
+  const int* blk;  // packed (i << 16 | j), i <= j, column-major over the pair triangle; nullptr = compute
+};
+
+// 2-D strided walk over an R x C index space starting at flat index `start`
+// with flat stride G, without divisions in the loop.
+struct Walk {
+  int r, c, dr, dc, C;
+  __device__ __forceinline__ Walk(int start, int G, int Cn) : C(Cn) {
+    r = start / Cn;
+    c = start - r * Cn;
+    dr = G / Cn;
+    dc = G - dr * Cn;
+  }
+  __device__ __forceinline__ void next() {
+    c += dc;
+    r += dr;
+    if (c >= C) {
+      c -= C;
+      ++r;
+    }
+  }
 };
 
 template <int G, int MODE>
@@ -109,16 +131,18 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
       A[e * ld + k] = 0.0;
     }
   }
-  for (int e = g.tid; e < kp * kp; e += G) {
-    const int r = e / kp, c = e - r * kp;
-    V[r * ld + c] = (r == c) ? 1.0 : 0.0;
+  {
+    Walk w(g.tid, G, kp);
+    for (; w.r < kp; w.next()) V[w.r * ld + w.c] = (w.r == w.c) ? 1.0 : 0.0;
   }
   g.sync();
   double fro2 = 0.0;
-  for (int e = g.tid; e < kp * kp; e += G) {
-    const int r = e / kp, c = e - r * kp;
-    const double v = A[r * ld + c];
-    fro2 += v * v;
+  {
+    Walk w(g.tid, G, kp);
+    for (; w.r < kp; w.next()) {
+      const double v = A[w.r * ld + w.c];
+      fro2 += v * v;
+    }
   }
   fro2 = g.sum(fro2);
   const double thr = kJacTol * kJacTol * fro2;
@@ -126,11 +150,13 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
   int sweep = 0;
   for (; sweep < kMaxSweeps; ++sweep) {
     double off2 = 0.0;
-    for (int e = g.tid; e < kp * kp; e += G) {
-      const int r = e / kp, c = e - r * kp;
-      if (r != c) {
-        const double v = A[r * ld + c];
-        off2 += v * v;
+    {
+      Walk w(g.tid, G, kp);
+      for (; w.r < kp; w.next()) {
+        if (w.r != w.c) {
+          const double v = A[w.r * ld + w.c];
+          off2 += v * v;
+        }
       }
     }
     off2 = g.sum(off2);
@@ -138,8 +164,13 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
     for (int step = 0; step < kp - 1; ++step) {
       // rotation parameters of the P disjoint pairs of this step
       for (int i = g.tid; i < P; i += G) {
-        const int p = (i == 0) ? 0 : 1 + (i - 1 + step) % (kp - 1);
-        const int q = 1 + (kp - 2 - i + step) % (kp - 1);
+        int p = 0, q;
+        if (i != 0) {
+          p = i - 1 + step;
+          p = 1 + (p >= kp - 1 ? p - (kp - 1) : p);
+        }
+        q = kp - 2 - i + step;
+        q = 1 + (q >= kp - 1 ? q - (kp - 1) : q);
         const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
         double cs = 1.0, sn = 0.0, t = 0.0;
         if (apq != 0.0) {
@@ -159,7 +190,13 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
       // A <- J^T A J on the 2x2 blocks (i <= j) of the pair partition, mirrored
       for (int b = g.tid; b < nblk; b += G) {
         int i, j;
-        packed_rc(b, i, j);
+        if (rot.blk) {
+          const int ij = rot.blk[b];
+          i = ij >> 16;
+          j = ij & 0xffff;
+        } else {
+          packed_rc(b, i, j);
+        }
         const int p1 = rot.p[i], q1 = rot.q[i];
         if (i == j) {
           const double apq = A[p1 * ld + q1], t = rot.t[i];
@@ -188,14 +225,17 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
           A[q2 * ld + q1] = n11;
         }
       }
-      // V <- V J
-      for (int e = g.tid; e < kp * P; e += G) {
-        const int r = e / P, i = e - r * P;
-        const int p = rot.p[i], q = rot.q[i];
-        const double cs = rot.c[i], sn = rot.s[i];
-        const double vp = V[r * ld + p], vq = V[r * ld + q];
-        V[r * ld + p] = cs * vp - sn * vq;
-        V[r * ld + q] = sn * vp + cs * vq;
+      // V <- V J  (row r, pair i)
+      {
+        Walk w(g.tid, G, P);
+        for (; w.r < kp; w.next()) {
+          const int p = rot.p[w.c], q = rot.q[w.c];
+          const double cs = rot.c[w.c], sn = rot.s[w.c];
+          double* Vr = V + w.r * ld;
+          const double vp = Vr[p], vq = Vr[q];
+          Vr[p] = cs * vp - sn * vq;
+          Vr[q] = sn * vp + cs * vq;
+        }
       }
       g.sync();
     }
@@ -207,9 +247,11 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
     int r, c;
     packed_rc(e, r, c);
     double acc = 0.0;
+    const double* Vr = V + r * ld;
+    const double* Vc = V + c * ld;
     for (int t = 0; t < kp; ++t) {
       const double l = A[t * ld + t];
-      if (l > 0.0) acc += l * V[r * ld + t] * V[c * ld + t];
+      if (l > 0.0) acc += l * Vr[t] * Vc[t];
     }
     if constexpr (MODE == PM_BATCH) {
       a.out[off + e] = acc;
@@ -240,66 +282,89 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
   g.sync();
 }
 
+// Pair-block table (i << 16 | j), column-major over i <= j < PMAX: the first
+// P(P+1)/2 entries are exactly the blocks of a matrix with P pairs.
+template <int PMAX, int NT>
+__device__ __forceinline__ void fill_blk_table(int* tab) {
+  for (int b = threadIdx.x; b < PMAX * (PMAX + 1) / 2; b += NT) {
+    int i, j;
+    packed_rc(b, i, j);
+    tab[b] = (i << 16) | j;
+  }
+  __syncthreads();
+}
+
 // --- small tiers: G lanes per matrix, NG groups per 128-thread CTA ---------
+template <int G, int KMAX>
+struct SmallLayout {
+  static constexpr int NG = 128 / G;
+  static constexpr int LD = KMAX + 1;
+  static constexpr int P = KMAX / 2;
+  static constexpr int PER = 2 * KMAX * LD + 4 * P;  // doubles per group
+  static constexpr int NBLK = P * (P + 1) / 2;
+  static constexpr size_t bytes() { return (size_t)NG * PER * sizeof(double) + NBLK * sizeof(int); }
+};
+
 template <int G, int KMAX, int MODE>
 __global__ void __launch_bounds__(128) k_psd_small(ProjArgs a) {
   if (a.done && *a.done) return;
-  constexpr int NG = 128 / G;
-  constexpr int LD = KMAX + 1;
-  constexpr int P = KMAX / 2;
+  using Lay = SmallLayout<G, KMAX>;
   extern __shared__ double smem[];
+  int* tab = (int*)(smem + Lay::NG * Lay::PER);
+  fill_blk_table<Lay::P, 128>(tab);
   const int grp = threadIdx.x / G;
-  const int task_slot = blockIdx.x * NG + grp;
+  const int task_slot = blockIdx.x * Lay::NG + grp;
   if (task_slot >= a.count) return;
-  double* base = smem + (size_t)grp * (2 * KMAX * LD + 3 * P + P);
+  double* base = smem + (size_t)grp * Lay::PER;
   double* A = base;
-  double* V = base + KMAX * LD;
-  double* rc = V + KMAX * LD;
-  double* rs = rc + P;
-  double* rt = rs + P;
-  int* rpq = (int*)(rt + P);
-  Rot rot{rpq, rpq + P, rc, rs, rt};
+  double* V = base + KMAX * Lay::LD;
+  double* rc = V + KMAX * Lay::LD;
+  double* rs = rc + Lay::P;
+  double* rt = rs + Lay::P;
+  int* rpq = (int*)(rt + Lay::P);
+  Rot rot{rpq, rpq + Lay::P, rc, rs, rt, tab};
   Group<G> g;
   g.tid = threadIdx.x % G;
   g.mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
   g.red = nullptr;
   const int task = a.ids ? a.ids[task_slot] : task_slot;
-  project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, LD, rot, a);
-}
-
-template <int G, int KMAX>
-constexpr size_t small_smem() {
-  return (size_t)(128 / G) * (2 * KMAX * (KMAX + 1) + 4 * (KMAX / 2)) * sizeof(double);
+  project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, Lay::LD, rot, a);
 }
 
 // --- CTA tiers: one CTA per matrix, A and V in shared memory ---------------
+template <int G, int KMAX>
+struct CtaLayout {
+  static constexpr int LD = KMAX + 1;
+  static constexpr int P = KMAX / 2;
+  static constexpr int NBLK = P * (P + 1) / 2;
+  static constexpr size_t bytes() {
+    return (size_t)(2 * KMAX * LD + 4 * P + G / 32) * sizeof(double) + NBLK * sizeof(int);
+  }
+};
+
 template <int G, int KMAX, int MODE>
 __global__ void __launch_bounds__(G) k_psd_cta(ProjArgs a) {
   if (a.done && *a.done) return;
-  constexpr int LD = KMAX + 1;
-  constexpr int P = KMAX / 2;
+  using Lay = CtaLayout<G, KMAX>;
   extern __shared__ double smem[];
   double* A = smem;
-  double* V = A + KMAX * LD;
-  double* rc = V + KMAX * LD;
-  double* rs = rc + P;
-  double* rt = rs + P;
-  int* rpq = (int*)(rt + P);
-  double* red = (double*)(rpq + 2 * P);
-  Rot rot{rpq, rpq + P, rc, rs, rt};
+  double* V = A + KMAX * Lay::LD;
+  double* rc = V + KMAX * Lay::LD;
+  double* rs = rc + Lay::P;
+  double* rt = rs + Lay::P;
+  int* rpq = (int*)(rt + Lay::P);
+  double* red = (double*)(rpq + 2 * Lay::P);
+  int* tab = (int*)(red + G / 32);
+  fill_blk_table<Lay::P, G>(tab);
+  Rot rot{rpq, rpq + Lay::P, rc, rs, rt, tab};
   Group<G> g;
   g.tid = threadIdx.x;
   g.mask = 0xffffffffu;
   g.red = red;
   for (int slot = blockIdx.x; slot < a.count; slot += gridDim.x) {
     const int task = a.ids ? a.ids[slot] : slot;
-    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, LD, rot, a);
+    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, Lay::LD, rot, a);
   }
-}
-
-template <int G, int KMAX>
-constexpr size_t cta_smem() {
-  return (size_t)(2 * KMAX * (KMAX + 1) + 4 * (KMAX / 2) + G / 32 + 2) * sizeof(double);
 }
 
 // --- GLOBAL tier: A, V in a global (L2-resident) workspace slot per CTA -----
@@ -309,8 +374,8 @@ __global__ void __launch_bounds__(G) k_psd_global(ProjArgs a) {
   constexpr int PMAX = SDP_MAX_K / 2;
   __shared__ double rc[PMAX], rs[PMAX], rt[PMAX];
   __shared__ int rpq[2 * PMAX];
-  __shared__ double red[G / 32 + 2];
-  Rot rot{rpq, rpq + PMAX, rc, rs, rt};
+  __shared__ double red[G / 32];
+  Rot rot{rpq, rpq + PMAX, rc, rs, rt, nullptr};
   Group<G> g;
   g.tid = threadIdx.x;
   g.mask = 0xffffffffu;
@@ -328,31 +393,24 @@ template <int MODE>
 void launch_mode(int bucket, const ProjArgs& a, cudaStream_t s) {
   if (a.count <= 0) return;
   switch (bucket) {
-    case B_G8: {
-      constexpr size_t sm = small_smem<8, 8>();
-      k_psd_small<8, 8, MODE><<<(a.count + 15) / 16, 128, sm, s>>>(a);
+    case B_G8:
+      k_psd_small<8, 8, MODE><<<(a.count + 15) / 16, 128, SmallLayout<8, 8>::bytes(), s>>>(a);
       break;
-    }
-    case B_G16: {
-      constexpr size_t sm = small_smem<16, 16>();
-      k_psd_small<16, 16, MODE><<<(a.count + 7) / 8, 128, sm, s>>>(a);
+    case B_G16:
+      k_psd_small<16, 16, MODE><<<(a.count + 7) / 8, 128, SmallLayout<16, 16>::bytes(), s>>>(a);
       break;
-    }
-    case B_G32: {
-      constexpr size_t sm = small_smem<32, 32>();
-      k_psd_small<32, 32, MODE><<<(a.count + 3) / 4, 128, sm, s>>>(a);
+    case B_G32:
+      k_psd_small<32, 32, MODE><<<(a.count + 3) / 4, 128, SmallLayout<32, 32>::bytes(), s>>>(a);
       break;
-    }
-    case B_CTA64: {
-      constexpr size_t sm = cta_smem<128, 64>();
-      k_psd_cta<128, 64, MODE><<<a.count, 128, sm, s>>>(a);
+    case B_CTA32:
+      k_psd_cta<128, 32, MODE><<<a.count, 128, CtaLayout<128, 32>::bytes(), s>>>(a);
       break;
-    }
-    case B_CTA96: {
-      constexpr size_t sm = cta_smem<256, 96>();
-      k_psd_cta<256, 96, MODE><<<a.count, 256, sm, s>>>(a);
+    case B_CTA64:
+      k_psd_cta<128, 64, MODE><<<a.count, 128, CtaLayout<128, 64>::bytes(), s>>>(a);
       break;
-    }
+    case B_CTA96:
+      k_psd_cta<256, 96, MODE><<<a.count, 256, CtaLayout<256, 96>::bytes(), s>>>(a);
+      break;
     case B_GLOBAL: {
       const int grid = a.count < a.work_slots ? a.count : a.work_slots;
       k_psd_global<256, MODE><<<grid, 256, 0, s>>>(a);
@@ -364,11 +422,13 @@ void launch_mode(int bucket, const ProjArgs& a, cudaStream_t s) {
 template <int MODE>
 void init_attrs_mode() {
   cudaFuncSetAttribute(k_psd_small<32, 32, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)small_smem<32, 32>());
+                       (int)SmallLayout<32, 32>::bytes());
+  cudaFuncSetAttribute(k_psd_cta<128, 32, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)CtaLayout<128, 32>::bytes());
   cudaFuncSetAttribute(k_psd_cta<128, 64, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)cta_smem<128, 64>());
+                       (int)CtaLayout<128, 64>::bytes());
   cudaFuncSetAttribute(k_psd_cta<256, 96, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)cta_smem<256, 96>());
+                       (int)CtaLayout<256, 96>::bytes());
 }
 
 }  // namespace
@@ -380,14 +440,18 @@ void psd_init_attributes() {
   init_attrs_mode<PM_DUAL>();
 }
 
-int bucket_of(int k) {
-  if (k <= 8) return B_G8;
-  if (k <= 16) return B_G16;
-  if (k <= 32) return B_G32;
+// Tier of a matrix of order k when `count` matrices fall in its size range.
+int bucket_of(int k, int64_t count_in_range) {
+  const bool few = count_in_range < kFewMatrices;
+  if (k <= 8) return few ? B_CTA32 : B_G8;
+  if (k <= 16) return few ? B_CTA32 : B_G16;
+  if (k <= 32) return few ? B_CTA32 : B_G32;
   if (k <= 64) return B_CTA64;
   if (k <= 96) return B_CTA96;
   return B_GLOBAL;
 }
+
+int size_range(int k) { return k <= 8 ? 0 : k <= 16 ? 1 : k <= 32 ? 2 : k <= 64 ? 3 : k <= 96 ? 4 : 5; }
 
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s) {
   if (mode == PM_BATCH)
