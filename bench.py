@@ -306,6 +306,7 @@ def run_ours(args, rank, world, local):
         "setup_s": setup_wall,
         "residuals_after": {"iters": fin["iters"], "eps_p": fin["eps_p"], "eps_d": fin["eps_d"],
                             "objective": fin["objective"]},
+        "jacobi_sweeps_per_projection": fin["jacobi_sweeps"] / max(1, fin["iters"] * info["p"]),
     })
     # e2e through the public API: per step, sdp_step(1) + sdp_get_info (D2H of the
     # step's result: eps_p, eps_d, objective, iteration count).

@@ -104,6 +104,7 @@ typedef struct {
   int32_t s_diagonal;        /* 1 if S = A D^-1 A^T is diagonal (elementwise KKT)   */
   int64_t jacobi_capped;     /* count of projections that hit the sweep cap          */
   int32_t launches_per_iter; /* kernels launched per ADMM iteration                   */
+  int64_t jacobi_sweeps;     /* total Jacobi sweeps over all projections since reset  */
 } sdp_info;
 
 typedef struct sdp_handle_s* sdp_handle;

@@ -161,6 +161,10 @@ struct sdp_handle_s {
   long long* iter = nullptr;
   int *done = nullptr, *numerical = nullptr;
   unsigned long long* capped = nullptr;
+  unsigned long long* sweeps = nullptr;
+  double* vprev = nullptr;
+  int64_t* voff = nullptr;
+  int warm_period = 64;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
@@ -176,6 +180,7 @@ struct sdp_psd_plan_s {
   double* work = nullptr;
   int work_slots = 0, ld_work = 0;
   unsigned long long* capped = nullptr;
+  unsigned long long* sweeps = nullptr;
   double *h_in_dev = nullptr, *h_out_dev = nullptr;
 };
 
@@ -231,7 +236,7 @@ void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_
   if (bcount[B_GLOBAL]) {
     ld_work = kg + (kg & 1);
     slots = std::min(bcount[B_GLOBAL], 148);
-    work = al.get<double>((size_t)slots * 2 * ld_work * ld_work);
+    work = al.get<double>((size_t)slots * 3 * ld_work * ld_work);
   }
 }
 
@@ -250,7 +255,12 @@ void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
   a.work_slots = h->work_slots;
   a.ld_work = h->ld_work;
   a.capped = h->capped;
+  a.sweeps = h->sweeps;
   a.done = h->done;
+  a.vprev = h->vprev;
+  a.voff = h->voff;
+  a.iter = h->iter;
+  a.warm_period = h->warm_period;
   // big tiers first: they are the long poles
   for (int b = B_NUM - 1; b >= 0; --b) {
     if (!h->bcount[b]) continue;
@@ -411,6 +421,7 @@ void reset_state(sdp_handle h) {
   SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->numerical, 0, sizeof(int), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->capped, 0, sizeof(unsigned long long), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->sweeps, 0, sizeof(unsigned long long), s));
   const double neg = -1.0;
   SDP_CUDA_TRY(cudaMemcpyAsync(h->tol, &neg, sizeof(double), cudaMemcpyHostToDevice, s));
   if (h->form == SDP_FORM_PRIMAL) enqueue_scatter(h, s);  // r1 = -c/rho for iteration 1
@@ -727,6 +738,16 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->done = al.zeros<int>(1);
   h->numerical = al.zeros<int>(1);
   h->capped = al.zeros<unsigned long long>(1);
+  h->sweeps = al.zeros<unsigned long long>(1);
+  {  // warm-start eigenvector storage: kp x kp per clique
+    std::vector<int64_t> voff(p + 1, 0);
+    for (int64_t k = 0; k < p; ++k) {
+      const int64_t kp = ksz[k] + (ksz[k] & 1);
+      voff[k + 1] = voff[k] + kp * kp;
+    }
+    h->voff = al.upload(voff);
+    h->vprev = al.zeros<double>((size_t)voff[p]);
+  }
   psd_init_attributes();
   SDP_CUDA_TRY(cudaDeviceSynchronize());
   reset_state(h);
@@ -738,8 +759,9 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
 void fill_info(sdp_handle h, sdp_info* info) {
   double res[3];
   long long it;
-  unsigned long long cap;
+  unsigned long long cap, sw;
   SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  SDP_CUDA_TRY(cudaMemcpy(&sw, h->sweeps, sizeof(sw), cudaMemcpyDeviceToHost));
   SDP_CUDA_TRY(cudaMemcpy(res, h->res, 3 * sizeof(double), cudaMemcpyDeviceToHost));
   SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(long long), cudaMemcpyDeviceToHost));
   SDP_CUDA_TRY(cudaMemcpy(&cap, h->capped, sizeof(cap), cudaMemcpyDeviceToHost));
@@ -760,6 +782,7 @@ void fill_info(sdp_handle h, sdp_info* info) {
   info->s_diagonal = h->s_diag;
   info->jacobi_capped = (int64_t)cap;
   info->launches_per_iter = launches_per_iter(h);
+  info->jacobi_sweeps = (int64_t)sw;
 }
 
 void launch_iterations(sdp_handle h, int32_t iters) {
@@ -1036,6 +1059,7 @@ int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, s
     pl->d_ksz = pl->alloc.upload(ksz);
     build_buckets(pl->alloc, ksz, pl->d_ids, pl->bcount, pl->work, pl->work_slots, pl->ld_work);
     pl->capped = pl->alloc.zeros<unsigned long long>(1);
+    pl->sweeps = pl->alloc.zeros<unsigned long long>(1);
     psd_init_attributes();
     *out = pl;
     return SDP_OK;
@@ -1062,6 +1086,7 @@ int sdp_project_psd_batch(sdp_psd_plan pl, const double* d_in, double* d_out, vo
     a.work_slots = pl->work_slots;
     a.ld_work = pl->ld_work;
     a.capped = pl->capped;
+    a.sweeps = pl->sweeps;
     a.done = nullptr;
     for (int b = B_NUM - 1; b >= 0; --b) {
       if (!pl->bcount[b]) continue;

@@ -69,7 +69,13 @@ struct ProjArgs {
   int32_t work_slots;
   int32_t ld_work;
   unsigned long long* capped;  // count of sweep-capped projections
+  unsigned long long* sweeps;  // total Jacobi sweeps (diagnostics)
   const int32_t* done;  // device stop flag (skip work when set)
+  // warm start (ADMM modes): per task eigenvector basis of the previous iteration
+  double* vprev;        // per task kp*kp doubles at voff[task]
+  const int64_t* voff;
+  const long long* iter;  // iteration counter; cold start when iter % warm_period == 0
+  int32_t warm_period;    // 0 = never warm start
 };
 
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);

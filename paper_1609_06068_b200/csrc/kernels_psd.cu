@@ -102,8 +102,8 @@ struct Walk {
 
 template <int G, int MODE>
 __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off, const int task,
-                               double* __restrict__ A, double* __restrict__ V, const int ld, Rot rot,
-                               const ProjArgs& a) {
+                               double* __restrict__ A, double* __restrict__ V, double* __restrict__ T,
+                               const int ld, Rot rot, const ProjArgs& a) {
   const int kp = k + (k & 1);
   const int P = kp >> 1;
   const int ns = k * (k + 1) / 2;
@@ -131,7 +131,36 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
       A[e * ld + k] = 0.0;
     }
   }
-  {
+  // Warm start (ADMM modes, T != nullptr): V = V_prev, A <- V_prev^T A V_prev.
+  const bool warm = (MODE != PM_BATCH) && T != nullptr && a.vprev != nullptr && a.warm_period > 0 &&
+                    (*a.iter % a.warm_period) != 0;
+  if (warm) {
+    const double* Vp = a.vprev + a.voff[task];
+    {
+      Walk w(g.tid, G, kp);
+      for (; w.r < kp; w.next()) V[w.r * ld + w.c] = Vp[w.r * kp + w.c];
+    }
+    g.sync();
+    {  // T = A V
+      Walk w(g.tid, G, kp);
+      for (; w.r < kp; w.next()) {
+        const double* Ar = A + w.r * ld;
+        double acc = 0.0;
+        for (int t = 0; t < kp; ++t) acc = fma(Ar[t], V[t * ld + w.c], acc);
+        T[w.r * ld + w.c] = acc;
+      }
+    }
+    g.sync();
+    // A = V^T T (upper triangle, mirrored)
+    for (int e = g.tid; e < kp * (kp + 1) / 2; e += G) {
+      int r, c;
+      packed_rc(e, r, c);
+      double acc = 0.0;
+      for (int t = 0; t < kp; ++t) acc = fma(V[t * ld + r], T[t * ld + c], acc);
+      A[r * ld + c] = acc;
+      A[c * ld + r] = acc;
+    }
+  } else {
     Walk w(g.tid, G, kp);
     for (; w.r < kp; w.next()) V[w.r * ld + w.c] = (w.r == w.c) ? 1.0 : 0.0;
   }
@@ -241,6 +270,12 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
     }
   }
   if (sweep == kMaxSweeps && g.tid == 0 && a.capped) atomicAdd(a.capped, 1ull);
+  if (g.tid == 0 && a.sweeps) atomicAdd(a.sweeps, (unsigned long long)sweep);
+  if (MODE != PM_BATCH && T != nullptr && a.vprev != nullptr) {
+    double* Vp = a.vprev + a.voff[task];
+    Walk w(g.tid, G, kp);
+    for (; w.r < kp; w.next()) Vp[w.r * kp + w.c] = V[w.r * ld + w.c];
+  }
   // ---- reconstruction sum_t max(l_t,0) v_t v_t^T, then the mode epilogue ----
   double p0 = 0.0, p1 = 0.0, p2 = 0.0;
   for (int e = g.tid; e < ns; e += G) {
@@ -295,12 +330,12 @@ __device__ __forceinline__ void fill_blk_table(int* tab) {
 }
 
 // --- small tiers: G lanes per matrix, NG groups per 128-thread CTA ---------
-template <int G, int KMAX>
+template <int G, int KMAX, int NBUF>
 struct SmallLayout {
   static constexpr int NG = 128 / G;
   static constexpr int LD = KMAX + 1;
   static constexpr int P = KMAX / 2;
-  static constexpr int PER = 2 * KMAX * LD + 4 * P;  // doubles per group
+  static constexpr int PER = NBUF * KMAX * LD + 4 * P;  // doubles per group
   static constexpr int NBLK = P * (P + 1) / 2;
   static constexpr size_t bytes() { return (size_t)NG * PER * sizeof(double) + NBLK * sizeof(int); }
 };
@@ -308,7 +343,8 @@ struct SmallLayout {
 template <int G, int KMAX, int MODE>
 __global__ void __launch_bounds__(128) k_psd_small(ProjArgs a) {
   if (a.done && *a.done) return;
-  using Lay = SmallLayout<G, KMAX>;
+  constexpr int NBUF = MODE == PM_BATCH ? 2 : 3;
+  using Lay = SmallLayout<G, KMAX, NBUF>;
   extern __shared__ double smem[];
   int* tab = (int*)(smem + Lay::NG * Lay::PER);
   fill_blk_table<Lay::P, 128>(tab);
@@ -318,7 +354,8 @@ __global__ void __launch_bounds__(128) k_psd_small(ProjArgs a) {
   double* base = smem + (size_t)grp * Lay::PER;
   double* A = base;
   double* V = base + KMAX * Lay::LD;
-  double* rc = V + KMAX * Lay::LD;
+  double* T = NBUF == 3 ? V + KMAX * Lay::LD : nullptr;
+  double* rc = V + (NBUF - 1) * KMAX * Lay::LD;
   double* rs = rc + Lay::P;
   double* rt = rs + Lay::P;
   int* rpq = (int*)(rt + Lay::P);
@@ -328,28 +365,35 @@ __global__ void __launch_bounds__(128) k_psd_small(ProjArgs a) {
   g.mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) / G * G));
   g.red = nullptr;
   const int task = a.ids ? a.ids[task_slot] : task_slot;
-  project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, Lay::LD, rot, a);
+  project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, T, Lay::LD, rot, a);
 }
 
 // --- CTA tiers: one CTA per matrix, A and V in shared memory ---------------
-template <int G, int KMAX>
+template <int G, int KMAX, int NBUF>
 struct CtaLayout {
   static constexpr int LD = KMAX + 1;
   static constexpr int P = KMAX / 2;
   static constexpr int NBLK = P * (P + 1) / 2;
   static constexpr size_t bytes() {
-    return (size_t)(2 * KMAX * LD + 4 * P + G / 32) * sizeof(double) + NBLK * sizeof(int);
+    return (size_t)(NBUF * KMAX * LD + 4 * P + G / 32) * sizeof(double) + NBLK * sizeof(int);
   }
 };
+// warm start needs a third k x k buffer; the 96-tier cannot afford it in 227 KB
+template <int KMAX, int MODE>
+constexpr int cta_nbuf() {
+  return (MODE == PM_BATCH || KMAX > 64) ? 2 : 3;
+}
 
 template <int G, int KMAX, int MODE>
 __global__ void __launch_bounds__(G) k_psd_cta(ProjArgs a) {
   if (a.done && *a.done) return;
-  using Lay = CtaLayout<G, KMAX>;
+  constexpr int NBUF = cta_nbuf<KMAX, MODE>();
+  using Lay = CtaLayout<G, KMAX, NBUF>;
   extern __shared__ double smem[];
   double* A = smem;
   double* V = A + KMAX * Lay::LD;
-  double* rc = V + KMAX * Lay::LD;
+  double* T = NBUF == 3 ? V + KMAX * Lay::LD : nullptr;
+  double* rc = V + (NBUF - 1) * KMAX * Lay::LD;
   double* rs = rc + Lay::P;
   double* rt = rs + Lay::P;
   int* rpq = (int*)(rt + Lay::P);
@@ -363,7 +407,7 @@ __global__ void __launch_bounds__(G) k_psd_cta(ProjArgs a) {
   g.red = red;
   for (int slot = blockIdx.x; slot < a.count; slot += gridDim.x) {
     const int task = a.ids ? a.ids[slot] : slot;
-    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, Lay::LD, rot, a);
+    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, T, Lay::LD, rot, a);
   }
 }
 
@@ -381,11 +425,12 @@ __global__ void __launch_bounds__(G) k_psd_global(ProjArgs a) {
   g.mask = 0xffffffffu;
   g.red = red;
   const int ld = a.ld_work;
-  double* A = a.work + (size_t)blockIdx.x * 2 * ld * ld;
+  double* A = a.work + (size_t)blockIdx.x * 3 * ld * ld;
   double* V = A + (size_t)ld * ld;
+  double* T = MODE == PM_BATCH ? nullptr : V + (size_t)ld * ld;
   for (int slot = blockIdx.x; slot < a.count; slot += gridDim.x) {
     const int task = a.ids ? a.ids[slot] : slot;
-    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, ld, rot, a);
+    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, T, ld, rot, a);
   }
 }
 
@@ -394,22 +439,22 @@ void launch_mode(int bucket, const ProjArgs& a, cudaStream_t s) {
   if (a.count <= 0) return;
   switch (bucket) {
     case B_G8:
-      k_psd_small<8, 8, MODE><<<(a.count + 15) / 16, 128, SmallLayout<8, 8>::bytes(), s>>>(a);
+      k_psd_small<8, 8, MODE><<<(a.count + 15) / 16, 128, SmallLayout<8, 8, MODE == PM_BATCH ? 2 : 3>::bytes(), s>>>(a);
       break;
     case B_G16:
-      k_psd_small<16, 16, MODE><<<(a.count + 7) / 8, 128, SmallLayout<16, 16>::bytes(), s>>>(a);
+      k_psd_small<16, 16, MODE><<<(a.count + 7) / 8, 128, SmallLayout<16, 16, MODE == PM_BATCH ? 2 : 3>::bytes(), s>>>(a);
       break;
     case B_G32:
-      k_psd_small<32, 32, MODE><<<(a.count + 3) / 4, 128, SmallLayout<32, 32>::bytes(), s>>>(a);
+      k_psd_small<32, 32, MODE><<<(a.count + 3) / 4, 128, SmallLayout<32, 32, MODE == PM_BATCH ? 2 : 3>::bytes(), s>>>(a);
       break;
     case B_CTA32:
-      k_psd_cta<128, 32, MODE><<<a.count, 128, CtaLayout<128, 32>::bytes(), s>>>(a);
+      k_psd_cta<128, 32, MODE><<<a.count, 128, CtaLayout<128, 32, cta_nbuf<32, MODE>()>::bytes(), s>>>(a);
       break;
     case B_CTA64:
-      k_psd_cta<128, 64, MODE><<<a.count, 128, CtaLayout<128, 64>::bytes(), s>>>(a);
+      k_psd_cta<128, 64, MODE><<<a.count, 128, CtaLayout<128, 64, cta_nbuf<64, MODE>()>::bytes(), s>>>(a);
       break;
     case B_CTA96:
-      k_psd_cta<256, 96, MODE><<<a.count, 256, CtaLayout<256, 96>::bytes(), s>>>(a);
+      k_psd_cta<256, 96, MODE><<<a.count, 256, CtaLayout<256, 96, cta_nbuf<96, MODE>()>::bytes(), s>>>(a);
       break;
     case B_GLOBAL: {
       const int grid = a.count < a.work_slots ? a.count : a.work_slots;
@@ -421,14 +466,16 @@ void launch_mode(int bucket, const ProjArgs& a, cudaStream_t s) {
 
 template <int MODE>
 void init_attrs_mode() {
+  cudaFuncSetAttribute(k_psd_small<16, 16, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)SmallLayout<16, 16, MODE == PM_BATCH ? 2 : 3>::bytes());
   cudaFuncSetAttribute(k_psd_small<32, 32, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)SmallLayout<32, 32>::bytes());
+                       (int)SmallLayout<32, 32, MODE == PM_BATCH ? 2 : 3>::bytes());
   cudaFuncSetAttribute(k_psd_cta<128, 32, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)CtaLayout<128, 32>::bytes());
+                       (int)CtaLayout<128, 32, cta_nbuf<32, MODE>()>::bytes());
   cudaFuncSetAttribute(k_psd_cta<128, 64, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)CtaLayout<128, 64>::bytes());
+                       (int)CtaLayout<128, 64, cta_nbuf<64, MODE>()>::bytes());
   cudaFuncSetAttribute(k_psd_cta<256, 96, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)CtaLayout<256, 96>::bytes());
+                       (int)CtaLayout<256, 96, cta_nbuf<96, MODE>()>::bytes());
 }
 
 }  // namespace

@@ -189,32 +189,47 @@ __global__ void __launch_bounds__(256) k_trmv(const double* __restrict__ M, int 
 
 // ---------------------------------------------------------------- dense GEMV^T
 // x_t = rD_t - Dinv_t * sum_i A[i][t] y_i    (x = D^-1 (r1 - A^T y))
-// CTA = 256 threads x 2 columns; y staged in shared memory in tiles.
+// CTA = 128 threads x 2 columns; y staged in shared memory in tiles; every
+// thread issues GT_U independent 16-byte evict-first loads before consuming
+// them (explicit batching keeps GT_U loads in flight per thread).
 // Partials: primal <c, x>; dual |D x|^2 (= |sum_k H_k^T lambda_k|^2 / rho^2).
+constexpr int GT_THREADS = 128;
+constexpr int GT_U = 16;
 template <int FORM>
-__global__ void __launch_bounds__(256) k_gemvT_dense(const double* __restrict__ A, int64_t lda, int m, int N,
-                                                      const double* __restrict__ y, const double* __restrict__ rD,
-                                                      const double* __restrict__ Dinv, const double* __restrict__ c,
-                                                      double* __restrict__ x, double* __restrict__ part,
-                                                      const int* done) {
+__global__ void __launch_bounds__(GT_THREADS) k_gemvT_dense(const double* __restrict__ A, int64_t lda, int m, int N,
+                                                             const double* __restrict__ y, const double* __restrict__ rD,
+                                                             const double* __restrict__ Dinv, const double* __restrict__ c,
+                                                             double* __restrict__ x, double* __restrict__ part,
+                                                             const int* done) {
   if (done && *done) return;
   constexpr int TILE = 4096;
   __shared__ double ys[TILE];
-  __shared__ double sm[8];
-  const int64_t t2 = (int64_t)blockIdx.x * 256 + threadIdx.x;  // column pair index
+  __shared__ double sm[GT_THREADS / 32];
+  const int64_t t2 = (int64_t)blockIdx.x * GT_THREADS + threadIdx.x;  // column pair index
   const bool act = 2 * t2 < lda;
-  const double2* Ac = reinterpret_cast<const double2*>(A) + t2;
   const int64_t ld2 = lda / 2;
+  const double2* Ac = reinterpret_cast<const double2*>(A) + (act ? t2 : 0);
   double w0 = 0.0, w1 = 0.0;
   for (int r0 = 0; r0 < m; r0 += TILE) {
     const int nr = (m - r0 < TILE) ? m - r0 : TILE;
     __syncthreads();
-    for (int i = threadIdx.x; i < nr; i += 256) ys[i] = y[r0 + i];
+    for (int i = threadIdx.x; i < nr; i += GT_THREADS) ys[i] = y[r0 + i];
     __syncthreads();
     if (act) {
       const double2* Ap = Ac + (int64_t)r0 * ld2;
-#pragma unroll 8
-      for (int i = 0; i < nr; ++i) {
+      int i = 0;
+      for (; i + GT_U <= nr; i += GT_U) {
+        double2 buf[GT_U];
+#pragma unroll
+        for (int u = 0; u < GT_U; ++u) buf[u] = __ldcs(Ap + (int64_t)(i + u) * ld2);
+#pragma unroll
+        for (int u = 0; u < GT_U; ++u) {
+          const double yi = ys[i + u];
+          w0 = fma(buf[u].x, yi, w0);
+          w1 = fma(buf[u].y, yi, w1);
+        }
+      }
+      for (; i < nr; ++i) {
         const double2 aa = __ldcs(Ap + (int64_t)i * ld2);
         const double yi = ys[i];
         w0 = fma(aa.x, yi, w0);
@@ -236,7 +251,7 @@ __global__ void __launch_bounds__(256) k_gemvT_dense(const double* __restrict__ 
       acc[0] += (FORM == 0) ? c[t + 1] * xv : (xv / Dinv[t + 1]) * (xv / Dinv[t + 1]);
     }
   }
-  block_sum<1, 256>(acc, sm);
+  block_sum<1, GT_THREADS>(acc, sm);
   if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
 }
 
@@ -473,16 +488,16 @@ void launch_trmv(int lower, const double* M, int m, const double* in, double* ou
     k_trmv<0><<<(m + 7) / 8, 256, 0, s>>>(M, m, in, out, done);
 }
 
-int gemvT_blocks(int64_t lda) { return (int)((lda / 2 + 255) / 256); }
+int gemvT_blocks(int64_t lda) { return (int)((lda / 2 + GT_THREADS - 1) / GT_THREADS); }
 
 void launch_gemvT_dense(int form, const double* A, int64_t lda, int m, int N, const double* y, const double* rD,
                         const double* Dinv, const double* c, double* x, double* part, const int* done,
                         cudaStream_t s) {
   const int grid = gemvT_blocks(lda);
   if (form == 0)
-    k_gemvT_dense<0><<<grid, 256, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
+    k_gemvT_dense<0><<<grid, GT_THREADS, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
   else
-    k_gemvT_dense<1><<<grid, 256, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
+    k_gemvT_dense<1><<<grid, GT_THREADS, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
 }
 
 void launch_gemv_csr(int form, const int32_t* rp, const int32_t* ci, const double* val, int m, const double* v,

@@ -175,6 +175,18 @@ def test_iterates_after_50(lib, gen, name, form):
     s.close()
 
 
+@pytest.mark.parametrize("form", ["primal", "dual"])
+def test_iterates_long_run_warm_start(lib, gen, form):
+    """130 iterations: the warm-started Jacobi (V_prev basis) crosses two cold
+    restarts (every 64 iterations); iterates still match the oracle."""
+    prob = gen.config(1)
+    dec, st, s = run_pair(lib, prob, form, 1.0, 130)
+    compare_state(dec, st, s, form)
+    info = s.info()
+    assert info["jacobi_capped"] == 0
+    s.close()
+
+
 def test_determinism_and_reset(lib, gen):
     prob = gen.config(1)
     s = lib.Solver(prob, form="primal", rho=1.0)
