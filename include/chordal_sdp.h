@@ -90,7 +90,8 @@ typedef struct {
   void* stream;              /* cudaStream_t to enqueue on (NULL = default stream)   */
   int32_t check_every;       /* sdp_solve: host reads the stop flag every K iterations (default 10) */
   int32_t use_graph;         /* 1 (default): replay one captured CUDA graph per iteration */
-  int32_t rank, world;       /* reserved for clique sharding; must be 0, 1           */
+  int32_t rank, world;       /* clique sharding over `world` ranks (one GPU each); default 0, 1 */
+  const void* nccl_id;       /* world > 1: 128-byte id from sdp_nccl_unique_id on rank 0, same on all ranks */
 } sdp_options;
 
 typedef struct {
@@ -114,6 +115,13 @@ void sdp_default_options(sdp_options* opt);
 
 /* Build the decomposed problem and upload it (host setup, run once; timed
  * separately, "Setup: Chordal decomposition, KKT factorization").
+ * Sharding (world > 1, collective: every rank calls it with the same full
+ * problem): cliques are split into contiguous ranges balanced by k^3, each rank
+ * runs the projections of its cliques and the affine step on the coordinates
+ * they touch; per iteration three NCCL all-reduces cross ranks (partial sums of
+ * shared coordinates, the m-vector A D^-1 r1 over owned columns, 6 residual
+ * scalars).  Getters of a sharded handle are collective and return the full
+ * (global) vectors.
  * prob, opt: host, read during the call.  out: receives the handle.
  * Errors: SDP_E_INVALID_ARG (index out of range, row > col, duplicate entry,
  * n <= 0, m <= 0, clique order > SDP_MAX_K), SDP_E_RANK_DEFICIENT, SDP_E_CUDA,
@@ -191,6 +199,20 @@ int sdp_project_psd_batch(sdp_psd_plan plan, const double* d_in, double* d_out, 
 int sdp_project_psd_batch_host(sdp_psd_plan plan, const double* h_in, double* h_out, void* stream);
 int64_t sdp_psd_plan_values(sdp_psd_plan plan);   /* total doubles of in/out */
 int sdp_psd_plan_destroy(sdp_psd_plan plan);
+
+/* ---- multi-GPU helpers ----------------------------------------------------- */
+/* 128-byte NCCL unique id (rank 0 calls it and broadcasts it, e.g. through
+ * torch.distributed).  NCCL is loaded with dlopen("libnccl.so.2"). */
+int sdp_nccl_unique_id(void* out128);
+/* Host-only shard plan of the pattern (row, col) for `rank` of `world`:
+ * clique_begin[world+1] (contiguous ranges in canonical clique order),
+ * local_coords[n_local] (pattern coordinates the rank's cliques touch, sorted),
+ * owned[n_local] (1 if the rank owns the coordinate: its first clique is local),
+ * shared_coords[n_shared] (coordinates touched by >= 2 ranks).  cap = capacity of
+ * the coordinate buffers. */
+int sdp_shard_plan(int32_t n, int64_t nnz, const int32_t* row, const int32_t* col, int32_t world, int32_t rank,
+                   int64_t* clique_begin, int64_t* n_local, int32_t* local_coords, uint8_t* owned,
+                   int64_t* n_shared, int32_t* shared_coords, int64_t cap);
 
 const char* sdp_last_error(void);
 

@@ -5,6 +5,7 @@ include/chordal_sdp.h); this package is its thin Python binding.
     from paper_1609_06068_b200 import Solver, PsdPlan, chordal_cliques
 """
 from ._lib import (EXPORTED, LIB_PATH, PsdPlan, SdpError, Solver, chordal_cliques,  # noqa: F401
-                   lib)
+                   lib, nccl_unique_id, shard_plan)
 
-__all__ = ["Solver", "PsdPlan", "chordal_cliques", "SdpError", "lib", "LIB_PATH", "EXPORTED"]
+__all__ = ["Solver", "PsdPlan", "chordal_cliques", "shard_plan", "nccl_unique_id", "SdpError", "lib", "LIB_PATH",
+           "EXPORTED"]

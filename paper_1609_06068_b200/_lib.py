@@ -46,7 +46,8 @@ class sdp_problem(C.Structure):
 
 class sdp_options(C.Structure):
     _fields_ = [("form", C.c_int32), ("rho", C.c_double), ("device", C.c_int32), ("stream", C.c_void_p),
-                ("check_every", C.c_int32), ("use_graph", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32)]
+                ("check_every", C.c_int32), ("use_graph", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
+                ("nccl_id", C.c_void_p)]
 
 
 class sdp_info(C.Structure):
@@ -83,6 +84,9 @@ _sig = {
     "sdp_project_psd_batch_host": (_i32, [_vp, _vp, _vp, _vp]),
     "sdp_psd_plan_values": (_i64, [_vp]),
     "sdp_psd_plan_destroy": (_i32, [_vp]),
+    "sdp_nccl_unique_id": (_i32, [_vp]),
+    "sdp_shard_plan": (_i32, [_i32, _i64, _vp, _vp, _i32, _i32, _vp, C.POINTER(_i64), _vp, _vp, C.POINTER(_i64), _vp,
+                              _i64]),
     "sdp_last_error": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _sig.items():
@@ -140,11 +144,37 @@ def chordal_cliques(n, row, col):
     return out, int(fill.value)
 
 
+def nccl_unique_id():
+    """128-byte NCCL id (bytes) for sharded handles (call on rank 0, broadcast)."""
+    buf = C.create_string_buffer(128)
+    _check(lib.sdp_nccl_unique_id(buf))
+    return buf.raw
+
+
+def shard_plan(n, row, col, world, rank):
+    """sdp_shard_plan: dict(clique_begin, local_coords, owned, shared_coords)."""
+    row = _arr(row, np.int32)
+    col = _arr(col, np.int32)
+    cap = max(16, int(n) * int(n))
+    cap = min(cap, 1 << 26)
+    cb = np.zeros(world + 1, np.int64)
+    loc = np.zeros(cap, np.int32)
+    own = np.zeros(cap, np.uint8)
+    shr = np.zeros(cap, np.int32)
+    nl = C.c_int64()
+    ns = C.c_int64()
+    _check(lib.sdp_shard_plan(n, row.size, _ptr(row), _ptr(col), world, rank, _ptr(cb), C.byref(nl), _ptr(loc),
+                              _ptr(own), C.byref(ns), _ptr(shr), cap))
+    return {"clique_begin": cb, "local_coords": loc[:nl.value].copy(), "owned": own[:nl.value].astype(bool),
+            "shared_coords": shr[:ns.value].copy()}
+
+
 class Solver:
     """Handle of sdp_setup().  `prob` needs the attributes n, m, c_row, c_col,
     c_val, b, a_fmt ("coo" | "dense"), a_con, a_row, a_col, a_val."""
 
-    def __init__(self, prob, form="primal", rho=1.0, device=0, stream=None, use_graph=True, check_every=10):
+    def __init__(self, prob, form="primal", rho=1.0, device=0, stream=None, use_graph=True, check_every=10,
+                 rank=0, world=1, nccl_id=None):
         self.form = form
         keep = []
 
@@ -173,6 +203,9 @@ class Solver:
         O.stream = _stream_ptr(stream)
         O.use_graph = int(bool(use_graph))
         O.check_every = int(check_every)
+        O.rank, O.world = int(rank), int(world)
+        self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        O.nccl_id = C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None
         h = C.c_void_p()
         _check(lib.sdp_setup(C.byref(P), C.byref(O), C.byref(h)))
         self.h = h

@@ -147,6 +147,8 @@ struct sdp_handle_s {
   // A
   int a_dense = 1;
   double* A = nullptr;
+  double* AT = nullptr;  // A^T copy (row-major N x ldm) so A^T y is a row-streaming GEMV
+  int64_t ldm = 0;
   int32_t *a_rp = nullptr, *a_ci = nullptr, *at_cp = nullptr, *at_ri = nullptr;
   double *a_val = nullptr, *at_val = nullptr;
   int s_diag = 0;
@@ -167,6 +169,15 @@ struct sdp_handle_s {
   int warm_period = 64;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
+  // sharding: this rank's local view
+  int world = 1, rank = 0;
+  void* comm = nullptr;         // ncclComm_t
+  int64_t cb = 0, pl = 0, Nl = 0, stotl = 0;  // first clique, local cliques / coordinates / stacked length
+  std::vector<int32_t> local_coords;
+  double* own = nullptr;        // 1.0 on owned local coordinates
+  int nshared = 0, n_fix = 0;
+  int32_t *shared_idx = nullptr, *shared_local = nullptr;
+  double *xbuf = nullptr, *fix_part = nullptr, *red = nullptr;
 };
 
 struct sdp_psd_plan_s {
@@ -216,13 +227,14 @@ int guarded(F&& f) {
 }
 
 void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_NUM], int bcount[B_NUM],
-                   double*& work, int& slots, int& ld_work) {
+                   double*& work, int& slots, int& ld_work, std::vector<int>* bucket_out = nullptr) {
   std::vector<std::vector<int32_t>> lists(B_NUM);
   int64_t in_range[6] = {0, 0, 0, 0, 0, 0};
   for (size_t i = 0; i < ksz.size(); ++i) in_range[size_range(ksz[i])]++;
   int kg = 0;
   for (size_t i = 0; i < ksz.size(); ++i) {
     const int b = bucket_of(ksz[i], in_range[size_range(ksz[i])]);
+    if (bucket_out) bucket_out->push_back(b);
     lists[b].push_back((int32_t)i);
     if (b == B_GLOBAL) kg = std::max(kg, (int)ksz[i]);
   }
@@ -272,7 +284,9 @@ void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
 
 void enqueue_scatter(sdp_handle h, cudaStream_t s) {
   ScatterArgs a{};
-  a.N = (int)h->N;
+  a.N = (int)h->Nl;
+  a.shared_idx = h->shared_idx;
+  a.xbuf = h->xbuf;
   a.seg_ptr = h->seg_ptr;
   a.seg_idx = h->seg_idx;
   a.longc = h->longc;
@@ -287,6 +301,12 @@ void enqueue_scatter(sdp_handle h, cudaStream_t s) {
   a.part = h->scat_part;
   a.done = h->done;
   launch_scatter(h->form, a, s);
+  if (h->world > 1 && h->nshared > 0) {
+    // exchange: partial sums of coordinates shared across ranks (allreduce #1)
+    nccl_allreduce_sum(h->comm, h->xbuf, 3 * (size_t)h->nshared, s);
+    launch_shared_fixup(h->nshared, h->shared_local, h->xbuf, h->Dinv, h->own, h->rD, h->sprev, h->fix_part,
+                        h->done, s);
+  }
 }
 
 // Phase hook: records an event at a phase boundary when profiling.
@@ -312,15 +332,28 @@ void enqueue_kkt(sdp_handle h, cudaStream_t s) {
   const int f = h->form;
   double* ydst = h->s_diag ? h->y : nullptr;
   phase(0, s);
+  const bool shard = h->world > 1;
   if (h->a_dense) {
     launch_gemv_dense(h->A, h->lda, h->m, h->rD, h->chunk, h->gemv_part, h->done, s);
     phase(1, s);
-    launch_reduce_u(f, h->gemv_part, h->nchunks, h->m, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr, ydst,
-                    h->done, s);
+    if (shard)  // partial u over owned columns
+      launch_reduce_u(f, h->gemv_part, h->nchunks, h->m, nullptr, h->rho, h->u, nullptr, nullptr, h->done, s);
+    else
+      launch_reduce_u(f, h->gemv_part, h->nchunks, h->m, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr, ydst,
+                      h->done, s);
   } else {
-    launch_gemv_csr(f, h->a_rp, h->a_ci, h->a_val, h->m, h->rD, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr,
-                    ydst, h->done, s);
+    if (shard)
+      launch_gemv_csr(f, h->a_rp, h->a_ci, h->a_val, h->m, h->rD, nullptr, h->rho, h->u, nullptr, nullptr, h->done,
+                      s);
+    else
+      launch_gemv_csr(f, h->a_rp, h->a_ci, h->a_val, h->m, h->rD, h->b, h->rho, h->u,
+                      h->s_diag ? h->sdiag : nullptr, ydst, h->done, s);
     phase(1, s);
+  }
+  if (shard) {
+    // exchange: u = sum over ranks of A[:, owned] D^-1 r1 (allreduce #2), then - r2 (and / S_ii)
+    nccl_allreduce_sum(h->comm, h->u, (size_t)h->m, s);
+    launch_reduce_u(f, h->u, 1, h->m, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr, ydst, h->done, s);
   }
   if (!h->s_diag) {
     launch_trmv(1, h->W, h->m, h->u, h->t, h->done, s);   // t = L^-1 u
@@ -328,16 +361,21 @@ void enqueue_kkt(sdp_handle h, cudaStream_t s) {
   }
   phase(2, s);
   if (h->a_dense)
-    launch_gemvT_dense(f, h->A, h->lda, h->m, (int)h->N, h->y, h->rD, h->Dinv, h->c, h->x, h->gT_part, h->done, s);
+    launch_gemvT_rows(f, h->AT, h->ldm, h->m, (int)h->Nl, h->y, h->rD, h->Dinv, h->c, h->own, h->x, h->gT_part,
+                      h->done, s);
   else
-    launch_gemvT_csc(f, h->at_cp, h->at_ri, h->at_val, (int)h->N, h->y, h->rD, h->Dinv, h->c, h->x, h->gT_part,
+    launch_gemvT_csc(f, h->at_cp, h->at_ri, h->at_val, (int)h->Nl, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+                     h->gT_part,
                      h->done, s);
 }
 
 void enqueue_finalize(sdp_handle h, cudaStream_t s) {
   FinalArgs a{};
   a.proj_part = h->proj_part;
-  a.n_proj = (int)h->p;
+  a.n_proj = (int)h->pl;
+  a.fix_part = h->fix_part;
+  a.n_fix = h->world > 1 ? h->n_fix : 0;
+  a.red = h->red;
   a.upd_part = h->upd_part;
   a.n_upd = h->nb_upd;
   a.scat_part = h->scat_part;
@@ -355,7 +393,13 @@ void enqueue_finalize(sdp_handle h, cudaStream_t s) {
   a.done = h->done;
   a.numerical = h->numerical;
   a.tol = h->tol;
-  launch_finalize(h->form, a, s);
+  if (h->world == 1) {
+    launch_finalize(h->form, 0, a, s);
+  } else {
+    launch_finalize(h->form, 1, a, s);
+    nccl_allreduce_sum(h->comm, h->red, 6, s);  // residual partials (allreduce #3)
+    launch_finalize(h->form, 2, a, s);
+  }
 }
 
 // One ADMM iteration (Algorithm 1 lines 4-7 / Algorithm 2 lines 4-8).
@@ -373,7 +417,7 @@ void enqueue_iteration(sdp_handle h, cudaStream_t s) {
     enqueue_scatter(h, s);                   // rhs of E:OptCondMinYDual
     enqueue_kkt(h, s);                       // x, y
     phase(5, s);
-    launch_update_dual(h->stot, h->G, h->x, h->xk, h->lam, h->vk, h->rho, h->upd_part, h->done, s);  // v_k, lambda_k
+    launch_update_dual(h->stotl, h->G, h->x, h->xk, h->lam, h->vk, h->rho, h->upd_part, h->done, s);  // v_k, lambda_k
   }
   phase(6, s);
   enqueue_finalize(h, s);
@@ -382,12 +426,13 @@ void enqueue_iteration(sdp_handle h, cudaStream_t s) {
 
 int launches_per_iter(sdp_handle h) {
   int n = 0;
-  for (int b = 0; b < B_NUM; ++b) n += h->bcount[b] ? 1 : 0;
+  for (int b = 0; b < B_NUM; ++b) n += h->bcount[b] ? 1 : 0;  // one projection launch per non-empty tier
   n += 1;                                       // scatter
   n += h->a_dense ? 3 : 2;                      // gemv (+ reduce) + gemvT
   n += h->s_diag ? 0 : 2;                       // triangular solves
   n += (h->form == SDP_FORM_DUAL) ? 1 : 0;      // dual update
   n += 1;                                       // finalize
+  if (h->world > 1) n += 2 + (h->nshared > 0 ? 1 : 0);  // second reduce_u, finalize phase 2, fixup
   return n;
 }
 
@@ -409,9 +454,10 @@ void rebuild_graph(sdp_handle h) {
 
 void reset_state(sdp_handle h) {
   cudaStream_t s = h->stream;
-  SDP_CUDA_TRY(cudaMemsetAsync(h->xk, 0, h->stot * sizeof(double), s));
-  SDP_CUDA_TRY(cudaMemsetAsync(h->lam, 0, h->stot * sizeof(double), s));
-  SDP_CUDA_TRY(cudaMemsetAsync(h->vk, 0, h->stot * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->xk, 0, h->stotl * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->lam, 0, h->stotl * sizeof(double), s));
+  SDP_CUDA_TRY(cudaMemsetAsync(h->vk, 0, h->stotl * sizeof(double), s));
+  if (h->xbuf) SDP_CUDA_TRY(cudaMemsetAsync(h->xbuf, 0, 3 * (size_t)h->nshared * sizeof(double), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->x, 0, h->lda * sizeof(double), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->rD, 0, h->lda * sizeof(double), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->sprev, 0, h->lda * sizeof(double), s));
@@ -447,6 +493,7 @@ void destroy_handle(sdp_handle h) {
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   h->alloc.free_all();
+  if (h->comm) nccl_comm_destroy(h->comm);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   if (cur >= 0) cudaSetDevice(cur);
@@ -466,8 +513,8 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   if (m <= 0) throw Error{SDP_E_INVALID_ARG, "m <= 0"};
   if (!(opt.rho > 0) || !std::isfinite(opt.rho)) throw Error{SDP_E_INVALID_ARG, "rho must be positive"};
   if (opt.form != SDP_FORM_PRIMAL && opt.form != SDP_FORM_DUAL) throw Error{SDP_E_INVALID_ARG, "bad form"};
-  if (opt.world != 1 || opt.rank != 0)
-    throw Error{SDP_E_INVALID_ARG, "clique sharding across ranks is not available in this build (world must be 1)"};
+  if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) throw Error{SDP_E_INVALID_ARG, "bad rank/world"};
+  if (opt.world > 1 && !opt.nccl_id) throw Error{SDP_E_INVALID_ARG, "world > 1 needs nccl_id (sdp_nccl_unique_id)"};
   if (!P->b) throw Error{SDP_E_INVALID_ARG, "b is NULL"};
   if (P->c_nnz < 0 || (P->c_nnz > 0 && (!P->c_row || !P->c_col || !P->c_val)))
     throw Error{SDP_E_INVALID_ARG, "C arrays missing"};
@@ -519,15 +566,17 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->fill_edges = cr.fill_edges;
   h->stream = (cudaStream_t)opt.stream;  // NULL = the legacy default stream, as in the CUDA runtime
   h->own_stream = false;
+  h->world = opt.world;
+  h->rank = opt.rank;
+  if (h->world > 1) h->comm = nccl_comm_init(opt.nccl_id, h->world, h->rank);  // collective
   SDP_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
   const int64_t N = (int64_t)cr.coord_row.size();
   h->N = N;
-  h->lda = (N + 31) / 32 * 32;
   h->coord_row = cr.coord_row;
   h->coord_col = cr.coord_col;
   if (N >= (1ll << 31)) throw Error{SDP_E_INVALID_ARG, "pattern too large"};
 
-  // ---- 2. layout: clique offsets, H_k maps, D, inverse map
+  // ---- 2. global layout: clique offsets, H_k maps, D, inverse map
   const int64_t p = (int64_t)cr.cliques.size();
   h->p = p;
   std::vector<int64_t> off(p + 1, 0);
@@ -550,7 +599,6 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->clique_off = off;
   if (stot >= (1ll << 31)) throw Error{SDP_E_INVALID_ARG, "stacked clique vectors too large"};
   std::vector<int32_t> Gmap(stot);
-  std::vector<int32_t> cnt(N + 1, 0);
 #pragma omp parallel for schedule(dynamic, 16)
   for (int64_t k = 0; k < p; ++k) {
     const auto& C = cr.cliques[k];
@@ -558,54 +606,114 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     for (size_t bcol = 0; bcol < C.size(); ++bcol)
       for (size_t arow = 0; arow <= bcol; ++arow) Gmap[e++] = (int32_t)coord_index(cr, C[arow], C[bcol]);
   }
-  for (int64_t s = 0; s < stot; ++s) cnt[Gmap[s] + 1]++;
-  std::vector<int32_t> seg_ptr(N + 1, 0);
-  for (int64_t t = 0; t < N; ++t) seg_ptr[t + 1] = seg_ptr[t] + cnt[t + 1];
-  std::vector<int32_t> seg_idx(stot), fillp(seg_ptr.begin(), seg_ptr.end() - 1);
-  for (int64_t s = 0; s < stot; ++s) seg_idx[fillp[Gmap[s]]++] = (int32_t)s;
-  std::vector<double> Dinv(h->lda, 0.0);
-  std::vector<int32_t> longc;
+  std::vector<int32_t> seg_ptr(N + 1, 0), seg_idx(stot);
+  {
+    std::vector<int32_t> cnt(N + 1, 0);
+    for (int64_t s = 0; s < stot; ++s) cnt[Gmap[s] + 1]++;
+    for (int64_t t = 0; t < N; ++t) seg_ptr[t + 1] = seg_ptr[t] + cnt[t + 1];
+    std::vector<int32_t> fillp(seg_ptr.begin(), seg_ptr.end() - 1);
+    for (int64_t s = 0; s < stot; ++s) seg_idx[fillp[Gmap[s]]++] = (int32_t)s;
+  }
+  std::vector<double> Dinv_g(N);
   for (int64_t t = 0; t < N; ++t) {
     const int d = seg_ptr[t + 1] - seg_ptr[t];
     if (d <= 0) throw Error{SDP_E_INVALID_ARG, "internal: pattern coordinate covered by no clique"};
-    Dinv[t] = 1.0 / (double)d;
-    if (d > kLongSeg) longc.push_back((int32_t)t);
+    Dinv_g[t] = 1.0 / (double)d;
   }
-  h->n_long = (int)longc.size();
-
-  // ---- 3. c = svec(C) on the pattern
-  std::vector<double> cvec(h->lda, 0.0);
+  // c = svec(C) on the pattern
+  std::vector<double> cglob(N, 0.0);
   {
     std::vector<char> seen(N, 0);
     for (int64_t e = 0; e < P->c_nnz; ++e) {
       const int64_t t = coord_index(cr, P->c_row[e], P->c_col[e]);
       if (seen[t]) throw Error{SDP_E_INVALID_ARG, "duplicate C entry " + std::to_string(e)};
       seen[t] = 1;
-      cvec[t] = P->c_val[e] * (P->c_row[e] == P->c_col[e] ? 1.0 : kSqrt2);
+      cglob[t] = P->c_val[e] * (P->c_row[e] == P->c_col[e] ? 1.0 : kSqrt2);
     }
   }
 
-  // ---- 4. device uploads of the layout
+  // ---- 3. shard plan and this rank's local view; identity when world == 1
+  if (h->world > p) throw Error{SDP_E_INVALID_ARG, "more ranks than cliques"};
+  ShardPlan sp;
+  if (h->world == 1) {
+    sp.clique_begin = {0, p};
+    sp.local_coords.resize(N);
+    std::iota(sp.local_coords.begin(), sp.local_coords.end(), 0);
+    sp.owned.assign(N, 1);
+  } else {
+    sp = make_shard_plan(ksz, off, seg_ptr, seg_idx, h->world, h->rank);
+  }
+  const int64_t cb = sp.clique_begin[h->rank], ce = sp.clique_begin[h->rank + 1];
+  const int64_t pl = ce - cb, Nl = (int64_t)sp.local_coords.size();
+  const int64_t stotl = off[ce] - off[cb];
+  h->cb = cb;
+  h->pl = pl;
+  h->Nl = Nl;
+  h->stotl = stotl;
+  h->lda = (Nl + 31) / 32 * 32;
+  h->local_coords = sp.local_coords;
+  h->nshared = (int)sp.shared_coords.size();
+  std::vector<int32_t> g2l(N, -1);
+  for (int64_t i = 0; i < Nl; ++i) g2l[sp.local_coords[i]] = (int32_t)i;
+  std::vector<int64_t> offl(pl + 1);
+  std::vector<int32_t> kszl(pl);
+  for (int64_t k = 0; k <= pl; ++k) offl[k] = off[cb + k] - off[cb];
+  for (int64_t k = 0; k < pl; ++k) kszl[k] = ksz[cb + k];
+  std::vector<int32_t> Gl(stotl);
+  for (int64_t s = 0; s < stotl; ++s) Gl[s] = g2l[Gmap[off[cb] + s]];
+  std::vector<int32_t> segl_ptr(Nl + 1, 0), segl_idx(stotl);
+  {
+    std::vector<int32_t> cnt(Nl + 1, 0);
+    for (int64_t s = 0; s < stotl; ++s) cnt[Gl[s] + 1]++;
+    for (int64_t t = 0; t < Nl; ++t) segl_ptr[t + 1] = segl_ptr[t] + cnt[t + 1];
+    std::vector<int32_t> fillp(segl_ptr.begin(), segl_ptr.end() - 1);
+    for (int64_t s = 0; s < stotl; ++s) segl_idx[fillp[Gl[s]]++] = (int32_t)s;
+  }
+  std::vector<double> Dinv(h->lda, 0.0), cvec(h->lda, 0.0), own(h->lda, 0.0);
+  std::vector<int32_t> longc, shared_idx(Nl, -1);
+  for (int64_t t = 0; t < Nl; ++t) {
+    const int64_t tg = sp.local_coords[t];
+    Dinv[t] = Dinv_g[tg];  // D counts every clique (all ranks) containing the coordinate
+    own[t] = sp.owned[t] ? 1.0 : 0.0;
+    cvec[t] = sp.owned[t] ? cglob[tg] : 0.0;  // c enters the partial sums once, at the owner
+    if (segl_ptr[t + 1] - segl_ptr[t] > kLongSeg) longc.push_back((int32_t)t);
+  }
+  for (int j = 0; j < h->nshared; ++j)
+    if (sp.shared_local[j] >= 0) shared_idx[sp.shared_local[j]] = j;
+  h->n_long = (int)longc.size();
+
+  // ---- 4. device uploads of the local layout
   Alloc& al = h->alloc;
-  h->G = al.upload(Gmap);
-  h->seg_ptr = al.upload(seg_ptr);
-  h->seg_idx = al.upload(seg_idx);
+  h->G = al.upload(Gl);
+  h->seg_ptr = al.upload(segl_ptr);
+  h->seg_idx = al.upload(segl_idx);
   h->longc = al.upload(longc);
   h->Dinv = al.upload(Dinv);
   h->c = al.upload(cvec);
-  h->d_off = al.upload(off);
-  h->d_ksz = al.upload(ksz);
+  h->own = al.upload(own);
+  h->d_off = al.upload(offl);
+  h->d_ksz = al.upload(kszl);
   h->b = al.upload(std::vector<double>(P->b, P->b + m));
   h->x = al.zeros<double>(h->lda);
   h->rD = al.zeros<double>(h->lda);
   h->sprev = al.zeros<double>(h->lda);
-  h->y = al.zeros<double>(m);
+  h->ldm = (m + 31) / 32 * 32;
+  h->y = al.zeros<double>(h->ldm);
   h->u = al.zeros<double>(m);
   h->t = al.zeros<double>(m);
-  h->xk = al.zeros<double>(stot);
-  h->lam = al.zeros<double>(stot);
-  h->vk = al.zeros<double>(stot);
-  build_buckets(al, ksz, h->d_ids, h->bcount, h->work, h->work_slots, h->ld_work);
+  h->xk = al.zeros<double>(stotl);
+  h->lam = al.zeros<double>(stotl);
+  h->vk = al.zeros<double>(stotl);
+  if (h->nshared > 0) {
+    h->shared_idx = al.upload(shared_idx);
+    h->shared_local = al.upload(sp.shared_local);
+    h->xbuf = al.zeros<double>(3 * (size_t)h->nshared);
+  }
+  h->n_fix = h->nshared > 0 ? fixup_blocks(h->nshared) : 0;
+  h->fix_part = al.zeros<double>(2 * (size_t)std::max(1, h->n_fix));
+  h->red = al.zeros<double>(8);
+  std::vector<int> task_bucket;
+  build_buckets(al, kszl, h->d_ids, h->bcount, h->work, h->work_slots, h->ld_work, &task_bucket);
 
   // ---- 5. A (svec rows) and S = A D^-1 A^T, factor cached once
   std::vector<double> S;
@@ -619,7 +727,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
       const int64_t t = coord_index(cr, P->a_row[e], P->a_col[e]);
       if (seen[t]) throw Error{SDP_E_INVALID_ARG, "duplicate A pattern entry " + std::to_string(e)};
       seen[t] = 1;
-      map[e] = t;
+      map[e] = g2l[t];  // -1: not on this rank
       scale[e] = (P->a_row[e] == P->a_col[e]) ? 1.0 : kSqrt2;
     }
     h->A = al.zeros<double>((size_t)m * h->lda);
@@ -642,12 +750,22 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
       al.release(dmap);
       al.release(dscale);
     }
+    // A^T copy over every local coordinate (x is needed on all of them) ...
+    h->AT = al.zeros<double>((size_t)Nl * h->ldm);
+    launch_transpose(h->A, h->lda, m, h->AT, h->ldm, Nl, nullptr);
+    SDP_CUDA_TRY(cudaGetLastError());
+    // ... while A keeps only the owned columns: u = A D^-1 r1 is summed over ranks
+    if (h->world > 1) {
+      launch_mask_cols(h->A, h->lda, m, h->own, nullptr);
+      SDP_CUDA_TRY(cudaGetLastError());
+    }
     h->chunk = 8192;
     h->nchunks = (int)((h->lda + h->chunk - 1) / h->chunk);
     h->gemv_part = al.zeros<double>((size_t)h->nchunks * m);
     double* dS = al.get<double>((size_t)m * m);
     launch_syrk_dense(h->A, h->lda, m, h->Dinv, dS, nullptr);
     SDP_CUDA_TRY(cudaGetLastError());
+    if (h->world > 1) nccl_allreduce_sum(h->comm, dS, (size_t)m * m, nullptr);  // S = sum of owned-column parts
     S.resize((size_t)m * m);
     SDP_CUDA_TRY(cudaMemcpy(S.data(), dS, S.size() * sizeof(double), cudaMemcpyDeviceToHost));
     al.release(dS);
@@ -669,26 +787,38 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     for (size_t e = 1; e < ents.size(); ++e)
       if (ents[e].con == ents[e - 1].con && ents[e].t == ents[e - 1].t)
         throw Error{SDP_E_INVALID_ARG, "duplicate A entry (constraint " + std::to_string(ents[e].con) + ")"};
-    std::vector<int32_t> rp(m + 1, 0), ci(ents.size());
-    std::vector<double> val(ents.size());
-    for (size_t e = 0; e < ents.size(); ++e) {
-      rp[ents[e].con + 1]++;
-      ci[e] = ents[e].t;
-      val[e] = ents[e].v;
+    // global column counts decide whether S is diagonal; S itself from all entries
+    std::vector<int32_t> colcnt(N, 0);
+    for (auto& en : ents) colcnt[en.t]++;
+    int maxcol = 0;
+    for (int64_t t = 0; t < N; ++t) maxcol = std::max(maxcol, colcnt[t]);
+    // local CSR (owned columns, for u) and CSC (all local columns, for x), local indices
+    std::vector<int32_t> rp(m + 1, 0), ci;
+    std::vector<double> val;
+    for (auto& en : ents) {
+      const int32_t tl = g2l[en.t];
+      if (tl < 0 || !sp.owned[tl]) continue;
+      rp[en.con + 1]++;
+      ci.push_back(tl);
+      val.push_back(en.v);
     }
     for (int i = 0; i < m; ++i) rp[i + 1] += rp[i];
-    // CSC
-    std::vector<int32_t> cp(N + 1, 0), ri(ents.size());
-    std::vector<double> cval(ents.size());
-    for (auto& en : ents) cp[en.t + 1]++;
-    for (int64_t t = 0; t < N; ++t) cp[t + 1] += cp[t];
-    std::vector<int32_t> pos(cp.begin(), cp.end() - 1);
-    int maxcol = 0;
-    for (auto& en : ents) {  // ents sorted by (con, t): rows ascend inside each column
-      ri[pos[en.t]] = en.con;
-      cval[pos[en.t]++] = en.v;
+    std::vector<int32_t> cp(Nl + 1, 0), ri;
+    std::vector<double> cval;
+    for (auto& en : ents)
+      if (g2l[en.t] >= 0) cp[g2l[en.t] + 1]++;
+    for (int64_t t = 0; t < Nl; ++t) cp[t + 1] += cp[t];
+    ri.resize(cp[Nl]);
+    cval.resize(cp[Nl]);
+    {
+      std::vector<int32_t> pos(cp.begin(), cp.end() - 1);
+      for (auto& en : ents) {  // ents sorted by (con, t): rows ascend inside each column
+        const int32_t tl = g2l[en.t];
+        if (tl < 0) continue;
+        ri[pos[tl]] = en.con;
+        cval[pos[tl]++] = en.v;
+      }
     }
-    for (int64_t t = 0; t < N; ++t) maxcol = std::max(maxcol, cp[t + 1] - cp[t]);
     h->a_rp = al.upload(rp);
     h->a_ci = al.upload(ci);
     h->a_val = al.upload(val);
@@ -698,17 +828,27 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     if (maxcol <= 1) {
       // rows of A have disjoint supports: S = A D^-1 A^T is diagonal
       std::vector<double> sd(m, 0.0);
-      for (int i = 0; i < m; ++i)
-        for (int e = rp[i]; e < rp[i + 1]; ++e) sd[i] += val[e] * val[e] * Dinv[ci[e]];
+      for (auto& en : ents) sd[en.con] += en.v * en.v * Dinv_g[en.t];
       for (int i = 0; i < m; ++i)
         if (!(sd[i] > 0)) throw Error{SDP_E_RANK_DEFICIENT, "constraint " + std::to_string(i) + " is empty"};
       h->s_diag = 1;
       h->sdiag = al.upload(sd);
     } else {
+      // S_ij = sum_t A_it A_jt / D_t over all coordinates (every rank holds the full problem)
+      std::vector<int32_t> gcp(N + 1, 0), gri(ents.size());
+      std::vector<double> gval(ents.size());
+      for (auto& en : ents) gcp[en.t + 1]++;
+      for (int64_t t = 0; t < N; ++t) gcp[t + 1] += gcp[t];
+      std::vector<int32_t> pos(gcp.begin(), gcp.end() - 1);
+      for (auto& en : ents) {
+        gri[pos[en.t]] = en.con;
+        gval[pos[en.t]++] = en.v;
+      }
       S.assign((size_t)m * m, 0.0);
       for (int64_t t = 0; t < N; ++t)
-        for (int e1 = cp[t]; e1 < cp[t + 1]; ++e1)
-          for (int e2 = cp[t]; e2 < cp[t + 1]; ++e2) S[(size_t)ri[e1] * m + ri[e2]] += cval[e1] * cval[e2] * Dinv[t];
+        for (int e1 = gcp[t]; e1 < gcp[t + 1]; ++e1)
+          for (int e2 = gcp[t]; e2 < gcp[t + 1]; ++e2)
+            S[(size_t)gri[e1] * m + gri[e2]] += gval[e1] * gval[e2] * Dinv_g[t];
     }
   }
   if (!h->s_diag) {
@@ -724,10 +864,10 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   }
 
   // ---- 6. residual buffers, state, graph
-  h->nb_scat = scatter_blocks((int)N, h->n_long);
-  h->nb_gT = h->a_dense ? gemvT_blocks(h->lda) : gemvT_csc_blocks((int)N);
-  h->nb_upd = update_blocks(stot);
-  h->proj_part = al.zeros<double>(3 * (size_t)p);
+  h->nb_scat = scatter_blocks((int)Nl, h->n_long);
+  h->nb_gT = h->a_dense ? gemvT_rows_blocks(Nl) : gemvT_csc_blocks((int)Nl);
+  h->nb_upd = update_blocks(stotl);
+  h->proj_part = al.zeros<double>(3 * (size_t)std::max<int64_t>(pl, 1));
   h->scat_part = al.zeros<double>(2 * (size_t)h->nb_scat);
   h->gT_part = al.zeros<double>(h->nb_gT);
   h->upd_part = al.zeros<double>(3 * (size_t)h->nb_upd);
@@ -740,13 +880,13 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->capped = al.zeros<unsigned long long>(1);
   h->sweeps = al.zeros<unsigned long long>(1);
   {  // warm-start eigenvector storage: kp x kp per clique
-    std::vector<int64_t> voff(p + 1, 0);
-    for (int64_t k = 0; k < p; ++k) {
-      const int64_t kp = ksz[k] + (ksz[k] & 1);
+    std::vector<int64_t> voff(pl + 1, 0);
+    for (int64_t k = 0; k < pl; ++k) {
+      const int64_t kp = store_kp(task_bucket[k], kszl[k]);
       voff[k + 1] = voff[k] + kp * kp;
     }
     h->voff = al.upload(voff);
-    h->vprev = al.zeros<double>((size_t)voff[p]);
+    h->vprev = al.zeros<double>((size_t)std::max<int64_t>(voff[pl], 1));
   }
   psd_init_attributes();
   SDP_CUDA_TRY(cudaDeviceSynchronize());
@@ -754,6 +894,17 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   rebuild_graph(h);
   h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return SDP_OK;
+}
+
+// Sum a host vector over the ranks (getters of a sharded handle; collective).
+void allreduce_host(sdp_handle h, std::vector<double>& v) {
+  double* d = nullptr;
+  SDP_CUDA_TRY(cudaMalloc(&d, std::max<size_t>(v.size(), 1) * sizeof(double)));
+  SDP_CUDA_TRY(cudaMemcpy(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+  nccl_allreduce_sum(h->comm, d, v.size(), h->stream);
+  SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  SDP_CUDA_TRY(cudaMemcpy(v.data(), d, v.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  cudaFree(d);
 }
 
 void fill_info(sdp_handle h, sdp_info* info) {
@@ -810,6 +961,7 @@ void sdp_default_options(sdp_options* opt) {
   opt->use_graph = 1;
   opt->rank = 0;
   opt->world = 1;
+  opt->nccl_id = nullptr;
 }
 
 int sdp_setup(const sdp_problem* prob, const sdp_options* opt, sdp_handle* out) {
@@ -906,7 +1058,18 @@ int sdp_get_vector(sdp_handle h, int32_t which, double* out) {
     DeviceGuard dg(h->device);
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (which == SDP_VEC_X || which == SDP_VEC_XMAT) {
-      SDP_CUDA_TRY(cudaMemcpy(out, h->x, h->N * sizeof(double), cudaMemcpyDeviceToHost));
+      if (h->world == 1) {
+        SDP_CUDA_TRY(cudaMemcpy(out, h->x, h->N * sizeof(double), cudaMemcpyDeviceToHost));
+      } else {  // collective: owners contribute their coordinates
+        std::vector<double> xl(h->Nl), own(h->Nl);
+        SDP_CUDA_TRY(cudaMemcpy(xl.data(), h->x, h->Nl * sizeof(double), cudaMemcpyDeviceToHost));
+        SDP_CUDA_TRY(cudaMemcpy(own.data(), h->own, h->Nl * sizeof(double), cudaMemcpyDeviceToHost));
+        std::vector<double> full(h->N, 0.0);
+        for (int64_t i = 0; i < h->Nl; ++i)
+          if (own[i] != 0.0) full[h->local_coords[i]] = xl[i];
+        allreduce_host(h, full);
+        std::memcpy(out, full.data(), h->N * sizeof(double));
+      }
       if (which == SDP_VEC_XMAT)
         for (int64_t t = 0; t < h->N; ++t)
           if (h->coord_row[t] != h->coord_col[t]) out[t] /= kSqrt2;
@@ -926,7 +1089,15 @@ int sdp_get_blocks(sdp_handle h, int32_t which, double* out) {
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
     const double* src = which == SDP_BLK_XK ? h->xk : which == SDP_BLK_LAMBDA ? h->lam : which == SDP_BLK_VK ? h->vk : nullptr;
     if (!src) throw Error{SDP_E_INVALID_ARG, "unknown block id"};
-    SDP_CUDA_TRY(cudaMemcpy(out, src, h->stot * sizeof(double), cudaMemcpyDeviceToHost));
+    if (h->world == 1) {
+      SDP_CUDA_TRY(cudaMemcpy(out, src, h->stot * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {  // collective: every rank places its clique range
+      std::vector<double> full(h->stot, 0.0);
+      SDP_CUDA_TRY(cudaMemcpy(full.data() + h->clique_off[h->cb], src, h->stotl * sizeof(double),
+                              cudaMemcpyDeviceToHost));
+      allreduce_host(h, full);
+      std::memcpy(out, full.data(), h->stot * sizeof(double));
+    }
     return SDP_OK;
   });
 }
@@ -1130,6 +1301,59 @@ int sdp_psd_plan_destroy(sdp_psd_plan pl) {
     pl->alloc.free_all();
     if (cur >= 0) cudaSetDevice(cur);
     delete pl;
+    return SDP_OK;
+  });
+}
+
+int sdp_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    if (!out128) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    nccl_unique_id(out128);
+    return SDP_OK;
+  });
+}
+
+int sdp_shard_plan(int32_t n, int64_t nnz, const int32_t* row, const int32_t* col, int32_t world, int32_t rank,
+                   int64_t* clique_begin, int64_t* n_local, int32_t* local_coords, uint8_t* owned,
+                   int64_t* n_shared, int32_t* shared_coords, int64_t cap) {
+  return guarded([&] {
+    if (n <= 0 || world < 1 || rank < 0 || rank >= world) throw Error{SDP_E_INVALID_ARG, "bad n/world/rank"};
+    if (nnz > 0 && (!row || !col)) throw Error{SDP_E_INVALID_ARG, "NULL pattern"};
+    if (!clique_begin || !n_local || !local_coords || !owned || !n_shared || !shared_coords)
+      throw Error{SDP_E_INVALID_ARG, "NULL output"};
+    check_indices("pattern", nnz, row, col, n);
+    std::vector<std::pair<int32_t, int32_t>> edges;
+    for (int64_t e = 0; e < nnz; ++e)
+      if (row[e] != col[e]) edges.push_back({row[e], col[e]});
+    ChordalResult cr = chordal_analysis(n, edges);
+    const int64_t p = (int64_t)cr.cliques.size(), N = (int64_t)cr.coord_row.size();
+    std::vector<int64_t> off(p + 1, 0);
+    std::vector<int32_t> ksz(p);
+    for (int64_t k = 0; k < p; ++k) {
+      ksz[k] = (int32_t)cr.cliques[k].size();
+      off[k + 1] = off[k] + (int64_t)ksz[k] * (ksz[k] + 1) / 2;
+    }
+    std::vector<int32_t> Gmap(off[p]);
+    for (int64_t k = 0; k < p; ++k) {
+      const auto& C = cr.cliques[k];
+      int64_t e = off[k];
+      for (size_t bcol = 0; bcol < C.size(); ++bcol)
+        for (size_t arow = 0; arow <= bcol; ++arow) Gmap[e++] = (int32_t)coord_index(cr, C[arow], C[bcol]);
+    }
+    std::vector<int32_t> seg_ptr(N + 1, 0), seg_idx(off[p]);
+    for (int64_t s2 = 0; s2 < off[p]; ++s2) seg_ptr[Gmap[s2] + 1]++;
+    for (int64_t t = 0; t < N; ++t) seg_ptr[t + 1] += seg_ptr[t];
+    std::vector<int32_t> fillp(seg_ptr.begin(), seg_ptr.end() - 1);
+    for (int64_t s2 = 0; s2 < off[p]; ++s2) seg_idx[fillp[Gmap[s2]]++] = (int32_t)s2;
+    if (world > p) throw Error{SDP_E_INVALID_ARG, "more ranks than cliques"};
+    ShardPlan sp = make_shard_plan(ksz, off, seg_ptr, seg_idx, world, rank);
+    for (int r = 0; r <= world; ++r) clique_begin[r] = sp.clique_begin[r];
+    *n_local = (int64_t)sp.local_coords.size();
+    *n_shared = (int64_t)sp.shared_coords.size();
+    if (*n_local > cap || *n_shared > cap) throw Error{SDP_E_INVALID_ARG, "output buffers too small"};
+    std::memcpy(local_coords, sp.local_coords.data(), sp.local_coords.size() * sizeof(int32_t));
+    std::memcpy(owned, sp.owned.data(), sp.owned.size());
+    std::memcpy(shared_coords, sp.shared_coords.data(), sp.shared_coords.size() * sizeof(int32_t));
     return SDP_OK;
   });
 }

@@ -37,9 +37,29 @@ struct ChordalResult {
 ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges);
 int64_t coord_index(const ChordalResult& cr, int32_t i, int32_t j);  // -1 if absent
 
+// ---------------------------------------------------------------- sharding (shard.cpp)
+struct ShardPlan {
+  int world = 1, rank = 0;
+  std::vector<int64_t> clique_begin;   // world + 1 boundaries of contiguous clique ranges
+  std::vector<int32_t> local_coords;   // sorted global coordinates touched by this rank
+  std::vector<uint8_t> owned;          // per local coordinate: 1 if this rank owns it
+  std::vector<int32_t> shared_coords;  // sorted global coordinates touched by >= 2 ranks
+  std::vector<int32_t> shared_local;   // per shared coordinate: local index here, or -1
+};
+ShardPlan make_shard_plan(const std::vector<int32_t>& ksz, const std::vector<int64_t>& off,
+                          const std::vector<int32_t>& seg_ptr, const std::vector<int32_t>& seg_idx, int world,
+                          int rank);
+
+// NCCL via dlopen (nccl_dl.cpp); every call throws Error{SDP_E_NCCL} on failure
+void nccl_unique_id(void* out128);
+void* nccl_comm_init(const void* id128, int world, int rank);
+void nccl_allreduce_sum(void* comm, double* buf, size_t count, cudaStream_t s);
+void nccl_comm_destroy(void* comm);
+
 // ---------------------------------------------------------------- projection buckets
 // Kernel tiers for the batched eigen-projection (kernels_psd.cu).
-enum BucketKind { B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_NUM };
+enum BucketKind { B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_RV8, B_RV16, B_RV32, B_RV64, B_NUM };
+inline bool is_rv(int b) { return b >= B_RV8 && b <= B_RV64; }
 // Size ranges (k <= 8, 16, 32, 64, 96, larger) with fewer than kFewMatrices
 // members use one CTA per matrix so that a small batch still fills the GPU.
 constexpr int64_t kFewMatrices = 2048;
@@ -79,5 +99,9 @@ struct ProjArgs {
 };
 
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
+void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
+int rv_kp(int bucket);
+// stride (kp) of the warm-start V storage of a matrix of order k in tier `bucket`
+inline int store_kp(int bucket, int k) { return is_rv(bucket) ? rv_kp(bucket) : k + (k & 1); }
 
 }  // namespace sdp

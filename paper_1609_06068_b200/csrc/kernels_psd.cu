@@ -19,8 +19,11 @@
 //   GLOBAL         : 256 threads, k <= SDP_MAX_K
 // Odd k is padded with one zero row/column (exact: P_+(diag(X,0)) = diag(P_+(X),0)).
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "internal.h"
+#include "jacobi_rot.cuh"
 
 namespace sdp {
 
@@ -169,8 +172,10 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
   {
     Walk w(g.tid, G, kp);
     for (; w.r < kp; w.next()) {
-      const double v = A[w.r * ld + w.c];
-      fro2 += v * v;
+      if (w.r <= w.c) {
+        const double v = A[w.r * ld + w.c];
+        fro2 += (w.r == w.c ? 1.0 : 2.0) * v * v;
+      }
     }
   }
   fro2 = g.sum(fro2);
@@ -182,9 +187,9 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
     {
       Walk w(g.tid, G, kp);
       for (; w.r < kp; w.next()) {
-        if (w.r != w.c) {
+        if (w.r < w.c) {
           const double v = A[w.r * ld + w.c];
-          off2 += v * v;
+          off2 += 2.0 * v * v;
         }
       }
     }
@@ -200,15 +205,9 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
         }
         q = kp - 2 - i + step;
         q = 1 + (q >= kp - 1 ? q - (kp - 1) : q);
-        const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[p * ld + q];
-        double cs = 1.0, sn = 0.0, t = 0.0;
-        if (apq != 0.0) {
-          const double tau = (aqq - app) / (2.0 * apq);
-          const double at = fabs(tau);
-          t = (at > 1e150) ? 0.5 / tau : copysign(1.0, tau) / (at + sqrt(1.0 + tau * tau));
-          cs = 1.0 / sqrt(1.0 + t * t);
-          sn = t * cs;
-        }
+        const double app = A[p * ld + p], aqq = A[q * ld + q], apq = A[min(p, q) * ld + max(p, q)];
+        const JRot jr = jacobi_rotation(app, aqq, apq);
+        const double cs = jr.c, sn = jr.s, t = 0.0;
         rot.p[i] = p;
         rot.q[i] = q;
         rot.c[i] = cs;
@@ -216,7 +215,9 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
         rot.t[i] = t;
       }
       g.sync();
-      // A <- J^T A J on the 2x2 blocks (i <= j) of the pair partition, mirrored
+      // A <- J^T A J on the 2x2 blocks (i <= j) of the pair partition.  Only the
+      // upper triangle is kept current: every entry is read and written once at
+      // (min, max) of its indices.
       for (int b = g.tid; b < nblk; b += G) {
         int i, j;
         if (rot.blk) {
@@ -227,31 +228,30 @@ __device__ void project_matrix(const Group<G>& g, const int k, const int64_t off
           packed_rc(b, i, j);
         }
         const int p1 = rot.p[i], q1 = rot.q[i];
+        const double c1 = rot.c[i], s1 = rot.s[i];
         if (i == j) {
-          const double apq = A[p1 * ld + q1], t = rot.t[i];
-          A[p1 * ld + p1] -= t * apq;
-          A[q1 * ld + q1] += t * apq;
-          A[p1 * ld + q1] = 0.0;
-          A[q1 * ld + p1] = 0.0;
+          // full J^T B J (the rotation annihilates a_pq only to ~1e-14 relative)
+          const int ipq = min(p1, q1) * ld + max(p1, q1);
+          const double app = A[p1 * ld + p1], aqq = A[q1 * ld + q1], apq = A[ipq];
+          const double r00 = c1 * app - s1 * apq, r01 = c1 * apq - s1 * aqq;
+          const double r10 = s1 * app + c1 * apq, r11 = s1 * apq + c1 * aqq;
+          A[p1 * ld + p1] = c1 * r00 - s1 * r01;
+          A[q1 * ld + q1] = s1 * r10 + c1 * r11;
+          A[ipq] = 0.5 * ((s1 * r00 + c1 * r01) + (c1 * r10 - s1 * r11));
         } else {
           const int p2 = rot.p[j], q2 = rot.q[j];
-          const double c1 = rot.c[i], s1 = rot.s[i], c2 = rot.c[j], s2 = rot.s[j];
-          const double b00 = A[p1 * ld + p2], b01 = A[p1 * ld + q2];
-          const double b10 = A[q1 * ld + p2], b11 = A[q1 * ld + q2];
+          const double c2 = rot.c[j], s2 = rot.s[j];
+          const int i00 = min(p1, p2) * ld + max(p1, p2), i01 = min(p1, q2) * ld + max(p1, q2);
+          const int i10 = min(q1, p2) * ld + max(q1, p2), i11 = min(q1, q2) * ld + max(q1, q2);
+          const double b00 = A[i00], b01 = A[i01], b10 = A[i10], b11 = A[i11];
           // rows: J_i^T B
           const double r00 = c1 * b00 - s1 * b10, r01 = c1 * b01 - s1 * b11;
           const double r10 = s1 * b00 + c1 * b10, r11 = s1 * b01 + c1 * b11;
           // cols: (J_i^T B) J_j
-          const double n00 = c2 * r00 - s2 * r01, n01 = s2 * r00 + c2 * r01;
-          const double n10 = c2 * r10 - s2 * r11, n11 = s2 * r10 + c2 * r11;
-          A[p1 * ld + p2] = n00;
-          A[p2 * ld + p1] = n00;
-          A[p1 * ld + q2] = n01;
-          A[q2 * ld + p1] = n01;
-          A[q1 * ld + p2] = n10;
-          A[p2 * ld + q1] = n10;
-          A[q1 * ld + q2] = n11;
-          A[q2 * ld + q1] = n11;
+          A[i00] = c2 * r00 - s2 * r01;
+          A[i01] = s2 * r00 + c2 * r01;
+          A[i10] = c2 * r10 - s2 * r11;
+          A[i11] = s2 * r10 + c2 * r11;
         }
       }
       // V <- V J  (row r, pair i)
@@ -481,15 +481,34 @@ void init_attrs_mode() {
 }  // namespace
 
 // Opt the large-shared-memory tiers into > 48 KB (per device; call before capture).
+void psd_rv_init_attributes();
 void psd_init_attributes() {
+  psd_rv_init_attributes();
   init_attrs_mode<PM_BATCH>();
   init_attrs_mode<PM_PRIMAL>();
   init_attrs_mode<PM_DUAL>();
 }
 
 // Tier of a matrix of order k when `count` matrices fall in its size range.
+// Default tiers for k <= 64: register-resident V (kernels_psd_rv.cu).
+// SDP_PSD_TIERS=smem selects the shared-memory-V tiers instead (comparison).
+static int use_smem_tiers() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SDP_PSD_TIERS");
+    v = (e && std::string(e) == "smem") ? 1 : 0;
+  }
+  return v;
+}
+
 int bucket_of(int k, int64_t count_in_range) {
   const bool few = count_in_range < kFewMatrices;
+  if (!use_smem_tiers() && k <= 64) {
+    // few mid-size matrices (e.g. 400 cliques of 30): one 128-thread CTA each is
+    // the lower-latency choice; otherwise the register-V tiers
+    if (few && k > 16) return k <= 32 ? B_CTA32 : B_CTA64;
+    return k <= 8 ? B_RV8 : k <= 16 ? B_RV16 : k <= 32 ? B_RV32 : B_RV64;
+  }
   if (k <= 8) return few ? B_CTA32 : B_G8;
   if (k <= 16) return few ? B_CTA32 : B_G16;
   if (k <= 32) return few ? B_CTA32 : B_G32;
@@ -501,6 +520,10 @@ int bucket_of(int k, int64_t count_in_range) {
 int size_range(int k) { return k <= 8 ? 0 : k <= 16 ? 1 : k <= 32 ? 2 : k <= 64 ? 3 : k <= 96 ? 4 : 5; }
 
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s) {
+  if (is_rv(bucket)) {
+    launch_projection_rv(bucket, mode, a, s);
+    return;
+  }
   if (mode == PM_BATCH)
     launch_mode<PM_BATCH>(bucket, a, s);
   else if (mode == PM_PRIMAL)

@@ -68,11 +68,18 @@ __global__ void __launch_bounds__(256) k_scatter(ScatterArgs a) {
           sl += lv;
         }
         const double r1 = (FORM == 0) ? sr - a.c[t] / a.rho : a.c[t] - sr;
-        a.rD[t] = r1 * a.Dinv[t];
-        const double d = sx - a.sprev[t];
-        a.sprev[t] = sx;
-        acc[0] = d * d;
-        acc[1] = sl * sl;
+        const int j = a.shared_idx ? a.shared_idx[t] : -1;
+        if (j >= 0) {  // partial sums of a coordinate shared across ranks
+          a.xbuf[3 * j] = r1;
+          a.xbuf[3 * j + 1] = sx;
+          a.xbuf[3 * j + 2] = sl;
+        } else {
+          a.rD[t] = r1 * a.Dinv[t];
+          const double d = sx - a.sprev[t];
+          a.sprev[t] = sx;
+          acc[0] = d * d;
+          acc[1] = sl * sl;
+        }
       }
     }
   } else {
@@ -94,11 +101,18 @@ __global__ void __launch_bounds__(256) k_scatter(ScatterArgs a) {
       sl = warp_sum(sl);
       if (lane == 0) {
         const double r1 = (FORM == 0) ? sr - a.c[t] / a.rho : a.c[t] - sr;
-        a.rD[t] = r1 * a.Dinv[t];
-        const double d = sx - a.sprev[t];
-        a.sprev[t] = sx;
-        acc[0] = d * d;
-        acc[1] = sl * sl;
+        const int j = a.shared_idx ? a.shared_idx[t] : -1;
+        if (j >= 0) {
+          a.xbuf[3 * j] = r1;
+          a.xbuf[3 * j + 1] = sx;
+          a.xbuf[3 * j + 2] = sl;
+        } else {
+          a.rD[t] = r1 * a.Dinv[t];
+          const double d = sx - a.sprev[t];
+          a.sprev[t] = sx;
+          acc[0] = d * d;
+          acc[1] = sl * sl;
+        }
       }
     }
   }
@@ -160,7 +174,7 @@ __global__ void k_reduce_u(const double* __restrict__ part, int nchunks, int m, 
   if (i >= m) return;
   double s = 0.0;
   for (int c = 0; c < nchunks; ++c) s += part[(int64_t)c * m + i];
-  const double ui = (FORM == 0) ? s - b[i] : s - (-b[i] / rho);
+  const double ui = !b ? s : (FORM == 0) ? s - b[i] : s - (-b[i] / rho);
   if (sdiag) {
     y[i] = ui / sdiag[i];
   } else {
@@ -255,6 +269,76 @@ __global__ void __launch_bounds__(GT_THREADS) k_gemvT_dense(const double* __rest
   if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
 }
 
+// ---------------------------------------------------------------- GEMV^T over the A^T copy
+// x_t = rD_t - Dinv_t * (A^T y)_t with A^T stored row-major (lda x ldm): each
+// warp streams whole rows of A^T (m doubles) with 16-byte evict-first loads
+// issued in batches of TR_U per lane, y comes from L1; deterministic warp
+// reduction.  8 warps x TR_ROWS rows per CTA; one partial per CTA.
+constexpr int TR_ROWS = 2;
+constexpr int TR_U = 16;
+template <int FORM>
+__global__ void __launch_bounds__(256) k_gemvT_rows(const double* __restrict__ AT, int64_t ldm, int m, int N,
+                                                     const double* __restrict__ y, const double* __restrict__ rD,
+                                                     const double* __restrict__ Dinv, const double* __restrict__ c,
+                                                     const double* __restrict__ own, double* __restrict__ x,
+                                                     double* __restrict__ part, const int* done) {
+  if (done && *done) return;
+  __shared__ double sm[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int np = (m + 1) / 2;  // column pairs (ldm even, zero padded)
+  const double2* y2 = reinterpret_cast<const double2*>(y);
+  double acc[1] = {0.0};
+#pragma unroll
+  for (int rr = 0; rr < TR_ROWS; ++rr) {
+    const int64_t t = ((int64_t)blockIdx.x * 8 + warp) * TR_ROWS + rr;
+    if (t >= N) break;
+    const double2* row = reinterpret_cast<const double2*>(AT + t * ldm);
+    double w0 = 0.0, w1 = 0.0;
+    // predicated batches: every load of a batch is issued before any is consumed
+    for (int j0 = lane; j0 < np; j0 += 32 * TR_U) {
+      double2 buf[TR_U];
+#pragma unroll
+      for (int u = 0; u < TR_U; ++u)
+        buf[u] = (j0 + 32 * u < np) ? __ldcs(row + j0 + 32 * u) : make_double2(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < TR_U; ++u) {
+        if (j0 + 32 * u < np) {
+          const double2 yy = __ldg(y2 + j0 + 32 * u);
+          w0 = fma(buf[u].x, yy.x, w0);
+          w1 = fma(buf[u].y, yy.y, w1);
+        }
+      }
+    }
+    const double w = warp_sum(w0 + w1);
+    if (lane == 0) {
+      const double xv = rD[t] - Dinv[t] * w;
+      x[t] = xv;
+      acc[0] += (FORM == 0) ? c[t] * xv : own[t] * (xv / Dinv[t]) * (xv / Dinv[t]);
+    }
+  }
+  block_sum<1, 256>(acc, sm);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
+}
+
+// AT[t][i] = A[i][t] (tiled transpose through shared memory, setup only)
+__global__ void k_transpose(const double* __restrict__ A, int64_t lda, int m, double* __restrict__ AT, int64_t ldm,
+                            int64_t ncols) {
+  __shared__ double tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32;
+  const int r0 = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int r = r0 + k;
+    const int64_t cidx = c0 + threadIdx.x;
+    tile[k][threadIdx.x] = (r < m && cidx < ncols) ? A[(int64_t)r * lda + cidx] : 0.0;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += 8) {
+    const int64_t cidx = c0 + k;
+    const int r = r0 + threadIdx.x;
+    if (cidx < ncols && r < ldm) AT[cidx * ldm + r] = tile[threadIdx.x][k];
+  }
+}
+
 // ---------------------------------------------------------------- sparse A (CSR / CSC)
 template <int FORM>
 __global__ void __launch_bounds__(256) k_gemv_csr(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
@@ -270,7 +354,7 @@ __global__ void __launch_bounds__(256) k_gemv_csr(const int32_t* __restrict__ rp
   for (int e = rp[row] + lane; e < rp[row + 1]; e += 32) s = fma(val[e], v[ci[e]], s);
   s = warp_sum(s);
   if (lane == 0) {
-    const double ui = (FORM == 0) ? s - b[row] : s - (-b[row] / rho);
+    const double ui = !b ? s : (FORM == 0) ? s - b[row] : s - (-b[row] / rho);
     if (sdiag)
       y[row] = ui / sdiag[row];
     else
@@ -282,8 +366,9 @@ template <int FORM>
 __global__ void __launch_bounds__(256) k_gemvT_csc(const int32_t* __restrict__ cp, const int32_t* __restrict__ ri,
                                                     const double* __restrict__ val, int N, const double* __restrict__ y,
                                                     const double* __restrict__ rD, const double* __restrict__ Dinv,
-                                                    const double* __restrict__ c, double* __restrict__ x,
-                                                    double* __restrict__ part, const int* done) {
+                                                    const double* __restrict__ c, const double* __restrict__ own,
+                                                    double* __restrict__ x, double* __restrict__ part,
+                                                    const int* done) {
   if (done && *done) return;
   __shared__ double sm[8];
   const int t = blockIdx.x * 256 + threadIdx.x;
@@ -293,7 +378,7 @@ __global__ void __launch_bounds__(256) k_gemvT_csc(const int32_t* __restrict__ c
     for (int e = cp[t]; e < cp[t + 1]; ++e) w = fma(val[e], y[ri[e]], w);
     const double xv = rD[t] - Dinv[t] * w;
     x[t] = xv;
-    acc[0] = (FORM == 0) ? c[t] * xv : (xv / Dinv[t]) * (xv / Dinv[t]);
+    acc[0] = (FORM == 0) ? c[t] * xv : own[t] * (xv / Dinv[t]) * (xv / Dinv[t]);
   }
   block_sum<1, 256>(acc, sm);
   if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
@@ -330,37 +415,52 @@ __global__ void __launch_bounds__(256) k_update_dual(int64_t stot, const int32_t
 
 // ---------------------------------------------------------------- finalize
 // Single CTA: fixed-order reduction of all partials, residuals (reading G9),
-// objective (G17), history, stop flag.
-template <int FORM>
+// objective (G17), history, stop flag.  PHASE 0: fused (one rank); PHASE 1:
+// reduce the local partials into red[0..5] (to be all-reduced across ranks);
+// PHASE 2: combine the all-reduced red[] on every rank.
+template <int FORM, int PHASE>
 __global__ void __launch_bounds__(256) k_finalize(FinalArgs a) {
   if (*a.done) return;
   __shared__ double sm[8 * 8];
   double v[6] = {0, 0, 0, 0, 0, 0};
-  if (FORM == 0) {
-    for (int i = threadIdx.x; i < a.n_proj; i += 256) {
-      v[0] += a.proj_part[3 * i + 0];
-      v[1] += a.proj_part[3 * i + 1];
-      v[2] += a.proj_part[3 * i + 2];
-    }
-  } else {
-    for (int i = threadIdx.x; i < a.n_upd; i += 256) {
-      v[0] += a.upd_part[3 * i + 0];
-      v[1] += a.upd_part[3 * i + 1];
-      v[2] += a.upd_part[3 * i + 2];
-    }
-  }
-  for (int i = threadIdx.x; i < a.n_scat; i += 256) {
-    v[3] += a.scat_part[2 * i + 0];
-    v[4] += a.scat_part[2 * i + 1];
-  }
-  for (int i = threadIdx.x; i < a.n_gT; i += 256) v[5] += a.gT_part[i];
   double w[1] = {0.0};
+  if (PHASE != 2) {
+    if (FORM == 0) {
+      for (int i = threadIdx.x; i < a.n_proj; i += 256) {
+        v[0] += a.proj_part[3 * i + 0];
+        v[1] += a.proj_part[3 * i + 1];
+        v[2] += a.proj_part[3 * i + 2];
+      }
+    } else {
+      for (int i = threadIdx.x; i < a.n_upd; i += 256) {
+        v[0] += a.upd_part[3 * i + 0];
+        v[1] += a.upd_part[3 * i + 1];
+        v[2] += a.upd_part[3 * i + 2];
+      }
+    }
+    for (int i = threadIdx.x; i < a.n_scat; i += 256) {
+      v[3] += a.scat_part[2 * i + 0];
+      v[4] += a.scat_part[2 * i + 1];
+    }
+    for (int i = threadIdx.x; i < a.n_fix; i += 256) {
+      v[3] += a.fix_part[2 * i + 0];
+      v[4] += a.fix_part[2 * i + 1];
+    }
+    for (int i = threadIdx.x; i < a.n_gT; i += 256) v[5] += a.gT_part[i];
+    block_sum<6, 256>(v, sm);
+    __syncthreads();
+    if (PHASE == 1) {
+      if (threadIdx.x == 0)
+        for (int j = 0; j < 6; ++j) a.red[j] = v[j];
+      return;
+    }
+  }
   if (FORM == 1)
     for (int i = threadIdx.x; i < a.m; i += 256) w[0] += a.b[i] * a.y[i];
-  block_sum<6, 256>(v, sm);
-  __syncthreads();
   block_sum<1, 256>(w, sm + 48);
   if (threadIdx.x == 0) {
+    if (PHASE == 2)
+      for (int j = 0; j < 6; ++j) v[j] = a.red[j];
     const double np = sqrt(v[0]);
     const double den_p = fmax(fmax(sqrt(v[1]), sqrt(v[2])), 1.0);
     const double eps_p = np / den_p;
@@ -390,6 +490,41 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs a) {
     } else if (fmax(eps_p, eps_d) < *a.tol) {
       *a.done = 1;
     }
+  }
+}
+
+// ---------------------------------------------------------------- shared-coordinate fixup
+// After the all-reduce of the scatter partials of coordinates shared across
+// ranks: r1 -> rD, eps_d partials (counted by the owner only), reset buffer.
+__global__ void __launch_bounds__(256) k_shared_fixup(int nshared, const int32_t* __restrict__ shared_local,
+                                                       double* __restrict__ xbuf, const double* __restrict__ Dinv,
+                                                       const double* __restrict__ own, double* __restrict__ rD,
+                                                       double* __restrict__ sprev, double* __restrict__ part,
+                                                       const int* done) {
+  if (done && *done) return;
+  __shared__ double sm[2 * 8];
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  double acc[2] = {0.0, 0.0};
+  if (j < nshared) {
+    const int t = shared_local[j];
+    const double r1 = xbuf[3 * j], sx = xbuf[3 * j + 1], sl = xbuf[3 * j + 2];
+    xbuf[3 * j] = 0.0;
+    xbuf[3 * j + 1] = 0.0;
+    xbuf[3 * j + 2] = 0.0;
+    if (t >= 0) {
+      rD[t] = r1 * Dinv[t];
+      const double d = sx - sprev[t];
+      sprev[t] = sx;
+      if (own[t] != 0.0) {
+        acc[0] = d * d;
+        acc[1] = sl * sl;
+      }
+    }
+  }
+  block_sum<2, 256>(acc, sm);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x + 0] = acc[0];
+    part[2 * blockIdx.x + 1] = acc[1];
   }
 }
 
@@ -445,13 +580,20 @@ __global__ void __launch_bounds__(256) k_syrk_dense(const double* __restrict__ A
     }
 }
 
+// Zero the columns of A whose mask entry is 0 (non-owned coordinates of a rank).
+__global__ void k_mask_cols(double* __restrict__ A, int64_t lda, int m, const double* __restrict__ mask) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= lda || mask[t] != 0.0) return;
+  for (int i = 0; i < m; ++i) A[(int64_t)i * lda + t] = 0.0;
+}
+
 // Column permutation + svec scaling of the user's dense-on-pattern A.
 __global__ void k_place_dense(const double* __restrict__ raw, int64_t npat, int m, const int64_t* __restrict__ map,
                               const double* __restrict__ scale, double* __restrict__ A, int64_t lda) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (e >= npat || i >= m) return;
-  A[(int64_t)i * lda + map[e]] = raw[(int64_t)i * npat + e] * scale[e];
+  if (map[e] >= 0) A[(int64_t)i * lda + map[e]] = raw[(int64_t)i * npat + e] * scale[e];
 }
 
 }  // namespace
@@ -500,6 +642,23 @@ void launch_gemvT_dense(int form, const double* A, int64_t lda, int m, int N, co
     k_gemvT_dense<1><<<grid, GT_THREADS, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
 }
 
+int gemvT_rows_blocks(int64_t N) { return (int)((N + 8 * TR_ROWS - 1) / (8 * TR_ROWS)); }
+
+void launch_gemvT_rows(int form, const double* AT, int64_t ldm, int m, int N, const double* y, const double* rD,
+                       const double* Dinv, const double* c, const double* own, double* x, double* part,
+                       const int* done, cudaStream_t s) {
+  const int grid = gemvT_rows_blocks(N);
+  if (form == 0)
+    k_gemvT_rows<0><<<grid, 256, 0, s>>>(AT, ldm, m, N, y, rD, Dinv, c, own, x, part, done);
+  else
+    k_gemvT_rows<1><<<grid, 256, 0, s>>>(AT, ldm, m, N, y, rD, Dinv, c, own, x, part, done);
+}
+
+void launch_transpose(const double* A, int64_t lda, int m, double* AT, int64_t ldm, int64_t ncols, cudaStream_t s) {
+  dim3 grid((unsigned)((ncols + 31) / 32), (unsigned)((ldm + 31) / 32));
+  k_transpose<<<grid, dim3(32, 8), 0, s>>>(A, lda, m, AT, ldm, ncols);
+}
+
 void launch_gemv_csr(int form, const int32_t* rp, const int32_t* ci, const double* val, int m, const double* v,
                      const double* b, double rho, double* u, const double* sdiag, double* y, const int* done,
                      cudaStream_t s) {
@@ -512,13 +671,13 @@ void launch_gemv_csr(int form, const int32_t* rp, const int32_t* ci, const doubl
 int gemvT_csc_blocks(int N) { return (N + 255) / 256; }
 
 void launch_gemvT_csc(int form, const int32_t* cp, const int32_t* ri, const double* val, int N, const double* y,
-                      const double* rD, const double* Dinv, const double* c, double* x, double* part,
-                      const int* done, cudaStream_t s) {
+                      const double* rD, const double* Dinv, const double* c, const double* own, double* x,
+                      double* part, const int* done, cudaStream_t s) {
   const int grid = gemvT_csc_blocks(N);
   if (form == 0)
-    k_gemvT_csc<0><<<grid, 256, 0, s>>>(cp, ri, val, N, y, rD, Dinv, c, x, part, done);
+    k_gemvT_csc<0><<<grid, 256, 0, s>>>(cp, ri, val, N, y, rD, Dinv, c, own, x, part, done);
   else
-    k_gemvT_csc<1><<<grid, 256, 0, s>>>(cp, ri, val, N, y, rD, Dinv, c, x, part, done);
+    k_gemvT_csc<1><<<grid, 256, 0, s>>>(cp, ri, val, N, y, rD, Dinv, c, own, x, part, done);
 }
 
 int update_blocks(int64_t stot) { return (int)((stot + 255) / 256); }
@@ -529,17 +688,36 @@ void launch_update_dual(int64_t stot, const int32_t* G, const double* x, const d
   k_update_dual<<<update_blocks(stot), 256, 0, s>>>(stot, G, x, z, lam, v, rho, part, done);
 }
 
-void launch_finalize(int form, const FinalArgs& a, cudaStream_t s) {
-  if (form == 0)
-    k_finalize<0><<<1, 256, 0, s>>>(a);
-  else
-    k_finalize<1><<<1, 256, 0, s>>>(a);
+void launch_finalize(int form, int phase, const FinalArgs& a, cudaStream_t s) {
+  if (form == 0) {
+    if (phase == 0) k_finalize<0, 0><<<1, 256, 0, s>>>(a);
+    if (phase == 1) k_finalize<0, 1><<<1, 256, 0, s>>>(a);
+    if (phase == 2) k_finalize<0, 2><<<1, 256, 0, s>>>(a);
+  } else {
+    if (phase == 0) k_finalize<1, 0><<<1, 256, 0, s>>>(a);
+    if (phase == 1) k_finalize<1, 1><<<1, 256, 0, s>>>(a);
+    if (phase == 2) k_finalize<1, 2><<<1, 256, 0, s>>>(a);
+  }
+}
+
+int fixup_blocks(int nshared) { return (nshared + 255) / 256; }
+
+void launch_shared_fixup(int nshared, const int32_t* shared_local, double* xbuf, const double* Dinv,
+                         const double* own, double* rD, double* sprev, double* part, const int* done,
+                         cudaStream_t s) {
+  if (nshared <= 0) return;
+  k_shared_fixup<<<fixup_blocks(nshared), 256, 0, s>>>(nshared, shared_local, xbuf, Dinv, own, rD, sprev, part,
+                                                       done);
 }
 
 void launch_syrk_dense(const double* A, int64_t lda, int m, const double* Dinv, double* S, cudaStream_t s) {
   const int nt = (m + 63) / 64;
   dim3 grid(nt, nt);
   k_syrk_dense<<<grid, 256, 0, s>>>(A, lda, m, Dinv, S);
+}
+
+void launch_mask_cols(double* A, int64_t lda, int m, const double* mask, cudaStream_t s) {
+  k_mask_cols<<<(unsigned)((lda + 255) / 256), 256, 0, s>>>(A, lda, m, mask);
 }
 
 void launch_place_dense(const double* raw, int64_t npat, int m, const int64_t* map, const double* scale, double* A,

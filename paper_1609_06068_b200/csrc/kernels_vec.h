@@ -20,6 +20,8 @@ struct ScatterArgs {
   double* sprev;           // in/out: previous sum_k H_k^T x_k
   double* part;            // out: 2 per block
   const int* done;
+  const int32_t* shared_idx;  // per coordinate: slot in xbuf if shared across ranks, else -1 (NULL: none)
+  double* xbuf;               // 3 doubles per shared coordinate: r1, sum H^T x_k, sum H^T lam_k partials
 };
 
 struct FinalArgs {
@@ -31,6 +33,9 @@ struct FinalArgs {
   int n_scat;
   const double* gT_part;
   int n_gT;
+  const double* fix_part;
+  int n_fix;
+  double* red;        // 6 partial sums (PHASE 1 out, PHASE 2 in)
   const double* b;
   const double* y;
   int m;
@@ -55,18 +60,28 @@ int gemvT_blocks(int64_t lda);
 void launch_gemvT_dense(int form, const double* A, int64_t lda, int m, int N, const double* y, const double* rD,
                         const double* Dinv, const double* c, double* x, double* part, const int* done,
                         cudaStream_t s);
+int gemvT_rows_blocks(int64_t N);
+void launch_gemvT_rows(int form, const double* AT, int64_t ldm, int m, int N, const double* y, const double* rD,
+                       const double* Dinv, const double* c, const double* own, double* x, double* part,
+                       const int* done, cudaStream_t s);
+void launch_transpose(const double* A, int64_t lda, int m, double* AT, int64_t ldm, int64_t ncols, cudaStream_t s);
 void launch_gemv_csr(int form, const int32_t* rp, const int32_t* ci, const double* val, int m, const double* v,
                      const double* b, double rho, double* u, const double* sdiag, double* y, const int* done,
                      cudaStream_t s);
 int gemvT_csc_blocks(int N);
 void launch_gemvT_csc(int form, const int32_t* cp, const int32_t* ri, const double* val, int N, const double* y,
-                      const double* rD, const double* Dinv, const double* c, double* x, double* part,
-                      const int* done, cudaStream_t s);
+                      const double* rD, const double* Dinv, const double* c, const double* own, double* x,
+                      double* part, const int* done, cudaStream_t s);
 int update_blocks(int64_t stot);
 void launch_update_dual(int64_t stot, const int32_t* G, const double* x, const double* z, double* lam, double* v,
                         double rho, double* part, const int* done, cudaStream_t s);
-void launch_finalize(int form, const FinalArgs& a, cudaStream_t s);
+void launch_finalize(int form, int phase, const FinalArgs& a, cudaStream_t s);
+int fixup_blocks(int nshared);
+void launch_shared_fixup(int nshared, const int32_t* shared_local, double* xbuf, const double* Dinv,
+                         const double* own, double* rD, double* sprev, double* part, const int* done,
+                         cudaStream_t s);
 void launch_syrk_dense(const double* A, int64_t lda, int m, const double* Dinv, double* S, cudaStream_t s);
+void launch_mask_cols(double* A, int64_t lda, int m, const double* mask, cudaStream_t s);
 void launch_place_dense(const double* raw, int64_t npat, int m, const int64_t* map, const double* scale, double* A,
                         int64_t lda, cudaStream_t s);
 

@@ -79,3 +79,18 @@ def test_invalid_pattern_rejected():
         lib_mod.chordal_cliques(3, np.array([0]), np.array([5]))
     with pytest.raises(lib_mod.SdpError):
         lib_mod.chordal_cliques(3, np.array([2]), np.array([1]))
+
+
+def test_nccl_unique_id_via_dlopen():
+    """The sharded path resolves NCCL at run time (dlopen libnccl.so.2)."""
+    a = lib_mod.nccl_unique_id()
+    b = lib_mod.nccl_unique_id()
+    assert len(a) == 128 and len(b) == 128 and a != b
+
+
+def test_sharded_setup_option_validation(gen):
+    prob = gen.config(0)
+    with pytest.raises(lib_mod.SdpError, match="nccl_id"):
+        lib_mod.Solver(prob, world=2, rank=0)
+    with pytest.raises(lib_mod.SdpError, match="rank"):
+        lib_mod.Solver(prob, world=2, rank=2, nccl_id=b"\0" * 128)
