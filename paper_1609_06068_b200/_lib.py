@@ -18,6 +18,23 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(
         f"{LIB_PATH} is missing: build it with `python -m paper_1609_06068_b200.build` "
         "(or __graft_entry__.build()); there is no CPU fallback")
+
+def _torch_nccl():
+    """Path of the NCCL bundled with torch (nvidia-nccl wheel), without importing torch."""
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return None
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        p = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(p):
+            return p
+    return None
+
+
+if "SDP_NCCL_LIB" not in os.environ and _torch_nccl():
+    os.environ["SDP_NCCL_LIB"] = _torch_nccl()
 lib = C.CDLL(LIB_PATH)
 
 SDP_OK, SDP_MAX_ITER = 0, 1

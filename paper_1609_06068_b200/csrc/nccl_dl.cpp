@@ -1,9 +1,12 @@
-// NCCL, resolved at run time with dlopen("libnccl.so.2") so that single-GPU use
-// has no NCCL dependency.  In a process that already imported torch the
-// torch-bundled NCCL is the one found (same soname).
+// NCCL, resolved at run time with dlopen so that single-GPU use has no NCCL
+// dependency.  Search order: an NCCL already loaded in the process (torch's,
+// RTLD_NOLOAD), $SDP_NCCL_LIB (the binding points it at torch's bundled copy),
+// then the soname.  Always RTLD_LOCAL: loading the system libnccl globally
+// before torch would make torch bind its newer NCCL symbols to the older one.
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -27,10 +30,13 @@ std::once_flag g_once;
 std::string g_load_error;
 
 void load() {
+  g_nccl.lib = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL | RTLD_NOLOAD);
+  const char* env = getenv("SDP_NCCL_LIB");
+  if (!g_nccl.lib && env && *env) g_nccl.lib = dlopen(env, RTLD_NOW | RTLD_LOCAL);
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
   for (const char* nm : names) {
-    g_nccl.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
     if (g_nccl.lib) break;
+    g_nccl.lib = dlopen(nm, RTLD_NOW | RTLD_LOCAL);
   }
   if (!g_nccl.lib) {
     g_load_error = std::string("dlopen(libnccl.so.2) failed: ") + dlerror();
