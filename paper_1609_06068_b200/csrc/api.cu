@@ -142,8 +142,7 @@ struct sdp_handle_s {
   int32_t* d_ksz = nullptr;
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
-  double* work = nullptr;
-  int work_slots = 0, ld_work = 0;
+  GiantDev gd;
   // A
   int a_dense = 1;
   double* A = nullptr;
@@ -188,8 +187,7 @@ struct sdp_psd_plan_s {
   int32_t* d_ksz = nullptr;
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
-  double* work = nullptr;
-  int work_slots = 0, ld_work = 0;
+  GiantDev gd;
   unsigned long long* capped = nullptr;
   unsigned long long* sweeps = nullptr;
   double *h_in_dev = nullptr, *h_out_dev = nullptr;
@@ -226,30 +224,75 @@ int guarded(F&& f) {
   }
 }
 
+// Giant-tier metadata and workspace (kernels_psd_giant.cu) for the tasks `ids`.
+void build_giant(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<int32_t>& ids, GiantDev& gd) {
+  gd = GiantDev{};
+  const int ng = (int)ids.size();
+  if (!ng) return;
+  std::vector<int32_t> kp(ng), inner(ng + 1, 0), tile(ng + 1, 0), rb(ng + 1, 0), out(ng + 1, 0), full(ng + 1, 0);
+  std::vector<int64_t> wsoff(ng), qoff(ng);
+  int64_t ws = 0, qb = 0, ti = 0;
+  int maxs = 0;
+  for (int g = 0; g < ng; ++g) {
+    const int k = ksz[ids[g]];
+    kp[g] = (k + 31) / 32 * 32;
+    const int64_t P = kp[g] / 32;
+    wsoff[g] = ws;
+    ws += 3 * (int64_t)kp[g] * kp[g];
+    qoff[g] = qb;
+    qb += P * 1024;
+    ti += P * (P + 1) / 2 + P * P;
+    if (ti >= (1ll << 31)) throw Error{SDP_E_INVALID_ARG, "giant tier: too many work items"};
+    inner[g + 1] = inner[g] + (int32_t)P;
+    tile[g + 1] = tile[g] + (int32_t)(P * (P + 1) / 2 + P * P);
+    rb[g + 1] = rb[g] + (int32_t)P;
+    out[g + 1] = out[g] + (int32_t)(P * (P + 1) / 2);
+    full[g + 1] = full[g] + (int32_t)(P * P);
+    maxs = std::max(maxs, (int)(2 * P - 1));
+  }
+  gd.ng = ng;
+  gd.max_steps = maxs;
+  gd.tot_inner = inner[ng];
+  gd.tot_tile = tile[ng];
+  gd.tot_rb = rb[ng];
+  gd.tot_out = out[ng];
+  gd.tot_full = full[ng];
+  gd.task = al.upload(ids);
+  gd.kp = al.upload(kp);
+  gd.wsoff = al.upload(wsoff);
+  gd.qoff = al.upload(qoff);
+  gd.inner_pre = al.upload(inner);
+  gd.tile_pre = al.upload(tile);
+  gd.rb_pre = al.upload(rb);
+  gd.out_pre = al.upload(out);
+  gd.full_pre = al.upload(full);
+  gd.ws = al.get<double>((size_t)ws);
+  gd.qbuf = al.get<double>((size_t)qb);
+  gd.part_fro = al.zeros<double>((size_t)gd.tot_rb);
+  gd.part_off = al.zeros<double>((size_t)gd.tot_out);
+  gd.part_out = al.zeros<double>(3 * (size_t)gd.tot_out);
+  gd.gsweeps = al.zeros<int32_t>((size_t)ng);
+  gd.bar = al.zeros<unsigned>(2);
+  gd.grid = giant_grid();
+  const char* tr = getenv("SDP_GIANT_TRACE");
+  gd.trace = (tr && *tr == '1') ? 1 : 0;
+}
+
 void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_NUM], int bcount[B_NUM],
-                   double*& work, int& slots, int& ld_work, std::vector<int>* bucket_out = nullptr) {
+                   GiantDev& gd, std::vector<int>* bucket_out = nullptr) {
   std::vector<std::vector<int32_t>> lists(B_NUM);
   int64_t in_range[6] = {0, 0, 0, 0, 0, 0};
   for (size_t i = 0; i < ksz.size(); ++i) in_range[size_range(ksz[i])]++;
-  int kg = 0;
   for (size_t i = 0; i < ksz.size(); ++i) {
     const int b = bucket_of(ksz[i], in_range[size_range(ksz[i])]);
     if (bucket_out) bucket_out->push_back(b);
     lists[b].push_back((int32_t)i);
-    if (b == B_GLOBAL) kg = std::max(kg, (int)ksz[i]);
   }
-  // GLOBAL tier: biggest first so the long projections start early
-  std::stable_sort(lists[B_GLOBAL].begin(), lists[B_GLOBAL].end(),
-                   [&](int32_t a, int32_t b) { return ksz[a] > ksz[b]; });
   for (int b = 0; b < B_NUM; ++b) {
     bcount[b] = (int)lists[b].size();
     d_ids[b] = bcount[b] ? al.upload(lists[b]) : nullptr;
   }
-  if (bcount[B_GLOBAL]) {
-    ld_work = kg + (kg & 1);
-    slots = std::min(bcount[B_GLOBAL], 148);
-    work = al.get<double>((size_t)slots * 3 * ld_work * ld_work);
-  }
+  build_giant(al, ksz, lists[B_GLOBAL], gd);
 }
 
 void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
@@ -263,9 +306,7 @@ void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
   a.vk = h->vk;
   a.rho = h->rho;
   a.part = h->proj_part;
-  a.work = h->work;
-  a.work_slots = h->work_slots;
-  a.ld_work = h->ld_work;
+  a.gd = h->gd;
   a.capped = h->capped;
   a.sweeps = h->sweeps;
   a.done = h->done;
@@ -713,7 +754,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->fix_part = al.zeros<double>(2 * (size_t)std::max(1, h->n_fix));
   h->red = al.zeros<double>(8);
   std::vector<int> task_bucket;
-  build_buckets(al, kszl, h->d_ids, h->bcount, h->work, h->work_slots, h->ld_work, &task_bucket);
+  build_buckets(al, kszl, h->d_ids, h->bcount, h->gd, &task_bucket);
 
   // ---- 5. A (svec rows) and S = A D^-1 A^T, factor cached once
   std::vector<double> S;
@@ -1228,7 +1269,7 @@ int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, s
     pl->values = off[count];
     pl->d_off = pl->alloc.upload(off);
     pl->d_ksz = pl->alloc.upload(ksz);
-    build_buckets(pl->alloc, ksz, pl->d_ids, pl->bcount, pl->work, pl->work_slots, pl->ld_work);
+    build_buckets(pl->alloc, ksz, pl->d_ids, pl->bcount, pl->gd);
     pl->capped = pl->alloc.zeros<unsigned long long>(1);
     pl->sweeps = pl->alloc.zeros<unsigned long long>(1);
     psd_init_attributes();
@@ -1253,9 +1294,7 @@ int sdp_project_psd_batch(sdp_psd_plan pl, const double* d_in, double* d_out, vo
     a.ksz = pl->d_ksz;
     a.in = d_in;
     a.out = d_out;
-    a.work = pl->work;
-    a.work_slots = pl->work_slots;
-    a.ld_work = pl->ld_work;
+    a.gd = pl->gd;
     a.capped = pl->capped;
     a.sweeps = pl->sweeps;
     a.done = nullptr;

@@ -69,6 +69,33 @@ int bucket_of(int k, int64_t count_in_range);
 // Projection modes
 enum ProjMode { PM_BATCH = 0, PM_PRIMAL = 1, PM_DUAL = 2 };
 
+// Giant tier (kernels_psd_giant.cu): block-Jacobi over 16-wide blocks, one
+// persistent grid for all matrices of order > the CTA tiers.  Per giant g:
+// kp = k rounded up to 32, P = kp / 32 pair blocks per step, A / V / T are
+// kp x kp row-major at ws + wsoff[g] (+ kp^2, + 2 kp^2), Q (P blocks of 32x32)
+// at qbuf + qoff[g].  *_pre are prefix sums (ng + 1) of the per-giant item
+// counts of each phase.
+struct GiantDev {
+  int ng = 0;
+  int max_steps = 0;                    // max over giants of 2P - 1 (steps per sweep)
+  int tot_inner = 0, tot_tile = 0, tot_rb = 0, tot_out = 0, tot_full = 0;
+  int grid = 0;                         // CTAs of the persistent launch (all co-resident)
+  const int32_t* task = nullptr;        // task id of giant g
+  const int32_t* kp = nullptr;
+  const int64_t* wsoff = nullptr;
+  const int64_t* qoff = nullptr;
+  const int32_t *inner_pre = nullptr, *tile_pre = nullptr, *rb_pre = nullptr, *out_pre = nullptr,
+                *full_pre = nullptr;
+  double* ws = nullptr;
+  double* qbuf = nullptr;
+  double* part_fro = nullptr;           // tot_rb (per 32-column block)
+  double* part_off = nullptr;           // tot_out (per upper 32x32 tile)
+  double* part_out = nullptr;           // 3 * tot_out
+  int32_t* gsweeps = nullptr;           // ng
+  unsigned* bar = nullptr;              // grid barrier {count, generation}
+  int trace = 0;                        // SDP_GIANT_TRACE=1: CTA 0 printf's the per-phase times
+};
+
 struct ProjArgs {
   const int64_t* off;   // per task: offset of its packed values
   const int32_t* ksz;   // per task: order k
@@ -85,9 +112,7 @@ struct ProjArgs {
   const double* vk;     // dual: stacked v_k
   double rho;
   double* part;         // primal: per task 3 partials (|xk-hx|^2, |xk|^2, |hx|^2)
-  double* work;         // global workspace for B_GLOBAL (2 * kmax_even^2 doubles per slot)
-  int32_t work_slots;
-  int32_t ld_work;
+  GiantDev gd;          // B_GLOBAL (giant) tier
   unsigned long long* capped;  // count of sweep-capped projections
   unsigned long long* sweeps;  // total Jacobi sweeps (diagnostics)
   const int32_t* done;  // device stop flag (skip work when set)
@@ -100,8 +125,13 @@ struct ProjArgs {
 
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
+void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s);
+int giant_grid();        // CTAs of the persistent giant kernel on the current device
+int giant_min_order();   // smallest order routed to the giant tier (SDP_GIANT_MIN, default 97)
 int rv_kp(int bucket);
 // stride (kp) of the warm-start V storage of a matrix of order k in tier `bucket`
-inline int store_kp(int bucket, int k) { return is_rv(bucket) ? rv_kp(bucket) : k + (k & 1); }
+inline int store_kp(int bucket, int k) {
+  return is_rv(bucket) ? rv_kp(bucket) : bucket == B_GLOBAL ? (k + 31) / 32 * 32 : k + (k & 1);
+}
 
 }  // namespace sdp

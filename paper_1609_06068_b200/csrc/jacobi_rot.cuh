@@ -25,15 +25,27 @@ __device__ __forceinline__ JRot jacobi_rotation(double app, double aqq, double a
   const double d = aqq - app;
   // power-of-two scale so that max(|d|, |apq|) is in [1, 2)
   const double mx = fmax(fabs(d), fabs(apq));
-  const int e = ilogb(mx);
-  const float df = (float)scalbn(d, -e), af = (float)scalbn(apq, -e);
+  // 2^-e with e = ilogb(mx), from the exponent bits (exact power of two, so
+  // multiplying by it equals scalbn(., -e)); libm ilogb/scalbn only for
+  // subnormal / extreme mx
+  const int ex = ((__double2hiint(mx) >> 20) & 0x7ff) - 1023;
+  double ds, as;
+  if (ex > -1022 && ex < 1022) {
+    const double sc = __hiloint2double((1023 - ex) << 20, 0);
+    ds = d * sc;
+    as = apq * sc;
+  } else {
+    const int e = ilogb(mx);
+    ds = scalbn(d, -e);
+    as = scalbn(apq, -e);
+  }
+  const float df = (float)ds, af = (float)as;
   // fp32 smaller root: t = 2 apq sign(d) / (|d| + sqrt(d^2 + 4 apq^2))
   const float rf = sqrtf(df * df + 4.0f * af * af);
   const float den = fabsf(df) + rf;
   float tf = (df >= 0.0f ? 2.0f : -2.0f) * af / den;
   double t = (double)tf;
   // one fp64 Newton step on g(t) = apq t^2 + d t - apq (scaled coefficients)
-  const double as = scalbn(apq, -e), ds = scalbn(d, -e);
   const double g = fma(fma(as, t, ds), t, -as);
   const float gp = 2.0f * af * tf + df;  // g'(t) in fp32
   if (gp != 0.0f) t -= g * (double)(1.0f / gp);

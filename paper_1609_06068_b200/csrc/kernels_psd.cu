@@ -12,11 +12,11 @@
 //
 // Tiers (chosen per bucket by order k and by how many matrices share it,
 // see bucket assignment in api.cu): a group of G threads owns one matrix whose
-// A and V live in shared memory (GLOBAL: in an L2-resident workspace).
+// A and V live in shared memory.
 //   G8 / G16 / G32 : 8 / 16 / 32 lanes per matrix, k <= 8 / 16 / 32, many matrices
 //   CTA32          : 128 threads per matrix, k <= 32, few matrices (fills the GPU)
 //   CTA64          : 128 threads, k <= 64;  CTA96: 256 threads, k <= 96
-//   GLOBAL         : 256 threads, k <= SDP_MAX_K
+//   GLOBAL (giant) : block Jacobi over the whole grid, k >= SDP_GIANT_MIN (kernels_psd_giant.cu)
 // Odd k is padded with one zero row/column (exact: P_+(diag(X,0)) = diag(P_+(X),0)).
 #include <cmath>
 #include <cstdlib>
@@ -411,29 +411,6 @@ __global__ void __launch_bounds__(G) k_psd_cta(ProjArgs a) {
   }
 }
 
-// --- GLOBAL tier: A, V in a global (L2-resident) workspace slot per CTA -----
-template <int G, int MODE>
-__global__ void __launch_bounds__(G) k_psd_global(ProjArgs a) {
-  if (a.done && *a.done) return;
-  constexpr int PMAX = SDP_MAX_K / 2;
-  __shared__ double rc[PMAX], rs[PMAX], rt[PMAX];
-  __shared__ int rpq[2 * PMAX];
-  __shared__ double red[G / 32];
-  Rot rot{rpq, rpq + PMAX, rc, rs, rt, nullptr};
-  Group<G> g;
-  g.tid = threadIdx.x;
-  g.mask = 0xffffffffu;
-  g.red = red;
-  const int ld = a.ld_work;
-  double* A = a.work + (size_t)blockIdx.x * 3 * ld * ld;
-  double* V = A + (size_t)ld * ld;
-  double* T = MODE == PM_BATCH ? nullptr : V + (size_t)ld * ld;
-  for (int slot = blockIdx.x; slot < a.count; slot += gridDim.x) {
-    const int task = a.ids ? a.ids[slot] : slot;
-    project_matrix<G, MODE>(g, a.ksz[task], a.off[task], task, A, V, T, ld, rot, a);
-  }
-}
-
 template <int MODE>
 void launch_mode(int bucket, const ProjArgs& a, cudaStream_t s) {
   if (a.count <= 0) return;
@@ -456,11 +433,6 @@ void launch_mode(int bucket, const ProjArgs& a, cudaStream_t s) {
     case B_CTA96:
       k_psd_cta<256, 96, MODE><<<a.count, 256, CtaLayout<256, 96, cta_nbuf<96, MODE>()>::bytes(), s>>>(a);
       break;
-    case B_GLOBAL: {
-      const int grid = a.count < a.work_slots ? a.count : a.work_slots;
-      k_psd_global<256, MODE><<<grid, 256, 0, s>>>(a);
-      break;
-    }
   }
 }
 
@@ -502,6 +474,7 @@ static int use_smem_tiers() {
 }
 
 int bucket_of(int k, int64_t count_in_range) {
+  if (k >= giant_min_order()) return B_GLOBAL;
   const bool few = count_in_range < kFewMatrices;
   if (!use_smem_tiers() && k <= 64) {
     // few mid-size matrices (e.g. 400 cliques of 30): one 128-thread CTA each is
@@ -520,6 +493,10 @@ int bucket_of(int k, int64_t count_in_range) {
 int size_range(int k) { return k <= 8 ? 0 : k <= 16 ? 1 : k <= 32 ? 2 : k <= 64 ? 3 : k <= 96 ? 4 : 5; }
 
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s) {
+  if (bucket == B_GLOBAL) {
+    launch_projection_giant(mode, a, s);
+    return;
+  }
   if (is_rv(bucket)) {
     launch_projection_rv(bucket, mode, a, s);
     return;

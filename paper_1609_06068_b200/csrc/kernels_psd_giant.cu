@@ -1,0 +1,692 @@
+// Giant tier of the PSD projection P_k(X) = V max(Lambda, 0) V^T
+// (E:XkUpdate P:244-253, E:zkUpdate P:403-410) for clique blocks / batch
+// matrices of order k > the CTA tiers (SDP_GIANT_MIN, default 97; up to
+// SDP_MAX_K).  Max-cut chordal extensions produce a handful of these (k up to
+// ~650) and they carry > 90 % of the projection flops.
+//
+// Method: the same two-sided cyclic Jacobi as the other tiers (reading G16:
+// stop at off(A)_F <= 1e-15 ||A||_F, cap 30 sweeps; clip at exactly 0, G15),
+// organised as BLOCK Jacobi so that it spreads over the whole GPU and runs on
+// the FP64 tensor pipe:
+//   * A (kp x kp, kp = k rounded up to 32, zero padded: exact, P_+(diag(X,0)) =
+//     diag(P_+(X),0)) is split into nb = kp/16 blocks of 16; a sweep is nb - 1
+//     steps of the round-robin ("circle") ordering over the blocks, each step
+//     pairing the blocks into P = nb/2 disjoint 32-index pairs.
+//   * INNER phase: one warp per (matrix, pair) runs one parallel-ordered Jacobi
+//     sweep (31 steps of 16 rotations, Golub-Van Loan sym.schur2) on the 32x32
+//     diagonal sub-block and accumulates the 32x32 rotation Q.
+//   * TILE phase: one warp per 32x32 tile applies A[P1,P2] <- Q1^T A[P1,P2] Q2
+//     (upper tiles, mirrored) and V[:,P2] <- V[:,P2] Q2, both as DMMA
+//     (mma.sync m8n8k4 f64) products from shared memory.
+//   * OFF phase: off(A)_F per matrix -> per-matrix convergence test.
+//   * Warm start (ADMM modes, E:XkUpdate's input changes slowly): A <- V_prev^T
+//     A V_prev by two DMMA GEMM phases, V = V_prev.
+//   * RECON phase: P_+ = (V diag(max(l,0))) V^T as DMMA tiles, written with the
+//     mode epilogue (primal: lambda_k += rho (x_k - H_k x), E:LambdakUpdate).
+// All phases run in ONE persistent launch (grid = SMs x occupancy, every CTA
+// co-resident), separated by a grid barrier; work items are distributed
+// warp-wise over the whole grid.  Reductions are fixed-order (deterministic).
+#include <cmath>
+#include <cstdlib>
+
+#include "internal.h"
+#include "jacobi_rot.cuh"
+
+namespace sdp {
+
+namespace {
+
+constexpr int NW = 8;            // warps per CTA
+constexpr int NT = NW * 32;
+constexpr int LDS = 36;          // shared row stride (doubles): conflict-free DMMA fragments
+constexpr int TILE = 32 * LDS;
+constexpr int kMaxSweeps = 30;
+constexpr double kJacTol = 1e-15;
+constexpr double kInvSqrt2 = 0.70710678118654752440;
+constexpr double kSqrt2 = 1.41421356237309504880;
+
+struct WarpSmem {
+  double S[TILE];
+  double Q[TILE];
+  double rc[16], rs[16];
+  int rp[16], rq[16];
+};
+constexpr size_t kSmemBytes = NW * sizeof(WarpSmem);
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// acc += op(X) op(Y) over one 32-deep chunk.  X is [m][k] (TX: [k][m]); Y is
+// [k][n] (TY: [n][k]).  Fragment layout of m8n8k4: A(row r4, col c4),
+// B(row c4, col r4), C(row r4, cols 2c4, 2c4+1) with r4 = lane/4, c4 = lane%4.
+template <bool TX, bool TY>
+__device__ __forceinline__ void mma_chunk(double (&acc)[4][4][2], const double* X, const double* Y, int lane) {
+  const int r4 = lane >> 2, c4 = lane & 3;
+#pragma unroll
+  for (int ks = 0; ks < 8; ++ks) {
+    double af[4], bf[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      af[t] = TX ? X[(ks * 4 + c4) * LDS + t * 8 + r4] : X[(t * 8 + r4) * LDS + ks * 4 + c4];
+      bf[t] = TY ? Y[(t * 8 + r4) * LDS + ks * 4 + c4] : Y[(ks * 4 + c4) * LDS + t * 8 + r4];
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+  }
+}
+
+__device__ __forceinline__ void zero_acc(double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+}
+
+__device__ __forceinline__ void store_acc(double* S, const double (&acc)[4][4][2], int lane) {
+  const int r4 = lane >> 2, c4 = lane & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      S[(i * 8 + r4) * LDS + j * 8 + 2 * c4] = acc[i][j][0];
+      S[(i * 8 + r4) * LDS + j * 8 + 2 * c4 + 1] = acc[i][j][1];
+    }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void packed_rc(int e, int& r, int& c) {
+  int cc = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  while ((cc + 1) * (cc + 2) / 2 <= e) ++cc;
+  while (cc * (cc + 1) / 2 > e) --cc;
+  c = cc;
+  r = e - cc * (cc + 1) / 2;
+}
+
+// round-robin ("circle") pairing of n slots: pair i of step s
+__device__ __forceinline__ void circle(int n, int s, int i, int& p, int& q) {
+  p = (i == 0) ? 0 : 1 + (i - 1 + s) % (n - 1);
+  q = 1 + (n - 2 - i + s) % (n - 1);
+}
+// local index l in [0,32) of the block pair (I, J) -> matrix index
+__device__ __forceinline__ int gidx(int I, int J, int l) { return l < 16 ? I * 16 + l : J * 16 + (l - 16); }
+
+// giant g owning work item w of a phase with prefix counts pre[0..ng]
+__device__ __forceinline__ int find_g(const int32_t* __restrict__ pre, int ng, int w) {
+  int lo = 0, hi = ng - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(pre + mid) <= w)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+// Grid-wide barrier (every CTA of the launch is co-resident: grid <= SMs x occupancy).
+__device__ void grid_sync(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned g = *vgen;
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u);
+    if (arrived == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == g) __nanosleep(40);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// per-phase wall time accumulated by CTA 0 / thread 0 (SDP_GIANT_TRACE=1)
+struct PhaseClock {
+  bool on;
+  unsigned long long last, acc[8];
+  int cnt[8];
+  __device__ void init(bool enable) {
+    on = enable && blockIdx.x == 0 && threadIdx.x == 0;
+    for (int i = 0; i < 8; ++i) acc[i] = 0, cnt[i] = 0;
+    if (on) last = gtimer();
+  }
+  __device__ void mark(int ph) {
+    if (!on) return;
+    const unsigned long long t = gtimer();
+    acc[ph] += t - last;
+    cnt[ph]++;
+    last = t;
+  }
+  __device__ void report(int ng, int mode) const {
+    if (!on) return;
+    printf("[giant mode=%d ng=%d] load %.1f | warm %.1f (%d) | off %.1f (%d) | inner %.1f (%d) | tile %.1f (%d) | recon %.1f | fin %.1f us\n",
+           mode, ng, acc[0] * 1e-3, acc[1] * 1e-3, cnt[1], acc[2] * 1e-3, cnt[2], acc[3] * 1e-3, cnt[3], acc[4] * 1e-3,
+           cnt[4], acc[5] * 1e-3, acc[6] * 1e-3);
+  }
+};
+
+// off(A)_F^2 > tol^2 ||A||_F^2 ?  (fixed-order sums: every CTA gets the same answer)
+__device__ __forceinline__ bool giant_active(const GiantDev& d, int g) {
+  double off = 0.0, fro = 0.0;
+  for (int j = d.out_pre[g]; j < d.out_pre[g + 1]; ++j) off += d.part_off[j];
+  for (int j = d.rb_pre[g]; j < d.rb_pre[g + 1]; ++j) fro += d.part_fro[j];
+  return off > kJacTol * kJacTol * fro;
+}
+
+// projection input entry (r <= c < k) of task `task` in the given mode (unscaled X_rc)
+template <int MODE>
+__device__ __forceinline__ double input_entry(const ProjArgs& a, int64_t off, int r, int c) {
+  const int64_t e = off + (int64_t)c * (c + 1) / 2 + r;
+  if constexpr (MODE == PM_BATCH) {
+    return __ldg(a.in + e);
+  } else if constexpr (MODE == PM_PRIMAL) {
+    const double v = __ldg(a.x + __ldg(a.G + e)) - __ldg(a.lam + e) / a.rho;  // H_k x - lambda_k / rho
+    return r == c ? v : v * kInvSqrt2;
+  } else {
+    const double v = __ldg(a.vk + e) - __ldg(a.lam + e) / a.rho;              // v_k - lambda_k / rho
+    return r == c ? v : v * kInvSqrt2;
+  }
+}
+
+__device__ __forceinline__ void cp16(double* sdst, const double* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// Stage a 32x32 tile of M (row-major, stride ld) into S (stride LDS): local rows
+// 0..15 / 16..31 start at matrix rows r0 / r1, local columns 0..15 / 16..31 at
+// c0 / c1 (16-contiguous halves: a pair of blocks, or r1 = r0 + 16 for a natural tile).
+__device__ __forceinline__ void stage_tile(double* S, const double* M, int64_t ld, int r0, int r1, int c0, int c1,
+                                           int lane) {
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int ch = lane + 32 * u;
+    const int i = ch >> 4, jj = (ch & 15) * 2;
+    const int r = i < 16 ? r0 + i : r1 + (i - 16);
+    const int c = jj < 16 ? c0 + jj : c1 + (jj - 16);
+    cp16(S + i * LDS + jj, M + (size_t)r * ld + c);
+  }
+}
+// contiguous row-major 32x32 (a Q block)
+__device__ __forceinline__ void stage_q(double* S, const double* Q, int lane) {
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int ch = lane + 32 * u;
+    const int i = ch >> 4, jj = (ch & 15) * 2;
+    cp16(S + i * LDS + jj, Q + i * 32 + jj);
+  }
+}
+
+constexpr int LDQ = 33;  // inner phase: row-per-lane Q updates are conflict-free at stride 33
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GiantDev& d = a.gd;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int blk[136];  // pair-block table (i << 8 | j), i <= j < 16
+  for (int b = threadIdx.x; b < 136; b += NT) {
+    int i, j;
+    packed_rc(b, i, j);
+    blk[b] = (i << 8) | j;
+  }
+  __syncthreads();
+  WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * NW + (threadIdx.x >> 5);  // global warp
+  const int nwarps = gridDim.x * NW;
+  const bool adm = MODE != PM_BATCH;
+  const bool warm = adm && a.vprev != nullptr && a.warm_period > 0 && (*a.iter % a.warm_period) != 0;
+  PhaseClock clk;
+  clk.init(d.trace != 0);
+
+  // ---------------- LOAD (item = 32-column block cb): the upper entries (r <= c) of its
+  // columns from the packed input (contiguous along the column) and their mirrors, so
+  // every A entry is written once; zero padding; V rows of the block = I or V_prev
+  for (int w = gw; w < d.tot_rb; w += nwarps) {
+    const int g = find_g(d.rb_pre, d.ng, w);
+    const int cb = w - d.rb_pre[g];
+    const int task = d.task[g];
+    const int k = a.ksz[task], kp = d.kp[g];
+    const int64_t off = a.off[task];
+    double* A = d.ws + d.wsoff[g];
+    double* V = A + (size_t)kp * kp;
+    double fro = 0.0;
+    for (int c = cb * 32; c < cb * 32 + 32; ++c) {
+#pragma unroll 4
+      for (int r = lane; r <= c; r += 32) {
+        const double v = c < k ? input_entry<MODE>(a, off, r, c) : 0.0;
+        A[(size_t)c * kp + r] = v;
+        A[(size_t)r * kp + c] = v;
+        fro += (r == c ? 1.0 : 2.0) * v * v;
+      }
+    }
+    if (warm) {
+      const double* Vp = a.vprev + a.voff[task];
+      for (int e = lane; e < 32 * kp; e += 32) V[(size_t)cb * 32 * kp + e] = __ldg(Vp + (size_t)cb * 32 * kp + e);
+    } else {
+      for (int e = lane; e < 32 * kp; e += 32) {
+        const int i = e / kp, c = e - i * kp;
+        V[(size_t)cb * 32 * kp + e] = (cb * 32 + i == c) ? 1.0 : 0.0;
+      }
+    }
+    fro = warp_sum(fro);
+    if (lane == 0) d.part_fro[w] = fro;
+  }
+  grid_sync(d.bar, gridDim.x);
+  clk.mark(0);
+
+  if (warm) {
+    // ---------------- warm start: T = A V_prev, then A = V_prev^T T (+ off-norm partials)
+    for (int w = gw; w < d.tot_full; w += nwarps) {
+      const int g = find_g(d.full_pre, d.ng, w);
+      const int t = w - d.full_pre[g];
+      const int kp = d.kp[g], P = kp >> 5;
+      const int rt = t / P, ct = t - rt * P;
+      double* A = d.ws + d.wsoff[g];
+      const double* V = A + (size_t)kp * kp;
+      double* T = A + 2 * (size_t)kp * kp;
+      double acc[4][4][2];
+      zero_acc(acc);
+      for (int kk = 0; kk < kp; kk += 32) {
+        __syncwarp();
+        stage_tile(sm.S, A, kp, rt * 32, rt * 32 + 16, kk, kk + 16, lane);
+        stage_tile(sm.Q, V, kp, kk, kk + 16, ct * 32, ct * 32 + 16, lane);
+        cp_wait();
+        __syncwarp();
+        mma_chunk<false, false>(acc, sm.S, sm.Q, lane);
+      }
+      __syncwarp();
+      store_acc(sm.S, acc, lane);
+      __syncwarp();
+      for (int e = lane; e < 1024; e += 32) {
+        const int i = e >> 5, j = e & 31;
+        T[(size_t)(rt * 32 + i) * kp + ct * 32 + j] = sm.S[i * LDS + j];
+      }
+    }
+    grid_sync(d.bar, gridDim.x);
+    clk.mark(1);
+    for (int w = gw; w < d.tot_out; w += nwarps) {
+      const int g = find_g(d.out_pre, d.ng, w);
+      int rb, cb;
+      packed_rc(w - d.out_pre[g], rb, cb);
+      const int kp = d.kp[g];
+      double* A = d.ws + d.wsoff[g];
+      const double* V = A + (size_t)kp * kp;
+      const double* T = A + 2 * (size_t)kp * kp;
+      double acc[4][4][2];
+      zero_acc(acc);
+      for (int kk = 0; kk < kp; kk += 32) {
+        __syncwarp();
+        stage_tile(sm.S, V, kp, kk, kk + 16, rb * 32, rb * 32 + 16, lane);  // [k][m]
+        stage_tile(sm.Q, T, kp, kk, kk + 16, cb * 32, cb * 32 + 16, lane);  // [k][n]
+        cp_wait();
+        __syncwarp();
+        mma_chunk<true, false>(acc, sm.S, sm.Q, lane);
+      }
+      __syncwarp();
+      store_acc(sm.S, acc, lane);
+      __syncwarp();
+      double off2 = 0.0;
+      for (int e = lane; e < 1024; e += 32) {
+        const int i = e >> 5, j = e & 31;
+        const double v = rb == cb ? 0.5 * (sm.S[i * LDS + j] + sm.S[j * LDS + i]) : sm.S[i * LDS + j];
+        A[(size_t)(rb * 32 + i) * kp + cb * 32 + j] = v;
+        off2 += rb != cb ? 2.0 * v * v : (i != j ? v * v : 0.0);
+      }
+      if (rb != cb)
+        for (int e = lane; e < 1024; e += 32) {
+          const int j = e >> 5, i = e & 31;
+          A[(size_t)(cb * 32 + j) * kp + rb * 32 + i] = sm.S[i * LDS + j];
+        }
+      off2 = warp_sum(off2);
+      if (lane == 0) d.part_off[w] = off2;
+    }
+  } else {
+    // ---------------- cold: off-norm partials of the loaded A per upper tile
+    for (int w = gw; w < d.tot_out; w += nwarps) {
+      const int g = find_g(d.out_pre, d.ng, w);
+      int rb, cb;
+      packed_rc(w - d.out_pre[g], rb, cb);
+      const int kp = d.kp[g];
+      const double* A = d.ws + d.wsoff[g];
+      __syncwarp();
+      stage_tile(sm.S, A, kp, rb * 32, rb * 32 + 16, cb * 32, cb * 32 + 16, lane);
+      cp_wait();
+      __syncwarp();
+      double off2 = 0.0;
+      for (int e = lane; e < 1024; e += 32) {
+        const int i = e >> 5, j = e & 31;
+        const double v = sm.S[i * LDS + j];
+        off2 += rb != cb ? 2.0 * v * v : (i != j ? v * v : 0.0);
+      }
+      off2 = warp_sum(off2);
+      if (lane == 0) d.part_off[w] = off2;
+    }
+  }
+  grid_sync(d.bar, gridDim.x);
+  clk.mark(2);
+
+  // ---------------- sweeps
+  for (int sweep = 0;; ++sweep) {
+    int any = 0;
+    for (int g = threadIdx.x; g < d.ng; g += NT) any |= giant_active(d, g) ? 1 : 0;
+    any = __syncthreads_or(any);
+    if (!any || sweep == kMaxSweeps) break;
+    if (blockIdx.x == 0)
+      for (int g = threadIdx.x; g < d.ng; g += NT)
+        if (giant_active(d, g)) d.gsweeps[g] = sweep + 1;
+    for (int s = 0; s < d.max_steps; ++s) {
+      // INNER: one Jacobi sweep on the 32x32 diagonal block of every pair -> Q
+      for (int w = gw; w < d.tot_inner; w += nwarps) {
+        const int g = find_g(d.inner_pre, d.ng, w);
+        const int kp = d.kp[g], nb = kp >> 4;
+        if (s >= nb - 1 || !giant_active(d, g)) continue;
+        const int pi = w - d.inner_pre[g];
+        int I, J;
+        circle(nb, s, pi, I, J);
+        const double* A = d.ws + d.wsoff[g];
+        __syncwarp();
+        stage_tile(sm.S, A, kp, I * 16, J * 16, I * 16, J * 16, lane);
+        for (int e = lane; e < 1024; e += 32) {
+          const int i = e >> 5, j = e & 31;
+          sm.Q[i * LDQ + j] = (i == j) ? 1.0 : 0.0;
+        }
+        cp_wait();
+        __syncwarp();
+        for (int t = 0; t < 31; ++t) {
+          if (lane < 16) {
+            int p, q;
+            circle(32, t, lane, p, q);
+            const JRot jr = jacobi_rotation(sm.S[p * LDS + p], sm.S[q * LDS + q], sm.S[min(p, q) * LDS + max(p, q)]);
+            sm.rp[lane] = p;
+            sm.rq[lane] = q;
+            sm.rc[lane] = jr.c;
+            sm.rs[lane] = jr.s;
+          }
+          __syncwarp();
+          // S <- J^T S J on the 2x2 blocks (i <= j) of the pair partition, upper triangle kept
+#pragma unroll
+          for (int u = 0; u < 5; ++u) {
+            const int b = lane + 32 * u;
+            if (b >= 136) break;
+            const int ij = blk[b];
+            const int i = ij >> 8, j = ij & 0xff;
+            const int p1 = sm.rp[i], q1 = sm.rq[i];
+            const double c1 = sm.rc[i], s1 = sm.rs[i];
+            if (i == j) {
+              const int ipq = min(p1, q1) * LDS + max(p1, q1);
+              const double app = sm.S[p1 * LDS + p1], aqq = sm.S[q1 * LDS + q1], apq = sm.S[ipq];
+              const double r00 = c1 * app - s1 * apq, r01 = c1 * apq - s1 * aqq;
+              const double r10 = s1 * app + c1 * apq, r11 = s1 * apq + c1 * aqq;
+              sm.S[p1 * LDS + p1] = c1 * r00 - s1 * r01;
+              sm.S[q1 * LDS + q1] = s1 * r10 + c1 * r11;
+              sm.S[ipq] = 0.5 * ((s1 * r00 + c1 * r01) + (c1 * r10 - s1 * r11));
+            } else {
+              const int p2 = sm.rp[j], q2 = sm.rq[j];
+              const double c2 = sm.rc[j], s2 = sm.rs[j];
+              const int i00 = min(p1, p2) * LDS + max(p1, p2), i01 = min(p1, q2) * LDS + max(p1, q2);
+              const int i10 = min(q1, p2) * LDS + max(q1, p2), i11 = min(q1, q2) * LDS + max(q1, q2);
+              const double b00 = sm.S[i00], b01 = sm.S[i01], b10 = sm.S[i10], b11 = sm.S[i11];
+              const double r00 = c1 * b00 - s1 * b10, r01 = c1 * b01 - s1 * b11;
+              const double r10 = s1 * b00 + c1 * b10, r11 = s1 * b01 + c1 * b11;
+              sm.S[i00] = c2 * r00 - s2 * r01;
+              sm.S[i01] = s2 * r00 + c2 * r01;
+              sm.S[i10] = c2 * r10 - s2 * r11;
+              sm.S[i11] = s2 * r10 + c2 * r11;
+            }
+          }
+          // Q <- Q J (row `lane`)
+          double* Qr = sm.Q + lane * LDQ;
+#pragma unroll 8
+          for (int i = 0; i < 16; ++i) {
+            const int p = sm.rp[i], q = sm.rq[i];
+            const double cs = sm.rc[i], sn = sm.rs[i];
+            const double vp = Qr[p], vq = Qr[q];
+            Qr[p] = cs * vp - sn * vq;
+            Qr[q] = sn * vp + cs * vq;
+          }
+          __syncwarp();
+        }
+        double* Qg = d.qbuf + d.qoff[g] + (size_t)pi * 1024;
+        for (int e = lane; e < 1024; e += 32) Qg[e] = sm.Q[(e >> 5) * LDQ + (e & 31)];
+      }
+      grid_sync(d.bar, gridDim.x);
+      clk.mark(3);
+      // TILE: A[P1,P2] <- Q1^T A[P1,P2] Q2 (upper tiles, mirrored); V[rb, P2] <- V[rb, P2] Q2.
+      // On a matrix's last step of the sweep the A tiles also leave the off-norm partials.
+      for (int w = gw; w < d.tot_tile; w += nwarps) {
+        const int g = find_g(d.tile_pre, d.ng, w);
+        const int kp = d.kp[g], nb = kp >> 4, P = kp >> 5;
+        if (s >= nb - 1 || !giant_active(d, g)) continue;
+        const int t = w - d.tile_pre[g];
+        const int nA = P * (P + 1) / 2;
+        double* A = d.ws + d.wsoff[g];
+        double* V = A + (size_t)kp * kp;
+        const double* Qb = d.qbuf + d.qoff[g];
+        double acc[4][4][2];
+        if (t < nA) {
+          int i1, i2;
+          packed_rc(t, i1, i2);
+          int I1, J1, I2, J2;
+          circle(nb, s, i1, I1, J1);
+          circle(nb, s, i2, I2, J2);
+          __syncwarp();
+          stage_tile(sm.S, A, kp, I1 * 16, J1 * 16, I2 * 16, J2 * 16, lane);
+          stage_q(sm.Q, Qb + (size_t)i2 * 1024, lane);
+          cp_wait();
+          __syncwarp();
+          zero_acc(acc);
+          mma_chunk<false, false>(acc, sm.S, sm.Q, lane);  // M Q2
+          __syncwarp();
+          store_acc(sm.S, acc, lane);
+          stage_q(sm.Q, Qb + (size_t)i1 * 1024, lane);
+          cp_wait();
+          __syncwarp();
+          zero_acc(acc);
+          mma_chunk<true, false>(acc, sm.Q, sm.S, lane);   // Q1^T (M Q2)
+          __syncwarp();
+          store_acc(sm.S, acc, lane);
+          __syncwarp();
+          double off2 = 0.0;
+          for (int e = lane; e < 1024; e += 32) {
+            const int i = e >> 5, j = e & 31;
+            const double v = i1 == i2 ? 0.5 * (sm.S[i * LDS + j] + sm.S[j * LDS + i]) : sm.S[i * LDS + j];
+            A[(size_t)gidx(I1, J1, i) * kp + gidx(I2, J2, j)] = v;
+            off2 += i1 != i2 ? 2.0 * v * v : (i != j ? v * v : 0.0);
+          }
+          if (i1 != i2)
+            for (int e = lane; e < 1024; e += 32) {
+              const int j = e >> 5, i = e & 31;
+              A[(size_t)gidx(I2, J2, j) * kp + gidx(I1, J1, i)] = sm.S[i * LDS + j];
+            }
+          if (s == nb - 2) {
+            off2 = warp_sum(off2);
+            if (lane == 0) d.part_off[d.out_pre[g] + t] = off2;
+          }
+        } else {
+          const int tv = t - nA;
+          const int rb = tv / P, i2 = tv - rb * P;
+          int I2, J2;
+          circle(nb, s, i2, I2, J2);
+          __syncwarp();
+          stage_tile(sm.S, V, kp, rb * 32, rb * 32 + 16, I2 * 16, J2 * 16, lane);
+          stage_q(sm.Q, Qb + (size_t)i2 * 1024, lane);
+          cp_wait();
+          __syncwarp();
+          zero_acc(acc);
+          mma_chunk<false, false>(acc, sm.S, sm.Q, lane);
+          __syncwarp();
+          store_acc(sm.S, acc, lane);
+          __syncwarp();
+          for (int e = lane; e < 1024; e += 32) {
+            const int i = e >> 5, j = e & 31;
+            V[(size_t)(rb * 32 + i) * kp + gidx(I2, J2, j)] = sm.S[i * LDS + j];
+          }
+        }
+      }
+      grid_sync(d.bar, gridDim.x);
+      clk.mark(4);
+    }
+  }
+
+  // ---------------- RECON: P_+ = (V diag(max(l,0))) V^T, mode epilogue; V_prev save
+  const int n_save = (adm && a.vprev) ? d.tot_rb : 0;
+  for (int w = gw; w < d.tot_out + n_save; w += nwarps) {
+    if (w >= d.tot_out) {
+      const int ws_ = w - d.tot_out;
+      const int g = find_g(d.rb_pre, d.ng, ws_);
+      const int rb = ws_ - d.rb_pre[g];
+      const int kp = d.kp[g];
+      const double* V = d.ws + d.wsoff[g] + (size_t)kp * kp;
+      double* Vp = a.vprev + a.voff[d.task[g]];
+      for (int e = lane; e < 32 * kp; e += 32) Vp[(size_t)rb * 32 * kp + e] = V[(size_t)rb * 32 * kp + e];
+      continue;
+    }
+    const int g = find_g(d.out_pre, d.ng, w);
+    int rb, cb;
+    packed_rc(w - d.out_pre[g], rb, cb);
+    const int task = d.task[g];
+    const int k = a.ksz[task], kp = d.kp[g];
+    const int64_t off = a.off[task];
+    const double* A = d.ws + d.wsoff[g];
+    const double* V = A + (size_t)kp * kp;
+    double acc[4][4][2];
+    zero_acc(acc);
+    for (int kk = 0; kk < k; kk += 32) {
+      __syncwarp();
+      stage_tile(sm.S, V, kp, rb * 32, rb * 32 + 16, kk, kk + 16, lane);  // [m][k]
+      stage_tile(sm.Q, V, kp, cb * 32, cb * 32 + 16, kk, kk + 16, lane);  // [n][k]
+      const double l = A[(size_t)(kk + lane) * (kp + 1)];
+      const double lp = l > 0.0 ? l : 0.0;
+      cp_wait();
+      __syncwarp();
+      for (int i = 0; i < 32; ++i) sm.S[i * LDS + lane] *= lp;
+      __syncwarp();
+      mma_chunk<false, true>(acc, sm.S, sm.Q, lane);
+    }
+    __syncwarp();
+    store_acc(sm.S, acc, lane);
+    __syncwarp();
+    double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+    for (int e = lane; e < 1024; e += 32) {
+      // column-major walk of the tile so that consecutive lanes write consecutive packed entries
+      const int j = e >> 5, i = e & 31;
+      const int r = rb * 32 + i, c = cb * 32 + j;
+      if (r > c || c >= k) continue;
+      const double v = sm.S[i * LDS + j];
+      const int64_t pe = off + (int64_t)c * (c + 1) / 2 + r;
+      if constexpr (MODE == PM_BATCH) {
+        a.out[pe] = v;
+      } else if constexpr (MODE == PM_PRIMAL) {
+        const double xkv = (r == c) ? v : v * kSqrt2;
+        const double hx = __ldg(a.x + a.G[pe]);
+        const double dd = xkv - hx;
+        a.xk[pe] = xkv;
+        a.lam[pe] = a.lam[pe] + a.rho * dd;  // E:LambdakUpdate
+        p0 += dd * dd;
+        p1 += xkv * xkv;
+        p2 += hx * hx;
+      } else {
+        a.xk[pe] = (r == c) ? v : v * kSqrt2;
+      }
+    }
+    if constexpr (MODE == PM_PRIMAL) {
+      p0 = warp_sum(p0);
+      p1 = warp_sum(p1);
+      p2 = warp_sum(p2);
+      if (lane == 0) {
+        d.part_out[3 * (size_t)w + 0] = p0;
+        d.part_out[3 * (size_t)w + 1] = p1;
+        d.part_out[3 * (size_t)w + 2] = p2;
+      }
+    }
+  }
+  grid_sync(d.bar, gridDim.x);
+  clk.mark(5);
+  // ---------------- FIN: per-matrix partials (fixed order), sweep / cap counters
+  for (int g = blockIdx.x * NT + threadIdx.x; g < d.ng; g += gridDim.x * NT) {
+    const int task = d.task[g];
+    if constexpr (MODE == PM_PRIMAL) {
+      double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+      for (int t = d.out_pre[g]; t < d.out_pre[g + 1]; ++t) {
+        p0 += d.part_out[3 * (size_t)t + 0];
+        p1 += d.part_out[3 * (size_t)t + 1];
+        p2 += d.part_out[3 * (size_t)t + 2];
+      }
+      a.part[3 * (int64_t)task + 0] = p0;
+      a.part[3 * (int64_t)task + 1] = p1;
+      a.part[3 * (int64_t)task + 2] = p2;
+    }
+    if (a.sweeps) atomicAdd(a.sweeps, (unsigned long long)d.gsweeps[g]);
+    if (a.capped && giant_active(d, g)) atomicAdd(a.capped, 1ull);
+    d.gsweeps[g] = 0;
+  }
+  clk.mark(6);
+  clk.report(d.ng, MODE);
+}
+
+template <int MODE>
+void launch_mode(const ProjArgs& a, cudaStream_t s) {
+  k_psd_giant<MODE><<<a.gd.grid, NT, kSmemBytes, s>>>(a);
+}
+
+}  // namespace
+
+int giant_min_order() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("SDP_GIANT_MIN");
+    v = e ? atoi(e) : 97;
+    if (v < 33) v = 33;
+    if (v > 97) v = 97;  // the CTA tiers stop at 96
+  }
+  return v;
+}
+
+int giant_grid() {
+  int dev = 0, sms = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(k_psd_giant<PM_BATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  cudaFuncSetAttribute(k_psd_giant<PM_PRIMAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  cudaFuncSetAttribute(k_psd_giant<PM_DUAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+  int o1 = 0, o2 = 0, o3 = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_psd_giant<PM_BATCH>, NT, kSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_psd_giant<PM_PRIMAL>, NT, kSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o3, k_psd_giant<PM_DUAL>, NT, kSmemBytes);
+  occ = std::min(o1, std::min(o2, o3));
+  if (occ < 1) occ = 1;
+  return sms * occ;
+}
+
+void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s) {
+  if (a.gd.ng <= 0) return;
+  if (mode == PM_BATCH)
+    launch_mode<PM_BATCH>(a, s);
+  else if (mode == PM_PRIMAL)
+    launch_mode<PM_PRIMAL>(a, s);
+  else
+    launch_mode<PM_DUAL>(a, s);
+}
+
+}  // namespace sdp

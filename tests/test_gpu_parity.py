@@ -7,6 +7,8 @@ same seeded inputs.  Bars (BASELINE.json north_star):
   * batched P_+: ||P_gpu - P_oracle||_F <= 1e-11 ||X||_F per matrix (Jacobi
     stops at off(A) <= 1e-15 ||A||_F; P_+ is 1-Lipschitz).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -15,6 +17,7 @@ from oracle import decompose as dc
 from oracle import psd as opsd
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def rel(g, o):
@@ -310,3 +313,54 @@ def test_cfg3_full_size_iterations(lib, gen):
         assert s.info()["s_diagonal"] == 1
         compare_state(dec, st, s, form)
         s.close()
+
+
+# ------------------------------------------------------------------ giant (block-Jacobi) tier
+
+def test_giant_tier_iterates_warm_restarts(lib, gen):
+    """Max-cut on ER(700, 4/n): cliques up to ~150 go to the giant tier
+    (block Jacobi + DMMA); 70 iterations cross a cold restart of the warm start."""
+    prob = gen.maxcut_er(700, 21)
+    dec = dc.decompose(prob)
+    assert max(len(c) for c in dec.cliques) >= 97
+    for form, rho in (("primal", 0.1), ("dual", 10.0)):
+        st = admm.step(dec, admm.zero_state(dec), rho, form, 70)
+        s = lib.Solver(prob, form=form, rho=rho)
+        s.step(70)
+        compare_state(dec, st, s, form)
+        assert s.info()["jacobi_capped"] == 0
+        s.close()
+
+
+def test_giant_tier_determinism(lib, gen):
+    prob = gen.maxcut_er(700, 21)
+    s = lib.Solver(prob, form="primal", rho=0.1)
+    s.step(12)
+    a = (s.x(), s.blocks("xk"), s.blocks("lambda"))
+    s.reset()
+    s.step(12)
+    b = (s.x(), s.blocks("xk"), s.blocks("lambda"))
+    for u, v in zip(a, b):
+        assert np.array_equal(u, v)
+    s.close()
+
+
+def test_giant_tier_small_orders_subprocess(tmp_path):
+    """SDP_GIANT_MIN=33 routes every order 33..100 through the giant tier
+    (padding 33 -> 64 etc.); batch results still match the oracle."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L\n"
+        "from oracle import psd as opsd\n"
+        "rng = np.random.default_rng(5)\n"
+        "ks = np.array(list(range(30, 101)), np.int32); rng.shuffle(ks)\n"
+        "vals = np.concatenate([rng.standard_normal(k*(k+1)//2) for k in ks])\n"
+        "p = L.PsdPlan(ks); out = p.project_host(vals)\n"
+        "want = opsd.project_psd_packed_batch(ks, vals)\n"
+        "e = np.linalg.norm(out - want) / np.linalg.norm(want)\n"
+        "print(e); assert e <= 1e-12, e\n" % ROOT)
+    env = dict(os.environ, SDP_GIANT_MIN="33")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
