@@ -143,6 +143,7 @@ struct sdp_handle_s {
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
   GiantDev gd;
+  TrdDev td[2];  // B_TRD32, B_TRD64
   // A
   int a_dense = 1;
   double* A = nullptr;
@@ -188,6 +189,7 @@ struct sdp_psd_plan_s {
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
   GiantDev gd;
+  TrdDev td[2];
   unsigned long long* capped = nullptr;
   unsigned long long* sweeps = nullptr;
   double *h_in_dev = nullptr, *h_out_dev = nullptr;
@@ -272,14 +274,50 @@ void build_giant(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<i
   gd.part_off = al.zeros<double>((size_t)gd.tot_out);
   gd.part_out = al.zeros<double>(3 * (size_t)gd.tot_out);
   gd.gsweeps = al.zeros<int32_t>((size_t)ng);
+  gd.gflag = al.zeros<int32_t>((size_t)ng);
   gd.bar = al.zeros<unsigned>(2);
   gd.grid = giant_grid();
   const char* tr = getenv("SDP_GIANT_TRACE");
-  gd.trace = (tr && *tr == '1') ? 1 : 0;
+  gd.trace = tr ? atoi(tr) : 0;
+}
+
+// Tridiagonal-QL tier workspace (kernels_psd_trd.cu) for the tasks `ids` of storage order kp,
+// processed in chunks so that the workspace stays under SDP_TRD_BUDGET_MB (default 2048).
+void build_trd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<int32_t>& ids, int kp, TrdDev& td) {
+  td = TrdDev{};
+  const int n = (int)ids.size();
+  if (!n) return;
+  const char* bud = getenv("SDP_TRD_BUDGET_MB");
+  const int64_t budget = (bud ? std::max(16ll, atoll(bud)) : 2048ll) << 20;
+  const int64_t per = 8 * trd_hsize(kp, kp) + (int64_t)(sizeof(double2) + sizeof(int16_t)) * trd_rot_cap(kp);
+  const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(n, budget / per));
+  std::vector<int64_t> hoff(n), roff(n);
+  std::vector<int32_t> rcap(n);
+  int64_t hmax = 0, rmax = 0, h = 0, r = 0;
+  for (int i = 0; i < n; ++i) {
+    if (i % chunk == 0) h = r = 0;
+    const int k = ksz[ids[i]];
+    hoff[i] = h;
+    roff[i] = r;
+    rcap[i] = (int32_t)trd_rot_cap(k);
+    h += trd_hsize(kp, k);
+    r += rcap[i];
+    hmax = std::max(hmax, h);
+    rmax = std::max(rmax, r);
+  }
+  td.count = n;
+  td.chunk = chunk;
+  td.hoff = al.upload(hoff);
+  td.roff = al.upload(roff);
+  td.rcap = al.upload(rcap);
+  td.hbuf = al.get<double>((size_t)hmax);
+  td.rot = al.get<double2>((size_t)rmax);
+  td.ridx = al.get<int16_t>((size_t)rmax);
+  td.rcount = al.zeros<int32_t>((size_t)n);
 }
 
 void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_NUM], int bcount[B_NUM],
-                   GiantDev& gd, std::vector<int>* bucket_out = nullptr) {
+                   GiantDev& gd, TrdDev td[2], std::vector<int>* bucket_out = nullptr) {
   std::vector<std::vector<int32_t>> lists(B_NUM);
   int64_t in_range[6] = {0, 0, 0, 0, 0, 0};
   for (size_t i = 0; i < ksz.size(); ++i) in_range[size_range(ksz[i])]++;
@@ -293,6 +331,8 @@ void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_
     d_ids[b] = bcount[b] ? al.upload(lists[b]) : nullptr;
   }
   build_giant(al, ksz, lists[B_GLOBAL], gd);
+  build_trd(al, ksz, lists[B_TRD32], 32, td[0]);
+  build_trd(al, ksz, lists[B_TRD64], 64, td[1]);
 }
 
 void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
@@ -319,6 +359,7 @@ void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
     if (!h->bcount[b]) continue;
     a.ids = h->d_ids[b];
     a.count = h->bcount[b];
+    if (is_trd(b)) a.td = h->td[b - B_TRD32];
     launch_projection(b, mode, a, s);
   }
 }
@@ -467,7 +508,15 @@ void enqueue_iteration(sdp_handle h, cudaStream_t s) {
 
 int launches_per_iter(sdp_handle h) {
   int n = 0;
-  for (int b = 0; b < B_NUM; ++b) n += h->bcount[b] ? 1 : 0;  // one projection launch per non-empty tier
+  for (int b = 0; b < B_NUM; ++b) {  // one launch per non-empty tier; 3 per chunk for the QL tiers
+    if (!h->bcount[b]) continue;
+    if (is_trd(b)) {
+      const TrdDev& t = h->td[b - B_TRD32];
+      n += 3 * ((t.count + t.chunk - 1) / t.chunk);
+    } else {
+      n += 1;
+    }
+  }
   n += 1;                                       // scatter
   n += h->a_dense ? 3 : 2;                      // gemv (+ reduce) + gemvT
   n += h->s_diag ? 0 : 2;                       // triangular solves
@@ -754,7 +803,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->fix_part = al.zeros<double>(2 * (size_t)std::max(1, h->n_fix));
   h->red = al.zeros<double>(8);
   std::vector<int> task_bucket;
-  build_buckets(al, kszl, h->d_ids, h->bcount, h->gd, &task_bucket);
+  build_buckets(al, kszl, h->d_ids, h->bcount, h->gd, h->td, &task_bucket);
 
   // ---- 5. A (svec rows) and S = A D^-1 A^T, factor cached once
   std::vector<double> S;
@@ -1269,7 +1318,7 @@ int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, s
     pl->values = off[count];
     pl->d_off = pl->alloc.upload(off);
     pl->d_ksz = pl->alloc.upload(ksz);
-    build_buckets(pl->alloc, ksz, pl->d_ids, pl->bcount, pl->gd);
+    build_buckets(pl->alloc, ksz, pl->d_ids, pl->bcount, pl->gd, pl->td);
     pl->capped = pl->alloc.zeros<unsigned long long>(1);
     pl->sweeps = pl->alloc.zeros<unsigned long long>(1);
     psd_init_attributes();
@@ -1302,6 +1351,7 @@ int sdp_project_psd_batch(sdp_psd_plan pl, const double* d_in, double* d_out, vo
       if (!pl->bcount[b]) continue;
       a.ids = pl->d_ids[b];
       a.count = pl->bcount[b];
+      if (is_trd(b)) a.td = pl->td[b - B_TRD32];
       launch_projection(b, PM_BATCH, a, s);
     }
     SDP_CUDA_TRY(cudaGetLastError());

@@ -58,8 +58,12 @@ void nccl_comm_destroy(void* comm);
 
 // ---------------------------------------------------------------- projection buckets
 // Kernel tiers for the batched eigen-projection (kernels_psd.cu).
-enum BucketKind { B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_RV8, B_RV16, B_RV32, B_RV64, B_NUM };
+enum BucketKind {
+  B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_RV8, B_RV16, B_RV32, B_RV64, B_TRD32, B_TRD64, B_NUM
+};
 inline bool is_rv(int b) { return b >= B_RV8 && b <= B_RV64; }
+inline bool is_trd(int b) { return b == B_TRD32 || b == B_TRD64; }
+inline int trd_kp(int b) { return b == B_TRD32 ? 32 : 64; }
 // Size ranges (k <= 8, 16, 32, 64, 96, larger) with fewer than kFewMatrices
 // members use one CTA per matrix so that a small batch still fills the GPU.
 constexpr int64_t kFewMatrices = 2048;
@@ -92,8 +96,26 @@ struct GiantDev {
   double* part_off = nullptr;           // tot_out (per upper 32x32 tile)
   double* part_out = nullptr;           // 3 * tot_out
   int32_t* gsweeps = nullptr;           // ng
+  int32_t* gflag = nullptr;             // ng: active in the current sweep
   unsigned* bar = nullptr;              // grid barrier {count, generation}
   int trace = 0;                        // SDP_GIANT_TRACE=1: CTA 0 printf's the per-phase times
+};
+
+// Tridiagonal-QL tiers (kernels_psd_trd.cu), per bucket.  Slots = positions in
+// the bucket list; processed in chunks of `chunk` slots whose workspace
+// offsets (hoff: doubles into hbuf, roff: rotations into rot / ridx) are
+// relative to the chunk's first slot.  Per slot hbuf holds d, e, tau, lambda
+// (KP each) followed by the packed Householder vectors.
+struct TrdDev {
+  int count = 0;
+  int chunk = 0;
+  const int64_t* hoff = nullptr;
+  const int64_t* roff = nullptr;
+  const int32_t* rcap = nullptr;
+  double* hbuf = nullptr;
+  double2* rot = nullptr;
+  int16_t* ridx = nullptr;
+  int32_t* rcount = nullptr;  // per slot (chunk-relative): rotations stored, -1 = QL fell back
 };
 
 struct ProjArgs {
@@ -113,6 +135,7 @@ struct ProjArgs {
   double rho;
   double* part;         // primal: per task 3 partials (|xk-hx|^2, |xk|^2, |hx|^2)
   GiantDev gd;          // B_GLOBAL (giant) tier
+  TrdDev td;            // tridiagonal-QL tier being launched
   unsigned long long* capped;  // count of sweep-capped projections
   unsigned long long* sweeps;  // total Jacobi sweeps (diagnostics)
   const int32_t* done;  // device stop flag (skip work when set)
@@ -126,12 +149,15 @@ struct ProjArgs {
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s);
+void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
+int64_t trd_rot_cap(int k);      // rotation-list capacity of one matrix of order k
+int64_t trd_hsize(int kp, int k);  // doubles of per-slot Householder workspace
 int giant_grid();        // CTAs of the persistent giant kernel on the current device
 int giant_min_order();   // smallest order routed to the giant tier (SDP_GIANT_MIN, default 97)
 int rv_kp(int bucket);
 // stride (kp) of the warm-start V storage of a matrix of order k in tier `bucket`
 inline int store_kp(int bucket, int k) {
-  return is_rv(bucket) ? rv_kp(bucket) : bucket == B_GLOBAL ? (k + 31) / 32 * 32 : k + (k & 1);
+  return is_trd(bucket) ? 0 : is_rv(bucket) ? rv_kp(bucket) : bucket == B_GLOBAL ? (k + 31) / 32 * 32 : k + (k & 1);
 }
 
 }  // namespace sdp

@@ -454,28 +454,39 @@ void init_attrs_mode() {
 
 // Opt the large-shared-memory tiers into > 48 KB (per device; call before capture).
 void psd_rv_init_attributes();
+void psd_trd_init_attributes();
 void psd_init_attributes() {
   psd_rv_init_attributes();
+  psd_trd_init_attributes();
   init_attrs_mode<PM_BATCH>();
   init_attrs_mode<PM_PRIMAL>();
   init_attrs_mode<PM_DUAL>();
 }
 
 // Tier of a matrix of order k when `count` matrices fall in its size range.
-// Default tiers for k <= 64: register-resident V (kernels_psd_rv.cu).
-// SDP_PSD_TIERS=smem selects the shared-memory-V tiers instead (comparison).
-static int use_smem_tiers() {
+// Default tiers: k <= 16 register-resident-V Jacobi (kernels_psd_rv.cu),
+// 16 < k <= 64 tridiagonal-QL (kernels_psd_trd.cu).  SDP_PSD_TIERS=jacobi keeps
+// Jacobi for k <= 64; SDP_PSD_TIERS=smem selects the shared-memory-V Jacobi
+// tiers; SDP_PSD_TIERS=trd uses tridiagonal-QL for every 16 < k <= 64 (tests,
+// comparisons).
+static int tier_mode() {  // 0 default, 1 smem Jacobi, 2 Jacobi (register V), 3 QL for every 16 < k <= 64
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("SDP_PSD_TIERS");
-    v = (e && std::string(e) == "smem") ? 1 : 0;
+    const std::string t = e ? e : "";
+    v = t == "smem" ? 1 : t == "jacobi" ? 2 : t == "trd" ? 3 : 0;
   }
   return v;
 }
+static int use_smem_tiers() { return tier_mode() == 1; }
 
 int bucket_of(int k, int64_t count_in_range) {
   if (k >= giant_min_order()) return B_GLOBAL;
   const bool few = count_in_range < kFewMatrices;
+  // many mid-size matrices: tridiagonal-QL (throughput); a few (e.g. 400 cliques of
+  // 30): one CTA each with warm-started Jacobi is the lower-latency choice
+  if (k > 16 && k <= 64 && (tier_mode() == 3 || (tier_mode() == 0 && count_in_range >= kFewMatrices)))
+    return k <= 32 ? B_TRD32 : B_TRD64;
   if (!use_smem_tiers() && k <= 64) {
     // few mid-size matrices (e.g. 400 cliques of 30): one 128-thread CTA each is
     // the lower-latency choice; otherwise the register-V tiers
@@ -495,6 +506,10 @@ int size_range(int k) { return k <= 8 ? 0 : k <= 16 ? 1 : k <= 32 ? 2 : k <= 64 
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s) {
   if (bucket == B_GLOBAL) {
     launch_projection_giant(mode, a, s);
+    return;
+  }
+  if (is_trd(bucket)) {
+    launch_projection_trd(bucket, mode, a, s);
     return;
   }
   if (is_rv(bucket)) {

@@ -184,10 +184,12 @@ struct PhaseClock {
 };
 
 // off(A)_F^2 > tol^2 ||A||_F^2 ?  (fixed-order sums: every CTA gets the same answer)
+// Data written by other CTAs during this launch is read with ld.global.cg (L2,
+// bypassing L1, which is not coherent across SMs): partials, sweep counters, A, V.
 __device__ __forceinline__ bool giant_active(const GiantDev& d, int g) {
   double off = 0.0, fro = 0.0;
-  for (int j = d.out_pre[g]; j < d.out_pre[g + 1]; ++j) off += d.part_off[j];
-  for (int j = d.rb_pre[g]; j < d.rb_pre[g + 1]; ++j) fro += d.part_fro[j];
+  for (int j = d.out_pre[g]; j < d.out_pre[g + 1]; ++j) off += __ldcg(d.part_off + j);
+  for (int j = d.rb_pre[g]; j < d.rb_pre[g + 1]; ++j) fro += __ldcg(d.part_fro + j);
   return off > kJacTol * kJacTol * fro;
 }
 
@@ -391,16 +393,23 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
     int any = 0;
     for (int g = threadIdx.x; g < d.ng; g += NT) any |= giant_active(d, g) ? 1 : 0;
     any = __syncthreads_or(any);
-    if (!any || sweep == kMaxSweeps) break;
+    if (!any || sweep == kMaxSweeps) {
+      if (d.trace && blockIdx.x == 0 && threadIdx.x == 0) printf("[giant] sweeps=%d any_active=%d\n", sweep, any);
+      break;
+    }
     if (blockIdx.x == 0)
-      for (int g = threadIdx.x; g < d.ng; g += NT)
-        if (giant_active(d, g)) d.gsweeps[g] = sweep + 1;
+      for (int g = threadIdx.x; g < d.ng; g += NT) {
+        const int act = giant_active(d, g) ? 1 : 0;
+        d.gflag[g] = act;
+        if (act) d.gsweeps[g] = sweep + 1;
+      }
+    grid_sync(d.bar, gridDim.x);
     for (int s = 0; s < d.max_steps; ++s) {
       // INNER: one Jacobi sweep on the 32x32 diagonal block of every pair -> Q
       for (int w = gw; w < d.tot_inner; w += nwarps) {
         const int g = find_g(d.inner_pre, d.ng, w);
         const int kp = d.kp[g], nb = kp >> 4;
-        if (s >= nb - 1 || !giant_active(d, g)) continue;
+        if (s >= nb - 1 || !__ldcg(d.gflag + g)) continue;
         const int pi = w - d.inner_pre[g];
         int I, J;
         circle(nb, s, pi, I, J);
@@ -477,7 +486,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
       for (int w = gw; w < d.tot_tile; w += nwarps) {
         const int g = find_g(d.tile_pre, d.ng, w);
         const int kp = d.kp[g], nb = kp >> 4, P = kp >> 5;
-        if (s >= nb - 1 || !giant_active(d, g)) continue;
+        if (s >= nb - 1 || !__ldcg(d.gflag + g)) continue;
         const int t = w - d.tile_pre[g];
         const int nA = P * (P + 1) / 2;
         double* A = d.ws + d.wsoff[g];
@@ -559,7 +568,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
       const int kp = d.kp[g];
       const double* V = d.ws + d.wsoff[g] + (size_t)kp * kp;
       double* Vp = a.vprev + a.voff[d.task[g]];
-      for (int e = lane; e < 32 * kp; e += 32) Vp[(size_t)rb * 32 * kp + e] = V[(size_t)rb * 32 * kp + e];
+      for (int e = lane; e < 32 * kp; e += 32) Vp[(size_t)rb * 32 * kp + e] = __ldcg(V + (size_t)rb * 32 * kp + e);
       continue;
     }
     const int g = find_g(d.out_pre, d.ng, w);
@@ -576,7 +585,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
       __syncwarp();
       stage_tile(sm.S, V, kp, rb * 32, rb * 32 + 16, kk, kk + 16, lane);  // [m][k]
       stage_tile(sm.Q, V, kp, cb * 32, cb * 32 + 16, kk, kk + 16, lane);  // [n][k]
-      const double l = A[(size_t)(kk + lane) * (kp + 1)];
+      const double l = __ldcg(A + (size_t)(kk + lane) * (kp + 1));
       const double lp = l > 0.0 ? l : 0.0;
       cp_wait();
       __syncwarp();
@@ -629,20 +638,28 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
     if constexpr (MODE == PM_PRIMAL) {
       double p0 = 0.0, p1 = 0.0, p2 = 0.0;
       for (int t = d.out_pre[g]; t < d.out_pre[g + 1]; ++t) {
-        p0 += d.part_out[3 * (size_t)t + 0];
-        p1 += d.part_out[3 * (size_t)t + 1];
-        p2 += d.part_out[3 * (size_t)t + 2];
+        p0 += __ldcg(d.part_out + 3 * (size_t)t + 0);
+        p1 += __ldcg(d.part_out + 3 * (size_t)t + 1);
+        p2 += __ldcg(d.part_out + 3 * (size_t)t + 2);
       }
       a.part[3 * (int64_t)task + 0] = p0;
       a.part[3 * (int64_t)task + 1] = p1;
       a.part[3 * (int64_t)task + 2] = p2;
     }
-    if (a.sweeps) atomicAdd(a.sweeps, (unsigned long long)d.gsweeps[g]);
+    if (a.sweeps) atomicAdd(a.sweeps, (unsigned long long)__ldcg(d.gsweeps + g));
     if (a.capped && giant_active(d, g)) atomicAdd(a.capped, 1ull);
     d.gsweeps[g] = 0;
   }
   clk.mark(6);
   clk.report(d.ng, MODE);
+  if (d.trace > 1 && blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int g = 0; g < d.ng; ++g) {
+      double off = 0.0, fro = 0.0;
+      for (int j = d.out_pre[g]; j < d.out_pre[g + 1]; ++j) off += __ldcg(d.part_off + j);
+      for (int j = d.rb_pre[g]; j < d.rb_pre[g + 1]; ++j) fro += __ldcg(d.part_fro + j);
+      printf("  giant %d k=%d off/fro=%.3e\n", g, a.ksz[d.task[g]], sqrt(off / fro));
+    }
+  }
 }
 
 template <int MODE>

@@ -364,3 +364,56 @@ def test_giant_tier_small_orders_subprocess(tmp_path):
     env = dict(os.environ, SDP_GIANT_MIN="33")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ tridiagonal-QL tier
+
+def _structured(k, rng):
+    """Degenerate inputs for the QL path: zero, identity, repeated / clustered
+    eigenvalues, rank one, +-pairs, sparse (max-cut-like identity + few entries)."""
+    Q, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    lam = np.repeat([2.0, -1.0, 0.0, 1.0 + 1e-9], (k + 3) // 4)[:k]
+    sparse = np.eye(k)
+    for _ in range(k // 4):
+        i, j = rng.integers(0, k, 2)
+        if i != j:
+            sparse[i, j] = sparse[j, i] = rng.uniform(-0.3, 0.3)
+    v = rng.standard_normal(k)
+    pm = Q @ np.diag(np.concatenate([np.full(k // 2, 3.0), np.full(k - k // 2, -3.0)])) @ Q.T
+    return [np.zeros((k, k)), np.eye(k), Q @ np.diag(lam) @ Q.T, np.outer(v, v), pm, sparse, -np.eye(k) * 0.5]
+
+
+def test_trd_tier_batch_many(lib, gen):
+    """>= 2048 matrices per size range select the tridiagonal-QL tier; random orders
+    17..64 (odd and even) plus degenerate structured inputs, against the oracle."""
+    rng = np.random.default_rng(11)
+    mats = []
+    for k in (17, 23, 32, 33, 47, 64):
+        mats += _structured(k, rng)
+    ks = list(rng.integers(17, 65, 4400))
+    vals = [rng.standard_normal(k * (k + 1) // 2) for k in ks]
+    ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)
+    vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)
+    check_batch(lib, ks, vals, tol=1e-12)
+
+
+def test_trd_tier_admm_subprocess():
+    """SDP_PSD_TIERS=trd: every clique of order 17..64 takes the QL tier inside
+    the ADMM iteration (primal and dual), iterates match the oracle."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L, sdp_inputs as gen\n"
+        "from oracle import admm, decompose as dc\n"
+        "prob = gen.maxcut_er(400, 3); dec = dc.decompose(prob)\n"
+        "ks = [len(c) for c in dec.cliques]; assert sum(17 <= k <= 64 for k in ks) >= 5, ks\n"
+        "for form, rho in (('primal', 0.1), ('dual', 10.0)):\n"
+        "    st = admm.step(dec, admm.zero_state(dec), rho, form, 30)\n"
+        "    s = L.Solver(prob, form=form, rho=rho); s.step(30)\n"
+        "    r = lambda g, o: np.linalg.norm(g - o) / np.linalg.norm(o)\n"
+        "    e = max(r(s.x(), st.x), r(s.blocks('xk'), st.xk), r(s.blocks('lambda'), st.lam))\n"
+        "    print(form, e); assert e <= 1e-9, (form, e)\n" % ROOT)
+    env = dict(os.environ, SDP_PSD_TIERS="trd")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
