@@ -59,7 +59,7 @@ void nccl_comm_destroy(void* comm);
 // ---------------------------------------------------------------- projection buckets
 // Kernel tiers for the batched eigen-projection (kernels_psd.cu).
 enum BucketKind {
-  B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_RV8, B_RV16, B_RV32, B_RV64, B_TRD32, B_TRD64, B_NUM
+  B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_RV8, B_RV16, B_RV32, B_RV64, B_TRD32, B_TRD64, B_WJ32, B_NUM
 };
 inline bool is_rv(int b) { return b >= B_RV8 && b <= B_RV64; }
 inline bool is_trd(int b) { return b == B_TRD32 || b == B_TRD64; }
@@ -150,6 +150,7 @@ void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
+void launch_projection_wj(int mode, const ProjArgs& a, cudaStream_t s);
 int64_t trd_rot_cap(int k);      // rotation-list capacity of one matrix of order k
 int64_t trd_hsize(int kp, int k);  // doubles of per-slot Householder workspace
 int giant_grid();        // CTAs of the persistent giant kernel on the current device
@@ -157,7 +158,7 @@ int giant_min_order();   // smallest order routed to the giant tier (SDP_GIANT_M
 int rv_kp(int bucket);
 // stride (kp) of the warm-start V storage of a matrix of order k in tier `bucket`
 inline int store_kp(int bucket, int k) {
-  return is_trd(bucket) ? 0 : is_rv(bucket) ? rv_kp(bucket) : bucket == B_GLOBAL ? (k + 31) / 32 * 32 : k + (k & 1);
+  return is_trd(bucket) ? 0 : bucket == B_WJ32 ? 32 : is_rv(bucket) ? rv_kp(bucket) : bucket == B_GLOBAL ? (k + 31) / 32 * 32 : k + (k & 1);
 }
 
 }  // namespace sdp

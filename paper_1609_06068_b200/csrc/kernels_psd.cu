@@ -455,7 +455,9 @@ void init_attrs_mode() {
 // Opt the large-shared-memory tiers into > 48 KB (per device; call before capture).
 void psd_rv_init_attributes();
 void psd_trd_init_attributes();
+void psd_wj_init_attributes();
 void psd_init_attributes() {
+  psd_wj_init_attributes();
   psd_rv_init_attributes();
   psd_trd_init_attributes();
   init_attrs_mode<PM_BATCH>();
@@ -490,7 +492,7 @@ int bucket_of(int k, int64_t count_in_range) {
   if (!use_smem_tiers() && k <= 64) {
     // few mid-size matrices (e.g. 400 cliques of 30): one 128-thread CTA each is
     // the lower-latency choice; otherwise the register-V tiers
-    if (few && k > 16) return k <= 32 ? B_CTA32 : B_CTA64;
+    if (few && k > 16) return k <= 32 ? (tier_mode() == 0 ? B_WJ32 : B_CTA32) : B_CTA64;
     return k <= 8 ? B_RV8 : k <= 16 ? B_RV16 : k <= 32 ? B_RV32 : B_RV64;
   }
   if (k <= 8) return few ? B_CTA32 : B_G8;
@@ -510,6 +512,10 @@ void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s) 
   }
   if (is_trd(bucket)) {
     launch_projection_trd(bucket, mode, a, s);
+    return;
+  }
+  if (bucket == B_WJ32) {
+    launch_projection_wj(mode, a, s);
     return;
   }
   if (is_rv(bucket)) {

@@ -179,6 +179,18 @@ def test_iterates_after_50(lib, gen, name, form):
 
 
 @pytest.mark.parametrize("form", ["primal", "dual"])
+def test_iterates_long_run_warm_start_k30(lib, gen, form):
+    """Cliques of 30 (the cfg2 shape, warp-register Jacobi tier, DMMA warm start):
+    130 iterations across two cold restarts."""
+    prob = gen.block_arrow(12, 20, 10, 40, seed=7)
+    dec, st, s = run_pair(lib, prob, form, 1.0, 130)
+    assert {len(c) for c in dec.cliques} == {30}
+    compare_state(dec, st, s, form)
+    assert s.info()["jacobi_capped"] == 0
+    s.close()
+
+
+@pytest.mark.parametrize("form", ["primal", "dual"])
 def test_iterates_long_run_warm_start(lib, gen, form):
     """130 iterations: the warm-started Jacobi (V_prev basis) crosses two cold
     restarts (every 64 iterations); iterates still match the oracle."""
