@@ -47,10 +47,17 @@ def load_peaks():
         p["sm_max_mhz"] = float(mp.get("sm_max_mhz", 1965.0))
     except Exception:
         pass
-    # FP64 (non-tensor and DMMA) peak: not in MEASURED_PEAKS.json; derived from
-    # the unit counts: 148 SMs x 64 FP64 FMA/clk x 2 flop x max SM clock.
-    p["fp64_tflops"] = 148 * 64 * 2 * p["sm_max_mhz"] * 1e6 / 1e12
-    p["fp64_src"] = "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz"
+    # FP64 peak: not in MEASURED_PEAKS.json.  Measured on this pool with
+    # tools/fp64_peak.cu (DMMA 37.0 TF, DFMA 33.8 TF; profiles/fp64_peak.json);
+    # fallback: derived from the unit counts (148 SMs x 64 FP64 FMA/clk x 2 x clock).
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            fp = json.load(f)
+        p["fp64_tflops"] = float(fp["dmma_tflops"])
+        p["fp64_src"] = "measured DMMA (mma.sync f64) throughput, profiles/fp64_peak.json"
+    except Exception:
+        p["fp64_tflops"] = 148 * 64 * 2 * p["sm_max_mhz"] * 1e6 / 1e12
+        p["fp64_src"] = "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz"
     return p
 
 
@@ -222,8 +229,7 @@ def run_ours(args, rank, world, local):
                                  "unit": "TFLOP/s", "frac": achieved_tf / peaks["fp64_tflops"],
                                  "traffic": traffic_lookup(wl, "psd"), "algorithmic": "F = sum 10 k^3",
                                  "peak_src": peaks["fp64_src"], "bytes_per_batch": B},
-                    "gpu_launches": sum(1 for _ in set(np.minimum(np.searchsorted([8, 16, 32, 64, 96], ks), 5)))
-                    * args.steps,
+                    "gpu_launches": plan.launches * args.steps,
                     "clocks": clk.summary()})
         # e2e: host buffers through the C ABI, copies inside the timed region
         h_out = np.empty_like(vals)

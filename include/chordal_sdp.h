@@ -198,6 +198,8 @@ int sdp_project_psd_batch(sdp_psd_plan plan, const double* d_in, double* d_out, 
 /* Same, from/to HOST buffers (copies inside the call; synchronous). */
 int sdp_project_psd_batch_host(sdp_psd_plan plan, const double* h_in, double* h_out, void* stream);
 int64_t sdp_psd_plan_values(sdp_psd_plan plan);   /* total doubles of in/out */
+/* Kernel launches one sdp_project_psd_batch call makes (diagnostics; -1 if plan is NULL). */
+int32_t sdp_psd_plan_launches(sdp_psd_plan plan);
 int sdp_psd_plan_destroy(sdp_psd_plan plan);
 
 /* ---- multi-GPU helpers ----------------------------------------------------- */

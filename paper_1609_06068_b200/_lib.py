@@ -100,6 +100,7 @@ _sig = {
     "sdp_project_psd_batch": (_i32, [_vp, _vp, _vp, _vp]),
     "sdp_project_psd_batch_host": (_i32, [_vp, _vp, _vp, _vp]),
     "sdp_psd_plan_values": (_i64, [_vp]),
+    "sdp_psd_plan_launches": (_i32, [_vp]),
     "sdp_psd_plan_destroy": (_i32, [_vp]),
     "sdp_nccl_unique_id": (_i32, [_vp]),
     "sdp_shard_plan": (_i32, [_i32, _i64, _vp, _vp, _i32, _i32, _vp, C.POINTER(_i64), _vp, _vp, C.POINTER(_i64), _vp,
@@ -325,6 +326,7 @@ class PsdPlan:
         _check(lib.sdp_psd_plan_create(self.sizes.size, _ptr(self.sizes), int(device), C.byref(h)))
         self.h = h
         self.values = int(lib.sdp_psd_plan_values(h))
+        self.launches = int(lib.sdp_psd_plan_launches(h))
 
     def project(self, d_in, d_out, stream=None):
         """d_in, d_out: device pointers (int) or torch CUDA float64 tensors."""

@@ -1380,6 +1380,21 @@ int sdp_project_psd_batch_host(sdp_psd_plan pl, const double* h_in, double* h_ou
 
 int64_t sdp_psd_plan_values(sdp_psd_plan pl) { return pl ? pl->values : -1; }
 
+int32_t sdp_psd_plan_launches(sdp_psd_plan pl) {
+  if (!pl) return -1;
+  int32_t n = 0;
+  for (int b = 0; b < B_NUM; ++b) {
+    if (!pl->bcount[b]) continue;
+    if (is_trd(b)) {
+      const TrdDev& t = pl->td[b - B_TRD32];
+      n += 3 * ((t.count + t.chunk - 1) / t.chunk);
+    } else {
+      n += 1;
+    }
+  }
+  return n;
+}
+
 int sdp_psd_plan_destroy(sdp_psd_plan pl) {
   return guarded([&] {
     if (!pl) return SDP_OK;

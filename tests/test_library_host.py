@@ -16,7 +16,7 @@ lib_mod = pytest.importorskip("paper_1609_06068_b200._lib", reason="libchordal_s
 
 def header_symbols():
     txt = open("include/chordal_sdp.h").read()
-    return sorted(set(re.findall(r"^(?:int|void|int64_t|const char\*)\s+(sdp_\w+)\(", txt, re.M)))
+    return sorted(set(re.findall(r"^(?:int|void|int32_t|int64_t|const char\*)\s+(sdp_\w+)\(", txt, re.M)))
 
 
 def test_exports_every_header_symbol():
