@@ -4,23 +4,25 @@
 //
 // Jacobi executes ~4k^3 instructions per sweep and needs 6-9 sweeps from a
 // cold start; this tier uses the flop-lean textbook pipeline instead:
-//   1. k_trd_tridiag (warp per matrix): Householder reduction to tridiagonal
-//      form A = Q T Q^T (LAPACK dsytd2, lower; Golub & Van Loan Alg. 8.3.1),
-//      ~4/3 k^3 flops, matrix in shared memory, lanes own rows.
+//   1. k_trd_tridiag (KP threads per matrix, one row each): Householder
+//      reduction to tridiagonal form A = Q T Q^T (LAPACK dsytd2, lower; Golub &
+//      Van Loan Alg. 8.3.1), ~4/3 k^3 flops, matrix in shared memory.
 //   2. k_trd_ql (lane per matrix): implicit QL with Wilkinson shifts on T
 //      (Golub & Van Loan Alg. 8.3.3 / "tqli"), eigenvalues plus the list of
 //      Givens rotations; the sequential rotation chain of one matrix runs in
 //      one lane, so a warp advances 32 matrices at once and the chain latency
 //      is hidden across matrices.
-//   3. k_trd_apply (warp per matrix): replays the rotations on Z = I (lanes own
-//      rows, the rotation pair is lane-local), back-transforms V = Q Z with the
-//      Householder vectors (lanes own columns; only eigenvectors with lambda > 0
-//      are formed), and rebuilds P_+ = sum_{lambda_t > 0} lambda_t v_t v_t^T with
-//      the mode epilogue (primal: lambda_k += rho (x_k - H_k x), E:LambdakUpdate).
+//   3. k_trd_apply (KP threads per matrix): replays the rotations on Z = I
+//      (threads own rows, the rotation pair is thread-local, and inside one QL
+//      sweep the descending pairs keep z_i in a register), back-transforms
+//      V = Q Z with the Householder vectors (threads own columns; only
+//      eigenvectors with lambda > 0 are formed), and rebuilds
+//      P_+ = sum_{lambda_t > 0} lambda_t v_t v_t^T with the mode epilogue
+//      (primal: lambda_k += rho (x_k - H_k x), E:LambdakUpdate).
 // If a matrix needs more QL rotations than its list holds (or > 30 iterations
 // for one eigenvalue), step 2 marks it and step 3 recomputes its QL inline
-// (all lanes run the same chain and rotate their rows directly): same
-// arithmetic, same result.  Eigenvalues are clipped at exactly 0 (G15).
+// (every thread runs the same chain on a private copy and rotates its row
+// directly): same arithmetic, same result.  Eigenvalues are clipped at exactly 0 (G15).
 #include <cmath>
 #include <cstdlib>
 
@@ -33,7 +35,7 @@ namespace {
 constexpr double kInvSqrt2 = 0.70710678118654752440;
 constexpr double kSqrt2 = 1.41421356237309504880;
 constexpr int kQlMaxIter = 30;
-constexpr int QL_T = 64;  // threads (= matrices) per CTA of the QL kernel
+constexpr int QL_T = 32;  // threads (= matrices) per CTA of the QL kernel
 
 __device__ __forceinline__ void packed_rc(int e, int& r, int& c) {
   int cc = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
@@ -75,54 +77,75 @@ struct HView {
   __device__ double* v() const { return p + 4 * KP; }
 };
 
+// A group of G = KP threads (one matrix row each); G = 64 spans two warps and
+// synchronises on a named barrier.  Sums are fixed-order (deterministic).
+template <int G>
+struct Grp {
+  int tid;
+  int bar;      // named barrier id (G > 32)
+  double* red;  // 2 doubles of scratch (G > 32)
+  __device__ __forceinline__ void sync() const {
+    if constexpr (G <= 32)
+      __syncwarp();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G) : "memory");
+  }
+  __device__ __forceinline__ double sum(double v) const {
+    v = warp_sum(v);
+    if constexpr (G > 32) {
+      sync();
+      if ((tid & 31) == 0) red[tid >> 5] = v;
+      sync();
+      v = red[0] + red[1];
+    }
+    return v;
+  }
+};
+
 // ---------------------------------------------------------------- 1. tridiagonalization
 template <int KP>
 struct TridiagLayout {
   static constexpr int LD = KP + 1;
-  static constexpr int PER = KP * LD + 2 * KP;  // M, v, w
+  static constexpr int PER = KP * LD + 2 * KP + 2;  // M, v, w, reduction scratch
+  static constexpr int NMAT = 128 / KP;              // matrices per 128-thread CTA
 };
 
-template <int KP, int MODE, int NWARP>
-__global__ void __launch_bounds__(NWARP * 32) k_trd_tridiag(ProjArgs a, int slot0, int nslots) {
+template <int KP, int MODE>
+__global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
-  constexpr int LD = TridiagLayout<KP>::LD;
-  constexpr int R = KP / 32;
+  using Lay = TridiagLayout<KP>;
+  constexpr int LD = Lay::LD;
   extern __shared__ double smem[];
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int sl = blockIdx.x * NWARP + wid;
-  if (sl >= nslots) return;
-  double* M = smem + (size_t)wid * TridiagLayout<KP>::PER;
+  const int grp = threadIdx.x / KP;
+  const int sl = blockIdx.x * Lay::NMAT + grp;
+  if (sl >= nslots) return;  // whole groups leave together
+  double* M = smem + (size_t)grp * Lay::PER;
   double* vv = M + KP * LD;
   double* wv = vv + KP;
+  Grp<KP> g{(int)(threadIdx.x % KP), 1 + grp, wv + KP};
+  const int i = g.tid;  // the row this thread owns
   const int slot = slot0 + sl;
   const int task = a.ids[slot];
   const int k = a.ksz[task];
   const int64_t off = a.off[task];
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
   const int ns = k * (k + 1) / 2;
-  for (int e = lane; e < ns; e += 32) {
+  for (int e = i; e < ns; e += KP) {
     int r, c;
     packed_rc(e, r, c);
     const double v = input_value<MODE>(a, off + e, r, c);
     M[r * LD + c] = v;
     M[c * LD + r] = v;
   }
-  __syncwarp();
+  g.sync();
+  double* Mi = M + i * LD;
   int64_t vpos = 0;
   for (int j = 0; j + 2 < k; ++j) {
     // Householder vector of x = M[j+1:k, j] (dlarfg): beta = -sign(alpha) ||x||,
     // tau = (beta - alpha) / beta, v = [1; x2 / (alpha - beta)]
     const double alpha = M[(j + 1) * LD + j];
-    double sig = 0.0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = lane + 32 * r;
-      if (i >= j + 2 && i < k) {
-        const double x = M[i * LD + j];
-        sig = fma(x, x, sig);
-      }
-    }
-    sig = warp_sum(sig);
+    const double xi = (i >= j + 2 && i < k) ? Mi[j] : 0.0;
+    const double sig = g.sum(xi * xi);
     double tau = 0.0, beta = alpha, scl = 0.0;
     if (sig > 0.0) {
       const double nrm = sqrt(fma(alpha, alpha, sig));
@@ -130,79 +153,66 @@ __global__ void __launch_bounds__(NWARP * 32) k_trd_tridiag(ProjArgs a, int slot
       tau = (beta - alpha) / beta;
       scl = 1.0 / (alpha - beta);
     }
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = lane + 32 * r;
-      if (i >= j + 1 && i < k) {
-        const double v = (i == j + 1) ? 1.0 : M[i * LD + j] * scl;
-        vv[i] = v;
-        if (i >= j + 2) H.v()[vpos + (i - j - 2)] = v;
-      }
-    }
-    if (lane == 0) {
+    const bool in = i >= j + 1 && i < k;
+    const double vi = in ? ((i == j + 1) ? 1.0 : xi * scl) : 0.0;
+    if (in) vv[i] = vi;
+    if (i >= j + 2 && i < k) H.v()[vpos + (i - j - 2)] = vi;
+    if (i == 0) {
       H.e()[j] = beta;
       H.tau()[j] = tau;
     }
     vpos += k - j - 2;
-    __syncwarp();
+    g.sync();
     if (tau != 0.0) {
       // p = tau A22 v ; w = p - (tau/2)(p.v) v ; A22 -= v w^T + w v^T
-      double p[R];
-      double part = 0.0;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
-        p[r] = 0.0;
-        if (i >= j + 1 && i < k) {
-          const double* Mi = M + i * LD;
-          double a0 = 0.0, a1 = 0.0;
-          int l = j + 1;
-          for (; l + 1 < k; l += 2) {
-            a0 = fma(Mi[l], vv[l], a0);
-            a1 = fma(Mi[l + 1], vv[l + 1], a1);
-          }
-          if (l < k) a0 = fma(Mi[l], vv[l], a0);
-          p[r] = tau * (a0 + a1);
-          part = fma(p[r], vv[i], part);
+      double pi = 0.0;
+      if (in) {
+        double a0 = 0.0, a1 = 0.0;
+        int l = j + 1;
+        for (; l + 1 < k; l += 2) {
+          a0 = fma(Mi[l], vv[l], a0);
+          a1 = fma(Mi[l + 1], vv[l + 1], a1);
         }
+        if (l < k) a0 = fma(Mi[l], vv[l], a0);
+        pi = tau * (a0 + a1);
       }
-      const double K = 0.5 * tau * warp_sum(part);
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
-        if (i >= j + 1 && i < k) wv[i] = p[r] - K * vv[i];
-      }
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
-        if (i >= j + 1 && i < k) {
-          double* Mi = M + i * LD;
-          const double vi = vv[i], wi = wv[i];
-          for (int l = j + 1; l < k; ++l) Mi[l] -= fma(vi, wv[l], wi * vv[l]);
-        }
-      }
-      __syncwarp();
+      const double K = 0.5 * tau * g.sum(pi * vi);
+      const double wi = pi - K * vi;
+      if (in) wv[i] = wi;
+      g.sync();
+      if (in)
+        for (int l = j + 1; l < k; ++l) Mi[l] -= fma(vi, wv[l], wi * vv[l]);
+      g.sync();
     }
   }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = lane + 32 * r;
-    if (i < k) H.d()[i] = M[i * LD + i];
-  }
-  if (lane == 0) {
+  if (i < k) H.d()[i] = Mi[i];
+  if (i == 0) {
     if (k >= 2) H.e()[k - 2] = M[(k - 1) * LD + k - 2];
     H.e()[k - 1] = 0.0;
   }
 }
 
 // ---------------------------------------------------------------- 2. implicit QL
-// One tqli step chain.  `emit(i, c, s)` receives every rotation acting on
-// columns (i, i+1) of the eigenvector matrix: z_i <- c z_i - s z_{i+1},
-// z_{i+1} <- s z_i + c z_{i+1}.  d, e are accessed as d[i * st], e[i * st].
-// Returns false if an eigenvalue needed more than kQlMaxIter iterations.
+// One tqli chain on T (d, e; e[i] couples i and i+1).  T is first scaled by a
+// power of two so that max |entry| is in [1, 2): then f^2 + g^2 cannot
+// overflow, hypot(f, g) = q rsqrt(q) with q = f^2 + g^2, and a coupling whose
+// square underflows is below 1e-300 ||T|| and is deflated (the r == 0 branch).
+// `emit(i, c, s)` receives every rotation acting on columns (i, i+1) of the
+// eigenvector matrix: z_i <- c z_i - s z_{i+1}, z_{i+1} <- s z_i + c z_{i+1}.
+// d, e are accessed as d[i * st], e[i * st].  Returns false if an eigenvalue
+// needed more than kQlMaxIter iterations.  Eigenvalues are returned unscaled.
 template <class Emit>
 __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& emit) {
+  double mx = 0.0;
+  for (int i = 0; i < k; ++i) mx = fmax(mx, fmax(fabs(d[i * st]), fabs(e[i * st])));
+  if (mx == 0.0) return true;
+  const int ex = ilogb(mx);
+  const double sc = scalbn(1.0, -ex), usc = scalbn(1.0, ex);
+  for (int i = 0; i < k; ++i) {
+    d[i * st] *= sc;
+    e[i * st] *= sc;
+  }
+  bool ok = true;
   for (int l = 0; l < k; ++l) {
     int iter = 0;
     int m;
@@ -212,23 +222,31 @@ __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& 
         if (fabs(e[m * st]) + dd == dd) break;
       }
       if (m != l) {
-        if (iter++ == kQlMaxIter) return false;
+        if (iter++ == kQlMaxIter) {
+          ok = false;
+          break;
+        }
         double g = (d[(l + 1) * st] - d[l * st]) / (2.0 * e[l * st]);
-        double r = hypot(g, 1.0);
+        double r = fabs(g) > 1e150 ? fabs(g) : sqrt(fma(g, g, 1.0));
         g = d[m * st] - d[l * st] + e[l * st] / (g + copysign(r, g));
         double s = 1.0, c = 1.0, p = 0.0;
         int i;
         for (i = m - 1; i >= l; --i) {
-          const double f = s * e[i * st], b = c * e[i * st];
-          r = hypot(f, g);
-          e[(i + 1) * st] = r;
-          if (r == 0.0) {
+          const double ei = e[i * st];
+          const double f = s * ei, b = c * ei;
+          const double q = fma(f, f, g * g);
+          if (q == 0.0) {
+            e[(i + 1) * st] = 0.0;
             d[(i + 1) * st] -= p;
             e[m * st] = 0.0;
+            r = 0.0;
             break;
           }
-          s = f / r;
-          c = g / r;
+          r = sqrt(q);
+          const double ri = 1.0 / r;
+          e[(i + 1) * st] = r;
+          s = f * ri;
+          c = g * ri;
           g = d[(i + 1) * st] - p;
           r = (d[i * st] - g) * s + 2.0 * c * b;
           p = s * r;
@@ -242,8 +260,10 @@ __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& 
         e[m * st] = 0.0;
       }
     } while (m != l);
+    if (!ok) break;
   }
-  return true;
+  for (int i = 0; i < k; ++i) d[i * st] *= usc;
+  return ok;
 }
 
 template <int KP>
@@ -281,18 +301,19 @@ __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslo
 template <int KP>
 struct ApplyLayout {
   static constexpr int LD = KP + 1;
+  static constexpr int NR = 64;  // rotations staged per round
   static constexpr size_t bytes() {
-    return (size_t)(KP * LD + 4 * KP + 2 * 32) * sizeof(double) + (KP + 32) * sizeof(int);
+    return (size_t)(KP * LD + 4 * KP + 2 + 2 * NR) * sizeof(double) + (KP + NR) * sizeof(int);
   }
 };
 
 template <int KP, int MODE>
-__global__ void __launch_bounds__(32) k_trd_apply(ProjArgs a, int slot0, int nslots) {
+__global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
-  constexpr int LD = ApplyLayout<KP>::LD;
-  constexpr int R = KP / 32;
+  using Lay = ApplyLayout<KP>;
+  constexpr int LD = Lay::LD;
+  constexpr int NR = Lay::NR;
   extern __shared__ double smem[];
-  const int lane = threadIdx.x;
   const int sl = blockIdx.x;
   if (sl >= nslots) return;
   double* Z = smem;
@@ -300,95 +321,99 @@ __global__ void __launch_bounds__(32) k_trd_apply(ProjArgs a, int slot0, int nsl
   double* lp = vv + KP;
   double* dsm = lp + KP;
   double* esm = dsm + KP;
-  double2* rsm = reinterpret_cast<double2*>(esm + KP);
-  int* pidx = reinterpret_cast<int*>(rsm + 32);
+  double* red = esm + KP;
+  double2* rsm = reinterpret_cast<double2*>(red + 2);
+  int* pidx = reinterpret_cast<int*>(rsm + NR);
   int* ism = pidx + KP;
+  Grp<KP> g{(int)threadIdx.x, 1, red};
+  const int row = g.tid;
   const int slot = slot0 + sl;
   const int task = a.ids[slot];
   const int k = a.ksz[task];
   const int64_t off = a.off[task];
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
-  for (int e = lane; e < k * KP; e += 32) {
-    const int i = e / KP, j = e - i * KP;
-    Z[i * LD + j] = (i == j) ? 1.0 : 0.0;
-  }
+  double* Zr = Z + row * LD;
+  for (int j = 0; j < KP; ++j) Zr[j] = (j == row) ? 1.0 : 0.0;
   const int nrot = a.td.rcount[slot];
-  __syncwarp();
   if (nrot >= 0) {
+    // replay the QL rotations on this row; inside one QL sweep the pairs descend
+    // (i+1, i+2), (i, i+1), ..., so z_i stays in a register ("carry")
     const double2* rot = a.td.rot + a.td.roff[slot];
     const int16_t* ridx = a.td.ridx + a.td.roff[slot];
-    for (int t0 = 0; t0 < nrot; t0 += 32) {
-      const int nt = min(32, nrot - t0);
-      __syncwarp();
-      if (lane < nt) {
-        rsm[lane] = rot[t0 + lane];
-        ism[lane] = ridx[t0 + lane];
+    double carry = 0.0;
+    int cur = -2;  // column held in `carry`
+    for (int t0 = 0; t0 < nrot; t0 += NR) {
+      const int nt = min(NR, nrot - t0);
+      g.sync();
+      for (int u = row; u < nt; u += KP) {
+        rsm[u] = rot[t0 + u];
+        ism[u] = ridx[t0 + u];
       }
-      __syncwarp();
-      for (int u = 0; u < nt; ++u) {
-        const double2 cs = rsm[u];
-        const int i = ism[u];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int row = lane + 32 * r;
-          if (row < k) {
-            double* Zr = Z + row * LD;
-            const double zi = Zr[i], zi1 = Zr[i + 1];
-            Zr[i + 1] = fma(cs.y, zi, cs.x * zi1);
-            Zr[i] = fma(cs.x, zi, -cs.y * zi1);
+      g.sync();
+      if (row < k) {
+        for (int u = 0; u < nt; ++u) {
+          const double2 cs = rsm[u];
+          const int i = ism[u];
+          double zi1;
+          if (i + 1 == cur) {
+            zi1 = carry;
+          } else {
+            if (cur >= 0) Zr[cur] = carry;
+            zi1 = Zr[i + 1];
           }
+          const double zi = Zr[i];
+          Zr[i + 1] = fma(cs.y, zi, cs.x * zi1);
+          carry = fma(cs.x, zi, -cs.y * zi1);
+          cur = i;
         }
       }
     }
-    for (int i = lane; i < k; i += 32) dsm[i] = H.lam()[i];
+    if (row < k && cur >= 0) Zr[cur] = carry;
+    if (row < k) dsm[row] = H.lam()[row];
   } else {
-    // fallback: the QL chain inline, every lane computing the same rotations
-    for (int i = lane; i < k; i += 32) {
-      dsm[i] = H.d()[i];
-      esm[i] = H.e()[i];
+    // fallback: the QL chain inline; every thread runs the same chain on a
+    // private copy of (d, e) (identical arithmetic, so identical rotations) and
+    // rotates its own row
+    double dl[KP], el[KP];
+    for (int i = 0; i < k; ++i) {
+      dl[i] = H.d()[i];
+      el[i] = H.e()[i];
     }
-    __syncwarp();
-    const bool ok = tql(k, dsm, esm, 1, [&](int i, double c, double s) {
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int row = lane + 32 * r;
-        if (row < k) {
-          double* Zr = Z + row * LD;
-          const double zi = Zr[i], zi1 = Zr[i + 1];
-          Zr[i + 1] = fma(s, zi, c * zi1);
-          Zr[i] = fma(c, zi, -s * zi1);
-        }
+    const bool ok = tql(k, dl, el, 1, [&](int i, double c, double s) {
+      if (row < k) {
+        const double zi = Zr[i], zi1 = Zr[i + 1];
+        Zr[i + 1] = fma(s, zi, c * zi1);
+        Zr[i] = fma(c, zi, -s * zi1);
       }
-      __syncwarp();
     });
-    if (!ok && lane == 0 && a.capped) atomicAdd(a.capped, 1ull);
+    if (row < k) dsm[row] = dl[row];
+    if (!ok && row == 0 && a.capped) atomicAdd(a.capped, 1ull);
   }
-  __syncwarp();
+  g.sync();
   // positive eigenvalues, compacted in index order (deterministic)
   int npos = 0;
   for (int t0 = 0; t0 < k; t0 += 32) {
-    const int t = t0 + lane;
+    const int t = t0 + (row & 31);
     const double l = t < k ? dsm[t] : 0.0;
     const bool pos = l > 0.0;
     const unsigned bal = __ballot_sync(0xffffffffu, pos);
-    if (pos) {
-      const int at = npos + __popc(bal & ((1u << lane) - 1u));
+    if (row < 32 && pos) {
+      const int at = npos + __popc(bal & ((1u << row) - 1u));
       pidx[at] = t;
       lp[at] = l;
     }
     npos += __popc(bal);
   }
-  __syncwarp();
+  g.sync();
   // back-transform the positive eigenvectors: V = H_0 H_1 ... H_{k-3} Z
   int64_t vpos = k >= 2 ? (int64_t)(k - 1) * (k - 2) / 2 : 0;
   for (int j = k - 3; j >= 0; --j) {
     vpos -= k - j - 2;
     const double tau = H.tau()[j];
     if (tau == 0.0) continue;
-    __syncwarp();
-    for (int i = j + 1 + lane; i < k; i += 32) vv[i] = (i == j + 1) ? 1.0 : H.v()[vpos + (i - j - 2)];
-    __syncwarp();
-    for (int u = lane; u < npos; u += 32) {
+    if (row >= j + 1 && row < k) vv[row] = (row == j + 1) ? 1.0 : H.v()[vpos + (row - j - 2)];
+    g.sync();
+    for (int u = row; u < npos; u += KP) {
       const int c = pidx[u];
       double y0 = 0.0, y1 = 0.0;
       int i = j + 1;
@@ -400,20 +425,20 @@ __global__ void __launch_bounds__(32) k_trd_apply(ProjArgs a, int slot0, int nsl
       const double y = tau * (y0 + y1);
       for (i = j + 1; i < k; ++i) Z[i * LD + c] = fma(-y, vv[i], Z[i * LD + c]);
     }
+    g.sync();
   }
-  __syncwarp();
   // P_+ = sum_{lambda_t > 0} lambda_t v_t v_t^T, packed upper, mode epilogue
   const int ns = k * (k + 1) / 2;
   double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-  for (int e = lane; e < ns; e += 32) {
+  for (int e = row; e < ns; e += KP) {
     int r, c;
     packed_rc(e, r, c);
-    const double* Zr = Z + r * LD;
+    const double* Zrr = Z + r * LD;
     const double* Zc = Z + c * LD;
     double acc = 0.0;
     for (int u = 0; u < npos; ++u) {
       const int t = pidx[u];
-      acc = fma(lp[u] * Zr[t], Zc[t], acc);
+      acc = fma(lp[u] * Zrr[t], Zc[t], acc);
     }
     const int64_t pe = off + e;
     if constexpr (MODE == PM_BATCH) {
@@ -432,10 +457,10 @@ __global__ void __launch_bounds__(32) k_trd_apply(ProjArgs a, int slot0, int nsl
     }
   }
   if constexpr (MODE == PM_PRIMAL) {
-    p0 = warp_sum(p0);
-    p1 = warp_sum(p1);
-    p2 = warp_sum(p2);
-    if (lane == 0) {
+    p0 = g.sum(p0);
+    p1 = g.sum(p1);
+    p2 = g.sum(p2);
+    if (row == 0) {
       a.part[3 * (int64_t)task + 0] = p0;
       a.part[3 * (int64_t)task + 1] = p1;
       a.part[3 * (int64_t)task + 2] = p2;
@@ -443,25 +468,19 @@ __global__ void __launch_bounds__(32) k_trd_apply(ProjArgs a, int slot0, int nsl
   }
 }
 
-template <int KP>
-constexpr int tridiag_warps() {
-  return KP == 64 ? 1 : 4;
-}
-
 template <int KP, int MODE>
 void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
-  constexpr int NW = tridiag_warps<KP>();
-  k_trd_tridiag<KP, MODE, NW><<<(n + NW - 1) / NW, NW * 32, NW * TridiagLayout<KP>::PER * sizeof(double), s>>>(
-      a, c0, n);
+  using TL = TridiagLayout<KP>;
+  k_trd_tridiag<KP, MODE><<<(n + TL::NMAT - 1) / TL::NMAT, 128, TL::NMAT * TL::PER * sizeof(double), s>>>(a, c0, n);
   k_trd_ql<KP><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
-  k_trd_apply<KP, MODE><<<n, 32, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
+  k_trd_apply<KP, MODE><<<n, KP, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
 }
 
 template <int KP, int MODE>
 void set_attrs() {
-  constexpr int NW = tridiag_warps<KP>();
-  cudaFuncSetAttribute(k_trd_tridiag<KP, MODE, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(NW * TridiagLayout<KP>::PER * sizeof(double)));
+  using TL = TridiagLayout<KP>;
+  cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(TL::NMAT * TL::PER * sizeof(double)));
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(2 * KP * QL_T * sizeof(double)));
   cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -479,7 +498,12 @@ void psd_trd_init_attributes() {
   set_attrs<64, PM_DUAL>();
 }
 
-int64_t trd_rot_cap(int k) { return std::max<int64_t>(64, (int64_t)3 * k * k / 2); }
+// SDP_TRD_ROTCAP overrides the capacity (tests force the inline-QL fallback with it)
+int64_t trd_rot_cap(int k) {
+  const char* e = getenv("SDP_TRD_ROTCAP");
+  if (e && *e) return std::max<int64_t>(0, atoll(e));
+  return std::max<int64_t>(64, (int64_t)3 * k * k / 2);
+}
 
 int64_t trd_hsize(int kp, int k) {
   const int64_t v = k >= 2 ? (int64_t)(k - 1) * (k - 2) / 2 : 0;

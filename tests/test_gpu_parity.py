@@ -429,3 +429,24 @@ def test_trd_tier_admm_subprocess():
     env = dict(os.environ, SDP_PSD_TIERS="trd")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_trd_tier_inline_ql_fallback_subprocess():
+    """SDP_TRD_ROTCAP=0: no rotation list fits, every matrix of the QL tier takes
+    the inline-QL fallback of the apply kernel; results still match the oracle."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L\n"
+        "from oracle import psd as opsd\n"
+        "rng = np.random.default_rng(4)\n"
+        "ks = rng.integers(17, 65, 2200).astype(np.int32)\n"
+        "vals = np.concatenate([rng.standard_normal(k*(k+1)//2) for k in ks])\n"
+        "out = L.PsdPlan(ks).project_host(vals)\n"
+        "want = opsd.project_psd_packed_batch(ks, vals)\n"
+        "e = np.linalg.norm(out - want) / np.linalg.norm(want)\n"
+        "print(e); assert e <= 1e-12, e\n" % ROOT)
+    env = dict(os.environ, SDP_TRD_ROTCAP="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
