@@ -289,30 +289,26 @@ void build_trd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<int
   if (!n) return;
   const char* bud = getenv("SDP_TRD_BUDGET_MB");
   const int64_t budget = (bud ? std::max(16ll, atoll(bud)) : 2048ll) << 20;
-  const int64_t per = 8 * trd_hsize(kp, kp) + (int64_t)(sizeof(double2) + sizeof(int16_t)) * trd_rot_cap(kp);
+  const int64_t zper = (int64_t)(kp / 2) * kp;
+  const int64_t per = 8 * (trd_hsize(kp, kp) + zper);
   const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(n, budget / per));
-  std::vector<int64_t> hoff(n), roff(n);
-  std::vector<int32_t> rcap(n);
-  int64_t hmax = 0, rmax = 0, h = 0, r = 0;
+  std::vector<int64_t> hoff(n), zoff(n);
+  int64_t hmax = 0, h = 0;
   for (int i = 0; i < n; ++i) {
-    if (i % chunk == 0) h = r = 0;
-    const int k = ksz[ids[i]];
+    if (i % chunk == 0) h = 0;
     hoff[i] = h;
-    roff[i] = r;
-    rcap[i] = (int32_t)trd_rot_cap(k);
-    h += trd_hsize(kp, k);
-    r += rcap[i];
+    zoff[i] = (int64_t)(i % chunk) * zper;
+    h += trd_hsize(kp, ksz[ids[i]]);
     hmax = std::max(hmax, h);
-    rmax = std::max(rmax, r);
   }
   td.count = n;
   td.chunk = chunk;
+  const char* ff = getenv("SDP_TRD_FORCE_FALLBACK");
+  td.force_fallback = (ff && *ff == '1') ? 1 : 0;
   td.hoff = al.upload(hoff);
-  td.roff = al.upload(roff);
-  td.rcap = al.upload(rcap);
+  td.zoff = al.upload(zoff);
   td.hbuf = al.get<double>((size_t)hmax);
-  td.rot = al.get<double2>((size_t)rmax);
-  td.ridx = al.get<int16_t>((size_t)rmax);
+  td.zbuf = al.get<double>((size_t)chunk * zper);
   td.rcount = al.zeros<int32_t>((size_t)n);
 }
 
@@ -512,7 +508,7 @@ int launches_per_iter(sdp_handle h) {
     if (!h->bcount[b]) continue;
     if (is_trd(b)) {
       const TrdDev& t = h->td[b - B_TRD32];
-      n += 3 * ((t.count + t.chunk - 1) / t.chunk);
+      n += 4 * ((t.count + t.chunk - 1) / t.chunk);
     } else {
       n += 1;
     }
@@ -1387,7 +1383,7 @@ int32_t sdp_psd_plan_launches(sdp_psd_plan pl) {
     if (!pl->bcount[b]) continue;
     if (is_trd(b)) {
       const TrdDev& t = pl->td[b - B_TRD32];
-      n += 3 * ((t.count + t.chunk - 1) / t.chunk);
+      n += 4 * ((t.count + t.chunk - 1) / t.chunk);
     } else {
       n += 1;
     }

@@ -103,19 +103,18 @@ struct GiantDev {
 
 // Tridiagonal-QL tiers (kernels_psd_trd.cu), per bucket.  Slots = positions in
 // the bucket list; processed in chunks of `chunk` slots whose workspace
-// offsets (hoff: doubles into hbuf, roff: rotations into rot / ridx) are
-// relative to the chunk's first slot.  Per slot hbuf holds d, e, tau, lambda
-// (KP each) followed by the packed Householder vectors.
+// offsets (hoff: doubles into hbuf) are relative to the chunk's first slot.
+// Per slot hbuf holds d, e, tau, lambda (KP each) followed by the packed
+// Householder vectors.
 struct TrdDev {
   int count = 0;
   int chunk = 0;
+  int force_fallback = 0;     // SDP_TRD_FORCE_FALLBACK=1 (tests): QL with vectors for every matrix
   const int64_t* hoff = nullptr;
-  const int64_t* roff = nullptr;
-  const int32_t* rcap = nullptr;
+  const int64_t* zoff = nullptr;  // per slot: offset (doubles) of its selected eigenvectors of T
   double* hbuf = nullptr;
-  double2* rot = nullptr;
-  int16_t* ridx = nullptr;
-  int32_t* rcount = nullptr;  // per slot (chunk-relative): rotations stored, -1 = QL fell back
+  double* zbuf = nullptr;         // per slot (KP/2) x KP doubles
+  int32_t* rcount = nullptr;  // per slot: 0, or -1 (QL iteration cap / inverse iteration residual)
 };
 
 struct ProjArgs {
@@ -151,7 +150,6 @@ void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t 
 void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_wj(int mode, const ProjArgs& a, cudaStream_t s);
-int64_t trd_rot_cap(int k);      // rotation-list capacity of one matrix of order k
 int64_t trd_hsize(int kp, int k);  // doubles of per-slot Householder workspace
 int giant_grid();        // CTAs of the persistent giant kernel on the current device
 int giant_min_order();   // smallest order routed to the giant tier (SDP_GIANT_MIN, default 97)

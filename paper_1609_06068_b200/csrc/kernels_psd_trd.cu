@@ -8,21 +8,22 @@
 //      reduction to tridiagonal form A = Q T Q^T (LAPACK dsytd2, lower; Golub &
 //      Van Loan Alg. 8.3.1), ~4/3 k^3 flops, matrix in shared memory.
 //   2. k_trd_ql (lane per matrix): implicit QL with Wilkinson shifts on T
-//      (Golub & Van Loan Alg. 8.3.3 / "tqli"), eigenvalues plus the list of
-//      Givens rotations; the sequential rotation chain of one matrix runs in
-//      one lane, so a warp advances 32 matrices at once and the chain latency
-//      is hidden across matrices.
-//   3. k_trd_apply (KP threads per matrix): replays the rotations on Z = I
-//      (threads own rows, the rotation pair is thread-local, and inside one QL
-//      sweep the descending pairs keep z_i in a register), back-transforms
-//      V = Q Z with the Householder vectors (threads own columns; only
-//      eigenvectors with lambda > 0 are formed), and rebuilds
-//      P_+ = sum_{lambda_t > 0} lambda_t v_t v_t^T with the mode epilogue
-//      (primal: lambda_k += rho (x_k - H_k x), E:LambdakUpdate).
-// If a matrix needs more QL rotations than its list holds (or > 30 iterations
-// for one eigenvalue), step 2 marks it and step 3 recomputes its QL inline
-// (every thread runs the same chain on a private copy and rotates its row
-// directly): same arithmetic, same result.  Eigenvalues are clipped at exactly 0 (G15).
+//      (Golub & Van Loan Alg. 8.3.3 / "tqli"), eigenvalues only; the sequential
+//      chain of one matrix runs in one lane, so a warp advances 32 matrices at
+//      once and the chain latency is hidden across matrices.
+//   3. k_trd_apply (KP threads per matrix): P_+ needs only the eigenvectors on
+//      one side of 0, so the smaller side is taken (P_+ = sum_{l>0} l v v^T, or
+//      A + sum_{l<0} |l| v v^T); its eigenvectors of T come from inverse
+//      iteration (LAPACK dstein: partial-pivoting tridiagonal LU, clusters of
+//      gap <= 1e-3 ||T|| reorthogonalised), O(k) per vector instead of the O(k^2)
+//      rotation accumulation of QL, then V = Q Z with the Householder vectors and
+//      the reconstruction with the mode epilogue (primal: lambda_k +=
+//      rho (x_k - H_k x), E:LambdakUpdate).
+// Every inverse-iteration vector is checked (||T z - lambda z|| <= 1e-9 ||T||);
+// if one fails, or QL hit its iteration cap, the matrix is redone inside the
+// apply kernel by QL with eigenvector accumulation (every thread runs the same
+// chain on a private copy and rotates its own row).  Eigenvalues are clipped at
+// exactly 0 (G15).
 #include <cmath>
 #include <cstdlib>
 
@@ -65,16 +66,21 @@ __device__ __forceinline__ double input_value(const ProjArgs& a, int64_t e, int 
   }
 }
 
-// per-slot Householder workspace: d, e, tau, lambda (KP each), packed v_j (j = 0..k-3,
-// entries j+2..k-1; v_j[j+1] = 1 implicit)
+// per-slot workspace (doubles): d, e, tau (KP each); the selected eigenvalues
+// (ascending, used as inverse-iteration shifts), their reconstruction weights
+// and cluster leaders (KP each); a header {nsel, side, ||T||, -}; the packed
+// Householder vectors v_j (j = 0..k-3, entries j+2..k-1; v_j[j+1] = 1 implicit)
 template <int KP>
 struct HView {
   double* p;
   __device__ double* d() const { return p; }
   __device__ double* e() const { return p + KP; }
   __device__ double* tau() const { return p + 2 * KP; }
-  __device__ double* lam() const { return p + 3 * KP; }
-  __device__ double* v() const { return p + 4 * KP; }
+  __device__ double* lsel() const { return p + 3 * KP; }
+  __device__ double* lw() const { return p + 4 * KP; }
+  __device__ double* clst() const { return p + 5 * KP; }
+  __device__ double* hdr() const { return p + 6 * KP; }
+  __device__ double* v() const { return p + 6 * KP + 4; }
 };
 
 // A group of G = KP threads (one matrix row each); G = 64 spans two warps and
@@ -282,29 +288,184 @@ __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslo
     d[i * QL_T] = H.d()[i];
     e[i * QL_T] = H.e()[i];
   }
-  double2* rot = a.td.rot + a.td.roff[slot];
-  int16_t* ridx = a.td.ridx + a.td.roff[slot];
-  const int64_t cap = a.td.rcap[slot];
-  int64_t n = 0;
-  const bool ok = tql(k, d, e, QL_T, [&](int i, double c, double s) {
-    if (n < cap) {
-      rot[n] = make_double2(c, s);
-      ridx[n] = (int16_t)i;
+  const bool ok = tql(k, d, e, QL_T, [](int, double, double) {});
+  // the side of 0 with fewer eigenvectors: P_+ = sum_{l>0} l v v^T (side 0) or
+  // A + sum_{l<0} |l| v v^T (side 1); selected eigenvalues sorted ascending,
+  // clusters (gap <= 1e-3 ||T||, LAPACK dstein's ORTOL) and distinct shifts
+  int npos = 0, nneg = 0;
+  double tnorm = 0.0;
+  for (int i = 0; i < k; ++i) {
+    const double l = d[i * QL_T];
+    npos += l > 0.0;
+    nneg += l < 0.0;
+    tnorm = fmax(tnorm, fabs(H.d()[i]) + (i > 0 ? fabs(H.e()[i - 1]) : 0.0) + (i + 1 < k ? fabs(H.e()[i]) : 0.0));
+  }
+  const int side = npos <= nneg ? 0 : 1;
+  double* ls = H.lsel();
+  int n = 0;
+  for (int i = 0; i < k; ++i) {
+    const double l = d[i * QL_T];
+    if (side == 0 ? l > 0.0 : l < 0.0) {
+      int j = n++ - 1;  // insertion sort, ascending
+      while (j >= 0 && ls[j] > l) {
+        ls[j + 1] = ls[j];
+        --j;
+      }
+      ls[j + 1] = l;
     }
-    ++n;
-  });
-  for (int i = 0; i < k; ++i) H.lam()[i] = d[i * QL_T];
-  a.td.rcount[slot] = (ok && n <= cap) ? (int32_t)n : -1;
+  }
+  const double ortol = 1e-3 * tnorm, pertol = 10.0 * 2.220446049250313e-16 * tnorm;
+  int lead = 0;
+  for (int i = 0; i < n; ++i) {
+    H.lw()[i] = side == 0 ? ls[i] : -ls[i];
+    if (i == 0 || ls[i] - ls[i - 1] > ortol) lead = i;
+    H.clst()[i] = (double)lead;
+    if (i > lead && ls[i] - ls[i - 1] < pertol) ls[i] = ls[i - 1] + pertol;
+  }
+  H.hdr()[0] = (double)n;
+  H.hdr()[1] = (double)side;
+  H.hdr()[2] = tnorm;
+  a.td.rcount[slot] = ok ? 0 : -1;
 }
 
-// ---------------------------------------------------------------- 3. rotations, back-transform, P_+
+// ---------------------------------------------------------------- 3. inverse iteration
+// One thread per cluster of selected eigenvalues (LAPACK dstein): for each
+// eigenvalue in the cluster, the partial-pivoting LU of T - lam I (dlagtf;
+// pivots below tol replaced by +-tol, stored inverted), then 3 solves
+// (dlagts) from a deterministic pseudo-random start, each followed by modified
+// Gram-Schmidt against the cluster's previous vectors and normalisation.  The
+// per-thread factors live in shared memory, thread-minor.  A vector whose
+// residual ||T z - lam z||_inf exceeds 1e-9 ||T|| marks the matrix (rcount = -1)
+// and the apply kernel redoes it by QL with eigenvector accumulation.
+constexpr int IV_T = 32;  // threads per CTA
+template <int KP>
+struct InvLayout {
+  static constexpr int HALF = KP / 2;        // selected eigenvalues per matrix <= k / 2
+  static constexpr int NMAT = IV_T / HALF;   // matrices per CTA
+  static constexpr size_t bytes() { return (size_t)5 * KP * IV_T * sizeof(double); }
+};
+
+template <int KP>
+__global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int nslots) {
+  if (a.done && *a.done) return;
+  using Lay = InvLayout<KP>;
+  extern __shared__ double smem[];
+  const int t = threadIdx.x;
+  const int sl = blockIdx.x * Lay::NMAT + t / Lay::HALF;
+  const int j0 = t % Lay::HALF;  // cluster leader this thread may own
+  if (sl >= nslots) return;
+  const int slot = slot0 + sl;
+  const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
+  const int nsel = (int)H.hdr()[0];
+  if (j0 >= nsel || (int)H.clst()[j0] != j0) return;
+  const int k = a.ksz[a.ids[slot]];
+  const double tnorm = H.hdr()[2];
+  const double tol = 2.220446049250313e-16 * fmax(tnorm, 1e-300);
+  const double* d = H.d();
+  const double* e = H.e();
+  double* ui = smem + t;  // inverse pivots, element i at [i * IV_T]
+  double* u2 = ui + KP * IV_T;
+  double* u3 = u2 + KP * IV_T;
+  double* mu = u3 + KP * IV_T;
+  double* x = mu + KP * IV_T;
+  double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [j][i]
+  bool fail = false;
+  for (int j = j0; j < nsel && (int)H.clst()[j] == j0; ++j) {
+    const double lam = H.lsel()[j];
+    unsigned long long pv = 0ull;  // pivot flags (k <= 64)
+    double r0 = d[0] - lam, r1 = k > 1 ? e[0] : 0.0, r2 = 0.0;
+    for (int i = 0; i + 1 < k; ++i) {
+      const double ci = e[i], ai = d[i + 1] - lam, bi = (i + 2 < k) ? e[i + 1] : 0.0;
+      double p1, p2, p3, m;
+      if (fabs(ci) > fabs(r0)) {
+        pv |= 1ull << i;
+        p1 = ci;
+        p2 = ai;
+        p3 = bi;
+        m = r0 / ci;
+        r0 = r1 - m * ai;
+        r1 = r2 - m * bi;
+      } else {
+        p1 = r0;
+        p2 = r1;
+        p3 = r2;
+        m = r0 != 0.0 ? ci / r0 : 0.0;
+        r0 = ai - m * r1;
+        r1 = bi - m * r2;
+      }
+      r2 = 0.0;
+      if (fabs(p1) < tol) p1 = p1 < 0.0 ? -tol : tol;
+      ui[i * IV_T] = 1.0 / p1;
+      u2[i * IV_T] = p2;
+      u3[i * IV_T] = p3;
+      mu[i * IV_T] = m;
+    }
+    if (fabs(r0) < tol) r0 = r0 < 0.0 ? -tol : tol;
+    ui[(k - 1) * IV_T] = 1.0 / r0;
+    for (int i = 0; i < k; ++i) {
+      unsigned long long h = (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull ^
+                             (unsigned long long)(j + 7) * 0xD1B54A32D192ED03ull;
+      h ^= h >> 31;
+      h *= 0xBF58476D1CE4E5B9ull;
+      h ^= h >> 29;
+      x[i * IV_T] = (double)(h >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    }
+    for (int it = 0; it < 3; ++it) {
+      double ry = x[0];
+      for (int i = 0; i + 1 < k; ++i) {
+        const double yn = x[(i + 1) * IV_T];
+        const double m = mu[i * IV_T];
+        if ((pv >> i) & 1ull) {
+          x[i * IV_T] = yn;
+          ry = fma(-m, yn, ry);
+        } else {
+          x[i * IV_T] = ry;
+          ry = fma(-m, ry, yn);
+        }
+      }
+      double xn = ry * ui[(k - 1) * IV_T], xn1 = 0.0;
+      x[(k - 1) * IV_T] = xn;
+      double mx = fabs(xn);
+      for (int i = k - 2; i >= 0; --i) {
+        const double xi = (x[i * IV_T] - u2[i * IV_T] * xn - u3[i * IV_T] * xn1) * ui[i * IV_T];
+        x[i * IV_T] = xi;
+        mx = fmax(mx, fabs(xi));
+        xn1 = xn;
+        xn = xi;
+      }
+      const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
+      for (int i = 0; i < k; ++i) x[i * IV_T] *= inv;
+      for (int p = j0; p < j; ++p) {
+        const double* zp = Zo + (size_t)p * KP;
+        double dot = 0.0;
+        for (int i = 0; i < k; ++i) dot = fma(zp[i], x[i * IV_T], dot);
+        for (int i = 0; i < k; ++i) x[i * IV_T] = fma(-dot, zp[i], x[i * IV_T]);
+      }
+      double nrm = 0.0;
+      for (int i = 0; i < k; ++i) nrm = fma(x[i * IV_T], x[i * IV_T], nrm);
+      const double in2 = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+      for (int i = 0; i < k; ++i) x[i * IV_T] *= in2;
+    }
+    double res = 0.0;
+    double* zj = Zo + (size_t)j * KP;
+    for (int i = 0; i < k; ++i) {
+      const double xi = x[i * IV_T];
+      double tz = (d[i] - lam) * xi;
+      if (i > 0) tz = fma(e[i - 1], x[(i - 1) * IV_T], tz);
+      if (i + 1 < k) tz = fma(e[i], x[(i + 1) * IV_T], tz);
+      res = fmax(res, fabs(tz));
+      zj[i] = xi;
+    }
+    if (!(res <= 1e-9 * fmax(tnorm, 1e-300))) fail = true;  // includes NaN
+  }
+  if (fail) a.td.rcount[slot] = -1;
+}
+
+// ---------------------------------------------------------------- 4. back-transform, P_+
 template <int KP>
 struct ApplyLayout {
   static constexpr int LD = KP + 1;
-  static constexpr int NR = 64;  // rotations staged per round
-  static constexpr size_t bytes() {
-    return (size_t)(KP * LD + 4 * KP + 2 + 2 * NR) * sizeof(double) + (KP + NR) * sizeof(int);
-  }
+  static constexpr size_t bytes() { return (size_t)(KP * LD + 2 * KP + 2) * sizeof(double); }
 };
 
 template <int KP, int MODE>
@@ -312,68 +473,37 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
   if (a.done && *a.done) return;
   using Lay = ApplyLayout<KP>;
   constexpr int LD = Lay::LD;
-  constexpr int NR = Lay::NR;
   extern __shared__ double smem[];
   const int sl = blockIdx.x;
   if (sl >= nslots) return;
-  double* Z = smem;
+  double* Z = smem;  // selected eigenvectors (columns), then back-transformed
   double* vv = Z + KP * LD;
-  double* lp = vv + KP;
-  double* dsm = lp + KP;
-  double* esm = dsm + KP;
-  double* red = esm + KP;
-  double2* rsm = reinterpret_cast<double2*>(red + 2);
-  int* pidx = reinterpret_cast<int*>(rsm + NR);
-  int* ism = pidx + KP;
+  double* lw = vv + KP;
+  double* red = lw + KP;
   Grp<KP> g{(int)threadIdx.x, 1, red};
-  const int row = g.tid;
+  const int tid = g.tid;
   const int slot = slot0 + sl;
   const int task = a.ids[slot];
   const int k = a.ksz[task];
   const int64_t off = a.off[task];
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
-  double* Zr = Z + row * LD;
-  for (int j = 0; j < KP; ++j) Zr[j] = (j == row) ? 1.0 : 0.0;
-  const int nrot = a.td.rcount[slot];
-  if (nrot >= 0) {
-    // replay the QL rotations on this row; inside one QL sweep the pairs descend
-    // (i+1, i+2), (i, i+1), ..., so z_i stays in a register ("carry")
-    const double2* rot = a.td.rot + a.td.roff[slot];
-    const int16_t* ridx = a.td.ridx + a.td.roff[slot];
-    double carry = 0.0;
-    int cur = -2;  // column held in `carry`
-    for (int t0 = 0; t0 < nrot; t0 += NR) {
-      const int nt = min(NR, nrot - t0);
-      g.sync();
-      for (int u = row; u < nt; u += KP) {
-        rsm[u] = rot[t0 + u];
-        ism[u] = ridx[t0 + u];
-      }
-      g.sync();
-      if (row < k) {
-        for (int u = 0; u < nt; ++u) {
-          const double2 cs = rsm[u];
-          const int i = ism[u];
-          double zi1;
-          if (i + 1 == cur) {
-            zi1 = carry;
-          } else {
-            if (cur >= 0) Zr[cur] = carry;
-            zi1 = Zr[i + 1];
-          }
-          const double zi = Zr[i];
-          Zr[i + 1] = fma(cs.y, zi, cs.x * zi1);
-          carry = fma(cs.x, zi, -cs.y * zi1);
-          cur = i;
-        }
-      }
+  int nsel = (int)H.hdr()[0];
+  int side = (int)H.hdr()[1];
+  const bool fallback = a.td.rcount[slot] < 0 || a.td.force_fallback;
+  if (!fallback) {
+    const double* Zo = a.td.zbuf + a.td.zoff[slot];
+    for (int e = tid; e < nsel * k; e += KP) {
+      const int j = e / k, i = e - j * k;
+      Z[i * LD + j] = Zo[(size_t)j * KP + i];
     }
-    if (row < k && cur >= 0) Zr[cur] = carry;
-    if (row < k) dsm[row] = H.lam()[row];
+    if (tid < nsel) lw[tid] = H.lw()[tid];
   } else {
-    // fallback: the QL chain inline; every thread runs the same chain on a
-    // private copy of (d, e) (identical arithmetic, so identical rotations) and
-    // rotates its own row
+    // QL with eigenvectors, every thread running the same chain on a private copy
+    // of (d, e) (identical arithmetic, identical rotations) and rotating its own
+    // row of Z; then the lambda > 0 columns, compacted in place
+    const int row = tid;
+    double* Zr = Z + row * LD;
+    for (int j = 0; j < KP; ++j) Zr[j] = (j == row) ? 1.0 : 0.0;
     double dl[KP], el[KP];
     for (int i = 0; i < k; ++i) {
       dl[i] = H.d()[i];
@@ -386,35 +516,29 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
         Zr[i] = fma(c, zi, -s * zi1);
       }
     });
-    if (row < k) dsm[row] = dl[row];
     if (!ok && row == 0 && a.capped) atomicAdd(a.capped, 1ull);
-  }
-  g.sync();
-  // positive eigenvalues, compacted in index order (deterministic)
-  int npos = 0;
-  for (int t0 = 0; t0 < k; t0 += 32) {
-    const int t = t0 + (row & 31);
-    const double l = t < k ? dsm[t] : 0.0;
-    const bool pos = l > 0.0;
-    const unsigned bal = __ballot_sync(0xffffffffu, pos);
-    if (row < 32 && pos) {
-      const int at = npos + __popc(bal & ((1u << row) - 1u));
-      pidx[at] = t;
-      lp[at] = l;
+    g.sync();
+    int n = 0;
+    for (int t = 0; t < k; ++t) {
+      if (dl[t] > 0.0) {
+        if (row < k && n != t) Zr[n] = Zr[t];
+        if (row == 0) lw[n] = dl[t];
+        ++n;
+      }
     }
-    npos += __popc(bal);
+    nsel = n;
+    side = 0;
   }
   g.sync();
-  // back-transform the positive eigenvectors: V = H_0 H_1 ... H_{k-3} Z
+  // back-transform the selected eigenvectors: V = H_0 H_1 ... H_{k-3} Z
   int64_t vpos = k >= 2 ? (int64_t)(k - 1) * (k - 2) / 2 : 0;
   for (int j = k - 3; j >= 0; --j) {
     vpos -= k - j - 2;
     const double tau = H.tau()[j];
     if (tau == 0.0) continue;
-    if (row >= j + 1 && row < k) vv[row] = (row == j + 1) ? 1.0 : H.v()[vpos + (row - j - 2)];
+    if (tid >= j + 1 && tid < k) vv[tid] = (tid == j + 1) ? 1.0 : H.v()[vpos + (tid - j - 2)];
     g.sync();
-    for (int u = row; u < npos; u += KP) {
-      const int c = pidx[u];
+    for (int c = tid; c < nsel; c += KP) {
       double y0 = 0.0, y1 = 0.0;
       int i = j + 1;
       for (; i + 1 < k; i += 2) {
@@ -427,20 +551,18 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     }
     g.sync();
   }
-  // P_+ = sum_{lambda_t > 0} lambda_t v_t v_t^T, packed upper, mode epilogue
+  // P_+ = [A] + sum_t w_t v_t v_t^T, packed upper, mode epilogue
   const int ns = k * (k + 1) / 2;
   double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-  for (int e = row; e < ns; e += KP) {
+  for (int e = tid; e < ns; e += KP) {
     int r, c;
     packed_rc(e, r, c);
     const double* Zrr = Z + r * LD;
     const double* Zc = Z + c * LD;
     double acc = 0.0;
-    for (int u = 0; u < npos; ++u) {
-      const int t = pidx[u];
-      acc = fma(lp[u] * Zrr[t], Zc[t], acc);
-    }
+    for (int u = 0; u < nsel; ++u) acc = fma(lw[u] * Zrr[u], Zc[u], acc);
     const int64_t pe = off + e;
+    if (side == 1) acc += input_value<MODE>(a, pe, r, c);
     if constexpr (MODE == PM_BATCH) {
       a.out[pe] = acc;
     } else if constexpr (MODE == PM_PRIMAL) {
@@ -460,7 +582,7 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     p0 = g.sum(p0);
     p1 = g.sum(p1);
     p2 = g.sum(p2);
-    if (row == 0) {
+    if (tid == 0) {
       a.part[3 * (int64_t)task + 0] = p0;
       a.part[3 * (int64_t)task + 1] = p1;
       a.part[3 * (int64_t)task + 2] = p2;
@@ -471,8 +593,10 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
 template <int KP, int MODE>
 void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
   using TL = TridiagLayout<KP>;
+  using IL = InvLayout<KP>;
   k_trd_tridiag<KP, MODE><<<(n + TL::NMAT - 1) / TL::NMAT, 128, TL::NMAT * TL::PER * sizeof(double), s>>>(a, c0, n);
   k_trd_ql<KP><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
+  k_trd_invit<KP><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
   k_trd_apply<KP, MODE><<<n, KP, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
 }
 
@@ -483,6 +607,7 @@ void set_attrs() {
                        (int)(TL::NMAT * TL::PER * sizeof(double)));
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(2 * KP * QL_T * sizeof(double)));
+  cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)InvLayout<KP>::bytes());
   cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)ApplyLayout<KP>::bytes());
 }
@@ -498,16 +623,9 @@ void psd_trd_init_attributes() {
   set_attrs<64, PM_DUAL>();
 }
 
-// SDP_TRD_ROTCAP overrides the capacity (tests force the inline-QL fallback with it)
-int64_t trd_rot_cap(int k) {
-  const char* e = getenv("SDP_TRD_ROTCAP");
-  if (e && *e) return std::max<int64_t>(0, atoll(e));
-  return std::max<int64_t>(64, (int64_t)3 * k * k / 2);
-}
-
 int64_t trd_hsize(int kp, int k) {
   const int64_t v = k >= 2 ? (int64_t)(k - 1) * (k - 2) / 2 : 0;
-  return (4 * (int64_t)kp + v + 1) & ~(int64_t)1;
+  return (6 * (int64_t)kp + 4 + v + 1) & ~(int64_t)1;
 }
 
 void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t s) {

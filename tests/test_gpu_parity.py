@@ -432,8 +432,9 @@ def test_trd_tier_admm_subprocess():
 
 
 def test_trd_tier_inline_ql_fallback_subprocess():
-    """SDP_TRD_ROTCAP=0: no rotation list fits, every matrix of the QL tier takes
-    the inline-QL fallback of the apply kernel; results still match the oracle."""
+    """SDP_TRD_FORCE_FALLBACK=1: every matrix of the QL tier takes the checked
+    fallback (QL with eigenvector accumulation inside the apply kernel); results
+    still match the oracle."""
     import subprocess
     import sys
     code = (
@@ -447,6 +448,6 @@ def test_trd_tier_inline_ql_fallback_subprocess():
         "want = opsd.project_psd_packed_batch(ks, vals)\n"
         "e = np.linalg.norm(out - want) / np.linalg.norm(want)\n"
         "print(e); assert e <= 1e-12, e\n" % ROOT)
-    env = dict(os.environ, SDP_TRD_ROTCAP="0")
+    env = dict(os.environ, SDP_TRD_FORCE_FALLBACK="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
