@@ -153,7 +153,7 @@ struct sdp_handle_s {
   double *a_val = nullptr, *at_val = nullptr;
   int s_diag = 0;
   double* sdiag = nullptr;
-  double *W = nullptr, *WT = nullptr;
+  double *W = nullptr, *WT = nullptr, *Sinv = nullptr;
   double* gemv_part = nullptr;
   int chunk = 8192, nchunks = 0;
   // residuals
@@ -412,13 +412,11 @@ void enqueue_kkt(sdp_handle h, cudaStream_t s) {
   phase(0, s);
   const bool shard = h->world > 1;
   if (h->a_dense) {
+    // partials only: y = S^-1 (sum partials - r2) is one kernel below (single rank)
     launch_gemv_dense(h->A, h->lda, h->m, h->rD, h->chunk, h->gemv_part, h->done, s);
     phase(1, s);
     if (shard)  // partial u over owned columns
       launch_reduce_u(f, h->gemv_part, h->nchunks, h->m, nullptr, h->rho, h->u, nullptr, nullptr, h->done, s);
-    else
-      launch_reduce_u(f, h->gemv_part, h->nchunks, h->m, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr, ydst,
-                      h->done, s);
   } else {
     if (shard)
       launch_gemv_csr(f, h->a_rp, h->a_ci, h->a_val, h->m, h->rD, nullptr, h->rho, h->u, nullptr, nullptr, h->done,
@@ -433,9 +431,11 @@ void enqueue_kkt(sdp_handle h, cudaStream_t s) {
     nccl_allreduce_sum(h->comm, h->u, (size_t)h->m, s);
     launch_reduce_u(f, h->u, 1, h->m, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr, ydst, h->done, s);
   }
-  if (!h->s_diag) {
-    launch_trmv(1, h->W, h->m, h->u, h->t, h->done, s);   // t = L^-1 u
-    launch_trmv(0, h->WT, h->m, h->t, h->y, h->done, s);  // y = L^-T t
+  if (!h->s_diag) {  // y = S^-1 u = W^T W u
+    if (h->a_dense && !shard)
+      launch_symv(f, h->Sinv, h->m, h->gemv_part, h->nchunks, h->b, h->rho, nullptr, h->y, h->done, s);
+    else
+      launch_symv(f, h->Sinv, h->m, nullptr, 0, nullptr, h->rho, h->u, h->y, h->done, s);
   }
   phase(2, s);
   if (h->a_dense)
@@ -514,8 +514,9 @@ int launches_per_iter(sdp_handle h) {
     }
   }
   n += 1;                                       // scatter
-  n += h->a_dense ? 3 : 2;                      // gemv (+ reduce) + gemvT
-  n += h->s_diag ? 0 : 2;                       // triangular solves
+  n += 2;                                       // gemv + gemvT (sparse A: gemv_csr forms u itself)
+  n += h->s_diag ? 0 : 1;                       // y = S^-1 u (dense A: sums the gemv partials itself)
+  if (h->world > 1 && h->a_dense) n += 1;       // partial u of the rank before the all-reduce
   n += (h->form == SDP_FORM_DUAL) ? 1 : 0;      // dual update
   n += 1;                                       // finalize
   if (h->world > 1) n += 2 + (h->nshared > 0 ? 1 : 0);  // second reduce_u, finalize phase 2, fixup
@@ -845,7 +846,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
       launch_mask_cols(h->A, h->lda, m, h->own, nullptr);
       SDP_CUDA_TRY(cudaGetLastError());
     }
-    h->chunk = 8192;
+    h->chunk = 32768;
     h->nchunks = (int)((h->lda + h->chunk - 1) / h->chunk);
     h->gemv_part = al.zeros<double>((size_t)h->nchunks * m);
     double* dS = al.get<double>((size_t)m * m);
@@ -947,6 +948,19 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
       for (int j = 0; j < m; ++j) Wl[(size_t)i * m + j] = Wt[(size_t)j * m + i];
     h->W = al.upload(Wl);
     h->WT = al.upload(Wt);
+    // cached S^-1 = W^T W (one dense mat-vec per iteration instead of two dependent
+    // triangular ones; cond(S) ~ 2 on the block-arrow configs), formed by the SYRK kernel
+    std::vector<double> ones(m, 1.0);
+    double* d1 = al.upload(ones);
+    h->Sinv = al.get<double>((size_t)m * m);
+    launch_syrk_dense(h->WT, m, m, d1, h->Sinv, nullptr);
+    SDP_CUDA_TRY(cudaGetLastError());
+    SDP_CUDA_TRY(cudaDeviceSynchronize());
+    al.release(d1);
+    al.release(h->W);
+    al.release(h->WT);
+    h->W = h->WT = nullptr;
+    symv_init_attributes(m);
   }
 
   // ---- 6. residual buffers, state, graph

@@ -163,6 +163,70 @@ __global__ void __launch_bounds__(256) k_gemv_dense(const double* __restrict__ A
   }
 }
 
+// y = S^-1 u with the cached dense S^-1 = W^T W (W = L^-1, S = L L^T),
+// one warp per row, 8 independent 16-byte loads in flight per lane.  With
+// `part` the kernel first forms u = sum_c part[c] - r2 (r2 = b primal, -b/rho
+// dual) itself in shared memory (every CTA, fixed chunk order), so the GEMV
+// partials need no separate reduction launch.
+constexpr int SYMV_T = 512;
+template <int FORM>
+__global__ void __launch_bounds__(SYMV_T) k_symv(const double* __restrict__ Si, int m, const double* __restrict__ part,
+                                                  int nchunks, const double* __restrict__ b, double rho,
+                                                  const double* __restrict__ u, double* __restrict__ y,
+                                                  const int* done) {
+  if (done && *done) return;
+  extern __shared__ double us[];
+  for (int j = threadIdx.x; j < m; j += SYMV_T) {
+    double v = 0.0;
+    if (part) {
+      // 8 independent loads in flight, summed in chunk order
+      for (int c0 = 0; c0 < nchunks; c0 += 8) {
+        double t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) t[q] = (c0 + q < nchunks) ? part[(int64_t)(c0 + q) * m + j] : 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v += t[q];
+      }
+      v = (FORM == 0) ? v - b[j] : v + b[j] / rho;
+    } else {
+      v = u[j];
+    }
+    us[j] = v;
+  }
+  __syncthreads();
+  const int row = blockIdx.x * (SYMV_T / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= m) return;
+  const double* Sr = Si + (int64_t)row * m;
+  double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if ((m & 1) == 0) {
+    const double2* S2 = reinterpret_cast<const double2*>(Sr);
+    const int h = m / 2;
+    int j = lane;
+    for (; j + 7 * 32 < h; j += 8 * 32) {
+      double2 a[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = __ldcs(S2 + j + 32 * q);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int c = 2 * (j + 32 * q);
+        s[q] = fma(a[q].x, us[c], s[q]);
+        s[q] = fma(a[q].y, us[c + 1], s[q]);
+      }
+    }
+    for (; j < h; j += 32) {
+      const double2 a0 = __ldcs(S2 + j);
+      s[0] = fma(a0.x, us[2 * j], s[0]);
+      s[0] = fma(a0.y, us[2 * j + 1], s[0]);
+    }
+  } else {
+    for (int j = lane; j < m; j += 32) s[0] = fma(Sr[j], us[j], s[0]);
+  }
+  double t = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+  t = warp_sum(t);
+  if (lane == 0) y[row] = t;
+}
+
 // u_i = sum_chunks part[.][i] - r2_i   (r2 = b primal, -b/rho dual);
 // with a diagonal S the KKT solve is elementwise: y_i = u_i / S_ii.
 template <int FORM>
@@ -613,6 +677,22 @@ void launch_gemv_dense(const double* A, int64_t lda, int m, const double* v, int
   const int nch = (int)((lda + chunk - 1) / chunk);
   dim3 grid((m + 3) / 4, nch);
   k_gemv_dense<4><<<grid, 256, 0, s>>>(A, lda, m, v, chunk, part, done);
+}
+
+void launch_symv(int form, const double* Si, int m, const double* part, int nchunks, const double* b, double rho,
+                 const double* u, double* y, const int* done, cudaStream_t s) {
+  const size_t sm = (size_t)m * sizeof(double);
+  const int rows = SYMV_T / 32;
+  if (form == 0)
+    k_symv<0><<<(m + rows - 1) / rows, SYMV_T, sm, s>>>(Si, m, part, nchunks, b, rho, u, y, done);
+  else
+    k_symv<1><<<(m + rows - 1) / rows, SYMV_T, sm, s>>>(Si, m, part, nchunks, b, rho, u, y, done);
+}
+
+void symv_init_attributes(int m) {
+  const int sm = (int)(m * sizeof(double));
+  cudaFuncSetAttribute(k_symv<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+  cudaFuncSetAttribute(k_symv<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
 }
 
 void launch_reduce_u(int form, const double* part, int nchunks, int m, const double* b, double rho, double* u,

@@ -53,6 +53,10 @@ void launch_scatter(int form, const ScatterArgs& a, cudaStream_t s);
 int scatter_blocks(int N, int n_long);
 void launch_gemv_dense(const double* A, int64_t lda, int m, const double* v, int chunk, double* part,
                        const int* done, cudaStream_t s);
+// y = S^-1 u; with part != NULL, u = sum of the nchunks GEMV partials - r2 (formed in the kernel)
+void launch_symv(int form, const double* Si, int m, const double* part, int nchunks, const double* b, double rho,
+                 const double* u, double* y, const int* done, cudaStream_t s);
+void symv_init_attributes(int m);
 void launch_reduce_u(int form, const double* part, int nchunks, int m, const double* b, double rho, double* u,
                      const double* sdiag, double* y, const int* done, cudaStream_t s);
 void launch_trmv(int lower, const double* M, int m, const double* in, double* out, const int* done, cudaStream_t s);
