@@ -14,7 +14,8 @@
 //     pairing the blocks into P = nb/2 disjoint 32-index pairs.
 //   * INNER phase: one warp per (matrix, pair) runs one parallel-ordered Jacobi
 //     sweep (31 steps of 16 rotations, Golub-Van Loan sym.schur2) on the 32x32
-//     diagonal sub-block and accumulates the 32x32 rotation Q.
+//     diagonal sub-block, in registers (jacobi_warp.cuh), and accumulates the
+//     32x32 rotation Q.
 //   * TILE phase: one warp per 32x32 tile applies A[P1,P2] <- Q1^T A[P1,P2] Q2
 //     (upper tiles, mirrored) and V[:,P2] <- V[:,P2] Q2, both as DMMA
 //     (mma.sync m8n8k4 f64) products from shared memory.
@@ -31,6 +32,7 @@
 
 #include "internal.h"
 #include "jacobi_rot.cuh"
+#include "jacobi_warp.cuh"
 
 namespace sdp {
 
@@ -48,8 +50,7 @@ constexpr double kSqrt2 = 1.41421356237309504880;
 struct WarpSmem {
   double S[TILE];
   double Q[TILE];
-  double rc[16], rs[16];
-  int rp[16], rq[16];
+  double rc[32];  // 16 rotations (c, s) of a Jacobi step
 };
 constexpr size_t kSmemBytes = NW * sizeof(WarpSmem);
 
@@ -238,20 +239,11 @@ __device__ __forceinline__ void stage_q(double* S, const double* Q, int lane) {
   }
 }
 
-constexpr int LDQ = 33;  // inner phase: row-per-lane Q updates are conflict-free at stride 33
-
 template <int MODE>
 __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
   if (a.done && *a.done) return;
   const GiantDev& d = a.gd;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ int blk[136];  // pair-block table (i << 8 | j), i <= j < 16
-  for (int b = threadIdx.x; b < 136; b += NT) {
-    int i, j;
-    packed_rc(b, i, j);
-    blk[b] = (i << 8) | j;
-  }
-  __syncthreads();
   WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[threadIdx.x >> 5];
   const int lane = threadIdx.x & 31;
   const int gw = blockIdx.x * NW + (threadIdx.x >> 5);  // global warp
@@ -416,68 +408,22 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
         const double* A = d.ws + d.wsoff[g];
         __syncwarp();
         stage_tile(sm.S, A, kp, I * 16, J * 16, I * 16, J * 16, lane);
-        for (int e = lane; e < 1024; e += 32) {
-          const int i = e >> 5, j = e & 31;
-          sm.Q[i * LDQ + j] = (i == j) ? 1.0 : 0.0;
-        }
         cp_wait();
         __syncwarp();
-        for (int t = 0; t < 31; ++t) {
-          if (lane < 16) {
-            int p, q;
-            circle(32, t, lane, p, q);
-            const JRot jr = jacobi_rotation(sm.S[p * LDS + p], sm.S[q * LDS + q], sm.S[min(p, q) * LDS + max(p, q)]);
-            sm.rp[lane] = p;
-            sm.rq[lane] = q;
-            sm.rc[lane] = jr.c;
-            sm.rs[lane] = jr.s;
-          }
-          __syncwarp();
-          // S <- J^T S J on the 2x2 blocks (i <= j) of the pair partition, upper triangle kept
+        // one round-robin sweep (31 steps of 16 rotations) in registers: lane j
+        // holds column j of the block and row j of Q (jacobi_warp.cuh)
+        double av[32], vv[32];
 #pragma unroll
-          for (int u = 0; u < 5; ++u) {
-            const int b = lane + 32 * u;
-            if (b >= 136) break;
-            const int ij = blk[b];
-            const int i = ij >> 8, j = ij & 0xff;
-            const int p1 = sm.rp[i], q1 = sm.rq[i];
-            const double c1 = sm.rc[i], s1 = sm.rs[i];
-            if (i == j) {
-              const int ipq = min(p1, q1) * LDS + max(p1, q1);
-              const double app = sm.S[p1 * LDS + p1], aqq = sm.S[q1 * LDS + q1], apq = sm.S[ipq];
-              const double r00 = c1 * app - s1 * apq, r01 = c1 * apq - s1 * aqq;
-              const double r10 = s1 * app + c1 * apq, r11 = s1 * apq + c1 * aqq;
-              sm.S[p1 * LDS + p1] = c1 * r00 - s1 * r01;
-              sm.S[q1 * LDS + q1] = s1 * r10 + c1 * r11;
-              sm.S[ipq] = 0.5 * ((s1 * r00 + c1 * r01) + (c1 * r10 - s1 * r11));
-            } else {
-              const int p2 = sm.rp[j], q2 = sm.rq[j];
-              const double c2 = sm.rc[j], s2 = sm.rs[j];
-              const int i00 = min(p1, p2) * LDS + max(p1, p2), i01 = min(p1, q2) * LDS + max(p1, q2);
-              const int i10 = min(q1, p2) * LDS + max(q1, p2), i11 = min(q1, q2) * LDS + max(q1, q2);
-              const double b00 = sm.S[i00], b01 = sm.S[i01], b10 = sm.S[i10], b11 = sm.S[i11];
-              const double r00 = c1 * b00 - s1 * b10, r01 = c1 * b01 - s1 * b11;
-              const double r10 = s1 * b00 + c1 * b10, r11 = s1 * b01 + c1 * b11;
-              sm.S[i00] = c2 * r00 - s2 * r01;
-              sm.S[i01] = s2 * r00 + c2 * r01;
-              sm.S[i10] = c2 * r10 - s2 * r11;
-              sm.S[i11] = s2 * r10 + c2 * r11;
-            }
-          }
-          // Q <- Q J (row `lane`)
-          double* Qr = sm.Q + lane * LDQ;
-#pragma unroll 8
-          for (int i = 0; i < 16; ++i) {
-            const int p = sm.rp[i], q = sm.rq[i];
-            const double cs = sm.rc[i], sn = sm.rs[i];
-            const double vp = Qr[p], vq = Qr[q];
-            Qr[p] = cs * vp - sn * vq;
-            Qr[q] = sn * vp + cs * vq;
-          }
-          __syncwarp();
+        for (int r = 0; r < 32; ++r) {
+          av[r] = sm.S[r * LDS + lane];
+          vv[r] = (r == lane) ? 1.0 : 0.0;
         }
-        double* Qg = d.qbuf + d.qoff[g] + (size_t)pi * 1024;
-        for (int e = lane; e < 1024; e += 32) Qg[e] = sm.Q[(e >> 5) * LDQ + (e & 31)];
+        double2* cs = reinterpret_cast<double2*>(sm.rc);
+#pragma unroll 1
+        for (int t = 0; t < 31; ++t) wj::step(av, vv, cs, lane);
+        double2* Qg = reinterpret_cast<double2*>(d.qbuf + d.qoff[g] + (size_t)pi * 1024 + lane * 32);
+#pragma unroll
+        for (int c = 0; c < 16; ++c) Qg[c] = make_double2(vv[2 * c], vv[2 * c + 1]);
       }
       grid_sync(d.bar, gridDim.x);
       clk.mark(3);
