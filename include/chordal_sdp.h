@@ -92,6 +92,13 @@ typedef struct {
   int32_t use_graph;         /* 1 (default): replay one captured CUDA graph per iteration */
   int32_t rank, world;       /* clique sharding over `world` ranks (one GPU each); default 0, 1 */
   const void* nccl_id;       /* world > 1: 128-byte id from sdp_nccl_unique_id on rank 0, same on all ranks */
+  /* sdp_solve residual balancing (Boyd et al. 2011 Sec. 3.4.1, cited for the residuals at P:263-265):
+   * after every check_every-th iteration that did not stop, rho <- adapt_tau * rho if
+   * eps_p > adapt_mu * eps_d, rho <- rho / adapt_tau if eps_d > adapt_mu * eps_p.  The KKT
+   * matrix is rho-free, so nothing is refactorised.  Default off (0), mu 10, tau 2. */
+  int32_t adapt_rho;
+  double adapt_mu;
+  double adapt_tau;
 } sdp_options;
 
 typedef struct {
@@ -106,6 +113,7 @@ typedef struct {
   int64_t jacobi_capped;     /* count of projections that hit the sweep cap          */
   int32_t launches_per_iter; /* kernels launched per ADMM iteration                   */
   int64_t jacobi_sweeps;     /* total Jacobi sweeps over all projections since reset  */
+  double rho;                /* penalty currently in force (changes with adapt_rho / sdp_set_rho) */
 } sdp_info;
 
 typedef struct sdp_handle_s* sdp_handle;

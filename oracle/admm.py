@@ -53,6 +53,7 @@ class State:
     eps_d: float = float("inf")
     objective: float = float("nan")
     history: list = field(default_factory=list)
+    rho: float = float("nan")  # set by solve(): the penalty in force at the end
 
 
 def zero_state(dec: Decomposition) -> State:
@@ -124,15 +125,35 @@ def step(dec: Decomposition, st: State, rho: float, form: str, iters: int, liter
     return st
 
 
+def adapt_rho(rho: float, eps_p: float, eps_d: float, mu: float = 10.0, tau: float = 2.0) -> float:
+    """Residual balancing (Boyd et al. 2011 Sec. 3.4.1, the reference the paper cites
+    for its residuals): rho <- tau rho if the primal
+    residual exceeds mu times the dual one, rho <- rho / tau in the opposite case.
+    The KKT matrix of E:OptCondMinYPrimal / E:OptCondMinYDual is rho-free,
+    so nothing is refactorised, and the multipliers lambda_k are kept unscaled."""
+    if eps_p > mu * eps_d:
+        return rho * tau
+    if eps_d > mu * eps_p:
+        return rho / tau
+    return rho
+
+
 def solve(dec: Decomposition, rho: float, form: str, tol: float, max_iter: int,
-          st: State = None, literal=False):
+          st: State = None, literal=False, adapt=None):
     """Iterate until max(eps_p, eps_d) < tol (Algorithm 1/2 line 3) or max_iter.
-    Returns (state, status) with status "solved" or "max_iter"."""
+    adapt = (mu, tau, every): after every `every`-th iteration that did not stop,
+    rho is updated by adapt_rho from that iteration's residuals.
+    Returns (state, status) with status "solved" or "max_iter"; the final rho is
+    st.rho."""
     st = zero_state(dec) if st is None else st
     while st.it < max_iter:
         st = step(dec, st, rho, form, 1, literal=literal)
         if max(st.eps_p, st.eps_d) < tol:
+            st.rho = rho
             return st, "solved"
+        if adapt is not None and st.it % adapt[2] == 0:
+            rho = adapt_rho(rho, st.eps_p, st.eps_d, adapt[0], adapt[1])
+    st.rho = rho
     return st, "max_iter"
 
 

@@ -64,7 +64,8 @@ class sdp_problem(C.Structure):
 class sdp_options(C.Structure):
     _fields_ = [("form", C.c_int32), ("rho", C.c_double), ("device", C.c_int32), ("stream", C.c_void_p),
                 ("check_every", C.c_int32), ("use_graph", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
-                ("nccl_id", C.c_void_p)]
+                ("nccl_id", C.c_void_p), ("adapt_rho", C.c_int32), ("adapt_mu", C.c_double),
+                ("adapt_tau", C.c_double)]
 
 
 class sdp_info(C.Structure):
@@ -72,7 +73,7 @@ class sdp_info(C.Structure):
                 ("setup_s", C.c_double), ("n", C.c_int64), ("m", C.c_int64), ("N", C.c_int64), ("p", C.c_int64),
                 ("kmin", C.c_int64), ("kmax", C.c_int64), ("stot", C.c_int64), ("form", C.c_int32),
                 ("s_diagonal", C.c_int32), ("jacobi_capped", C.c_int64),
-                ("launches_per_iter", C.c_int32), ("jacobi_sweeps", C.c_int64)]
+                ("launches_per_iter", C.c_int32), ("jacobi_sweeps", C.c_int64), ("rho", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -192,7 +193,7 @@ class Solver:
     c_val, b, a_fmt ("coo" | "dense"), a_con, a_row, a_col, a_val."""
 
     def __init__(self, prob, form="primal", rho=1.0, device=0, stream=None, use_graph=True, check_every=10,
-                 rank=0, world=1, nccl_id=None):
+                 rank=0, world=1, nccl_id=None, adapt_rho=False, adapt_mu=10.0, adapt_tau=2.0):
         self.form = form
         keep = []
 
@@ -221,6 +222,8 @@ class Solver:
         O.stream = _stream_ptr(stream)
         O.use_graph = int(bool(use_graph))
         O.check_every = int(check_every)
+        O.adapt_rho = 1 if adapt_rho else 0
+        O.adapt_mu, O.adapt_tau = float(adapt_mu), float(adapt_tau)
         O.rank, O.world = int(rank), int(world)
         self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         O.nccl_id = C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None

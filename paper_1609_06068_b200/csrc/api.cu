@@ -125,6 +125,8 @@ struct sdp_handle_s {
   cudaStream_t stream = nullptr, cap_stream = nullptr;
   bool own_stream = false;
   int check_every = 10, use_graph = 1;
+  int adapt = 0;
+  double adapt_mu = 10.0, adapt_tau = 2.0;
   double setup_s = 0;
   int64_t fill_edges = 0;
   // host copies
@@ -650,6 +652,9 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->device = opt.device;
   h->check_every = opt.check_every > 0 ? opt.check_every : 10;
   h->use_graph = opt.use_graph;
+  h->adapt = opt.adapt_rho ? 1 : 0;
+  h->adapt_mu = opt.adapt_mu > 1.0 ? opt.adapt_mu : 10.0;
+  h->adapt_tau = opt.adapt_tau > 1.0 ? opt.adapt_tau : 2.0;
   h->fill_edges = cr.fill_edges;
   h->stream = (cudaStream_t)opt.stream;  // NULL = the legacy default stream, as in the CUDA runtime
   h->own_stream = false;
@@ -1034,6 +1039,7 @@ void fill_info(sdp_handle h, sdp_info* info) {
   info->jacobi_capped = (int64_t)cap;
   info->launches_per_iter = launches_per_iter(h);
   info->jacobi_sweeps = (int64_t)sw;
+  info->rho = h->rho;
 }
 
 void launch_iterations(sdp_handle h, int32_t iters) {
@@ -1062,6 +1068,9 @@ void sdp_default_options(sdp_options* opt) {
   opt->rank = 0;
   opt->world = 1;
   opt->nccl_id = nullptr;
+  opt->adapt_rho = 0;
+  opt->adapt_mu = 10.0;
+  opt->adapt_tau = 2.0;
 }
 
 int sdp_setup(const sdp_problem* prob, const sdp_options* opt, sdp_handle* out) {
@@ -1084,6 +1093,25 @@ int sdp_step(sdp_handle h, int32_t iters) {
   });
 }
 
+namespace {
+// Change rho between iterations (the KKT factor is rho-free; lambda_k is
+// kept unscaled).  The primal right-hand side r1 depends on rho and is rebuilt
+// from the current x_k, lambda_k (sprev is unchanged); the graph is recaptured.
+void apply_rho(sdp_handle h, double rho) {
+  SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  h->rho = rho;
+  if (h->form == SDP_FORM_PRIMAL) {
+    int saved = 0;
+    SDP_CUDA_TRY(cudaMemcpy(&saved, h->done, sizeof(int), cudaMemcpyDeviceToHost));
+    SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
+    enqueue_scatter(h, h->stream);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    SDP_CUDA_TRY(cudaMemcpy(h->done, &saved, sizeof(int), cudaMemcpyHostToDevice));
+  }
+  rebuild_graph(h);
+}
+}  // namespace
+
 int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info) {
   return guarded([&] {
     if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
@@ -1096,13 +1124,25 @@ int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info) {
     int done = 0, num = 0;
     SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
     while (it < max_iters) {
-      const int chunk = (int)std::min<long long>(h->check_every, max_iters - it);
+      // chunks end on multiples of check_every (the adaptation points of adapt_rho)
+      const int chunk = (int)std::min<long long>(h->check_every - it % h->check_every, max_iters - it);
       launch_iterations(h, chunk);
       SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
       SDP_CUDA_TRY(cudaMemcpy(&done, h->done, sizeof(int), cudaMemcpyDeviceToHost));
       SDP_CUDA_TRY(cudaMemcpy(&num, h->numerical, sizeof(int), cudaMemcpyDeviceToHost));
       SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
       if (num || done) break;
+      if (h->adapt && it % h->check_every == 0) {
+        // residual balancing on the last iteration's eps_p, eps_d (same rule as oracle.admm.adapt_rho)
+        double res[2];
+        SDP_CUDA_TRY(cudaMemcpy(res, h->res, 2 * sizeof(double), cudaMemcpyDeviceToHost));
+        double rho = h->rho;
+        if (res[0] > h->adapt_mu * res[1])
+          rho = h->rho * h->adapt_tau;
+        else if (res[1] > h->adapt_mu * res[0])
+          rho = h->rho / h->adapt_tau;
+        if (rho != h->rho) apply_rho(h, rho);
+      }
     }
     const double neg = -1.0;
     SDP_CUDA_TRY(cudaMemcpy(h->tol, &neg, sizeof(double), cudaMemcpyHostToDevice));
@@ -1127,15 +1167,7 @@ int sdp_set_rho(sdp_handle h, double rho) {
     if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
     if (!(rho > 0) || !std::isfinite(rho)) throw Error{SDP_E_INVALID_ARG, "rho must be positive"};
     DeviceGuard dg(h->device);
-    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    h->rho = rho;
-    if (h->form == SDP_FORM_PRIMAL) {
-      // r1 depends on rho: recompute it from the current x_k, lambda_k (sprev is unchanged)
-      SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
-      enqueue_scatter(h, h->stream);
-      SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    }
-    rebuild_graph(h);
+    apply_rho(h, rho);
     return SDP_OK;
   });
 }

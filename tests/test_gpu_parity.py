@@ -451,3 +451,22 @@ def test_trd_tier_inline_ql_fallback_subprocess():
     env = dict(os.environ, SDP_TRD_FORCE_FALLBACK="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+# ------------------------------------------------------------------ adaptive rho
+
+@pytest.mark.parametrize("form,rho", [("primal", 1.0), ("dual", 1.0), ("primal", 50.0)])
+def test_solve_adaptive_rho(lib, gen, form, rho):
+    """Residual balancing inside sdp_solve (every check_every = 10 iterations,
+    mu = 10, tau = 2) against the oracle's same rule: same stop iteration, same
+    final rho, objective within 1e-6."""
+    prob = gen.config(1)
+    dec = dc.decompose(prob)
+    st, status = admm.solve(dec, rho, form, 1e-4, 5000, adapt=(10.0, 2.0, 10))
+    s = lib.Solver(prob, form=form, rho=rho, check_every=10, adapt_rho=True)
+    gstatus, info = s.solve(5000, 1e-4)
+    assert gstatus == status == "solved"
+    assert info["iters"] == st.it
+    assert info["rho"] == st.rho
+    assert abs(info["objective"] - st.objective) <= 1e-6 * abs(st.objective)
+    s.close()

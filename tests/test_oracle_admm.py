@@ -186,3 +186,26 @@ def test_cfg0_converges_both_forms(gen):
     d, sd = admm.solve(dec, 1.0, "dual", 1e-6, 5000)
     assert sp == sd == "solved"
     assert abs(p.objective - d.objective) <= 1e-4 * abs(p.objective)
+
+
+def test_adapt_rho_rule_spec_examples():
+    """Residual balancing rule (SPEC S:318-326 examples): balanced residuals leave
+    rho unchanged; ||r|| = 100 ||s|| with mu = 10, tau = 2 doubles it; the mirror
+    case halves it."""
+    assert admm.adapt_rho(1.0, 1e-3, 1e-3) == 1.0
+    assert admm.adapt_rho(1.0, 5e-3, 1e-3) == 1.0
+    assert admm.adapt_rho(1.0, 100.0, 1.0, mu=10, tau=2) == 2.0
+    assert admm.adapt_rho(1.0, 1.0, 100.0, mu=10, tau=2) == 0.5
+
+
+def test_adaptive_rho_reaches_same_optimum(gen):
+    """Adaptation changes iteration counts, not the solution: the adaptive solve
+    of the tiny block-arrow problem reaches the closed/dense objective within the
+    stopping tolerance, from a badly scaled rho (same objective within 1e-3)."""
+    prob = gen.block_arrow(3, 3, 2, 6, seed=1)
+    dec = dc.decompose(prob)
+    fixed, s1 = admm.solve(dec, 1.0, "primal", 1e-6, 20000)
+    adapt, s2 = admm.solve(dec, 50.0, "primal", 1e-6, 20000, adapt=(10.0, 2.0, 10))
+    assert s1 == "solved" and s2 == "solved"
+    assert abs(adapt.objective - fixed.objective) <= 1e-4 * abs(fixed.objective)
+    assert adapt.rho != 50.0
