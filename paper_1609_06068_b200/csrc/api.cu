@@ -307,6 +307,8 @@ void build_trd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<int
   td.chunk = chunk;
   const char* ff = getenv("SDP_TRD_FORCE_FALLBACK");
   td.force_fallback = (ff && *ff == '1') ? 1 : 0;
+  const char* dbg = getenv("SDP_TRD_DEBUG");
+  td.debug = (dbg && *dbg == '1') ? 1 : 0;
   td.hoff = al.upload(hoff);
   td.zoff = al.upload(zoff);
   td.hbuf = al.get<double>((size_t)hmax);

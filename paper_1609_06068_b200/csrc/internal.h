@@ -110,6 +110,7 @@ struct TrdDev {
   int count = 0;
   int chunk = 0;
   int force_fallback = 0;     // SDP_TRD_FORCE_FALLBACK=1 (tests): QL with vectors for every matrix
+  int debug = 0;              // SDP_TRD_DEBUG=1: printf slot 0's spectrum selection (diagnostics)
   const int64_t* hoff = nullptr;
   const int64_t* zoff = nullptr;  // per slot: offset (doubles) of its selected eigenvectors of T
   double* hbuf = nullptr;
@@ -152,7 +153,7 @@ void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t
 void launch_projection_wj(int mode, const ProjArgs& a, cudaStream_t s);
 int64_t trd_hsize(int kp, int k);  // doubles of per-slot Householder workspace
 int giant_grid();        // CTAs of the persistent giant kernel on the current device
-int giant_min_order();   // smallest order routed to the giant tier (SDP_GIANT_MIN, default 97)
+int giant_min_order();   // smallest order routed to the giant tier (SDP_GIANT_MIN, default 65)
 int rv_kp(int bucket);
 // stride (kp) of the warm-start V storage of a matrix of order k in tier `bucket`
 inline int store_kp(int bucket, int k) {

@@ -20,7 +20,7 @@
 //      the reconstruction with the mode epilogue (primal: lambda_k +=
 //      rho (x_k - H_k x), E:LambdakUpdate).
 // Every inverse-iteration vector is checked (||T z - lambda z|| <= 1e-9 ||T||);
-// if one fails, or QL hit its iteration cap, the matrix is redone inside the
+// if one fails, or QL hit its iteration cap (50 per eigenvalue), the matrix is redone inside the
 // apply kernel by QL with eigenvector accumulation (every thread runs the same
 // chain on a private copy and rotates its own row).  Eigenvalues are clipped at
 // exactly 0 (G15).
@@ -35,7 +35,7 @@ namespace {
 
 constexpr double kInvSqrt2 = 0.70710678118654752440;
 constexpr double kSqrt2 = 1.41421356237309504880;
-constexpr int kQlMaxIter = 30;
+constexpr int kQlMaxIter = 50;
 constexpr int QL_T = 32;  // threads (= matrices) per CTA of the QL kernel
 
 __device__ __forceinline__ void packed_rc(int e, int& r, int& c) {
@@ -171,15 +171,21 @@ __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int 
     g.sync();
     if (tau != 0.0) {
       // p = tau A22 v ; w = p - (tau/2)(p.v) v ; A22 -= v w^T + w v^T
+      // only the lower triangle of the trailing block is kept current: row i
+      // reads M[i][l] for l <= i and M[l][i] (column i) for l > i
+      // (uniform l across the threads: each access is either a row read, stride
+      // LD + 0, or a column read, consecutive -- both conflict-free)
       double pi = 0.0;
       if (in) {
         double a0 = 0.0, a1 = 0.0;
         int l = j + 1;
         for (; l + 1 < k; l += 2) {
-          a0 = fma(Mi[l], vv[l], a0);
-          a1 = fma(Mi[l + 1], vv[l + 1], a1);
+          const double m0 = (l <= i) ? Mi[l] : M[l * LD + i];
+          const double m1 = (l + 1 <= i) ? Mi[l + 1] : M[(l + 1) * LD + i];
+          a0 = fma(m0, vv[l], a0);
+          a1 = fma(m1, vv[l + 1], a1);
         }
-        if (l < k) a0 = fma(Mi[l], vv[l], a0);
+        if (l < k) a0 = fma((l <= i) ? Mi[l] : M[l * LD + i], vv[l], a0);
         pi = tau * (a0 + a1);
       }
       const double K = 0.5 * tau * g.sum(pi * vi);
@@ -187,7 +193,8 @@ __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int 
       if (in) wv[i] = wi;
       g.sync();
       if (in)
-        for (int l = j + 1; l < k; ++l) Mi[l] -= fma(vi, wv[l], wi * vv[l]);
+        for (int l = j + 1; l < k; ++l)
+          if (l <= i) Mi[l] -= fma(vi, wv[l], wi * vv[l]);
       g.sync();
     }
   }
@@ -214,10 +221,19 @@ __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& 
   if (mx == 0.0) return true;
   const int ex = ilogb(mx);
   const double sc = scalbn(1.0, -ex), usc = scalbn(1.0, ex);
+  double tn = 0.0;  // ||T||_inf of the scaled T
   for (int i = 0; i < k; ++i) {
     d[i * st] *= sc;
     e[i * st] *= sc;
   }
+  for (int i = 0; i < k; ++i)
+    tn = fmax(tn, fabs(d[i * st]) + fabs(e[i * st]) + (i > 0 ? fabs(e[(i - 1) * st]) : 0.0));
+  // a coupling is negligible if it is below the local test of tqli OR below
+  // eps ||T||: P_+ needs eigenvalues to eps ||T|| absolute accuracy, and the
+  // global test stops QL from iterating on noise-level blocks of graded T (e.g.
+  // the tridiagonal form of a rank-one matrix), where the local test alone can
+  // exhaust the iteration cap
+  const double gtol = 2.220446049250313e-16 * tn;
   bool ok = true;
   for (int l = 0; l < k; ++l) {
     int iter = 0;
@@ -225,7 +241,8 @@ __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& 
     do {
       for (m = l; m < k - 1; ++m) {
         const double dd = fabs(d[m * st]) + fabs(d[(m + 1) * st]);
-        if (fabs(e[m * st]) + dd == dd) break;
+        const double em = fabs(e[m * st]);
+        if (em + dd == dd || em <= gtol) break;
       }
       if (m != l) {
         if (iter++ == kQlMaxIter) {
@@ -342,7 +359,7 @@ template <int KP>
 struct InvLayout {
   static constexpr int HALF = KP / 2;        // selected eigenvalues per matrix <= k / 2
   static constexpr int NMAT = IV_T / HALF;   // matrices per CTA
-  static constexpr size_t bytes() { return (size_t)5 * KP * IV_T * sizeof(double); }
+  static constexpr size_t bytes() { return (size_t)4 * KP * IV_T * sizeof(double); }
 };
 
 template <int KP>
@@ -365,39 +382,35 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   const double* e = H.e();
   double* ui = smem + t;  // inverse pivots, element i at [i * IV_T]
   double* u2 = ui + KP * IV_T;
-  double* u3 = u2 + KP * IV_T;
-  double* mu = u3 + KP * IV_T;
+  double* mu = u2 + KP * IV_T;
   double* x = mu + KP * IV_T;
+  // (the second superdiagonal of U is e[i+1] where row i pivoted, else 0)
   double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [j][i]
   bool fail = false;
   for (int j = j0; j < nsel && (int)H.clst()[j] == j0; ++j) {
     const double lam = H.lsel()[j];
     unsigned long long pv = 0ull;  // pivot flags (k <= 64)
-    double r0 = d[0] - lam, r1 = k > 1 ? e[0] : 0.0, r2 = 0.0;
+    double r0 = d[0] - lam, r1 = k > 1 ? e[0] : 0.0;
     for (int i = 0; i + 1 < k; ++i) {
       const double ci = e[i], ai = d[i + 1] - lam, bi = (i + 2 < k) ? e[i + 1] : 0.0;
-      double p1, p2, p3, m;
+      double p1, p2, m;
       if (fabs(ci) > fabs(r0)) {
         pv |= 1ull << i;
         p1 = ci;
         p2 = ai;
-        p3 = bi;
         m = r0 / ci;
         r0 = r1 - m * ai;
-        r1 = r2 - m * bi;
+        r1 = -m * bi;
       } else {
         p1 = r0;
         p2 = r1;
-        p3 = r2;
         m = r0 != 0.0 ? ci / r0 : 0.0;
         r0 = ai - m * r1;
-        r1 = bi - m * r2;
+        r1 = bi;
       }
-      r2 = 0.0;
       if (fabs(p1) < tol) p1 = p1 < 0.0 ? -tol : tol;
       ui[i * IV_T] = 1.0 / p1;
       u2[i * IV_T] = p2;
-      u3[i * IV_T] = p3;
       mu[i * IV_T] = m;
     }
     if (fabs(r0) < tol) r0 = r0 < 0.0 ? -tol : tol;
@@ -427,7 +440,8 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
       x[(k - 1) * IV_T] = xn;
       double mx = fabs(xn);
       for (int i = k - 2; i >= 0; --i) {
-        const double xi = (x[i * IV_T] - u2[i * IV_T] * xn - u3[i * IV_T] * xn1) * ui[i * IV_T];
+        const double u3 = ((pv >> i) & 1ull) ? e[i + 1] : 0.0;  // i + 2 < k here
+        const double xi = (x[i * IV_T] - u2[i * IV_T] * xn - u3 * xn1) * ui[i * IV_T];
         x[i * IV_T] = xi;
         mx = fmax(mx, fabs(xi));
         xn1 = xn;
@@ -464,7 +478,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
 // ---------------------------------------------------------------- 4. back-transform, P_+
 template <int KP>
 struct ApplyLayout {
-  static constexpr int LD = KP + 1;
+  static constexpr int LD = KP + 4;  // == 4 (mod 16): conflict-free DMMA fragment loads
   static constexpr size_t bytes() { return (size_t)(KP * LD + 2 * KP + 2) * sizeof(double); }
 };
 
@@ -530,6 +544,12 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     side = 0;
   }
   g.sync();
+  if (a.td.debug && slot == 0 && tid == 0) {
+    printf("[trd] k=%d fallback=%d nsel=%d side=%d tnorm=%.3e rcount=%d\n", k, (int)fallback, nsel, side,
+           H.hdr()[2], a.td.rcount[slot]);
+    for (int i = 0; i < k; ++i) printf("  d[%d]=% .6e e=% .6e tau=% .6e\n", i, H.d()[i], H.e()[i], H.tau()[i]);
+    for (int j = 0; j < nsel; ++j) printf("  sel %d: shift=% .6e w=% .6e clst=%d\n", j, H.lsel()[j], lw[j], (int)H.clst()[j]);
+  }
   // back-transform the selected eigenvectors: V = H_0 H_1 ... H_{k-3} Z
   int64_t vpos = k >= 2 ? (int64_t)(k - 1) * (k - 2) / 2 : 0;
   for (int j = k - 3; j >= 0; --j) {
@@ -551,31 +571,49 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     }
     g.sync();
   }
-  // P_+ = [A] + sum_t w_t v_t v_t^T, packed upper, mode epilogue
-  const int ns = k * (k + 1) / 2;
+  // P_+ = [A] + sum_t w_t v_t v_t^T as DMMA (mma.sync m8n8k4 f64) 8x8 tiles over the
+  // upper tile triangle, K = nsel; then the packed upper entries with the mode epilogue
   double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-  for (int e = tid; e < ns; e += KP) {
-    int r, c;
-    packed_rc(e, r, c);
-    const double* Zrr = Z + r * LD;
-    const double* Zc = Z + c * LD;
-    double acc = 0.0;
-    for (int u = 0; u < nsel; ++u) acc = fma(lw[u] * Zrr[u], Zc[u], acc);
-    const int64_t pe = off + e;
-    if (side == 1) acc += input_value<MODE>(a, pe, r, c);
-    if constexpr (MODE == PM_BATCH) {
-      a.out[pe] = acc;
-    } else if constexpr (MODE == PM_PRIMAL) {
-      const double xkv = (r == c) ? acc : acc * kSqrt2;
-      const double hx = __ldg(a.x + a.G[pe]);
-      const double dd = xkv - hx;
-      a.xk[pe] = xkv;
-      a.lam[pe] = a.lam[pe] + a.rho * dd;  // E:LambdakUpdate
-      p0 += dd * dd;
-      p1 += xkv * xkv;
-      p2 += hx * hx;
-    } else {
-      a.xk[pe] = (r == c) ? acc : acc * kSqrt2;
+  {
+    const int lane = tid & 31, warp = tid >> 5;
+    const int r4 = lane >> 2, c4 = lane & 3;
+    const int nt = (k + 7) / 8;
+    const int ntile = nt * (nt + 1) / 2;
+    for (int tl = warp; tl < ntile; tl += KP / 32) {
+      int rt, ct;
+      packed_rc(tl, rt, ct);
+      double acc[2] = {0.0, 0.0};
+      for (int u0 = 0; u0 < nsel; u0 += 4) {
+        const int u = u0 + c4;
+        const bool ok = u < nsel;
+        const double a = ok ? lw[u] * Z[(8 * rt + r4) * LD + u] : 0.0;
+        const double b = ok ? Z[(8 * ct + r4) * LD + u] : 0.0;
+        asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+            : "+d"(acc[0]), "+d"(acc[1])
+            : "d"(a), "d"(b));
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * rt + r4, c = 8 * ct + 2 * c4 + h;
+        if (r > c || c >= k) continue;
+        double v = acc[h];
+        const int64_t pe = off + (int64_t)c * (c + 1) / 2 + r;
+        if (side == 1) v += input_value<MODE>(a, pe, r, c);
+        if constexpr (MODE == PM_BATCH) {
+          a.out[pe] = v;
+        } else if constexpr (MODE == PM_PRIMAL) {
+          const double xkv = (r == c) ? v : v * kSqrt2;
+          const double hx = __ldg(a.x + a.G[pe]);
+          const double dd = xkv - hx;
+          a.xk[pe] = xkv;
+          a.lam[pe] = a.lam[pe] + a.rho * dd;  // E:LambdakUpdate
+          p0 += dd * dd;
+          p1 += xkv * xkv;
+          p2 += hx * hx;
+        } else {
+          a.xk[pe] = (r == c) ? v : v * kSqrt2;
+        }
+      }
     }
   }
   if constexpr (MODE == PM_PRIMAL) {
