@@ -177,24 +177,37 @@ __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int 
       // LD + 0, or a column read, consecutive -- both conflict-free)
       double pi = 0.0;
       if (in) {
-        double a0 = 0.0, a1 = 0.0;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int l = j + 1;
-        for (; l + 1 < k; l += 2) {
+        for (; l + 3 < k; l += 4) {
           const double m0 = (l <= i) ? Mi[l] : M[l * LD + i];
           const double m1 = (l + 1 <= i) ? Mi[l + 1] : M[(l + 1) * LD + i];
+          const double m2 = (l + 2 <= i) ? Mi[l + 2] : M[(l + 2) * LD + i];
+          const double m3 = (l + 3 <= i) ? Mi[l + 3] : M[(l + 3) * LD + i];
           a0 = fma(m0, vv[l], a0);
           a1 = fma(m1, vv[l + 1], a1);
+          a2 = fma(m2, vv[l + 2], a2);
+          a3 = fma(m3, vv[l + 3], a3);
         }
-        if (l < k) a0 = fma((l <= i) ? Mi[l] : M[l * LD + i], vv[l], a0);
-        pi = tau * (a0 + a1);
+        for (; l < k; ++l) a0 = fma((l <= i) ? Mi[l] : M[l * LD + i], vv[l], a0);
+        pi = tau * ((a0 + a1) + (a2 + a3));
       }
       const double K = 0.5 * tau * g.sum(pi * vi);
       const double wi = pi - K * vi;
       if (in) wv[i] = wi;
       g.sync();
-      if (in)
-        for (int l = j + 1; l < k; ++l)
-          if (l <= i) Mi[l] -= fma(vi, wv[l], wi * vv[l]);
+      if (in) {
+        int l = j + 1;
+        for (; l + 3 <= i; l += 4) {
+          const double u0 = fma(vi, wv[l], wi * vv[l]), u1 = fma(vi, wv[l + 1], wi * vv[l + 1]);
+          const double u2 = fma(vi, wv[l + 2], wi * vv[l + 2]), u3 = fma(vi, wv[l + 3], wi * vv[l + 3]);
+          Mi[l] -= u0;
+          Mi[l + 1] -= u1;
+          Mi[l + 2] -= u2;
+          Mi[l + 3] -= u3;
+        }
+        for (; l <= i; ++l) Mi[l] -= fma(vi, wv[l], wi * vv[l]);
+      }
       g.sync();
     }
   }
@@ -558,16 +571,25 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     if (tau == 0.0) continue;
     if (tid >= j + 1 && tid < k) vv[tid] = (tid == j + 1) ? 1.0 : H.v()[vpos + (tid - j - 2)];
     g.sync();
-    for (int c = tid; c < nsel; c += KP) {
+    // two adjacent lanes per column (even / odd rows), y combined by one shuffle
+    for (int c0 = 0; c0 < nsel; c0 += KP / 2) {
+      const int c = c0 + (tid >> 1);
+      const bool act = c < nsel;
+      const int h = tid & 1;
       double y0 = 0.0, y1 = 0.0;
-      int i = j + 1;
-      for (; i + 1 < k; i += 2) {
-        y0 = fma(vv[i], Z[i * LD + c], y0);
-        y1 = fma(vv[i + 1], Z[(i + 1) * LD + c], y1);
+      int i = j + 1 + h;
+      if (act) {
+        for (; i + 2 < k; i += 4) {
+          y0 = fma(vv[i], Z[i * LD + c], y0);
+          y1 = fma(vv[i + 2], Z[(i + 2) * LD + c], y1);
+        }
+        if (i < k) y0 = fma(vv[i], Z[i * LD + c], y0);
       }
-      if (i < k) y0 = fma(vv[i], Z[i * LD + c], y0);
-      const double y = tau * (y0 + y1);
-      for (i = j + 1; i < k; ++i) Z[i * LD + c] = fma(-y, vv[i], Z[i * LD + c]);
+      double y = y0 + y1;
+      y += __shfl_xor_sync(0xffffffffu, y, 1);
+      y *= tau;
+      if (act)
+        for (i = j + 1 + h; i < k; i += 2) Z[i * LD + c] = fma(-y, vv[i], Z[i * LD + c]);
     }
     g.sync();
   }
