@@ -181,6 +181,19 @@ int sdp_get_history(sdp_handle h, double* out, int64_t cap, int64_t* rows);
 #define SDP_NUM_PHASES 7
 int sdp_profile_phases(sdp_handle h, int32_t iters, double* out_ms);
 
+/* ---- checkpoint / resume (warm-start state I/O) -----------
+ * The device-resident ADMM state at an iteration boundary -- x_k / z_k, lambda_k,
+ * v_k, the KKT x and y, the next right-hand side r1 / D, sum_k H_k^T x_k of the
+ * previous iteration (for eps_d), residuals, iteration count, rho, residual
+ * history, warm-start eigenbases -- serialised into a caller-owned host buffer.
+ * Loading it into a handle set up from the same problem, form and sharding
+ * continues the run bit-identically (tested).  Sharded handles save their local
+ * view (one blob per rank).  Errors: SDP_E_INVALID_ARG (NULL, buffer too small,
+ * or a blob from a different problem / form / sharding). */
+int sdp_state_bytes(sdp_handle h, int64_t* bytes);   /* size of the blob for the current state */
+int sdp_save_state(sdp_handle h, void* host_out, int64_t capacity);
+int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes);
+
 /* Free all resources of the handle (synchronises). */
 int sdp_destroy(sdp_handle h);
 

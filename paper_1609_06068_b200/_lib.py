@@ -94,6 +94,9 @@ _sig = {
     "sdp_get_cliques": (_i32, [_vp, _vp, _vp]),
     "sdp_get_history": (_i32, [_vp, _vp, _i64, C.POINTER(_i64)]),
     "sdp_destroy": (_i32, [_vp]),
+    "sdp_state_bytes": (_i32, [_vp, C.POINTER(_i64)]),
+    "sdp_save_state": (_i32, [_vp, _vp, _i64]),
+    "sdp_load_state": (_i32, [_vp, _vp, _i64]),
     "sdp_profile_phases": (_i32, [_vp, _i32, _vp]),
     "sdp_chordal_cliques": (_i32, [_i32, _i64, _vp, _vp, C.POINTER(_i32), _vp, _i64, _vp, C.POINTER(_i64),
                                    C.POINTER(_i64)]),
@@ -246,6 +249,19 @@ class Solver:
 
     def set_rho(self, rho):
         _check(lib.sdp_set_rho(self.h, float(rho)))
+
+    def save_state(self) -> bytes:
+        """Checkpoint of the device-resident ADMM state (sdp_save_state)."""
+        n = C.c_int64()
+        _check(lib.sdp_state_bytes(self.h, C.byref(n)))
+        buf = C.create_string_buffer(n.value)
+        _check(lib.sdp_save_state(self.h, buf, n.value))
+        return buf.raw
+
+    def load_state(self, blob: bytes):
+        """Resume from a save_state() blob of the same problem, form and sharding."""
+        buf = C.create_string_buffer(bytes(blob), len(blob))
+        _check(lib.sdp_load_state(self.h, buf, len(blob)))
 
     def info(self):
         info = sdp_info()

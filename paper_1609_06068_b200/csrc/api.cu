@@ -167,6 +167,7 @@ struct sdp_handle_s {
   unsigned long long* capped = nullptr;
   unsigned long long* sweeps = nullptr;
   double* vprev = nullptr;
+  int64_t vprev_len = 0;
   int64_t* voff = nullptr;
   int warm_period = 64;
   cudaGraph_t graph = nullptr;
@@ -994,6 +995,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     }
     h->voff = al.upload(voff);
     h->vprev = al.zeros<double>((size_t)std::max<int64_t>(voff[pl], 1));
+    h->vprev_len = voff[pl];
   }
   psd_init_attributes();
   SDP_CUDA_TRY(cudaDeviceSynchronize());
@@ -1300,6 +1302,126 @@ int sdp_profile_phases(sdp_handle h, int32_t iters, double* out_ms) {
         if (ph < SDP_NUM_PHASES) out_ms[ph] += ms / iters;
       }
     for (auto& e : ev) cudaEventDestroy(e);
+    return SDP_OK;
+  });
+}
+
+namespace {
+constexpr int64_t kStateMagic = 0x3154415453504453ll;  // "SDPSTAT1"
+constexpr int kStateHeader = 16;                      // int64 words
+struct StateLayout {
+  int64_t stot, lda, m, vlen, hrows;
+  int64_t words() const { return kStateHeader + 3 * stot + 3 * lda + m + 4 + 3 * hrows + vlen; }
+};
+StateLayout state_layout(sdp_handle h, long long iter) {
+  StateLayout L;
+  L.stot = h->stotl;
+  L.lda = h->lda;
+  L.m = h->m;
+  L.vlen = h->vprev ? h->vprev_len : 0;
+  L.hrows = std::min<long long>(iter, kHistCap);
+  return L;
+}
+}  // namespace
+
+int sdp_state_bytes(sdp_handle h, int64_t* bytes) {
+  return guarded([&] {
+    if (!h || !bytes) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    long long it = 0;
+    SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
+    *bytes = 8 * state_layout(h, it).words();
+    return SDP_OK;
+  });
+}
+
+int sdp_save_state(sdp_handle h, void* host_out, int64_t capacity) {
+  return guarded([&] {
+    if (!h || !host_out) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    long long it = 0;
+    unsigned long long cap = 0, sw = 0;
+    SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
+    SDP_CUDA_TRY(cudaMemcpy(&cap, h->capped, sizeof(cap), cudaMemcpyDeviceToHost));
+    SDP_CUDA_TRY(cudaMemcpy(&sw, h->sweeps, sizeof(sw), cudaMemcpyDeviceToHost));
+    const StateLayout L = state_layout(h, it);
+    if (capacity < 8 * L.words()) throw Error{SDP_E_INVALID_ARG, "state buffer too small (see sdp_state_bytes)"};
+    int64_t* hd = static_cast<int64_t*>(host_out);
+    std::memset(hd, 0, 8 * kStateHeader);
+    hd[0] = kStateMagic;
+    hd[1] = h->form;
+    hd[2] = h->world;
+    hd[3] = h->rank;
+    hd[4] = L.stot;
+    hd[5] = L.lda;
+    hd[6] = L.m;
+    hd[7] = L.vlen;
+    hd[8] = L.hrows;
+    hd[9] = it;
+    hd[10] = (int64_t)cap;
+    hd[11] = (int64_t)sw;
+    std::memcpy(&hd[12], &h->rho, 8);
+    hd[13] = h->N;
+    hd[14] = h->p;
+    double* w = reinterpret_cast<double*>(hd + kStateHeader);
+    auto get = [&](const double* dev, int64_t n) {
+      if (n) SDP_CUDA_TRY(cudaMemcpy(w, dev, n * sizeof(double), cudaMemcpyDeviceToHost));
+      w += n;
+    };
+    get(h->xk, L.stot);
+    get(h->lam, L.stot);
+    get(h->vk, L.stot);
+    get(h->x, L.lda);
+    get(h->rD, L.lda);
+    get(h->sprev, L.lda);
+    get(h->y, L.m);
+    get(h->res, 4);
+    get(h->hist, 3 * L.hrows);
+    get(h->vprev, L.vlen);
+    return SDP_OK;
+  });
+}
+
+int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes) {
+  return guarded([&] {
+    if (!h || !host_in) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    const int64_t* hd = static_cast<const int64_t*>(host_in);
+    if (bytes < 8 * kStateHeader || hd[0] != kStateMagic) throw Error{SDP_E_INVALID_ARG, "not an sdp state blob"};
+    StateLayout L = state_layout(h, hd[9]);
+    if (hd[1] != h->form || hd[2] != h->world || hd[3] != h->rank || hd[4] != L.stot || hd[5] != L.lda ||
+        hd[6] != L.m || hd[7] != L.vlen || hd[8] != L.hrows || hd[13] != h->N || hd[14] != h->p)
+      throw Error{SDP_E_INVALID_ARG, "state blob is from a different problem, form or sharding"};
+    if (bytes < 8 * L.words()) throw Error{SDP_E_INVALID_ARG, "state blob truncated"};
+    const double* w = reinterpret_cast<const double*>(hd + kStateHeader);
+    auto put = [&](double* dev, int64_t n) {
+      if (n) SDP_CUDA_TRY(cudaMemcpy(dev, w, n * sizeof(double), cudaMemcpyHostToDevice));
+      w += n;
+    };
+    put(h->xk, L.stot);
+    put(h->lam, L.stot);
+    put(h->vk, L.stot);
+    put(h->x, L.lda);
+    put(h->rD, L.lda);
+    put(h->sprev, L.lda);
+    put(h->y, L.m);
+    put(h->res, 4);
+    put(h->hist, 3 * L.hrows);
+    put(h->vprev, L.vlen);
+    const long long it = hd[9];
+    const unsigned long long cap = (unsigned long long)hd[10], sw = (unsigned long long)hd[11];
+    SDP_CUDA_TRY(cudaMemcpy(h->iter, &it, sizeof(it), cudaMemcpyHostToDevice));
+    SDP_CUDA_TRY(cudaMemcpy(h->capped, &cap, sizeof(cap), cudaMemcpyHostToDevice));
+    SDP_CUDA_TRY(cudaMemcpy(h->sweeps, &sw, sizeof(sw), cudaMemcpyHostToDevice));
+    SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
+    SDP_CUDA_TRY(cudaMemset(h->numerical, 0, sizeof(int)));
+    double rho;
+    std::memcpy(&rho, &hd[12], 8);
+    h->rho = rho;  // r1 / D was restored as saved: no rebuild from x_k, lambda_k
+    rebuild_graph(h);
     return SDP_OK;
   });
 }

@@ -637,7 +637,9 @@ __global__ void __launch_bounds__(256) k_syrk_dense(const double* __restrict__ A
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int i = i0 + ty + 16 * p, j = j0 + tx + 16 * q;
-      if (i < m && j < m) {
+      // a diagonal tile computes both (i, j) and (j, i) with D^-1 on different
+      // operands (different rounding): only i <= j writes, so S is deterministic
+      if (i < m && j < m && (bi != bj || i <= j)) {
         S[(int64_t)i * m + j] = acc[p][q];
         S[(int64_t)j * m + i] = acc[p][q];
       }

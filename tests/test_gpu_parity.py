@@ -470,3 +470,50 @@ def test_solve_adaptive_rho(lib, gen, form, rho):
     assert info["rho"] == st.rho
     assert abs(info["objective"] - st.objective) <= 1e-6 * abs(st.objective)
     s.close()
+
+
+# ------------------------------------------------------------------ checkpoint / resume
+
+@pytest.mark.parametrize("name,form", [("cfg1", "primal"), ("cfg1", "dual"), ("maxcut200", "primal"),
+                                       ("arrow30", "dual")])
+def test_checkpoint_resume_bit_identical(lib, gen, name, form):
+    """save_state after 37 iterations, continue 29 more; a fresh handle that loads
+    the blob and runs 29 iterations ends bit-identical (x, y, blocks, history,
+    iteration count); the resumed run also matches the oracle."""
+    prob = gen.block_arrow(12, 20, 10, 40, seed=7) if name == "arrow30" else PROBLEMS[name](gen)
+    a = lib.Solver(prob, form=form, rho=1.0)
+    a.step(37)
+    blob = a.save_state()
+    a.step(29)
+    b = lib.Solver(prob, form=form, rho=1.0)
+    b.load_state(blob)
+    b.step(29)
+    for fam in ("xk", "lambda") + (("vk",) if form == "dual" else ()):
+        assert np.array_equal(a.blocks(fam), b.blocks(fam)), fam
+    assert np.array_equal(a.x(), b.x()) and np.array_equal(a.y(), b.y())
+    assert np.array_equal(a.history(), b.history())
+    assert a.info()["iters"] == b.info()["iters"] == 66
+    dec = dc.decompose(prob)
+    st = admm.step(dec, admm.zero_state(dec), 1.0, form, 66)
+    compare_state(dec, st, b, form)
+    # a blob of another problem / form is rejected
+    c = lib.Solver(gen.config(0), form=form, rho=1.0)
+    with pytest.raises(lib.SdpError, match="INVALID_ARG"):
+        c.load_state(blob)
+    for s_ in (a, b, c):
+        s_.close()
+
+
+def test_two_handles_bit_identical(lib, gen):
+    """Setup is deterministic too: two handles of the same problem produce
+    bit-identical iterates (the dense S = A D^-1 A^T tiles write each (i, j)
+    once)."""
+    prob = gen.block_arrow(12, 20, 10, 40, seed=7)
+    for form in ("primal", "dual"):
+        a = lib.Solver(prob, form=form, rho=1.0)
+        b = lib.Solver(prob, form=form, rho=1.0)
+        a.step(12)
+        b.step(12)
+        assert np.array_equal(a.x(), b.x()) and np.array_equal(a.blocks("xk"), b.blocks("xk"))
+        a.close()
+        b.close()
