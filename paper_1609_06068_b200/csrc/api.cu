@@ -285,14 +285,14 @@ void build_giant(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<i
 }
 
 // Tridiagonal-QL tier workspace (kernels_psd_trd.cu) for the tasks `ids` of storage order kp,
-// processed in chunks so that the workspace stays under SDP_TRD_BUDGET_MB (default 2048).
+// processed in chunks so that the workspace stays under SDP_TRD_BUDGET_MB (default 4096).
 void build_trd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<int32_t>& ids, int kp, TrdDev& td) {
   td = TrdDev{};
   const int n = (int)ids.size();
   if (!n) return;
   const char* bud = getenv("SDP_TRD_BUDGET_MB");
-  const int64_t budget = (bud ? std::max(16ll, atoll(bud)) : 2048ll) << 20;
-  const int64_t zper = (int64_t)(kp / 2) * kp;
+  const int64_t budget = (bud ? std::max(16ll, atoll(bud)) : 4096ll) << 20;
+  const int64_t zper = (int64_t)kp * kp;  // KP/2 inverse-iteration vectors, or the QL fallback's full Z
   const int64_t per = 8 * (trd_hsize(kp, kp) + zper);
   const int chunk = (int)std::max<int64_t>(1, std::min<int64_t>(n, budget / per));
   std::vector<int64_t> hoff(n), zoff(n);

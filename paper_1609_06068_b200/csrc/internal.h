@@ -114,7 +114,7 @@ struct TrdDev {
   const int64_t* hoff = nullptr;
   const int64_t* zoff = nullptr;  // per slot: offset (doubles) of its selected eigenvectors of T
   double* hbuf = nullptr;
-  double* zbuf = nullptr;         // per slot (KP/2) x KP doubles
+  double* zbuf = nullptr;         // per slot KP x KP doubles
   int32_t* rcount = nullptr;  // per slot: 0, or -1 (QL iteration cap / inverse iteration residual)
 };
 

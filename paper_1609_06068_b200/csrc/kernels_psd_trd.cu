@@ -109,24 +109,26 @@ struct Grp {
 };
 
 // ---------------------------------------------------------------- 1. tridiagonalization
+// M is the packed LOWER triangle (row r at r(r+1)/2): 17.7 KB for k = 64, so
+// 12 matrices fit on an SM; row reads at r(r+1)/2 + l are bank-conflict-free
+// across 32 consecutive rows, column reads l(l+1)/2 + i are consecutive.
 template <int KP>
 struct TridiagLayout {
-  static constexpr int LD = KP + 1;
-  static constexpr int PER = KP * LD + 2 * KP + 2;  // M, v, w, reduction scratch
-  static constexpr int NMAT = 128 / KP;              // matrices per 128-thread CTA
+  static constexpr int PER = KP * (KP + 1) / 2 + 2 * KP + 2;  // M, v, w, reduction scratch
+  static constexpr int NMAT = 128 / KP;                       // matrices per 128-thread CTA
 };
+__device__ __forceinline__ int tri(int r) { return r * (r + 1) / 2; }
 
 template <int KP, int MODE>
 __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = TridiagLayout<KP>;
-  constexpr int LD = Lay::LD;
   extern __shared__ double smem[];
   const int grp = threadIdx.x / KP;
   const int sl = blockIdx.x * Lay::NMAT + grp;
   if (sl >= nslots) return;  // whole groups leave together
   double* M = smem + (size_t)grp * Lay::PER;
-  double* vv = M + KP * LD;
+  double* vv = M + KP * (KP + 1) / 2;
   double* wv = vv + KP;
   Grp<KP> g{(int)(threadIdx.x % KP), 1 + grp, wv + KP};
   const int i = g.tid;  // the row this thread owns
@@ -139,17 +141,15 @@ __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int 
   for (int e = i; e < ns; e += KP) {
     int r, c;
     packed_rc(e, r, c);
-    const double v = input_value<MODE>(a, off + e, r, c);
-    M[r * LD + c] = v;
-    M[c * LD + r] = v;
+    M[tri(c) + r] = input_value<MODE>(a, off + e, r, c);  // (c, r), c >= r: lower
   }
   g.sync();
-  double* Mi = M + i * LD;
+  double* Mi = M + tri(i);
   int64_t vpos = 0;
   for (int j = 0; j + 2 < k; ++j) {
     // Householder vector of x = M[j+1:k, j] (dlarfg): beta = -sign(alpha) ||x||,
     // tau = (beta - alpha) / beta, v = [1; x2 / (alpha - beta)]
-    const double alpha = M[(j + 1) * LD + j];
+    const double alpha = M[tri(j + 1) + j];
     const double xi = (i >= j + 2 && i < k) ? Mi[j] : 0.0;
     const double sig = g.sum(xi * xi);
     double tau = 0.0, beta = alpha, scl = 0.0;
@@ -171,25 +171,23 @@ __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int 
     g.sync();
     if (tau != 0.0) {
       // p = tau A22 v ; w = p - (tau/2)(p.v) v ; A22 -= v w^T + w v^T
-      // only the lower triangle of the trailing block is kept current: row i
-      // reads M[i][l] for l <= i and M[l][i] (column i) for l > i
-      // (uniform l across the threads: each access is either a row read, stride
-      // LD + 0, or a column read, consecutive -- both conflict-free)
+      // only the lower triangle is stored: row i reads M(i, l) for l <= i and
+      // M(l, i) (column i) for l > i, with l uniform across the threads
       double pi = 0.0;
       if (in) {
         double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
         int l = j + 1;
         for (; l + 3 < k; l += 4) {
-          const double m0 = (l <= i) ? Mi[l] : M[l * LD + i];
-          const double m1 = (l + 1 <= i) ? Mi[l + 1] : M[(l + 1) * LD + i];
-          const double m2 = (l + 2 <= i) ? Mi[l + 2] : M[(l + 2) * LD + i];
-          const double m3 = (l + 3 <= i) ? Mi[l + 3] : M[(l + 3) * LD + i];
+          const double m0 = (l <= i) ? Mi[l] : M[tri(l) + i];
+          const double m1 = (l + 1 <= i) ? Mi[l + 1] : M[tri(l + 1) + i];
+          const double m2 = (l + 2 <= i) ? Mi[l + 2] : M[tri(l + 2) + i];
+          const double m3 = (l + 3 <= i) ? Mi[l + 3] : M[tri(l + 3) + i];
           a0 = fma(m0, vv[l], a0);
           a1 = fma(m1, vv[l + 1], a1);
           a2 = fma(m2, vv[l + 2], a2);
           a3 = fma(m3, vv[l + 3], a3);
         }
-        for (; l < k; ++l) a0 = fma((l <= i) ? Mi[l] : M[l * LD + i], vv[l], a0);
+        for (; l < k; ++l) a0 = fma((l <= i) ? Mi[l] : M[tri(l) + i], vv[l], a0);
         pi = tau * ((a0 + a1) + (a2 + a3));
       }
       const double K = 0.5 * tau * g.sum(pi * vi);
@@ -213,7 +211,7 @@ __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int 
   }
   if (i < k) H.d()[i] = Mi[i];
   if (i == 0) {
-    if (k >= 2) H.e()[k - 2] = M[(k - 1) * LD + k - 2];
+    if (k >= 2) H.e()[k - 2] = M[tri(k - 1) + k - 2];
     H.e()[k - 1] = 0.0;
   }
 }
@@ -489,9 +487,11 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
 }
 
 // ---------------------------------------------------------------- 4. back-transform, P_+
+// Z holds at most KP/2 columns (the selected side has <= k/2 eigenvectors);
+// row stride KP/2 + 4 == 4 (mod 16) keeps the DMMA fragment loads conflict-free
 template <int KP>
 struct ApplyLayout {
-  static constexpr int LD = KP + 4;  // == 4 (mod 16): conflict-free DMMA fragment loads
+  static constexpr int LD = KP / 2 + 4;
   static constexpr size_t bytes() { return (size_t)(KP * LD + 2 * KP + 2) * sizeof(double); }
 };
 
@@ -525,11 +525,13 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     }
     if (tid < nsel) lw[tid] = H.lw()[tid];
   } else {
-    // QL with eigenvectors, every thread running the same chain on a private copy
-    // of (d, e) (identical arithmetic, identical rotations) and rotating its own
-    // row of Z; then the lambda > 0 columns, compacted in place
+    // QL with eigenvectors in the slot's global scratch (KP x KP), every thread
+    // running the same chain on a private copy of (d, e) (identical arithmetic,
+    // identical rotations) and rotating its own row; then the side of 0 with
+    // fewer eigenvectors, in index order, into the shared Z
     const int row = tid;
-    double* Zr = Z + row * LD;
+    double* Zg = a.td.zbuf + a.td.zoff[slot];
+    double* Zr = Zg + (size_t)row * KP;
     for (int j = 0; j < KP; ++j) Zr[j] = (j == row) ? 1.0 : 0.0;
     double dl[KP], el[KP];
     for (int i = 0; i < k; ++i) {
@@ -544,17 +546,21 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
       }
     });
     if (!ok && row == 0 && a.capped) atomicAdd(a.capped, 1ull);
-    g.sync();
+    int npos = 0, nneg = 0;
+    for (int t = 0; t < k; ++t) {
+      npos += dl[t] > 0.0;
+      nneg += dl[t] < 0.0;
+    }
+    side = npos <= nneg ? 0 : 1;
     int n = 0;
     for (int t = 0; t < k; ++t) {
-      if (dl[t] > 0.0) {
-        if (row < k && n != t) Zr[n] = Zr[t];
-        if (row == 0) lw[n] = dl[t];
+      if (side == 0 ? dl[t] > 0.0 : dl[t] < 0.0) {
+        if (row < k) Z[row * LD + n] = Zr[t];
+        if (row == 0) lw[n] = side == 0 ? dl[t] : -dl[t];
         ++n;
       }
     }
     nsel = n;
-    side = 0;
   }
   g.sync();
   if (a.td.debug && slot == 0 && tid == 0) {
