@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   double* mu = u2 + KP * IV_T;
   double* x = mu + KP * IV_T;
   // (the second superdiagonal of U is e[i+1] where row i pivoted, else 0)
-  double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [j][i]
+  double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [i][j], row length KP/2
   bool fail = false;
   for (int j = j0; j < nsel && (int)H.clst()[j] == j0; ++j) {
     const double lam = H.lsel()[j];
@@ -461,10 +461,10 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
       const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
       for (int i = 0; i < k; ++i) x[i * IV_T] *= inv;
       for (int p = j0; p < j; ++p) {
-        const double* zp = Zo + (size_t)p * KP;
+        const double* zp = Zo + p;  // column p of the [i][j] block (row length KP/2)
         double dot = 0.0;
-        for (int i = 0; i < k; ++i) dot = fma(zp[i], x[i * IV_T], dot);
-        for (int i = 0; i < k; ++i) x[i * IV_T] = fma(-dot, zp[i], x[i * IV_T]);
+        for (int i = 0; i < k; ++i) dot = fma(zp[i * (KP / 2)], x[i * IV_T], dot);
+        for (int i = 0; i < k; ++i) x[i * IV_T] = fma(-dot, zp[i * (KP / 2)], x[i * IV_T]);
       }
       double nrm = 0.0;
       for (int i = 0; i < k; ++i) nrm = fma(x[i * IV_T], x[i * IV_T], nrm);
@@ -472,14 +472,14 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
       for (int i = 0; i < k; ++i) x[i * IV_T] *= in2;
     }
     double res = 0.0;
-    double* zj = Zo + (size_t)j * KP;
+    double* zj = Zo + j;
     for (int i = 0; i < k; ++i) {
       const double xi = x[i * IV_T];
       double tz = (d[i] - lam) * xi;
       if (i > 0) tz = fma(e[i - 1], x[(i - 1) * IV_T], tz);
       if (i + 1 < k) tz = fma(e[i], x[(i + 1) * IV_T], tz);
       res = fmax(res, fabs(tz));
-      zj[i] = xi;
+      zj[i * (KP / 2)] = xi;  // [i][j]: the threads of a matrix write consecutive j
     }
     if (!(res <= 1e-9 * fmax(tnorm, 1e-300))) fail = true;  // includes NaN
   }
@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
 template <int KP>
 struct ApplyLayout {
   static constexpr int LD = KP / 2 + 4;
-  static constexpr size_t bytes() { return (size_t)(KP * LD + 2 * KP + 2) * sizeof(double); }
+  static constexpr size_t bytes() { return (size_t)(KP * LD + 3 * KP + 2) * sizeof(double); }
 };
 
 template <int KP, int MODE>
@@ -506,7 +506,8 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
   double* Z = smem;  // selected eigenvectors (columns), then back-transformed
   double* vv = Z + KP * LD;
   double* lw = vv + KP;
-  double* red = lw + KP;
+  double* ysm = lw + KP;  // back-transform partials of the two warps
+  double* red = ysm + KP;
   Grp<KP> g{(int)threadIdx.x, 1, red};
   const int tid = g.tid;
   const int slot = slot0 + sl;
@@ -518,10 +519,10 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
   int side = (int)H.hdr()[1];
   const bool fallback = a.td.rcount[slot] < 0 || a.td.force_fallback;
   if (!fallback) {
-    const double* Zo = a.td.zbuf + a.td.zoff[slot];
-    for (int e = tid; e < nsel * k; e += KP) {
-      const int j = e / k, i = e - j * k;
-      Z[i * LD + j] = Zo[(size_t)j * KP + i];
+    const double* Zo = a.td.zbuf + a.td.zoff[slot];  // [i][j], row length KP/2
+    for (int e = tid; e < k * (KP / 2); e += KP) {
+      const int i = e / (KP / 2), j = e - i * (KP / 2);
+      if (j < nsel) Z[i * LD + j] = Zo[e];
     }
     if (tid < nsel) lw[tid] = H.lw()[tid];
   } else {
@@ -577,26 +578,29 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     if (tau == 0.0) continue;
     if (tid >= j + 1 && tid < k) vv[tid] = (tid == j + 1) ? 1.0 : H.v()[vpos + (tid - j - 2)];
     g.sync();
-    // two adjacent lanes per column (even / odd rows), y combined by one shuffle
-    for (int c0 = 0; c0 < nsel; c0 += KP / 2) {
-      const int c = c0 + (tid >> 1);
-      const bool act = c < nsel;
-      const int h = tid & 1;
-      double y0 = 0.0, y1 = 0.0;
-      int i = j + 1 + h;
-      if (act) {
-        for (; i + 2 < k; i += 4) {
-          y0 = fma(vv[i], Z[i * LD + c], y0);
-          y1 = fma(vv[i + 2], Z[(i + 2) * LD + c], y1);
-        }
-        if (i < k) y0 = fma(vv[i], Z[i * LD + c], y0);
+    // lane = column (conflict-free row reads); with two warps each takes the
+    // rows of one parity and the partial y meet in shared memory
+    constexpr int NWB = KP / 32;
+    const int h = tid >> 5, c = tid & 31;
+    const bool act = c < nsel;
+    double y0 = 0.0, y1 = 0.0;
+    int i = j + 1 + h;
+    if (act) {
+      for (; i + NWB < k; i += 2 * NWB) {
+        y0 = fma(vv[i], Z[i * LD + c], y0);
+        y1 = fma(vv[i + NWB], Z[(i + NWB) * LD + c], y1);
       }
-      double y = y0 + y1;
-      y += __shfl_xor_sync(0xffffffffu, y, 1);
-      y *= tau;
-      if (act)
-        for (i = j + 1 + h; i < k; i += 2) Z[i * LD + c] = fma(-y, vv[i], Z[i * LD + c]);
+      if (i < k) y0 = fma(vv[i], Z[i * LD + c], y0);
     }
+    double y = y0 + y1;
+    if constexpr (NWB == 2) {
+      ysm[tid] = y;
+      g.sync();
+      y = ysm[c] + ysm[32 + c];
+    }
+    y *= tau;
+    if (act)
+      for (i = j + 1 + h; i < k; i += NWB) Z[i * LD + c] = fma(-y, vv[i], Z[i * LD + c]);
     g.sync();
   }
   // P_+ = [A] + sum_t w_t v_t v_t^T as DMMA (mma.sync m8n8k4 f64) 8x8 tiles over the
@@ -669,6 +673,10 @@ void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
 template <int KP, int MODE>
 void set_attrs() {
   using TL = TridiagLayout<KP>;
+  cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(TL::NMAT * TL::PER * sizeof(double)));
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
