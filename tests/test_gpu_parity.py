@@ -517,3 +517,19 @@ def test_two_handles_bit_identical(lib, gen):
         assert np.array_equal(a.x(), b.x()) and np.array_equal(a.blocks("xk"), b.blocks("xk"))
         a.close()
         b.close()
+
+
+# ------------------------------------------------------------------ SDPA input (reader part)
+
+@pytest.mark.parametrize("fname,want", [("theta_c5.dat-s", -5 ** 0.5),
+                                        ("maxcut_c5.dat-s", -(25 + 5 * 5 ** 0.5) / 8),
+                                        ("mixed_blocks.dat-s", -1.5)])
+def test_sdpa_golden_solves(lib, fname, want):
+    from paper_1609_06068_b200 import sdpa
+    p = sdpa.read_sdpa(os.path.join(ROOT, "tests", "golden", fname))
+    for form in ("primal", "dual"):
+        s = lib.Solver(p, form=form, rho=1.0)
+        status, info = s.solve(20000, 1e-10)
+        assert status == "solved"
+        assert abs(info["objective"] - want) <= 1e-8 * abs(want), (form, info["objective"])
+        s.close()
