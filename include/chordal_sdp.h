@@ -175,7 +175,7 @@ int sdp_get_history(sdp_handle h, double* out, int64_t cap, int64_t* rows);
 /* Per-phase timing: run `iters` iterations (no graph) with CUDA events recorded
  * on the handle's stream around every phase; out_ms[ph] (host, capacity
  * SDP_NUM_PHASES) receives the mean device time per iteration of phase ph:
- * 0 gemv (A.v), 1 kkt-small (reduce + triangular solves), 2 gemvT (A^T.y + x),
+ * 0 gemv (A.v), 1 kkt-small (y = S^-1 u), 2 gemvT (A^T.y + x),
  * 3 projection (all tiers), 4 scatter, 5 dual update, 6 finalize.
  * Advances the state like sdp_step.  Synchronises. */
 #define SDP_NUM_PHASES 7

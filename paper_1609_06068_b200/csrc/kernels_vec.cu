@@ -2,7 +2,8 @@
 // clique projection):
 //   scatter   r1 = sum_k H_k^T(.)  (E:OptCondMinYPrimal / E:OptCondMinYDual rhs)
 //   gemv      u  = A (D^-1 r1) - r2           (block elimination)
-//   trsv      y  = L^-T L^-1 u  with the cached inverse factor W = L^-1
+//   symv      y  = S^-1 u with the cached S^-1 = W^T W (W = L^-1); the kernel
+//             also sums the gemv partials into u (single rank)
 //   gemvT     x  = D^-1 (r1 - A^T y)
 //   update    v_k, lambda_k of the dual (E:vkEqn, E:MultUpdateDualSDP)
 //   finalize  eps_p, eps_d, objective, stop flag   (reading G9)
@@ -246,92 +247,6 @@ __global__ void k_reduce_u(const double* __restrict__ part, int nchunks, int m, 
   }
 }
 
-// Triangular matrix-vector product with the cached inverse factor:
-// out_i = sum_{j in [lo_i, hi_i)} M[i][j] in_j, lower (LOWER=1: j <= i) or upper
-// (j >= i).  One warp per row.
-template <int LOWER>
-__global__ void __launch_bounds__(256) k_trmv(const double* __restrict__ M, int m, const double* __restrict__ in,
-                                               double* __restrict__ out, const int* done) {
-  if (done && *done) return;
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= m) return;
-  const int lo = LOWER ? 0 : row;
-  const int hi = LOWER ? row + 1 : m;
-  const double* Mr = M + (int64_t)row * m;
-  double s = 0.0;
-  for (int j = lo + lane; j < hi; j += 32) s = fma(Mr[j], in[j], s);
-  s = warp_sum(s);
-  if (lane == 0) out[row] = s;
-}
-
-// ---------------------------------------------------------------- dense GEMV^T
-// x_t = rD_t - Dinv_t * sum_i A[i][t] y_i    (x = D^-1 (r1 - A^T y))
-// CTA = 128 threads x 2 columns; y staged in shared memory in tiles; every
-// thread issues GT_U independent 16-byte evict-first loads before consuming
-// them (explicit batching keeps GT_U loads in flight per thread).
-// Partials: primal <c, x>; dual |D x|^2 (= |sum_k H_k^T lambda_k|^2 / rho^2).
-constexpr int GT_THREADS = 128;
-constexpr int GT_U = 16;
-template <int FORM>
-__global__ void __launch_bounds__(GT_THREADS) k_gemvT_dense(const double* __restrict__ A, int64_t lda, int m, int N,
-                                                             const double* __restrict__ y, const double* __restrict__ rD,
-                                                             const double* __restrict__ Dinv, const double* __restrict__ c,
-                                                             double* __restrict__ x, double* __restrict__ part,
-                                                             const int* done) {
-  if (done && *done) return;
-  constexpr int TILE = 4096;
-  __shared__ double ys[TILE];
-  __shared__ double sm[GT_THREADS / 32];
-  const int64_t t2 = (int64_t)blockIdx.x * GT_THREADS + threadIdx.x;  // column pair index
-  const bool act = 2 * t2 < lda;
-  const int64_t ld2 = lda / 2;
-  const double2* Ac = reinterpret_cast<const double2*>(A) + (act ? t2 : 0);
-  double w0 = 0.0, w1 = 0.0;
-  for (int r0 = 0; r0 < m; r0 += TILE) {
-    const int nr = (m - r0 < TILE) ? m - r0 : TILE;
-    __syncthreads();
-    for (int i = threadIdx.x; i < nr; i += GT_THREADS) ys[i] = y[r0 + i];
-    __syncthreads();
-    if (act) {
-      const double2* Ap = Ac + (int64_t)r0 * ld2;
-      int i = 0;
-      for (; i + GT_U <= nr; i += GT_U) {
-        double2 buf[GT_U];
-#pragma unroll
-        for (int u = 0; u < GT_U; ++u) buf[u] = __ldcs(Ap + (int64_t)(i + u) * ld2);
-#pragma unroll
-        for (int u = 0; u < GT_U; ++u) {
-          const double yi = ys[i + u];
-          w0 = fma(buf[u].x, yi, w0);
-          w1 = fma(buf[u].y, yi, w1);
-        }
-      }
-      for (; i < nr; ++i) {
-        const double2 aa = __ldcs(Ap + (int64_t)i * ld2);
-        const double yi = ys[i];
-        w0 = fma(aa.x, yi, w0);
-        w1 = fma(aa.y, yi, w1);
-      }
-    }
-  }
-  double acc[1] = {0.0};
-  if (act) {
-    const int64_t t = 2 * t2;
-    if (t < N) {
-      const double xv = rD[t] - Dinv[t] * w0;
-      x[t] = xv;
-      acc[0] += (FORM == 0) ? c[t] * xv : (xv / Dinv[t]) * (xv / Dinv[t]);
-    }
-    if (t + 1 < N) {
-      const double xv = rD[t + 1] - Dinv[t + 1] * w1;
-      x[t + 1] = xv;
-      acc[0] += (FORM == 0) ? c[t + 1] * xv : (xv / Dinv[t + 1]) * (xv / Dinv[t + 1]);
-    }
-  }
-  block_sum<1, GT_THREADS>(acc, sm);
-  if (threadIdx.x == 0) part[blockIdx.x] = acc[0];
-}
 
 // ---------------------------------------------------------------- GEMV^T over the A^T copy
 // x_t = rD_t - Dinv_t * (A^T y)_t with A^T stored row-major (lda x ldm): each
@@ -705,24 +620,7 @@ void launch_reduce_u(int form, const double* part, int nchunks, int m, const dou
     k_reduce_u<1><<<(m + 255) / 256, 256, 0, s>>>(part, nchunks, m, b, rho, u, sdiag, y, done);
 }
 
-void launch_trmv(int lower, const double* M, int m, const double* in, double* out, const int* done, cudaStream_t s) {
-  if (lower)
-    k_trmv<1><<<(m + 7) / 8, 256, 0, s>>>(M, m, in, out, done);
-  else
-    k_trmv<0><<<(m + 7) / 8, 256, 0, s>>>(M, m, in, out, done);
-}
 
-int gemvT_blocks(int64_t lda) { return (int)((lda / 2 + GT_THREADS - 1) / GT_THREADS); }
-
-void launch_gemvT_dense(int form, const double* A, int64_t lda, int m, int N, const double* y, const double* rD,
-                        const double* Dinv, const double* c, double* x, double* part, const int* done,
-                        cudaStream_t s) {
-  const int grid = gemvT_blocks(lda);
-  if (form == 0)
-    k_gemvT_dense<0><<<grid, GT_THREADS, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
-  else
-    k_gemvT_dense<1><<<grid, GT_THREADS, 0, s>>>(A, lda, m, N, y, rD, Dinv, c, x, part, done);
-}
 
 int gemvT_rows_blocks(int64_t N) { return (int)((N + 8 * TR_ROWS - 1) / (8 * TR_ROWS)); }
 

@@ -59,11 +59,6 @@ void launch_symv(int form, const double* Si, int m, const double* part, int nchu
 void symv_init_attributes(int m);
 void launch_reduce_u(int form, const double* part, int nchunks, int m, const double* b, double rho, double* u,
                      const double* sdiag, double* y, const int* done, cudaStream_t s);
-void launch_trmv(int lower, const double* M, int m, const double* in, double* out, const int* done, cudaStream_t s);
-int gemvT_blocks(int64_t lda);
-void launch_gemvT_dense(int form, const double* A, int64_t lda, int m, int N, const double* y, const double* rD,
-                        const double* Dinv, const double* c, double* x, double* part, const int* done,
-                        cudaStream_t s);
 int gemvT_rows_blocks(int64_t N);
 void launch_gemvT_rows(int form, const double* AT, int64_t ldm, int m, int N, const double* y, const double* rD,
                        const double* Dinv, const double* c, const double* own, double* x, double* part,
