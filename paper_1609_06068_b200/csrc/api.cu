@@ -229,6 +229,80 @@ int guarded(F&& f) {
   }
 }
 
+// Tridiagonal path of the giant tier (kernels_psd_gtrd.cu); SDP_GIANT_METHOD=jacobi turns it off.
+void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<int32_t>& ids, GiantDev& gd) {
+  const char* meth = getenv("SDP_GIANT_METHOD");
+  if (meth && std::string(meth) == "jacobi") return;
+  GtrdDev& gt = gd.gt;
+  const int ng = (int)ids.size();
+  const int kcap = gtrd_max_order();
+  std::vector<int64_t> moff(ng, 0);
+  std::vector<int32_t> hsel(ng), ev(ng + 1, 0), vg(ng + 1, 0), bt(ng + 1, 0), rc(ng + 1, 0);
+  int64_t ws = 0;
+  int kmax = 0;
+  for (int g = 0; g < ng; ++g) {
+    const int k = ksz[ids[g]];
+    hsel[g] = k;  // the computed side may be the larger one (k_gtrd_cluster)
+    const bool ok = k <= kcap;
+    moff[g] = ws;
+    if (ok) {
+      ws += (gtrd_ws_doubles(k) + 31) / 32 * 32;
+      kmax = std::max(kmax, k);
+    }
+    const int R = (k + 31) / 32;
+    ev[g + 1] = ev[g] + (ok ? (k + 31) / 32 : 0);
+    vg[g + 1] = vg[g] + (ok ? 2 * ((k + 31) / 32) + 1 : 0);
+    bt[g + 1] = bt[g] + (ok ? (k + 15) / 16 : 0);
+    rc[g + 1] = rc[g] + (ok ? R * (R + 1) / 2 : 0);
+  }
+  // tridiagonalization jobs: one 8-CTA cluster per order >= SDP_GTRD_COOP_MIN (default 200),
+  // the smaller ones 8 per cluster (one CTA each), largest first
+  const char* cm = getenv("SDP_GTRD_COOP_MIN");
+  const int coop_min = cm ? std::max(1, atoi(cm)) : 200;
+  std::vector<int> order(ng);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return ksz[ids[x]] > ksz[ids[y]]; });
+  std::vector<int32_t> job_g, job_coop;
+  std::vector<int> solo;
+  for (int g : order) {
+    if (ksz[ids[g]] >= coop_min) {
+      job_coop.push_back(1);
+      for (int r = 0; r < 8; ++r) job_g.push_back(r == 0 ? g : -1);
+    } else {
+      solo.push_back(g);
+    }
+  }
+  for (size_t i = 0; i < solo.size(); i += 8) {
+    job_coop.push_back(0);
+    for (size_t r = 0; r < 8; ++r) job_g.push_back(i + r < solo.size() ? solo[i + r] : -1);
+  }
+  gt.njob = (int)job_coop.size();
+  gt.job_g = al.upload(job_g);
+  gt.job_coop = al.upload(job_coop);
+  gt.ng = ng;
+  gt.kmax = std::max(kmax, 1);
+  gt.task = al.upload(ids);
+  gt.moff = al.upload(moff);
+  gt.hsel = al.upload(hsel);
+  gt.ws = al.get<double>((size_t)std::max<int64_t>(ws, 32));
+  gt.status = al.zeros<int32_t>((size_t)ng);
+  gt.ev_pre = al.upload(ev);
+  gt.tot_ev = ev[ng];
+  gt.vg_pre = al.upload(vg);
+  gt.tot_vg = vg[ng];
+  gt.ngrp = al.zeros<int32_t>((size_t)ng);
+  gt.bt_pre = al.upload(bt);
+  gt.rc_pre = al.upload(rc);
+  gt.tot_bt = bt[ng];
+  gt.tot_rc = rc[ng];
+  gt.part = al.zeros<double>(3 * (size_t)std::max(gt.tot_rc, 1));
+  const char* ff = getenv("SDP_GTRD_FORCE_FALLBACK");
+  gt.force_fallback = (ff && *ff == '1') ? 1 : 0;
+  const char* gdb = getenv("SDP_GTRD_DEBUG");
+  gt.debug = (gdb && *gdb == '1') ? 1 : 0;
+  gd.only = gt.status;
+}
+
 // Giant-tier metadata and workspace (kernels_psd_giant.cu) for the tasks `ids`.
 void build_giant(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<int32_t>& ids, GiantDev& gd) {
   gd = GiantDev{};
@@ -282,6 +356,7 @@ void build_giant(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<i
   gd.grid = giant_grid();
   const char* tr = getenv("SDP_GIANT_TRACE");
   gd.trace = tr ? atoi(tr) : 0;
+  build_gtrd(al, ksz, ids, gd);
 }
 
 // Tridiagonal-QL tier workspace (kernels_psd_trd.cu) for the tasks `ids` of storage order kp,
@@ -560,6 +635,7 @@ void reset_state(sdp_handle h) {
   SDP_CUDA_TRY(cudaMemsetAsync(h->numerical, 0, sizeof(int), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->capped, 0, sizeof(unsigned long long), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->sweeps, 0, sizeof(unsigned long long), s));
+  if (h->vprev) SDP_CUDA_TRY(cudaMemsetAsync(h->vprev, 0, (size_t)std::max<int64_t>(h->vprev_len, 1) * sizeof(double), s));
   const double neg = -1.0;
   SDP_CUDA_TRY(cudaMemcpyAsync(h->tol, &neg, sizeof(double), cudaMemcpyHostToDevice, s));
   if (h->form == SDP_FORM_PRIMAL) enqueue_scatter(h, s);  // r1 = -c/rho for iteration 1

@@ -73,6 +73,32 @@ int bucket_of(int k, int64_t count_in_range);
 // Projection modes
 enum ProjMode { PM_BATCH = 0, PM_PRIMAL = 1, PM_DUAL = 2 };
 
+// Tridiagonal path for the giant orders (kernels_psd_gtrd.cu): one CTA per
+// matrix, blocked Householder tridiagonalization of an L2-resident matrix, bisection + inverse iteration on the smaller side of the spectrum,
+// back-transform, DMMA reconstruction.  status[g] = -1 hands matrix g to the
+// block-Jacobi kernel (GiantDev::only).
+struct GtrdDev {
+  int ng = 0;
+  int kmax = 0;
+  const int32_t* task = nullptr;       // per giant (same order as GiantDev)
+  const int64_t* moff = nullptr;       // per giant: offset (doubles) of its workspace in ws
+  const int32_t* hsel = nullptr;       // per giant: H = k (max selected eigenvectors, row length of Z)
+  double* ws = nullptr;
+  int32_t* status = nullptr;           // per giant
+  int njob = 0;                        // tridiagonalization jobs (thread-block clusters of 8 CTAs)
+  const int32_t* job_g = nullptr;      // njob * 8: giant per CTA (solo) or in slot 0 (coop); -1 unused
+  const int32_t* job_coop = nullptr;   // njob: 1 = the cluster reduces one matrix together
+  const int32_t* ev_pre = nullptr;     // ng + 1: bisection warps (32 indices each)
+  const int32_t* vg_pre = nullptr;     // ng + 1: inverse-iteration warps (2 ceil(H / 32) + 1 groups)
+  int32_t* ngrp = nullptr;             // per giant: groups in use (device-computed)
+  const int32_t* bt_pre = nullptr;     // ng + 1: back-transform CTAs (16 columns each)
+  const int32_t* rc_pre = nullptr;     // ng + 1: reconstruction tiles (32 x 32, upper)
+  double* part = nullptr;              // 3 per reconstruction tile (primal residual partials)
+  int tot_ev = 0, tot_vg = 0, tot_bt = 0, tot_rc = 0;
+  int force_fallback = 0;              // SDP_GTRD_FORCE_FALLBACK=1: mark every matrix failed (tests)
+  int debug = 0;                       // SDP_GTRD_DEBUG=1: per-matrix spectrum / cluster printf
+};
+
 // Giant tier (kernels_psd_giant.cu): block-Jacobi over 16-wide blocks, one
 // persistent grid for all matrices of order > the CTA tiers.  Per giant g:
 // kp = k rounded up to 32, P = kp / 32 pair blocks per step, A / V / T are
@@ -99,6 +125,8 @@ struct GiantDev {
   int32_t* gflag = nullptr;             // ng: active in the current sweep
   unsigned* bar = nullptr;              // grid barrier {count, generation}
   int trace = 0;                        // SDP_GIANT_TRACE=1: CTA 0 printf's the per-phase times
+  const int32_t* only = nullptr;        // if set: process only giants with only[g] < 0, cold start
+  GtrdDev gt;                           // tridiagonal path (runs first; only = gt.status)
 };
 
 // Tridiagonal-QL tiers (kernels_psd_trd.cu), per bucket.  Slots = positions in
@@ -134,7 +162,7 @@ struct ProjArgs {
   const double* vk;     // dual: stacked v_k
   double rho;
   double* part;         // primal: per task 3 partials (|xk-hx|^2, |xk|^2, |hx|^2)
-  GiantDev gd;          // B_GLOBAL (giant) tier
+  GiantDev gd;          // B_GLOBAL (giant) tier: tridiagonal path + block-Jacobi fallback
   TrdDev td;            // tridiagonal-QL tier being launched
   unsigned long long* capped;  // count of sweep-capped projections
   unsigned long long* sweeps;  // total Jacobi sweeps (diagnostics)
@@ -149,6 +177,9 @@ struct ProjArgs {
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s);
+void launch_projection_gtrd(int mode, const ProjArgs& a, cudaStream_t s);
+int gtrd_max_order();          // largest order the giant tridiagonal path takes (shared-memory bound)
+int64_t gtrd_ws_doubles(int k);  // workspace of one matrix of order k
 void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_wj(int mode, const ProjArgs& a, cudaStream_t s);
 int64_t trd_hsize(int kp, int k);  // doubles of per-slot Householder workspace

@@ -456,8 +456,10 @@ void init_attrs_mode() {
 void psd_rv_init_attributes();
 void psd_trd_init_attributes();
 void psd_wj_init_attributes();
+void psd_gtrd_init_attributes();
 void psd_init_attributes() {
   psd_wj_init_attributes();
+  psd_gtrd_init_attributes();
   psd_rv_init_attributes();
   psd_trd_init_attributes();
   init_attrs_mode<PM_BATCH>();

@@ -184,6 +184,9 @@ struct PhaseClock {
   }
 };
 
+// giant g is handled by the tridiagonal path (kernels_psd_gtrd.cu) in this call
+__device__ __forceinline__ bool skip_g(const GiantDev& d, int g) { return d.only && d.only[g] >= 0; }
+
 // off(A)_F^2 > tol^2 ||A||_F^2 ?  (fixed-order sums: every CTA gets the same answer)
 // Data written by other CTAs during this launch is read with ld.global.cg (L2,
 // bypassing L1, which is not coherent across SMs): partials, sweep counters, A, V.
@@ -249,7 +252,18 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
   const int gw = blockIdx.x * NW + (threadIdx.x >> 5);  // global warp
   const int nwarps = gridDim.x * NW;
   const bool adm = MODE != PM_BATCH;
-  const bool warm = adm && a.vprev != nullptr && a.warm_period > 0 && (*a.iter % a.warm_period) != 0;
+  const bool warm_any = adm && a.vprev != nullptr && a.warm_period > 0 && (*a.iter % a.warm_period) != 0;
+  // per giant (warp-uniform): warm start from V_prev when one exists.  With the tridiagonal path
+  // in front (d.only) a giant reaches this kernel only in some iterations; its V_prev is valid
+  // iff it is nonzero (orthogonal; the buffer starts and resets at zero)
+  auto warm_g = [&](int g) -> bool {
+    if (!warm_any) return false;
+    if (!d.only) return true;
+    const double* Vp = a.vprev + a.voff[d.task[g]];
+    bool nz = false;
+    for (int c = lane; c < d.kp[g]; c += 32) nz |= __ldcg(Vp + c) != 0.0;
+    return __any_sync(0xffffffffu, nz);
+  };
   PhaseClock clk;
   clk.init(d.trace != 0);
 
@@ -258,6 +272,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
   // every A entry is written once; zero padding; V rows of the block = I or V_prev
   for (int w = gw; w < d.tot_rb; w += nwarps) {
     const int g = find_g(d.rb_pre, d.ng, w);
+      if (skip_g(d, g)) continue;
     const int cb = w - d.rb_pre[g];
     const int task = d.task[g];
     const int k = a.ksz[task], kp = d.kp[g];
@@ -274,7 +289,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
         fro += (r == c ? 1.0 : 2.0) * v * v;
       }
     }
-    if (warm) {
+    if (warm_g(g)) {
       const double* Vp = a.vprev + a.voff[task];
       for (int e = lane; e < 32 * kp; e += 32) V[(size_t)cb * 32 * kp + e] = __ldg(Vp + (size_t)cb * 32 * kp + e);
     } else {
@@ -289,10 +304,11 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
   grid_sync(d.bar, gridDim.x);
   clk.mark(0);
 
-  if (warm) {
+  if (warm_any) {
     // ---------------- warm start: T = A V_prev, then A = V_prev^T T (+ off-norm partials)
     for (int w = gw; w < d.tot_full; w += nwarps) {
       const int g = find_g(d.full_pre, d.ng, w);
+      if (skip_g(d, g) || !warm_g(g)) continue;
       const int t = w - d.full_pre[g];
       const int kp = d.kp[g], P = kp >> 5;
       const int rt = t / P, ct = t - rt * P;
@@ -321,6 +337,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
     clk.mark(1);
     for (int w = gw; w < d.tot_out; w += nwarps) {
       const int g = find_g(d.out_pre, d.ng, w);
+      if (skip_g(d, g) || !warm_g(g)) continue;
       int rb, cb;
       packed_rc(w - d.out_pre[g], rb, cb);
       const int kp = d.kp[g];
@@ -355,10 +372,12 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
       off2 = warp_sum(off2);
       if (lane == 0) d.part_off[w] = off2;
     }
-  } else {
-    // ---------------- cold: off-norm partials of the loaded A per upper tile
+  }
+  {
+    // ---------------- cold giants: off-norm partials of the loaded A per upper tile
     for (int w = gw; w < d.tot_out; w += nwarps) {
       const int g = find_g(d.out_pre, d.ng, w);
+      if (skip_g(d, g) || warm_g(g)) continue;
       int rb, cb;
       packed_rc(w - d.out_pre[g], rb, cb);
       const int kp = d.kp[g];
@@ -383,7 +402,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
   // ---------------- sweeps
   for (int sweep = 0;; ++sweep) {
     int any = 0;
-    for (int g = threadIdx.x; g < d.ng; g += NT) any |= giant_active(d, g) ? 1 : 0;
+    for (int g = threadIdx.x; g < d.ng; g += NT) any |= (!skip_g(d, g) && giant_active(d, g)) ? 1 : 0;
     any = __syncthreads_or(any);
     if (!any || sweep == kMaxSweeps) {
       if (d.trace && blockIdx.x == 0 && threadIdx.x == 0) printf("[giant] sweeps=%d any_active=%d\n", sweep, any);
@@ -391,7 +410,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
     }
     if (blockIdx.x == 0)
       for (int g = threadIdx.x; g < d.ng; g += NT) {
-        const int act = giant_active(d, g) ? 1 : 0;
+        const int act = (!skip_g(d, g) && giant_active(d, g)) ? 1 : 0;
         d.gflag[g] = act;
         if (act) d.gsweeps[g] = sweep + 1;
       }
@@ -400,6 +419,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
       // INNER: one Jacobi sweep on the 32x32 diagonal block of every pair -> Q
       for (int w = gw; w < d.tot_inner; w += nwarps) {
         const int g = find_g(d.inner_pre, d.ng, w);
+          if (skip_g(d, g)) continue;
         const int kp = d.kp[g], nb = kp >> 4;
         if (s >= nb - 1 || !__ldcg(d.gflag + g)) continue;
         const int pi = w - d.inner_pre[g];
@@ -431,6 +451,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
       // On a matrix's last step of the sweep the A tiles also leave the off-norm partials.
       for (int w = gw; w < d.tot_tile; w += nwarps) {
         const int g = find_g(d.tile_pre, d.ng, w);
+          if (skip_g(d, g)) continue;
         const int kp = d.kp[g], nb = kp >> 4, P = kp >> 5;
         if (s >= nb - 1 || !__ldcg(d.gflag + g)) continue;
         const int t = w - d.tile_pre[g];
@@ -510,6 +531,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
     if (w >= d.tot_out) {
       const int ws_ = w - d.tot_out;
       const int g = find_g(d.rb_pre, d.ng, ws_);
+        if (skip_g(d, g)) continue;
       const int rb = ws_ - d.rb_pre[g];
       const int kp = d.kp[g];
       const double* V = d.ws + d.wsoff[g] + (size_t)kp * kp;
@@ -518,6 +540,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
       continue;
     }
     const int g = find_g(d.out_pre, d.ng, w);
+      if (skip_g(d, g)) continue;
     int rb, cb;
     packed_rc(w - d.out_pre[g], rb, cb);
     const int task = d.task[g];
@@ -580,6 +603,7 @@ __global__ void __launch_bounds__(NT, 1) k_psd_giant(ProjArgs a) {
   clk.mark(5);
   // ---------------- FIN: per-matrix partials (fixed order), sweep / cap counters
   for (int g = blockIdx.x * NT + threadIdx.x; g < d.ng; g += gridDim.x * NT) {
+      if (skip_g(d, g)) continue;
     const int task = d.task[g];
     if constexpr (MODE == PM_PRIMAL) {
       double p0 = 0.0, p1 = 0.0, p2 = 0.0;
@@ -644,6 +668,9 @@ int giant_grid() {
 
 void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s) {
   if (a.gd.ng <= 0) return;
+  // tridiagonal path first; the block-Jacobi kernel then redoes the giants it marked
+  // (status -1) and returns after its first barrier phase when there are none
+  launch_projection_gtrd(mode, a, s);
   if (mode == PM_BATCH)
     launch_mode<PM_BATCH>(a, s);
   else if (mode == PM_PRIMAL)

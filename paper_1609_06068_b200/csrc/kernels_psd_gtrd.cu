@@ -1,0 +1,1068 @@
+// Tridiagonal path of the giant tier: P_k(X) = V max(Lambda, 0) V^T
+// (E:XkUpdate P:244-253, E:zkUpdate P:403-410) for 65 <= k <= 800, the
+// max-cut clique blocks that carry > 90 % of cfg3's projection flops.
+//
+// Block Jacobi (kernels_psd_giant.cu) executes ~12 k^3 flops per sweep and
+// needs several sweeps; this path executes ~4.5 k^3 (Golub & Van Loan 8.3):
+//   1. k_gtrd_tridiag (one 1024-thread CTA per matrix): Householder reduction
+//      A = Q T Q^T in the blocked form of LAPACK dsytrd / dlatrd (panels of 16
+//      columns: per column only the column update, the Householder vector and
+//      w = tau (A22 v - V W^T v - W V^T v) - (tau/2)(w.v) v; the trailing
+//      rank-32 update A22 -= V W^T + W V^T once per panel).  The matrix is the
+//      packed lower triangle in an L2-resident workspace, thread i owns row i,
+//      the panel's V and W live in shared memory.
+//   2. k_gtrd_eig (one CTA per matrix): inertia of T by a Sturm count at 0,
+//      the side of 0 with fewer eigenvalues, those eigenvalues by bisection
+//      (one thread each, Sturm counts with the LAPACK pivmin guard), clusters
+//      (gap <= 1e-3 ||T||) and inverse iteration as in LAPACK dstein (partial-
+//      pivoting tridiagonal LU, 3 solves, modified Gram-Schmidt in the cluster),
+//      residual-checked.
+//   3. k_gtrd_back (one CTA per 32 selected vectors): V = H_0 ... H_{k-3} Z,
+//      reflectors staged 16 at a time in shared memory, a warp per column with
+//      the column in registers.
+//   4. k_gtrd_recon (a warp per 32x32 tile): P_+ = [A] + sum_t w_t v_t v_t^T as
+//      DMMA (mma.sync m8n8k4 f64) products, mode epilogue, partials;
+//      k_gtrd_fin sums the partials per matrix in a fixed order.
+// A matrix whose inverse iteration fails its residual test (or with k > 800)
+// is marked status = -1 and redone by the block-Jacobi kernel in the same
+// projection call (GiantDev::only).  Eigenvalues are clipped at exactly 0.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
+
+#include "internal.h"
+
+namespace sdp {
+
+namespace {
+
+constexpr int GT_KMAX = 800;
+constexpr int GT_RT = GT_KMAX / 32;  // rows per lane in the back-transform (25)
+constexpr double kInvSqrt2 = 0.70710678118654752440;
+constexpr double kSqrt2 = 1.41421356237309504880;
+constexpr double kEps = 2.220446049250313e-16;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void packed_rc(int e, int& r, int& c) {
+  int cc = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
+  while ((cc + 1) * (cc + 2) / 2 <= e) ++cc;
+  while (cc * (cc + 1) / 2 > e) --cc;
+  c = cc;
+  r = e - cc * (cc + 1) / 2;
+}
+
+// projection input X_rc (r <= c), packed index e (absolute)
+template <int MODE>
+__device__ __forceinline__ double input_value(const ProjArgs& a, int64_t e, int r, int c) {
+  if constexpr (MODE == PM_BATCH) {
+    return a.in[e];
+  } else if constexpr (MODE == PM_PRIMAL) {
+    const double v = __ldg(a.x + a.G[e]) - a.lam[e] / a.rho;  // H_k x - lambda_k / rho
+    return r == c ? v : v * kInvSqrt2;
+  } else {
+    const double v = a.vk[e] - a.lam[e] / a.rho;              // v_k - lambda_k / rho
+    return r == c ? v : v * kInvSqrt2;
+  }
+}
+
+// per-matrix workspace (doubles)
+struct GView {
+  double* p;
+  int k, H;
+  __host__ __device__ static int ld_of(int k) { return (k + 3) & ~3; }
+  __device__ int ld() const { return ld_of(k); }
+  __device__ double* M() const { return p; }                        // full symmetric, row-major; v_j in row j
+  __device__ double* d() const { return p + (int64_t)k * ld(); }
+  __device__ double* e() const { return d() + k; }
+  __device__ double* tau() const { return e() + k; }
+  __device__ double* lall() const { return tau() + k; }            // all eigenvalues (bisection)
+  __device__ double* lsel() const { return lall() + k; }           // selected eigenvalues (shifts)
+  __device__ double* lw() const { return lsel() + H; }             // reconstruction weights
+  __device__ double* clst() const { return lw() + H; }             // cluster leaders
+  __device__ double* gsr() const { return clst() + H; }            // vector-kernel groups: first index
+  // hdr: nsel, side, ||T|| (scaled), pivmin, scale, Gershgorin lo, hi, index of the first selected
+  __device__ double* hdr() const { return gsr() + H; }
+  __device__ double* Z() const { return hdr() + 8; }               // k x H, [i][j]
+  __device__ double* iv() const { return Z() + (int64_t)k * H; }   // 3 x k x H LU factors + pivot words
+};
+__host__ __device__ inline int64_t gview_doubles(int k) {
+  const int64_t H = k;
+  return (int64_t)k * GView::ld_of(k) + 4 * k + 4 * H + 8 + 4 * (int64_t)k * H + ((k + 63) / 64) * H + 4;
+}
+
+// ---------------------------------------------------------------- 1. tridiagonalization
+// Jobs: a thread-block cluster of TC_CS CTAs either reduces one large matrix together ("coop",
+// k >= SDP_GTRD_COOP_MIN) or each of its CTAs reduces one smaller matrix alone ("solo").
+// In a coop job, CTA r owns the 32-column chunks r, r + TC_CS, ... of the matrix (full height):
+// the symmetric product A22 v and the trailing update touch only owned columns, so the matrix
+// streams from L2 into TC_CS SMs at once.  Everything that needs whole vectors (the updated row
+// j, its norm, v, V^T v / W^T v, w) is computed redundantly and identically in every CTA from
+// the replicated panel V / W; the one exchange per column is A22 v (each owner writes its part
+// into every CTA's shared memory, double-buffered by column parity) followed by one cluster
+// barrier; one more cluster barrier per panel publishes the trailing update.
+namespace cg = cooperative_groups;
+constexpr int TC_NT = 512;
+constexpr int TC_NB = 6;
+constexpr int TC_CS = 8;
+constexpr int TC_NR = 1 + 2 * TC_NB;  // block-reduced values per column: |x|^2, W^T x, V^T x
+constexpr int TC_PS = GT_KMAX > TC_NT ? GT_KMAX : TC_NT;
+constexpr size_t kTriSmem =
+    (size_t)(2 * TC_NB * GT_KMAX + 3 * GT_KMAX + TC_PS + 32 * TC_NR + TC_NR + 32 + 4) * sizeof(double);
+
+template <int MODE>
+__global__ void __launch_bounds__(TC_NT) k_gtrd_tridiag(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int job = blockIdx.x / TC_CS, rank = blockIdx.x % TC_CS;
+  const bool coop = gt.job_coop[job] != 0;
+  const int g = gt.job_g[job * TC_CS + (coop ? 0 : rank)];
+  if (g < 0) return;  // unused solo slot (never inside a coop cluster)
+  const int ncta = coop ? TC_CS : 1, r = coop ? rank : 0;
+  const int task = gt.task[g];
+  const int k = a.ksz[task];
+  const int t = threadIdx.x;
+  if (k > GT_KMAX) {
+    if (r == 0 && t == 0) gt.status[g] = -1;
+    return;
+  }
+  if (r == 0 && t == 0) gt.status[g] = 0;
+  cg::cluster_group cl = cg::this_cluster();
+  auto csync = [&]() {
+    if (coop)
+      cl.sync();
+    else
+      __syncthreads();
+  };
+  extern __shared__ double smem[];
+  double* Vs = smem;                      // [q][i]
+  double* Ws = Vs + TC_NB * GT_KMAX;
+  double* pbuf = Ws + TC_NB * GT_KMAX;    // [2][GT_KMAX]: tau (A22 v - V y1 - W y2), all columns
+  double* xrow = pbuf + 2 * GT_KMAX;      // updated row j
+  double* psum = xrow + GT_KMAX;          // TC_PS partial sums
+  double* red = psum + TC_PS;             // 32 x TC_NR
+  double* yv = red + 32 * TC_NR;          // TC_NR
+  double* red1 = yv + TC_NR;              // 32
+  const GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
+  const int LD = W.ld();
+  double* M = W.M();
+  const int64_t off = a.off[task];
+  // load (both triangles), split over the job's CTAs
+  const int ns = k * (k + 1) / 2;
+  for (int e = r * TC_NT + t; e < ns; e += ncta * TC_NT) {
+    int rr, c;
+    packed_rc(e, rr, c);
+    const double v = input_value<MODE>(a, off + e, rr, c);
+    M[(int64_t)rr * LD + c] = v;
+    M[(int64_t)c * LD + rr] = v;
+  }
+  for (int e = t; e < 2 * TC_NB * GT_KMAX; e += TC_NT) smem[e] = 0.0;
+  csync();
+  const int nchunk = (k + 31) >> 5;
+  const int nown = (nchunk > r ? (nchunk - r + ncta - 1) / ncta : 0) * 32;  // owned columns (may pass k)
+  auto own_col = [&](int oc) { return ((oc >> 5) * ncta + r) * 32 + (oc & 31); };
+  auto first_oc = [&](int col) {  // first owned-column index of the chunks that reach column col
+    const int cj = col >> 5;
+    return (cj > r ? (cj - r + ncta - 1) / ncta : 0) * 32;
+  };
+  const int wid = t >> 5, lane = t & 31;
+  for (int j0 = 0; j0 + 2 < k; j0 += TC_NB) {
+    const int nbp = min(TC_NB, k - 2 - j0);
+    for (int c = 0; c < nbp; ++c) {
+      const int j = j0 + c;
+      // (a) row j (== column j) from j on, with the panel's previous reflectors applied;
+      //     partial sums of |x|^2, W^T x, V^T x over x = A(j+2:k, j)
+      double part[TC_NR];
+#pragma unroll
+      for (int q = 0; q < TC_NR; ++q) part[q] = 0.0;
+      for (int i = j + t; i < k; i += TC_NT) {
+        double x = __ldcg(M + (int64_t)j * LD + i);
+        for (int q = 0; q < c; ++q) x -= fma(Vs[q * GT_KMAX + i], Ws[q * GT_KMAX + j], Ws[q * GT_KMAX + i] * Vs[q * GT_KMAX + j]);
+        xrow[i] = x;
+        if (i >= j + 2) {
+          part[0] = fma(x, x, part[0]);
+#pragma unroll
+          for (int q = 0; q < TC_NB; ++q) {
+            part[1 + q] = fma(Ws[q * GT_KMAX + i], x, part[1 + q]);
+            part[1 + TC_NB + q] = fma(Vs[q * GT_KMAX + i], x, part[1 + TC_NB + q]);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < TC_NR; ++q) {
+        const double v = warp_sum(part[q]);
+        if (lane == 0) red[wid * TC_NR + q] = v;
+      }
+      __syncthreads();
+      if (t < TC_NR) {
+        double sacc = 0.0;
+        for (int w = 0; w < TC_NT / 32; ++w) sacc += red[w * TC_NR + t];
+        yv[t] = sacc;
+      }
+      __syncthreads();
+      // (b) Householder vector of x (dlarfg); y1 = W^T v, y2 = V^T v
+      const double alpha = xrow[j + 1], sig = yv[0];
+      double tau = 0.0, beta = alpha, scl = 0.0;
+      if (sig > 0.0) {
+        const double nrm = sqrt(fma(alpha, alpha, sig));
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scl = 1.0 / (alpha - beta);
+      }
+      for (int i = j + 1 + t; i < k; i += TC_NT) {
+        const double vi = i == j + 1 ? 1.0 : xrow[i] * scl;
+        Vs[c * GT_KMAX + i] = vi;
+        if (r == 0 && i >= j + 2) M[(int64_t)i * LD + j] = vi;  // v_j kept in column j (back-transform)
+      }
+      if (r == 0 && t == 0) {
+        W.d()[j] = xrow[j];
+        W.e()[j] = beta;
+        W.tau()[j] = tau;
+      }
+      double y1[TC_NB], y2[TC_NB];
+#pragma unroll
+      for (int q = 0; q < TC_NB; ++q) {
+        y1[q] = fma(scl, yv[1 + q], Ws[q * GT_KMAX + j + 1]);
+        y2[q] = fma(scl, yv[1 + TC_NB + q], Vs[q * GT_KMAX + j + 1]);
+      }
+      __syncthreads();
+      if (tau != 0.0) {  // identical in every CTA of the job
+        // (c) p = tau (A22 v - V y1 - W y2) on the owned columns, rows split in G groups
+        const double* Vc = Vs + c * GT_KMAX;
+        const int oc0 = first_oc(j + 1);
+        const int nact = nown - oc0;
+        const int G = nact > 0 ? max(1, min(8, TC_NT / nact)) : 1;
+        for (int it = t; it < nact * G; it += TC_NT) {
+          const int oc = oc0 + it % nact, gg = it / nact;
+          const int col = own_col(oc);
+          double pacc = 0.0;
+          if (col > j && col < k) {
+            int l = j + 1 + gg;
+            const int64_t st = (int64_t)G * LD;
+            const double* Ml = M + (int64_t)l * LD + col;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+            for (; l < k; l += 16 * G, Ml += 16 * st) {  // 16 rows in flight (the last batch masked)
+              double m[16], vv[16];
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const bool in = l + u * G < k;
+                m[u] = in ? __ldcg(Ml + u * st) : 0.0;
+                vv[u] = in ? Vc[l + u * G] : 0.0;
+              }
+#pragma unroll
+              for (int u = 0; u < 16; u += 4) {
+                a0 = fma(m[u], vv[u], a0);
+                a1 = fma(m[u + 1], vv[u + 1], a1);
+                a2 = fma(m[u + 2], vv[u + 2], a2);
+                a3 = fma(m[u + 3], vv[u + 3], a3);
+              }
+            }
+            pacc = (a0 + a1) + (a2 + a3);
+          }
+          psum[it] = pacc;
+        }
+        __syncthreads();
+        double* pb = pbuf + (j & 1) * GT_KMAX;
+        for (int oc = oc0 + t; oc < nown; oc += TC_NT) {
+          const int col = own_col(oc);
+          if (col <= j || col >= k) continue;
+          double p = 0.0;
+          for (int gg = 0; gg < G; ++gg) p += psum[gg * nact + (oc - oc0)];
+#pragma unroll
+          for (int q = 0; q < TC_NB; ++q) p -= fma(Vs[q * GT_KMAX + col], y1[q], Ws[q * GT_KMAX + col] * y2[q]);
+          p *= tau;
+          if (coop) {
+            for (int rr = 0; rr < TC_CS; ++rr) cl.map_shared_rank(pb, rr)[col] = p;
+          } else {
+            pb[col] = p;
+          }
+        }
+        csync();
+        // K = (tau / 2) p.v ; w = p - K v   (whole vectors, every CTA)
+        double kp = 0.0;
+        for (int i = j + 1 + t; i < k; i += TC_NT) kp = fma(pb[i], Vc[i], kp);
+        kp = warp_sum(kp);
+        if (lane == 0) red1[wid] = kp;
+        __syncthreads();
+        double K = 0.0;
+        for (int w = 0; w < TC_NT / 32; ++w) K += red1[w];
+        K *= 0.5 * tau;
+        for (int i = j + 1 + t; i < k; i += TC_NT) Ws[c * GT_KMAX + i] = pb[i] - K * Vc[i];
+      }
+      __syncthreads();
+    }
+    // trailing rank-2*nbp update of the owned columns >= J, rows >= J
+    const int J = j0 + nbp;
+    {
+      const int oc0 = first_oc(J);
+      const int nact = nown - oc0;
+      const int G = nact > 0 ? max(1, TC_NT / nact) : 1;
+      for (int it = t; it < nact * G; it += TC_NT) {
+        const int oc = oc0 + it % nact, gg = it / nact;
+        const int col = own_col(oc);
+        if (col < J || col >= k) continue;
+        double vr[TC_NB], wr[TC_NB];
+#pragma unroll
+        for (int q = 0; q < TC_NB; ++q) {
+          vr[q] = Vs[q * GT_KMAX + col];
+          wr[q] = Ws[q * GT_KMAX + col];
+        }
+        auto upd = [&](int row) {
+          double acc = 0.0;
+#pragma unroll
+          for (int q = 0; q < TC_NB; ++q) acc = fma(Vs[q * GT_KMAX + row], wr[q], fma(Ws[q * GT_KMAX + row], vr[q], acc));
+          return acc;
+        };
+        int l = J + gg;
+        const int64_t st = (int64_t)G * LD;
+        double* Ml = M + (int64_t)l * LD + col;
+        for (; l < k; l += 8 * G, Ml += 8 * st) {  // 8 rows per round (the last masked): loads, then stores
+          double m[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) m[u] = l + u * G < k ? __ldcg(Ml + u * st) : 0.0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (l + u * G < k) Ml[u * st] = m[u] - upd(l + u * G);
+        }
+      }
+    }
+    csync();
+    for (int e = t; e < 2 * TC_NB * GT_KMAX; e += TC_NT) smem[e] = 0.0;
+    __syncthreads();
+  }
+  if (r != 0) return;
+  // T (d, e) into shared memory; the last 2x2 block from the reduced matrix
+  double* d = xrow;
+  double* e = pbuf;
+  for (int i = t; i < k; i += TC_NT) {
+    d[i] = i < k - 2 ? W.d()[i] : __ldcg(M + (int64_t)i * LD + i);
+    e[i] = i < k - 2 ? W.e()[i] : (i == k - 2 ? __ldcg(M + (int64_t)i * LD + i + 1) : 0.0);
+  }
+  __syncthreads();
+  if (t == 0) {
+    // T scaled by a power of two (max entry in [1, 2)), Gershgorin interval, ||T||,
+    // inertia at 0 (exact Sturm count)
+    double mx = 0.0;
+    for (int i = 0; i < k; ++i) mx = fmax(mx, fmax(fabs(d[i]), fabs(e[i])));
+    const double sc = mx > 0.0 ? scalbn(1.0, -ilogb(mx)) : 1.0;
+    double gl = 0.0, gu = 0.0, tn = 0.0, me2 = 0.0;
+    for (int i = 0; i < k; ++i) {
+      d[i] *= sc;
+      e[i] *= sc;
+    }
+    for (int i = 0; i < k; ++i) {
+      const double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + fabs(e[i]);
+      gl = i ? fmin(gl, d[i] - rad) : d[i] - rad;
+      gu = i ? fmax(gu, d[i] + rad) : d[i] + rad;
+      tn = fmax(tn, fabs(d[i]) + rad);
+      me2 = fmax(me2, e[i] * e[i]);
+    }
+    const double pivmin = 1e-290 * fmax(1.0, me2);
+    double q = d[0];
+    if (fabs(q) < pivmin) q = -pivmin;
+    int nneg = q < 0.0;
+    for (int i = 1; i < k; ++i) {
+      q = d[i] - e[i - 1] * e[i - 1] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      nneg += q < 0.0;
+    }
+    const double w = gu - gl;
+    double* h = W.hdr();
+    h[0] = 0;  // k_gtrd_cluster decides the side and the count
+    h[1] = 0;
+    h[2] = tn;
+    h[3] = pivmin;
+    h[4] = sc;
+    h[5] = gl - 2.0 * kEps * fabs(gl) - 2.0 * kEps * w - pivmin;
+    h[6] = gu + 2.0 * kEps * fabs(gu) + 2.0 * kEps * w + pivmin;
+    h[7] = nneg;
+  }
+  __syncthreads();
+  for (int i = t; i < k; i += TC_NT) {
+    W.d()[i] = d[i];
+    W.e()[i] = e[i];
+  }
+}
+
+// ---------------------------------------------------------------- 2. eigenvalues and vectors of T
+// Work items: per giant ceil(H / 32) warps, thread s of the giant <-> selected eigenvalue s.
+__device__ __forceinline__ int find_item(const int32_t* pre, int ng, int item) {
+  int lo = 0, hi = ng - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (pre[mid] <= item) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// 1/q to ~2^-44 relative (approximate reciprocal + one Newton step): a Sturm count with these
+// quotients is the exact count of a relative ~1e-13 perturbation of T
+__device__ __forceinline__ double rcp_fast(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+  return fma(r, fma(-q, r, 1.0), r);
+}
+
+// Multisection (3 shifts per pass, 2 bits per pass) for every eigenvalue (the idx-th smallest) of the
+// scaled T; Sturm counts of the LDL^T pivots with the LAPACK pivmin guard (dstebz), stopped at
+// width <= 1e-11 ||T|| (the vectors then come from inverse iteration, the weights from Rayleigh
+// quotients, so the shift only has to separate the eigenvalue from its neighbours' clusters)
+__global__ void __launch_bounds__(32) k_gtrd_bisect(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int g = find_item(gt.ev_pre, gt.ng, blockIdx.x);
+  if (gt.status[g] < 0) return;
+  const int k = a.ksz[gt.task[g]];
+  const GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
+  const double* h = W.hdr();
+  const int s = (blockIdx.x - gt.ev_pre[g]) * 32 + threadIdx.x;
+  extern __shared__ double sm[];
+  double* d = sm;
+  double* e2 = sm + k;
+  for (int i = threadIdx.x; i < k; i += 32) {
+    d[i] = W.d()[i];
+    const double ei = W.e()[i];
+    e2[i] = ei * ei;
+  }
+  __syncwarp();
+  if (s >= k) return;
+  const int idx = s;
+  const double pivmin = h[3], tol = 1e-11 * fmax(h[2], 1e-300);
+  double lo = h[5], hi = h[6];
+  for (int it = 0; it < 40 && hi - lo > tol; ++it) {
+    const double w = 0.25 * (hi - lo);
+    const double s1 = lo + w, s2 = lo + 2.0 * w, s3 = hi - w;
+    double q1 = d[0] - s1, q2 = d[0] - s2, q3 = d[0] - s3;
+    if (fabs(q1) < pivmin) q1 = -pivmin;
+    if (fabs(q2) < pivmin) q2 = -pivmin;
+    if (fabs(q3) < pivmin) q3 = -pivmin;
+    int c1 = q1 < 0.0, c2 = q2 < 0.0, c3 = q3 < 0.0;
+    for (int i = 1; i < k; ++i) {
+      const double di = d[i], ei = e2[i - 1];
+      q1 = (di - s1) - ei * rcp_fast(q1);
+      q2 = (di - s2) - ei * rcp_fast(q2);
+      q3 = (di - s3) - ei * rcp_fast(q3);
+      if (fabs(q1) < pivmin) q1 = -pivmin;
+      if (fabs(q2) < pivmin) q2 = -pivmin;
+      if (fabs(q3) < pivmin) q3 = -pivmin;
+      c1 += q1 < 0.0;
+      c2 += q2 < 0.0;
+      c3 += q3 < 0.0;
+    }
+    // count(x) <= idx  <=>  eigenvalue idx >= x
+    if (c3 <= idx) lo = s3;
+    else if (c2 <= idx) { lo = s2; hi = s3; }
+    else if (c1 <= idx) { lo = s1; hi = s2; }
+    else hi = s1;
+  }
+  W.lall()[s] = 0.5 * (lo + hi);
+}
+
+// Side and clusters.  Clusters: runs of eigenvalues with gaps <= 1e-3 ||T|| (dstein's ortol).
+// The side of 0 whose eigenvectors are computed is the one with fewer eigenvalues, unless it
+// has a cluster of more than 32 (the vector kernel orthogonalises a cluster inside one warp) and
+// the other side has none: ADMM iterates on max-cut cliques develop a large near-degenerate
+// negative eigenvalue cluster while the positive side stays well separated.  Both sides with
+// such a cluster hand the matrix to the block-Jacobi fallback.  Then: distinct shifts inside
+// the clusters, and the groups of the vector kernel (consecutive whole clusters packed
+// first-fit into groups of <= 32 indices, <= 2 ceil(k / 32) + 1 groups).  One thread per giant.
+__global__ void k_gtrd_cluster(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= gt.ng || gt.status[g] < 0) return;
+  const int k = a.ksz[gt.task[g]];
+  const GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
+  double* h = W.hdr();
+  const double tn = h[2], ortol = 1e-3 * tn, pertol = 10.0 * kEps * tn;
+  const double* la = W.lall();
+  const int nneg = (int)h[7];
+  auto max_cluster = [&](int b, int e) {
+    int m = 0, run = 0;
+    for (int t = b; t < e; ++t) {
+      if (t == b || la[t] - la[t - 1] > ortol) run = 0;
+      m = max(m, ++run);
+    }
+    return m;
+  };
+  const bool okn = max_cluster(0, nneg) <= 32, okp = max_cluster(nneg, k) <= 32;
+  int side = (k - nneg) <= nneg ? 0 : 1;
+  if (side == 0 && !okp && okn) side = 1;
+  if (side == 1 && !okn && okp) side = 0;
+  const int nsel = side ? nneg : k - nneg, base = side ? 0 : nneg;
+  h[0] = nsel;
+  h[1] = side;
+  double* ls = W.lsel();
+  for (int t = 0; t < nsel; ++t) ls[t] = la[base + t];
+  double* cl = W.clst();
+  double* gs = W.gsr();
+  int lead = 0, grp = 0, gbeg = 0;
+  bool big = !okn && !okp;
+  for (int s = 0; s <= nsel; ++s) {
+    const bool newc = s == nsel || s == 0 || ls[s] - ls[s - 1] > ortol;
+    if (newc && s > 0) {
+      // cluster [lead, s) is complete: place it
+      if (s - lead > 32) big = true;
+      if (s - gbeg > 32 && !big) {  // does not fit the open group: close it at lead
+        gs[grp++] = gbeg;
+        gbeg = lead;
+      }
+    }
+    if (s == nsel) break;
+    if (newc) lead = s;
+    cl[s] = (double)lead;
+    if (s > lead && ls[s] - ls[s - 1] < pertol) ls[s] = ls[s - 1] + pertol;
+  }
+  if (nsel > 0) gs[grp++] = gbeg;
+  gs[grp] = nsel;  // sentinel
+  if (gt.debug) {
+    int ncl = 0, cmax = 0, run = 0;
+    for (int s = 0; s < nsel; ++s) {
+      if ((int)cl[s] == s) {
+        ++ncl;
+        run = 0;
+      }
+      cmax = max(cmax, ++run);
+    }
+    printf("gtrd giant %d k %d nneg %d side %d nsel %d clusters %d max %d groups %d%s\n", g, k, nneg, side, nsel, ncl,
+           cmax, grp, big ? " FALLBACK" : "");
+  }
+  if (big) gt.status[g] = -1;
+  gt.ngrp[g] = grp;
+}
+
+// Inverse iteration (LAPACK dstein) for one group of <= 32 selected eigenvalues per warp, one
+// thread per eigenvalue: partial-pivoting LU of T - lam I in global memory ([i][s], coalesced,
+// loads batched 8 deep), the iterate in shared memory (column per thread), 3 solves from a
+// deterministic start vector, each followed by normalisation and modified Gram-Schmidt inside
+// the cluster (members are consecutive threads of the warp).  Weight of vector z: its Rayleigh
+// quotient z^T T z clipped at 0 on the selected side; a residual ||T z - rq z||_inf above
+// 1e-9 ||T|| hands the matrix to the fallback.
+constexpr int VB = 8;
+__global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int g = find_item(gt.vg_pre, gt.ng, blockIdx.x);
+  const int grp = blockIdx.x - gt.vg_pre[g];
+  if (gt.status[g] < 0 || grp >= gt.ngrp[g]) return;
+  const int k = a.ksz[gt.task[g]];
+  const int H = gt.hsel[g];
+  const GView W{gt.ws + gt.moff[g], k, H};
+  const double* hd = W.hdr();
+  const int side = (int)hd[1];
+  const int sb = (int)W.gsr()[grp], se = (int)W.gsr()[grp + 1];
+  const int t = threadIdx.x;
+  const int s = sb + t;
+  const bool act = s < se;
+  extern __shared__ double sm[];
+  double* d = sm;
+  double* e = sm + k;
+  double* xs = sm + 2 * k;  // [i][32]
+  for (int i = t; i < k; i += 32) {
+    d[i] = W.d()[i];
+    e[i] = W.e()[i];
+  }
+  const int lead = act ? (int)W.clst()[s] : -1;
+  __syncwarp();
+  const double tn = hd[2], sc = hd[4];
+  const double tol = kEps * fmax(tn, 1e-300);
+  double* ui = W.iv();
+  double* u2 = ui + (int64_t)k * H;
+  double* mu = u2 + (int64_t)k * H;
+  uint64_t* pw = reinterpret_cast<uint64_t*>(mu + (int64_t)k * H);  // [i / 64][s]
+  double* x = xs + t;  // element i at x[i * 32]
+  if (act) {
+    const double lam = W.lsel()[s];
+    // partial-pivoting LU of T - lam I (dlagtf); pivots below tol -> +-tol, stored inverted;
+    // the second superdiagonal of U is e[i+1] where row i pivoted, else 0
+    double r0 = d[0] - lam, r1 = e[0];
+    uint64_t word = 0ull;
+    for (int i = 0; i + 1 < k; ++i) {
+      const double ci = e[i], ai = d[i + 1] - lam, bi = e[i + 1];  // e[k-1] == 0
+      double p1, p2, m;
+      const bool pv = fabs(ci) > fabs(r0);
+      if (pv) {
+        p1 = ci;
+        p2 = ai;
+        m = r0 / ci;
+        r0 = r1 - m * ai;
+        r1 = -m * bi;
+      } else {
+        p1 = r0;
+        p2 = r1;
+        m = r0 != 0.0 ? ci / r0 : 0.0;
+        r0 = ai - m * r1;
+        r1 = bi;
+      }
+      if (fabs(p1) < tol) p1 = p1 < 0.0 ? -tol : tol;
+      ui[(int64_t)i * H + s] = 1.0 / p1;
+      u2[(int64_t)i * H + s] = p2;
+      mu[(int64_t)i * H + s] = m;
+      word |= (uint64_t)pv << (i & 63);
+      if ((i & 63) == 63) {
+        pw[(int64_t)(i >> 6) * H + s] = word;
+        word = 0ull;
+      }
+    }
+    if (((k - 2) & 63) != 63) pw[(int64_t)((k - 2) >> 6) * H + s] = word;  // the last partial word
+    if (fabs(r0) < tol) r0 = r0 < 0.0 ? -tol : tol;
+    ui[(int64_t)(k - 1) * H + s] = 1.0 / r0;
+    for (int i = 0; i < k; ++i) {  // deterministic start vector in [-1, 1]
+      unsigned long long hh = (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull ^
+                              (unsigned long long)(s + 7) * 0xD1B54A32D192ED03ull;
+      hh ^= hh >> 31;
+      hh *= 0xBF58476D1CE4E5B9ull;
+      hh ^= hh >> 29;
+      x[i * 32] = (double)(hh >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    }
+  }
+  // does any cluster of this group have more than one member?
+  const bool multi = __any_sync(0xffffffffu, act && (s > lead || (s + 1 < se && (int)W.clst()[s + 1] == s)));
+  for (int it = 0; it < 3; ++it) {
+    if (act) {
+      // forward: L^{-1} x (row interchanges as recorded)
+      double ry = x[0];
+      int i = 0;
+      for (; i + VB < k; i += VB) {
+        double m[VB];
+#pragma unroll
+        for (int u = 0; u < VB; ++u) m[u] = mu[(int64_t)(i + u) * H + s];
+        const uint64_t wd = pw[(int64_t)(i >> 6) * H + s];  // i .. i+7 share a word (VB | 64)
+#pragma unroll
+        for (int u = 0; u < VB; ++u) {
+          const double yn = x[(i + 1 + u) * 32];
+          if ((wd >> ((i + u) & 63)) & 1ull) {
+            x[(i + u) * 32] = yn;
+            ry = fma(-m[u], yn, ry);
+          } else {
+            x[(i + u) * 32] = ry;
+            ry = fma(-m[u], ry, yn);
+          }
+        }
+      }
+      for (; i + 1 < k; ++i) {
+        const double yn = x[(i + 1) * 32], m = mu[(int64_t)i * H + s];
+        if ((pw[(int64_t)(i >> 6) * H + s] >> (i & 63)) & 1ull) {
+          x[i * 32] = yn;
+          ry = fma(-m, yn, ry);
+        } else {
+          x[i * 32] = ry;
+          ry = fma(-m, ry, yn);
+        }
+      }
+      // backward: U^{-1}
+      double xn = ry * ui[(int64_t)(k - 1) * H + s], xn1 = 0.0;
+      x[(k - 1) * 32] = xn;
+      double mx = fabs(xn);
+      i = k - 2;
+      for (; i - (VB - 1) >= 0; i -= VB) {
+        double a2[VB], ai[VB];
+        uint64_t wd[2];
+        wd[0] = pw[(int64_t)(i >> 6) * H + s];
+        wd[1] = pw[(int64_t)((i - VB + 1) >> 6) * H + s];
+#pragma unroll
+        for (int u = 0; u < VB; ++u) {
+          a2[u] = u2[(int64_t)(i - u) * H + s];
+          ai[u] = ui[(int64_t)(i - u) * H + s];
+        }
+#pragma unroll
+        for (int u = 0; u < VB; ++u) {
+          const int r = i - u;
+          const uint64_t w = ((r >> 6) == (i >> 6)) ? wd[0] : wd[1];
+          const double u3 = ((w >> (r & 63)) & 1ull) ? e[r + 1] : 0.0;
+          const double xi = (x[r * 32] - a2[u] * xn - u3 * xn1) * ai[u];
+          x[r * 32] = xi;
+          mx = fmax(mx, fabs(xi));
+          xn1 = xn;
+          xn = xi;
+        }
+      }
+      for (; i >= 0; --i) {
+        const double u3 = ((pw[(int64_t)(i >> 6) * H + s] >> (i & 63)) & 1ull) ? e[i + 1] : 0.0;
+        const double xi = (x[i * 32] - u2[(int64_t)i * H + s] * xn - u3 * xn1) * ui[(int64_t)i * H + s];
+        x[i * 32] = xi;
+        mx = fmax(mx, fabs(xi));
+        xn1 = xn;
+        xn = xi;
+      }
+      // normalise (scaled by 1/max first so that the sum of squares cannot overflow)
+      const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
+      double nrm = 0.0;
+      for (i = 0; i < k; ++i) {
+        const double v = x[i * 32] * inv;
+        nrm = fma(v, v, nrm);
+      }
+      const double in2 = nrm > 0.0 ? inv / sqrt(nrm) : 0.0;
+      for (i = 0; i < k; ++i) x[i * 32] *= in2;
+    }
+    if (multi) {
+      // modified Gram-Schmidt inside each cluster, in index order
+      for (int p = 0; p < se - sb; ++p) {
+        __syncwarp();
+        const int sp = sb + p;
+        const int lp = (int)W.clst()[sp];
+        const bool mine = act && s > sp && lead == lp;
+        if (!__any_sync(0xffffffffu, mine)) continue;
+        if (mine) {
+          const double* xp = xs + p;
+          double dot = 0.0;
+          for (int i = 0; i < k; ++i) dot = fma(xp[i * 32], x[i * 32], dot);
+          double nrm = 0.0;
+          for (int i = 0; i < k; ++i) {
+            const double v = fma(-dot, xp[i * 32], x[i * 32]);
+            x[i * 32] = v;
+            nrm = fma(v, v, nrm);
+          }
+          const double in2 = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+          for (int i = 0; i < k; ++i) x[i * 32] *= in2;
+        }
+      }
+      __syncwarp();
+    }
+  }
+  if (!act) return;
+  // Rayleigh quotient, residual, output column
+  double rq = 0.0;
+  for (int i = 0; i < k; ++i) {
+    double tz = d[i] * x[i * 32];
+    if (i > 0) tz = fma(e[i - 1], x[(i - 1) * 32], tz);
+    if (i + 1 < k) tz = fma(e[i], x[(i + 1) * 32], tz);
+    rq = fma(x[i * 32], tz, rq);
+  }
+  double res = 0.0;
+  double* Z = W.Z();
+  for (int i = 0; i < k; ++i) {
+    const double xi = x[i * 32];
+    double tz = (d[i] - rq) * xi;
+    if (i > 0) tz = fma(e[i - 1], x[(i - 1) * 32], tz);
+    if (i + 1 < k) tz = fma(e[i], x[(i + 1) * 32], tz);
+    res = fmax(res, fabs(tz));
+    Z[(int64_t)i * H + s] = xi;
+  }
+  if (!(res <= 1e-9 * fmax(tn, 1e-300)) || gt.force_fallback) {  // includes NaN
+    gt.status[g] = -1;
+    if (gt.debug)
+      printf("gtrd giant %d k %d: vector %d (lam %.3e rq %.3e) residual %.2e ||T|| %.2e -> fallback\n", g, k, s,
+             W.lsel()[s], rq, res, tn);
+  }
+  const double lw = side == 0 ? fmax(rq, 0.0) : fmax(-rq, 0.0);
+  W.lw()[s] = lw / sc;
+}
+
+// ---------------------------------------------------------------- 3. back-transform V = Q Z
+// Q = H_0 H_1 ... H_{k-3}; the reflectors are applied in groups of GB_NR from the last one down,
+// each group in compact WY form H_lo ... H_hi = I - Y T Y^T (LAPACK dlarft, forward): Y staged in
+// shared memory, Y^T Y by the CTA's warps, T by warp 0, then per column (a warp, the column in
+// registers) z <- z - Y (T (Y^T z)): one 16-wide warp reduction per group instead of 16.
+constexpr int GB_NT = 512;   // 16 warps = 16 columns
+constexpr int GB_NR = 16;    // reflectors per group
+
+__global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int item = blockIdx.x;
+  const int g = find_item(gt.bt_pre, gt.ng, item);
+  if (gt.status[g] < 0) return;
+  const int k = a.ksz[gt.task[g]];
+  const int H = gt.hsel[g];
+  const GView W{gt.ws + gt.moff[g], k, H};
+  const int nsel = (int)W.hdr()[0];
+  const int col0 = (item - gt.bt_pre[g]) * (GB_NT / 32);
+  if (col0 >= nsel) return;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int col = col0 + wid;
+  extern __shared__ double vb[];          // Y: GB_NR x GT_KMAX
+  double* Gm = vb + GB_NR * GT_KMAX;      // Y^T Y (upper)
+  double* Tm = Gm + GB_NR * GB_NR;        // T (upper)
+  const double* M = W.M();
+  const int LD = W.ld();
+  double* Z = W.Z();
+  double z[GT_RT];
+#pragma unroll
+  for (int r = 0; r < GT_RT; ++r) {
+    const int i = lane + 32 * r;
+    z[r] = (col < nsel && i < k) ? Z[(int64_t)i * H + col] : 0.0;
+  }
+  for (int jhi = k - 3; jhi >= 0; jhi -= GB_NR) {
+    const int nr = min(GB_NR, jhi + 1);
+    const int jlo = jhi - nr + 1;           // Y column c <-> reflector jlo + c
+    __syncthreads();
+    for (int e = threadIdx.x; e < GB_NR * k; e += GB_NT) {  // v_j lives in column j: c fastest
+      const int c = e % GB_NR, i = e / GB_NR;
+      const int j = jlo + c;
+      vb[c * GT_KMAX + i] = (c >= nr || i < j + 1) ? 0.0 : (i == j + 1 ? 1.0 : M[(int64_t)i * LD + j]);
+    }
+    __syncthreads();
+    // Gram matrix Y^T Y, pairs a < b (rows below jlo are zero in every column)
+    for (int pr = wid; pr < GB_NR * (GB_NR - 1) / 2; pr += GB_NT / 32) {
+      int aa = 0, rem = pr;
+      while (rem >= GB_NR - 1 - aa) {
+        rem -= GB_NR - 1 - aa;
+        ++aa;
+      }
+      const int bb = aa + 1 + rem;
+      double sacc = 0.0;
+      if (bb < nr)
+        for (int i = jlo + 1 + lane; i < k; i += 32) sacc = fma(vb[aa * GT_KMAX + i], vb[bb * GT_KMAX + i], sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) Gm[aa * GB_NR + bb] = sacc;
+    }
+    __syncthreads();
+    if (wid == 0) {
+      // T[c][c] = tau_c;  T[0:c, c] = -tau_c T[0:c, 0:c] (Y^T y_c)[0:c]
+      for (int c = 0; c < GB_NR; ++c) {
+        const double tau = c < nr ? W.tau()[jlo + c] : 0.0;
+        double tv = 0.0;
+        if (lane < c)
+          for (int q = lane; q < c; ++q) tv = fma(Tm[lane * GB_NR + q], Gm[q * GB_NR + c], tv);
+        __syncwarp();
+        if (lane < c) Tm[lane * GB_NR + c] = -tau * tv;
+        if (lane == c) Tm[c * GB_NR + c] = tau;
+        if (lane > c && lane < GB_NR) Tm[lane * GB_NR + c] = 0.0;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    if (col < nsel) {
+      double w[GB_NR];
+#pragma unroll
+      for (int c = 0; c < GB_NR; ++c) w[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < GT_RT; ++r) {
+        const int i = lane + 32 * r;
+        if (i < k && i > jlo) {
+#pragma unroll
+          for (int c = 0; c < GB_NR; ++c) w[c] = fma(vb[c * GT_KMAX + i], z[r], w[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < GB_NR; ++c) w[c] = warp_sum(w[c]);
+      // u = T w (T upper), kept in w (row c needs w[c..] only: ascending order is safe)
+#pragma unroll
+      for (int c = 0; c < GB_NR; ++c) {
+        double u = 0.0;
+#pragma unroll
+        for (int q = c; q < GB_NR; ++q) u = fma(Tm[c * GB_NR + q], w[q], u);
+        w[c] = u;
+      }
+#pragma unroll
+      for (int r = 0; r < GT_RT; ++r) {
+        const int i = lane + 32 * r;
+        if (i < k && i > jlo) {
+          double acc = z[r];
+#pragma unroll
+          for (int c = 0; c < GB_NR; ++c) acc = fma(-vb[c * GT_KMAX + i], w[c], acc);
+          z[r] = acc;
+        }
+      }
+    }
+  }
+  if (col < nsel) {
+#pragma unroll
+    for (int r = 0; r < GT_RT; ++r) {
+      const int i = lane + 32 * r;
+      if (i < k) Z[(int64_t)i * H + col] = z[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- 4. reconstruction
+constexpr int GR_NW = 8;
+constexpr int GR_LDS = 36;
+struct GrSmem {
+  double X[32 * GR_LDS];
+  double Y[32 * GR_LDS];
+};
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(GR_NW * 32) k_gtrd_recon(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  GrSmem& sm = reinterpret_cast<GrSmem*>(smraw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31, r4 = lane >> 2, c4 = lane & 3;
+  const int item = blockIdx.x * GR_NW + (threadIdx.x >> 5);
+  if (item >= gt.tot_rc) return;
+  int g = 0;
+  {
+    int lo = 0, hi = gt.ng - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (gt.rc_pre[mid] <= item) lo = mid; else hi = mid - 1;
+    }
+    g = lo;
+  }
+  if (gt.status[g] < 0) return;
+  const int task = gt.task[g];
+  const int k = a.ksz[task];
+  const int H = gt.hsel[g];
+  const GView W{gt.ws + gt.moff[g], k, H};
+  const int nsel = (int)W.hdr()[0], side = (int)W.hdr()[1];
+  int rb, cb;
+  packed_rc(item - gt.rc_pre[g], rb, cb);
+  const double* Z = W.Z();
+  double acc[4][4][2];
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[p][q][0] = acc[p][q][1] = 0.0;
+  for (int kk = 0; kk < nsel; kk += 32) {
+    __syncwarp();
+    for (int e = lane; e < 1024; e += 32) {
+      const int m = e >> 5, u = e & 31;
+      const int rr = rb * 32 + m, cc = cb * 32 + m, uu = kk + u;
+      const bool ok = uu < nsel;
+      sm.X[m * GR_LDS + u] = (ok && rr < k) ? Z[(int64_t)rr * H + uu] * W.lw()[uu] : 0.0;  // [m][k]
+      sm.Y[m * GR_LDS + u] = (ok && cc < k) ? Z[(int64_t)cc * H + uu] : 0.0;               // [n][k]
+    }
+    __syncwarp();
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        af[q] = sm.X[(q * 8 + r4) * GR_LDS + ks * 4 + c4];
+        bf[q] = sm.Y[(q * 8 + r4) * GR_LDS + ks * 4 + c4];
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dmma(acc[p][q], af[p], bf[q]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int p = 0; p < 4; ++p)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      sm.X[(p * 8 + r4) * GR_LDS + q * 8 + 2 * c4] = acc[p][q][0];
+      sm.X[(p * 8 + r4) * GR_LDS + q * 8 + 2 * c4 + 1] = acc[p][q][1];
+    }
+  __syncwarp();
+  const int64_t off = a.off[task];
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+  for (int e = lane; e < 1024; e += 32) {
+    const int jj = e >> 5, ii = e & 31;  // column-major walk: consecutive packed entries
+    const int r = rb * 32 + ii, c = cb * 32 + jj;
+    if (r > c || c >= k) continue;
+    double v = sm.X[ii * GR_LDS + jj];
+    const int64_t pe = off + (int64_t)c * (c + 1) / 2 + r;
+    if (side == 1) v += input_value<MODE>(a, pe, r, c);
+    if constexpr (MODE == PM_BATCH) {
+      a.out[pe] = v;
+    } else if constexpr (MODE == PM_PRIMAL) {
+      const double xkv = (r == c) ? v : v * kSqrt2;
+      const double hx = __ldg(a.x + a.G[pe]);
+      const double dd = xkv - hx;
+      a.xk[pe] = xkv;
+      a.lam[pe] = a.lam[pe] + a.rho * dd;  // E:LambdakUpdate
+      p0 += dd * dd;
+      p1 += xkv * xkv;
+      p2 += hx * hx;
+    } else {
+      a.xk[pe] = (r == c) ? v : v * kSqrt2;
+    }
+  }
+  if constexpr (MODE == PM_PRIMAL) {
+    p0 = warp_sum(p0);
+    p1 = warp_sum(p1);
+    p2 = warp_sum(p2);
+    if (lane == 0) {
+      gt.part[3 * (int64_t)item + 0] = p0;
+      gt.part[3 * (int64_t)item + 1] = p1;
+      gt.part[3 * (int64_t)item + 2] = p2;
+    }
+  }
+}
+
+__global__ void k_gtrd_fin(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= gt.ng || gt.status[g] < 0) return;
+  const int task = gt.task[g];
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0;
+  for (int t = gt.rc_pre[g]; t < gt.rc_pre[g + 1]; ++t) {
+    p0 += gt.part[3 * (int64_t)t + 0];
+    p1 += gt.part[3 * (int64_t)t + 1];
+    p2 += gt.part[3 * (int64_t)t + 2];
+  }
+  a.part[3 * (int64_t)task + 0] = p0;
+  a.part[3 * (int64_t)task + 1] = p1;
+  a.part[3 * (int64_t)task + 2] = p2;
+}
+
+
+constexpr size_t kBackSmem = (size_t)(GB_NR * GT_KMAX + 2 * GB_NR * GB_NR) * sizeof(double);
+
+template <int MODE>
+void launch_mode(const ProjArgs& a, cudaStream_t s) {
+  const GtrdDev& gt = a.gd.gt;
+  {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gt.njob * TC_CS);
+    cfg.blockDim = dim3(TC_NT);
+    cfg.dynamicSmemBytes = kTriSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = TC_CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_gtrd_tridiag<MODE>, a);
+  }
+  if (gt.tot_ev) {
+    k_gtrd_bisect<<<gt.tot_ev, 32, (size_t)2 * gt.kmax * sizeof(double), s>>>(a);
+    k_gtrd_cluster<<<(gt.ng + 31) / 32, 32, 0, s>>>(a);
+    k_gtrd_vec<<<gt.tot_vg, 32, (size_t)34 * gt.kmax * sizeof(double), s>>>(a);
+  }
+  if (gt.tot_bt) k_gtrd_back<<<gt.tot_bt, GB_NT, kBackSmem, s>>>(a);
+  if (gt.tot_rc) k_gtrd_recon<MODE><<<(gt.tot_rc + GR_NW - 1) / GR_NW, GR_NW * 32, GR_NW * sizeof(GrSmem), s>>>(a);
+  if (MODE == PM_PRIMAL) k_gtrd_fin<<<(gt.ng + 127) / 128, 128, 0, s>>>(a);
+}
+
+template <int MODE>
+void set_attrs() {
+  cudaFuncSetAttribute(k_gtrd_tridiag<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmem);
+  cudaFuncSetAttribute(k_gtrd_recon<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(GR_NW * sizeof(GrSmem)));
+}
+
+}  // namespace
+
+void psd_gtrd_init_attributes() {
+  set_attrs<PM_BATCH>();
+  set_attrs<PM_PRIMAL>();
+  set_attrs<PM_DUAL>();
+
+  cudaFuncSetAttribute(k_gtrd_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(34 * GT_KMAX * sizeof(double)));
+  cudaFuncSetAttribute(k_gtrd_back, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBackSmem);
+}
+
+int gtrd_max_order() { return GT_KMAX; }
+int64_t gtrd_ws_doubles(int k) { return gview_doubles(k); }
+
+void launch_projection_gtrd(int mode, const ProjArgs& a, cudaStream_t s) {
+  if (a.gd.gt.ng <= 0) return;
+  if (mode == PM_BATCH)
+    launch_mode<PM_BATCH>(a, s);
+  else if (mode == PM_PRIMAL)
+    launch_mode<PM_PRIMAL>(a, s);
+  else
+    launch_mode<PM_DUAL>(a, s);
+}
+
+}  // namespace sdp

@@ -378,6 +378,55 @@ def test_giant_tier_small_orders_subprocess(tmp_path):
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+# ------------------------------------------------------------------ giant tier, tridiagonal path
+
+def test_gtrd_batch_orders_and_structured(lib, gen):
+    """Giant orders take the tridiagonal path (Householder + bisection + inverse
+    iteration + WY back-transform): random orders 65..800, structured inputs
+    (zero, identity, repeated / clustered eigenvalues, rank one, +-pairs; the big
+    clusters go to the block-Jacobi fallback) and k = 801 (> the path's maximum,
+    block Jacobi), against the oracle."""
+    rng = np.random.default_rng(12)
+    mats = []
+    for k in (65, 130):
+        mats += _structured(k, rng)
+    ks = [66, 97, 128, 129, 255, 400, 631, 800, 801]
+    vals = [rng.standard_normal(k * (k + 1) // 2) for k in ks]
+    ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)
+    vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)
+    check_batch(lib, ks, vals, tol=1e-12)
+
+
+def _giant_env_batch(env_extra):
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L\n"
+        "from oracle import psd as opsd\n"
+        "rng = np.random.default_rng(6)\n"
+        "ks = np.array([65, 90, 150, 333, 64, 20], np.int32)\n"
+        "vals = np.concatenate([rng.standard_normal(k*(k+1)//2) for k in ks])\n"
+        "out = L.PsdPlan(ks).project_host(vals)\n"
+        "want = opsd.project_psd_packed_batch(ks, vals)\n"
+        "e = np.linalg.norm(out - want) / np.linalg.norm(want)\n"
+        "print(e); assert e <= 1e-12, e\n" % ROOT)
+    env = dict(os.environ, **env_extra)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_gtrd_forced_fallback_subprocess():
+    """SDP_GTRD_FORCE_FALLBACK=1 marks every matrix of the tridiagonal path failed:
+    the block-Jacobi kernel redoes them (GiantDev::only) in the same call."""
+    _giant_env_batch({"SDP_GTRD_FORCE_FALLBACK": "1"})
+
+
+def test_giant_block_jacobi_only_subprocess():
+    """SDP_GIANT_METHOD=jacobi: the giant tier without the tridiagonal path."""
+    _giant_env_batch({"SDP_GIANT_METHOD": "jacobi"})
+
+
 # ------------------------------------------------------------------ tridiagonal-QL tier
 
 def _structured(k, rng):
