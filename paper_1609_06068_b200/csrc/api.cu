@@ -251,7 +251,7 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
     }
     const int R = (k + 31) / 32;
     ev[g + 1] = ev[g] + (ok ? (k + 31) / 32 : 0);
-    vg[g + 1] = vg[g] + (ok ? 2 * ((k + 31) / 32) + 1 : 0);
+    vg[g + 1] = vg[g] + (ok ? 2 * ((k + gtrd_vec_cap(k) - 1) / gtrd_vec_cap(k)) + 1 : 0);
     bt[g + 1] = bt[g] + (ok ? (k + 15) / 16 : 0);
     rc[g + 1] = rc[g] + (ok ? R * (R + 1) / 2 : 0);
   }

@@ -178,6 +178,12 @@ void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_gtrd(int mode, const ProjArgs& a, cudaStream_t s);
+// vector-kernel group capacity of the giant tridiagonal path for order k (shared-memory bound)
+constexpr int kVecSmemDoubles = 26000;
+__host__ __device__ inline int gtrd_vec_cap(int k) {
+  const int c = (kVecSmemDoubles - 2 * k) / (k > 0 ? k : 1);
+  return c < 128 ? c : 128;
+}
 int gtrd_max_order();          // largest order the giant tridiagonal path takes (shared-memory bound)
 int64_t gtrd_ws_doubles(int k);  // workspace of one matrix of order k
 void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t s);

@@ -465,19 +465,23 @@ __global__ void __launch_bounds__(32) k_gtrd_bisect(ProjArgs a) {
 }
 
 // Side and clusters.  Clusters: runs of eigenvalues with gaps <= 1e-3 ||T|| (dstein's ortol).
-// The side of 0 whose eigenvectors are computed is the one with fewer eigenvalues, unless it
-// has a cluster of more than 32 (the vector kernel orthogonalises a cluster inside one warp) and
-// the other side has none: ADMM iterates on max-cut cliques develop a large near-degenerate
-// negative eigenvalue cluster while the positive side stays well separated.  Both sides with
-// such a cluster hand the matrix to the block-Jacobi fallback.  Then: distinct shifts inside
-// the clusters, and the groups of the vector kernel (consecutive whole clusters packed
-// first-fit into groups of <= 32 indices, <= 2 ceil(k / 32) + 1 groups).  One thread per giant.
+// The vector kernel orthogonalises a cluster inside one CTA whose shared memory holds the
+// iterates: cap(k) = min(128, (26000 - 2k) / k) vectors.  The side of 0 whose eigenvectors are
+// computed is the one with fewer eigenvalues, unless it has a cluster larger than cap(k) and the
+// other side has none (ADMM iterates on max-cut cliques develop a dense band of negative
+// eigenvalues while the positive side stays well separated).  A cluster larger than cap(k) is
+// cut at its largest gaps into pieces of <= cap(k) (vectors of different pieces are then
+// orthogonal to eps ||T|| / gap, gap being the largest gap in a window of cap(k) eigenvalues;
+// the residual test below still guards every vector).  Then: distinct shifts inside the pieces
+// and the groups of the vector kernel (consecutive pieces packed first-fit into <= cap(k)
+// indices, <= 2 ceil(k / cap) + 1 groups).  One thread per giant.
 __global__ void k_gtrd_cluster(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= gt.ng || gt.status[g] < 0) return;
   const int k = a.ksz[gt.task[g]];
+  const int cap = gtrd_vec_cap(k);
   const GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
   double* h = W.hdr();
   const double tn = h[2], ortol = 1e-3 * tn, pertol = 10.0 * kEps * tn;
@@ -491,7 +495,7 @@ __global__ void k_gtrd_cluster(ProjArgs a) {
     }
     return m;
   };
-  const bool okn = max_cluster(0, nneg) <= 32, okp = max_cluster(nneg, k) <= 32;
+  const bool okn = max_cluster(0, nneg) <= cap, okp = max_cluster(nneg, k) <= cap;
   int side = (k - nneg) <= nneg ? 0 : 1;
   if (side == 0 && !okp && okn) side = 1;
   if (side == 1 && !okn && okp) side = 0;
@@ -502,50 +506,58 @@ __global__ void k_gtrd_cluster(ProjArgs a) {
   for (int t = 0; t < nsel; ++t) ls[t] = la[base + t];
   double* cl = W.clst();
   double* gs = W.gsr();
-  int lead = 0, grp = 0, gbeg = 0;
-  bool big = !okn && !okp;
-  for (int s = 0; s <= nsel; ++s) {
-    const bool newc = s == nsel || s == 0 || ls[s] - ls[s - 1] > ortol;
-    if (newc && s > 0) {
-      // cluster [lead, s) is complete: place it
-      if (s - lead > 32) big = true;
-      if (s - gbeg > 32 && !big) {  // does not fit the open group: close it at lead
-        gs[grp++] = gbeg;
-        gbeg = lead;
-      }
+  int grp = 0, gbeg = 0, npiece = 0, pmax = 0, nsplit = 0;
+  auto place = [&](int pb, int pe) {  // piece [pb, pe)
+    for (int t = pb; t < pe; ++t) {
+      cl[t] = (double)pb;
+      if (t > pb && ls[t] - ls[t - 1] < pertol) ls[t] = ls[t - 1] + pertol;
     }
-    if (s == nsel) break;
-    if (newc) lead = s;
-    cl[s] = (double)lead;
-    if (s > lead && ls[s] - ls[s - 1] < pertol) ls[s] = ls[s - 1] + pertol;
+    if (pe - gbeg > cap) {  // does not fit the open group: close it at pb
+      gs[grp++] = gbeg;
+      gbeg = pb;
+    }
+    ++npiece;
+    pmax = max(pmax, pe - pb);
+  };
+  for (int s0 = 0; s0 < nsel;) {
+    int e = s0 + 1;
+    while (e < nsel && la[base + e] - la[base + e - 1] <= ortol) ++e;
+    int b = s0;
+    while (e - b > cap) {  // cut at the largest gap among the first cap + 1 eigenvalues
+      int best = b + cap;
+      double bg = -1.0;
+      for (int x = b + 1; x <= b + cap; ++x) {
+        const double gap = la[base + x] - la[base + x - 1];
+        if (gap > bg) {
+          bg = gap;
+          best = x;
+        }
+      }
+      place(b, best);
+      ++nsplit;
+      b = best;
+    }
+    place(b, e);
+    s0 = e;
   }
   if (nsel > 0) gs[grp++] = gbeg;
   gs[grp] = nsel;  // sentinel
-  if (gt.debug) {
-    int ncl = 0, cmax = 0, run = 0;
-    for (int s = 0; s < nsel; ++s) {
-      if ((int)cl[s] == s) {
-        ++ncl;
-        run = 0;
-      }
-      cmax = max(cmax, ++run);
-    }
-    printf("gtrd giant %d k %d nneg %d side %d nsel %d clusters %d max %d groups %d%s\n", g, k, nneg, side, nsel, ncl,
-           cmax, grp, big ? " FALLBACK" : "");
-  }
-  if (big) gt.status[g] = -1;
+  if (gt.debug)
+    printf("gtrd giant %d k %d nneg %d side %d nsel %d cap %d pieces %d max %d cuts %d groups %d\n", g, k, nneg, side,
+           nsel, cap, npiece, pmax, nsplit, grp);
   gt.ngrp[g] = grp;
 }
 
-// Inverse iteration (LAPACK dstein) for one group of <= 32 selected eigenvalues per warp, one
+// Inverse iteration (LAPACK dstein) for one group of <= cap(k) selected eigenvalues per CTA, one
 // thread per eigenvalue: partial-pivoting LU of T - lam I in global memory ([i][s], coalesced,
 // loads batched 8 deep), the iterate in shared memory (column per thread), 3 solves from a
 // deterministic start vector, each followed by normalisation and modified Gram-Schmidt inside
-// the cluster (members are consecutive threads of the warp).  Weight of vector z: its Rayleigh
-// quotient z^T T z clipped at 0 on the selected side; a residual ||T z - rq z||_inf above
-// 1e-9 ||T|| hands the matrix to the fallback.
+// the cluster piece (its members are consecutive threads of the CTA).  Weight of vector z: its
+// Rayleigh quotient z^T T z clipped at 0 on the selected side; a residual ||T z - rq z||_inf
+// above 1e-9 ||T|| hands the matrix to the fallback.
 constexpr int VB = 8;
-__global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
+constexpr int VT = 128;
+__global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
   const int g = find_item(gt.vg_pre, gt.ng, blockIdx.x);
@@ -553,6 +565,7 @@ __global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
   if (gt.status[g] < 0 || grp >= gt.ngrp[g]) return;
   const int k = a.ksz[gt.task[g]];
   const int H = gt.hsel[g];
+  const int cap = gtrd_vec_cap(k);
   const GView W{gt.ws + gt.moff[g], k, H};
   const double* hd = W.hdr();
   const int side = (int)hd[1];
@@ -563,20 +576,20 @@ __global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
   extern __shared__ double sm[];
   double* d = sm;
   double* e = sm + k;
-  double* xs = sm + 2 * k;  // [i][32]
-  for (int i = t; i < k; i += 32) {
+  double* xs = sm + 2 * k;  // [i][cap]
+  for (int i = t; i < k; i += VT) {
     d[i] = W.d()[i];
     e[i] = W.e()[i];
   }
   const int lead = act ? (int)W.clst()[s] : -1;
-  __syncwarp();
+  __syncthreads();
   const double tn = hd[2], sc = hd[4];
   const double tol = kEps * fmax(tn, 1e-300);
   double* ui = W.iv();
   double* u2 = ui + (int64_t)k * H;
   double* mu = u2 + (int64_t)k * H;
   uint64_t* pw = reinterpret_cast<uint64_t*>(mu + (int64_t)k * H);  // [i / 64][s]
-  double* x = xs + t;  // element i at x[i * 32]
+  double* x = xs + t;  // element i at x[i * cap]
   if (act) {
     const double lam = W.lsel()[s];
     // partial-pivoting LU of T - lam I (dlagtf); pivots below tol -> +-tol, stored inverted;
@@ -619,11 +632,11 @@ __global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
       hh ^= hh >> 31;
       hh *= 0xBF58476D1CE4E5B9ull;
       hh ^= hh >> 29;
-      x[i * 32] = (double)(hh >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+      x[i * cap] = (double)(hh >> 11) * (2.0 / 9007199254740992.0) - 1.0;
     }
   }
   // does any cluster of this group have more than one member?
-  const bool multi = __any_sync(0xffffffffu, act && (s > lead || (s + 1 < se && (int)W.clst()[s + 1] == s)));
+  const bool multi = __syncthreads_or(act && (s > lead || (s + 1 < se && (int)W.clst()[s + 1] == s)));
   for (int it = 0; it < 3; ++it) {
     if (act) {
       // forward: L^{-1} x (row interchanges as recorded)
@@ -636,29 +649,29 @@ __global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
         const uint64_t wd = pw[(int64_t)(i >> 6) * H + s];  // i .. i+7 share a word (VB | 64)
 #pragma unroll
         for (int u = 0; u < VB; ++u) {
-          const double yn = x[(i + 1 + u) * 32];
+          const double yn = x[(i + 1 + u) * cap];
           if ((wd >> ((i + u) & 63)) & 1ull) {
-            x[(i + u) * 32] = yn;
+            x[(i + u) * cap] = yn;
             ry = fma(-m[u], yn, ry);
           } else {
-            x[(i + u) * 32] = ry;
+            x[(i + u) * cap] = ry;
             ry = fma(-m[u], ry, yn);
           }
         }
       }
       for (; i + 1 < k; ++i) {
-        const double yn = x[(i + 1) * 32], m = mu[(int64_t)i * H + s];
+        const double yn = x[(i + 1) * cap], m = mu[(int64_t)i * H + s];
         if ((pw[(int64_t)(i >> 6) * H + s] >> (i & 63)) & 1ull) {
-          x[i * 32] = yn;
+          x[i * cap] = yn;
           ry = fma(-m, yn, ry);
         } else {
-          x[i * 32] = ry;
+          x[i * cap] = ry;
           ry = fma(-m, ry, yn);
         }
       }
       // backward: U^{-1}
       double xn = ry * ui[(int64_t)(k - 1) * H + s], xn1 = 0.0;
-      x[(k - 1) * 32] = xn;
+      x[(k - 1) * cap] = xn;
       double mx = fabs(xn);
       i = k - 2;
       for (; i - (VB - 1) >= 0; i -= VB) {
@@ -676,8 +689,8 @@ __global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
           const int r = i - u;
           const uint64_t w = ((r >> 6) == (i >> 6)) ? wd[0] : wd[1];
           const double u3 = ((w >> (r & 63)) & 1ull) ? e[r + 1] : 0.0;
-          const double xi = (x[r * 32] - a2[u] * xn - u3 * xn1) * ai[u];
-          x[r * 32] = xi;
+          const double xi = (x[r * cap] - a2[u] * xn - u3 * xn1) * ai[u];
+          x[r * cap] = xi;
           mx = fmax(mx, fabs(xi));
           xn1 = xn;
           xn = xi;
@@ -685,8 +698,8 @@ __global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
       }
       for (; i >= 0; --i) {
         const double u3 = ((pw[(int64_t)(i >> 6) * H + s] >> (i & 63)) & 1ull) ? e[i + 1] : 0.0;
-        const double xi = (x[i * 32] - u2[(int64_t)i * H + s] * xn - u3 * xn1) * ui[(int64_t)i * H + s];
-        x[i * 32] = xi;
+        const double xi = (x[i * cap] - u2[(int64_t)i * H + s] * xn - u3 * xn1) * ui[(int64_t)i * H + s];
+        x[i * cap] = xi;
         mx = fmax(mx, fabs(xi));
         xn1 = xn;
         xn = xi;
@@ -695,53 +708,52 @@ __global__ void __launch_bounds__(32) k_gtrd_vec(ProjArgs a) {
       const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
       double nrm = 0.0;
       for (i = 0; i < k; ++i) {
-        const double v = x[i * 32] * inv;
+        const double v = x[i * cap] * inv;
         nrm = fma(v, v, nrm);
       }
       const double in2 = nrm > 0.0 ? inv / sqrt(nrm) : 0.0;
-      for (i = 0; i < k; ++i) x[i * 32] *= in2;
+      for (i = 0; i < k; ++i) x[i * cap] *= in2;
     }
     if (multi) {
       // modified Gram-Schmidt inside each cluster, in index order
       for (int p = 0; p < se - sb; ++p) {
-        __syncwarp();
         const int sp = sb + p;
         const int lp = (int)W.clst()[sp];
         const bool mine = act && s > sp && lead == lp;
-        if (!__any_sync(0xffffffffu, mine)) continue;
+        if (!__syncthreads_or(mine)) continue;
         if (mine) {
           const double* xp = xs + p;
           double dot = 0.0;
-          for (int i = 0; i < k; ++i) dot = fma(xp[i * 32], x[i * 32], dot);
+          for (int i = 0; i < k; ++i) dot = fma(xp[i * cap], x[i * cap], dot);
           double nrm = 0.0;
           for (int i = 0; i < k; ++i) {
-            const double v = fma(-dot, xp[i * 32], x[i * 32]);
-            x[i * 32] = v;
+            const double v = fma(-dot, xp[i * cap], x[i * cap]);
+            x[i * cap] = v;
             nrm = fma(v, v, nrm);
           }
           const double in2 = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
-          for (int i = 0; i < k; ++i) x[i * 32] *= in2;
+          for (int i = 0; i < k; ++i) x[i * cap] *= in2;
         }
       }
-      __syncwarp();
+      __syncthreads();
     }
   }
   if (!act) return;
   // Rayleigh quotient, residual, output column
   double rq = 0.0;
   for (int i = 0; i < k; ++i) {
-    double tz = d[i] * x[i * 32];
-    if (i > 0) tz = fma(e[i - 1], x[(i - 1) * 32], tz);
-    if (i + 1 < k) tz = fma(e[i], x[(i + 1) * 32], tz);
-    rq = fma(x[i * 32], tz, rq);
+    double tz = d[i] * x[i * cap];
+    if (i > 0) tz = fma(e[i - 1], x[(i - 1) * cap], tz);
+    if (i + 1 < k) tz = fma(e[i], x[(i + 1) * cap], tz);
+    rq = fma(x[i * cap], tz, rq);
   }
   double res = 0.0;
   double* Z = W.Z();
   for (int i = 0; i < k; ++i) {
-    const double xi = x[i * 32];
+    const double xi = x[i * cap];
     double tz = (d[i] - rq) * xi;
-    if (i > 0) tz = fma(e[i - 1], x[(i - 1) * 32], tz);
-    if (i + 1 < k) tz = fma(e[i], x[(i + 1) * 32], tz);
+    if (i > 0) tz = fma(e[i - 1], x[(i - 1) * cap], tz);
+    if (i + 1 < k) tz = fma(e[i], x[(i + 1) * cap], tz);
     res = fmax(res, fabs(tz));
     Z[(int64_t)i * H + s] = xi;
   }
@@ -1028,7 +1040,7 @@ void launch_mode(const ProjArgs& a, cudaStream_t s) {
   if (gt.tot_ev) {
     k_gtrd_bisect<<<gt.tot_ev, 32, (size_t)2 * gt.kmax * sizeof(double), s>>>(a);
     k_gtrd_cluster<<<(gt.ng + 31) / 32, 32, 0, s>>>(a);
-    k_gtrd_vec<<<gt.tot_vg, 32, (size_t)34 * gt.kmax * sizeof(double), s>>>(a);
+    k_gtrd_vec<<<gt.tot_vg, VT, (size_t)kVecSmemDoubles * sizeof(double), s>>>(a);
   }
   if (gt.tot_bt) k_gtrd_back<<<gt.tot_bt, GB_NT, kBackSmem, s>>>(a);
   if (gt.tot_rc) k_gtrd_recon<MODE><<<(gt.tot_rc + GR_NW - 1) / GR_NW, GR_NW * 32, GR_NW * sizeof(GrSmem), s>>>(a);
@@ -1048,7 +1060,7 @@ void psd_gtrd_init_attributes() {
   set_attrs<PM_PRIMAL>();
   set_attrs<PM_DUAL>();
 
-  cudaFuncSetAttribute(k_gtrd_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(34 * GT_KMAX * sizeof(double)));
+  cudaFuncSetAttribute(k_gtrd_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kVecSmemDoubles * sizeof(double)));
   cudaFuncSetAttribute(k_gtrd_back, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBackSmem);
 }
 

@@ -327,6 +327,19 @@ def test_cfg3_full_size_iterations(lib, gen):
         s.close()
 
 
+def test_cfg3_clustered_spectra_20_iterations(lib, gen):
+    """configs[3], primal rho = 0.1, 20 iterations: the giant cliques' projection
+    inputs develop dense bands of negative eigenvalues (clusters beyond one
+    vector-kernel group, cut at their largest gaps); iterates still match."""
+    prob = gen.config(3)
+    dec = dc.decompose(prob)
+    st = admm.step(dec, admm.zero_state(dec), 0.1, "primal", 20)
+    s = lib.Solver(prob, form="primal", rho=0.1)
+    s.step(20)
+    compare_state(dec, st, s, "primal")
+    s.close()
+
+
 # ------------------------------------------------------------------ giant (block-Jacobi) tier
 
 def test_giant_tier_iterates_warm_restarts(lib, gen):
