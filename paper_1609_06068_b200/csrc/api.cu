@@ -116,6 +116,26 @@ void tri_inverse_T(const std::vector<double>& L, int m, std::vector<double>& Wt)
 
 using namespace sdp;
 
+// Side stream for the projection tiers: the giant tier (a chain of kernels whose tail leaves
+// most SMs idle) runs on the calling stream while every other tier runs concurrently on `side`
+// (fork / join by events, captured into the iteration graph as a branch).
+struct TierFork {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  void create() {
+    SDP_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    SDP_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    SDP_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+  }
+  void destroy() {
+    if (side) cudaStreamDestroy(side);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    side = nullptr;
+    fork = join = nullptr;
+  }
+};
+
 struct sdp_handle_s {
   int n = 0, m = 0;
   int64_t N = 0, lda = 0, p = 0, stot = 0;
@@ -146,6 +166,7 @@ struct sdp_handle_s {
   int bcount[B_NUM] = {};
   GiantDev gd;
   TrdDev td[2];  // B_TRD32, B_TRD64
+  TierFork tiers;
   // A
   int a_dense = 1;
   double* A = nullptr;
@@ -193,6 +214,7 @@ struct sdp_psd_plan_s {
   int bcount[B_NUM] = {};
   GiantDev gd;
   TrdDev td[2];
+  TierFork tiers;
   unsigned long long* capped = nullptr;
   unsigned long long* sweeps = nullptr;
   double *h_in_dev = nullptr, *h_out_dev = nullptr;
@@ -411,6 +433,36 @@ void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_
   build_trd(al, ksz, lists[B_TRD64], 64, td[1]);
 }
 
+void launch_tiers(ProjArgs a, int mode, int32_t* const d_ids[B_NUM], const int bcount[B_NUM], const TrdDev td[2],
+                  const TierFork& tf, cudaStream_t s) {
+  bool others = false;
+  for (int b = 0; b < B_NUM; ++b) others |= b != B_GLOBAL && bcount[b] > 0;
+  const bool fork = tf.side && bcount[B_GLOBAL] > 0 && others;
+  cudaStream_t so = s;
+  if (fork) {
+    SDP_CUDA_TRY(cudaEventRecord(tf.fork, s));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(tf.side, tf.fork, 0));
+    so = tf.side;
+  }
+  if (bcount[B_GLOBAL]) {
+    a.ids = d_ids[B_GLOBAL];
+    a.count = bcount[B_GLOBAL];
+    launch_projection(B_GLOBAL, mode, a, s);
+  }
+  // then the other tiers, larger first
+  for (int b = B_NUM - 1; b >= 0; --b) {
+    if (b == B_GLOBAL || !bcount[b]) continue;
+    a.ids = d_ids[b];
+    a.count = bcount[b];
+    if (is_trd(b)) a.td = td[b - B_TRD32];
+    launch_projection(b, mode, a, so);
+  }
+  if (fork) {
+    SDP_CUDA_TRY(cudaEventRecord(tf.join, tf.side));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, tf.join, 0));
+  }
+}
+
 void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
   ProjArgs a{};
   a.off = h->d_off;
@@ -430,14 +482,7 @@ void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
   a.voff = h->voff;
   a.iter = h->iter;
   a.warm_period = h->warm_period;
-  // big tiers first: they are the long poles
-  for (int b = B_NUM - 1; b >= 0; --b) {
-    if (!h->bcount[b]) continue;
-    a.ids = h->d_ids[b];
-    a.count = h->bcount[b];
-    if (is_trd(b)) a.td = h->td[b - B_TRD32];
-    launch_projection(b, mode, a, s);
-  }
+  launch_tiers(a, mode, h->d_ids, h->bcount, h->td, h->tiers, s);
 }
 
 void enqueue_scatter(sdp_handle h, cudaStream_t s) {
@@ -663,6 +708,7 @@ void destroy_handle(sdp_handle h) {
   h->alloc.free_all();
   if (h->comm) nccl_comm_destroy(h->comm);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+  h->tiers.destroy();
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   if (cur >= 0) cudaSetDevice(cur);
   delete h;
@@ -741,6 +787,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->rank = opt.rank;
   if (h->world > 1) h->comm = nccl_comm_init(opt.nccl_id, h->world, h->rank);  // collective
   SDP_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+  h->tiers.create();
   const int64_t N = (int64_t)cr.coord_row.size();
   h->N = N;
   h->coord_row = cr.coord_row;
@@ -1563,12 +1610,14 @@ int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, s
     build_buckets(pl->alloc, ksz, pl->d_ids, pl->bcount, pl->gd, pl->td);
     pl->capped = pl->alloc.zeros<unsigned long long>(1);
     pl->sweeps = pl->alloc.zeros<unsigned long long>(1);
+    pl->tiers.create();
     psd_init_attributes();
     *out = pl;
     return SDP_OK;
   });
   if (rc != SDP_OK && pl) {
     pl->alloc.free_all();
+    pl->tiers.destroy();
     delete pl;
   }
   return rc;
@@ -1589,13 +1638,7 @@ int sdp_project_psd_batch(sdp_psd_plan pl, const double* d_in, double* d_out, vo
     a.capped = pl->capped;
     a.sweeps = pl->sweeps;
     a.done = nullptr;
-    for (int b = B_NUM - 1; b >= 0; --b) {
-      if (!pl->bcount[b]) continue;
-      a.ids = pl->d_ids[b];
-      a.count = pl->bcount[b];
-      if (is_trd(b)) a.td = pl->td[b - B_TRD32];
-      launch_projection(b, PM_BATCH, a, s);
-    }
+    launch_tiers(a, PM_BATCH, pl->d_ids, pl->bcount, pl->td, pl->tiers, s);
     SDP_CUDA_TRY(cudaGetLastError());
     return SDP_OK;
   });
@@ -1645,6 +1688,7 @@ int sdp_psd_plan_destroy(sdp_psd_plan pl) {
     cudaSetDevice(pl->device);
     cudaDeviceSynchronize();
     pl->alloc.free_all();
+    pl->tiers.destroy();
     if (cur >= 0) cudaSetDevice(cur);
     delete pl;
     return SDP_OK;
