@@ -259,7 +259,7 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
   const int ng = (int)ids.size();
   const int kcap = gtrd_max_order();
   std::vector<int64_t> moff(ng, 0);
-  std::vector<int32_t> hsel(ng), ev(ng + 1, 0), vg(ng + 1, 0), bt(ng + 1, 0), rc(ng + 1, 0);
+  std::vector<int32_t> hsel(ng), ev(ng + 1, 0), vg(ng + 1, 0), wy(ng + 1, 0), bt(ng + 1, 0), rc(ng + 1, 0);
   int64_t ws = 0;
   int kmax = 0;
   for (int g = 0; g < ng; ++g) {
@@ -274,6 +274,7 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
     const int R = (k + 31) / 32;
     ev[g + 1] = ev[g] + (ok ? (k + 31) / 32 : 0);
     vg[g + 1] = vg[g] + (ok ? 2 * ((k + gtrd_vec_cap(k) - 1) / gtrd_vec_cap(k)) + 1 : 0);
+    wy[g + 1] = wy[g] + (ok ? (k - 2 + 15) / 16 : 0);
     bt[g + 1] = bt[g] + (ok ? (k + 15) / 16 : 0);
     rc[g + 1] = rc[g] + (ok ? R * (R + 1) / 2 : 0);
   }
@@ -313,6 +314,8 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
   gt.vg_pre = al.upload(vg);
   gt.tot_vg = vg[ng];
   gt.ngrp = al.zeros<int32_t>((size_t)ng);
+  gt.wy_pre = al.upload(wy);
+  gt.tot_wy = wy[ng];
   gt.bt_pre = al.upload(bt);
   gt.rc_pre = al.upload(rc);
   gt.tot_bt = bt[ng];

@@ -91,10 +91,11 @@ struct GtrdDev {
   const int32_t* ev_pre = nullptr;     // ng + 1: bisection warps (32 indices each)
   const int32_t* vg_pre = nullptr;     // ng + 1: inverse-iteration warps (2 ceil(H / 32) + 1 groups)
   int32_t* ngrp = nullptr;             // per giant: groups in use (device-computed)
+  const int32_t* wy_pre = nullptr;     // ng + 1: WY groups (16 reflectors each)
   const int32_t* bt_pre = nullptr;     // ng + 1: back-transform CTAs (16 columns each)
   const int32_t* rc_pre = nullptr;     // ng + 1: reconstruction tiles (32 x 32, upper)
   double* part = nullptr;              // 3 per reconstruction tile (primal residual partials)
-  int tot_ev = 0, tot_vg = 0, tot_bt = 0, tot_rc = 0;
+  int tot_ev = 0, tot_vg = 0, tot_wy = 0, tot_bt = 0, tot_rc = 0;
   int force_fallback = 0;              // SDP_GTRD_FORCE_FALLBACK=1: mark every matrix failed (tests)
   int debug = 0;                       // SDP_GTRD_DEBUG=1: per-matrix spectrum / cluster printf
 };

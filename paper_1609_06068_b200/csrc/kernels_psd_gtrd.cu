@@ -50,6 +50,11 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_src) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem_src) : "memory");
+}
+
 __device__ __forceinline__ void packed_rc(int e, int& r, int& c) {
   int cc = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
   while ((cc + 1) * (cc + 2) / 2 <= e) ++cc;
@@ -89,12 +94,15 @@ struct GView {
   __device__ double* gsr() const { return clst() + H; }            // vector-kernel groups: first index
   // hdr: nsel, side, ||T|| (scaled), pivmin, scale, Gershgorin lo, hi, index of the first selected
   __device__ double* hdr() const { return gsr() + H; }
-  __device__ double* Z() const { return hdr() + 8; }               // k x H, [i][j]
+  __device__ double* Z() const { return hdr() + 8; }               // selected vectors, column j at j * k
   __device__ double* iv() const { return Z() + (int64_t)k * H; }   // 3 x k x H LU factors + pivot words
+  __device__ int nwy() const { return (k - 2 + 15) / 16; }            // WY groups of 16 reflectors
+  __device__ double* wyT() const { return iv() + 3 * (int64_t)k * H + ((k + 63) / 64) * (int64_t)H; }
 };
 __host__ __device__ inline int64_t gview_doubles(int k) {
   const int64_t H = k;
-  return (int64_t)k * GView::ld_of(k) + 4 * k + 4 * H + 8 + 4 * (int64_t)k * H + ((k + 63) / 64) * H + 4;
+  return (int64_t)k * GView::ld_of(k) + 4 * k + 4 * H + 8 + 4 * (int64_t)k * H + ((k + 63) / 64) * H +
+         (int64_t)((k - 2 + 15) / 16) * 256 + 4;
 }
 
 // ---------------------------------------------------------------- 1. tridiagonalization
@@ -117,7 +125,7 @@ constexpr size_t kTriSmem =
     (size_t)(2 * TC_NB * GT_KMAX + 3 * GT_KMAX + TC_PS + 32 * TC_NR + TC_NR + 32 + 4) * sizeof(double);
 
 template <int MODE>
-__global__ void __launch_bounds__(TC_NT) k_gtrd_tridiag(ProjArgs a) {
+__global__ void __launch_bounds__(TC_NT, 2) k_gtrd_tridiag(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
   const int job = blockIdx.x / TC_CS, rank = blockIdx.x % TC_CS;
@@ -172,8 +180,10 @@ __global__ void __launch_bounds__(TC_NT) k_gtrd_tridiag(ProjArgs a) {
     return (cj > r ? (cj - r + ncta - 1) / ncta : 0) * 32;
   };
   const int wid = t >> 5, lane = t & 31;
+  static_assert(GT_KMAX <= 2 * TC_NT, "row prefetch holds two entries per thread");
   for (int j0 = 0; j0 + 2 < k; j0 += TC_NB) {
     const int nbp = min(TC_NB, k - 2 - j0);
+    double pre[2] = {0.0, 0.0};  // raw row j, prefetched during column j - 1 (inside a panel)
     for (int c = 0; c < nbp; ++c) {
       const int j = j0 + c;
       // (a) row j (== column j) from j on, with the panel's previous reflectors applied;
@@ -181,8 +191,11 @@ __global__ void __launch_bounds__(TC_NT) k_gtrd_tridiag(ProjArgs a) {
       double part[TC_NR];
 #pragma unroll
       for (int q = 0; q < TC_NR; ++q) part[q] = 0.0;
-      for (int i = j + t; i < k; i += TC_NT) {
-        double x = __ldcg(M + (int64_t)j * LD + i);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int i = j + t + u * TC_NT;
+        if (i >= k) continue;
+        double x = c > 0 ? pre[u] : __ldcg(M + (int64_t)j * LD + i);
         for (int q = 0; q < c; ++q) x -= fma(Vs[q * GT_KMAX + i], Ws[q * GT_KMAX + j], Ws[q * GT_KMAX + i] * Vs[q * GT_KMAX + j]);
         xrow[i] = x;
         if (i >= j + 2) {
@@ -224,6 +237,13 @@ __global__ void __launch_bounds__(TC_NT) k_gtrd_tridiag(ProjArgs a) {
         W.d()[j] = xrow[j];
         W.e()[j] = beta;
         W.tau()[j] = tau;
+      }
+      if (c + 1 < nbp) {  // rows of the panel are final (the trailing update ran before it)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int i = j + 1 + t + u * TC_NT;
+          if (i < k) pre[u] = __ldcg(M + (int64_t)(j + 1) * LD + i);
+        }
       }
       double y1[TC_NB], y2[TC_NB];
 #pragma unroll
@@ -590,6 +610,7 @@ __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
   double* mu = u2 + (int64_t)k * H;
   uint64_t* pw = reinterpret_cast<uint64_t*>(mu + (int64_t)k * H);  // [i / 64][s]
   double* x = xs + t;  // element i at x[i * cap]
+  __shared__ double nrm2s[VT];
   if (act) {
     const double lam = W.lsel()[s];
     // partial-pivoting LU of T - lam I (dlagtf); pivots below tol -> +-tol, stored inverted;
@@ -706,36 +727,64 @@ __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
       }
       // normalise (scaled by 1/max first so that the sum of squares cannot overflow)
       const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
-      double nrm = 0.0;
-      for (i = 0; i < k; ++i) {
-        const double v = x[i * cap] * inv;
-        nrm = fma(v, v, nrm);
+      double n4[4] = {0.0, 0.0, 0.0, 0.0};
+      for (i = 0; i + 3 < k; i += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const double v = x[(i + u) * cap] * inv;
+          n4[u] = fma(v, v, n4[u]);
+        }
       }
+      for (; i < k; ++i) {
+        const double v = x[i * cap] * inv;
+        n4[0] = fma(v, v, n4[0]);
+      }
+      const double nrm = (n4[0] + n4[1]) + (n4[2] + n4[3]);
       const double in2 = nrm > 0.0 ? inv / sqrt(nrm) : 0.0;
       for (i = 0; i < k; ++i) x[i * cap] *= in2;
     }
     if (multi) {
-      // modified Gram-Schmidt inside each cluster, in index order
-      for (int p = 0; p < se - sb; ++p) {
-        const int sp = sb + p;
-        const int lp = (int)W.clst()[sp];
-        const bool mine = act && s > sp && lead == lp;
-        if (!__syncthreads_or(mine)) continue;
-        if (mine) {
-          const double* xp = xs + p;
-          double dot = 0.0;
-          for (int i = 0; i < k; ++i) dot = fma(xp[i * cap], x[i * cap], dot);
-          double nrm = 0.0;
-          for (int i = 0; i < k; ++i) {
-            const double v = fma(-dot, xp[i * cap], x[i * cap]);
-            x[i * cap] = v;
-            nrm = fma(v, v, nrm);
+      // modified Gram-Schmidt inside each cluster piece, all pieces of the group in step: at step
+      // pr the member of rank pr (= s - lead) is the pivot of its piece and every member of higher
+      // rank removes its component, x_q -= (x_p.x_q / |x_p|^2) x_p (pivots are left unnormalised;
+      // |x|^2 is kept up to date by the fused update pass), then one final normalisation
+      nrm2s[t] = 1.0;
+      const int rank = act ? s - lead : 0;
+      for (int pr = 0; __syncthreads_or(act && rank > pr); ++pr) {
+        if (act && rank > pr) {
+          const int pt = lead + pr - sb;  // pivot's thread = its column in xs
+          const double* xp = xs + pt;
+          const double np = nrm2s[pt];
+          double d4[4] = {0.0, 0.0, 0.0, 0.0}, n4[4] = {0.0, 0.0, 0.0, 0.0};  // 4 chains (ILP)
+          int i = 0;
+          for (; i + 3 < k; i += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) d4[u] = fma(xp[(i + u) * cap], x[(i + u) * cap], d4[u]);
           }
-          const double in2 = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
-          for (int i = 0; i < k; ++i) x[i * cap] *= in2;
+          for (; i < k; ++i) d4[0] = fma(xp[i * cap], x[i * cap], d4[0]);
+          const double coef = np > 0.0 ? ((d4[0] + d4[1]) + (d4[2] + d4[3])) / np : 0.0;
+          for (i = 0; i + 3 < k; i += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double v = fma(-coef, xp[(i + u) * cap], x[(i + u) * cap]);
+              x[(i + u) * cap] = v;
+              n4[u] = fma(v, v, n4[u]);
+            }
+          }
+          for (; i < k; ++i) {
+            const double v = fma(-coef, xp[i * cap], x[i * cap]);
+            x[i * cap] = v;
+            n4[0] = fma(v, v, n4[0]);
+          }
+          nrm2s[t] = (n4[0] + n4[1]) + (n4[2] + n4[3]);
         }
       }
-      __syncthreads();
+      if (act && rank > 0) {
+        const double nq = nrm2s[t];
+        const double in2 = nq > 0.0 ? 1.0 / sqrt(nq) : 0.0;
+        for (int i = 0; i < k; ++i) x[i * cap] *= in2;
+      }
+      __syncthreads();  // rank-0 pivots are read by nobody after this; next solve reads only own x
     }
   }
   if (!act) return;
@@ -755,7 +804,7 @@ __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
     if (i > 0) tz = fma(e[i - 1], x[(i - 1) * cap], tz);
     if (i + 1 < k) tz = fma(e[i], x[(i + 1) * cap], tz);
     res = fmax(res, fabs(tz));
-    Z[(int64_t)i * H + s] = xi;
+    Z[(int64_t)s * k + i] = xi;
   }
   if (!(res <= 1e-9 * fmax(tn, 1e-300)) || gt.force_fallback) {  // includes NaN
     gt.status[g] = -1;
@@ -769,11 +818,68 @@ __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
 
 // ---------------------------------------------------------------- 3. back-transform V = Q Z
 // Q = H_0 H_1 ... H_{k-3}; the reflectors are applied in groups of GB_NR from the last one down,
-// each group in compact WY form H_lo ... H_hi = I - Y T Y^T (LAPACK dlarft, forward): Y staged in
-// shared memory, Y^T Y by the CTA's warps, T by warp 0, then per column (a warp, the column in
-// registers) z <- z - Y (T (Y^T z)): one 16-wide warp reduction per group instead of 16.
+// each group in compact WY form H_lo ... H_hi = I - Y T Y^T (LAPACK dlarft, forward).
+// k_gtrd_wy forms every group's T once per matrix (Y^T Y by the CTA's warps, T by warp 0);
+// k_gtrd_back stages Y (double-buffered: the next group's loads are issued before the current
+// group is applied) and, per column (a warp, the column in registers), z <- z - Y (T (Y^T z)):
+// one 16-wide warp reduction per group.
 constexpr int GB_NT = 512;   // 16 warps = 16 columns
 constexpr int GB_NR = 16;    // reflectors per group
+
+__global__ void __launch_bounds__(GB_NT) k_gtrd_wy(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int g = find_item(gt.wy_pre, gt.ng, blockIdx.x);
+  if (gt.status[g] < 0) return;
+  const int k = a.ksz[gt.task[g]];
+  const GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
+  const int gi = blockIdx.x - gt.wy_pre[g];
+  const int jhi = k - 3 - gi * GB_NR;
+  const int nr = min(GB_NR, jhi + 1);
+  const int jlo = jhi - nr + 1;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  extern __shared__ double vb[];          // Y: GB_NR x GT_KMAX
+  double* Gm = vb + GB_NR * GT_KMAX;      // Y^T Y (upper)
+  double* Tm = Gm + GB_NR * GB_NR;
+  const double* M = W.M();
+  const int LD = W.ld();
+  for (int e = threadIdx.x; e < GB_NR * k; e += GB_NT) {  // v_j lives in column j: c fastest
+    const int c = e % GB_NR, i = e / GB_NR;
+    const int j = jlo + c;
+    vb[c * GT_KMAX + i] = (c >= nr || i < j + 1) ? 0.0 : (i == j + 1 ? 1.0 : M[(int64_t)i * LD + j]);
+  }
+  __syncthreads();
+  for (int pr = wid; pr < GB_NR * (GB_NR - 1) / 2; pr += GB_NT / 32) {
+    int aa = 0, rem = pr;
+    while (rem >= GB_NR - 1 - aa) {
+      rem -= GB_NR - 1 - aa;
+      ++aa;
+    }
+    const int bb = aa + 1 + rem;
+    double sacc = 0.0;
+    if (bb < nr)
+      for (int i = jlo + 1 + lane; i < k; i += 32) sacc = fma(vb[aa * GT_KMAX + i], vb[bb * GT_KMAX + i], sacc);
+    sacc = warp_sum(sacc);
+    if (lane == 0) Gm[aa * GB_NR + bb] = sacc;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    // T[c][c] = tau_c;  T[0:c, c] = -tau_c T[0:c, 0:c] (Y^T y_c)[0:c]
+    for (int c = 0; c < GB_NR; ++c) {
+      const double tau = c < nr ? W.tau()[jlo + c] : 0.0;
+      double tv = 0.0;
+      if (lane < c)
+        for (int q = lane; q < c; ++q) tv = fma(Tm[lane * GB_NR + q], Gm[q * GB_NR + c], tv);
+      __syncwarp();
+      if (lane < c) Tm[lane * GB_NR + c] = -tau * tv;
+      if (lane == c) Tm[c * GB_NR + c] = tau;
+      if (lane > c && lane < GB_NR) Tm[lane * GB_NR + c] = 0.0;
+      __syncwarp();
+    }
+    double* out = W.wyT() + (int64_t)gi * GB_NR * GB_NR;
+    for (int e = lane; e < GB_NR * GB_NR; e += 32) out[e] = Tm[e];
+  }
+}
 
 __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
   if (a.done && *a.done) return;
@@ -789,9 +895,8 @@ __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
   if (col0 >= nsel) return;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = col0 + wid;
-  extern __shared__ double vb[];          // Y: GB_NR x GT_KMAX
-  double* Gm = vb + GB_NR * GT_KMAX;      // Y^T Y (upper)
-  double* Tm = Gm + GB_NR * GB_NR;        // T (upper)
+  extern __shared__ double vb[];          // Y: 2 x GB_NR x GT_KMAX (double buffer)
+  double* Tm = vb + 2 * GB_NR * GT_KMAX;  // 2 x T
   const double* M = W.M();
   const int LD = W.ld();
   double* Z = W.Z();
@@ -799,49 +904,40 @@ __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
 #pragma unroll
   for (int r = 0; r < GT_RT; ++r) {
     const int i = lane + 32 * r;
-    z[r] = (col < nsel && i < k) ? Z[(int64_t)i * H + col] : 0.0;
+    z[r] = (col < nsel && i < k) ? Z[(int64_t)col * k + i] : 0.0;
   }
-  for (int jhi = k - 3; jhi >= 0; jhi -= GB_NR) {
+  const int ngr = W.nwy();
+  // group gi -> buffer b: cp.async (8-byte LDGSTS) for the stored reflector entries, plain stores
+  // for the implicit zeros / ones, T from k_gtrd_wy; in flight while the previous group is applied
+  auto stage = [&](int gi, int b) {
+    const int jhi = k - 3 - gi * GB_NR;
     const int nr = min(GB_NR, jhi + 1);
-    const int jlo = jhi - nr + 1;           // Y column c <-> reflector jlo + c
-    __syncthreads();
-    for (int e = threadIdx.x; e < GB_NR * k; e += GB_NT) {  // v_j lives in column j: c fastest
+    const int jlo = jhi - nr + 1;
+    double* dst = vb + b * GB_NR * GT_KMAX;
+    for (int e = threadIdx.x; e < GB_NR * k; e += GB_NT) {
       const int c = e % GB_NR, i = e / GB_NR;
       const int j = jlo + c;
-      vb[c * GT_KMAX + i] = (c >= nr || i < j + 1) ? 0.0 : (i == j + 1 ? 1.0 : M[(int64_t)i * LD + j]);
+      if (c >= nr || i < j + 1)
+        dst[c * GT_KMAX + i] = 0.0;
+      else if (i == j + 1)
+        dst[c * GT_KMAX + i] = 1.0;
+      else
+        cp_async8(dst + c * GT_KMAX + i, M + (int64_t)i * LD + j);
     }
-    __syncthreads();
-    // Gram matrix Y^T Y, pairs a < b (rows below jlo are zero in every column)
-    for (int pr = wid; pr < GB_NR * (GB_NR - 1) / 2; pr += GB_NT / 32) {
-      int aa = 0, rem = pr;
-      while (rem >= GB_NR - 1 - aa) {
-        rem -= GB_NR - 1 - aa;
-        ++aa;
-      }
-      const int bb = aa + 1 + rem;
-      double sacc = 0.0;
-      if (bb < nr)
-        for (int i = jlo + 1 + lane; i < k; i += 32) sacc = fma(vb[aa * GT_KMAX + i], vb[bb * GT_KMAX + i], sacc);
-      sacc = warp_sum(sacc);
-      if (lane == 0) Gm[aa * GB_NR + bb] = sacc;
-    }
-    __syncthreads();
-    if (wid == 0) {
-      // T[c][c] = tau_c;  T[0:c, c] = -tau_c T[0:c, 0:c] (Y^T y_c)[0:c]
-      for (int c = 0; c < GB_NR; ++c) {
-        const double tau = c < nr ? W.tau()[jlo + c] : 0.0;
-        double tv = 0.0;
-        if (lane < c)
-          for (int q = lane; q < c; ++q) tv = fma(Tm[lane * GB_NR + q], Gm[q * GB_NR + c], tv);
-        __syncwarp();
-        if (lane < c) Tm[lane * GB_NR + c] = -tau * tv;
-        if (lane == c) Tm[c * GB_NR + c] = tau;
-        if (lane > c && lane < GB_NR) Tm[lane * GB_NR + c] = 0.0;
-        __syncwarp();
-      }
-    }
-    __syncthreads();
+    if (threadIdx.x < GB_NR * GB_NR)
+      cp_async8(Tm + b * GB_NR * GB_NR + threadIdx.x, W.wyT() + (int64_t)gi * GB_NR * GB_NR + threadIdx.x);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  stage(0, 0);
+  for (int gi = 0; gi < ngr; ++gi) {
+    const int b = gi & 1;
+    const int jlo = max(0, k - 3 - gi * GB_NR - GB_NR + 1);
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();  // buffer b complete; buffer b ^ 1 no longer read
+    if (gi + 1 < ngr) stage(gi + 1, b ^ 1);
     if (col < nsel) {
+      const double* Y = vb + b * GB_NR * GT_KMAX;
+      const double* T = Tm + b * GB_NR * GB_NR;
       double w[GB_NR];
 #pragma unroll
       for (int c = 0; c < GB_NR; ++c) w[c] = 0.0;
@@ -850,17 +946,16 @@ __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
         const int i = lane + 32 * r;
         if (i < k && i > jlo) {
 #pragma unroll
-          for (int c = 0; c < GB_NR; ++c) w[c] = fma(vb[c * GT_KMAX + i], z[r], w[c]);
+          for (int c = 0; c < GB_NR; ++c) w[c] = fma(Y[c * GT_KMAX + i], z[r], w[c]);
         }
       }
 #pragma unroll
       for (int c = 0; c < GB_NR; ++c) w[c] = warp_sum(w[c]);
-      // u = T w (T upper), kept in w (row c needs w[c..] only: ascending order is safe)
 #pragma unroll
-      for (int c = 0; c < GB_NR; ++c) {
+      for (int c = 0; c < GB_NR; ++c) {  // u = T w (T upper), in place in ascending order
         double u = 0.0;
 #pragma unroll
-        for (int q = c; q < GB_NR; ++q) u = fma(Tm[c * GB_NR + q], w[q], u);
+        for (int q = c; q < GB_NR; ++q) u = fma(T[c * GB_NR + q], w[q], u);
         w[c] = u;
       }
 #pragma unroll
@@ -869,7 +964,7 @@ __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
         if (i < k && i > jlo) {
           double acc = z[r];
 #pragma unroll
-          for (int c = 0; c < GB_NR; ++c) acc = fma(-vb[c * GT_KMAX + i], w[c], acc);
+          for (int c = 0; c < GB_NR; ++c) acc = fma(-Y[c * GT_KMAX + i], w[c], acc);
           z[r] = acc;
         }
       }
@@ -879,7 +974,7 @@ __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
 #pragma unroll
     for (int r = 0; r < GT_RT; ++r) {
       const int i = lane + 32 * r;
-      if (i < k) Z[(int64_t)i * H + col] = z[r];
+      if (i < k) Z[(int64_t)col * k + i] = z[r];
     }
   }
 }
@@ -932,12 +1027,12 @@ __global__ void __launch_bounds__(GR_NW * 32) k_gtrd_recon(ProjArgs a) {
     for (int q = 0; q < 4; ++q) acc[p][q][0] = acc[p][q][1] = 0.0;
   for (int kk = 0; kk < nsel; kk += 32) {
     __syncwarp();
-    for (int e = lane; e < 1024; e += 32) {
-      const int m = e >> 5, u = e & 31;
+    for (int e = lane; e < 1024; e += 32) {  // lanes along the rows: Z is column-major
+      const int m = e & 31, u = e >> 5;
       const int rr = rb * 32 + m, cc = cb * 32 + m, uu = kk + u;
       const bool ok = uu < nsel;
-      sm.X[m * GR_LDS + u] = (ok && rr < k) ? Z[(int64_t)rr * H + uu] * W.lw()[uu] : 0.0;  // [m][k]
-      sm.Y[m * GR_LDS + u] = (ok && cc < k) ? Z[(int64_t)cc * H + uu] : 0.0;               // [n][k]
+      sm.X[m * GR_LDS + u] = (ok && rr < k) ? Z[(int64_t)uu * k + rr] * W.lw()[uu] : 0.0;  // [m][k]
+      sm.Y[m * GR_LDS + u] = (ok && cc < k) ? Z[(int64_t)uu * k + cc] : 0.0;               // [n][k]
     }
     __syncwarp();
 #pragma unroll
@@ -1017,7 +1112,8 @@ __global__ void k_gtrd_fin(ProjArgs a) {
 }
 
 
-constexpr size_t kBackSmem = (size_t)(GB_NR * GT_KMAX + 2 * GB_NR * GB_NR) * sizeof(double);
+constexpr size_t kWySmem = (size_t)(GB_NR * GT_KMAX + 2 * GB_NR * GB_NR) * sizeof(double);
+constexpr size_t kBackSmem = (size_t)(2 * GB_NR * GT_KMAX + 2 * GB_NR * GB_NR) * sizeof(double);
 
 template <int MODE>
 void launch_mode(const ProjArgs& a, cudaStream_t s) {
@@ -1042,6 +1138,7 @@ void launch_mode(const ProjArgs& a, cudaStream_t s) {
     k_gtrd_cluster<<<(gt.ng + 31) / 32, 32, 0, s>>>(a);
     k_gtrd_vec<<<gt.tot_vg, VT, (size_t)kVecSmemDoubles * sizeof(double), s>>>(a);
   }
+  if (gt.tot_wy) k_gtrd_wy<<<gt.tot_wy, GB_NT, kWySmem, s>>>(a);
   if (gt.tot_bt) k_gtrd_back<<<gt.tot_bt, GB_NT, kBackSmem, s>>>(a);
   if (gt.tot_rc) k_gtrd_recon<MODE><<<(gt.tot_rc + GR_NW - 1) / GR_NW, GR_NW * 32, GR_NW * sizeof(GrSmem), s>>>(a);
   if (MODE == PM_PRIMAL) k_gtrd_fin<<<(gt.ng + 127) / 128, 128, 0, s>>>(a);
@@ -1062,6 +1159,7 @@ void psd_gtrd_init_attributes() {
 
   cudaFuncSetAttribute(k_gtrd_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kVecSmemDoubles * sizeof(double)));
   cudaFuncSetAttribute(k_gtrd_back, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBackSmem);
+  cudaFuncSetAttribute(k_gtrd_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWySmem);
 }
 
 int gtrd_max_order() { return GT_KMAX; }
