@@ -125,7 +125,7 @@ constexpr size_t kTriSmem =
     (size_t)(2 * TC_NB * GT_KMAX + 3 * GT_KMAX + TC_PS + 32 * TC_NR + TC_NR + 32 + 4) * sizeof(double);
 
 template <int MODE>
-__global__ void __launch_bounds__(TC_NT, 2) k_gtrd_tridiag(ProjArgs a) {
+__global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
   const int job = blockIdx.x / TC_CS, rank = blockIdx.x % TC_CS;
