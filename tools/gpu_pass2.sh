@@ -24,4 +24,6 @@ python bench.py --workload cfg4 --steps 2 --warmup 3 --no-cpu > "$OUT/plain_cfg4
     --log-file "$OUT/launches_cfg4.csv" python bench.py --workload cfg4 --steps 2 --warmup 3 --no-cpu > "$OUT/ncu_l4.log" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gemv_dense|k_gemvT_rows|k_psd_wj32" -s 6 -c 3 \
   -o "$OUT/full_cfg2" python bench.py --steps 3 --warmup 3 --no-cpu > "$OUT/ncu_f2.log" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gtrd_tridiag|k_gtrd_vec|k_gtrd_back" -s 30 -c 3 \
+  -o "$OUT/full_cfg3" python bench.py --workload cfg3 --steps 3 --warmup 3 --no-cpu > "$OUT/ncu_f3.log" 2>&1
 echo done >> "$OUT/rc.txt"
