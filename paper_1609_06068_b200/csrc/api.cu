@@ -324,7 +324,7 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
   const char* ff = getenv("SDP_GTRD_FORCE_FALLBACK");
   gt.force_fallback = (ff && *ff == '1') ? 1 : 0;
   const char* gdb = getenv("SDP_GTRD_DEBUG");
-  gt.debug = (gdb && *gdb == '1') ? 1 : 0;
+  gt.debug = gdb ? atoi(gdb) : 0;
   gd.only = gt.status;
 }
 

@@ -140,6 +140,16 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
     if (r == 0 && t == 0) gt.status[g] = -1;
     return;
   }
+  // SDP_GTRD_DEBUG=2: per-phase clock64 totals of CTA 0 of the first job (thread 0)
+  const bool trace = gt.debug == 2 && blockIdx.x == 0 && t == 0;
+  long long tr_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tr_last = clock64();
+#define TR_MARK(ph)                         \
+  if (trace) {                              \
+    const long long now_ = clock64();       \
+    tr_acc[ph] += now_ - tr_last;           \
+    tr_last = now_;                         \
+  }
   if (r == 0 && t == 0) gt.status[g] = 0;
   cg::cluster_group cl = cg::this_cluster();
   auto csync = [&]() {
@@ -172,12 +182,14 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
   }
   for (int e = t; e < 2 * TC_NB * GT_KMAX; e += TC_NT) smem[e] = 0.0;
   csync();
-  const int nchunk = (k + 31) >> 5;
-  const int nown = (nchunk > r ? (nchunk - r + ncta - 1) / ncta : 0) * 32;  // owned columns (may pass k)
-  auto own_col = [&](int oc) { return ((oc >> 5) * ncta + r) * 32 + (oc & 31); };
+  // column chunks of 16 (one 128-byte line per row) dealt round-robin to the job's CTAs
+  constexpr int CW = 16;
+  const int nchunk = (k + CW - 1) / CW;
+  const int nown = (nchunk > r ? (nchunk - r + ncta - 1) / ncta : 0) * CW;  // owned columns (may pass k)
+  auto own_col = [&](int oc) { return ((oc / CW) * ncta + r) * CW + (oc % CW); };
   auto first_oc = [&](int col) {  // first owned-column index of the chunks that reach column col
-    const int cj = col >> 5;
-    return (cj > r ? (cj - r + ncta - 1) / ncta : 0) * 32;
+    const int cj = col / CW;
+    return (cj > r ? (cj - r + ncta - 1) / ncta : 0) * CW;
   };
   const int wid = t >> 5, lane = t & 31;
   static_assert(GT_KMAX <= 2 * TC_NT, "row prefetch holds two entries per thread");
@@ -207,18 +219,36 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
           }
         }
       }
+      {
+        // 16-value warp reduction in 15 exchanges (halving butterfly): lane L ends with the sum of
+        // value ((L >> 1) & 15) bit-reversed over L's bits 4..1 (see idx below)
+        double v16[16];
 #pragma unroll
-      for (int q = 0; q < TC_NR; ++q) {
-        const double v = warp_sum(part[q]);
-        if (lane == 0) red[wid * TC_NR + q] = v;
+        for (int q = 0; q < 16; ++q) v16[q] = q < TC_NR ? part[q] : 0.0;
+#pragma unroll
+        for (int h = 8; h >= 1; h >>= 1) {
+          const int o = 2 * h;  // lane offsets 16, 8, 4, 2
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int q = 0; q < h; ++q) {
+            const double send = up ? v16[q] : v16[q + h];
+            const double keep = up ? v16[q + h] : v16[q];
+            v16[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        const double tot = v16[0] + __shfl_xor_sync(0xffffffffu, v16[0], 1);
+        const int idx = ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
+        if ((lane & 1) == 0 && idx < TC_NR) red[wid * TC_NR + idx] = tot;
       }
       __syncthreads();
+      TR_MARK(1);
       if (t < TC_NR) {
         double sacc = 0.0;
         for (int w = 0; w < TC_NT / 32; ++w) sacc += red[w * TC_NR + t];
         yv[t] = sacc;
       }
       __syncthreads();
+      TR_MARK(2);
       // (b) Householder vector of x (dlarfg); y1 = W^T v, y2 = V^T v
       const double alpha = xrow[j + 1], sig = yv[0];
       double tau = 0.0, beta = alpha, scl = 0.0;
@@ -252,6 +282,7 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
         y2[q] = fma(scl, yv[1 + TC_NB + q], Vs[q * GT_KMAX + j + 1]);
       }
       __syncthreads();
+      TR_MARK(3);
       if (tau != 0.0) {  // identical in every CTA of the job
         // (c) p = tau (A22 v - V y1 - W y2) on the owned columns, rows split in G groups
         const double* Vc = Vs + c * GT_KMAX;
@@ -267,20 +298,16 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
             const int64_t st = (int64_t)G * LD;
             const double* Ml = M + (int64_t)l * LD + col;
             double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-            for (; l < k; l += 16 * G, Ml += 16 * st) {  // 16 rows in flight (the last batch masked)
-              double m[16], vv[16];
+            for (; l < k; l += 24 * G, Ml += 24 * st) {  // 24 rows in flight (the last batch masked)
+              double m[24];
 #pragma unroll
-              for (int u = 0; u < 16; ++u) {
-                const bool in = l + u * G < k;
-                m[u] = in ? __ldcg(Ml + u * st) : 0.0;
-                vv[u] = in ? Vc[l + u * G] : 0.0;
-              }
+              for (int u = 0; u < 24; ++u) m[u] = l + u * G < k ? __ldcg(Ml + u * st) : 0.0;
 #pragma unroll
-              for (int u = 0; u < 16; u += 4) {
-                a0 = fma(m[u], vv[u], a0);
-                a1 = fma(m[u + 1], vv[u + 1], a1);
-                a2 = fma(m[u + 2], vv[u + 2], a2);
-                a3 = fma(m[u + 3], vv[u + 3], a3);
+              for (int u = 0; u < 24; u += 4) {  // Vc beyond row k is zero (cleared per panel)
+                a0 = fma(m[u], Vc[min(l + u * G, GT_KMAX - 1)], a0);
+                a1 = fma(m[u + 1], Vc[min(l + (u + 1) * G, GT_KMAX - 1)], a1);
+                a2 = fma(m[u + 2], Vc[min(l + (u + 2) * G, GT_KMAX - 1)], a2);
+                a3 = fma(m[u + 3], Vc[min(l + (u + 3) * G, GT_KMAX - 1)], a3);
               }
             }
             pacc = (a0 + a1) + (a2 + a3);
@@ -288,6 +315,7 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
           psum[it] = pacc;
         }
         __syncthreads();
+        TR_MARK(4);
         double* pb = pbuf + (j & 1) * GT_KMAX;
         for (int oc = oc0 + t; oc < nown; oc += TC_NT) {
           const int col = own_col(oc);
@@ -304,6 +332,7 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
           }
         }
         csync();
+        TR_MARK(5);
         // K = (tau / 2) p.v ; w = p - K v   (whole vectors, every CTA)
         double kp = 0.0;
         for (int i = j + 1 + t; i < k; i += TC_NT) kp = fma(pb[i], Vc[i], kp);
@@ -316,6 +345,7 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
         for (int i = j + 1 + t; i < k; i += TC_NT) Ws[c * GT_KMAX + i] = pb[i] - K * Vc[i];
       }
       __syncthreads();
+      TR_MARK(6);
     }
     // trailing rank-2*nbp update of the owned columns >= J, rows >= J
     const int J = j0 + nbp;
@@ -353,9 +383,14 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
       }
     }
     csync();
+    TR_MARK(7);
     for (int e = t; e < 2 * TC_NB * GT_KMAX; e += TC_NT) smem[e] = 0.0;
     __syncthreads();
   }
+  if (trace)
+    printf("[gtrd tridiag k=%d coop=%d] cycles: reduce %lld | sum %lld | v %lld | A22v %lld | exchange %lld | w %lld | "
+           "trailing %lld\n", k, (int)coop, tr_acc[1], tr_acc[2], tr_acc[3], tr_acc[4], tr_acc[5], tr_acc[6], tr_acc[7]);
+#undef TR_MARK
   if (r != 0) return;
   // T (d, e) into shared memory; the last 2x2 block from the reduced matrix
   double* d = xrow;
@@ -562,7 +597,7 @@ __global__ void k_gtrd_cluster(ProjArgs a) {
   }
   if (nsel > 0) gs[grp++] = gbeg;
   gs[grp] = nsel;  // sentinel
-  if (gt.debug)
+  if (gt.debug == 1)
     printf("gtrd giant %d k %d nneg %d side %d nsel %d cap %d pieces %d max %d cuts %d groups %d\n", g, k, nneg, side,
            nsel, cap, npiece, pmax, nsplit, grp);
   gt.ngrp[g] = grp;
@@ -808,7 +843,7 @@ __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
   }
   if (!(res <= 1e-9 * fmax(tn, 1e-300)) || gt.force_fallback) {  // includes NaN
     gt.status[g] = -1;
-    if (gt.debug)
+    if (gt.debug == 1)
       printf("gtrd giant %d k %d: vector %d (lam %.3e rq %.3e) residual %.2e ||T|| %.2e -> fallback\n", g, k, s,
              W.lsel()[s], rq, res, tn);
   }
