@@ -530,17 +530,21 @@ __global__ void __launch_bounds__(32) k_gtrd_bisect(ProjArgs a) {
 // the residual test below still guards every vector).  Then: distinct shifts inside the pieces
 // and the groups of the vector kernel (consecutive pieces packed first-fit into <= cap(k)
 // indices, <= 2 ceil(k / cap) + 1 groups).  One thread per giant.
-__global__ void k_gtrd_cluster(ProjArgs a) {
+__global__ void __launch_bounds__(32) k_gtrd_cluster(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= gt.ng || gt.status[g] < 0) return;
+  const int g = blockIdx.x;
+  if (gt.status[g] < 0) return;
   const int k = a.ksz[gt.task[g]];
   const int cap = gtrd_vec_cap(k);
   const GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
+  // the eigenvalues into shared memory (the scan below is sequential: one lane)
+  extern __shared__ double la[];
+  for (int i = threadIdx.x; i < k; i += 32) la[i] = W.lall()[i];
+  __syncwarp();
+  if (threadIdx.x != 0) return;
   double* h = W.hdr();
   const double tn = h[2], ortol = 1e-3 * tn, pertol = 10.0 * kEps * tn;
-  const double* la = W.lall();
   const int nneg = (int)h[7];
   auto max_cluster = [&](int b, int e) {
     int m = 0, run = 0;
@@ -558,14 +562,15 @@ __global__ void k_gtrd_cluster(ProjArgs a) {
   h[0] = nsel;
   h[1] = side;
   double* ls = W.lsel();
-  for (int t = 0; t < nsel; ++t) ls[t] = la[base + t];
   double* cl = W.clst();
   double* gs = W.gsr();
   int grp = 0, gbeg = 0, npiece = 0, pmax = 0, nsplit = 0;
   auto place = [&](int pb, int pe) {  // piece [pb, pe)
     for (int t = pb; t < pe; ++t) {
       cl[t] = (double)pb;
-      if (t > pb && ls[t] - ls[t - 1] < pertol) ls[t] = ls[t - 1] + pertol;
+      double& lt = la[base + t];
+      if (t > pb && lt - la[base + t - 1] < pertol) lt = la[base + t - 1] + pertol;
+      ls[t] = lt;
     }
     if (pe - gbeg > cap) {  // does not fit the open group: close it at pb
       gs[grp++] = gbeg;
@@ -1170,7 +1175,7 @@ void launch_mode(const ProjArgs& a, cudaStream_t s) {
   }
   if (gt.tot_ev) {
     k_gtrd_bisect<<<gt.tot_ev, 32, (size_t)2 * gt.kmax * sizeof(double), s>>>(a);
-    k_gtrd_cluster<<<(gt.ng + 31) / 32, 32, 0, s>>>(a);
+    k_gtrd_cluster<<<gt.ng, 32, (size_t)gt.kmax * sizeof(double), s>>>(a);
     k_gtrd_vec<<<gt.tot_vg, VT, (size_t)kVecSmemDoubles * sizeof(double), s>>>(a);
   }
   if (gt.tot_wy) k_gtrd_wy<<<gt.tot_wy, GB_NT, kWySmem, s>>>(a);
