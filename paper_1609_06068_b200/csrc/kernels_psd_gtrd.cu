@@ -15,7 +15,7 @@
 //      the side of 0 with fewer eigenvalues, those eigenvalues by bisection
 //      (one thread each, Sturm counts with the LAPACK pivmin guard), clusters
 //      (gap <= 1e-3 ||T||) and inverse iteration as in LAPACK dstein (partial-
-//      pivoting tridiagonal LU, 3 solves, modified Gram-Schmidt in the cluster),
+//      pivoting tridiagonal LU, 2 solves, modified Gram-Schmidt in the cluster),
 //      residual-checked.
 //   3. k_gtrd_back (one CTA per 32 selected vectors): V = H_0 ... H_{k-3} Z,
 //      reflectors staged 16 at a time in shared memory, a warp per column with
@@ -610,13 +610,17 @@ __global__ void __launch_bounds__(32) k_gtrd_cluster(ProjArgs a) {
 
 // Inverse iteration (LAPACK dstein) for one group of <= cap(k) selected eigenvalues per CTA, one
 // thread per eigenvalue: partial-pivoting LU of T - lam I in global memory ([i][s], coalesced,
-// loads batched 8 deep), the iterate in shared memory (column per thread), 3 solves from a
+// loads batched 8 deep), the iterate in shared memory (column per thread), kInvIters solves from a
 // deterministic start vector, each followed by normalisation and modified Gram-Schmidt inside
 // the cluster piece (its members are consecutive threads of the CTA).  Weight of vector z: its
 // Rayleigh quotient z^T T z clipped at 0 on the selected side; a residual ||T z - rq z||_inf
 // above 1e-9 ||T|| hands the matrix to the fallback.
 constexpr int VB = 8;
 constexpr int VT = 128;
+// solves per vector: the shift is within 1e-11 ||T|| of the eigenvalue and clusters are
+// orthogonalised explicitly, so two solves leave other components below (1e-8)^2 of a
+// random start; the residual test below guards the exceptions
+constexpr int kInvIters = 2;
 __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
@@ -698,7 +702,7 @@ __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
   }
   // does any cluster of this group have more than one member?
   const bool multi = __syncthreads_or(act && (s > lead || (s + 1 < se && (int)W.clst()[s + 1] == s)));
-  for (int it = 0; it < 3; ++it) {
+  for (int it = 0; it < kInvIters; ++it) {
     if (act) {
       // forward: L^{-1} x (row interchanges as recorded)
       double ry = x[0];
