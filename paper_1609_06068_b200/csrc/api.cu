@@ -275,7 +275,7 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
     ev[g + 1] = ev[g] + (ok ? (k + 31) / 32 : 0);
     vg[g + 1] = vg[g] + (ok ? 2 * ((k + gtrd_vec_cap(k) - 1) / gtrd_vec_cap(k)) + 1 : 0);
     wy[g + 1] = wy[g] + (ok ? (k - 2 + 15) / 16 : 0);
-    bt[g + 1] = bt[g] + (ok ? (k + 15) / 16 : 0);
+    bt[g + 1] = bt[g] + (ok ? (k + kGtrdBackCols - 1) / kGtrdBackCols : 0);
     rc[g + 1] = rc[g] + (ok ? R * (R + 1) / 2 : 0);
   }
   // tridiagonalization jobs: one 8-CTA cluster per order >= SDP_GTRD_COOP_MIN (default 200),

@@ -92,7 +92,7 @@ struct GtrdDev {
   const int32_t* vg_pre = nullptr;     // ng + 1: inverse-iteration warps (2 ceil(H / 32) + 1 groups)
   int32_t* ngrp = nullptr;             // per giant: groups in use (device-computed)
   const int32_t* wy_pre = nullptr;     // ng + 1: WY groups (16 reflectors each)
-  const int32_t* bt_pre = nullptr;     // ng + 1: back-transform CTAs (16 columns each)
+  const int32_t* bt_pre = nullptr;     // ng + 1: back-transform CTAs (kGtrdBackCols columns each)
   const int32_t* rc_pre = nullptr;     // ng + 1: reconstruction tiles (32 x 32, upper)
   double* part = nullptr;              // 3 per reconstruction tile (primal residual partials)
   int tot_ev = 0, tot_vg = 0, tot_wy = 0, tot_bt = 0, tot_rc = 0;
@@ -179,6 +179,8 @@ void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_gtrd(int mode, const ProjArgs& a, cudaStream_t s);
+// columns per back-transform CTA of the giant tridiagonal path (one warp each)
+constexpr int kGtrdBackCols = 16;
 // vector-kernel group capacity of the giant tridiagonal path for order k (shared-memory bound)
 constexpr int kVecSmemDoubles = 26000;
 __host__ __device__ inline int gtrd_vec_cap(int k) {

@@ -925,7 +925,9 @@ __global__ void __launch_bounds__(GB_NT) k_gtrd_wy(ProjArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
+constexpr int GBC_NT = 32 * kGtrdBackCols;  // back-transform CTA: a warp per column
+
+__global__ void __launch_bounds__(GBC_NT, 1) k_gtrd_back(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
   const int item = blockIdx.x;
@@ -935,7 +937,7 @@ __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
   const int H = gt.hsel[g];
   const GView W{gt.ws + gt.moff[g], k, H};
   const int nsel = (int)W.hdr()[0];
-  const int col0 = (item - gt.bt_pre[g]) * (GB_NT / 32);
+  const int col0 = (item - gt.bt_pre[g]) * kGtrdBackCols;
   if (col0 >= nsel) return;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int col = col0 + wid;
@@ -958,7 +960,7 @@ __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
     const int nr = min(GB_NR, jhi + 1);
     const int jlo = jhi - nr + 1;
     double* dst = vb + b * GB_NR * GT_KMAX;
-    for (int e = threadIdx.x; e < GB_NR * k; e += GB_NT) {
+    for (int e = threadIdx.x; e < GB_NR * k; e += GBC_NT) {
       const int c = e % GB_NR, i = e / GB_NR;
       const int j = jlo + c;
       if (c >= nr || i < j + 1)
@@ -968,8 +970,8 @@ __global__ void __launch_bounds__(GB_NT, 1) k_gtrd_back(ProjArgs a) {
       else
         cp_async8(dst + c * GT_KMAX + i, M + (int64_t)i * LD + j);
     }
-    if (threadIdx.x < GB_NR * GB_NR)
-      cp_async8(Tm + b * GB_NR * GB_NR + threadIdx.x, W.wyT() + (int64_t)gi * GB_NR * GB_NR + threadIdx.x);
+    for (int e = threadIdx.x; e < GB_NR * GB_NR; e += GBC_NT)
+      cp_async8(Tm + b * GB_NR * GB_NR + e, W.wyT() + (int64_t)gi * GB_NR * GB_NR + e);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
   stage(0, 0);
@@ -1183,7 +1185,7 @@ void launch_mode(const ProjArgs& a, cudaStream_t s) {
     k_gtrd_vec<<<gt.tot_vg, VT, (size_t)kVecSmemDoubles * sizeof(double), s>>>(a);
   }
   if (gt.tot_wy) k_gtrd_wy<<<gt.tot_wy, GB_NT, kWySmem, s>>>(a);
-  if (gt.tot_bt) k_gtrd_back<<<gt.tot_bt, GB_NT, kBackSmem, s>>>(a);
+  if (gt.tot_bt) k_gtrd_back<<<gt.tot_bt, GBC_NT, kBackSmem, s>>>(a);
   if (gt.tot_rc) k_gtrd_recon<MODE><<<(gt.tot_rc + GR_NW - 1) / GR_NW, GR_NW * 32, GR_NW * sizeof(GrSmem), s>>>(a);
   if (MODE == PM_PRIMAL) k_gtrd_fin<<<(gt.ng + 127) / 128, 128, 0, s>>>(a);
 }
