@@ -39,7 +39,6 @@ namespace sdp {
 namespace {
 
 constexpr int GT_KMAX = 800;
-constexpr int GT_RT = GT_KMAX / 32;  // rows per lane in the back-transform (25)
 constexpr double kInvSqrt2 = 0.70710678118654752440;
 constexpr double kSqrt2 = 1.41421356237309504880;
 constexpr double kEps = 2.220446049250313e-16;
@@ -925,9 +924,24 @@ __global__ void __launch_bounds__(GB_NT) k_gtrd_wy(ProjArgs a) {
   }
 }
 
-constexpr int GBC_NT = 32 * kGtrdBackCols;  // back-transform CTA: a warp per column
+// k_gtrd_back: the columns of a CTA (kGtrdBackCols = 16) live in shared memory as a k x 16 block
+// Zs; 8 warps own 8-row-aligned slices of its rows.  Per group: S = Y^T Zs (16 x 16, DMMA
+// m8n8k4 over each warp's rows, partials summed in a fixed order), U = T S, Zs -= Y U (DMMA on
+// the warp's rows).  Y is staged with cp.async; shared memory: Y 16 x (k_max + 4), Zs 832 x 16.
+constexpr int BM_NW = 8;
+constexpr int BM_NT = 32 * BM_NW;
+constexpr int BM_ZROWS = 8 * (((GT_KMAX + 63) / 64) * 8);  // 8 warps x rows per warp (max)
+constexpr int BM_YLD = BM_ZROWS + 4;  // >= the rows the warps sweep; == 4 (mod 16): conflict-free Y^T fragments
+static_assert(BM_YLD % 16 == 4, "Y row stride");
+static_assert(kGtrdBackCols == 16, "two 8-wide DMMA column tiles");
 
-__global__ void __launch_bounds__(GBC_NT, 1) k_gtrd_back(ProjArgs a) {
+__device__ __forceinline__ void dmma_b(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(BM_NT, 1) k_gtrd_back(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
   const int item = blockIdx.x;
@@ -939,89 +953,103 @@ __global__ void __launch_bounds__(GBC_NT, 1) k_gtrd_back(ProjArgs a) {
   const int nsel = (int)W.hdr()[0];
   const int col0 = (item - gt.bt_pre[g]) * kGtrdBackCols;
   if (col0 >= nsel) return;
-  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int col = col0 + wid;
-  extern __shared__ double vb[];          // Y: 2 x GB_NR x GT_KMAX (double buffer)
-  double* Tm = vb + 2 * GB_NR * GT_KMAX;  // 2 x T
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31, r4 = lane >> 2, c4 = lane & 3;
+  extern __shared__ double smb[];
+  double* Ys = smb;                       // [c][i], 16 x BM_YLD
+  double* Zs = Ys + 16 * BM_YLD;          // [i][col], BM_ZROWS x 16
+  double* Sp = Zs + BM_ZROWS * 16;        // BM_NW x 256 partials of S, then S and U
+  double* Ts = Sp + BM_NW * 256;          // T of the group (16 x 16)
   const double* M = W.M();
   const int LD = W.ld();
   double* Z = W.Z();
-  double z[GT_RT];
-#pragma unroll
-  for (int r = 0; r < GT_RT; ++r) {
-    const int i = lane + 32 * r;
-    z[r] = (col < nsel && i < k) ? Z[(int64_t)col * k + i] : 0.0;
+  const int RS = ((k + 63) / 64) * 8;     // rows per warp (8 | RS, 8 RS >= k)
+  const int rb = wid * RS;
+  for (int e = t; e < 16 * BM_YLD; e += BM_NT) Ys[e] = 0.0;
+  for (int e = t; e < BM_ZROWS * 16; e += BM_NT) {
+    const int col = e / BM_ZROWS, i = e % BM_ZROWS;  // coalesced along a column of Z
+    Zs[i * 16 + col] = (i < k && col0 + col < nsel) ? Z[(int64_t)(col0 + col) * k + i] : 0.0;
   }
   const int ngr = W.nwy();
-  // group gi -> buffer b: cp.async (8-byte LDGSTS) for the stored reflector entries, plain stores
-  // for the implicit zeros / ones, T from k_gtrd_wy; in flight while the previous group is applied
-  auto stage = [&](int gi, int b) {
+  for (int gi = 0; gi < ngr; ++gi) {
     const int jhi = k - 3 - gi * GB_NR;
     const int nr = min(GB_NR, jhi + 1);
     const int jlo = jhi - nr + 1;
-    double* dst = vb + b * GB_NR * GT_KMAX;
-    for (int e = threadIdx.x; e < GB_NR * k; e += GBC_NT) {
+    __syncthreads();  // previous group's Y / U no longer read
+    for (int e = t; e < GB_NR * k; e += BM_NT) {  // v_j lives in column j of M: c fastest
       const int c = e % GB_NR, i = e / GB_NR;
       const int j = jlo + c;
       if (c >= nr || i < j + 1)
-        dst[c * GT_KMAX + i] = 0.0;
+        Ys[c * BM_YLD + i] = 0.0;
       else if (i == j + 1)
-        dst[c * GT_KMAX + i] = 1.0;
+        Ys[c * BM_YLD + i] = 1.0;
       else
-        cp_async8(dst + c * GT_KMAX + i, M + (int64_t)i * LD + j);
+        cp_async8(Ys + c * BM_YLD + i, M + (int64_t)i * LD + j);
     }
-    for (int e = threadIdx.x; e < GB_NR * GB_NR; e += GBC_NT)
-      cp_async8(Tm + b * GB_NR * GB_NR + e, W.wyT() + (int64_t)gi * GB_NR * GB_NR + e);
+    for (int e = t; e < GB_NR * GB_NR; e += BM_NT) cp_async8(Ts + e, W.wyT() + (int64_t)gi * GB_NR * GB_NR + e);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  stage(0, 0);
-  for (int gi = 0; gi < ngr; ++gi) {
-    const int b = gi & 1;
-    const int jlo = max(0, k - 3 - gi * GB_NR - GB_NR + 1);
     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-    __syncthreads();  // buffer b complete; buffer b ^ 1 no longer read
-    if (gi + 1 < ngr) stage(gi + 1, b ^ 1);
-    if (col < nsel) {
-      const double* Y = vb + b * GB_NR * GT_KMAX;
-      const double* T = Tm + b * GB_NR * GB_NR;
-      double w[GB_NR];
+    __syncthreads();
+    // S partial = Y(rows of this warp)^T Zs(rows of this warp)
+    {
+      double acc[2][2][2];
 #pragma unroll
-      for (int c = 0; c < GB_NR; ++c) w[c] = 0.0;
+      for (int m = 0; m < 2; ++m)
 #pragma unroll
-      for (int r = 0; r < GT_RT; ++r) {
-        const int i = lane + 32 * r;
-        if (i < k && i > jlo) {
-#pragma unroll
-          for (int c = 0; c < GB_NR; ++c) w[c] = fma(Y[c * GT_KMAX + i], z[r], w[c]);
-        }
+        for (int n = 0; n < 2; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
+      const int kb = max(rb, (jlo + 1) & ~3);  // rows <= jlo are zero in Y
+      for (int kk = kb; kk < rb + RS; kk += 4) {
+        const double a0 = Ys[r4 * BM_YLD + kk + c4], a1 = Ys[(8 + r4) * BM_YLD + kk + c4];
+        const double b0 = Zs[(kk + c4) * 16 + r4], b1 = Zs[(kk + c4) * 16 + 8 + r4];
+        dmma_b(acc[0][0], a0, b0);
+        dmma_b(acc[0][1], a0, b1);
+        dmma_b(acc[1][0], a1, b0);
+        dmma_b(acc[1][1], a1, b1);
       }
 #pragma unroll
-      for (int c = 0; c < GB_NR; ++c) w[c] = warp_sum(w[c]);
+      for (int m = 0; m < 2; ++m)
 #pragma unroll
-      for (int c = 0; c < GB_NR; ++c) {  // u = T w (T upper), in place in ascending order
-        double u = 0.0;
+        for (int n = 0; n < 2; ++n) {
+          Sp[wid * 256 + (m * 8 + r4) * 16 + n * 8 + 2 * c4] = acc[m][n][0];
+          Sp[wid * 256 + (m * 8 + r4) * 16 + n * 8 + 2 * c4 + 1] = acc[m][n][1];
+        }
+    }
+    __syncthreads();
+    // S = sum of the partials (fixed order), then U = T S (T upper)
+    double sv = 0.0;
+    for (int w = 0; w < BM_NW; ++w) sv += Sp[w * 256 + t];
+    __syncthreads();
+    Sp[t] = sv;  // S[c][col], t = c * 16 + col
+    __syncthreads();
+    {
+      const int c = t >> 4, col = t & 15;
+      double u = 0.0;
+      for (int q = c; q < GB_NR; ++q) u = fma(Ts[c * GB_NR + q], Sp[q * 16 + col], u);
+      Sp[256 + t] = u;  // U[c][col]
+    }
+    __syncthreads();
+    // Zs(rows of this warp) -= Y(rows) U
+    const double* U = Sp + 256;
+    for (int it = 0; it < RS; it += 8) {
+      if (rb + it + 7 <= jlo) continue;  // Y rows <= jlo are zero
+      double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-        for (int q = c; q < GB_NR; ++q) u = fma(T[c * GB_NR + q], w[q], u);
-        w[c] = u;
+      for (int ks = 0; ks < 4; ++ks) {
+        const double av = Ys[(ks * 4 + c4) * BM_YLD + rb + it + r4];
+        dmma_b(acc[0], av, U[(ks * 4 + c4) * 16 + r4]);
+        dmma_b(acc[1], av, U[(ks * 4 + c4) * 16 + 8 + r4]);
       }
 #pragma unroll
-      for (int r = 0; r < GT_RT; ++r) {
-        const int i = lane + 32 * r;
-        if (i < k && i > jlo) {
-          double acc = z[r];
-#pragma unroll
-          for (int c = 0; c < GB_NR; ++c) acc = fma(-Y[c * GT_KMAX + i], w[c], acc);
-          z[r] = acc;
-        }
+      for (int n = 0; n < 2; ++n) {
+        double* zp = Zs + (rb + it + r4) * 16 + n * 8 + 2 * c4;
+        zp[0] -= acc[n][0];
+        zp[1] -= acc[n][1];
       }
     }
   }
-  if (col < nsel) {
-#pragma unroll
-    for (int r = 0; r < GT_RT; ++r) {
-      const int i = lane + 32 * r;
-      if (i < k) Z[(int64_t)col * k + i] = z[r];
-    }
+  __syncthreads();
+  for (int e = t; e < k * 16; e += BM_NT) {
+    const int col = e / k, i = e % k;
+    if (col0 + col < nsel) Z[(int64_t)(col0 + col) * k + i] = Zs[i * 16 + col];
   }
 }
 
@@ -1159,7 +1187,7 @@ __global__ void k_gtrd_fin(ProjArgs a) {
 
 
 constexpr size_t kWySmem = (size_t)(GB_NR * GT_KMAX + 2 * GB_NR * GB_NR) * sizeof(double);
-constexpr size_t kBackSmem = (size_t)(2 * GB_NR * GT_KMAX + 2 * GB_NR * GB_NR) * sizeof(double);
+constexpr size_t kBackSmem = (size_t)(16 * BM_YLD + BM_ZROWS * 16 + BM_NW * 256 + GB_NR * GB_NR) * sizeof(double);
 
 template <int MODE>
 void launch_mode(const ProjArgs& a, cudaStream_t s) {
@@ -1185,7 +1213,7 @@ void launch_mode(const ProjArgs& a, cudaStream_t s) {
     k_gtrd_vec<<<gt.tot_vg, VT, (size_t)kVecSmemDoubles * sizeof(double), s>>>(a);
   }
   if (gt.tot_wy) k_gtrd_wy<<<gt.tot_wy, GB_NT, kWySmem, s>>>(a);
-  if (gt.tot_bt) k_gtrd_back<<<gt.tot_bt, GBC_NT, kBackSmem, s>>>(a);
+  if (gt.tot_bt) k_gtrd_back<<<gt.tot_bt, BM_NT, kBackSmem, s>>>(a);
   if (gt.tot_rc) k_gtrd_recon<MODE><<<(gt.tot_rc + GR_NW - 1) / GR_NW, GR_NW * 32, GR_NW * sizeof(GrSmem), s>>>(a);
   if (MODE == PM_PRIMAL) k_gtrd_fin<<<(gt.ng + 127) / 128, 128, 0, s>>>(a);
 }
