@@ -526,7 +526,8 @@ __global__ void __launch_bounds__(32) k_gtrd_bisect(ProjArgs a) {
 // eigenvalues while the positive side stays well separated).  A cluster larger than cap(k) is
 // cut at its largest gaps into pieces of <= cap(k) (vectors of different pieces are then
 // orthogonal to eps ||T|| / gap, gap being the largest gap in a window of cap(k) eigenvalues;
-// the residual test below still guards every vector).  Then: distinct shifts inside the pieces
+// a cut at a gap below 1e-6 ||T|| hands the matrix to the block-Jacobi fallback; the residual
+// test below still guards every vector).  Then: distinct shifts inside the pieces
 // and the groups of the vector kernel (consecutive pieces packed first-fit into <= cap(k)
 // indices, <= 2 ceil(k / cap) + 1 groups).  One thread per giant.
 __global__ void __launch_bounds__(32) k_gtrd_cluster(ProjArgs a) {
@@ -564,6 +565,7 @@ __global__ void __launch_bounds__(32) k_gtrd_cluster(ProjArgs a) {
   double* cl = W.clst();
   double* gs = W.gsr();
   int grp = 0, gbeg = 0, npiece = 0, pmax = 0, nsplit = 0;
+  bool bad_cut = false;
   auto place = [&](int pb, int pe) {  // piece [pb, pe)
     for (int t = pb; t < pe; ++t) {
       cl[t] = (double)pb;
@@ -592,6 +594,9 @@ __global__ void __launch_bounds__(32) k_gtrd_cluster(ProjArgs a) {
           best = x;
         }
       }
+      // vectors of different pieces are orthogonal only to ~(eps + 1e-11) ||T|| / gap: a cut inside
+      // a (near-)degenerate run would leave them unorthogonalised -> block-Jacobi fallback
+      if (bg < 1e-6 * tn) bad_cut = true;
       place(b, best);
       ++nsplit;
       b = best;
@@ -605,6 +610,7 @@ __global__ void __launch_bounds__(32) k_gtrd_cluster(ProjArgs a) {
     printf("gtrd giant %d k %d nneg %d side %d nsel %d cap %d pieces %d max %d cuts %d groups %d\n", g, k, nneg, side,
            nsel, cap, npiece, pmax, nsplit, grp);
   gt.ngrp[g] = grp;
+  if (bad_cut) gt.status[g] = -1;
 }
 
 // Inverse iteration (LAPACK dstein) for one group of <= cap(k) selected eigenvalues per CTA, one

@@ -410,6 +410,26 @@ def test_gtrd_batch_orders_and_structured(lib, gen):
     check_batch(lib, ks, vals, tol=1e-12)
 
 
+def test_gtrd_clusters_beyond_a_group(lib, gen):
+    """Clusters larger than a vector-kernel group (cap(k) = min(128, 26000/k - 2)):
+    a dense band of distinct eigenvalues is cut at its largest gaps (tridiagonal path);
+    exactly repeated eigenvalues on both sides of 0 cannot be cut safely and go to the
+    block-Jacobi fallback.  Both against the oracle."""
+    rng = np.random.default_rng(21)
+    mats = []
+    k = 500                                   # cap = 50
+    Q, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    lam = np.concatenate([np.linspace(-1.2, -1.0, 200), np.linspace(1.0, 1.5, 300)])
+    mats.append((Q * lam) @ Q.T)              # bands of 200 and 300: cuts at gaps ~5e-4 ||T||
+    k = 300                                   # cap = 84
+    Q, _ = np.linalg.qr(rng.standard_normal((k, k)))
+    lam = np.repeat([-1.0, 2.0], 150)
+    mats.append((Q * lam) @ Q.T)              # two multiplicity-150 eigenvalues: fallback
+    ks = np.array([M.shape[0] for M in mats], dtype=np.int32)
+    vals = np.concatenate([opsd.pack_upper(M) for M in mats])
+    check_batch(lib, ks, vals, tol=1e-11)
+
+
 def _giant_env_batch(env_extra):
     import subprocess
     import sys
