@@ -114,6 +114,9 @@ typedef struct {
   int32_t launches_per_iter; /* kernels launched per ADMM iteration                   */
   int64_t jacobi_sweeps;     /* total Jacobi sweeps over all projections since reset  */
   double rho;                /* penalty currently in force (changes with adapt_rho / sdp_set_rho) */
+  int32_t pipelined;         /* 1: the pipelined primal iteration is in use:
+                              * sdp_step(n) overlaps the projections with the A passes of the
+                              * neighbouring iterations; SDP_PIPELINE=0 at setup turns it off */
 } sdp_info;
 
 typedef struct sdp_handle_s* sdp_handle;

@@ -73,7 +73,8 @@ class sdp_info(C.Structure):
                 ("setup_s", C.c_double), ("n", C.c_int64), ("m", C.c_int64), ("N", C.c_int64), ("p", C.c_int64),
                 ("kmin", C.c_int64), ("kmax", C.c_int64), ("stot", C.c_int64), ("form", C.c_int32),
                 ("s_diagonal", C.c_int32), ("jacobi_capped", C.c_int64),
-                ("launches_per_iter", C.c_int32), ("jacobi_sweeps", C.c_int64), ("rho", C.c_double)]
+                ("launches_per_iter", C.c_int32), ("jacobi_sweeps", C.c_int64), ("rho", C.c_double),
+                ("pipelined", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

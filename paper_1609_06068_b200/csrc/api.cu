@@ -136,6 +136,55 @@ struct TierFork {
   }
 };
 
+// Pipelined primal iteration (dense A, one rank, no giant tier; DESIGN.md §7 "Pipelined iteration"):
+// the cliques are split in two halves H1 = [0, p1), H2 = [p1, p); coordinates are classed by the
+// halves that touch them.  One iteration = A: u = A D^-1 r1 (all column pieces), y = S^-1 u,
+// x on the coordinates H1 touches; B: x on the H2-only coordinates || P_+ of H1 and the scatter
+// of the H1-only coordinates, then P_+ of H2, the rest of the scatter, finalize.  sdp_step(n)
+// launches A (BA)^(n-1) B, and inside BA the next iteration's A-pass over the H1-only columns
+// runs concurrently with P_+ of H2: the projections hide under the two A passes.
+struct BucketSet {
+  int32_t* d_ids[B_NUM] = {};
+  int bcount[B_NUM] = {};
+  TrdDev td[2];
+};
+struct Pipe {
+  bool on = false;
+  int p1 = 0;
+  int32_t *rows1 = nullptr, *rows2 = nullptr;         // gemvT coordinates: touched by H1 / H2 only
+  int nr1 = 0, nr2 = 0;
+  int32_t *sc1 = nullptr, *sc2 = nullptr, *lc1 = nullptr, *lc2 = nullptr;  // scatter passes (short, long)
+  int ns1 = 0, ns2 = 0, nl1 = 0, nl2 = 0;
+  int64_t* pieces = nullptr;                          // gemv column pieces: H1-only first, then the rest
+  int npe = 0, npl = 0;
+  double *gemv_part = nullptr, *gT_part = nullptr, *scat_part = nullptr;
+  int nb_gT1 = 0, nb_gT2 = 0, nb_sc1 = 0, nb_sc2 = 0;
+  BucketSet half[2];
+  cudaStream_t sp = nullptr, sp2 = nullptr, sx = nullptr, sg = nullptr;  // projections (high priority), gemvT, gemv
+  int prio_hi = 0;
+  cudaEvent_t ev[8] = {};
+  cudaGraph_t g[3] = {};
+  cudaGraphExec_t x[3] = {};  // A, BA, B
+  void destroy_graphs() {
+    for (int i = 0; i < 3; ++i) {
+      if (x[i]) cudaGraphExecDestroy(x[i]);
+      if (g[i]) cudaGraphDestroy(g[i]);
+      x[i] = nullptr;
+      g[i] = nullptr;
+    }
+  }
+  void destroy() {
+    destroy_graphs();
+    if (sp) cudaStreamDestroy(sp);
+    if (sp2) cudaStreamDestroy(sp2);
+    if (sx) cudaStreamDestroy(sx);
+    if (sg) cudaStreamDestroy(sg);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+    sp = sp2 = sx = sg = nullptr;
+  }
+};
+
 struct sdp_handle_s {
   int n = 0, m = 0;
   int64_t N = 0, lda = 0, p = 0, stot = 0;
@@ -167,6 +216,7 @@ struct sdp_handle_s {
   GiantDev gd;
   TrdDev td[2];  // B_TRD32, B_TRD64
   TierFork tiers;
+  Pipe pipe;
   // A
   int a_dense = 1;
   double* A = nullptr;
@@ -198,6 +248,7 @@ struct sdp_handle_s {
   void* comm = nullptr;         // ncclComm_t
   int64_t cb = 0, pl = 0, Nl = 0, stotl = 0;  // first clique, local cliques / coordinates / stacked length
   std::vector<int32_t> local_coords;
+  bool coord_perm = false;      // world == 1 with a permuted local coordinate order (pipelined iteration)
   double* own = nullptr;        // 1.0 on owned local coordinates
   int nshared = 0, n_fix = 0;
   int32_t *shared_idx = nullptr, *shared_local = nullptr;
@@ -575,7 +626,8 @@ void enqueue_kkt(sdp_handle h, cudaStream_t s) {
                      h->done, s);
 }
 
-void enqueue_finalize(sdp_handle h, cudaStream_t s) {
+void enqueue_finalize(sdp_handle h, cudaStream_t s, const double* scat_part = nullptr, int n_scat = 0,
+                      const double* gT_part = nullptr, int n_gT = 0) {
   FinalArgs a{};
   a.proj_part = h->proj_part;
   a.n_proj = (int)h->pl;
@@ -584,10 +636,10 @@ void enqueue_finalize(sdp_handle h, cudaStream_t s) {
   a.red = h->red;
   a.upd_part = h->upd_part;
   a.n_upd = h->nb_upd;
-  a.scat_part = h->scat_part;
-  a.n_scat = h->nb_scat;
-  a.gT_part = h->gT_part;
-  a.n_gT = h->nb_gT;
+  a.scat_part = scat_part ? scat_part : h->scat_part;
+  a.n_scat = scat_part ? n_scat : h->nb_scat;
+  a.gT_part = gT_part ? gT_part : h->gT_part;
+  a.n_gT = gT_part ? n_gT : h->nb_gT;
   a.b = h->b;
   a.y = h->y;
   a.m = h->m;
@@ -609,7 +661,301 @@ void enqueue_finalize(sdp_handle h, cudaStream_t s) {
 }
 
 // One ADMM iteration (Algorithm 1 lines 4-7 / Algorithm 2 lines 4-8).
+// ---------------------------------------------------------------- pipelined primal iteration
+// Setup of the pipelined iteration (see struct Pipe).  SDP_PIPELINE=0 turns it off.
+void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vector<int64_t>& off,
+                    const std::vector<int32_t>& seg_ptr, const std::vector<int>& task_bucket) {
+  Pipe& P = h->pipe;
+  P = Pipe{};
+  const char* env = getenv("SDP_PIPELINE");
+  if (env && *env == '0') return;
+  const int64_t N = h->Nl, p = h->pl;
+  if (h->form != SDP_FORM_PRIMAL || !h->a_dense || h->world != 1 || h->bcount[B_GLOBAL] > 0 || N < 65536 || p < 8)
+    return;
+  Alloc& al = h->alloc;
+  // halves by stacked length
+  int p1 = 1;
+  while (p1 < p - 1 && off[p1] * 2 < off[p]) ++p1;
+  P.p1 = p1;
+  std::vector<uint8_t> cls(N, 0);  // bit 0: touched by H1, bit 1: by H2
+  for (int64_t k = 0; k < p; ++k)
+    for (int64_t e = off[k]; e < off[k + 1]; ++e) cls[G[e]] |= (k < p1) ? 1 : 2;
+  std::vector<int32_t> rows1, rows2, sc1, sc2, lc1, lc2;
+  for (int64_t t = 0; t < N; ++t) {
+    const bool lng = seg_ptr[t + 1] - seg_ptr[t] > kLongSeg;
+    if (cls[t] & 1) rows1.push_back((int32_t)t);
+    else rows2.push_back((int32_t)t);
+    if (cls[t] == 1) (lng ? lc1 : sc1).push_back((int32_t)t);
+    else (lng ? lc2 : sc2).push_back((int32_t)t);
+  }
+  // u = A D^-1 r1 column pieces: runs of H1-only coordinates, then runs of the rest, <= 32768 each
+  std::vector<int64_t> pe, pl2;
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<int64_t>& out = pass ? pl2 : pe;
+    int64_t t = 0;
+    while (t < N) {
+      const bool early = cls[t] == 1;
+      if (early != (pass == 0)) {
+        ++t;
+        continue;
+      }
+      int64_t e = t;
+      while (e < N && (cls[e] == 1) == early && e - t < 32768) ++e;
+      out.push_back(t);
+      out.push_back(e);
+      t = e;
+    }
+  }
+  P.npe = (int)pe.size() / 2;
+  P.npl = (int)pl2.size() / 2;
+  std::vector<int64_t> pieces(pe);
+  pieces.insert(pieces.end(), pl2.begin(), pl2.end());
+  if (P.npe == 0 || P.npl == 0 || rows2.empty()) return;  // nothing to overlap
+  P.pieces = al.upload(pieces);
+  P.rows1 = al.upload(rows1);
+  P.rows2 = al.upload(rows2);
+  P.nr1 = (int)rows1.size();
+  P.nr2 = (int)rows2.size();
+  P.sc1 = sc1.empty() ? nullptr : al.upload(sc1);
+  P.sc2 = sc2.empty() ? nullptr : al.upload(sc2);
+  P.lc1 = lc1.empty() ? nullptr : al.upload(lc1);
+  P.lc2 = lc2.empty() ? nullptr : al.upload(lc2);
+  P.ns1 = (int)sc1.size();
+  P.ns2 = (int)sc2.size();
+  P.nl1 = (int)lc1.size();
+  P.nl2 = (int)lc2.size();
+  P.gemv_part = al.zeros<double>((size_t)(P.npe + P.npl) * h->m);
+  P.nb_gT1 = gemvT_rows_blocks(P.nr1);
+  P.nb_gT2 = gemvT_rows_blocks(P.nr2);
+  P.gT_part = al.zeros<double>((size_t)(P.nb_gT1 + P.nb_gT2));
+  P.nb_sc1 = P.ns1 + P.nl1 > 0 ? scatter_blocks(P.ns1, P.nl1) : 0;
+  P.nb_sc2 = P.ns2 + P.nl2 > 0 ? scatter_blocks(P.ns2, P.nl2) : 0;
+  P.scat_part = al.zeros<double>(2 * (size_t)std::max(P.nb_sc1 + P.nb_sc2, 1));
+  // the two halves keep the tiers of the full assignment (the warm-start layout depends on it)
+  for (int hf = 0; hf < 2; ++hf) {
+    std::vector<std::vector<int32_t>> lists(B_NUM);
+    for (int64_t k = hf ? p1 : 0; k < (hf ? p : p1); ++k) lists[task_bucket[k]].push_back((int32_t)k);
+    BucketSet& B = P.half[hf];
+    for (int b = 0; b < B_NUM; ++b) {
+      B.bcount[b] = (int)lists[b].size();
+      B.d_ids[b] = B.bcount[b] ? al.upload(lists[b]) : nullptr;
+    }
+    std::vector<int32_t> ksz(p);
+    SDP_CUDA_TRY(cudaMemcpy(ksz.data(), h->d_ksz, p * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    build_trd(al, ksz, lists[B_TRD32], 32, B.td[0]);
+    build_trd(al, ksz, lists[B_TRD64], 64, B.td[1]);
+  }
+  int lo = 0, hi = 0;
+  SDP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  SDP_CUDA_TRY(cudaStreamCreateWithPriority(&P.sp, cudaStreamNonBlocking, hi));
+  SDP_CUDA_TRY(cudaStreamCreateWithPriority(&P.sp2, cudaStreamNonBlocking, hi));
+  P.prio_hi = hi;
+  SDP_CUDA_TRY(cudaStreamCreateWithFlags(&P.sx, cudaStreamNonBlocking));
+  SDP_CUDA_TRY(cudaStreamCreateWithFlags(&P.sg, cudaStreamNonBlocking));
+  for (auto& e : P.ev) SDP_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  P.on = true;
+}
+
+void pipe_gemv(sdp_handle h, cudaStream_t s, int first, int count) {
+  const Pipe& P = h->pipe;
+  launch_gemv_pieces(h->A, h->lda, h->m, h->rD, P.pieces + 2 * first, count, first, P.gemv_part, h->done, s);
+}
+
+void pipe_symv_gemvT1(sdp_handle h, cudaStream_t s) {
+  const Pipe& P = h->pipe;
+  launch_symv(SDP_FORM_PRIMAL, h->Sinv, h->m, P.gemv_part, P.npe + P.npl, h->b, h->rho, nullptr, h->y, h->done, s);
+  launch_gemvT_rows(SDP_FORM_PRIMAL, h->AT, h->ldm, h->m, P.nr1, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+                    P.gT_part, h->done, s, P.rows1);
+}
+
+void pipe_projection(sdp_handle h, int half, cudaStream_t s) {
+  const BucketSet& B = h->pipe.half[half];
+  ProjArgs a{};
+  a.off = h->d_off;
+  a.ksz = h->d_ksz;
+  a.x = h->x;
+  a.G = h->G;
+  a.xk = h->xk;
+  a.lam = h->lam;
+  a.vk = h->vk;
+  a.rho = h->rho;
+  a.part = h->proj_part;
+  a.capped = h->capped;
+  a.sweeps = h->sweeps;
+  a.done = h->done;
+  a.vprev = h->vprev;
+  a.voff = h->voff;
+  a.iter = h->iter;
+  a.warm_period = h->warm_period;
+  launch_tiers(a, PM_PRIMAL, B.d_ids, B.bcount, B.td, TierFork{}, s);
+}
+
+void pipe_scatter(sdp_handle h, int pass, cudaStream_t s) {
+  const Pipe& P = h->pipe;
+  ScatterArgs a{};
+  a.N = pass ? P.ns2 : P.ns1;
+  a.list = pass ? P.sc2 : P.sc1;
+  a.seg_ptr = h->seg_ptr;
+  a.seg_idx = h->seg_idx;
+  a.longc = pass ? P.lc2 : P.lc1;
+  a.n_long = pass ? P.nl2 : P.nl1;
+  a.xk = h->xk;
+  a.lam = h->lam;
+  a.c = h->c;
+  a.Dinv = h->Dinv;
+  a.rho = h->rho;
+  a.rD = h->rD;
+  a.sprev = h->sprev;
+  a.part = P.scat_part + 2 * (pass ? P.nb_sc1 : 0);
+  a.done = h->done;
+  launch_scatter(SDP_FORM_PRIMAL, a, s);
+}
+
+// SDP_PIPE_TRACE=1 with use_graph = 0: event timeline of the last launched B / BA (stderr)
+struct PipeTrace {
+  bool on = false;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  void mark(const char* name, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    ev.push_back({name, e});
+  }
+  void dump() {
+    if (!on || ev.empty()) return;
+    cudaDeviceSynchronize();
+    for (size_t i = 1; i < ev.size(); ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0].second, ev[i].second);
+      fprintf(stderr, "[pipe] %-14s %8.1f us\n", ev[i].first, ms * 1e3);
+    }
+    for (auto& e : ev) cudaEventDestroy(e.second);
+    ev.clear();
+  }
+};
+PipeTrace g_ptrace;
+
+void pipe_enqueue_A(sdp_handle h, cudaStream_t s) {
+  pipe_gemv(h, s, 0, h->pipe.npe + h->pipe.npl);
+  pipe_symv_gemvT1(h, s);
+}
+
+// B (with_A: then the next iteration's A, overlapped)
+void pipe_enqueue_B(sdp_handle h, cudaStream_t s, bool with_A) {
+  Pipe& P = h->pipe;
+  g_ptrace.mark("start", s);
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[0], s));
+  SDP_CUDA_TRY(cudaStreamWaitEvent(P.sx, P.ev[0], 0));
+  SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp, P.ev[0], 0));
+  // x on the H2-only coordinates || P_+ of H1, scatter of the H1-only coordinates
+  launch_gemvT_rows(SDP_FORM_PRIMAL, h->AT, h->ldm, h->m, P.nr2, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+                    P.gT_part + P.nb_gT1, h->done, P.sx, P.rows2);
+  g_ptrace.mark("gemvT2", P.sx);
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[1], P.sx));
+  pipe_projection(h, 0, P.sp);
+  g_ptrace.mark("projH1", P.sp);
+  pipe_scatter(h, 0, P.sp);
+  g_ptrace.mark("scatter1", P.sp);
+  if (with_A) {  // next iteration: u over the H1-only columns, while P_+ of H2 runs
+    SDP_CUDA_TRY(cudaEventRecord(P.ev[2], P.sp));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(P.sg, P.ev[2], 0));
+    pipe_gemv(h, P.sg, 0, P.npe);
+    g_ptrace.mark("gemv_early", P.sg);
+    SDP_CUDA_TRY(cudaEventRecord(P.ev[3], P.sg));
+  }
+  // P_+ of H2 as soon as x is complete on its coordinates (own stream: not behind P_+ of H1)
+  SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp2, P.ev[1], 0));
+  pipe_projection(h, 1, P.sp2);
+  g_ptrace.mark("projH2", P.sp2);
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[5], P.sp2));
+  SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp, P.ev[5], 0));
+  pipe_scatter(h, 1, P.sp);
+  enqueue_finalize(h, P.sp, P.scat_part, P.nb_sc1 + P.nb_sc2, P.gT_part, P.nb_gT1 + P.nb_gT2);
+  g_ptrace.mark("finalize", P.sp);
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[4], P.sp));
+  SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[4], 0));
+  if (with_A) {
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[3], 0));
+    pipe_gemv(h, s, P.npe, P.npl);
+    g_ptrace.mark("gemv_late", s);
+    pipe_symv_gemvT1(h, s);
+    g_ptrace.mark("symv+gemvT1", s);
+  }
+}
+
+void pipe_capture(sdp_handle h, int which, cudaGraph_t* g, cudaGraphExec_t* x) {
+  SDP_CUDA_TRY(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
+  if (which == 0)
+    pipe_enqueue_A(h, h->cap_stream);
+  else
+    pipe_enqueue_B(h, h->cap_stream, which == 1);
+  SDP_CUDA_TRY(cudaStreamEndCapture(h->cap_stream, g));
+  // stream priorities are not recorded by capture: every kernel node except the HBM-streaming
+  // passes gets the high priority, so that the projections are scheduled as soon as they are ready
+  size_t nn = 0;
+  SDP_CUDA_TRY(cudaGraphGetNodes(*g, nullptr, &nn));
+  std::vector<cudaGraphNode_t> nodes(nn);
+  SDP_CUDA_TRY(cudaGraphGetNodes(*g, nodes.data(), &nn));
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    SDP_CUDA_TRY(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp{};
+    if (cudaGraphKernelNodeGetParams(nd, &kp) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    if (is_stream_kernel(kp.func)) continue;
+    cudaKernelNodeAttrValue v{};
+    v.priority = h->pipe.prio_hi;
+    SDP_CUDA_TRY(cudaGraphKernelNodeSetAttribute(nd, cudaKernelNodeAttributePriority, &v));
+  }
+  SDP_CUDA_TRY(cudaGraphInstantiateWithFlags(x, *g, cudaGraphInstantiateFlagUseNodePriority));
+}
+
+int pipe_launches_per_iter(sdp_handle h) {
+  const Pipe& P = h->pipe;
+  int n = 0;
+  for (int hf = 0; hf < 2; ++hf)
+    for (int b = 0; b < B_NUM; ++b) {
+      if (!P.half[hf].bcount[b]) continue;
+      if (is_trd(b)) {
+        const TrdDev& t = P.half[hf].td[b - B_TRD32];
+        n += 4 * ((t.count + t.chunk - 1) / t.chunk);
+      } else {
+        n += 1;
+      }
+    }
+  n += (P.ns1 + P.nl1 > 0) + (P.ns2 + P.nl2 > 0);  // scatter passes
+  n += (P.npe > 0) + (P.npl > 0) + 1;              // u pieces (two launches) + y = S^-1 u
+  n += (P.nr1 > 0) + (P.nr2 > 0) + 1;              // two x passes + finalize
+  return n;
+}
+
 void enqueue_iteration(sdp_handle h, cudaStream_t s) {
+  if (h->pipe.on) {  // the pipelined iteration's kernels, in sequence (per-phase profile)
+    const Pipe& P = h->pipe;
+    phase(0, s);
+    pipe_gemv(h, s, 0, P.npe + P.npl);
+    phase(1, s);
+    launch_symv(SDP_FORM_PRIMAL, h->Sinv, h->m, P.gemv_part, P.npe + P.npl, h->b, h->rho, nullptr, h->y, h->done, s);
+    phase(2, s);
+    launch_gemvT_rows(SDP_FORM_PRIMAL, h->AT, h->ldm, h->m, P.nr1, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+                      P.gT_part, h->done, s, P.rows1);
+    launch_gemvT_rows(SDP_FORM_PRIMAL, h->AT, h->ldm, h->m, P.nr2, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+                      P.gT_part + P.nb_gT1, h->done, s, P.rows2);
+    phase(3, s);
+    pipe_projection(h, 0, s);
+    pipe_projection(h, 1, s);
+    phase(4, s);
+    pipe_scatter(h, 0, s);
+    pipe_scatter(h, 1, s);
+    phase(6, s);
+    enqueue_finalize(h, s, P.scat_part, P.nb_sc1 + P.nb_sc2, P.gT_part, P.nb_gT1 + P.nb_gT2);
+    phase(7, s);
+    return;
+  }
   if (h->form == SDP_FORM_PRIMAL) {
     enqueue_kkt(h, s);                       // x   (E:OptCondMinYPrimal)
     phase(3, s);
@@ -630,7 +976,9 @@ void enqueue_iteration(sdp_handle h, cudaStream_t s) {
   phase(7, s);
 }
 
+int pipe_launches_per_iter(sdp_handle h);
 int launches_per_iter(sdp_handle h) {
+  if (h->pipe.on) return pipe_launches_per_iter(h);
   int n = 0;
   for (int b = 0; b < B_NUM; ++b) {  // one launch per non-empty tier; 3 per chunk for the QL tiers
     if (!h->bcount[b]) continue;
@@ -661,6 +1009,16 @@ void rebuild_graph(sdp_handle h) {
     h->graph = nullptr;
   }
   if (!h->use_graph) return;
+  if (h->pipe.on) {
+    // direct launches by default: a pipelined iteration is ~1 ms of device work for ~15 launches,
+    // and the launches stream ahead of the device; measured 1123 it/s direct vs 1075 from the
+    // three graphs (cfg2).  SDP_PIPE_GRAPH=1 captures A, BA, B (per-node priorities).
+    h->pipe.destroy_graphs();
+    const char* pg = getenv("SDP_PIPE_GRAPH");
+    if (pg && *pg == '1')
+      for (int w = 0; w < 3; ++w) pipe_capture(h, w, &h->pipe.g[w], &h->pipe.x[w]);
+    return;
+  }
   SDP_CUDA_TRY(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
   enqueue_iteration(h, h->cap_stream);
   SDP_CUDA_TRY(cudaStreamEndCapture(h->cap_stream, &h->graph));
@@ -712,6 +1070,7 @@ void destroy_handle(sdp_handle h) {
   if (h->comm) nccl_comm_destroy(h->comm);
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   h->tiers.destroy();
+  h->pipe.destroy();
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   if (cur >= 0) cudaSetDevice(cur);
   delete h;
@@ -861,6 +1220,22 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     sp.local_coords.resize(N);
     std::iota(sp.local_coords.begin(), sp.local_coords.end(), 0);
     sp.owned.assign(N, 1);
+    // pipelined-iteration candidates (struct Pipe): coordinates touched only by the first half of
+    // the cliques first, then the shared ones, then those of the second half only (stable), so
+    // that every pass of the pipelined iteration is one contiguous coordinate range
+    const char* penv = getenv("SDP_PIPELINE");
+    if (!(penv && *penv == '0') && h->form == SDP_FORM_PRIMAL && N >= 65536 && p >= 8) {
+      int64_t p1 = 1;
+      while (p1 < p - 1 && off[p1] * 2 < off[p]) ++p1;
+      std::vector<uint8_t> cls(N, 0);
+      for (int64_t k = 0; k < p; ++k)
+        for (int64_t e = off[k]; e < off[k + 1]; ++e) cls[Gmap[e]] |= (k < p1) ? 1 : 2;
+      std::stable_sort(sp.local_coords.begin(), sp.local_coords.end(), [&](int32_t a, int32_t b) {
+        auto rank = [&](int32_t t) { return cls[t] == 1 ? 0 : cls[t] == 3 ? 1 : 2; };
+        return rank(a) < rank(b);
+      });
+      h->coord_perm = true;
+    }
   } else {
     sp = make_shard_plan(ksz, off, seg_ptr, seg_idx, h->world, h->rank);
   }
@@ -1123,6 +1498,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     h->vprev = al.zeros<double>((size_t)std::max<int64_t>(voff[pl], 1));
     h->vprev_len = voff[pl];
   }
+  build_pipeline(h, Gl, offl, segl_ptr, task_bucket);
   psd_init_attributes();
   SDP_CUDA_TRY(cudaDeviceSynchronize());
   reset_state(h);
@@ -1170,9 +1546,31 @@ void fill_info(sdp_handle h, sdp_info* info) {
   info->launches_per_iter = launches_per_iter(h);
   info->jacobi_sweeps = (int64_t)sw;
   info->rho = h->rho;
+  info->pipelined = h->pipe.on ? 1 : 0;
 }
 
 void launch_iterations(sdp_handle h, int32_t iters) {
+  if (h->pipe.on && iters > 0) {  // A (BA)^(iters-1) B
+    Pipe& P = h->pipe;
+    const bool gr = h->use_graph && P.x[0];
+    const char* tr = getenv("SDP_PIPE_TRACE");
+    for (int32_t i = 0; i <= iters; ++i) {
+      const int w = i == 0 ? 0 : (i == iters ? 2 : 1);
+      g_ptrace.on = tr && !gr && w == 1 && i == iters - 1;
+      if (gr) {
+        SDP_CUDA_TRY(cudaGraphLaunch(P.x[w], h->stream));
+      } else if (w == 0) {
+        pipe_enqueue_A(h, h->stream);
+      } else {
+        pipe_enqueue_B(h, h->stream, w == 1);
+      }
+    }
+    g_ptrace.on = tr != nullptr;
+    g_ptrace.dump();
+    g_ptrace.on = false;
+    SDP_CUDA_TRY(cudaGetLastError());
+    return;
+  }
   for (int32_t i = 0; i < iters; ++i) {
     if (h->exec)
       SDP_CUDA_TRY(cudaGraphLaunch(h->exec, h->stream));
@@ -1320,8 +1718,12 @@ int sdp_get_vector(sdp_handle h, int32_t which, double* out) {
     DeviceGuard dg(h->device);
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (which == SDP_VEC_X || which == SDP_VEC_XMAT) {
-      if (h->world == 1) {
+      if (h->world == 1 && !h->coord_perm) {
         SDP_CUDA_TRY(cudaMemcpy(out, h->x, h->N * sizeof(double), cudaMemcpyDeviceToHost));
+      } else if (h->world == 1) {  // local order = a permutation of the canonical one
+        std::vector<double> xl(h->Nl);
+        SDP_CUDA_TRY(cudaMemcpy(xl.data(), h->x, h->Nl * sizeof(double), cudaMemcpyDeviceToHost));
+        for (int64_t i = 0; i < h->Nl; ++i) out[h->local_coords[i]] = xl[i];
       } else {  // collective: owners contribute their coordinates
         std::vector<double> xl(h->Nl), own(h->Nl);
         SDP_CUDA_TRY(cudaMemcpy(xl.data(), h->x, h->Nl * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1491,6 +1893,7 @@ int sdp_save_state(sdp_handle h, void* host_out, int64_t capacity) {
     std::memcpy(&hd[12], &h->rho, 8);
     hd[13] = h->N;
     hd[14] = h->p;
+    hd[15] = h->coord_perm ? 1 : 0;  // coordinate layout of x, r1/D, sprev
     double* w = reinterpret_cast<double*>(hd + kStateHeader);
     auto get = [&](const double* dev, int64_t n) {
       if (n) SDP_CUDA_TRY(cudaMemcpy(w, dev, n * sizeof(double), cudaMemcpyDeviceToHost));
@@ -1521,6 +1924,8 @@ int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes) {
     if (hd[1] != h->form || hd[2] != h->world || hd[3] != h->rank || hd[4] != L.stot || hd[5] != L.lda ||
         hd[6] != L.m || hd[7] != L.vlen || hd[8] != L.hrows || hd[13] != h->N || hd[14] != h->p)
       throw Error{SDP_E_INVALID_ARG, "state blob is from a different problem, form or sharding"};
+    if (hd[15] != (h->coord_perm ? 1 : 0))
+      throw Error{SDP_E_INVALID_ARG, "state blob has a different coordinate layout (SDP_PIPELINE differs)"};
     if (bytes < 8 * L.words()) throw Error{SDP_E_INVALID_ARG, "state blob truncated"};
     const double* w = reinterpret_cast<const double*>(hd + kStateHeader);
     auto put = [&](double* dev, int64_t n) {

@@ -56,8 +56,9 @@ __global__ void __launch_bounds__(256) k_scatter(ScatterArgs a) {
   double acc[2] = {0.0, 0.0};
   const int nb_short = (a.N + 255) / 256;
   if ((int)blockIdx.x < nb_short) {
-    const int t = blockIdx.x * 256 + threadIdx.x;
-    if (t < a.N) {
+    const int tt = blockIdx.x * 256 + threadIdx.x;
+    const int t = (tt < a.N && a.list) ? a.list[tt] : tt;  // a subset of the coordinates (pipelined)
+    if (tt < a.N) {
       const int b = a.seg_ptr[t], e = a.seg_ptr[t + 1];
       if (e - b <= kLongSeg) {
         double sr = 0.0, sx = 0.0, sl = 0.0;
@@ -257,6 +258,7 @@ constexpr int TR_ROWS = 2;
 constexpr int TR_U = 16;
 template <int FORM>
 __global__ void __launch_bounds__(256) k_gemvT_rows(const double* __restrict__ AT, int64_t ldm, int m, int N,
+                                                     const int32_t* __restrict__ rows,
                                                      const double* __restrict__ y, const double* __restrict__ rD,
                                                      const double* __restrict__ Dinv, const double* __restrict__ c,
                                                      const double* __restrict__ own, double* __restrict__ x,
@@ -269,8 +271,9 @@ __global__ void __launch_bounds__(256) k_gemvT_rows(const double* __restrict__ A
   double acc[1] = {0.0};
 #pragma unroll
   for (int rr = 0; rr < TR_ROWS; ++rr) {
-    const int64_t t = ((int64_t)blockIdx.x * 8 + warp) * TR_ROWS + rr;
-    if (t >= N) break;
+    const int64_t tt = ((int64_t)blockIdx.x * 8 + warp) * TR_ROWS + rr;
+    if (tt >= N) break;
+    const int64_t t = rows ? rows[tt] : tt;  // a subset of the coordinates (pipelined iteration)
     const double2* row = reinterpret_cast<const double2*>(AT + t * ldm);
     double w0 = 0.0, w1 = 0.0;
     // predicated batches: every load of a batch is issued before any is consumed
@@ -582,12 +585,75 @@ __global__ void k_place_dense(const double* __restrict__ raw, int64_t npat, int 
 // ---------------------------------------------------------------- launchers
 void launch_scatter(int form, const ScatterArgs& a, cudaStream_t s) {
   const int grid = (a.N + 255) / 256 + (a.n_long + 7) / 8;
+  if (grid <= 0) return;
   if (form == 0)
     k_scatter<0><<<grid, 256, 0, s>>>(a);
   else
     k_scatter<1><<<grid, 256, 0, s>>>(a);
 }
 int scatter_blocks(int N, int n_long) { return (N + 255) / 256 + (n_long + 7) / 8; }
+
+// u partials over column pieces [pieces[2q], pieces[2q+1]) into part[(slot0 + q) * m ...]
+template <int RB>
+__global__ void __launch_bounds__(256) k_gemv_pieces(const double* __restrict__ A, int64_t lda, int m,
+                                                      const double* __restrict__ v,
+                                                      const int64_t* __restrict__ pieces, int slot0,
+                                                      double* __restrict__ part, const int* done) {
+  if (done && *done) return;
+  __shared__ double sm[RB * 8];
+  const int row0 = blockIdx.x * RB;
+  const int64_t c0 = pieces[2 * blockIdx.y], c1 = pieces[2 * blockIdx.y + 1];
+  double acc[RB];
+  const double* Ar[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) {
+    acc[r] = 0.0;
+    const int rr = (row0 + r < m) ? row0 + r : m - 1;
+    Ar[r] = A + (int64_t)rr * lda;
+  }
+  // scalar head / tail for odd ends, 16-byte evict-first loads in between
+  const int64_t e0 = (c0 + 1) & ~(int64_t)1, e1 = c1 & ~(int64_t)1;
+  if (threadIdx.x == 0 && (c0 & 1) && c0 < c1) {
+    const double vv = __ldg(v + c0);
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = fma(__ldcs(Ar[r] + c0), vv, acc[r]);
+  }
+  if (threadIdx.x == 1 && (c1 & 1) && e1 >= c0 && e1 < c1 && !(e1 == c0 && (c0 & 1))) {
+    const double vv = __ldg(v + e1);
+#pragma unroll
+    for (int r = 0; r < RB; ++r) acc[r] = fma(__ldcs(Ar[r] + e1), vv, acc[r]);
+  }
+  const double2* v2 = reinterpret_cast<const double2*>(v);
+#pragma unroll 4
+  for (int64_t t = e0 / 2 + threadIdx.x; t < e1 / 2; t += 256) {
+    const double2 vv = __ldg(v2 + t);
+#pragma unroll
+    for (int r = 0; r < RB; ++r) {
+      const double2 aa = __ldcs(reinterpret_cast<const double2*>(Ar[r]) + t);
+      acc[r] = fma(aa.x, vv.x, acc[r]);
+      acc[r] = fma(aa.y, vv.y, acc[r]);
+    }
+  }
+  block_sum<RB, 256>(acc, sm);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int r = 0; r < RB; ++r)
+      if (row0 + r < m) part[(int64_t)(slot0 + blockIdx.y) * m + row0 + r] = acc[r];
+  }
+}
+
+// the HBM-streaming kernels of the pipelined iteration (graph nodes that keep the default priority)
+bool is_stream_kernel(const void* fn) {
+  return fn == (const void*)k_gemv_pieces<4> || fn == (const void*)k_gemvT_rows<0> ||
+         fn == (const void*)k_gemvT_rows<1> || fn == (const void*)k_symv<0> || fn == (const void*)k_symv<1>;
+}
+
+void launch_gemv_pieces(const double* A, int64_t lda, int m, const double* v, const int64_t* pieces, int npieces,
+                        int slot0, double* part, const int* done, cudaStream_t s) {
+  if (npieces <= 0) return;
+  dim3 grid((m + 3) / 4, npieces);
+  k_gemv_pieces<4><<<grid, 256, 0, s>>>(A, lda, m, v, pieces, slot0, part, done);
+}
 
 void launch_gemv_dense(const double* A, int64_t lda, int m, const double* v, int chunk, double* part,
                        const int* done, cudaStream_t s) {
@@ -626,12 +692,13 @@ int gemvT_rows_blocks(int64_t N) { return (int)((N + 8 * TR_ROWS - 1) / (8 * TR_
 
 void launch_gemvT_rows(int form, const double* AT, int64_t ldm, int m, int N, const double* y, const double* rD,
                        const double* Dinv, const double* c, const double* own, double* x, double* part,
-                       const int* done, cudaStream_t s) {
+                       const int* done, cudaStream_t s, const int32_t* rows) {
+  if (N <= 0) return;
   const int grid = gemvT_rows_blocks(N);
   if (form == 0)
-    k_gemvT_rows<0><<<grid, 256, 0, s>>>(AT, ldm, m, N, y, rD, Dinv, c, own, x, part, done);
+    k_gemvT_rows<0><<<grid, 256, 0, s>>>(AT, ldm, m, N, rows, y, rD, Dinv, c, own, x, part, done);
   else
-    k_gemvT_rows<1><<<grid, 256, 0, s>>>(AT, ldm, m, N, y, rD, Dinv, c, own, x, part, done);
+    k_gemvT_rows<1><<<grid, 256, 0, s>>>(AT, ldm, m, N, rows, y, rD, Dinv, c, own, x, part, done);
 }
 
 void launch_transpose(const double* A, int64_t lda, int m, double* AT, int64_t ldm, int64_t ncols, cudaStream_t s) {

@@ -22,6 +22,7 @@ struct ScatterArgs {
   const int* done;
   const int32_t* shared_idx;  // per coordinate: slot in xbuf if shared across ranks, else -1 (NULL: none)
   double* xbuf;               // 3 doubles per shared coordinate: r1, sum H^T x_k, sum H^T lam_k partials
+  const int32_t* list = nullptr;  // short coordinates: list[0..N) instead of 0..N-1 (pipelined iteration)
 };
 
 struct FinalArgs {
@@ -60,9 +61,13 @@ void symv_init_attributes(int m);
 void launch_reduce_u(int form, const double* part, int nchunks, int m, const double* b, double rho, double* u,
                      const double* sdiag, double* y, const int* done, cudaStream_t s);
 int gemvT_rows_blocks(int64_t N);
+// rows != NULL: the N coordinates rows[0..N) instead of 0..N-1
 void launch_gemvT_rows(int form, const double* AT, int64_t ldm, int m, int N, const double* y, const double* rD,
                        const double* Dinv, const double* c, const double* own, double* x, double* part,
-                       const int* done, cudaStream_t s);
+                       const int* done, cudaStream_t s, const int32_t* rows = nullptr);
+bool is_stream_kernel(const void* fn);
+void launch_gemv_pieces(const double* A, int64_t lda, int m, const double* v, const int64_t* pieces, int npieces,
+                        int slot0, double* part, const int* done, cudaStream_t s);
 void launch_transpose(const double* A, int64_t lda, int m, double* AT, int64_t ldm, int64_t ncols, cudaStream_t s);
 void launch_gemv_csr(int form, const int32_t* rp, const int32_t* ci, const double* val, int m, const double* v,
                      const double* b, double rho, double* u, const double* sdiag, double* y, const int* done,
