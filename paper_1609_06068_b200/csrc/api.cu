@@ -116,6 +116,17 @@ void tri_inverse_T(const std::vector<double>& L, int m, std::vector<double>& Wt)
 
 using namespace sdp;
 
+// First clique of the second half of the pipelined iteration: the stacked-length fraction
+// SDP_PIPE_SPLIT (default 0.5) of the cliques goes to the first half.
+inline int64_t pipe_split(const std::vector<int64_t>& off, int64_t p) {
+  const char* e = getenv("SDP_PIPE_SPLIT");
+  double f = e ? atof(e) : 0.5;
+  if (!(f > 0.05 && f < 0.95)) f = 0.5;
+  int64_t p1 = 1;
+  while (p1 < p - 1 && (double)off[p1] < f * (double)off[p]) ++p1;
+  return p1;
+}
+
 // Side stream for the projection tiers: the giant tier (a chain of kernels whose tail leaves
 // most SMs idle) runs on the calling stream while every other tier runs concurrently on `side`
 // (fork / join by events, captured into the iteration graph as a branch).
@@ -674,8 +685,7 @@ void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vect
     return;
   Alloc& al = h->alloc;
   // halves by stacked length
-  int p1 = 1;
-  while (p1 < p - 1 && off[p1] * 2 < off[p]) ++p1;
+  const int p1 = (int)pipe_split(off, p);
   P.p1 = p1;
   std::vector<uint8_t> cls(N, 0);  // bit 0: touched by H1, bit 1: by H2
   for (int64_t k = 0; k < p; ++k)
@@ -1225,8 +1235,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     // that every pass of the pipelined iteration is one contiguous coordinate range
     const char* penv = getenv("SDP_PIPELINE");
     if (!(penv && *penv == '0') && h->form == SDP_FORM_PRIMAL && N >= 65536 && p >= 8) {
-      int64_t p1 = 1;
-      while (p1 < p - 1 && off[p1] * 2 < off[p]) ++p1;
+      const int64_t p1 = pipe_split(off, p);
       std::vector<uint8_t> cls(N, 0);
       for (int64_t k = 0; k < p; ++k)
         for (int64_t e = off[k]; e < off[k + 1]; ++e) cls[Gmap[e]] |= (k < p1) ? 1 : 2;
