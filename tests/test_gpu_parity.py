@@ -312,6 +312,65 @@ def test_cfg2_full_size_50_iterations(lib, gen, form):
     s.close()
 
 
+def test_cfg2_pipelined_path_checkpoint_and_layout(lib, gen, tmp_path):
+    """configs[2] primal runs the pipelined iteration: a checkpoint taken
+    between sdp_step calls resumes bit-identically, single steps and one multi-step call
+    give the same iterates, and a blob is rejected by a handle with the canonical coordinate
+    layout (SDP_PIPELINE=0)."""
+    import subprocess
+    import sys
+    prob = gen.config(2)
+    a = lib.Solver(prob, form="primal", rho=10.0)
+    assert a.info()["pipelined"] == 1
+    a.step(4)
+    blob = a.save_state()
+    a.step(3)
+    b = lib.Solver(prob, form="primal", rho=10.0)
+    b.load_state(blob)
+    for _ in range(3):
+        b.step(1)
+    assert np.array_equal(a.x(), b.x()) and np.array_equal(a.y(), b.y())
+    assert np.array_equal(a.blocks("xk"), b.blocks("xk"))
+    assert np.array_equal(a.blocks("lambda"), b.blocks("lambda"))
+    a.close()
+    b.close()
+    path = tmp_path / "state.bin"
+    path.write_bytes(bytes(blob))
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L, sdp_inputs as gen\n"
+        "s = L.Solver(gen.config(2), form='primal', rho=10.0)\n"
+        "assert s.info()['pipelined'] == 0\n"
+        "try:\n"
+        "    s.load_state(open(%r, 'rb').read())\n"
+        "except L.SdpError as e:\n"
+        "    print('rejected', e); sys.exit(0)\n"
+        "sys.exit(3)\n" % (ROOT, str(path)))
+    env = dict(os.environ, SDP_PIPELINE="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "rejected" in r.stdout, r.stdout + r.stderr
+
+
+def test_cfg2_unpipelined_subprocess():
+    """SDP_PIPELINE=0: the one-graph iteration on configs[2] still matches the oracle."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L, sdp_inputs as gen\n"
+        "from oracle import admm, decompose as dc\n"
+        "prob = gen.config(2); dec = dc.decompose(prob)\n"
+        "st = admm.step(dec, admm.zero_state(dec), 10.0, 'primal', 12)\n"
+        "s = L.Solver(prob, form='primal', rho=10.0); assert s.info()['pipelined'] == 0\n"
+        "s.step(12)\n"
+        "r = lambda g, o: np.linalg.norm(g - o) / np.linalg.norm(o)\n"
+        "e = max(r(s.x(), st.x), r(s.y(), st.y), r(s.blocks('xk'), st.xk), r(s.blocks('lambda'), st.lam))\n"
+        "print(e); assert e <= 1e-9, e\n" % ROOT)
+    env = dict(os.environ, SDP_PIPELINE="0")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 @pytest.mark.slow
 def test_cfg3_full_size_iterations(lib, gen):
     """BASELINE configs[3] (max-cut, n = 3000): giant cliques (GLOBAL tier) and a
