@@ -112,21 +112,36 @@ __global__ void __launch_bounds__(NWARP * 32) k_psd_wj32(ProjArgs a) {
   // ---- load (zero padded, mirrored; gather H_k x for the primal form)
   for (int e = lane; e < KP * KP; e += 32) sm.S[(e >> 5) * LDS + (e & 31)] = 0.0;
   __syncwarp();
-  for (int e = lane; e < ns; e += 32) {
-    int r, c;
-    packed_rc(e, r, c);
-    double v;
-    if constexpr (MODE == PM_BATCH) {
-      v = a.in[off + e];
-    } else if constexpr (MODE == PM_PRIMAL) {
-      v = __ldg(a.x + a.G[off + e]) - a.lam[off + e] / a.rho;
-      if (r != c) v *= kInvSqrt2;
+  // gathers batched: every lane's loads (index, then value) are issued before any is used
+  constexpr int NE = (KP * (KP + 1) / 2 + 31) / 32;  // packed entries per lane (17)
+  {
+    double v[NE];
+    if constexpr (MODE == PM_PRIMAL) {
+      int32_t gi[NE];
+#pragma unroll
+      for (int u = 0; u < NE; ++u) gi[u] = lane + 32 * u < ns ? __ldg(a.G + off + lane + 32 * u) : 0;
+#pragma unroll
+      for (int u = 0; u < NE; ++u) {
+        const int e = lane + 32 * u;
+        v[u] = e < ns ? __ldg(a.x + gi[u]) - a.lam[off + e] / a.rho : 0.0;
+      }
     } else {
-      v = a.vk[off + e] - a.lam[off + e] / a.rho;
-      if (r != c) v *= kInvSqrt2;
+#pragma unroll
+      for (int u = 0; u < NE; ++u) {
+        const int e = lane + 32 * u;
+        v[u] = e >= ns ? 0.0 : (MODE == PM_BATCH) ? a.in[off + e] : a.vk[off + e] - a.lam[off + e] / a.rho;
+      }
     }
-    sm.S[r * LDS + c] = v;
-    sm.S[c * LDS + r] = v;
+#pragma unroll
+    for (int u = 0; u < NE; ++u) {
+      const int e = lane + 32 * u;
+      if (e >= ns) continue;
+      int r, c;
+      packed_rc(e, r, c);
+      const double w = (MODE != PM_BATCH && r != c) ? v[u] * kInvSqrt2 : v[u];
+      sm.S[r * LDS + c] = w;
+      sm.S[c * LDS + r] = w;
+    }
   }
   __syncwarp();
   double av[KP], vv[KP];
@@ -196,23 +211,45 @@ __global__ void __launch_bounds__(NWARP * 32) k_psd_wj32(ProjArgs a) {
   store32(sm.W, acc, lane);
   __syncwarp();
   double p0 = 0.0, p1 = 0.0, p2 = 0.0;
-  for (int e = lane; e < ns; e += 32) {
-    int r, c;
-    packed_rc(e, r, c);
-    const double v = sm.W[r * LDS + c];
-    if constexpr (MODE == PM_BATCH) {
-      a.out[off + e] = v;
-    } else if constexpr (MODE == PM_PRIMAL) {
+  if constexpr (MODE == PM_PRIMAL) {
+    // H_k x and lambda_k gathered up front (batched), then x_k, the multiplier update and the
+    // residual partials
+    double hx[NE], lv[NE];
+    {
+      int32_t gi[NE];
+#pragma unroll
+      for (int u = 0; u < NE; ++u) gi[u] = lane + 32 * u < ns ? __ldg(a.G + off + lane + 32 * u) : 0;
+#pragma unroll
+      for (int u = 0; u < NE; ++u) {
+        const int e = lane + 32 * u;
+        hx[u] = e < ns ? __ldg(a.x + gi[u]) : 0.0;
+        lv[u] = e < ns ? a.lam[off + e] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NE; ++u) {
+      const int e = lane + 32 * u;
+      if (e >= ns) continue;
+      int r, c;
+      packed_rc(e, r, c);
+      const double v = sm.W[r * LDS + c];
       const double xkv = (r == c) ? v : v * kSqrt2;
-      const double hx = __ldg(a.x + a.G[off + e]);
-      const double d = xkv - hx;
+      const double d = xkv - hx[u];
       a.xk[off + e] = xkv;
-      a.lam[off + e] = a.lam[off + e] + a.rho * d;  // E:LambdakUpdate
+      a.lam[off + e] = lv[u] + a.rho * d;  // E:LambdakUpdate
       p0 += d * d;
       p1 += xkv * xkv;
-      p2 += hx * hx;
-    } else {
-      a.xk[off + e] = (r == c) ? v : v * kSqrt2;
+      p2 += hx[u] * hx[u];
+    }
+  } else {
+    for (int e = lane; e < ns; e += 32) {
+      int r, c;
+      packed_rc(e, r, c);
+      const double v = sm.W[r * LDS + c];
+      if constexpr (MODE == PM_BATCH)
+        a.out[off + e] = v;
+      else
+        a.xk[off + e] = (r == c) ? v : v * kSqrt2;
     }
   }
   if constexpr (MODE == PM_PRIMAL) {
