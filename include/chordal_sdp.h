@@ -140,7 +140,12 @@ void sdp_default_options(sdp_options* opt);
 int sdp_setup(const sdp_problem* prob, const sdp_options* opt, sdp_handle* out);
 
 /* Run exactly `iters` ADMM iterations from the current state, no stopping test.
- * Asynchronous on the handle's stream; returns after enqueueing. */
+ * Asynchronous on the handle's stream; returns after enqueueing.  When
+ * sdp_info.pipelined is 1 the iterations are issued as the pipelined schedule
+ * (projections of one half of the cliques overlap the A
+ * passes of the neighbouring iterations) on helper streams that fork from and
+ * join back into the handle's stream; every call still ends on an iteration
+ * boundary, so getters and checkpoints see the same state as without it. */
 int sdp_step(sdp_handle h, int32_t iters);
 
 /* Iterate until max(eps_p, eps_d) < tol (Algorithm 1/2 line 3) or until
