@@ -881,16 +881,22 @@ void pipe_enqueue_B(sdp_handle h, cudaStream_t s, bool with_A) {
   SDP_CUDA_TRY(cudaEventRecord(P.ev[5], P.sp2));
   SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp, P.ev[5], 0));
   pipe_scatter(h, 1, P.sp);
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[6], P.sp));
   enqueue_finalize(h, P.sp, P.scat_part, P.nb_sc1 + P.nb_sc2, P.gT_part, P.nb_gT1 + P.nb_gT2);
   g_ptrace.mark("finalize", P.sp);
   SDP_CUDA_TRY(cudaEventRecord(P.ev[4], P.sp));
-  SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[4], 0));
   if (with_A) {
-    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[3], 0));
+    // the rest of u needs the scatter only (finalize runs alongside); y = S^-1 u and the
+    // x-pass of the next iteration wait for finalize (its stop flag)
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[6], 0));
     pipe_gemv(h, s, P.npe, P.npl);
     g_ptrace.mark("gemv_late", s);
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[3], 0));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[4], 0));
     pipe_symv_gemvT1(h, s);
     g_ptrace.mark("symv+gemvT1", s);
+  } else {
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[4], 0));
   }
 }
 
