@@ -169,6 +169,11 @@ struct Pipe {
   int64_t* pieces = nullptr;                          // gemv column pieces: H1-only first, then the rest
   int npe = 0, npl = 0;
   double *gemv_part = nullptr, *gT_part = nullptr, *scat_part = nullptr;
+  // every sdp_step call ends with the next iteration's A already issued ("pending"): x on the
+  // H1-touched coordinates and y of the finished iteration are kept in x_save / y_save, and
+  // settle() puts them back before the state is read or changed through the API
+  bool pending = false;
+  double *x_save = nullptr, *y_save = nullptr;
   int nb_gT1 = 0, nb_gT2 = 0, nb_sc1 = 0, nb_sc2 = 0;
   BucketSet half[2];
   cudaStream_t sp = nullptr, sp2 = nullptr, sx = nullptr, sg = nullptr;  // projections (high priority), gemvT, gemv
@@ -735,6 +740,8 @@ void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vect
   P.nl1 = (int)lc1.size();
   P.nl2 = (int)lc2.size();
   P.gemv_part = al.zeros<double>((size_t)(P.npe + P.npl) * h->m);
+  P.x_save = al.zeros<double>((size_t)rows1.size());
+  P.y_save = al.zeros<double>((size_t)h->m);
   P.nb_gT1 = gemvT_rows_blocks(P.nr1);
   P.nb_gT2 = gemvT_rows_blocks(P.nr2);
   P.gT_part = al.zeros<double>((size_t)(P.nb_gT1 + P.nb_gT2));
@@ -893,6 +900,10 @@ void pipe_enqueue_B(sdp_handle h, cudaStream_t s, bool with_A) {
     g_ptrace.mark("gemv_late", s);
     SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[3], 0));
     SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[4], 0));
+    // the finished iteration's y and x on the coordinates the next x-pass overwrites (rows1 is
+    // the contiguous range [0, nr1) of the local order)
+    SDP_CUDA_TRY(cudaMemcpyAsync(P.y_save, h->y, (size_t)h->m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    SDP_CUDA_TRY(cudaMemcpyAsync(P.x_save, h->x, (size_t)P.nr1 * sizeof(double), cudaMemcpyDeviceToDevice, s));
     pipe_symv_gemvT1(h, s);
     g_ptrace.mark("symv+gemvT1", s);
   } else {
@@ -1565,21 +1576,22 @@ void fill_info(sdp_handle h, sdp_info* info) {
 }
 
 void launch_iterations(sdp_handle h, int32_t iters) {
-  if (h->pipe.on && iters > 0) {  // A (BA)^(iters-1) B
+  if (h->pipe.on && iters > 0) {  // [A] (BA)^iters: the next iteration's A is left issued (pending)
     Pipe& P = h->pipe;
     const bool gr = h->use_graph && P.x[0];
     const char* tr = getenv("SDP_PIPE_TRACE");
-    for (int32_t i = 0; i <= iters; ++i) {
-      const int w = i == 0 ? 0 : (i == iters ? 2 : 1);
-      g_ptrace.on = tr && !gr && w == 1 && i == iters - 1;
+    for (int32_t i = P.pending ? 1 : 0; i <= iters; ++i) {
+      const int w = i == 0 ? 0 : 1;
+      g_ptrace.on = tr && !gr && w == 1 && i == iters;
       if (gr) {
         SDP_CUDA_TRY(cudaGraphLaunch(P.x[w], h->stream));
       } else if (w == 0) {
         pipe_enqueue_A(h, h->stream);
       } else {
-        pipe_enqueue_B(h, h->stream, w == 1);
+        pipe_enqueue_B(h, h->stream, true);
       }
     }
+    P.pending = true;
     g_ptrace.on = tr != nullptr;
     g_ptrace.dump();
     g_ptrace.on = false;
@@ -1593,6 +1605,17 @@ void launch_iterations(sdp_handle h, int32_t iters) {
       enqueue_iteration(h, h->stream);
   }
   SDP_CUDA_TRY(cudaGetLastError());
+}
+
+// Put back the finished iteration's x (H1-touched coordinates) and y when the next iteration's A
+// is pending (see Pipe::pending); the next sdp_step then starts with A again.
+void settle(sdp_handle h) {
+  Pipe& P = h->pipe;
+  if (!P.on || !P.pending) return;
+  SDP_CUDA_TRY(cudaMemcpyAsync(h->y, P.y_save, (size_t)h->m * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  SDP_CUDA_TRY(cudaMemcpyAsync(h->x, P.x_save, (size_t)P.nr1 * sizeof(double), cudaMemcpyDeviceToDevice, h->stream));
+  SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+  P.pending = false;
 }
 
 }  // namespace
@@ -1641,6 +1664,7 @@ namespace {
 // kept unscaled).  The primal right-hand side r1 depends on rho and is rebuilt
 // from the current x_k, lambda_k (sprev is unchanged); the graph is recaptured.
 void apply_rho(sdp_handle h, double rho) {
+  settle(h);
   SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
   h->rho = rho;
   if (h->form == SDP_FORM_PRIMAL) {
@@ -1687,6 +1711,8 @@ int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info) {
         if (rho != h->rho) apply_rho(h, rho);
       }
     }
+    // a stop skips the pending next-iteration A: put the finished iteration's x / y back
+    settle(h);
     const double neg = -1.0;
     SDP_CUDA_TRY(cudaMemcpy(h->tol, &neg, sizeof(double), cudaMemcpyHostToDevice));
     SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
@@ -1700,6 +1726,7 @@ int sdp_reset(sdp_handle h) {
   return guarded([&] {
     if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
     DeviceGuard dg(h->device);
+    settle(h);
     reset_state(h);
     return SDP_OK;
   });
@@ -1731,6 +1758,7 @@ int sdp_get_vector(sdp_handle h, int32_t which, double* out) {
   return guarded([&] {
     if (!h || !out) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
     DeviceGuard dg(h->device);
+    settle(h);
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (which == SDP_VEC_X || which == SDP_VEC_XMAT) {
       if (h->world == 1 && !h->coord_perm) {
@@ -1817,6 +1845,7 @@ int sdp_profile_phases(sdp_handle h, int32_t iters, double* out_ms) {
   return guarded([&] {
     if (!h || !out_ms || iters <= 0) throw Error{SDP_E_INVALID_ARG, "bad argument"};
     DeviceGuard dg(h->device);
+    settle(h);
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
     SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
     std::vector<cudaEvent_t> ev(16 * (size_t)iters);
@@ -1883,6 +1912,7 @@ int sdp_save_state(sdp_handle h, void* host_out, int64_t capacity) {
   return guarded([&] {
     if (!h || !host_out) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
     DeviceGuard dg(h->device);
+    settle(h);
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
     long long it = 0;
     unsigned long long cap = 0, sw = 0;
@@ -1932,6 +1962,7 @@ int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes) {
   return guarded([&] {
     if (!h || !host_in) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
     DeviceGuard dg(h->device);
+    settle(h);
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
     const int64_t* hd = static_cast<const int64_t*>(host_in);
     if (bytes < 8 * kStateHeader || hd[0] != kStateMagic) throw Error{SDP_E_INVALID_ARG, "not an sdp state blob"};
