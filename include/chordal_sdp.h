@@ -144,8 +144,10 @@ int sdp_setup(const sdp_problem* prob, const sdp_options* opt, sdp_handle* out);
  * sdp_info.pipelined is 1 the iterations are issued as the pipelined schedule
  * (projections of one half of the cliques overlap the A
  * passes of the neighbouring iterations) on helper streams that fork from and
- * join back into the handle's stream; every call still ends on an iteration
- * boundary, so getters and checkpoints see the same state as without it. */
+ * join back into the handle's stream.  The call also leaves the first part of
+ * the next iteration issued; every getter, checkpoint, rho change and reset
+ * first restores the finished iteration's x and y, so the state seen through
+ * this API is always the iteration boundary. */
 int sdp_step(sdp_handle h, int32_t iters);
 
 /* Iterate until max(eps_p, eps_d) < tol (Algorithm 1/2 line 3) or until
