@@ -3,29 +3,29 @@
 // max-cut clique blocks that carry > 90 % of cfg3's projection flops.
 //
 // Block Jacobi (kernels_psd_giant.cu) executes ~12 k^3 flops per sweep and
-// needs several sweeps; this path executes ~4.5 k^3 (Golub & Van Loan 8.3):
-//   1. k_gtrd_tridiag (one 1024-thread CTA per matrix): Householder reduction
-//      A = Q T Q^T in the blocked form of LAPACK dsytrd / dlatrd (panels of 16
-//      columns: per column only the column update, the Householder vector and
-//      w = tau (A22 v - V W^T v - W V^T v) - (tau/2)(w.v) v; the trailing
-//      rank-32 update A22 -= V W^T + W V^T once per panel).  The matrix is the
-//      packed lower triangle in an L2-resident workspace, thread i owns row i,
-//      the panel's V and W live in shared memory.
-//   2. k_gtrd_eig (one CTA per matrix): inertia of T by a Sturm count at 0,
-//      the side of 0 with fewer eigenvalues, those eigenvalues by bisection
-//      (one thread each, Sturm counts with the LAPACK pivmin guard), clusters
-//      (gap <= 1e-3 ||T||) and inverse iteration as in LAPACK dstein (partial-
-//      pivoting tridiagonal LU, 2 solves, modified Gram-Schmidt in the cluster),
-//      residual-checked.
-//   3. k_gtrd_back (one CTA per 32 selected vectors): V = H_0 ... H_{k-3} Z,
-//      reflectors staged 16 at a time in shared memory, a warp per column with
-//      the column in registers.
-//   4. k_gtrd_recon (a warp per 32x32 tile): P_+ = [A] + sum_t w_t v_t v_t^T as
-//      DMMA (mma.sync m8n8k4 f64) products, mode epilogue, partials;
-//      k_gtrd_fin sums the partials per matrix in a fixed order.
-// A matrix whose inverse iteration fails its residual test (or with k > 800)
-// is marked status = -1 and redone by the block-Jacobi kernel in the same
-// projection call (GiantDev::only).  Eigenvalues are clipped at exactly 0.
+// needs several sweeps; this path executes ~4.5 k^3 (Golub & Van Loan 8.3),
+// the LAPACK dsytrd -> dstebz -> dstein -> dormtr pipeline re-designed for the GPU:
+//   1. k_gtrd_tridiag: blocked Householder reduction A = Q T Q^T (dsytrd / dlatrd,
+//      panels of TC_NB columns), full-storage matrix in an L2-resident workspace;
+//      orders >= SDP_GTRD_COOP_MIN are reduced by an 8-CTA thread-block cluster
+//      (column chunks dealt to the CTAs, A22 v exchanged through DSMEM), smaller
+//      ones one CTA each; tail: scaled T, Gershgorin bounds, exact inertia.
+//   2. k_gtrd_bisect: every eigenvalue of T by multisection (3 Sturm chains).
+//   3. k_gtrd_cluster: side of 0 to compute (fewer eigenvalues, or the side
+//      without oversize clusters), clusters (gap <= 1e-3 ||T||), cuts of clusters
+//      beyond a vector group at their largest gaps, vector-kernel groups.
+//   4. k_gtrd_vec: inverse iteration (dstein): a CTA per group, a thread per
+//      eigenvalue, LU factors in global memory, iterates in shared memory, MGS
+//      inside cluster pieces, Rayleigh-quotient weights, residual check.
+//   5. k_gtrd_wy + k_gtrd_back: V = H_0 ... H_{k-3} Z in compact-WY groups of 16
+//      reflectors, S = Y^T Z, U = T S, Z -= Y U as DMMA products.
+//   6. k_gtrd_recon + k_gtrd_fin: P_+ = [A] + sum_t w_t v_t v_t^T as DMMA
+//      (mma.sync m8n8k4 f64) products over 32x32 tiles with the mode epilogue;
+//      per-matrix partial sums in a fixed order.
+// A matrix whose vectors fail the residual test, whose clusters cannot be cut
+// safely, or with k > 800 is marked status = -1 and redone by the block-Jacobi
+// kernel in the same projection call (GiantDev::only).  Eigenvalues are
+// clipped at exactly 0.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
