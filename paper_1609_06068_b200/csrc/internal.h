@@ -73,10 +73,11 @@ int bucket_of(int k, int64_t count_in_range);
 // Projection modes
 enum ProjMode { PM_BATCH = 0, PM_PRIMAL = 1, PM_DUAL = 2 };
 
-// Tridiagonal path for the giant orders (kernels_psd_gtrd.cu): one CTA per
-// matrix, blocked Householder tridiagonalization of an L2-resident matrix, bisection + inverse iteration on the smaller side of the spectrum,
-// back-transform, DMMA reconstruction.  status[g] = -1 hands matrix g to the
-// block-Jacobi kernel (GiantDev::only).
+// Tridiagonal path for the giant orders (kernels_psd_gtrd.cu): blocked Householder
+// reduction of an L2-resident matrix (8-CTA clusters for the large orders),
+// multisection bisection, inverse iteration on one side of the spectrum, WY
+// back-transform and reconstruction as DMMA products.  status[g] = -1 hands
+// matrix g to the block-Jacobi kernel (GiantDev::only).
 struct GtrdDev {
   int ng = 0;
   int kmax = 0;
