@@ -166,6 +166,25 @@ int sdp_set_rho(sdp_handle h, double rho);
 /* Synchronise and report sizes, residuals and objective (host out). */
 int sdp_get_info(sdp_handle h, sdp_info* info);
 
+/* PSD completion of the current X (Theorem 1).
+ * X = smat(x) is known on the extended chordal pattern E' only; out (host, n*n
+ * doubles, row-major, written entirely) receives a completion that agrees with X
+ * on E' and fills every other entry by the perfect-elimination construction:
+ * vertices in reverse elimination order, X[v,u] = X[v,a] X[a,a]^+ X[a,u] with
+ * a = the later neighbours of v (a clique of E'); the pseudo-inverse drops
+ * eigenvalues below rtol * max|lambda| (take it near the solve accuracy, e.g.
+ * 1e-8: separator blocks of a converged X are singular to that accuracy).  When every
+ * maximal-clique block of X is PSD (a converged primal solve) the result is PSD
+ * (Grone); for definite blocks it is the maximum-determinant completion.  Host
+ * computation, O(n^2 * max clique) once per call; world == 1 or collective.
+ * Errors: SDP_E_INVALID_ARG. */
+int sdp_complete_x(sdp_handle h, double rtol, double* out);
+
+/* The elimination order of the chordal analysis (n vertices, host int32): a
+ * perfect elimination order of E' (exact minimum degree, ties to the lowest
+ * index; reading G13). */
+int sdp_get_elimination_order(sdp_handle h, int32_t* order);
+
 /* ---- getters: synchronise the stream, copy into host buffers ----------- */
 #define SDP_VEC_X 0        /* N: x (svec on the pattern, primal KKT x / dual KKT x)   */
 #define SDP_VEC_Y 1        /* m: KKT y                                               */

@@ -94,6 +94,8 @@ _sig = {
     "sdp_get_pattern": (_i32, [_vp, _vp, _vp]),
     "sdp_get_cliques": (_i32, [_vp, _vp, _vp]),
     "sdp_get_history": (_i32, [_vp, _vp, _i64, C.POINTER(_i64)]),
+    "sdp_complete_x": (_i32, [_vp, _d, _vp]),
+    "sdp_get_elimination_order": (_i32, [_vp, _vp]),
     "sdp_destroy": (_i32, [_vp]),
     "sdp_state_bytes": (_i32, [_vp, C.POINTER(_i64)]),
     "sdp_save_state": (_i32, [_vp, _vp, _i64]),
@@ -310,6 +312,19 @@ class Solver:
         for k in sizes:
             out.append(verts[e:e + k].copy())
             e += k
+        return out
+
+    def complete_x(self, rtol=1e-8):
+        """PSD completion of X = smat(x) off the chordal pattern (sdp_complete_x), n x n."""
+        n = self._info["n"]
+        out = np.empty((n, n))
+        _check(lib.sdp_complete_x(self.h, float(rtol), _ptr(out)))
+        return out
+
+    def elimination_order(self):
+        n = self._info["n"]
+        out = np.empty(n, dtype=np.int32)
+        _check(lib.sdp_get_elimination_order(self.h, _ptr(out)))
         return out
 
     def history(self, cap=1 << 20):

@@ -216,6 +216,7 @@ struct sdp_handle_s {
   int64_t fill_edges = 0;
   // host copies
   std::vector<int32_t> coord_row, coord_col, clique_size, clique_vert;
+  ChordalResult chordal;  // pattern analysis kept for the PSD completion (order, later neighbours, E')
   std::vector<int64_t> clique_off;
   int64_t kmin = 0, kmax = 0;
   // device buffers
@@ -1181,6 +1182,9 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->N = N;
   h->coord_row = cr.coord_row;
   h->coord_col = cr.coord_col;
+  h->chordal.order = cr.order;
+  h->chordal.later_ptr = cr.later_ptr;
+  h->chordal.later_idx = cr.later_idx;
   if (N >= (1ll << 31)) throw Error{SDP_E_INVALID_ARG, "pattern too large"};
 
   // ---- 2. global layout: clique offsets, H_k maps, D, inverse map
@@ -1785,6 +1789,34 @@ int sdp_get_vector(sdp_handle h, int32_t which, double* out) {
     } else {
       throw Error{SDP_E_INVALID_ARG, "unknown vector id"};
     }
+    return SDP_OK;
+  });
+}
+
+int sdp_get_elimination_order(sdp_handle h, int32_t* order) {
+  return guarded([&] {
+    if (!h || !order) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    std::memcpy(order, h->chordal.order.data(), h->n * sizeof(int32_t));
+    return SDP_OK;
+  });
+}
+
+int sdp_complete_x(sdp_handle h, double rtol, double* out) {
+  return guarded([&] {
+    if (!h || !out) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
+    if (!(rtol >= 0.0)) throw Error{SDP_E_INVALID_ARG, "rtol must be >= 0"};
+    const int32_t n = (int32_t)h->n;
+    std::vector<double> xm(h->N);
+    const int rc = sdp_get_vector(h, SDP_VEC_XMAT, xm.data());  // matrix entries, canonical order
+    if (rc != SDP_OK) return rc;
+    std::vector<uint8_t> known((size_t)n * n, 0);
+    for (int64_t i = 0; i < (int64_t)n * n; ++i) out[i] = 0.0;
+    for (int64_t t = 0; t < h->N; ++t) {
+      const int r = h->coord_row[t], c = h->coord_col[t];
+      out[(size_t)r * n + c] = out[(size_t)c * n + r] = xm[t];
+      known[(size_t)r * n + c] = known[(size_t)c * n + r] = 1;
+    }
+    complete_psd_host(n, h->chordal, known, rtol, out);
     return SDP_OK;
   });
 }

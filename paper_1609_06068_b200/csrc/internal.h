@@ -32,7 +32,14 @@ struct ChordalResult {
   std::vector<int32_t> coord_row, coord_col;
   std::vector<int64_t> col_ptr;  // coordinates of column j are [col_ptr[j], col_ptr[j+1])
   int64_t fill_edges = 0;
+  std::vector<int32_t> order;                 // elimination order (a perfect elimination order of E')
+  std::vector<int64_t> later_ptr;             // n + 1: later neighbours of v at [later_ptr[v], later_ptr[v+1])
+  std::vector<int32_t> later_idx;
 };
+// PSD completion (completion.cpp): X (n x n row-major, known entries set) completed in place on the
+// chordal pattern of cr (Theorem 1; see oracle/completion.py)
+void complete_psd_host(int32_t n, const ChordalResult& cr, const std::vector<uint8_t>& known, double rtol,
+                       double* X);
 // edges: off-diagonal upper pairs (i<j), may contain duplicates
 ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges);
 int64_t coord_index(const ChordalResult& cr, int32_t i, int32_t j);  // -1 if absent

@@ -88,6 +88,12 @@ ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, i
     }
   }
   ChordalResult cr;
+  cr.order.resize(n);
+  for (int v = 0; v < n; ++v) cr.order[pos[v]] = v;
+  cr.later_ptr.assign(n + 1, 0);
+  for (int v = 0; v < n; ++v) cr.later_ptr[v + 1] = cr.later_ptr[v] + (int64_t)later[v].size();
+  cr.later_idx.reserve(cr.later_ptr[n]);
+  for (int v = 0; v < n; ++v) cr.later_idx.insert(cr.later_idx.end(), later[v].begin(), later[v].end());
   // elimination tree: parent(v) = first-eliminated later neighbour
   std::vector<int32_t> parent(n, -1);
   for (int v = 0; v < n; ++v) {

@@ -399,6 +399,37 @@ def test_cfg3_clustered_spectra_20_iterations(lib, gen):
     s.close()
 
 
+@pytest.mark.parametrize("name", ["cfg0", "maxcut200", "theta5", "arrow_odd"])
+def test_psd_completion_matches_oracle(lib, gen, name):
+    """sdp_complete_x (Theorem 1) against oracle.completion on the same
+    elimination order: agreement on and off the pattern; after a primal solve the completion
+    is PSD to solver accuracy (Grone)."""
+    from oracle import chordal
+    from oracle import completion
+    prob = PROBLEMS[name](gen)
+    s = lib.Solver(prob, form="primal", rho=1.0)
+    s.solve(20000, 1e-7)
+    order_l = s.elimination_order()
+    adj = chordal.aggregate_adjacency(prob)
+    order, later, filled = chordal.minimum_degree_elimination(adj)
+    assert np.array_equal(order_l, np.asarray(order))
+    n = prob.n
+    known = filled | np.eye(n, dtype=bool)
+    r, c = s.pattern()
+    X = np.zeros((n, n))
+    xm = s.x_mat()
+    X[r, c] = xm
+    X[c, r] = xm
+    # the converged blocks are singular to solver accuracy: drop eigenvalues below 1e-8 max|lambda|
+    # on both sides (a kept eigenvalue at the noise level would amplify rounding by its inverse)
+    want = completion.complete_psd(X, known, order, later, rtol=1e-8)
+    got = s.complete_x(rtol=1e-8)
+    assert np.allclose(got[known], X[known], rtol=0, atol=0)
+    assert np.linalg.norm(got - want) <= 1e-9 * np.linalg.norm(want)
+    assert np.linalg.eigvalsh(got).min() >= -1e-5 * np.linalg.norm(got)
+    s.close()
+
+
 # ------------------------------------------------------------------ giant (block-Jacobi) tier
 
 def test_giant_tier_iterates_warm_restarts(lib, gen):

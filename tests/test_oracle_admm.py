@@ -10,7 +10,8 @@ import scipy.sparse
 from oracle import admm, chordal
 from oracle import decompose as dc
 from oracle.psd import project_psd
-from tests.helpers import golden, grone_completion
+from oracle import completion
+from tests.helpers import golden
 
 OBJ = {o["cite"].split(":")[0]: o["value"] for o in golden("spec_examples.json")["objectives"]}
 
@@ -146,7 +147,7 @@ def test_grone_and_agler(gen):
         known[dec.coord_col, dec.coord_row] = True
         adj = chordal.aggregate_adjacency(pr)
         order, later, filled = chordal.minimum_degree_elimination(adj)
-        M = grone_completion(X, known, order, later)
+        M = completion.complete_psd(X, known, order, later)
         assert np.allclose(M[known], X[known])
         assert np.linalg.eigvalsh(M).min() >= -1e-7 * np.linalg.norm(M)
         # Agler: Z from the multipliers (primal form: Z_k = lam_k)
