@@ -22,7 +22,7 @@ python bench.py --workload cfg3 --steps 3 --warmup 3 --no-cpu > "$OUT/plain_cfg3
 python bench.py --workload cfg4 --steps 2 --warmup 3 --no-cpu > "$OUT/plain_cfg4.json" 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv \
     --log-file "$OUT/launches_cfg4.csv" python bench.py --workload cfg4 --steps 2 --warmup 3 --no-cpu > "$OUT/ncu_l4.log" 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gemv_dense|k_gemvT_rows|k_psd_wj32" -s 6 -c 3 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gemv_pieces|k_gemv_dense|k_gemvT_rows|k_psd_wj32" -s 6 -c 4 \
   -o "$OUT/full_cfg2" python bench.py --steps 3 --warmup 3 --no-cpu > "$OUT/ncu_f2.log" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gtrd_tridiag|k_gtrd_vec|k_gtrd_back" -s 30 -c 3 \
   -o "$OUT/full_cfg3" python bench.py --workload cfg3 --steps 3 --warmup 3 --no-cpu > "$OUT/ncu_f3.log" 2>&1
