@@ -351,6 +351,30 @@ def test_cfg2_pipelined_path_checkpoint_and_layout(lib, gen, tmp_path):
     assert r.returncode == 0 and "rejected" in r.stdout, r.stdout + r.stderr
 
 
+def test_cfg2_pipelined_settle_between_calls(lib, gen):
+    """The next iteration's A is left issued at the end of every sdp_step call; reading the
+    state in between (getters put the finished iteration's x / y back) and then stepping on
+    gives exactly the iterates of an uninterrupted run, and the state read is the iteration
+    boundary (x, y of the same iteration as the residuals)."""
+    prob = gen.config(2)
+    a = lib.Solver(prob, form="primal", rho=10.0)
+    b = lib.Solver(prob, form="primal", rho=10.0)
+    a.step(6)
+    for _ in range(3):
+        b.step(2)
+        xb, yb = b.x(), b.y()          # settle between calls
+    assert b.info()["iters"] == 6
+    assert np.array_equal(a.x(), xb) and np.array_equal(a.y(), yb)
+    assert np.array_equal(a.blocks("lambda"), b.blocks("lambda"))
+    a.step(3)
+    b.step(1)
+    b.set_rho(10.0)                    # a rho change settles and rebuilds r1 (same rho: same state)
+    b.step(2)
+    assert np.array_equal(a.x(), b.x()) and np.array_equal(a.blocks("xk"), b.blocks("xk"))
+    a.close()
+    b.close()
+
+
 def test_cfg2_unpipelined_subprocess():
     """SDP_PIPELINE=0: the one-graph iteration on configs[2] still matches the oracle."""
     import subprocess
