@@ -174,6 +174,12 @@ struct Pipe {
   // settle() puts them back before the state is read or changed through the API
   bool pending = false;
   double *x_save = nullptr, *y_save = nullptr;
+  // dual form: scatter partials double-buffered by iteration parity (the next iteration's scatter
+  // runs before the current finalize), dual-update partials per half
+  int par = 0;
+  int64_t soff1 = 0;  // stacked offset of the first clique of H2
+  double *scat_part2 = nullptr, *upd_part = nullptr;
+  int nb_u1 = 0, nb_u2 = 0;
   int nb_gT1 = 0, nb_gT2 = 0, nb_sc1 = 0, nb_sc2 = 0;
   BucketSet half[2];
   cudaStream_t sp = nullptr, sp2 = nullptr, sx = nullptr, sg = nullptr;  // projections (high priority), gemvT, gemv
@@ -644,15 +650,16 @@ void enqueue_kkt(sdp_handle h, cudaStream_t s) {
 }
 
 void enqueue_finalize(sdp_handle h, cudaStream_t s, const double* scat_part = nullptr, int n_scat = 0,
-                      const double* gT_part = nullptr, int n_gT = 0) {
+                      const double* gT_part = nullptr, int n_gT = 0, const double* upd_part = nullptr,
+                      int n_upd = 0) {
   FinalArgs a{};
   a.proj_part = h->proj_part;
   a.n_proj = (int)h->pl;
   a.fix_part = h->fix_part;
   a.n_fix = h->world > 1 ? h->n_fix : 0;
   a.red = h->red;
-  a.upd_part = h->upd_part;
-  a.n_upd = h->nb_upd;
+  a.upd_part = upd_part ? upd_part : h->upd_part;
+  a.n_upd = upd_part ? n_upd : h->nb_upd;
   a.scat_part = scat_part ? scat_part : h->scat_part;
   a.n_scat = scat_part ? n_scat : h->nb_scat;
   a.gT_part = gT_part ? gT_part : h->gT_part;
@@ -687,7 +694,7 @@ void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vect
   const char* env = getenv("SDP_PIPELINE");
   if (env && *env == '0') return;
   const int64_t N = h->Nl, p = h->pl;
-  if (h->form != SDP_FORM_PRIMAL || !h->a_dense || h->world != 1 || h->bcount[B_GLOBAL] > 0 || N < 65536 || p < 8)
+  if (!h->a_dense || h->world != 1 || h->bcount[B_GLOBAL] > 0 || N < 65536 || p < 8)
     return;
   Alloc& al = h->alloc;
   // halves by stacked length
@@ -728,6 +735,7 @@ void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vect
   pieces.insert(pieces.end(), pl2.begin(), pl2.end());
   if (P.npe == 0 || P.npl == 0 || rows2.empty()) return;  // nothing to overlap
   P.pieces = al.upload(pieces);
+  P.soff1 = off[p1];
   P.rows1 = al.upload(rows1);
   P.rows2 = al.upload(rows2);
   P.nr1 = (int)rows1.size();
@@ -749,6 +757,12 @@ void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vect
   P.nb_sc1 = P.ns1 + P.nl1 > 0 ? scatter_blocks(P.ns1, P.nl1) : 0;
   P.nb_sc2 = P.ns2 + P.nl2 > 0 ? scatter_blocks(P.ns2, P.nl2) : 0;
   P.scat_part = al.zeros<double>(2 * (size_t)std::max(P.nb_sc1 + P.nb_sc2, 1));
+  if (h->form == SDP_FORM_DUAL) {
+    P.scat_part2 = al.zeros<double>(2 * (size_t)std::max(P.nb_sc1 + P.nb_sc2, 1));
+    P.nb_u1 = update_blocks(off[p1]);
+    P.nb_u2 = update_blocks(off[p] - off[p1]);
+    P.upd_part = al.zeros<double>(3 * (size_t)(P.nb_u1 + P.nb_u2));
+  }
   // the two halves keep the tiers of the full assignment (the warm-start layout depends on it)
   for (int hf = 0; hf < 2; ++hf) {
     std::vector<std::vector<int32_t>> lists(B_NUM);
@@ -781,8 +795,8 @@ void pipe_gemv(sdp_handle h, cudaStream_t s, int first, int count) {
 
 void pipe_symv_gemvT1(sdp_handle h, cudaStream_t s) {
   const Pipe& P = h->pipe;
-  launch_symv(SDP_FORM_PRIMAL, h->Sinv, h->m, P.gemv_part, P.npe + P.npl, h->b, h->rho, nullptr, h->y, h->done, s);
-  launch_gemvT_rows(SDP_FORM_PRIMAL, h->AT, h->ldm, h->m, P.nr1, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+  launch_symv(h->form, h->Sinv, h->m, P.gemv_part, P.npe + P.npl, h->b, h->rho, nullptr, h->y, h->done, s);
+  launch_gemvT_rows(h->form, h->AT, h->ldm, h->m, P.nr1, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
                     P.gT_part, h->done, s, P.rows1);
 }
 
@@ -805,7 +819,7 @@ void pipe_projection(sdp_handle h, int half, cudaStream_t s) {
   a.voff = h->voff;
   a.iter = h->iter;
   a.warm_period = h->warm_period;
-  launch_tiers(a, PM_PRIMAL, B.d_ids, B.bcount, B.td, TierFork{}, s);
+  launch_tiers(a, h->form == SDP_FORM_PRIMAL ? PM_PRIMAL : PM_DUAL, B.d_ids, B.bcount, B.td, TierFork{}, s);
 }
 
 void pipe_scatter(sdp_handle h, int pass, cudaStream_t s) {
@@ -824,9 +838,9 @@ void pipe_scatter(sdp_handle h, int pass, cudaStream_t s) {
   a.rho = h->rho;
   a.rD = h->rD;
   a.sprev = h->sprev;
-  a.part = P.scat_part + 2 * (pass ? P.nb_sc1 : 0);
+  a.part = (P.par ? P.scat_part2 : P.scat_part) + 2 * (pass ? P.nb_sc1 : 0);
   a.done = h->done;
-  launch_scatter(SDP_FORM_PRIMAL, a, s);
+  launch_scatter(h->form, a, s);
 }
 
 // SDP_PIPE_TRACE=1 with use_graph = 0: event timeline of the last launched B / BA (stderr)
@@ -867,7 +881,7 @@ void pipe_enqueue_B(sdp_handle h, cudaStream_t s, bool with_A) {
   SDP_CUDA_TRY(cudaStreamWaitEvent(P.sx, P.ev[0], 0));
   SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp, P.ev[0], 0));
   // x on the H2-only coordinates || P_+ of H1, scatter of the H1-only coordinates
-  launch_gemvT_rows(SDP_FORM_PRIMAL, h->AT, h->ldm, h->m, P.nr2, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+  launch_gemvT_rows(h->form, h->AT, h->ldm, h->m, P.nr2, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
                     P.gT_part + P.nb_gT1, h->done, P.sx, P.rows2);
   g_ptrace.mark("gemvT2", P.sx);
   SDP_CUDA_TRY(cudaEventRecord(P.ev[1], P.sx));
@@ -909,6 +923,80 @@ void pipe_enqueue_B(sdp_handle h, cudaStream_t s, bool with_A) {
     g_ptrace.mark("symv+gemvT1", s);
   } else {
     SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[4], 0));
+  }
+}
+
+// ---------------------------------------------------------------- pipelined dual iteration
+// Alg. 2 order per iteration: P_+ (z) -> scatter -> u, y, x -> dual update (v, lambda) -> finalize.
+// Prefix D_A: P_+ and scatter of the first iteration, u, y, x on the H1-touched coordinates.
+// D_BA(t -> t+1): x on the H2-only coordinates || [dual update of H1 (x is complete on its
+// coordinates), P_+ of H1 for t+1, scatter of the H1-only coordinates]; dual update of H2,
+// finalize(t), P_+ of H2 for t+1, the rest of the scatter; the u-pass over the H1-only columns runs
+// alongside P_+ of H2; then the rest of u, y, x on the H1-touched coordinates.  Suffix D_B: x on the
+// H2-only coordinates, dual updates, finalize.  The next iteration's P_+ runs before the current
+// finalize, so this schedule is used by sdp_step only (no stopping test); sdp_solve runs the
+// one-graph iteration.  Scatter partials alternate between two buffers (P.par).
+void pipe_dual_update_range(sdp_handle h, int half, cudaStream_t s) {
+  const Pipe& P = h->pipe;
+  const int64_t b = half ? P.soff1 : 0, e = half ? h->stotl : P.soff1;
+  launch_update_dual(e - b, h->G + b, h->x, h->xk + b, h->lam + b, h->vk + b, h->rho,
+                     P.upd_part + 3 * (half ? P.nb_u1 : 0), h->done, s);
+}
+
+void pipe_dual_finalize(sdp_handle h, int par, cudaStream_t s) {
+  const Pipe& P = h->pipe;
+  enqueue_finalize(h, s, par ? P.scat_part2 : P.scat_part, P.nb_sc1 + P.nb_sc2, P.gT_part, P.nb_gT1 + P.nb_gT2,
+                   P.upd_part, P.nb_u1 + P.nb_u2);
+}
+
+void pipe_dual_A(sdp_handle h, cudaStream_t s) {
+  Pipe& P = h->pipe;
+  P.par = 0;
+  pipe_projection(h, 0, s);
+  pipe_projection(h, 1, s);
+  pipe_scatter(h, 0, s);
+  pipe_scatter(h, 1, s);
+  pipe_gemv(h, s, 0, P.npe + P.npl);
+  pipe_symv_gemvT1(h, s);
+}
+
+void pipe_dual_B(sdp_handle h, cudaStream_t s, bool with_A) {
+  Pipe& P = h->pipe;
+  const int cur = P.par;  // scatter buffer of iteration t
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[0], s));
+  SDP_CUDA_TRY(cudaStreamWaitEvent(P.sx, P.ev[0], 0));
+  SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp, P.ev[0], 0));
+  launch_gemvT_rows(h->form, h->AT, h->ldm, h->m, P.nr2, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+                    P.gT_part + P.nb_gT1, h->done, P.sx, P.rows2);
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[1], P.sx));
+  pipe_dual_update_range(h, 0, P.sp);
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[2], P.sp));
+  if (with_A) {
+    P.par = cur ^ 1;  // iteration t+1 scatters into the other buffer
+    pipe_projection(h, 0, P.sp);
+    pipe_scatter(h, 0, P.sp);
+    SDP_CUDA_TRY(cudaEventRecord(P.ev[3], P.sp));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(P.sg, P.ev[3], 0));
+    pipe_gemv(h, P.sg, 0, P.npe);
+    SDP_CUDA_TRY(cudaEventRecord(P.ev[4], P.sg));
+  }
+  SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp2, P.ev[1], 0));
+  pipe_dual_update_range(h, 1, P.sp2);
+  SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp2, P.ev[2], 0));
+  pipe_dual_finalize(h, cur, P.sp2);
+  SDP_CUDA_TRY(cudaEventRecord(P.ev[5], P.sp2));
+  if (with_A) {
+    pipe_projection(h, 1, P.sp2);
+    SDP_CUDA_TRY(cudaStreamWaitEvent(P.sp2, P.ev[3], 0));  // shared coordinates need P_+ of H1 too
+    pipe_scatter(h, 1, P.sp2);
+    SDP_CUDA_TRY(cudaEventRecord(P.ev[6], P.sp2));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[6], 0));
+    pipe_gemv(h, s, P.npe, P.npl);
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[4], 0));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[5], 0));
+    pipe_symv_gemvT1(h, s);
+  } else {
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, P.ev[5], 0));
   }
 }
 
@@ -958,11 +1046,12 @@ int pipe_launches_per_iter(sdp_handle h) {
   n += (P.ns1 + P.nl1 > 0) + (P.ns2 + P.nl2 > 0);  // scatter passes
   n += (P.npe > 0) + (P.npl > 0) + 1;              // u pieces (two launches) + y = S^-1 u
   n += (P.nr1 > 0) + (P.nr2 > 0) + 1;              // two x passes + finalize
+  if (h->form == SDP_FORM_DUAL) n += 2;              // dual updates per half
   return n;
 }
 
 void enqueue_iteration(sdp_handle h, cudaStream_t s) {
-  if (h->pipe.on) {  // the pipelined iteration's kernels, in sequence (per-phase profile)
+  if (h->pipe.on && h->form == SDP_FORM_PRIMAL) {  // the pipelined kernels, in sequence (per-phase profile)
     const Pipe& P = h->pipe;
     phase(0, s);
     pipe_gemv(h, s, 0, P.npe + P.npl);
@@ -971,7 +1060,7 @@ void enqueue_iteration(sdp_handle h, cudaStream_t s) {
     phase(2, s);
     launch_gemvT_rows(SDP_FORM_PRIMAL, h->AT, h->ldm, h->m, P.nr1, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
                       P.gT_part, h->done, s, P.rows1);
-    launch_gemvT_rows(SDP_FORM_PRIMAL, h->AT, h->ldm, h->m, P.nr2, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
+    launch_gemvT_rows(h->form, h->AT, h->ldm, h->m, P.nr2, h->y, h->rD, h->Dinv, h->c, h->own, h->x,
                       P.gT_part + P.nb_gT1, h->done, s, P.rows2);
     phase(3, s);
     pipe_projection(h, 0, s);
@@ -1037,7 +1126,7 @@ void rebuild_graph(sdp_handle h) {
     h->graph = nullptr;
   }
   if (!h->use_graph) return;
-  if (h->pipe.on) {
+  if (h->pipe.on && h->form == SDP_FORM_PRIMAL) {
     // direct launches by default: a pipelined iteration is ~1 ms of device work for ~15 launches,
     // and the launches stream ahead of the device; measured 1123 it/s direct vs 1075 from the
     // three graphs (cfg2).  SDP_PIPE_GRAPH=1 captures A, BA, B (per-node priorities).
@@ -1255,7 +1344,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     // the cliques first, then the shared ones, then those of the second half only (stable), so
     // that every pass of the pipelined iteration is one contiguous coordinate range
     const char* penv = getenv("SDP_PIPELINE");
-    if (!(penv && *penv == '0') && h->form == SDP_FORM_PRIMAL && N >= 65536 && p >= 8) {
+    if (!(penv && *penv == '0') && N >= 65536 && p >= 8) {
       const int64_t p1 = pipe_split(off, p);
       std::vector<uint8_t> cls(N, 0);
       for (int64_t k = 0; k < p; ++k)
@@ -1579,8 +1668,20 @@ void fill_info(sdp_handle h, sdp_info* info) {
   info->pipelined = h->pipe.on ? 1 : 0;
 }
 
-void launch_iterations(sdp_handle h, int32_t iters) {
-  if (h->pipe.on && iters > 0) {  // [A] (BA)^iters: the next iteration's A is left issued (pending)
+void launch_iterations(sdp_handle h, int32_t iters, bool for_solve = false) {
+  // dual: the pipelined schedule pays off from two iterations per call on (D_A + D_B alone has no
+  // overlap); a single iteration runs the one-graph iteration
+  if (h->pipe.on && h->form == SDP_FORM_DUAL && !for_solve && iters > 1) {  // D_A (D_BA)^(iters-1) D_B
+    for (int32_t i = 0; i <= iters; ++i) {
+      if (i == 0)
+        pipe_dual_A(h, h->stream);
+      else
+        pipe_dual_B(h, h->stream, i < iters);
+    }
+    SDP_CUDA_TRY(cudaGetLastError());
+    return;
+  }
+  if (h->pipe.on && h->form == SDP_FORM_PRIMAL && iters > 0) {  // [A] (BA)^iters, next A left issued
     Pipe& P = h->pipe;
     const bool gr = h->use_graph && P.x[0];
     const char* tr = getenv("SDP_PIPE_TRACE");
@@ -1697,7 +1798,7 @@ int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info) {
     while (it < max_iters) {
       // chunks end on multiples of check_every (the adaptation points of adapt_rho)
       const int chunk = (int)std::min<long long>(h->check_every - it % h->check_every, max_iters - it);
-      launch_iterations(h, chunk);
+      launch_iterations(h, chunk, true);
       SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
       SDP_CUDA_TRY(cudaMemcpy(&done, h->done, sizeof(int), cudaMemcpyDeviceToHost));
       SDP_CUDA_TRY(cudaMemcpy(&num, h->numerical, sizeof(int), cudaMemcpyDeviceToHost));
