@@ -375,6 +375,28 @@ def test_cfg2_pipelined_settle_between_calls(lib, gen):
     b.close()
 
 
+def test_cfg2_dual_pipelined_call_patterns(lib, gen):
+    """Dual form on configs[2]: sdp_step(4) and two sdp_step(2) calls (pipelined schedule) give
+    bit-identical iterates; single-step calls (one-graph iteration) agree to rounding."""
+    prob = gen.config(2)
+    a = lib.Solver(prob, form="dual", rho=0.1)
+    b = lib.Solver(prob, form="dual", rho=0.1)
+    c = lib.Solver(prob, form="dual", rho=0.1)
+    assert a.info()["pipelined"] == 1
+    a.step(4)
+    b.step(2)
+    b.step(2)
+    for _ in range(4):
+        c.step(1)
+    for fam in ("xk", "lambda", "vk"):
+        assert np.array_equal(a.blocks(fam), b.blocks(fam)), fam
+        assert rel(c.blocks(fam), a.blocks(fam)) <= 1e-12, fam
+    assert np.array_equal(a.x(), b.x()) and np.array_equal(a.y(), b.y())
+    assert np.array_equal(a.history(), b.history())
+    for s_ in (a, b, c):
+        s_.close()
+
+
 def test_cfg2_unpipelined_subprocess():
     """SDP_PIPELINE=0: the one-graph iteration on configs[2] still matches the oracle."""
     import subprocess
