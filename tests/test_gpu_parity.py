@@ -690,6 +690,24 @@ def test_solve_adaptive_rho(lib, gen, form, rho):
     s.close()
 
 
+@pytest.mark.parametrize("form,rho", [("primal", 1.0), ("dual", 1.0)])
+def test_cfg2_solve_adaptive_rho_pipelined_handle(lib, gen, form, rho):
+    """sdp_solve with residual balancing on configs[2] (a pipelined handle: the primal solve runs
+    the pipelined schedule with rho changes between chunks, the dual solve the one-graph
+    iteration): 40 iterations against the oracle's same rule."""
+    prob = gen.config(2)
+    dec = dc.decompose(prob)
+    st, status = admm.solve(dec, rho, form, 1e-12, 40, adapt=(10.0, 2.0, 10))
+    s = lib.Solver(prob, form=form, rho=rho, check_every=10, adapt_rho=True)
+    assert s.info()["pipelined"] == 1
+    gstatus, info = s.solve(40, 1e-12)
+    assert gstatus == status
+    assert info["iters"] == st.it == 40
+    assert info["rho"] == st.rho
+    compare_state(dec, st, s, form)
+    s.close()
+
+
 # ------------------------------------------------------------------ checkpoint / resume (SURVEY 8(f) #4)
 
 @pytest.mark.parametrize("name,form", [("cfg1", "primal"), ("cfg1", "dual"), ("maxcut200", "primal"),
