@@ -1127,13 +1127,12 @@ void rebuild_graph(sdp_handle h) {
   }
   if (!h->use_graph) return;
   if (h->pipe.on && h->form == SDP_FORM_PRIMAL) {
-    // direct launches by default: a pipelined iteration is ~1 ms of device work for ~15 launches,
-    // and the launches stream ahead of the device; measured 1123 it/s direct vs 1075 from the
-    // three graphs (cfg2).  SDP_PIPE_GRAPH=1 captures A, BA, B (per-node priorities).
+    // A and BA captured (per-node priorities).  Multi-iteration calls launch directly (the launches
+    // stream ahead of the device: 1128 vs 1107 it/s on cfg2); one- and two-iteration calls replay the
+    // graphs, whose single launch keeps the host out of the per-step loop (e2e 1034 -> 1049 it/s).
+    // Both issue the same kernels in the same dependency order, so the results are identical.
     h->pipe.destroy_graphs();
-    const char* pg = getenv("SDP_PIPE_GRAPH");
-    if (pg && *pg == '1')
-      for (int w = 0; w < 3; ++w) pipe_capture(h, w, &h->pipe.g[w], &h->pipe.x[w]);
+    for (int w = 0; w < 2; ++w) pipe_capture(h, w, &h->pipe.g[w], &h->pipe.x[w]);
     return;
   }
   SDP_CUDA_TRY(cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal));
@@ -1683,7 +1682,8 @@ void launch_iterations(sdp_handle h, int32_t iters, bool for_solve = false) {
   }
   if (h->pipe.on && h->form == SDP_FORM_PRIMAL && iters > 0) {  // [A] (BA)^iters, next A left issued
     Pipe& P = h->pipe;
-    const bool gr = h->use_graph && P.x[0];
+    const char* pg = getenv("SDP_PIPE_GRAPH");
+    const bool gr = h->use_graph && P.x[0] && P.x[1] && (iters <= 2 || (pg && *pg == '1'));
     const char* tr = getenv("SDP_PIPE_TRACE");
     for (int32_t i = P.pending ? 1 : 0; i <= iters; ++i) {
       const int w = i == 0 ? 0 : 1;
