@@ -292,9 +292,27 @@ struct sdp_psd_plan_s {
   unsigned long long* capped = nullptr;
   unsigned long long* sweeps = nullptr;
   double *h_in_dev = nullptr, *h_out_dev = nullptr;
+  // host-buffer path: two pinned staging chunks; the host side of each chunk is copied by all host
+  // threads while the DMA of the other chunk is in flight
+  double* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  void free_stage() {
+    for (int b = 0; b < 2; ++b) {
+      if (stage[b]) cudaFreeHost(stage[b]);
+      if (stage_ev[b]) cudaEventDestroy(stage_ev[b]);
+      stage[b] = nullptr;
+      stage_ev[b] = nullptr;
+    }
+  }
 };
 
 namespace {
+constexpr int64_t kStageDoubles = 8 << 20;  // 64 MB per staging chunk
+
+void host_copy_parallel(double* dst, const double* src, int64_t n) {
+#pragma omp parallel for schedule(static)
+  for (int64_t b = 0; b < n; b += 65536) std::memcpy(dst + b, src + b, std::min<int64_t>(65536, n - b) * sizeof(double));
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -2241,10 +2259,40 @@ int sdp_project_psd_batch_host(sdp_psd_plan pl, const double* h_in, double* h_ou
       pl->h_in_dev = pl->alloc.get<double>(pl->values);
       pl->h_out_dev = pl->alloc.get<double>(pl->values);
     }
-    SDP_CUDA_TRY(cudaMemcpyAsync(pl->h_in_dev, h_in, pl->values * sizeof(double), cudaMemcpyHostToDevice, s));
+    if (!pl->stage[0]) {
+      for (int b = 0; b < 2; ++b) {
+        SDP_CUDA_TRY(cudaHostAlloc(&pl->stage[b], kStageDoubles * sizeof(double), cudaHostAllocDefault));
+        SDP_CUDA_TRY(cudaEventCreateWithFlags(&pl->stage_ev[b], cudaEventDisableTiming));
+      }
+    }
+    const int64_t nv = pl->values;
+    // H2D: host -> pinned chunk (all host threads) -> async DMA, two chunks in flight
+    for (int64_t c0 = 0, it = 0; c0 < nv; c0 += kStageDoubles, ++it) {
+      const int b = (int)(it & 1);
+      const int64_t n = std::min<int64_t>(kStageDoubles, nv - c0);
+      if (it >= 2) SDP_CUDA_TRY(cudaEventSynchronize(pl->stage_ev[b]));
+      host_copy_parallel(pl->stage[b], h_in + c0, n);
+      SDP_CUDA_TRY(cudaMemcpyAsync(pl->h_in_dev + c0, pl->stage[b], n * sizeof(double), cudaMemcpyHostToDevice, s));
+      SDP_CUDA_TRY(cudaEventRecord(pl->stage_ev[b], s));
+    }
     int rc = sdp_project_psd_batch(pl, pl->h_in_dev, pl->h_out_dev, stream);
     if (rc != SDP_OK) return rc;
-    SDP_CUDA_TRY(cudaMemcpyAsync(h_out, pl->h_out_dev, pl->values * sizeof(double), cudaMemcpyDeviceToHost, s));
+    // D2H: async DMA into a pinned chunk, then pinned -> host while the next chunk's DMA runs
+    const int64_t nch = (nv + kStageDoubles - 1) / kStageDoubles;
+    auto issue = [&](int64_t it) {
+      const int b = (int)(it & 1);
+      const int64_t c0 = it * kStageDoubles, n = std::min<int64_t>(kStageDoubles, nv - c0);
+      SDP_CUDA_TRY(cudaMemcpyAsync(pl->stage[b], pl->h_out_dev + c0, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+      SDP_CUDA_TRY(cudaEventRecord(pl->stage_ev[b], s));
+    };
+    if (nch > 0) issue(0);
+    for (int64_t it = 0; it < nch; ++it) {
+      if (it + 1 < nch) issue(it + 1);
+      const int b = (int)(it & 1);
+      const int64_t c0 = it * kStageDoubles, n = std::min<int64_t>(kStageDoubles, nv - c0);
+      SDP_CUDA_TRY(cudaEventSynchronize(pl->stage_ev[b]));
+      host_copy_parallel(h_out + c0, pl->stage[b], n);
+    }
     SDP_CUDA_TRY(cudaStreamSynchronize(s));
     return SDP_OK;
   });
@@ -2276,6 +2324,7 @@ int sdp_psd_plan_destroy(sdp_psd_plan pl) {
     cudaDeviceSynchronize();
     pl->alloc.free_all();
     pl->tiers.destroy();
+    pl->free_stage();
     if (cur >= 0) cudaSetDevice(cur);
     delete pl;
     return SDP_OK;
