@@ -178,22 +178,32 @@ __global__ void __launch_bounds__(SYMV_T) k_symv(const double* __restrict__ Si, 
                                                   const int* done) {
   if (done && *done) return;
   extern __shared__ double us[];
-  for (int j = threadIdx.x; j < m; j += SYMV_T) {
-    double v = 0.0;
+  // u = sum of the GEMV partials (chunk order) - r2: four entries per thread per round, all of
+  // their partial loads in flight together
+  for (int j0 = threadIdx.x; j0 < m; j0 += 4 * SYMV_T) {
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
     if (part) {
-      // 8 independent loads in flight, summed in chunk order
       for (int c0 = 0; c0 < nchunks; c0 += 8) {
-        double t[8];
+        double t[4][8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) t[q] = (c0 + q < nchunks) ? part[(int64_t)(c0 + q) * m + j] : 0.0;
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v += t[q];
+          for (int q = 0; q < 8; ++q) {
+            const int j = j0 + r * SYMV_T;
+            t[r][q] = (j < m && c0 + q < nchunks) ? part[(int64_t)(c0 + q) * m + j] : 0.0;
+          }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) v[r] += t[r][q];
       }
-      v = (FORM == 0) ? v - b[j] : v + b[j] / rho;
-    } else {
-      v = u[j];
     }
-    us[j] = v;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int j = j0 + r * SYMV_T;
+      if (j >= m) continue;
+      us[j] = part ? ((FORM == 0) ? v[r] - b[j] : v[r] + b[j] / rho) : u[j];
+    }
   }
   __syncthreads();
   const int row = blockIdx.x * (SYMV_T / 32) + (threadIdx.x >> 5);
@@ -204,22 +214,16 @@ __global__ void __launch_bounds__(SYMV_T) k_symv(const double* __restrict__ Si, 
   if ((m & 1) == 0) {
     const double2* S2 = reinterpret_cast<const double2*>(Sr);
     const int h = m / 2;
-    int j = lane;
-    for (; j + 7 * 32 < h; j += 8 * 32) {
+    for (int j = lane; j < h; j += 8 * 32) {  // 8 loads in flight per lane (the last batch masked)
       double2 a[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) a[q] = __ldcs(S2 + j + 32 * q);
+      for (int q = 0; q < 8; ++q) a[q] = (j + 32 * q < h) ? __ldcs(S2 + j + 32 * q) : make_double2(0.0, 0.0);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const int c = 2 * (j + 32 * q);
+        const int c = 2 * min(j + 32 * q, h - 1);
         s[q] = fma(a[q].x, us[c], s[q]);
         s[q] = fma(a[q].y, us[c + 1], s[q]);
       }
-    }
-    for (; j < h; j += 32) {
-      const double2 a0 = __ldcs(S2 + j);
-      s[0] = fma(a0.x, us[2 * j], s[0]);
-      s[0] = fma(a0.y, us[2 * j + 1], s[0]);
     }
   } else {
     for (int j = lane; j < m; j += 32) s[0] = fma(Sr[j], us[j], s[0]);
