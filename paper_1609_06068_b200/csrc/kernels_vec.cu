@@ -411,28 +411,32 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs a) {
   double v[6] = {0, 0, 0, 0, 0, 0};
   double w[1] = {0.0};
   if (PHASE != 2) {
-    if (FORM == 0) {
-      for (int i = threadIdx.x; i < a.n_proj; i += 256) {
-        v[0] += a.proj_part[3 * i + 0];
-        v[1] += a.proj_part[3 * i + 1];
-        v[2] += a.proj_part[3 * i + 2];
+    // partials in rounds of 4 per thread and array, all loads of a round in flight together
+    // (the per-thread summation order is fixed, so the result is deterministic)
+    auto gather = [&](const double* src, int n, int comps, int v0) {
+      for (int i0 = threadIdx.x; i0 < n; i0 += 4 * 256) {
+        double t[4][3];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const int i = i0 + r * 256;
+            t[r][q] = (q < comps && i < n) ? src[(int64_t)comps * i + q] : 0.0;
+          }
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int q = 0; q < 3; ++q)
+            if (q < comps) v[v0 + q] += t[r][q];
       }
-    } else {
-      for (int i = threadIdx.x; i < a.n_upd; i += 256) {
-        v[0] += a.upd_part[3 * i + 0];
-        v[1] += a.upd_part[3 * i + 1];
-        v[2] += a.upd_part[3 * i + 2];
-      }
-    }
-    for (int i = threadIdx.x; i < a.n_scat; i += 256) {
-      v[3] += a.scat_part[2 * i + 0];
-      v[4] += a.scat_part[2 * i + 1];
-    }
-    for (int i = threadIdx.x; i < a.n_fix; i += 256) {
-      v[3] += a.fix_part[2 * i + 0];
-      v[4] += a.fix_part[2 * i + 1];
-    }
-    for (int i = threadIdx.x; i < a.n_gT; i += 256) v[5] += a.gT_part[i];
+    };
+    if (FORM == 0)
+      gather(a.proj_part, a.n_proj, 3, 0);
+    else
+      gather(a.upd_part, a.n_upd, 3, 0);
+    gather(a.scat_part, a.n_scat, 2, 3);
+    if (a.n_fix) gather(a.fix_part, a.n_fix, 2, 3);
+    gather(a.gT_part, a.n_gT, 1, 5);
     block_sum<6, 256>(v, sm);
     __syncthreads();
     if (PHASE == 1) {
