@@ -397,6 +397,20 @@ def test_cfg2_dual_pipelined_call_patterns(lib, gen):
         s_.close()
 
 
+@pytest.mark.parametrize("form,rho", [("primal", 10.0), ("dual", 0.1)])
+def test_pipelined_odd_block_arrow(lib, gen, form, rho):
+    """A second pipelined instance with odd sizes (330 blocks of 19, arrow width 7, m = 900):
+    uneven clique halves and coordinate classes; 12 iterations against the oracle."""
+    prob = gen.block_arrow(330, 19, 7, 900, seed=3)
+    dec = dc.decompose(prob)
+    st = admm.step(dec, admm.zero_state(dec), rho, form, 12)
+    s = lib.Solver(prob, form=form, rho=rho)
+    assert s.info()["pipelined"] == 1
+    s.step(12)
+    compare_state(dec, st, s, form)
+    s.close()
+
+
 def test_cfg2_unpipelined_subprocess():
     """SDP_PIPELINE=0: the one-graph iteration on configs[2] still matches the oracle."""
     import subprocess
