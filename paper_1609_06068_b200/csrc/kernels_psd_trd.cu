@@ -26,6 +26,7 @@
 // exactly 0 (G15).
 #include <cmath>
 #include <cstdlib>
+#include <utility>
 
 #include "internal.h"
 
@@ -216,6 +217,155 @@ __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int 
   }
 }
 
+// ---- 1'. register-resident tridiagonalization (default; SDP_TRD_REG=0 selects the one above)
+// Thread i holds the whole row i of A in registers (KP doubles), so the symmetric
+// product A22 v and the rank-2 update read only the broadcast vectors v, w from shared
+// memory (one LDS.128 per 2 columns) instead of one shared-memory element per FMA: the
+// shared-memory-bound loops above become FP64-issue-bound.  Full rows cost twice the
+// flops of the packed triangle (both triangles are updated), in exchange for no
+// per-element shared traffic.  Register indices must be compile-time constants, so the
+// column loop is split into KP/8 unrolled blocks of 8 steps (block JB works on columns
+// >= 8 JB; the few columns <= j inside the block see v = w = 0 and stay unchanged).
+// Same reflectors (dlarfg), same outputs (d, e, tau, packed v) as the kernel above.
+template <int KP>
+struct RegLayout {
+  static constexpr int NMAT = 128 / KP;
+  static constexpr int TRI = KP * (KP + 1) / 2;
+  static constexpr int PER = ((TRI + 1) & ~1) + 3 * KP + 4;  // staging (packed), xs, vs, ws, red
+};
+
+template <int KP, int JB>
+__device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const Grp<KP>& g, double* xs, double* vs,
+                                          double* ws, const HView<KP>& H, int64_t& vpos) {
+  constexpr int L0 = 8 * JB;
+  constexpr int UNR = KP <= 32 ? 8 : 1;  // KP = 32: steps unrolled too (all register indices static)
+#pragma unroll UNR
+  for (int j = L0; j < L0 + 8; ++j) {
+    if (j + 2 >= k) break;
+    double xi = A[L0];  // A(i, j), j dynamic inside the block
+#pragma unroll
+    for (int s = 1; s < 8; ++s)
+      if (j == L0 + s) xi = A[L0 + s];
+    const bool below = i >= j + 2 && i < k;
+    if (i == j) H.d()[j] = xi;  // row j is final: d_j = A(j, j)
+    double alpha;
+    if constexpr (KP <= 32) {
+      alpha = __shfl_sync(0xffffffffu, xi, j + 1);
+    } else {
+      xs[i] = xi;  // published by the barriers inside g.sum
+    }
+    const double sig = g.sum(below ? xi * xi : 0.0);
+    if constexpr (KP > 32) alpha = xs[j + 1];
+    double tau = 0.0, beta = alpha, scl = 0.0;
+    if (sig > 0.0) {
+      const double nrm = sqrt(fma(alpha, alpha, sig));
+      beta = alpha >= 0.0 ? -nrm : nrm;
+      tau = (beta - alpha) / beta;
+      scl = 1.0 / (alpha - beta);
+    }
+    const bool in = i >= j + 1 && i < k;
+    const double vi = in ? ((i == j + 1) ? 1.0 : xi * scl) : 0.0;
+    vs[i] = vi;
+    if (below) H.v()[vpos + (i - j - 2)] = vi;
+    if (i == 0) {
+      H.e()[j] = beta;
+      H.tau()[j] = tau;
+    }
+    vpos += k - j - 2;
+    g.sync();  // vs visible; every thread has read alpha
+    if (tau != 0.0) {
+      // p = tau A22 v ; w = p - (tau/2)(p.v) v ; A22 -= v w^T + w v^T  (rows / columns <= j: v = w = 0)
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+      for (int l = L0; l < KP; l += 4) {
+        const double2 v01 = *reinterpret_cast<const double2*>(vs + l);
+        const double2 v23 = *reinterpret_cast<const double2*>(vs + l + 2);
+        a0 = fma(A[l], v01.x, a0);
+        a1 = fma(A[l + 1], v01.y, a1);
+        a2 = fma(A[l + 2], v23.x, a2);
+        a3 = fma(A[l + 3], v23.y, a3);
+      }
+      const double pi = tau * ((a0 + a1) + (a2 + a3));
+      const double K = 0.5 * tau * g.sum(pi * vi);
+      const double wi = in ? pi - K * vi : 0.0;
+      ws[i] = wi;
+      g.sync();
+#pragma unroll
+      for (int l = L0; l < KP; l += 2) {
+        const double2 w2 = *reinterpret_cast<const double2*>(ws + l);
+        const double2 v2 = *reinterpret_cast<const double2*>(vs + l);
+        A[l] -= fma(vi, w2.x, wi * v2.x);
+        A[l + 1] -= fma(vi, w2.y, wi * v2.y);
+      }
+      // (the next column writes vs / ws only after the barriers of its g.sum)
+    }
+  }
+}
+
+template <int KP, int... JB>
+__device__ __forceinline__ void reg_blocks(double (&A)[KP], int i, int k, const Grp<KP>& g, double* xs, double* vs,
+                                           double* ws, const HView<KP>& H, std::integer_sequence<int, JB...>) {
+  int64_t vpos = 0;
+  (reg_block<KP, JB>(A, i, k, g, xs, vs, ws, H, vpos), ...);
+}
+
+template <int KP, int MODE>
+__global__ void __launch_bounds__(128, 3) k_trd_tridiag_reg(ProjArgs a, int slot0, int nslots) {
+  if (a.done && *a.done) return;
+  using Lay = RegLayout<KP>;
+  extern __shared__ double smem[];
+  const int grp = threadIdx.x / KP;
+  const int sl = blockIdx.x * Lay::NMAT + grp;
+  if (sl >= nslots) return;  // whole groups leave together
+  double* st = smem + (size_t)grp * Lay::PER;
+  double* xs = st + ((Lay::TRI + 1) & ~1);
+  double* vs = xs + KP;
+  double* ws = vs + KP;
+  Grp<KP> g{(int)(threadIdx.x % KP), 1 + grp, ws + KP};
+  const int i = g.tid;
+  const int slot = slot0 + sl;
+  const int task = a.ids[slot];
+  const int k = a.ksz[task];
+  const int64_t off = a.off[task];
+  const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
+  const int ns = k * (k + 1) / 2;
+  for (int e = i; e < ns; e += KP) {
+    int r, c;
+    packed_rc(e, r, c);
+    st[e] = input_value<MODE>(a, off + e, r, c);  // (r, c), r <= c at c(c+1)/2 + r
+  }
+  g.sync();
+  double A[KP];
+#pragma unroll
+  for (int l = 0; l < KP; ++l) A[l] = (i < k && l < k) ? st[l >= i ? tri(l) + i : tri(i) + l] : 0.0;
+  reg_blocks<KP>(A, i, k, g, xs, vs, ws, H, std::make_integer_sequence<int, KP / 8>{});
+  // d_j (j < k - 2) was stored at step j; the last 2 x 2 block of T from rows k-2, k-1 through the
+  // (free) staging area, so that no register is indexed dynamically
+  static_assert(Lay::TRI >= 2 * KP, "staging holds two rows");
+  if (k >= 2 && (i == k - 1 || i == k - 2)) {
+    double* row = st + (i == k - 1 ? KP : 0);
+#pragma unroll
+    for (int l = 0; l < KP; ++l) row[l] = A[l];
+  } else if (k == 1 && i == 0) {
+#pragma unroll
+    for (int l = 0; l < KP; ++l) st[l] = A[l];
+  }
+  g.sync();
+  if (i == 0) {
+    if (k >= 2) {
+      H.d()[k - 2] = st[k - 2];
+      H.d()[k - 1] = st[KP + k - 1];
+      H.e()[k - 2] = st[KP + k - 2];
+    } else {
+      H.d()[0] = st[0];
+    }
+  }
+  if (i == 0) H.e()[k - 1] = 0.0;
+}
+
+static int g_trd_reg = 1;    // SDP_TRD_REG=0: the shared-memory tridiagonalization
+static int g_ql_rsqrt = 1;  // SDP_TRD_QLRSQ=0: QL rotations with sqrt + reciprocal
+
 // ---------------------------------------------------------------- 2. implicit QL
 // One tqli chain on T (d, e; e[i] couples i and i+1).  T is first scaled by a
 // power of two so that max |entry| is in [1, 2): then f^2 + g^2 cannot
@@ -225,7 +375,7 @@ __global__ void __launch_bounds__(128) k_trd_tridiag(ProjArgs a, int slot0, int 
 // eigenvector matrix: z_i <- c z_i - s z_{i+1}, z_{i+1} <- s z_i + c z_{i+1}.
 // d, e are accessed as d[i * st], e[i * st].  Returns false if an eigenvalue
 // needed more than kQlMaxIter iterations.  Eigenvalues are returned unscaled.
-template <class Emit>
+template <bool RSQ = false, class Emit>
 __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& emit) {
   double mx = 0.0;
   for (int i = 0; i < k; ++i) mx = fmax(mx, fmax(fabs(d[i * st]), fabs(e[i * st])));
@@ -276,8 +426,14 @@ __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& 
             r = 0.0;
             break;
           }
-          r = sqrt(q);
-          const double ri = 1.0 / r;
+          double ri;
+          if constexpr (RSQ) {  // one rsqrt instead of sqrt + reciprocal (c, s within 2 ulp)
+            ri = rsqrt(q);
+            r = q * ri;
+          } else {
+            r = sqrt(q);
+            ri = 1.0 / r;
+          }
           e[(i + 1) * st] = r;
           s = f * ri;
           c = g * ri;
@@ -300,7 +456,7 @@ __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& 
   return ok;
 }
 
-template <int KP>
+template <int KP, bool RSQ = false>
 __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   extern __shared__ double smem[];
@@ -316,7 +472,7 @@ __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslo
     d[i * QL_T] = H.d()[i];
     e[i * QL_T] = H.e()[i];
   }
-  const bool ok = tql(k, d, e, QL_T, [](int, double, double) {});
+  const bool ok = tql<RSQ>(k, d, e, QL_T, [](int, double, double) {});
   // the side of 0 with fewer eigenvectors: P_+ = sum_{l>0} l v v^T (side 0) or
   // A + sum_{l<0} |l| v v^T (side 1); selected eigenvalues sorted ascending,
   // clusters (gap <= 1e-3 ||T||, LAPACK dstein's ORTOL) and distinct shifts
@@ -359,18 +515,19 @@ __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslo
 // ---------------------------------------------------------------- 3. inverse iteration
 // One thread per cluster of selected eigenvalues (LAPACK dstein): for each
 // eigenvalue in the cluster, the partial-pivoting LU of T - lam I (dlagtf;
-// pivots below tol replaced by +-tol, stored inverted), then 3 solves
+// pivots below tol replaced by +-tol, stored inverted), then kTrdInvIters = 2 solves
 // (dlagts) from a deterministic pseudo-random start, each followed by modified
 // Gram-Schmidt against the cluster's previous vectors and normalisation.  The
 // per-thread factors live in shared memory, thread-minor.  A vector whose
 // residual ||T z - lam z||_inf exceeds 1e-9 ||T|| marks the matrix (rcount = -1)
 // and the apply kernel redoes it by QL with eigenvector accumulation.
 constexpr int IV_T = 32;  // threads per CTA
+constexpr int kTrdInvIters = 2;  // solves per vector (eigenvalues from QL are accurate to eps ||T||)
 template <int KP>
 struct InvLayout {
   static constexpr int HALF = KP / 2;        // selected eigenvalues per matrix <= k / 2
   static constexpr int NMAT = IV_T / HALF;   // matrices per CTA
-  static constexpr size_t bytes() { return (size_t)4 * KP * IV_T * sizeof(double); }
+  static constexpr size_t bytes() { return (size_t)(3 * KP * IV_T + NMAT * 2 * KP) * sizeof(double); }
 };
 
 template <int KP>
@@ -385,17 +542,26 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   const int slot = slot0 + sl;
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
   const int nsel = (int)H.hdr()[0];
-  if (j0 >= nsel || (int)H.clst()[j0] != j0) return;
   const int k = a.ksz[a.ids[slot]];
+  // T (d, e) into shared memory: the recurrences below read it element by element, and the
+  // workspace is far larger than L2 / L1, so global reads would each pay a DRAM round trip
+  double* d = smem + 3 * KP * IV_T + (t / Lay::HALF) * 2 * KP;
+  double* e = d + KP;
+  for (int i = j0; i < k; i += Lay::HALF) {
+    d[i] = H.d()[i];
+    e[i] = H.e()[i];
+  }
+  __syncwarp(Lay::HALF == 32 ? 0xffffffffu : (0xffffu << (16 * ((t / Lay::HALF) & 1))));
+  if (j0 >= nsel || (int)H.clst()[j0] != j0) return;
   const double tnorm = H.hdr()[2];
   const double tol = 2.220446049250313e-16 * fmax(tnorm, 1e-300);
-  const double* d = H.d();
-  const double* e = H.e();
   double* ui = smem + t;  // inverse pivots, element i at [i * IV_T]
-  double* u2 = ui + KP * IV_T;
-  double* mu = u2 + KP * IV_T;
+  double* mu = ui + KP * IV_T;
   double* x = mu + KP * IV_T;
-  // (the second superdiagonal of U is e[i+1] where row i pivoted, else 0)
+  // the first superdiagonal of U is recomputed in the back substitution (3 instead of 4
+  // per-thread arrays: 33 % more resident threads): u2_i = d_{i+1} - lam where row i
+  // pivoted, else the carried r1 = e_0 (i = 0), -mu_{i-1} e_i (row i-1 pivoted) or e_i;
+  // the second superdiagonal is e_{i+1} where row i pivoted, else 0
   double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [i][j], row length KP/2
   bool fail = false;
   for (int j = j0; j < nsel && (int)H.clst()[j] == j0; ++j) {
@@ -421,8 +587,8 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
       }
       if (fabs(p1) < tol) p1 = p1 < 0.0 ? -tol : tol;
       ui[i * IV_T] = 1.0 / p1;
-      u2[i * IV_T] = p2;
       mu[i * IV_T] = m;
+      (void)p2;
     }
     if (fabs(r0) < tol) r0 = r0 < 0.0 ? -tol : tol;
     ui[(k - 1) * IV_T] = 1.0 / r0;
@@ -434,7 +600,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
       h ^= h >> 29;
       x[i * IV_T] = (double)(h >> 11) * (2.0 / 9007199254740992.0) - 1.0;
     }
-    for (int it = 0; it < 3; ++it) {
+    for (int it = 0; it < kTrdInvIters; ++it) {
       double ry = x[0];
       for (int i = 0; i + 1 < k; ++i) {
         const double yn = x[(i + 1) * IV_T];
@@ -451,8 +617,11 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
       x[(k - 1) * IV_T] = xn;
       double mx = fabs(xn);
       for (int i = k - 2; i >= 0; --i) {
-        const double u3 = ((pv >> i) & 1ull) ? e[i + 1] : 0.0;  // i + 2 < k here
-        const double xi = (x[i * IV_T] - u2[i * IV_T] * xn - u3 * xn1) * ui[i * IV_T];
+        const bool piv = (pv >> i) & 1ull;
+        const double u3 = piv ? e[i + 1] : 0.0;  // i + 2 < k here
+        const double u2 = piv ? d[i + 1] - lam
+                              : (i == 0 ? e[0] : (((pv >> (i - 1)) & 1ull) ? -mu[(i - 1) * IV_T] * e[i] : e[i]));
+        const double xi = (x[i * IV_T] - u2 * xn - u3 * xn1) * ui[i * IV_T];
         x[i * IV_T] = xi;
         mx = fmax(mx, fabs(xi));
         xn1 = xn;
@@ -488,12 +657,26 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
 
 // ---------------------------------------------------------------- 4. back-transform, P_+
 // Z holds at most KP/2 columns (the selected side has <= k/2 eigenvectors);
-// row stride KP/2 + 4 == 4 (mod 16) keeps the DMMA fragment loads conflict-free
+// row stride KP/2 + 4 == 4 (mod 16) keeps the DMMA fragment loads conflict-free.
+// The back-transform applies the reflectors in blocks of 8 (compact WY, LAPACK dlarft /
+// dlarfb): H_j0 ... H_j0+7 = I - Y T Y^T, Z <- Z - Y (T (Y^T Z)), all three products as
+// DMMA (mma.sync m8n8k4 f64) on 8 x 8 tiles; each warp owns 8-column tiles of Z, so only
+// the Y / T block is shared (2 CTA barriers per block instead of 3 per reflector).
 template <int KP>
 struct ApplyLayout {
   static constexpr int LD = KP / 2 + 4;
-  static constexpr size_t bytes() { return (size_t)(KP * LD + 3 * KP + 2) * sizeof(double); }
+  static constexpr int YLD = 12;  // Y block row stride (8 reflectors + pad)
+  static constexpr int NW = KP / 32;
+  static constexpr size_t bytes() {
+    return (size_t)(KP * LD + KP * YLD + 128 + NW * 128 + KP + 4) * sizeof(double);
+  }
 };
+
+__device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
 
 template <int KP, int MODE>
 __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nslots) {
@@ -503,11 +686,14 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
   extern __shared__ double smem[];
   const int sl = blockIdx.x;
   if (sl >= nslots) return;
+  constexpr int YLD = Lay::YLD, NW = Lay::NW;
   double* Z = smem;  // selected eigenvectors (columns), then back-transformed
-  double* vv = Z + KP * LD;
-  double* lw = vv + KP;
-  double* ysm = lw + KP;  // back-transform partials of the two warps
-  double* red = ysm + KP;
+  double* Ys = Z + KP * LD;     // Y block [row][8]
+  double* Gs = Ys + KP * YLD;   // Y^T Y (8 x 8)
+  double* Ts = Gs + 64;         // T (8 x 8, upper)
+  double* Wsm = Ts + 64;        // per warp: W = Y^T Z tile, then T W
+  double* lw = Wsm + NW * 128;
+  double* red = lw + KP;
   Grp<KP> g{(int)threadIdx.x, 1, red};
   const int tid = g.tid;
   const int slot = slot0 + sl;
@@ -518,6 +704,8 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
   int nsel = (int)H.hdr()[0];
   int side = (int)H.hdr()[1];
   const bool fallback = a.td.rcount[slot] < 0 || a.td.force_fallback;
+  for (int e = tid; e < KP * LD; e += KP) Z[e] = 0.0;  // rows >= k, columns >= nsel stay 0 (DMMA tiles)
+  g.sync();
   if (!fallback) {
     const double* Zo = a.td.zbuf + a.td.zoff[slot];  // [i][j], row length KP/2
     for (int e = tid; e < k * (KP / 2); e += KP) {
@@ -570,38 +758,78 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     for (int i = 0; i < k; ++i) printf("  d[%d]=% .6e e=% .6e tau=% .6e\n", i, H.d()[i], H.e()[i], H.tau()[i]);
     for (int j = 0; j < nsel; ++j) printf("  sel %d: shift=% .6e w=% .6e clst=%d\n", j, H.lsel()[j], lw[j], (int)H.clst()[j]);
   }
-  // back-transform the selected eigenvectors: V = H_0 H_1 ... H_{k-3} Z
-  int64_t vpos = k >= 2 ? (int64_t)(k - 1) * (k - 2) / 2 : 0;
-  for (int j = k - 3; j >= 0; --j) {
-    vpos -= k - j - 2;
-    const double tau = H.tau()[j];
-    if (tau == 0.0) continue;
-    if (tid >= j + 1 && tid < k) vv[tid] = (tid == j + 1) ? 1.0 : H.v()[vpos + (tid - j - 2)];
-    g.sync();
-    // lane = column (conflict-free row reads); with two warps each takes the
-    // rows of one parity and the partial y meet in shared memory
-    constexpr int NWB = KP / 32;
-    const int h = tid >> 5, c = tid & 31;
-    const bool act = c < nsel;
-    double y0 = 0.0, y1 = 0.0;
-    int i = j + 1 + h;
-    if (act) {
-      for (; i + NWB < k; i += 2 * NWB) {
-        y0 = fma(vv[i], Z[i * LD + c], y0);
-        y1 = fma(vv[i + NWB], Z[(i + NWB) * LD + c], y1);
+  // back-transform the selected eigenvectors: V = H_0 H_1 ... H_{k-3} Z, blocks of 8 reflectors
+  // from the last; reflector j (j <= k-3) has v_j = e_{j+1} + packed entries j+2 .. k-1
+  {
+    const int lane = tid & 31, warp = tid >> 5, r4 = lane >> 2, c4 = lane & 3;
+    const int nref = k - 2;
+    const int ntile = (nsel + 7) / 8;
+    double* Wt = Wsm + warp * 128;
+    for (int j0 = nref > 0 ? ((nref - 1) / 8) * 8 : -1; j0 >= 0; j0 -= 8) {
+      for (int e = tid; e < 8 * KP; e += KP) {
+        const int c = e / KP, i = e - c * KP, j = j0 + c;
+        double y = 0.0;
+        if (j < nref) {
+          if (i == j + 1)
+            y = 1.0;
+          else if (i >= j + 2 && i < k)
+            y = H.v()[(int64_t)j * (k - 2) - (int64_t)j * (j - 1) / 2 + (i - j - 2)];
+        }
+        Ys[i * YLD + c] = y;
       }
-      if (i < k) y0 = fma(vv[i], Z[i * LD + c], y0);
-    }
-    double y = y0 + y1;
-    if constexpr (NWB == 2) {
-      ysm[tid] = y;
       g.sync();
-      y = ysm[c] + ysm[32 + c];
+      const int kb = (j0 + 1) & ~3;  // first row (multiple of 4) where the block is nonzero
+      if (warp == 0) {
+        double gacc[2] = {0.0, 0.0};  // G = Y^T Y
+        for (int k0 = kb; k0 < k; k0 += 4) {
+          const double y = Ys[(k0 + c4) * YLD + r4];
+          dmma8(gacc, y, y);
+        }
+        Gs[r4 * 8 + 2 * c4] = gacc[0];
+        Gs[r4 * 8 + 2 * c4 + 1] = gacc[1];
+        __syncwarp();
+        if (lane < 8) {
+          // row r = lane of T (dlarft, forward columnwise): T_rc = tau_c (r = c),
+          // -tau_c sum_{q<c} T_rq G_qc (r < c), 0 (r > c)
+          double trow[8];
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const double tc = (j0 + c < nref) ? H.tau()[j0 + c] : 0.0;
+            double sacc = 0.0;
+#pragma unroll
+            for (int q = 0; q < c; ++q) sacc = fma(trow[q], Gs[q * 8 + c], sacc);
+            trow[c] = lane < c ? -tc * sacc : (lane == c ? tc : 0.0);
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) Ts[lane * 8 + c] = trow[c];
+        }
+      }
+      g.sync();
+      for (int nt = warp; nt < ntile; nt += NW) {
+        const int n0 = 8 * nt;
+        double w[2] = {0.0, 0.0};  // W = Y^T Z (8 reflectors x 8 columns)
+        for (int k0 = kb; k0 < k; k0 += 4) dmma8(w, Ys[(k0 + c4) * YLD + r4], Z[(k0 + c4) * LD + n0 + r4]);
+        Wt[r4 * 8 + 2 * c4] = w[0];
+        Wt[r4 * 8 + 2 * c4 + 1] = w[1];
+        __syncwarp();
+        double w2[2] = {0.0, 0.0};  // T W
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 4) dmma8(w2, Ts[r4 * 8 + kk + c4], Wt[(kk + c4) * 8 + r4]);
+        Wt[64 + r4 * 8 + 2 * c4] = w2[0];
+        Wt[64 + r4 * 8 + 2 * c4 + 1] = w2[1];
+        __syncwarp();
+        for (int m0 = ((j0 + 1) / 8) * 8; m0 < k; m0 += 8) {  // Z -= Y (T W)
+          double* zr = Z + (m0 + r4) * LD + n0 + 2 * c4;
+          double z[2] = {zr[0], zr[1]};
+#pragma unroll
+          for (int kk = 0; kk < 8; kk += 4) dmma8(z, -Ys[(m0 + r4) * YLD + kk + c4], Wt[64 + (kk + c4) * 8 + r4]);
+          zr[0] = z[0];
+          zr[1] = z[1];
+        }
+        __syncwarp();
+      }
+      g.sync();  // Y / T are rewritten by the next block
     }
-    y *= tau;
-    if (act)
-      for (i = j + 1 + h; i < k; i += NWB) Z[i * LD + c] = fma(-y, vv[i], Z[i * LD + c]);
-    g.sync();
   }
   // P_+ = [A] + sum_t w_t v_t v_t^T as DMMA (mma.sync m8n8k4 f64) 8x8 tiles over the
   // upper tile triangle, K = nsel; then the packed upper entries with the mode epilogue
@@ -664,8 +892,15 @@ template <int KP, int MODE>
 void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
   using TL = TridiagLayout<KP>;
   using IL = InvLayout<KP>;
-  k_trd_tridiag<KP, MODE><<<(n + TL::NMAT - 1) / TL::NMAT, 128, TL::NMAT * TL::PER * sizeof(double), s>>>(a, c0, n);
-  k_trd_ql<KP><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
+  using RL = RegLayout<KP>;
+  if (g_trd_reg)
+    k_trd_tridiag_reg<KP, MODE><<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
+  else
+    k_trd_tridiag<KP, MODE><<<(n + TL::NMAT - 1) / TL::NMAT, 128, TL::NMAT * TL::PER * sizeof(double), s>>>(a, c0, n);
+  if (g_ql_rsqrt)
+    k_trd_ql<KP, true><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
+  else
+    k_trd_ql<KP><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
   k_trd_invit<KP><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
   k_trd_apply<KP, MODE><<<n, KP, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
 }
@@ -674,12 +909,17 @@ template <int KP, int MODE>
 void set_attrs() {
   using TL = TridiagLayout<KP>;
   cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(TL::NMAT * TL::PER * sizeof(double)));
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(2 * KP * QL_T * sizeof(double)));
+  cudaFuncSetAttribute(k_trd_ql<KP, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_ql<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(2 * KP * QL_T * sizeof(double)));
   cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)InvLayout<KP>::bytes());
   cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -689,6 +929,10 @@ void set_attrs() {
 }  // namespace
 
 void psd_trd_init_attributes() {
+  const char* ev = std::getenv("SDP_TRD_REG");
+  g_trd_reg = (ev && ev[0] == '0') ? 0 : 1;
+  const char* eq = std::getenv("SDP_TRD_QLRSQ");
+  g_ql_rsqrt = (eq && eq[0] == '0') ? 0 : 1;
   set_attrs<32, PM_BATCH>();
   set_attrs<32, PM_PRIMAL>();
   set_attrs<32, PM_DUAL>();
