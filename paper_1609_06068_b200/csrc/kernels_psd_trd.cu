@@ -234,8 +234,8 @@ struct RegLayout {
   static constexpr int PER = ((TRI + 1) & ~1) + 3 * KP + 4;  // staging (packed), xs, vs, ws, red
 };
 
-template <int KP, int JB>
-__device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const Grp<KP>& g, double* xs, double* vs,
+template <int KP, int JB, int G>
+__device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const Grp<G>& g, double* xs, double* vs,
                                           double* ws, const HView<KP>& H, int64_t& vpos) {
   constexpr int L0 = 8 * JB;
   constexpr int UNR = KP <= 32 ? 8 : 1;  // KP = 32: steps unrolled too (all register indices static)
@@ -249,13 +249,13 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
     const bool below = i >= j + 2 && i < k;
     if (i == j) H.d()[j] = xi;  // row j is final: d_j = A(j, j)
     double alpha;
-    if constexpr (KP <= 32) {
-      alpha = __shfl_sync(0xffffffffu, xi, j + 1);
+    if constexpr (G <= 32) {
+      alpha = __shfl_sync(0xffffffffu, xi, (j + 1) & 31);
     } else {
       xs[i] = xi;  // published by the barriers inside g.sum
     }
     const double sig = g.sum(below ? xi * xi : 0.0);
-    if constexpr (KP > 32) alpha = xs[j + 1];
+    if constexpr (G > 32) alpha = xs[j + 1];
     double tau = 0.0, beta = alpha, scl = 0.0;
     if (sig > 0.0) {
       const double nrm = sqrt(fma(alpha, alpha, sig));
@@ -267,7 +267,7 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
     const double vi = in ? ((i == j + 1) ? 1.0 : xi * scl) : 0.0;
     vs[i] = vi;
     if (below) H.v()[vpos + (i - j - 2)] = vi;
-    if (i == 0) {
+    if (i == KP - 1) {  // (row KP-1 takes part in every block)
       H.e()[j] = beta;
       H.tau()[j] = tau;
     }
@@ -302,11 +302,23 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
   }
 }
 
+// KP = 64: once j >= 32 (blocks JB >= 4) rows 0..31 are final, so the first warp waits at the
+// closing barrier and the second continues alone with warp-level sums and syncs
+template <int KP, int JB>
+__device__ __forceinline__ void reg_block_any(double (&A)[KP], int i, int k, const Grp<KP>& g, double* xs, double* vs,
+                                              double* ws, const HView<KP>& H, int64_t& vpos) {
+  if constexpr (KP > 32 && 8 * JB >= 32) {
+    if (i >= 32) reg_block<KP, JB, 32>(A, i, k, Grp<32>{i & 31, 0, nullptr}, xs, vs, ws, H, vpos);
+  } else {
+    reg_block<KP, JB, KP>(A, i, k, g, xs, vs, ws, H, vpos);
+  }
+}
+
 template <int KP, int... JB>
 __device__ __forceinline__ void reg_blocks(double (&A)[KP], int i, int k, const Grp<KP>& g, double* xs, double* vs,
                                            double* ws, const HView<KP>& H, std::integer_sequence<int, JB...>) {
   int64_t vpos = 0;
-  (reg_block<KP, JB>(A, i, k, g, xs, vs, ws, H, vpos), ...);
+  (reg_block_any<KP, JB>(A, i, k, g, xs, vs, ws, H, vpos), ...);
 }
 
 template <int KP, int MODE>
