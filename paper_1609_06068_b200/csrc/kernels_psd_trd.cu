@@ -680,7 +680,7 @@ struct ApplyLayout {
   static constexpr int YLD = 12;  // Y block row stride (8 reflectors + pad)
   static constexpr int NW = KP / 32;
   static constexpr size_t bytes() {
-    return (size_t)(KP * LD + KP * YLD + 128 + NW * 128 + KP + 4) * sizeof(double);
+    return (size_t)(KP * LD + KP * YLD + 128 + NW * 128 + KP + 12) * sizeof(double);
   }
 };
 
@@ -777,9 +777,15 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     const int nref = k - 2;
     const int ntile = (nsel + 7) / 8;
     double* Wt = Wsm + warp * 128;
-    for (int j0 = nref > 0 ? ((nref - 1) / 8) * 8 : -1; j0 >= 0; j0 -= 8) {
-      for (int e = tid; e < 8 * KP; e += KP) {
-        const int c = e / KP, i = e - c * KP, j = j0 + c;
+    double* taus = red + 4;  // tau of the block's reflectors
+    // the next block's Y row (thread = row) and tau are fetched into registers while the current
+    // block is applied (the reflectors come from DRAM)
+    double ypre[8], tpre = 0.0;
+    auto fetch = [&](int j0) {
+      const int i = tid;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int j = j0 + c;
         double y = 0.0;
         if (j < nref) {
           if (i == j + 1)
@@ -787,8 +793,17 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
           else if (i >= j + 2 && i < k)
             y = H.v()[(int64_t)j * (k - 2) - (int64_t)j * (j - 1) / 2 + (i - j - 2)];
         }
-        Ys[i * YLD + c] = y;
+        ypre[c] = y;
       }
+      if (tid < 8) tpre = (j0 + tid < nref) ? H.tau()[j0 + tid] : 0.0;
+    };
+    const int jlast = nref > 0 ? ((nref - 1) / 8) * 8 : -1;
+    if (jlast >= 0) fetch(jlast);
+    for (int j0 = jlast; j0 >= 0; j0 -= 8) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) Ys[tid * YLD + c] = ypre[c];
+      if (tid < 8) taus[tid] = tpre;
+      if (j0 >= 8) fetch(j0 - 8);
       g.sync();
       const int kb = (j0 + 1) & ~3;  // first row (multiple of 4) where the block is nonzero
       if (warp == 0) {
@@ -806,7 +821,7 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
           double trow[8];
 #pragma unroll
           for (int c = 0; c < 8; ++c) {
-            const double tc = (j0 + c < nref) ? H.tau()[j0 + c] : 0.0;
+            const double tc = taus[c];
             double sacc = 0.0;
 #pragma unroll
             for (int q = 0; q < c; ++q) sacc = fma(trow[q], Gs[q * 8 + c], sacc);
