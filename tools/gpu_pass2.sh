@@ -26,4 +26,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_g
   -o "$OUT/full_cfg2" python bench.py --steps 3 --warmup 3 --no-cpu > "$OUT/ncu_f2.log" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gtrd_tridiag|k_gtrd_vec|k_gtrd_back" -s 30 -c 3 \
   -o "$OUT/full_cfg3" python bench.py --workload cfg3 --steps 3 --warmup 3 --no-cpu > "$OUT/ncu_f3.log" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_trd_(tridiag_reg|ql|invit|apply)<.int.64" -c 4 \
+  -o "$OUT/full_cfg4" python bench.py --workload cfg4 --steps 1 --warmup 0 --no-cpu > "$OUT/ncu_f4.log" 2>&1
 echo done >> "$OUT/rc.txt"
