@@ -4,21 +4,23 @@
 //
 // Jacobi executes ~4k^3 instructions per sweep and needs 6-9 sweeps from a
 // cold start; this tier uses the flop-lean textbook pipeline instead:
-//   1. k_trd_tridiag (KP threads per matrix, one row each): Householder
-//      reduction to tridiagonal form A = Q T Q^T (LAPACK dsytd2, lower; Golub &
-//      Van Loan Alg. 8.3.1), ~4/3 k^3 flops, matrix in shared memory.
+//   1. k_trd_tridiag_reg (KP threads per matrix, row i of A in thread i's
+//      registers): Householder reduction to tridiagonal form A = Q T Q^T (LAPACK
+//      dsytd2, lower; Golub & Van Loan Alg. 8.3.1); k_trd_tridiag is the
+//      shared-memory variant (SDP_TRD_REG=0).
 //   2. k_trd_ql (lane per matrix): implicit QL with Wilkinson shifts on T
 //      (Golub & Van Loan Alg. 8.3.3 / "tqli"), eigenvalues only; the sequential
 //      chain of one matrix runs in one lane, so a warp advances 32 matrices at
-//      once and the chain latency is hidden across matrices.
-//   3. k_trd_apply (KP threads per matrix): P_+ needs only the eigenvectors on
-//      one side of 0, so the smaller side is taken (P_+ = sum_{l>0} l v v^T, or
-//      A + sum_{l<0} |l| v v^T); its eigenvectors of T come from inverse
-//      iteration (LAPACK dstein: partial-pivoting tridiagonal LU, clusters of
-//      gap <= 1e-3 ||T|| reorthogonalised), O(k) per vector instead of the O(k^2)
-//      rotation accumulation of QL, then V = Q Z with the Householder vectors and
-//      the reconstruction with the mode epilogue (primal: lambda_k +=
-//      rho (x_k - H_k x), E:LambdakUpdate).
+//      once and the chain latency is hidden across matrices.  P_+ needs only the
+//      eigenvectors on one side of 0, so the smaller side is selected (P_+ =
+//      sum_{l>0} l v v^T, or A + sum_{l<0} |l| v v^T).
+//   3. k_trd_invit (thread per cluster of selected eigenvalues): their
+//      eigenvectors of T by inverse iteration (LAPACK dstein: partial-pivoting
+//      tridiagonal LU, clusters of gap <= 1e-3 ||T|| reorthogonalised), O(k) per
+//      vector instead of the O(k^2) rotation accumulation of QL.
+//   4. k_trd_apply (KP threads per matrix): V = Q Z with the Householder vectors
+//      in compact-WY blocks of 8 (DMMA), then the reconstruction (DMMA) with the
+//      mode epilogue (primal: lambda_k += rho (x_k - H_k x), E:LambdakUpdate).
 // Every inverse-iteration vector is checked (||T z - lambda z|| <= 1e-9 ||T||);
 // if one fails, or QL hit its iteration cap (50 per eigenvalue), the matrix is redone inside the
 // apply kernel by QL with eigenvector accumulation (every thread runs the same
