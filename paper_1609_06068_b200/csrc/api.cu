@@ -403,8 +403,20 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
   gt.status = al.zeros<int32_t>((size_t)ng);
   gt.ev_pre = al.upload(ev);
   gt.tot_ev = ev[ng];
-  gt.vg_pre = al.upload(vg);
-  gt.tot_vg = vg[ng];
+  {
+    // inverse-iteration CTA slots in descending order (the k = 630 groups' chains are the longest)
+    std::vector<int32_t> vgo(ng + 1, 0), vgg(ng, 0);
+    const char* vo = getenv("SDP_GTRD_VEC_ORDER");
+    const bool desc = !(vo && vo[0] == '0');
+    for (int q = 0; q < ng; ++q) {
+      const int g = desc ? order[q] : q;
+      vgg[q] = g;
+      vgo[q + 1] = vgo[q] + (vg[g + 1] - vg[g]);
+    }
+    gt.vg_pre = al.upload(vgo);
+    gt.vg_g = al.upload(vgg);
+    gt.tot_vg = vgo[ng];
+  }
   gt.ngrp = al.zeros<int32_t>((size_t)ng);
   gt.wy_pre = al.upload(wy);
   gt.tot_wy = wy[ng];

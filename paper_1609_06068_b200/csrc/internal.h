@@ -97,7 +97,8 @@ struct GtrdDev {
   const int32_t* job_g = nullptr;      // njob * 8: giant per CTA (solo) or in slot 0 (coop); -1 unused
   const int32_t* job_coop = nullptr;   // njob: 1 = the cluster reduces one matrix together
   const int32_t* ev_pre = nullptr;     // ng + 1: bisection warps (32 indices each)
-  const int32_t* vg_pre = nullptr;     // ng + 1: inverse-iteration warps (2 ceil(H / 32) + 1 groups)
+  const int32_t* vg_pre = nullptr;     // ng + 1: inverse-iteration CTA slots (2 ceil(k / cap) + 1), giants by descending k
+  const int32_t* vg_g = nullptr;       // ng: the giant of each vg_pre position (largest first: longest chains start first)
   int32_t* ngrp = nullptr;             // per giant: groups in use (device-computed)
   const int32_t* wy_pre = nullptr;     // ng + 1: WY groups (16 reflectors each)
   const int32_t* bt_pre = nullptr;     // ng + 1: back-transform CTAs (kGtrdBackCols columns each)

@@ -629,8 +629,9 @@ constexpr int kInvIters = 2;
 __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
   if (a.done && *a.done) return;
   const GtrdDev& gt = a.gd.gt;
-  const int g = find_item(gt.vg_pre, gt.ng, blockIdx.x);
-  const int grp = blockIdx.x - gt.vg_pre[g];
+  const int gi = find_item(gt.vg_pre, gt.ng, blockIdx.x);
+  const int g = gt.vg_g[gi];
+  const int grp = blockIdx.x - gt.vg_pre[gi];
   if (gt.status[g] < 0 || grp >= gt.ngrp[g]) return;
   const int k = a.ksz[gt.task[g]];
   const int H = gt.hsel[g];
