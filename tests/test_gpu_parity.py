@@ -685,6 +685,33 @@ def test_trd_tier_inline_ql_fallback_subprocess():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
+@pytest.mark.parametrize("variant", [{"SDP_TRD_REG": "0"}, {"SDP_TRD_QLRSQ": "0"}])
+def test_trd_tier_variants_subprocess(variant):
+    """The A/B variants of the QL tier kept for measurement (shared-memory
+    tridiagonalization; sqrt + reciprocal QL rotations) stay correct: random orders
+    17..64 plus the degenerate structured inputs, against the oracle."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L\n"
+        "from oracle import psd as opsd\n"
+        "from test_gpu_parity import _structured\n"
+        "rng = np.random.default_rng(5)\n"
+        "mats = [M for k in (17, 32, 33, 64) for M in _structured(k, rng)]\n"
+        "ks = list(rng.integers(17, 65, 2200))\n"
+        "vals = [rng.standard_normal(k*(k+1)//2) for k in ks]\n"
+        "ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)\n"
+        "vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)\n"
+        "out = L.PsdPlan(ks).project_host(vals)\n"
+        "want = opsd.project_psd_packed_batch(ks, vals)\n"
+        "e = np.linalg.norm(out - want) / np.linalg.norm(want)\n"
+        "print(e); assert e <= 1e-12, e\n" % (ROOT, os.path.dirname(os.path.abspath(__file__))))
+    env = dict(os.environ, **variant)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 # ------------------------------------------------------------------ adaptive rho (SURVEY 8(f) #2)
 
 @pytest.mark.parametrize("form,rho", [("primal", 1.0), ("dual", 1.0), ("primal", 50.0)])
