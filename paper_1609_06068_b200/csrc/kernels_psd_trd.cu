@@ -356,6 +356,7 @@ __global__ void __launch_bounds__(128, 3) k_trd_tridiag_reg(ProjArgs a, int slot
   // d_j (j < k - 2) was stored at step j; the last 2 x 2 block of T from rows k-2, k-1 through the
   // (free) staging area, so that no register is indexed dynamically
   static_assert(Lay::TRI >= 2 * KP, "staging holds two rows");
+  g.sync();  // every thread has loaded its row from the staging area (k <= 2 runs no step barrier)
   if (k >= 2 && (i == k - 1 || i == k - 2)) {
     double* row = st + (i == k - 1 ? KP : 0);
 #pragma unroll
