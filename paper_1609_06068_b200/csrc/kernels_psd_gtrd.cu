@@ -53,6 +53,12 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gmem_s
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem_src) : "memory");
 }
+// 8-byte asynchronous copy, or 8 zero bytes when !valid (src-size 0)
+__device__ __forceinline__ void cp_async8z(double* smem_dst, const double* gmem_src, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_dst);
+  const int n = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem_src), "r"(n) : "memory");
+}
 
 __device__ __forceinline__ void packed_rc(int e, int& r, int& c) {
   int cc = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
@@ -1106,22 +1112,34 @@ __global__ void __launch_bounds__(GR_NW * 32) k_gtrd_recon(ProjArgs a) {
   for (int p = 0; p < 4; ++p)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[p][q][0] = acc[p][q][1] = 0.0;
+  const double* lwg = W.lw();
   for (int kk = 0; kk < nsel; kk += 32) {
     __syncwarp();
-    for (int e = lane; e < 1024; e += 32) {  // lanes along the rows: Z is column-major
-      const int m = e & 31, u = e >> 5;
-      const int rr = rb * 32 + m, cc = cb * 32 + m, uu = kk + u;
-      const bool ok = uu < nsel;
-      sm.X[m * GR_LDS + u] = (ok && rr < k) ? Z[(int64_t)uu * k + rr] * W.lw()[uu] : 0.0;  // [m][k]
-      sm.Y[m * GR_LDS + u] = (ok && cc < k) ? Z[(int64_t)uu * k + cc] : 0.0;               // [n][k]
+    // 64 asynchronous 8-byte copies per lane (lanes along the rows: Z is column-major), zero-filled
+    // outside the matrix / the selected columns: one L2 round trip per K chunk instead of one per
+    // few loads; the weights lw scale the A fragments below
+    {
+      const int rr = rb * 32 + lane, cc = cb * 32 + lane;
+#pragma unroll 8
+      for (int u = 0; u < 32; ++u) {
+        const int uu = kk + u;
+        const bool ok = uu < nsel;
+        const double* zx = Z + (int64_t)(ok ? uu : 0) * k;
+        cp_async8z(&sm.X[lane * GR_LDS + u], zx + (rr < k ? rr : 0), ok && rr < k);  // [m][k]
+        cp_async8z(&sm.Y[lane * GR_LDS + u], zx + (cc < k ? cc : 0), ok && cc < k);  // [n][k]
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
+    const double lwl = kk + lane < nsel ? lwg[kk + lane] : 0.0;
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     __syncwarp();
 #pragma unroll
     for (int ks = 0; ks < 8; ++ks) {
+      const double w = __shfl_sync(0xffffffffu, lwl, ks * 4 + c4);
       double af[4], bf[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        af[q] = sm.X[(q * 8 + r4) * GR_LDS + ks * 4 + c4];
+        af[q] = sm.X[(q * 8 + r4) * GR_LDS + ks * 4 + c4] * w;
         bf[q] = sm.Y[(q * 8 + r4) * GR_LDS + ks * 4 + c4];
       }
 #pragma unroll
