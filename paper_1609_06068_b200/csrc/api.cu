@@ -118,10 +118,10 @@ using namespace sdp;
 
 // First clique of the second half of the pipelined iteration: the stacked-length fraction
 // SDP_PIPE_SPLIT of the cliques goes to the first half.  Defaults measured on cfg2 (B200, A/B over
-// 0.35 .. 0.8): primal 0.65 (1166 vs 1121 it/s at 0.5), dual 0.6 (1139 vs 1123 it/s) -- a larger
+// 0.35 .. 0.8): primal 0.65 (1166 vs 1121 it/s at 0.5), dual 0.55 (1150 vs 1119 it/s) -- a larger
 // first half shortens the second half's projection, which is the exposed tail of the iteration.
 inline int64_t pipe_split(const std::vector<int64_t>& off, int64_t p, int form) {
-  const double def = form == SDP_FORM_DUAL ? 0.6 : 0.65;
+  const double def = form == SDP_FORM_DUAL ? 0.55 : 0.65;
   const char* e = getenv("SDP_PIPE_SPLIT");
   double f = e ? atof(e) : def;
   if (!(f > 0.05 && f < 0.95)) f = def;
