@@ -83,6 +83,18 @@ typedef struct {
   const int32_t* e_col;
 } sdp_problem;
 
+/* Optional device-memory allocator (lets the caller -- e.g. PyTorch's caching
+ * allocator through torch uint8 tensors -- own every device byte of a handle or plan).
+ * alloc(ctx, bytes, device) returns a device pointer on `device` aligned to >= 256 B,
+ * or NULL on failure (the call then fails with SDP_E_OOM); free(ctx, ptr, device)
+ * releases it.  The library calls free only for pointers it got from alloc, after
+ * synchronising the work that used them.  NULL allocator = cudaMalloc / cudaFree. */
+typedef struct {
+  void* (*alloc)(void* ctx, size_t bytes, int32_t device);
+  void (*free)(void* ctx, void* ptr, int32_t device);
+  void* ctx;
+} sdp_allocator;
+
 typedef struct {
   int32_t form;              /* SDP_FORM_PRIMAL or SDP_FORM_DUAL                     */
   double rho;                /* ADMM penalty rho > 0; default 1.0     */
@@ -99,6 +111,12 @@ typedef struct {
   int32_t adapt_rho;
   double adapt_mu;
   double adapt_tau;
+  const sdp_allocator* allocator;  /* NULL: cudaMalloc; else every device buffer of the handle
+                                    * (state, A, factor, workspaces, setup scratch) comes from it;
+                                    * the struct is copied, ctx must outlive the handle */
+  void* comm;                /* world > 1 without NCCL: an in-process loopback group
+                              * (sdp_loopback_create) shared by the `world` handles of one
+                              * process; NULL = NCCL (nccl_id) */
 } sdp_options;
 
 typedef struct {
@@ -166,15 +184,16 @@ int sdp_set_rho(sdp_handle h, double rho);
 /* Synchronise and report sizes, residuals and objective (host out). */
 int sdp_get_info(sdp_handle h, sdp_info* info);
 
-/* PSD completion of the current X (Theorem 1).
- * X = smat(x) is known on the extended chordal pattern E' only; out (host, n*n
+/* PSD completion of the current SDP primal X (SDP_VEC_SDP_X: x in the primal form,
+ * -rho x in the dual form; Theorem 1).
+ * X is known on the extended chordal pattern E' only; out (host, n*n
  * doubles, row-major, written entirely) receives a completion that agrees with X
  * on E' and fills every other entry by the perfect-elimination construction:
  * vertices in reverse elimination order, X[v,u] = X[v,a] X[a,a]^+ X[a,u] with
  * a = the later neighbours of v (a clique of E'); the pseudo-inverse drops
  * eigenvalues below rtol * max|lambda| (take it near the solve accuracy, e.g.
  * 1e-8: separator blocks of a converged X are singular to that accuracy).  When every
- * maximal-clique block of X is PSD (a converged primal solve) the result is PSD
+ * maximal-clique block of X is PSD (a converged solve, either form) the result is PSD
  * (Grone); for definite blocks it is the maximum-determinant completion.  Host
  * computation, O(n^2 * max clique) once per call; world == 1 or collective.
  * Errors: SDP_E_INVALID_ARG. */
@@ -186,12 +205,22 @@ int sdp_complete_x(sdp_handle h, double rtol, double* out);
 int sdp_get_elimination_order(sdp_handle h, int32_t* order);
 
 /* ---- getters: synchronise the stream, copy into host buffers ----------- */
-#define SDP_VEC_X 0        /* N: x (svec on the pattern, primal KKT x / dual KKT x)   */
+/* Iterates of the decomposed problem (the state of Algorithm 1 / 2): */
+#define SDP_VEC_X 0        /* N: KKT x (svec on the pattern; E:OptCondMinYPrimal / E:OptCondMinYDual) */
 #define SDP_VEC_Y 1        /* m: KKT y                                               */
-#define SDP_VEC_XMAT 2     /* N: unscaled matrix entries of x on the pattern         */
+#define SDP_VEC_XMAT 2     /* N: unscaled matrix entries of the KKT x on the pattern */
+/* The primal-dual SDP pair those iterates carry (Remark 1; the KKT
+ * multipliers are rho*y, and rho*x), the same in both forms:
+ *   primal form (Alg. 1): X = x,        yhat = -rho y,  Z_k = lambda_k
+ *   dual form   (Alg. 2): X = -rho x,   yhat = y,       Z_k = z_k
+ * with rho the penalty of the last iteration.  X satisfies A(X) = b exactly in both
+ * forms (every iterate); <C,X> - <b,yhat> -> 0 and X, Z_k -> PSD at convergence. */
+#define SDP_VEC_SDP_X 3    /* N: unscaled matrix entries X_ij of the SDP primal X on the pattern */
+#define SDP_VEC_SDP_Y 4    /* m: the SDP dual yhat (E:DualSDP)                        */
 #define SDP_BLK_XK 0       /* stacked x_k (primal) or z_k (dual)                      */
 #define SDP_BLK_LAMBDA 1   /* stacked lambda_k                                       */
 #define SDP_BLK_VK 2       /* stacked v_k (dual only)                                */
+#define SDP_BLK_SDP_Z 3    /* stacked svec Z_k of the SDP dual slack Z = sum_k E_k^T Z_k E_k (Theorem 2) */
 int sdp_get_vector(sdp_handle h, int32_t which, double* out);
 int sdp_get_blocks(sdp_handle h, int32_t which, double* out);   /* stot values */
 /* Pattern coordinates (row[N], col[N]) in canonical order. */
@@ -223,6 +252,10 @@ int sdp_state_bytes(sdp_handle h, int64_t* bytes);   /* size of the blob for the
 int sdp_save_state(sdp_handle h, void* host_out, int64_t capacity);
 int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes);
 
+/* Device bytes the handle currently holds (live allocations, from the allocator of
+ * sdp_options or cudaMalloc) and the peak during setup (host out, either may be NULL). */
+int sdp_workspace_bytes(sdp_handle h, int64_t* live_bytes, int64_t* peak_bytes);
+
 /* Free all resources of the handle (synchronises). */
 int sdp_destroy(sdp_handle h);
 
@@ -242,6 +275,10 @@ typedef struct sdp_psd_plan_s* sdp_psd_plan;
  * Matrix i occupies k(k+1)/2 doubles at offset sum_{j<i} k_j(k_j+1)/2 of the
  * in/out arrays, packed upper column-major, UNSCALED entries. */
 int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, sdp_psd_plan* out);
+/* Same, with every device buffer of the plan (workspaces and the host-path staging
+ * buffers) taken from `allocator` (copied; NULL = cudaMalloc). */
+int sdp_psd_plan_create_ex(int64_t count, const int32_t* h_sizes, int32_t device, const sdp_allocator* allocator,
+                           sdp_psd_plan* out);
 /* out_i = argmin_{P PSD} ||P - in_i||_F for every i.  d_in, d_out: device,
  * may alias (in place).  Asynchronous on `stream` (cudaStream_t, NULL = default). */
 int sdp_project_psd_batch(sdp_psd_plan plan, const double* d_in, double* d_out, void* stream);
@@ -256,6 +293,20 @@ int sdp_psd_plan_destroy(sdp_psd_plan plan);
 /* 128-byte NCCL unique id (rank 0 calls it and broadcasts it, e.g. through
  * torch.distributed).  NCCL is loaded with dlopen("libnccl.so.2"). */
 int sdp_nccl_unique_id(void* out128);
+/* In-process loopback group for `world` sharded handles of ONE process (one host
+ * thread per rank, handles on `device` or on devices with peer access to it): pass it
+ * as sdp_options.comm with rank / world and no nccl_id.  Each all-reduce of the
+ * iteration meets on the host (a barrier inside the call that enqueues it) and is
+ * ordered on the devices by CUDA events only (no kernel waits for another rank):
+ * rank 0 sums the ranks' buffers in rank order, every rank copies the sum back, so
+ * results do not depend on timing.  It exists to run and test the sharded device
+ * path on one GPU; one process per GPU over NCCL is the product path.
+ * Handles using it do not capture CUDA graphs (use_graph is ignored).  Every call
+ * on such handles must be made by all ranks (collective), each from its own thread.
+ * world <= 16.  Destroy the group after its handles. */
+int sdp_loopback_create(int32_t world, int32_t device, void** out);
+int sdp_loopback_destroy(void* group);
+
 /* Host-only shard plan of the pattern (row, col) for `rank` of `world`:
  * clique_begin[world+1] (contiguous ranges in canonical clique order),
  * local_coords[n_local] (pattern coordinates the rank's cliques touch, sorted),

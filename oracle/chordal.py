@@ -24,11 +24,16 @@ import numpy as np
 def aggregate_adjacency(prob) -> np.ndarray:
     """Boolean n x n adjacency of the aggregate sparsity pattern.
 
-    (i, j) is an edge iff entry ij is listed in C or in some A_i; diagonal
+    (i, j) is an edge iff entry ij is listed in C, in some A_i or in the
+    optional user pattern E (the pattern "described by the graph
+    G(V,E)"; attributes e_row / e_col, may be absent or None); diagonal
     self-loops are implicit and not stored here."""
     n = prob.n
     adj = np.zeros((n, n), dtype=bool)
-    for r, c in ((prob.c_row, prob.c_col), (prob.a_row, prob.a_col)):
+    pairs = [(prob.c_row, prob.c_col), (prob.a_row, prob.a_col)]
+    if getattr(prob, "e_row", None) is not None:
+        pairs.append((prob.e_row, prob.e_col))
+    for r, c in pairs:
         r = np.asarray(r, dtype=np.int64)
         c = np.asarray(c, dtype=np.int64)
         adj[r, c] = True

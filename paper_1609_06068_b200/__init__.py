@@ -5,8 +5,8 @@ include/chordal_sdp.h); this package is its thin Python binding.
     from paper_1609_06068_b200 import Solver, PsdPlan, chordal_cliques
     from paper_1609_06068_b200.sdpa import read_sdpa   # SDPA sparse (.dat-s) input
 """
-from ._lib import (EXPORTED, LIB_PATH, PsdPlan, SdpError, Solver, chordal_cliques,  # noqa: F401
-                   lib, nccl_unique_id, shard_plan)
+from ._lib import (EXPORTED, LIB_PATH, LoopbackGroup, PsdPlan, SdpError, Solver, TorchAllocator,  # noqa: F401
+                   chordal_cliques, lib, nccl_unique_id, shard_plan)
 
-__all__ = ["Solver", "PsdPlan", "chordal_cliques", "shard_plan", "nccl_unique_id", "SdpError", "lib", "LIB_PATH",
+__all__ = ["Solver", "PsdPlan", "LoopbackGroup", "TorchAllocator", "chordal_cliques", "shard_plan", "nccl_unique_id", "SdpError", "lib", "LIB_PATH",
            "EXPORTED"]

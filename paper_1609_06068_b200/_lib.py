@@ -42,8 +42,8 @@ SDP_E = {-1: "SDP_E_INVALID_ARG", -2: "SDP_E_RANK_DEFICIENT", -3: "SDP_E_CUDA", 
          -5: "SDP_E_OOM", -6: "SDP_E_NUMERICAL", -7: "SDP_E_STATE"}
 FORM = {"primal": 0, "dual": 1}
 SDP_A_COO, SDP_A_DENSE = 0, 1
-VEC_X, VEC_Y, VEC_XMAT = 0, 1, 2
-BLK_XK, BLK_LAMBDA, BLK_VK = 0, 1, 2
+VEC_X, VEC_Y, VEC_XMAT, VEC_SDP_X, VEC_SDP_Y = 0, 1, 2, 3, 4
+BLK_XK, BLK_LAMBDA, BLK_VK, BLK_SDP_Z = 0, 1, 2, 3
 SDP_MAX_K = 1024
 
 
@@ -61,11 +61,19 @@ class sdp_problem(C.Structure):
                 ("e_nnz", C.c_int64), ("e_row", C.c_void_p), ("e_col", C.c_void_p)]
 
 
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_int32)
+
+
+class sdp_allocator(C.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", C.c_void_p)]
+
+
 class sdp_options(C.Structure):
     _fields_ = [("form", C.c_int32), ("rho", C.c_double), ("device", C.c_int32), ("stream", C.c_void_p),
                 ("check_every", C.c_int32), ("use_graph", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32),
                 ("nccl_id", C.c_void_p), ("adapt_rho", C.c_int32), ("adapt_mu", C.c_double),
-                ("adapt_tau", C.c_double)]
+                ("adapt_tau", C.c_double), ("allocator", C.POINTER(sdp_allocator)), ("comm", C.c_void_p)]
 
 
 class sdp_info(C.Structure):
@@ -97,6 +105,10 @@ _sig = {
     "sdp_complete_x": (_i32, [_vp, _d, _vp]),
     "sdp_get_elimination_order": (_i32, [_vp, _vp]),
     "sdp_destroy": (_i32, [_vp]),
+    "sdp_workspace_bytes": (_i32, [_vp, C.POINTER(_i64), C.POINTER(_i64)]),
+    "sdp_loopback_create": (_i32, [_i32, _i32, C.POINTER(_vp)]),
+    "sdp_loopback_destroy": (_i32, [_vp]),
+    "sdp_psd_plan_create_ex": (_i32, [_i64, _vp, _i32, C.POINTER(sdp_allocator), C.POINTER(_vp)]),
     "sdp_state_bytes": (_i32, [_vp, C.POINTER(_i64)]),
     "sdp_save_state": (_i32, [_vp, _vp, _i64]),
     "sdp_load_state": (_i32, [_vp, _vp, _i64]),
@@ -194,13 +206,66 @@ def shard_plan(n, row, col, world, rank):
             "shared_coords": shr[:ns.value].copy()}
 
 
+class TorchAllocator:
+    """sdp_allocator backed by torch uint8 tensors: PyTorch's caching allocator owns every
+    device byte of the handles / plans that use it (include/chordal_sdp.h, sdp_allocator)."""
+
+    def __init__(self):
+        import torch
+        self._torch = torch
+        self.live = {}
+
+        def _alloc(ctx, nbytes, device):
+            try:
+                t = self._torch.empty(int(nbytes), dtype=self._torch.uint8, device=f"cuda:{int(device)}")
+            except Exception:  # noqa: BLE001  (OOM -> NULL -> SDP_E_OOM)
+                return None
+            self.live[t.data_ptr()] = t
+            return t.data_ptr()
+
+        def _free(ctx, ptr, device):
+            self.live.pop(int(ptr), None)
+
+        self._cb = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+        self.struct = sdp_allocator(self._cb[0], self._cb[1], None)
+
+    def bytes_held(self):
+        return sum(t.numel() for t in self.live.values())
+
+
+class LoopbackGroup:
+    """sdp_loopback_create: an in-process group of `world` sharded handles (one host thread
+    per rank, collective calls) -- runs the clique-sharded device path on one GPU."""
+
+    def __init__(self, world, device=0):
+        h = C.c_void_p()
+        _check(lib.sdp_loopback_create(int(world), int(device), C.byref(h)))
+        self.h, self.world = h, int(world)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib.sdp_loopback_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class Solver:
     """Handle of sdp_setup().  `prob` needs the attributes n, m, c_row, c_col,
-    c_val, b, a_fmt ("coo" | "dense"), a_con, a_row, a_col, a_val."""
+    c_val, b, a_fmt ("coo" | "dense"), a_con, a_row, a_col, a_val (optional e_row,
+    e_col: the user pattern E).  allocator: None (cudaMalloc), "torch" or a
+    TorchAllocator.  comm: a LoopbackGroup for world > 1 inside one process."""
 
     def __init__(self, prob, form="primal", rho=1.0, device=0, stream=None, use_graph=True, check_every=10,
-                 rank=0, world=1, nccl_id=None, adapt_rho=False, adapt_mu=10.0, adapt_tau=2.0):
+                 rank=0, world=1, nccl_id=None, adapt_rho=False, adapt_mu=10.0, adapt_tau=2.0, allocator=None,
+                 comm=None):
         self.form = form
+        self.allocator = TorchAllocator() if allocator == "torch" else allocator
+        self.comm = comm
         keep = []
 
         def k(a, dt):
@@ -221,7 +286,11 @@ class Solver:
         P.a_row, P.a_col, P.a_val = _ptr(ar), _ptr(ac), _ptr(av)
         bb = k(prob.b, np.float64)
         P.b = _ptr(bb)
-        P.e_nnz, P.e_row, P.e_col = 0, None, None
+        if getattr(prob, "e_row", None) is not None:
+            er, ec = k(prob.e_row, np.int32), k(prob.e_col, np.int32)
+            P.e_nnz, P.e_row, P.e_col = er.size, _ptr(er), _ptr(ec)
+        else:
+            P.e_nnz, P.e_row, P.e_col = 0, None, None
         O = sdp_options()
         lib.sdp_default_options(C.byref(O))
         O.form, O.rho, O.device = FORM[form], float(rho), int(device)
@@ -233,6 +302,9 @@ class Solver:
         O.rank, O.world = int(rank), int(world)
         self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         O.nccl_id = C.cast(self._nccl_id, C.c_void_p) if self._nccl_id is not None else None
+        if self.allocator is not None:
+            O.allocator = C.pointer(self.allocator.struct)
+        O.comm = comm.h if comm is not None else None
         h = C.c_void_p()
         _check(lib.sdp_setup(C.byref(P), C.byref(O), C.byref(h)))
         self.h = h
@@ -290,8 +362,26 @@ class Solver:
     def y(self):
         return self._vec(VEC_Y, self._info["m"])
 
+    # the primal-dual SDP pair carried by the iterates (Remark 1; header: SDP_VEC_SDP_X)
+    def sdp_x(self):
+        """Unscaled entries X_ij of the SDP primal X on the pattern (canonical order)."""
+        return self._vec(VEC_SDP_X, self._info["N"])
+
+    def sdp_y(self):
+        """The SDP dual multipliers yhat."""
+        return self._vec(VEC_SDP_Y, self._info["m"])
+
+    def sdp_z(self):
+        """Stacked svec Agler blocks Z_k of the SDP dual slack (Theorem 2)."""
+        return self.blocks("sdp_z")
+
+    def workspace_bytes(self):
+        live, peak = C.c_int64(), C.c_int64()
+        _check(lib.sdp_workspace_bytes(self.h, C.byref(live), C.byref(peak)))
+        return int(live.value), int(peak.value)
+
     def blocks(self, which):
-        idx = {"xk": BLK_XK, "zk": BLK_XK, "lambda": BLK_LAMBDA, "vk": BLK_VK}[which]
+        idx = {"xk": BLK_XK, "zk": BLK_XK, "lambda": BLK_LAMBDA, "vk": BLK_VK, "sdp_z": BLK_SDP_Z}[which]
         out = np.empty(self._info["stot"])
         _check(lib.sdp_get_blocks(self.h, idx, _ptr(out)))
         return out
@@ -355,24 +445,42 @@ class Solver:
 class PsdPlan:
     """sdp_psd_plan_create / sdp_project_psd_batch (packed upper, unscaled)."""
 
-    def __init__(self, sizes, device=0):
+    def __init__(self, sizes, device=0, allocator=None):
         self.sizes = _arr(sizes, np.int32)
+        self.device = int(device)
+        self.allocator = TorchAllocator() if allocator == "torch" else allocator
         h = C.c_void_p()
-        _check(lib.sdp_psd_plan_create(self.sizes.size, _ptr(self.sizes), int(device), C.byref(h)))
+        al = C.pointer(self.allocator.struct) if self.allocator is not None else None
+        _check(lib.sdp_psd_plan_create_ex(self.sizes.size, _ptr(self.sizes), self.device, al, C.byref(h)))
         self.h = h
         self.values = int(lib.sdp_psd_plan_values(h))
         self.launches = int(lib.sdp_psd_plan_launches(h))
 
+    def _dev(self, t, name):
+        """Device pointer of an int (trusted) or a torch tensor (checked: CUDA, float64, contiguous,
+        at least plan.values elements)."""
+        if isinstance(t, int):
+            return t
+        if not (t.is_cuda and t.dtype.is_floating_point and t.element_size() == 8 and t.is_contiguous()):
+            raise ValueError(f"{name}: need a contiguous float64 CUDA tensor")
+        if t.numel() < self.values:
+            raise ValueError(f"{name}: {t.numel()} elements < plan.values = {self.values}")
+        return int(t.data_ptr())
+
     def project(self, d_in, d_out, stream=None):
         """d_in, d_out: device pointers (int) or torch CUDA float64 tensors."""
-        pin = d_in if isinstance(d_in, int) else int(d_in.data_ptr())
-        pout = d_out if isinstance(d_out, int) else int(d_out.data_ptr())
+        pin, pout = self._dev(d_in, "d_in"), self._dev(d_out, "d_out")
         _check(lib.sdp_project_psd_batch(self.h, pin, pout, _stream_ptr(stream)))
 
     def project_host(self, h_in, h_out=None, stream=None):
-        h_in = _arr(h_in, np.float64)
+        h_in = _arr(h_in, np.float64).reshape(-1)
+        if h_in.size != self.values:
+            raise ValueError(f"h_in has {h_in.size} values, the plan needs {self.values}")
         if h_out is None:
             h_out = np.empty_like(h_in)
+        if not (isinstance(h_out, np.ndarray) and h_out.dtype == np.float64 and h_out.flags.c_contiguous
+                and h_out.size == self.values):
+            raise ValueError("h_out must be a C-contiguous float64 array of plan.values elements")
         _check(lib.sdp_project_psd_batch_host(self.h, _ptr(h_in), h_out.ctypes.data_as(C.c_void_p),
                                               _stream_ptr(stream)))
         return h_out

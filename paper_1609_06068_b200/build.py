@@ -12,7 +12,7 @@ OUT = os.path.join(HERE, "libchordal_sdp.so")
 BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 SOURCES = ["api.cu", "kernels_psd.cu", "kernels_psd_rv.cu", "kernels_psd_giant.cu", "kernels_psd_trd.cu", "kernels_psd_wj.cu", "kernels_psd_gtrd.cu", "kernels_vec.cu", "setup_host.cpp", "completion.cpp", "shard.cpp",
-           "nccl_dl.cpp"]
+           "nccl_dl.cpp", "comm.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp,-O3", "--expt-relaxed-constexpr"]
 
@@ -20,7 +20,7 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp,-O3", "
 def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, src + ".o")
     srcp = os.path.join(CSRC, src)
-    deps = [srcp] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".h")]
+    deps = [srcp] + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".h", ".cuh"))]
     deps.append(os.path.join(HERE, "..", "include", "chordal_sdp.h"))
     if os.path.exists(obj) and all(os.path.getmtime(obj) >= os.path.getmtime(d) for d in deps):
         return obj

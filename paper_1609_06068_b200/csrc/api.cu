@@ -24,14 +24,39 @@ namespace {
 constexpr double kSqrt2 = 1.41421356237309504880;
 constexpr long long kHistCap = 1 << 20;
 
+// Every device buffer of a handle / plan: cudaMalloc, or the caller's allocator
+// (sdp_options.allocator: e.g. torch uint8 tensors, so that PyTorch owns the memory).
 struct Alloc {
-  std::vector<void*> ptrs;
+  std::vector<std::pair<void*, size_t>> ptrs;
+  sdp_allocator hook{};
+  bool has_hook = false;
+  int device = 0;
+  int64_t live = 0, peak = 0;
+  void set_hook(const sdp_allocator* a, int dev) {
+    device = dev;
+    has_hook = a && a->alloc && a->free;
+    if (has_hook) hook = *a;
+  }
+  void* raw(size_t bytes) {
+    bytes = std::max<size_t>(bytes, 1);
+    void* p = nullptr;
+    if (has_hook) {
+      p = hook.alloc(hook.ctx, bytes, device);
+      if (!p)
+        throw Error{SDP_E_OOM, "allocator returned NULL for " + std::to_string(bytes) + " bytes"};
+      if ((uintptr_t)p % 256)
+        throw Error{SDP_E_INVALID_ARG, "allocator returned a pointer not aligned to 256 bytes"};
+    } else {
+      SDP_CUDA_TRY(cudaMalloc(&p, bytes));
+    }
+    ptrs.push_back({p, bytes});
+    live += (int64_t)bytes;
+    peak = std::max(peak, live);
+    return p;
+  }
   template <class T>
   T* get(size_t n) {
-    void* p = nullptr;
-    SDP_CUDA_TRY(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-    ptrs.push_back(p);
-    return (T*)p;
+    return (T*)raw(std::max<size_t>(n, 1) * sizeof(T));
   }
   template <class T>
   T* zeros(size_t n) {
@@ -46,16 +71,25 @@ struct Alloc {
     if (!v.empty()) SDP_CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
     return p;
   }
-  void release(void* p) {
-    auto it = std::find(ptrs.begin(), ptrs.end(), p);
-    if (it != ptrs.end()) {
+  void free_one(void* p) {
+    if (has_hook)
+      hook.free(hook.ctx, p, device);
+    else
       cudaFree(p);
+  }
+  void release(void* p) {
+    auto it = std::find_if(ptrs.begin(), ptrs.end(), [&](const std::pair<void*, size_t>& q) { return q.first == p; });
+    if (it != ptrs.end()) {
+      cudaDeviceSynchronize();
+      free_one(p);
+      live -= (int64_t)it->second;
       ptrs.erase(it);
     }
   }
   void free_all() {
-    for (void* p : ptrs) cudaFree(p);
+    for (auto& q : ptrs) free_one(q.first);
     ptrs.clear();
+    live = 0;
   }
 };
 
@@ -177,6 +211,9 @@ struct Pipe {
   // settle() puts them back before the state is read or changed through the API
   bool pending = false;
   double *x_save = nullptr, *y_save = nullptr;
+  // dual form: the iteration index the next iteration's P_+(H1) reads (it runs concurrently with
+  // the current finalize, which advances the handle's counter)
+  long long* iter_next = nullptr;
   // dual form: scatter partials double-buffered by iteration parity (the next iteration's scatter
   // runs before the current finalize), dual-update partials per half
   int par = 0;
@@ -271,7 +308,7 @@ struct sdp_handle_s {
   cudaGraphExec_t exec = nullptr;
   // sharding: this rank's local view
   int world = 1, rank = 0;
-  void* comm = nullptr;         // ncclComm_t
+  Comm* comm = nullptr;         // NCCL or in-process loopback (comm.cu)
   int64_t cb = 0, pl = 0, Nl = 0, stotl = 0;  // first clique, local cliques / coordinates / stacked length
   std::vector<int32_t> local_coords;
   bool coord_perm = false;      // world == 1 with a permuted local coordinate order (pipelined iteration)
@@ -616,7 +653,7 @@ void enqueue_scatter(sdp_handle h, cudaStream_t s) {
   launch_scatter(h->form, a, s);
   if (h->world > 1 && h->nshared > 0) {
     // exchange: partial sums of coordinates shared across ranks (allreduce #1)
-    nccl_allreduce_sum(h->comm, h->xbuf, 3 * (size_t)h->nshared, s);
+    h->comm->allreduce_sum(h->xbuf, 3 * (size_t)h->nshared, s);
     launch_shared_fixup(h->nshared, h->shared_local, h->xbuf, h->Dinv, h->own, h->rD, h->sprev, h->fix_part,
                         h->done, s);
   }
@@ -663,7 +700,7 @@ void enqueue_kkt(sdp_handle h, cudaStream_t s) {
   }
   if (shard) {
     // exchange: u = sum over ranks of A[:, owned] D^-1 r1 (allreduce #2), then - r2 (and / S_ii)
-    nccl_allreduce_sum(h->comm, h->u, (size_t)h->m, s);
+    h->comm->allreduce_sum(h->u, (size_t)h->m, s);
     launch_reduce_u(f, h->u, 1, h->m, h->b, h->rho, h->u, h->s_diag ? h->sdiag : nullptr, ydst, h->done, s);
   }
   if (!h->s_diag) {  // y = S^-1 u = W^T W u
@@ -712,7 +749,7 @@ void enqueue_finalize(sdp_handle h, cudaStream_t s, const double* scat_part = nu
     launch_finalize(h->form, 0, a, s);
   } else {
     launch_finalize(h->form, 1, a, s);
-    nccl_allreduce_sum(h->comm, h->red, 6, s);  // residual partials (allreduce #3)
+    h->comm->allreduce_sum(h->red, 6, s);  // residual partials (allreduce #3)
     launch_finalize(h->form, 2, a, s);
   }
 }
@@ -795,6 +832,7 @@ void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vect
     P.nb_u1 = update_blocks(off[p1]);
     P.nb_u2 = update_blocks(off[p] - off[p1]);
     P.upd_part = al.zeros<double>(3 * (size_t)(P.nb_u1 + P.nb_u2));
+    P.iter_next = al.zeros<long long>(1);
   }
   // the two halves keep the tiers of the full assignment (the warm-start layout depends on it)
   for (int hf = 0; hf < 2; ++hf) {
@@ -833,7 +871,7 @@ void pipe_symv_gemvT1(sdp_handle h, cudaStream_t s) {
                     P.gT_part, h->done, s, P.rows1);
 }
 
-void pipe_projection(sdp_handle h, int half, cudaStream_t s) {
+void pipe_projection(sdp_handle h, int half, cudaStream_t s, const long long* iter = nullptr) {
   const BucketSet& B = h->pipe.half[half];
   ProjArgs a{};
   a.off = h->d_off;
@@ -850,7 +888,7 @@ void pipe_projection(sdp_handle h, int half, cudaStream_t s) {
   a.done = h->done;
   a.vprev = h->vprev;
   a.voff = h->voff;
-  a.iter = h->iter;
+  a.iter = iter ? iter : h->iter;
   a.warm_period = h->warm_period;
   launch_tiers(a, h->form == SDP_FORM_PRIMAL ? PM_PRIMAL : PM_DUAL, B.d_ids, B.bcount, B.td, TierFork{}, s);
 }
@@ -972,8 +1010,10 @@ void pipe_enqueue_B(sdp_handle h, cudaStream_t s, bool with_A) {
 void pipe_dual_update_range(sdp_handle h, int half, cudaStream_t s) {
   const Pipe& P = h->pipe;
   const int64_t b = half ? P.soff1 : 0, e = half ? h->stotl : P.soff1;
+  // the H1 update also publishes iter + 1 for the next P_+(H1) (finalize waits for this kernel)
   launch_update_dual(e - b, h->G + b, h->x, h->xk + b, h->lam + b, h->vk + b, h->rho,
-                     P.upd_part + 3 * (half ? P.nb_u1 : 0), h->done, s);
+                     P.upd_part + 3 * (half ? P.nb_u1 : 0), h->done, s, half ? nullptr : h->iter,
+                     half ? nullptr : P.iter_next);
 }
 
 void pipe_dual_finalize(sdp_handle h, int par, cudaStream_t s) {
@@ -1006,7 +1046,7 @@ void pipe_dual_B(sdp_handle h, cudaStream_t s, bool with_A) {
   SDP_CUDA_TRY(cudaEventRecord(P.ev[2], P.sp));
   if (with_A) {
     P.par = cur ^ 1;  // iteration t+1 scatters into the other buffer
-    pipe_projection(h, 0, P.sp);
+    pipe_projection(h, 0, P.sp, P.iter_next);
     pipe_scatter(h, 0, P.sp);
     SDP_CUDA_TRY(cudaEventRecord(P.ev[3], P.sp));
     SDP_CUDA_TRY(cudaStreamWaitEvent(P.sg, P.ev[3], 0));
@@ -1216,7 +1256,8 @@ void destroy_handle(sdp_handle h) {
   if (h->exec) cudaGraphExecDestroy(h->exec);
   if (h->graph) cudaGraphDestroy(h->graph);
   h->alloc.free_all();
-  if (h->comm) nccl_comm_destroy(h->comm);
+  delete h->comm;
+  h->comm = nullptr;
   if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
   h->tiers.destroy();
   h->pipe.destroy();
@@ -1239,7 +1280,8 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   if (!(opt.rho > 0) || !std::isfinite(opt.rho)) throw Error{SDP_E_INVALID_ARG, "rho must be positive"};
   if (opt.form != SDP_FORM_PRIMAL && opt.form != SDP_FORM_DUAL) throw Error{SDP_E_INVALID_ARG, "bad form"};
   if (opt.world < 1 || opt.rank < 0 || opt.rank >= opt.world) throw Error{SDP_E_INVALID_ARG, "bad rank/world"};
-  if (opt.world > 1 && !opt.nccl_id) throw Error{SDP_E_INVALID_ARG, "world > 1 needs nccl_id (sdp_nccl_unique_id)"};
+  if (opt.world > 1 && !opt.nccl_id && !opt.comm)
+    throw Error{SDP_E_INVALID_ARG, "world > 1 needs nccl_id (sdp_nccl_unique_id) or a loopback comm"};
   if (!P->b) throw Error{SDP_E_INVALID_ARG, "b is NULL"};
   if (P->c_nnz < 0 || (P->c_nnz > 0 && (!P->c_row || !P->c_col || !P->c_val)))
     throw Error{SDP_E_INVALID_ARG, "C arrays missing"};
@@ -1296,7 +1338,10 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->own_stream = false;
   h->world = opt.world;
   h->rank = opt.rank;
-  if (h->world > 1) h->comm = nccl_comm_init(opt.nccl_id, h->world, h->rank);  // collective
+  h->alloc.set_hook(opt.allocator, opt.device);
+  if (h->world > 1)  // collective
+    h->comm = opt.comm ? make_loop_comm(opt.comm, h->world, h->rank) : make_nccl_comm(opt.nccl_id, h->world, h->rank);
+  if (h->comm && h->comm->loopback()) h->use_graph = 0;  // capture cannot cross the ranks' streams
   SDP_CUDA_TRY(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
   h->tiers.create();
   const int64_t N = (int64_t)cr.coord_row.size();
@@ -1512,7 +1557,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     double* dS = al.get<double>((size_t)m * m);
     launch_syrk_dense(h->A, h->lda, m, h->Dinv, dS, nullptr);
     SDP_CUDA_TRY(cudaGetLastError());
-    if (h->world > 1) nccl_allreduce_sum(h->comm, dS, (size_t)m * m, nullptr);  // S = sum of owned-column parts
+    if (h->world > 1) h->comm->allreduce_sum(dS, (size_t)m * m, nullptr);  // S = sum of owned-column parts
     S.resize((size_t)m * m);
     SDP_CUDA_TRY(cudaMemcpy(S.data(), dS, S.size() * sizeof(double), cudaMemcpyDeviceToHost));
     al.release(dS);
@@ -1660,13 +1705,12 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
 
 // Sum a host vector over the ranks (getters of a sharded handle; collective).
 void allreduce_host(sdp_handle h, std::vector<double>& v) {
-  double* d = nullptr;
-  SDP_CUDA_TRY(cudaMalloc(&d, std::max<size_t>(v.size(), 1) * sizeof(double)));
+  double* d = h->alloc.get<double>(v.size());
   SDP_CUDA_TRY(cudaMemcpy(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
-  nccl_allreduce_sum(h->comm, d, v.size(), h->stream);
+  h->comm->allreduce_sum(d, v.size(), h->stream);
   SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
   SDP_CUDA_TRY(cudaMemcpy(v.data(), d, v.size() * sizeof(double), cudaMemcpyDeviceToHost));
-  cudaFree(d);
+  h->alloc.release(d);
 }
 
 void fill_info(sdp_handle h, sdp_info* info) {
@@ -1772,6 +1816,8 @@ void sdp_default_options(sdp_options* opt) {
   opt->rank = 0;
   opt->world = 1;
   opt->nccl_id = nullptr;
+  opt->allocator = nullptr;
+  opt->comm = nullptr;
   opt->adapt_rho = 0;
   opt->adapt_mu = 10.0;
   opt->adapt_tau = 2.0;
@@ -1898,7 +1944,7 @@ int sdp_get_vector(sdp_handle h, int32_t which, double* out) {
     DeviceGuard dg(h->device);
     settle(h);
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    if (which == SDP_VEC_X || which == SDP_VEC_XMAT) {
+    if (which == SDP_VEC_X || which == SDP_VEC_XMAT || which == SDP_VEC_SDP_X) {
       if (h->world == 1 && !h->coord_perm) {
         SDP_CUDA_TRY(cudaMemcpy(out, h->x, h->N * sizeof(double), cudaMemcpyDeviceToHost));
       } else if (h->world == 1) {  // local order = a permutation of the canonical one
@@ -1915,11 +1961,17 @@ int sdp_get_vector(sdp_handle h, int32_t which, double* out) {
         allreduce_host(h, full);
         std::memcpy(out, full.data(), h->N * sizeof(double));
       }
-      if (which == SDP_VEC_XMAT)
+      if (which != SDP_VEC_X)
         for (int64_t t = 0; t < h->N; ++t)
           if (h->coord_row[t] != h->coord_col[t]) out[t] /= kSqrt2;
-    } else if (which == SDP_VEC_Y) {
+      // recovered SDP primal (Remark 1): X = x (Alg. 1), X = -rho x (Alg. 2)
+      if (which == SDP_VEC_SDP_X && h->form == SDP_FORM_DUAL)
+        for (int64_t t = 0; t < h->N; ++t) out[t] *= -h->rho;
+    } else if (which == SDP_VEC_Y || which == SDP_VEC_SDP_Y) {
       SDP_CUDA_TRY(cudaMemcpy(out, h->y, h->m * sizeof(double), cudaMemcpyDeviceToHost));
+      // recovered SDP dual: yhat = -rho y (Alg. 1), yhat = y (Alg. 2)
+      if (which == SDP_VEC_SDP_Y && h->form == SDP_FORM_PRIMAL)
+        for (int i = 0; i < h->m; ++i) out[i] *= -h->rho;
     } else {
       throw Error{SDP_E_INVALID_ARG, "unknown vector id"};
     }
@@ -1941,7 +1993,7 @@ int sdp_complete_x(sdp_handle h, double rtol, double* out) {
     if (!(rtol >= 0.0)) throw Error{SDP_E_INVALID_ARG, "rtol must be >= 0"};
     const int32_t n = (int32_t)h->n;
     std::vector<double> xm(h->N);
-    const int rc = sdp_get_vector(h, SDP_VEC_XMAT, xm.data());  // matrix entries, canonical order
+    const int rc = sdp_get_vector(h, SDP_VEC_SDP_X, xm.data());  // SDP X entries, canonical order (both forms)
     if (rc != SDP_OK) return rc;
     std::vector<uint8_t> known((size_t)n * n, 0);
     for (int64_t i = 0; i < (int64_t)n * n; ++i) out[i] = 0.0;
@@ -1960,6 +2012,9 @@ int sdp_get_blocks(sdp_handle h, int32_t which, double* out) {
     if (!h || !out) throw Error{SDP_E_INVALID_ARG, "NULL argument"};
     DeviceGuard dg(h->device);
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+    // SDP_BLK_SDP_Z: the Agler blocks Z_k of the recovered dual slack (Theorem 2): lambda_k in the
+    // primal form, z_k in the dual form (Remark 1)
+    if (which == SDP_BLK_SDP_Z) which = h->form == SDP_FORM_PRIMAL ? SDP_BLK_LAMBDA : SDP_BLK_XK;
     const double* src = which == SDP_BLK_XK ? h->xk : which == SDP_BLK_LAMBDA ? h->lam : which == SDP_BLK_VK ? h->vk : nullptr;
     if (!src) throw Error{SDP_E_INVALID_ARG, "unknown block id"};
     if (h->world == 1) {
@@ -2045,8 +2100,24 @@ int sdp_profile_phases(sdp_handle h, int32_t iters, double* out_ms) {
 }
 
 namespace {
-constexpr int64_t kStateMagic = 0x3154415453504453ll;  // "SDPSTAT1"
-constexpr int kStateHeader = 16;                      // int64 words
+constexpr int64_t kStateMagic = 0x3254415453504453ll;  // "SDPSTAT2"
+constexpr int kStateHeader = 20;                      // int64 words
+// FNV-1a over the local coordinate order (the layout of x, r1/D and sprev in the blob: a
+// permutation of the canonical order that depends on the pipelined split)
+int64_t layout_hash(sdp_handle h) {
+  uint64_t x = 1469598103934665603ull;
+  auto mix = [&](uint64_t v) {
+    for (int b = 0; b < 8; ++b) {
+      x ^= (v >> (8 * b)) & 0xff;
+      x *= 1099511628211ull;
+    }
+  };
+  mix((uint64_t)h->Nl);
+  for (int32_t t : h->local_coords) mix((uint64_t)(uint32_t)t);
+  mix((uint64_t)h->cb);
+  mix((uint64_t)h->pl);
+  return (int64_t)(x & 0x7fffffffffffffffull);
+}
 struct StateLayout {
   int64_t stot, lda, m, vlen, hrows;
   int64_t words() const { return kStateHeader + 3 * stot + 3 * lda + m + 4 + 3 * hrows + vlen; }
@@ -2105,6 +2176,8 @@ int sdp_save_state(sdp_handle h, void* host_out, int64_t capacity) {
     hd[13] = h->N;
     hd[14] = h->p;
     hd[15] = h->coord_perm ? 1 : 0;  // coordinate layout of x, r1/D, sprev
+    hd[16] = layout_hash(h);         // ... and the exact order
+    hd[17] = h->pipe.on ? h->pipe.p1 : 0;
     double* w = reinterpret_cast<double*>(hd + kStateHeader);
     auto get = [&](const double* dev, int64_t n) {
       if (n) SDP_CUDA_TRY(cudaMemcpy(w, dev, n * sizeof(double), cudaMemcpyDeviceToHost));
@@ -2136,8 +2209,9 @@ int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes) {
     if (hd[1] != h->form || hd[2] != h->world || hd[3] != h->rank || hd[4] != L.stot || hd[5] != L.lda ||
         hd[6] != L.m || hd[7] != L.vlen || hd[8] != L.hrows || hd[13] != h->N || hd[14] != h->p)
       throw Error{SDP_E_INVALID_ARG, "state blob is from a different problem, form or sharding"};
-    if (hd[15] != (h->coord_perm ? 1 : 0))
-      throw Error{SDP_E_INVALID_ARG, "state blob has a different coordinate layout (SDP_PIPELINE differs)"};
+    if (hd[15] != (h->coord_perm ? 1 : 0) || hd[16] != layout_hash(h) || hd[17] != (h->pipe.on ? h->pipe.p1 : 0))
+      throw Error{SDP_E_INVALID_ARG,
+                  "state blob has a different coordinate layout (SDP_PIPELINE / SDP_PIPE_SPLIT or the build differ)"};
     if (bytes < 8 * L.words()) throw Error{SDP_E_INVALID_ARG, "state blob truncated"};
     const double* w = reinterpret_cast<const double*>(hd + kStateHeader);
     auto put = [&](double* dev, int64_t n) {
@@ -2165,6 +2239,15 @@ int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes) {
     std::memcpy(&rho, &hd[12], 8);
     h->rho = rho;  // r1 / D was restored as saved: no rebuild from x_k, lambda_k
     rebuild_graph(h);
+    return SDP_OK;
+  });
+}
+
+int sdp_workspace_bytes(sdp_handle h, int64_t* live_bytes, int64_t* peak_bytes) {
+  return guarded([&] {
+    if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
+    if (live_bytes) *live_bytes = h->alloc.live;
+    if (peak_bytes) *peak_bytes = h->alloc.peak;
     return SDP_OK;
   });
 }
@@ -2203,6 +2286,11 @@ int sdp_chordal_cliques(int32_t n, int64_t nnz, const int32_t* row, const int32_
 }
 
 int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, sdp_psd_plan* out) {
+  return sdp_psd_plan_create_ex(count, h_sizes, device, nullptr, out);
+}
+
+int sdp_psd_plan_create_ex(int64_t count, const int32_t* h_sizes, int32_t device, const sdp_allocator* allocator,
+                           sdp_psd_plan* out) {
   sdp_psd_plan pl = nullptr;
   int rc = guarded([&] {
     if (!out) throw Error{SDP_E_INVALID_ARG, "out is NULL"};
@@ -2216,6 +2304,7 @@ int sdp_psd_plan_create(int64_t count, const int32_t* h_sizes, int32_t device, s
     pl = new sdp_psd_plan_s();
     pl->device = device;
     pl->count = count;
+    pl->alloc.set_hook(allocator, device);
     std::vector<int64_t> off(count + 1, 0);
     std::vector<int32_t> ksz(h_sizes, h_sizes + count);
     for (int64_t i = 0; i < count; ++i) {

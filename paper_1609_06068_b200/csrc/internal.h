@@ -63,6 +63,17 @@ void* nccl_comm_init(const void* id128, int world, int rank);
 void nccl_allreduce_sum(void* comm, double* buf, size_t count, cudaStream_t s);
 void nccl_comm_destroy(void* comm);
 
+// Communicator of a sharded handle (comm.cu): in-place sum all-reduce of a device buffer on a
+// stream; NCCL across processes or the in-process loopback group (sdp_loopback_create).
+struct Comm {
+  int world = 1, rank = 0;
+  virtual ~Comm() {}
+  virtual void allreduce_sum(double* buf, size_t n, cudaStream_t s) = 0;
+  virtual bool loopback() const { return false; }
+};
+Comm* make_nccl_comm(const void* id128, int world, int rank);
+Comm* make_loop_comm(void* group, int world, int rank);
+
 // ---------------------------------------------------------------- projection buckets
 // Kernel tiers for the batched eigen-projection (kernels_psd.cu).
 enum BucketKind {

@@ -375,7 +375,11 @@ __global__ void __launch_bounds__(256) k_gemvT_csc(const int32_t* __restrict__ c
 __global__ void __launch_bounds__(256) k_update_dual(int64_t stot, const int32_t* __restrict__ G,
                                                       const double* __restrict__ x, const double* __restrict__ z,
                                                       double* __restrict__ lam, double* __restrict__ v, double rho,
-                                                      double* __restrict__ part, const int* done) {
+                                                      double* __restrict__ part, const int* done,
+                                                      const long long* iter_in, long long* iter_out) {
+  // iter_out = iter_in + 1: the iteration index of the next projection, published before the
+  // current finalize can run (pipelined dual schedule, api.cu pipe_dual_B)
+  if (iter_out && blockIdx.x == 0 && threadIdx.x == 0) *iter_out = *iter_in + 1;
   if (done && *done) return;
   __shared__ double sm[3 * 8];
   const int64_t s = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -738,9 +742,11 @@ void launch_gemvT_csc(int form, const int32_t* cp, const int32_t* ri, const doub
 int update_blocks(int64_t stot) { return (int)((stot + 255) / 256); }
 
 void launch_update_dual(int64_t stot, const int32_t* G, const double* x, const double* z, double* lam, double* v,
-                        double rho, double* part, const int* done, cudaStream_t s) {
-  if (stot <= 0) return;
-  k_update_dual<<<update_blocks(stot), 256, 0, s>>>(stot, G, x, z, lam, v, rho, part, done);
+                        double rho, double* part, const int* done, cudaStream_t s, const long long* iter_in,
+                        long long* iter_out) {
+  if (stot <= 0 && !iter_out) return;
+  k_update_dual<<<std::max(1, update_blocks(stot)), 256, 0, s>>>(stot, G, x, z, lam, v, rho, part, done, iter_in,
+                                                                 iter_out);
 }
 
 void launch_finalize(int form, int phase, const FinalArgs& a, cudaStream_t s) {

@@ -77,8 +77,10 @@ void launch_gemvT_csc(int form, const int32_t* cp, const int32_t* ri, const doub
                       const double* rD, const double* Dinv, const double* c, const double* own, double* x,
                       double* part, const int* done, cudaStream_t s);
 int update_blocks(int64_t stot);
+// iter_out (optional): *iter_out = *iter_in + 1 written by the kernel (next projection's iteration index)
 void launch_update_dual(int64_t stot, const int32_t* G, const double* x, const double* z, double* lam, double* v,
-                        double rho, double* part, const int* done, cudaStream_t s);
+                        double rho, double* part, const int* done, cudaStream_t s,
+                        const long long* iter_in = nullptr, long long* iter_out = nullptr);
 void launch_finalize(int form, int phase, const FinalArgs& a, cudaStream_t s);
 int fixup_blocks(int nshared);
 void launch_shared_fixup(int nshared, const int32_t* shared_local, double* xbuf, const double* Dinv,

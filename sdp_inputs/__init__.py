@@ -42,6 +42,10 @@ class Problem:
     a_col: Optional[np.ndarray] = None
     a_val: Optional[np.ndarray] = None  # coo: (nnz,), dense: (m, npat)
     meta: dict = field(default_factory=dict)
+    # optional user sparsity pattern E ("described by the graph G(V,E)"): upper entries
+    # that belong to the pattern even though C and every A_i are zero there
+    e_row: Optional[np.ndarray] = None
+    e_col: Optional[np.ndarray] = None
 
     def a_support(self):
         """(row, col) arrays of every structurally present A entry (may repeat across cons)."""

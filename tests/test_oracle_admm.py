@@ -210,3 +210,37 @@ def test_adaptive_rho_reaches_same_optimum(gen):
     assert s1 == "solved" and s2 == "solved"
     assert abs(adapt.objective - fixed.objective) <= 1e-4 * abs(fixed.objective)
     assert adapt.rho != 50.0
+
+
+def test_user_pattern_E(gen):
+    """Optional user pattern E ("described by the graph G(V,E)"): its entries join the
+    aggregate pattern even where C and every A_i vanish.  With E = all pairs the chordal
+    extension is complete (p = 1, the undecomposed cone); with E = one extra edge between two
+    diagonal blocks the extension and cliques change (checked against brute force) while the
+    SDP optimum does not (Theorems 1-2: the decomposition is exact for any chordal pattern
+    containing the aggregate one)."""
+    from tests.helpers import adj_from_edges, is_chordal_bruteforce, maximal_cliques_bruteforce
+    prob = gen.block_arrow(3, 3, 2, 6, seed=0)
+    n = prob.n
+    base = dc.decompose(prob)
+    st0, status = admm.solve(base, 1.0, "primal", 1e-9, 30000)
+    assert status == "solved"
+    iu, ju = np.triu_indices(n, 1)
+    full = gen.block_arrow(3, 3, 2, 6, seed=0)
+    full.e_row, full.e_col = iu.astype(np.int32), ju.astype(np.int32)
+    dfull = dc.decompose(full)
+    assert dfull.p == 1 and dfull.N == n * (n + 1) // 2
+    one = gen.block_arrow(3, 3, 2, 6, seed=0)
+    one.e_row, one.e_col = np.array([0], np.int32), np.array([3], np.int32)   # block 0 - block 1
+    done = dc.decompose(one)
+    adj = chordal.aggregate_adjacency(one)
+    assert adj[0, 3] and not chordal.aggregate_adjacency(prob)[0, 3]
+    pat = [(int(i), int(j)) for i, j in zip(done.coord_row, done.coord_col) if i != j]
+    A2 = adj_from_edges(n, pat)
+    assert is_chordal_bruteforce(A2)
+    assert [tuple(c.tolist()) for c in done.cliques] == maximal_cliques_bruteforce(A2)
+    assert [c.tolist() for c in done.cliques] != [c.tolist() for c in base.cliques]
+    for d in (dfull, done):
+        st, status = admm.solve(d, 1.0, "primal", 1e-9, 30000)
+        assert status == "solved"
+        assert abs(st.objective - st0.objective) <= 1e-6 * abs(st0.objective)
