@@ -93,32 +93,66 @@ struct Alloc {
   }
 };
 
-// Host Cholesky S = L L^T (row-major, lower).  Returns false if S is not
-// numerically positive definite (pivot <= 1e-12 * S_ii).
+// Host Cholesky S = L L^T (row-major, lower), blocked right-looking with the panel solve and the
+// trailing update spread over the host threads (OpenMP).  Returns false if S is not numerically
+// positive definite (a pivot <= 1e-12 * the original S_ii).
 bool cholesky_host(std::vector<double>& S, int m) {
-  for (int i = 0; i < m; ++i) {
-    double* Li = S.data() + (size_t)i * m;
-    for (int j = 0; j <= i; ++j) {
-      const double* Lj = S.data() + (size_t)j * m;
-      double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-      int k = 0;
-      for (; k + 4 <= j; k += 4) {
-        a0 += Li[k] * Lj[k];
-        a1 += Li[k + 1] * Lj[k + 1];
-        a2 += Li[k + 2] * Lj[k + 2];
-        a3 += Li[k + 3] * Lj[k + 3];
-      }
-      for (; k < j; ++k) a0 += Li[k] * Lj[k];
-      const double s = Li[j] - ((a0 + a1) + (a2 + a3));
-      if (i == j) {
-        if (!(s > 1e-12 * Li[i]) || !std::isfinite(s)) return false;
-        Li[i] = std::sqrt(s);
-      } else {
-        Li[j] = s / Lj[j];
+  constexpr int NB = 64;
+  std::vector<double> diag0(m);
+  for (int i = 0; i < m; ++i) diag0[i] = S[(size_t)i * m + i];
+  auto dot = [](const double* a, const double* b, int n) {
+    double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+    int k = 0;
+    for (; k + 4 <= n; k += 4) {
+      a0 += a[k] * b[k];
+      a1 += a[k + 1] * b[k + 1];
+      a2 += a[k + 2] * b[k + 2];
+      a3 += a[k + 3] * b[k + 3];
+    }
+    for (; k < n; ++k) a0 += a[k] * b[k];
+    return (a0 + a1) + (a2 + a3);
+  };
+  bool ok = true;
+  for (int k0 = 0; k0 < m && ok; k0 += NB) {
+    const int k1 = std::min(m, k0 + NB);
+    // diagonal block (the columns < k0 were applied by the trailing updates)
+    for (int i = k0; i < k1 && ok; ++i) {
+      double* Li = S.data() + (size_t)i * m;
+      for (int j = k0; j <= i; ++j) {
+        const double* Lj = S.data() + (size_t)j * m;
+        const double sv = Li[j] - dot(Li + k0, Lj + k0, j - k0);
+        if (i == j) {
+          if (!(sv > 1e-12 * diag0[i]) || !std::isfinite(sv)) {
+            ok = false;
+            break;
+          }
+          Li[i] = std::sqrt(sv);
+        } else {
+          Li[j] = sv / Lj[j];
+        }
       }
     }
-    for (int j = i + 1; j < m; ++j) Li[j] = 0.0;
+    if (!ok) break;
+    // panel rows i >= k1: L[i][k0:k1] = A[i][k0:k1] L11^-T
+#pragma omp parallel for schedule(static)
+    for (int i = k1; i < m; ++i) {
+      double* Li = S.data() + (size_t)i * m;
+      for (int j = k0; j < k1; ++j) {
+        const double* Lj = S.data() + (size_t)j * m;
+        Li[j] = (Li[j] - dot(Li + k0, Lj + k0, j - k0)) / Lj[j];
+      }
+    }
+    // trailing update of the lower part: A[i][j] -= L[i][k0:k1] . L[j][k0:k1], k1 <= j <= i
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int i = k1; i < m; ++i) {
+      double* Li = S.data() + (size_t)i * m;
+      for (int j = k1; j <= i; ++j) Li[j] -= dot(Li + k0, S.data() + (size_t)j * m + k0, k1 - k0);
+    }
   }
+  if (!ok) return false;
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < m; ++i)
+    for (int j = i + 1; j < m; ++j) S[(size_t)i * m + j] = 0.0;
   return true;
 }
 
@@ -316,6 +350,7 @@ struct sdp_handle_s {
   int nshared = 0, n_fix = 0;
   int32_t *shared_idx = nullptr, *shared_local = nullptr;
   double *xbuf = nullptr, *fix_part = nullptr, *red = nullptr;
+  double* prevall = nullptr;    // packed primal exchange: previous sums of every shared coordinate
 };
 
 struct sdp_psd_plan_s {
@@ -414,26 +449,47 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
   // the smaller ones 8 per cluster (one CTA each), largest first
   const char* cm = getenv("SDP_GTRD_COOP_MIN");
   const int coop_min = cm ? std::max(1, atoi(cm)) : 200;
+  // two-stage reduction (dense -> band -> tridiagonal) for orders >= SDP_GTRD_SBR_MIN; default off
+  // (0): measured slower than the one-stage reduction on B200 ("two-stage")
+  const char* sm = getenv("SDP_GTRD_SBR_MIN");
+  int sbr_min = sm ? atoi(sm) : 0;
+  if (sbr_min <= 0) sbr_min = 1 << 30;
+  gt.sbr_min = sbr_min;
   std::vector<int> order(ng);
   std::iota(order.begin(), order.end(), 0);
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return ksz[ids[x]] > ksz[ids[y]]; });
-  std::vector<int32_t> job_g, job_coop;
-  std::vector<int> solo;
+  std::vector<int32_t> job_g, job_coop, job2_g, job2_coop, sb_g;
+  std::vector<int> solo, solo2;
   for (int g : order) {
-    if (ksz[ids[g]] >= coop_min) {
-      job_coop.push_back(1);
-      for (int r = 0; r < 8; ++r) job_g.push_back(r == 0 ? g : -1);
+    const int kk = ksz[ids[g]];
+    const bool two = kk >= sbr_min && kk <= kcap;
+    std::vector<int32_t>& jg = two ? job2_g : job_g;
+    std::vector<int32_t>& jc = two ? job2_coop : job_coop;
+    if (two) sb_g.push_back(g);
+    if (kk >= coop_min) {
+      jc.push_back(1);
+      for (int r = 0; r < 8; ++r) jg.push_back(r == 0 ? g : -1);
     } else {
-      solo.push_back(g);
+      (two ? solo2 : solo).push_back(g);
     }
   }
-  for (size_t i = 0; i < solo.size(); i += 8) {
-    job_coop.push_back(0);
-    for (size_t r = 0; r < 8; ++r) job_g.push_back(i + r < solo.size() ? solo[i + r] : -1);
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<int>& so = pass ? solo2 : solo;
+    std::vector<int32_t>& jg = pass ? job2_g : job_g;
+    std::vector<int32_t>& jc = pass ? job2_coop : job_coop;
+    for (size_t i = 0; i < so.size(); i += 8) {
+      jc.push_back(0);
+      for (size_t r = 0; r < 8; ++r) jg.push_back(i + r < so.size() ? so[i + r] : -1);
+    }
   }
   gt.njob = (int)job_coop.size();
-  gt.job_g = al.upload(job_g);
-  gt.job_coop = al.upload(job_coop);
+  gt.job_g = job_g.empty() ? nullptr : al.upload(job_g);
+  gt.job_coop = job_coop.empty() ? nullptr : al.upload(job_coop);
+  gt.njob2 = (int)job2_coop.size();
+  gt.job2_g = job2_g.empty() ? nullptr : al.upload(job2_g);
+  gt.job2_coop = job2_coop.empty() ? nullptr : al.upload(job2_coop);
+  gt.nsb = (int)sb_g.size();
+  gt.sb_g = sb_g.empty() ? nullptr : al.upload(sb_g);
   gt.ng = ng;
   gt.kmax = std::max(kmax, 1);
   gt.task = al.upload(ids);
@@ -632,6 +688,14 @@ void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
   launch_tiers(a, mode, h->d_ids, h->bcount, h->td, h->tiers, s);
 }
 
+FinalArgs final_args(sdp_handle h);
+
+// Sharded primal iteration: the residual partials of the rank (projection, scatter,
+// objective) ride in the tail of the shared-coordinate exchange (allreduce #1), and the
+// shared-coordinate eps_d partials are then computed identically on every rank from a replicated
+// copy of the previous sums, so the iteration needs two all-reduces (#1 and u), not three.
+bool packed_exchange(sdp_handle h) { return h->world > 1 && h->form == SDP_FORM_PRIMAL; }
+
 void enqueue_scatter(sdp_handle h, cudaStream_t s) {
   ScatterArgs a{};
   a.N = (int)h->Nl;
@@ -651,7 +715,15 @@ void enqueue_scatter(sdp_handle h, cudaStream_t s) {
   a.part = h->scat_part;
   a.done = h->done;
   launch_scatter(h->form, a, s);
-  if (h->world > 1 && h->nshared > 0) {
+  if (packed_exchange(h)) {
+    FinalArgs fa = final_args(h);
+    fa.n_fix = 0;
+    fa.red = h->xbuf + 3 * (size_t)h->nshared;  // the 6 local residual partials
+    launch_finalize(h->form, 1, fa, s);
+    h->comm->allreduce_sum(h->xbuf, 3 * (size_t)h->nshared + 6, s);  // allreduce #1 (+ residual scalars)
+    launch_shared_fixup(h->nshared, h->shared_local, h->xbuf, h->Dinv, h->own, h->rD, h->sprev, h->fix_part,
+                        h->done, s, h->prevall);
+  } else if (h->world > 1 && h->nshared > 0) {
     // exchange: partial sums of coordinates shared across ranks (allreduce #1)
     h->comm->allreduce_sum(h->xbuf, 3 * (size_t)h->nshared, s);
     launch_shared_fixup(h->nshared, h->shared_local, h->xbuf, h->Dinv, h->own, h->rD, h->sprev, h->fix_part,
@@ -719,6 +791,33 @@ void enqueue_kkt(sdp_handle h, cudaStream_t s) {
                      h->done, s);
 }
 
+FinalArgs final_args(sdp_handle h) {
+  FinalArgs a{};
+  a.proj_part = h->proj_part;
+  a.n_proj = (int)h->pl;
+  a.fix_part = h->fix_part;
+  a.n_fix = h->world > 1 ? h->n_fix : 0;
+  a.red = h->red;
+  a.upd_part = h->upd_part;
+  a.n_upd = h->nb_upd;
+  a.scat_part = h->scat_part;
+  a.n_scat = h->nb_scat;
+  a.gT_part = h->gT_part;
+  a.n_gT = h->nb_gT;
+  a.b = h->b;
+  a.y = h->y;
+  a.m = h->m;
+  a.rho = h->rho;
+  a.res = h->res;
+  a.hist = h->hist;
+  a.hist_cap = kHistCap;
+  a.iter = h->iter;
+  a.done = h->done;
+  a.numerical = h->numerical;
+  a.tol = h->tol;
+  return a;
+}
+
 void enqueue_finalize(sdp_handle h, cudaStream_t s, const double* scat_part = nullptr, int n_scat = 0,
                       const double* gT_part = nullptr, int n_gT = 0, const double* upd_part = nullptr,
                       int n_upd = 0) {
@@ -747,6 +846,13 @@ void enqueue_finalize(sdp_handle h, cudaStream_t s, const double* scat_part = nu
   a.tol = h->tol;
   if (h->world == 1) {
     launch_finalize(h->form, 0, a, s);
+  } else if (packed_exchange(h)) {
+    // the rank partials were all-reduced with the scatter exchange; add the shared-coordinate
+    // partials (identical on every rank) and finish
+    a.red = h->xbuf + 3 * (size_t)h->nshared;
+    a.n_fix2 = h->n_fix;
+    a.n_fix = 0;
+    launch_finalize(h->form, 2, a, s);
   } else {
     launch_finalize(h->form, 1, a, s);
     h->comm->allreduce_sum(h->red, 6, s);  // residual partials (allreduce #3)
@@ -1185,7 +1291,7 @@ int launches_per_iter(sdp_handle h) {
   if (h->world > 1 && h->a_dense) n += 1;       // partial u of the rank before the all-reduce
   n += (h->form == SDP_FORM_DUAL) ? 1 : 0;      // dual update
   n += 1;                                       // finalize
-  if (h->world > 1) n += 2 + (h->nshared > 0 ? 1 : 0);  // second reduce_u, finalize phase 2, fixup
+  if (h->world > 1) n += 2 + (h->nshared > 0 ? 1 : 0);  // second reduce_u, finalize phase 2 (or packed phase 1), fixup
   return n;
 }
 
@@ -1219,7 +1325,8 @@ void reset_state(sdp_handle h) {
   SDP_CUDA_TRY(cudaMemsetAsync(h->xk, 0, h->stotl * sizeof(double), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->lam, 0, h->stotl * sizeof(double), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->vk, 0, h->stotl * sizeof(double), s));
-  if (h->xbuf) SDP_CUDA_TRY(cudaMemsetAsync(h->xbuf, 0, 3 * (size_t)h->nshared * sizeof(double), s));
+  if (h->xbuf) SDP_CUDA_TRY(cudaMemsetAsync(h->xbuf, 0, (3 * (size_t)h->nshared + 8) * sizeof(double), s));
+  if (h->prevall) SDP_CUDA_TRY(cudaMemsetAsync(h->prevall, 0, std::max(1, h->nshared) * sizeof(double), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->x, 0, h->lda * sizeof(double), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->rD, 0, h->lda * sizeof(double), s));
   SDP_CUDA_TRY(cudaMemsetAsync(h->sprev, 0, h->lda * sizeof(double), s));
@@ -1268,6 +1375,16 @@ void destroy_handle(sdp_handle h) {
 
 int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out) {
   auto t0 = std::chrono::steady_clock::now();
+  // SDP_SETUP_TRACE=1: wall time of the setup phases on stderr
+  const bool strace = getenv("SDP_SETUP_TRACE") != nullptr;
+  auto tlast = t0;
+  auto smark = [&](const char* what) {
+    if (!strace) return;
+    cudaDeviceSynchronize();
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[setup] %-28s %9.2f ms\n", what, std::chrono::duration<double>(now - tlast).count() * 1e3);
+    tlast = now;
+  };
   if (!out) throw Error{SDP_E_INVALID_ARG, "out is NULL"};
   *out = nullptr;
   if (!P) throw Error{SDP_E_INVALID_ARG, "problem is NULL"};
@@ -1307,6 +1424,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   if (opt.device < 0 || opt.device >= ndev) throw Error{SDP_E_INVALID_ARG, "bad device ordinal"};
   DeviceGuard dg(opt.device);
 
+  smark("validation");
   // ---- 1. aggregate pattern and chordal analysis
   std::vector<std::pair<int32_t, int32_t>> edges;
   edges.reserve((size_t)(P->c_nnz + P->a_nnz + P->e_nnz));
@@ -1353,6 +1471,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->chordal.later_idx = cr.later_idx;
   if (N >= (1ll << 31)) throw Error{SDP_E_INVALID_ARG, "pattern too large"};
 
+  smark("chordal analysis");
   // ---- 2. global layout: clique offsets, H_k maps, D, inverse map
   const int64_t p = (int64_t)cr.cliques.size();
   h->p = p;
@@ -1409,6 +1528,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     }
   }
 
+  smark("layout, maps, D");
   // ---- 3. shard plan and this rank's local view; identity when world == 1
   if (h->world > p) throw Error{SDP_E_INVALID_ARG, "more ranks than cliques"};
   ShardPlan sp;
@@ -1474,6 +1594,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     if (sp.shared_local[j] >= 0) shared_idx[sp.shared_local[j]] = j;
   h->n_long = (int)longc.size();
 
+  smark("shard plan / local view");
   // ---- 4. device uploads of the local layout
   Alloc& al = h->alloc;
   h->G = al.upload(Gl);
@@ -1499,7 +1620,10 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   if (h->nshared > 0) {
     h->shared_idx = al.upload(shared_idx);
     h->shared_local = al.upload(sp.shared_local);
-    h->xbuf = al.zeros<double>(3 * (size_t)h->nshared);
+  }
+  if (h->world > 1) {
+    h->xbuf = al.zeros<double>(3 * (size_t)h->nshared + 8);  // + the packed residual partials
+    h->prevall = al.zeros<double>((size_t)std::max(1, h->nshared));
   }
   h->n_fix = h->nshared > 0 ? fixup_blocks(h->nshared) : 0;
   h->fix_part = al.zeros<double>(2 * (size_t)std::max(1, h->n_fix));
@@ -1507,6 +1631,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   std::vector<int> task_bucket;
   build_buckets(al, kszl, h->d_ids, h->bcount, h->gd, h->td, &task_bucket);
 
+  smark("uploads, tiers");
   // ---- 5. A (svec rows) and S = A D^-1 A^T, factor cached once
   std::vector<double> S;
   if (P->a_fmt == SDP_A_DENSE_ON_PATTERN) {
@@ -1543,6 +1668,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
       al.release(dscale);
     }
     // A^T copy over every local coordinate (x is needed on all of them) ...
+    smark("A upload + placement");
     h->AT = al.zeros<double>((size_t)Nl * h->ldm);
     launch_transpose(h->A, h->lda, m, h->AT, h->ldm, Nl, nullptr);
     SDP_CUDA_TRY(cudaGetLastError());
@@ -1555,6 +1681,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     h->nchunks = (int)((h->lda + h->chunk - 1) / h->chunk);
     h->gemv_part = al.zeros<double>((size_t)h->nchunks * m);
     double* dS = al.get<double>((size_t)m * m);
+    smark("A^T copy");
     launch_syrk_dense(h->A, h->lda, m, h->Dinv, dS, nullptr);
     SDP_CUDA_TRY(cudaGetLastError());
     if (h->world > 1) h->comm->allreduce_sum(dS, (size_t)m * m, nullptr);  // S = sum of owned-column parts
@@ -1643,10 +1770,13 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
             S[(size_t)gri[e1] * m + gri[e2]] += gval[e1] * gval[e2] * Dinv_g[t];
     }
   }
+  smark("S = A D^-1 A^T (+ D2H)");
   if (!h->s_diag) {
     if (!cholesky_host(S, m)) throw Error{SDP_E_RANK_DEFICIENT, "S = A D^-1 A^T is not positive definite"};
+    smark("Cholesky (host)");
     std::vector<double> Wt;
     tri_inverse_T(S, m, Wt);
+    smark("L^-1 (host)");
     std::vector<double> Wl((size_t)m * m);
 #pragma omp parallel for
     for (int i = 0; i < m; ++i)
@@ -1668,6 +1798,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     symv_init_attributes(m);
   }
 
+  smark("A, S, factor, S^-1");
   // ---- 6. residual buffers, state, graph
   h->nb_scat = scatter_blocks((int)Nl, h->n_long);
   h->nb_gT = h->a_dense ? gemvT_rows_blocks(Nl) : gemvT_csc_blocks((int)Nl);
@@ -1699,6 +1830,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   SDP_CUDA_TRY(cudaDeviceSynchronize());
   reset_state(h);
   rebuild_graph(h);
+  smark("state, graphs");
   h->setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return SDP_OK;
 }
@@ -2119,8 +2251,8 @@ int64_t layout_hash(sdp_handle h) {
   return (int64_t)(x & 0x7fffffffffffffffull);
 }
 struct StateLayout {
-  int64_t stot, lda, m, vlen, hrows;
-  int64_t words() const { return kStateHeader + 3 * stot + 3 * lda + m + 4 + 3 * hrows + vlen; }
+  int64_t stot, lda, m, vlen, hrows, nprev;
+  int64_t words() const { return kStateHeader + 3 * stot + 3 * lda + m + 4 + 3 * hrows + vlen + nprev; }
 };
 StateLayout state_layout(sdp_handle h, long long iter) {
   StateLayout L;
@@ -2129,6 +2261,7 @@ StateLayout state_layout(sdp_handle h, long long iter) {
   L.m = h->m;
   L.vlen = h->vprev ? h->vprev_len : 0;
   L.hrows = std::min<long long>(iter, kHistCap);
+  L.nprev = h->prevall ? std::max(1, h->nshared) : 0;
   return L;
 }
 }  // namespace
@@ -2193,6 +2326,7 @@ int sdp_save_state(sdp_handle h, void* host_out, int64_t capacity) {
     get(h->res, 4);
     get(h->hist, 3 * L.hrows);
     get(h->vprev, L.vlen);
+    get(h->prevall, L.nprev);
     return SDP_OK;
   });
 }
@@ -2228,6 +2362,7 @@ int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes) {
     put(h->res, 4);
     put(h->hist, 3 * L.hrows);
     put(h->vprev, L.vlen);
+    put(h->prevall, L.nprev);
     const long long it = hd[9];
     const unsigned long long cap = (unsigned long long)hd[10], sw = (unsigned long long)hd[11];
     SDP_CUDA_TRY(cudaMemcpy(h->iter, &it, sizeof(it), cudaMemcpyHostToDevice));

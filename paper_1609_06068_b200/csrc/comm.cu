@@ -68,6 +68,7 @@ struct LoopGroup {
   double* scratch = nullptr;
   size_t cap = 0;
   bool first = true;
+  bool ok = true;  // rank 0's count check of the current call (read after the second barrier)
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const long long g = gen;
@@ -98,6 +99,7 @@ struct LoopComm final : Comm {
     bool ok = true;
     if (rank == 0) {
       for (int r = 0; r < world; ++r) ok &= G.counts[r] == n;
+      G.ok = ok;
       if (ok && n > 0) {
         for (int r = 0; r < world; ++r) {
           SDP_CUDA_TRY(cudaStreamWaitEvent(s, G.ready[r], 0));
@@ -120,7 +122,8 @@ struct LoopComm final : Comm {
       G.first = false;
     }
     G.barrier();
-    for (int r = 0; r < world; ++r) ok &= G.counts[r] == n;
+    // (counts[] may already hold a fast rank's next call here: use rank 0's verdict)
+    ok = G.ok;
     if (!ok) throw Error{SDP_E_INVALID_ARG, "loopback all-reduce: ranks passed different counts"};
     if (n > 0) {
       SDP_CUDA_TRY(cudaStreamWaitEvent(s, G.done, 0));

@@ -116,6 +116,13 @@ struct GtrdDev {
   const int32_t* rc_pre = nullptr;     // ng + 1: reconstruction tiles (32 x 32, upper)
   double* part = nullptr;              // 3 per reconstruction tile (primal residual partials)
   int tot_ev = 0, tot_vg = 0, tot_wy = 0, tot_bt = 0, tot_rc = 0;
+  // two-stage reduction (dense -> band -> tridiagonal) for orders >= sbr_min (SDP_GTRD_SBR_MIN)
+  int sbr_min = 1 << 30;
+  int njob2 = 0;                       // stage-A jobs (clusters of 8 CTAs, like job_g / job_coop)
+  const int32_t* job2_g = nullptr;
+  const int32_t* job2_coop = nullptr;
+  int nsb = 0;                         // stage-B CTAs: one per two-stage giant
+  const int32_t* sb_g = nullptr;
   int force_fallback = 0;              // SDP_GTRD_FORCE_FALLBACK=1: mark every matrix failed (tests)
   int debug = 0;                       // SDP_GTRD_DEBUG=1: per-matrix spectrum / cluster printf
 };

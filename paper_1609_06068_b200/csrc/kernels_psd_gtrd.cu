@@ -82,10 +82,18 @@ __device__ __forceinline__ double input_value(const ProjArgs& a, int64_t e, int 
   }
 }
 
+// two-stage reduction (section 1b): bandwidth of stage A = reflectors per panel
+constexpr int SB_NB = 8;
+// bulge-chasing reflectors of stage B: per sweep s, ceil((k - 1 - s) / SB_NB) reflectors of
+// SB_NB doubles (tau in slot 0, v_1 .. v_{NB-1} after it; v_0 = 1 implicit)
+__host__ __device__ inline int64_t q2_doubles(int k) { return (int64_t)k * k / 2 + (int64_t)k * SB_NB + 64; }
+
 // per-matrix workspace (doubles)
 struct GView {
   double* p;
   int k, H;
+  int ro = 1;  // row offset of the back-transform reflectors: v_j has its unit at row j + ro
+               // (1: one-stage dsytrd reflectors; SB_NB: stage-A panel reflectors of the two-stage path)
   __host__ __device__ static int ld_of(int k) { return (k + 3) & ~3; }
   __device__ int ld() const { return ld_of(k); }
   __device__ double* M() const { return p; }                        // full symmetric, row-major; v_j in row j
@@ -101,13 +109,67 @@ struct GView {
   __device__ double* hdr() const { return gsr() + H; }
   __device__ double* Z() const { return hdr() + 8; }               // selected vectors, column j at j * k
   __device__ double* iv() const { return Z() + (int64_t)k * H; }   // 3 x k x H LU factors + pivot words
-  __device__ int nwy() const { return (k - 2 + 15) / 16; }            // WY groups of 16 reflectors
+  __device__ int nref() const { return k - 1 - ro; }                 // reflectors j = 0 .. k - 2 - ro
+  __device__ int nwy() const { return (nref() + 15) / 16; }            // WY groups of 16 reflectors
   __device__ double* wyT() const { return iv() + 3 * (int64_t)k * H + ((k + 63) / 64) * (int64_t)H; }
+  __device__ double* Q2() const {  // stage-B reflectors (64-byte aligned: written by bulk async copies)
+    const uintptr_t raw = reinterpret_cast<uintptr_t>(wyT() + (int64_t)((k - 2 + 15) / 16) * 256 + 4);
+    return reinterpret_cast<double*>((raw + 63) & ~uintptr_t(63));
+  }
+  __device__ double* Wg() const { return Q2() + q2_doubles(k); }     // stage-A W (k x SB_NB)
 };
 __host__ __device__ inline int64_t gview_doubles(int k) {
   const int64_t H = k;
   return (int64_t)k * GView::ld_of(k) + 4 * k + 4 * H + 8 + 4 * (int64_t)k * H + ((k + 63) / 64) * H +
-         (int64_t)((k - 2 + 15) / 16) * 256 + 4;
+         (int64_t)((k - 2 + 15) / 16) * 256 + 4 + 8 + q2_doubles(k) + (int64_t)k * SB_NB + 8;
+}
+
+// T (d, e raw, in shared memory, e[k-1] = 0) -> the workspace: T scaled by a power of two (max
+// entry in [1, 2)), Gershgorin interval, ||T||, pivmin, inertia at 0 (exact Sturm count).  Called
+// by every thread of one CTA (nt threads).
+__device__ void tri_tail(const GView& W, double* d, double* e, int k, int t, int nt) {
+  __syncthreads();
+  if (t == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < k; ++i) mx = fmax(mx, fmax(fabs(d[i]), fabs(e[i])));
+    const double sc = mx > 0.0 ? scalbn(1.0, -ilogb(mx)) : 1.0;
+    double gl = 0.0, gu = 0.0, tn = 0.0, me2 = 0.0;
+    for (int i = 0; i < k; ++i) {
+      d[i] *= sc;
+      e[i] *= sc;
+    }
+    for (int i = 0; i < k; ++i) {
+      const double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + fabs(e[i]);
+      gl = i ? fmin(gl, d[i] - rad) : d[i] - rad;
+      gu = i ? fmax(gu, d[i] + rad) : d[i] + rad;
+      tn = fmax(tn, fabs(d[i]) + rad);
+      me2 = fmax(me2, e[i] * e[i]);
+    }
+    const double pivmin = 1e-290 * fmax(1.0, me2);
+    double q = d[0];
+    if (fabs(q) < pivmin) q = -pivmin;
+    int nneg = q < 0.0;
+    for (int i = 1; i < k; ++i) {
+      q = d[i] - e[i - 1] * e[i - 1] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      nneg += q < 0.0;
+    }
+    const double w = gu - gl;
+    double* h = W.hdr();
+    h[0] = 0;  // k_gtrd_cluster decides the side and the count
+    h[1] = 0;
+    h[2] = tn;
+    h[3] = pivmin;
+    h[4] = sc;
+    h[5] = gl - 2.0 * kEps * fabs(gl) - 2.0 * kEps * w - pivmin;
+    h[6] = gu + 2.0 * kEps * fabs(gu) + 2.0 * kEps * w + pivmin;
+    h[7] = nneg;
+  }
+  __syncthreads();
+  for (int i = t; i < k; i += nt) {
+    W.d()[i] = d[i];
+    W.e()[i] = e[i];
+  }
 }
 
 // ---------------------------------------------------------------- 1. tridiagonalization
@@ -404,50 +466,7 @@ __global__ void __launch_bounds__(TC_NT, 1) k_gtrd_tridiag(ProjArgs a) {
     d[i] = i < k - 2 ? W.d()[i] : __ldcg(M + (int64_t)i * LD + i);
     e[i] = i < k - 2 ? W.e()[i] : (i == k - 2 ? __ldcg(M + (int64_t)i * LD + i + 1) : 0.0);
   }
-  __syncthreads();
-  if (t == 0) {
-    // T scaled by a power of two (max entry in [1, 2)), Gershgorin interval, ||T||,
-    // inertia at 0 (exact Sturm count)
-    double mx = 0.0;
-    for (int i = 0; i < k; ++i) mx = fmax(mx, fmax(fabs(d[i]), fabs(e[i])));
-    const double sc = mx > 0.0 ? scalbn(1.0, -ilogb(mx)) : 1.0;
-    double gl = 0.0, gu = 0.0, tn = 0.0, me2 = 0.0;
-    for (int i = 0; i < k; ++i) {
-      d[i] *= sc;
-      e[i] *= sc;
-    }
-    for (int i = 0; i < k; ++i) {
-      const double rad = (i > 0 ? fabs(e[i - 1]) : 0.0) + fabs(e[i]);
-      gl = i ? fmin(gl, d[i] - rad) : d[i] - rad;
-      gu = i ? fmax(gu, d[i] + rad) : d[i] + rad;
-      tn = fmax(tn, fabs(d[i]) + rad);
-      me2 = fmax(me2, e[i] * e[i]);
-    }
-    const double pivmin = 1e-290 * fmax(1.0, me2);
-    double q = d[0];
-    if (fabs(q) < pivmin) q = -pivmin;
-    int nneg = q < 0.0;
-    for (int i = 1; i < k; ++i) {
-      q = d[i] - e[i - 1] * e[i - 1] / q;
-      if (fabs(q) < pivmin) q = -pivmin;
-      nneg += q < 0.0;
-    }
-    const double w = gu - gl;
-    double* h = W.hdr();
-    h[0] = 0;  // k_gtrd_cluster decides the side and the count
-    h[1] = 0;
-    h[2] = tn;
-    h[3] = pivmin;
-    h[4] = sc;
-    h[5] = gl - 2.0 * kEps * fabs(gl) - 2.0 * kEps * w - pivmin;
-    h[6] = gu + 2.0 * kEps * fabs(gu) + 2.0 * kEps * w + pivmin;
-    h[7] = nneg;
-  }
-  __syncthreads();
-  for (int i = t; i < k; i += TC_NT) {
-    W.d()[i] = d[i];
-    W.e()[i] = e[i];
-  }
+  tri_tail(W, d, e, k, t, TC_NT);
 }
 
 // ---------------------------------------------------------------- 2. eigenvalues and vectors of T
@@ -872,6 +891,769 @@ __global__ void __launch_bounds__(VT) k_gtrd_vec(ProjArgs a) {
   W.lw()[s] = lw / sc;
 }
 
+// ---------------------------------------------------------------- 1b. two-stage reduction
+// For orders >= SDP_GTRD_SBR_MIN the one-column-at-a-time reduction above (one A22 v product
+// and one cluster exchange per column: a latency chain of k steps) is replaced by successive
+// band reduction (Bischof, Lang & Sun):
+//  Stage A, k_sbr_band: dense -> band of bandwidth SB_NB.  Panel p (columns j0 = p NB .. J - 1,
+//   J = j0 + NB): QR of the block below the band, A[J:k, j0:J] = (I - V T V^T) R, then the
+//   trailing matrix A22 = A[J:k, J:k] <- Q^T A22 Q = A22 - V W^T - W V^T with X = A22 V T and
+//   W = X - 1/2 V (T^T V^T X) (the rank-2nb form of dsytrd).  The m x 8 panel QR is computed
+//   redundantly and identically in every CTA of the job from shared memory; X (rows = the CTA's
+//   owned columns, A22 symmetric) and the trailing update of the owned columns are DMMA
+//   (mma.sync m8n8k4 f64) products streamed from L2; per panel three cluster exchanges (the
+//   V^T X partials through DSMEM, the W rows through L2, the updated matrix).  The panel
+//   reflectors stay below the band (v_j with its unit at row j + NB) for the back-transform.
+//  Stage B, k_sbr_chase: the band (plus room for the bulge: 2 NB subdiagonals) in one CTA's
+//   shared memory is reduced to tridiagonal by bulge chasing (Schwarz; Lang): sweep s
+//   annihilates column s below the subdiagonal with a reflector on rows s+1 .. s+NB and chases
+//   the bulge this creates down the band, one NB-row block per step.  One warp per sweep; step i
+//   of sweep s touches rows [s+1+i NB, s+(i+2) NB] and columns [s+1+(i-1) NB, s+(i+1) NB], so
+//   it waits until sweep s-1 has finished its step i+2 (the last one whose elements overlap).
+//  Back-transform V = Q1 Q2 Z: k_sbr_q2 applies the stage-B reflectors to Z (sweeps in reverse
+//   order; the reflectors of one sweep touch disjoint rows and commute), then k_gtrd_wy /
+//   k_gtrd_back apply the stage-A reflectors exactly like dsytrd's (row offset ro = NB).
+constexpr int SA_NT = 512;
+constexpr int SA_NW = SA_NT / 32;
+constexpr int SA_CS = 8;
+constexpr int SA_PAD = ((GT_KMAX + 7) / 8) * 8;
+constexpr int SA_LC = 64;    // rows per partial-X task
+constexpr int SA_MAXT = 64;  // partial X tiles held in shared memory at once
+constexpr int SA_PLD = SB_NB + 1;  // row stride of the panel / V and of V T, W: conflict-free row-per-thread access
+static_assert(SB_NB == 8, "the DMMA tiles and the chase lanes assume NB = 8");
+constexpr size_t kSbrASmem =
+    (size_t)(2 * SA_PAD * SA_PLD + SA_PAD * SB_NB + SA_MAXT * 64 + 2 * (SA_NW * 32 + 32) + 2 * 64 + SA_CS * 64 + 64) *
+    sizeof(double);
+
+// acquire-release fence at CTA scope (MEMBAR.ALL.CTA): orders this thread's shared-memory accesses
+// around a progress flag without the sequentially consistent fence of __threadfence_block()
+__device__ __forceinline__ void fence_cta() { asm volatile("fence.acq_rel.cta;\n" ::: "memory"); }
+
+__device__ __forceinline__ void sb_mma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// CTA sum of one value per thread (every thread gets the total, fixed order); red: SA_NW
+// doubles, used ping-pong by the caller so that one barrier per reduction suffices
+__device__ __forceinline__ double sa_sum1(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int w = 0; w < SA_NW; ++w) s += red[w];
+  return s;
+}
+
+// CTA sums of NV = 8 or 32 values per thread (halving butterfly in the warp, then fixed-order sums
+// of the warps' partials by the first NV threads); red: SA_NW * NV + NV doubles, used ping-pong by
+// the caller (two barriers per reduction)
+template <int NV>
+__device__ __forceinline__ void sa_sumv(double (&v)[NV], double* red) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int hh = NV / 2; hh >= 1; hh >>= 1) {
+    const int o = (32 / NV) * hh;  // lane offsets: NV = 8: 16, 8, 4; NV = 32: 16, 8, 4, 2, 1
+    const bool up = (lane & o) != 0;
+#pragma unroll
+    for (int q = 0; q < hh; ++q) {
+      const double send = up ? v[q] : v[q + hh];
+      const double keep = up ? v[q + hh] : v[q];
+      v[q] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  double tot = v[0];
+#pragma unroll
+  for (int o = 32 / NV / 2; o >= 1; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+  // lane L holds value idx = bit-reversal of L's bits (4 .. 5 - log2 NV)
+  int idx = 0;
+#pragma unroll
+  for (int b = 0; (1 << b) < NV; ++b) idx = idx * 2 + ((lane >> (4 - b)) & 1);
+  if ((lane & (32 / NV - 1)) == 0) red[(threadIdx.x >> 5) * NV + idx] = tot;
+  __syncthreads();
+  double* fin = red + SA_NW * NV;
+  if (threadIdx.x < NV) {
+    double sacc = 0.0;
+#pragma unroll
+    for (int w = 0; w < SA_NW; ++w) sacc += red[w * NV + threadIdx.x];
+    fin[threadIdx.x] = sacc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < NV; ++c) v[c] = fin[c];
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(SA_NT, 1) k_sbr_band(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int job = blockIdx.x / SA_CS, rank = blockIdx.x % SA_CS;
+  const bool coop = gt.job2_coop[job] != 0;
+  const int g = gt.job2_g[job * SA_CS + (coop ? 0 : rank)];
+  if (g < 0) return;
+  const int ncta = coop ? SA_CS : 1, r = coop ? rank : 0;
+  const int task = gt.task[g];
+  const int k = a.ksz[task];
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31, r4 = lane >> 2, c4 = lane & 3;
+  if (k > GT_KMAX) {
+    if (r == 0 && t == 0) gt.status[g] = -1;
+    return;
+  }
+  if (r == 0 && t == 0) gt.status[g] = 0;
+  cg::cluster_group cl = cg::this_cluster();
+  auto csync = [&]() {
+    if (coop)
+      cl.sync();
+    else
+      __syncthreads();
+  };
+  extern __shared__ double smem[];
+  double* Pv = smem;                    // panel -> V, [l][q] (row stride SA_PLD), SA_PAD rows
+  double* VT = Pv + SA_PAD * SA_PLD;    // V T, then W of all rows (row stride SA_PLD)
+  double* Xo = VT + SA_PAD * SA_PLD;    // X -> W of the owned rows, [tile][r][q]
+  double* Xp = Xo + SA_PAD * SB_NB;     // partial X tiles
+  double* red = Xp + SA_MAXT * 64;      // 2 x (SA_NW x 32 + 32) (ping-pong)
+  double* Mp = red + 2 * (SA_NW * 32 + 32);  // M' = T^T V^T X (8 x 8)
+  double* Tm = Mp + 64;                 // T (8 x 8, upper)
+  double* xch = Tm + 64;                // SA_CS x 64 partials of V^T X (DSMEM)
+  GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
+  const int LD = W.ld();
+  double* M = W.M();
+  double* Wg = W.Wg();
+  const int64_t off = a.off[task];
+  const int ns = k * (k + 1) / 2;
+  for (int e = r * SA_NT + t; e < ns; e += ncta * SA_NT) {
+    int rr, c;
+    packed_rc(e, rr, c);
+    const double v = input_value<MODE>(a, off + e, rr, c);
+    M[(int64_t)rr * LD + c] = v;
+    M[(int64_t)c * LD + rr] = v;
+  }
+  int rp = 0;  // ping-pong index of red
+  auto R1 = [&]() { double* p = red + rp * (SA_NW * 32 + 32); rp ^= 1; return p; };
+  const int nchunk = (k + SB_NB - 1) / SB_NB;
+  csync();
+  // SDP_GTRD_DEBUG=3: per-phase clock64 totals of thread 0 of CTA 0 of the first job
+  const bool trace = gt.debug == 3 && blockIdx.x == 0 && t == 0;
+  long long tr_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long tr_last = clock64();
+#define SA_MARK(ph)                         \
+  if (trace) {                              \
+    const long long now_ = clock64();       \
+    tr_acc[ph] += now_ - tr_last;           \
+    tr_last = now_;                         \
+  }
+  for (int p = 0;; ++p) {
+    const int j0 = p * SB_NB, J = j0 + SB_NB, m = k - J;
+    if (m < 2) break;
+    const int nq = min(SB_NB, m - 1);
+    // (1) panel A[J:k, j0:J] -> shared memory (rows >= m zero)
+    for (int e = t; e < SA_PAD * SB_NB; e += SA_NT) {
+      const int l = e >> 3, q = e & 7;
+      Pv[l * SA_PLD + q] = l < m ? __ldcg(M + (int64_t)(J + l) * LD + j0 + q) : 0.0;
+    }
+    __syncthreads();
+    // (2) Householder QR of the panel (dgeqr2), identical in every CTA
+    double taus[SB_NB], betas[SB_NB];
+#pragma unroll
+    for (int q = 0; q < SB_NB; ++q) {
+      taus[q] = 0.0;
+      betas[q] = q < m ? Pv[q * SA_PLD + q] : 0.0;  // no reflector: the diagonal entry is R's
+      if (q >= nq) continue;
+      const double alpha = Pv[q * SA_PLD + q];
+      double part = 0.0;
+      for (int l = q + 1 + t; l < m; l += SA_NT) part = fma(Pv[l * SA_PLD + q], Pv[l * SA_PLD + q], part);
+      const double sig = sa_sum1(part, R1());
+      double tau = 0.0, beta = alpha, scl = 0.0;
+      if (sig > 0.0) {
+        const double nrm = sqrt(fma(alpha, alpha, sig));
+        beta = alpha >= 0.0 ? -nrm : nrm;
+        tau = (beta - alpha) / beta;
+        scl = 1.0 / (alpha - beta);
+      }
+      double wp[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) wp[c] = 0.0;
+      for (int l = q + t; l < m; l += SA_NT) {
+        double vl = 1.0;
+        if (l > q) {
+          vl = Pv[l * SA_PLD + q] * scl;
+          Pv[l * SA_PLD + q] = vl;
+        }
+#pragma unroll
+        for (int c = q + 1; c < 8; ++c) wp[c] = fma(vl, Pv[l * SA_PLD + c], wp[c]);
+      }
+      sa_sumv<8>(wp, R1());
+      if (tau != 0.0)
+        for (int l = q + t; l < m; l += SA_NT) {
+          const double vl = l > q ? Pv[l * SA_PLD + q] : 1.0;
+#pragma unroll
+          for (int c = q + 1; c < 8; ++c) Pv[l * SA_PLD + c] -= tau * vl * wp[c];
+        }
+      __syncthreads();
+      taus[q] = tau;
+      betas[q] = beta;
+    }
+    SA_MARK(0);
+    // (3) R and the reflectors back into the matrix (rank 0), tau
+    if (r == 0) {
+      for (int e = t; e < m * SB_NB; e += SA_NT) {
+        const int l = e >> 3, q = e & 7;
+        double v = Pv[l * SA_PLD + q];
+#pragma unroll
+        for (int qq = 0; qq < SB_NB; ++qq)
+          if (qq == q && l == q) v = betas[qq];
+        M[(int64_t)(J + l) * LD + j0 + q] = v;
+      }
+      if (t < SB_NB) {
+        double tv = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < SB_NB; ++qq)
+          if (qq == t) tv = taus[qq];
+        W.tau()[j0 + t] = tv;
+      }
+    }
+    __syncthreads();
+    // Pv -> V with an explicit unit diagonal and zeros above it
+    if (t < 64) {
+      const int l = t >> 3, q = t & 7;
+      if (l < q) Pv[l * SA_PLD + q] = 0.0;
+      if (l == q) Pv[l * SA_PLD + q] = 1.0;
+    }
+    __syncthreads();
+    SA_MARK(1);
+    // (4) T (dlarft forward, columnwise): T[q][q] = tau_q, T[0:q, q] = -tau_q T[0:q, 0:q] G[0:q, q],
+    //     G = V^T V (one 32-value reduction: the 28 pairs a < b), T by warp 0 into shared memory
+    {
+      double gp[32];
+#pragma unroll
+      for (int u = 0; u < 32; ++u) gp[u] = 0.0;
+      for (int l = t; l < m; l += SA_NT) {
+        double vr[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) vr[q] = Pv[l * SA_PLD + q];
+        int u = 0;
+#pragma unroll
+        for (int x = 0; x < 8; ++x)
+#pragma unroll
+          for (int y = x + 1; y < 8; ++y) {
+            gp[u] = fma(vr[x], vr[y], gp[u]);
+            ++u;
+          }
+      }
+      sa_sumv<32>(gp, R1());
+      if (wid == 0) {
+        // column c of T by lanes rr < c: T[rr][c] = -tau_c sum_{q = rr}^{c-1} T[rr][q] G[q][c]
+        double trow[8];  // row `lane` of T (lanes 0..7)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) trow[c] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          double acc = 0.0;
+          int u = 0;
+#pragma unroll
+          for (int x = 0; x < 8; ++x)
+#pragma unroll
+            for (int y = x + 1; y < 8; ++y) {
+              if (y == c && x >= lane) acc = fma(trow[x], gp[u], acc);  // G[x][c], x in [lane, c)
+              ++u;
+            }
+          double tc = 0.0;
+#pragma unroll
+          for (int qq = 0; qq < 8; ++qq)
+            if (qq == c) tc = taus[qq];
+          trow[c] = lane < c ? -tc * acc : (lane == c ? tc : 0.0);
+        }
+        if (lane < 8) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) Tm[lane * 8 + c] = trow[c];
+        }
+      }
+      __syncthreads();
+    }
+    // (5) VT = V T for every row (rows >= m: 0)
+    for (int l = t; l < SA_PAD; l += SA_NT) {
+      double vr[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) vr[q] = Pv[l * SA_PLD + q];  // rows >= m are zero
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        double acc = 0.0;
+#pragma unroll
+        for (int q = 0; q <= c; ++q) acc = fma(vr[q], Tm[q * 8 + c], acc);
+        VT[l * SA_PLD + c] = acc;
+      }
+    }
+    __syncthreads();
+    // owned column tiles (chunks of 8 columns, round-robin over the job's CTAs) at or after J
+    const int ch0 = p + 1;                                        // first chunk of A22
+    const int first = ch0 <= r ? r : r + ((ch0 - r + ncta - 1) / ncta) * ncta;
+    const int nit = first < nchunk ? (nchunk - 1 - first) / ncta + 1 : 0;
+    SA_MARK(2);
+    // (6) X rows of the owned columns: X[i][:] = sum_l A22[l][i] VT[l][:] (DMMA, l split in
+    //     chunks of SA_LC rows; partial tiles reduced in a fixed order)
+    const int nlc = (m + SA_LC - 1) / SA_LC;
+    for (int e = t; e < nit * 64; e += SA_NT) Xo[e] = 0.0;
+    for (int tb = 0; tb < nit * nlc; tb += SA_MAXT) {
+      const int nt = min(SA_MAXT, nit * nlc - tb);
+      for (int u0 = wid; u0 < nt; u0 += 2 * SA_NW) {  // two tasks per warp: 32 loads in flight
+        double av[2][SA_LC / 4];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int u = u0 + b * SA_NW;
+          const int it = (tb + u) / nlc, lc = (tb + u) % nlc;
+          const int icol = (first + it * ncta) * SB_NB + r4;
+          const bool ok = u < nt && icol < k;
+#pragma unroll
+          for (int s4 = 0; s4 < SA_LC / 4; ++s4) {
+            const int l = lc * SA_LC + s4 * 4 + c4;  // row of A22 (local)
+            av[b][s4] = (ok && l < m) ? __ldcg(M + (int64_t)(J + l) * LD + icol) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int u = u0 + b * SA_NW;
+          if (u >= nt) break;
+          const int lc = (tb + u) % nlc;
+          double acc[2] = {0.0, 0.0};
+#pragma unroll
+          for (int s4 = 0; s4 < SA_LC / 4; ++s4) {
+            const int l = lc * SA_LC + s4 * 4 + c4;
+            sb_mma(acc, av[b][s4], l < SA_PAD ? VT[l * SA_PLD + r4] : 0.0);
+          }
+          Xp[u * 64 + r4 * 8 + 2 * c4] = acc[0];
+          Xp[u * 64 + r4 * 8 + 2 * c4 + 1] = acc[1];
+        }
+      }
+      __syncthreads();
+      for (int e = t; e < nit * 64; e += SA_NT) {  // fixed order: batches, then chunks
+        const int it = e >> 6;
+        double sacc = Xo[e];
+        for (int lc = 0; lc < nlc; ++lc) {
+          const int u = it * nlc + lc - tb;
+          if (u >= 0 && u < nt) sacc += Xp[u * 64 + (e & 63)];
+        }
+        Xo[e] = sacc;
+      }
+      __syncthreads();
+    }
+    SA_MARK(3);
+    // (7) V^T X over the owned rows -> every CTA (DSMEM), summed in rank order; M' = T^T (V^T X)
+    if (t < 64) {
+      const int q = t >> 3, q2 = t & 7;
+      double sacc = 0.0;
+      for (int it = 0; it < nit; ++it) {
+        const int i0 = (first + it * ncta) * SB_NB;
+        for (int rr = 0; rr < 8; ++rr) {
+          const int l = i0 + rr - J;
+          if (i0 + rr < k) sacc = fma(Pv[l * SA_PLD + q], Xo[it * 64 + rr * 8 + q2], sacc);
+        }
+      }
+      if (coop) {
+        for (int rr = 0; rr < SA_CS; ++rr) cl.map_shared_rank(xch, rr)[r * 64 + t] = sacc;
+      } else {
+        xch[t] = sacc;
+      }
+    }
+    csync();
+    if (t < 64) {
+      double m0[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double sacc = 0.0;
+        for (int rr = 0; rr < ncta; ++rr) sacc += xch[rr * 64 + q * 8 + (t & 7)];
+        m0[q] = sacc;
+      }
+      const int q = t >> 3;
+      double mp = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq)
+        if (qq <= q) mp = fma(Tm[qq * 8 + q], m0[qq], mp);  // (T^T)[q][qq] = T[qq][q]
+      Mp[t] = mp;
+    }
+    __syncthreads();
+    SA_MARK(4);
+    // (8) W = X - 1/2 V M' for the owned rows -> Xo and the global W rows
+    for (int e = t; e < nit * 64; e += SA_NT) {
+      const int it = e >> 6, rr = (e >> 3) & 7, q = e & 7;
+      const int i = (first + it * ncta) * SB_NB + rr;
+      if (i >= k) {
+        Xo[e] = 0.0;
+        continue;
+      }
+      const int l = i - J;
+      double vm = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < 8; ++qq) vm = fma(Pv[l * SA_PLD + qq], Mp[qq * 8 + q], vm);
+      const double w = Xo[e] - 0.5 * vm;
+      Xo[e] = w;
+      Wg[(int64_t)l * SB_NB + q] = w;
+    }
+    csync();
+    for (int e = t; e < SA_PAD * SB_NB; e += SA_NT) VT[(e >> 3) * SA_PLD + (e & 7)] = (e >> 3) < m ? __ldcg(Wg + e) : 0.0;
+    __syncthreads();
+    SA_MARK(5);
+    // (9) A22[:, owned] -= V W^T + W V^T  (DMMA: [V | W](l, 16) x [W | V](i, 16)^T); every warp
+    //     loads the C tiles of 8 of its tasks at once (L2 latency), then multiplies and stores
+    const int nlt = (m + 7) / 8;
+    const int ntask = nlt * nit;
+    for (int u0 = wid; u0 < ntask; u0 += 16 * SA_NW) {
+      double2 cur[16];
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const int u = u0 + b * SA_NW;
+        cur[b] = make_double2(0.0, 0.0);
+        if (u < ntask) {
+          const int lt = u / nit, it = u % nit;
+          const int row = J + lt * 8 + r4, col = (first + it * ncta) * SB_NB + 2 * c4;
+          if (row < k && col < k) cur[b] = __ldcg(reinterpret_cast<const double2*>(M + (int64_t)row * LD + col));
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < 16; ++b) {
+        const int u = u0 + b * SA_NW;
+        if (u >= ntask) break;
+        const int lt = u / nit, it = u % nit;
+        const int i0 = (first + it * ncta) * SB_NB;
+        const int l0 = lt * 8;
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const int q = (ks & 1) * 4 + c4;
+          const double av = ks < 2 ? Pv[(l0 + r4) * SA_PLD + q] : VT[(l0 + r4) * SA_PLD + q];
+          const double bv = ks < 2 ? Xo[it * 64 + r4 * 8 + q] : Pv[(i0 + r4 - J) * SA_PLD + q];
+          sb_mma(acc, av, bv);
+        }
+        const int row = J + l0 + r4, col = i0 + 2 * c4;
+        if (row < k && col < k) {
+          double* pm = M + (int64_t)row * LD + col;
+          pm[0] = cur[b].x - acc[0];
+          if (col + 1 < k) pm[1] = cur[b].y - acc[1];
+        }
+      }
+    }
+    csync();
+    SA_MARK(6);
+  }
+  if (trace)
+    printf("[sbr band k=%d coop=%d] cycles: qr %lld | T,VT %lld | X %lld | VtX+exch %lld | W+exch %lld | update+sync %lld\n",
+           k, (int)coop, tr_acc[0], tr_acc[1], tr_acc[2], tr_acc[3], tr_acc[4], tr_acc[6]);
+#undef SA_MARK
+  // the band stays in M (lower part, distance <= NB); stage B reads it
+}
+
+// Stage B.  AB[c * SB_LDB + d] = A[c + d][c], d = 0 .. SB_LDB - 1 (room for the bulge: d <= 2 NB - 1).
+// Each warp chases SB_G consecutive sweeps in lockstep, one 8-lane group per sweep, group g lagging
+// SB_LAG steps behind group g - 1 (step i of sweep s needs step i + 2 of sweep s - 1 finished, so a
+// fixed lag of 4 satisfies every dependency inside the warp without waiting); group 0 waits for the
+// previous warp's group SB_G - 1 through a per-block progress counter in shared memory.  The code of
+// a step is branch-free across the lanes (inactive groups compute on a valid dummy block and store
+// nothing), so the warp issues one instruction stream for SB_G sweeps.
+constexpr int SB_LDB = 2 * SB_NB + 2;  // A[r][c] at c (SB_LDB - 1) + r: columns 17 doubles apart (conflict-free per lane)
+constexpr int SB_NW = 8;
+constexpr int SB_NT = SB_NW * 32;
+constexpr int SB_G = 4;
+constexpr int SB_LAG = 4;
+constexpr int SB_NBLK = (GT_KMAX + SB_G - 1) / SB_G + 1;
+constexpr size_t kSbrBSmem =
+    (size_t)(GT_KMAX + 2 * SB_NB + 1) * SB_LDB * sizeof(double) + (size_t)(GT_KMAX + 1 + SB_NBLK) * sizeof(int);
+
+__global__ void __launch_bounds__(SB_NT, 1) k_sbr_chase(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int g = gt.sb_g[blockIdx.x];
+  if (gt.status[g] < 0) return;
+  const int k = a.ksz[gt.task[g]];
+  const GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
+  const int LD = W.ld();
+  const double* M = W.M();
+  double* Q2 = W.Q2();
+  extern __shared__ double smb2[];
+  double* AB = smb2;
+  int* qoff = reinterpret_cast<int*>(AB + (GT_KMAX + 2 * SB_NB + 1) * SB_LDB);
+  int* sprog = qoff + (GT_KMAX + 1);  // per block of SB_G sweeps: super-steps completed
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
+  for (int e = t; e < (k + 2 * SB_NB + 1) * SB_LDB; e += SB_NT) {
+    const int c = e / SB_LDB, d = e % SB_LDB;
+    AB[e] = (c < k && d <= SB_NB && c + d < k) ? __ldcg(M + (int64_t)(c + d) * LD + c) : 0.0;
+  }
+  const int nsw = k - 2;  // sweeps s = 0 .. k - 3 (s = k - 2 has nothing to annihilate)
+  auto nsteps = [&](int s) { return (k - 1 - s + SB_NB - 1) / SB_NB; };
+  const int nblk = nsw > 0 ? (nsw + SB_G - 1) / SB_G : 0;
+  for (int b = t; b < SB_NBLK; b += SB_NT) sprog[b] = 0;
+  if (t == 0) {
+    int acc = 0;
+    for (int s = 0; s < nsw; ++s) {
+      qoff[s] = acc;
+      acc += nsteps(s);
+    }
+  }
+  __syncthreads();
+  volatile int* vsp = sprog;
+  auto A = [&](int rr, int c) -> double& { return AB[c * (SB_LDB - 1) + rr]; };  // rr >= c, rr - c <= 2 NB
+  const int gq = lane >> 3, l = lane & 7;
+  const bool trace = gt.debug == 3 && blockIdx.x == 0 && lane == 0;
+  long long t_wait = 0, t_start = clock64(), nsup = 0;
+  for (int b = wid; b < nblk; b += SB_NW) {
+    const int s = b * SB_G + gq;  // this group's sweep
+    const bool sv = s < nsw;
+    const int nst = sv ? nsteps(s) : 0;
+    int jmax = 0;
+#pragma unroll
+    for (int gg = 0; gg < SB_G; ++gg)
+      if (b * SB_G + gg < nsw) jmax = max(jmax, nsteps(b * SB_G + gg) + SB_LAG * gg);
+    const int sp = b * SB_G - 1;  // previous block's last sweep (group 0's dependency)
+    const int nsp = sp >= 0 ? nsteps(sp) : 0;
+    const int nst0 = nsteps(b * SB_G);
+    for (int j = 0; j < jmax; ++j) {
+      if (b > 0 && j < nst0) {  // group 0's step j needs sweep sp to have finished step j + 2
+        const int need = min(j + 3, nsp) + SB_LAG * (SB_G - 1);
+        const long long tw0 = trace ? clock64() : 0;
+        while (vsp[b - 1] < need) __nanosleep(32);
+        if (trace) t_wait += clock64() - tw0;
+        fence_cta();
+      }
+      const int i = j - SB_LAG * gq;
+      const bool act = sv && i >= 0 && i < nst;
+      const int sg = act ? s : 0, ig = act ? i : 0;
+      const int r0 = sg + 1 + ig * SB_NB;
+      const int L = min(SB_NB, k - r0);
+      const int cb = ig == 0 ? sg : r0 - SB_NB;  // column whose part in rows r0.. is annihilated
+      // (a) reflector of x = A[r0 .. r0 + L - 1][cb]: beta = -sign(alpha) ||x||, v = x / (alpha - beta),
+      //     tau = (beta - alpha) / beta, from one reciprocal 1 / (beta (alpha - beta))
+      const double xl = l < L ? A(r0 + l, cb) : 0.0;
+      const double alpha = __shfl_sync(0xffffffffu, xl, 0, SB_NB);
+      double sq = (l >= 1) ? xl * xl : 0.0;
+      sq += __shfl_xor_sync(0xffffffffu, sq, 1, SB_NB);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 2, SB_NB);
+      sq += __shfl_xor_sync(0xffffffffu, sq, 4, SB_NB);
+      const double nrm = sqrt(fma(alpha, alpha, sq));
+      const double beta = sq > 0.0 ? (alpha >= 0.0 ? -nrm : nrm) : alpha;
+      const double dd = alpha - beta;
+      const double rr = sq > 0.0 ? 1.0 / (beta * dd) : 0.0;
+      const double scl = beta * rr, tau = -dd * dd * rr;
+      const double vl = l == 0 ? 1.0 : (l < L ? xl * scl : 0.0);
+      if (act) {
+        Q2[(int64_t)(qoff[sg] + ig) * SB_NB + l] = l == 0 ? tau : vl;
+        if (l < L) A(r0 + l, cb) = l == 0 ? beta : 0.0;
+      }
+      double v[SB_NB];
+#pragma unroll
+      for (int r = 0; r < SB_NB; ++r) v[r] = __shfl_sync(0xffffffffu, vl, r, SB_NB);
+      // (b) H from the left on the left block (columns cb + 1 .. cb + 7, steps i >= 1): lane = column
+      {
+        double z[SB_NB], d = 0.0;
+#pragma unroll
+        for (int r = 0; r < SB_NB; ++r) {
+          z[r] = r < L ? A(r0 + r, cb + l) : 0.0;
+          d = fma(v[r], z[r], d);
+        }
+        d *= tau;
+        if (act && ig > 0 && l >= 1)
+#pragma unroll
+          for (int r = 0; r < SB_NB; ++r)
+            if (r < L) A(r0 + r, cb + l) = fma(-d, v[r], z[r]);
+      }
+      // (c) two-sided on D = A[R][R]: lane = column l of D; y = tau D v, w = y - (tau/2)(y.v) v,
+      //     D -= v w^T + w v^T (lower part, column l: rows r >= l)
+      double dcol[SB_NB], y = 0.0;
+#pragma unroll
+      for (int r = 0; r < SB_NB; ++r) {
+        dcol[r] = (r < L && l < L) ? (r >= l ? A(r0 + r, r0 + l) : A(r0 + l, r0 + r)) : 0.0;
+        y = fma(dcol[r], v[r], y);
+      }
+      y *= tau;
+      double vlv = v[0];
+#pragma unroll
+      for (int r = 1; r < SB_NB; ++r) vlv = (l == r) ? v[r] : vlv;
+      double yv = y * vlv;
+      yv += __shfl_xor_sync(0xffffffffu, yv, 1, SB_NB);
+      yv += __shfl_xor_sync(0xffffffffu, yv, 2, SB_NB);
+      yv += __shfl_xor_sync(0xffffffffu, yv, 4, SB_NB);
+      const double wl = y - 0.5 * tau * yv * vlv;
+      double w[SB_NB];
+#pragma unroll
+      for (int r = 0; r < SB_NB; ++r) w[r] = __shfl_sync(0xffffffffu, wl, r, SB_NB);
+      if (act && l < L)
+#pragma unroll
+        for (int r = 0; r < SB_NB; ++r)
+          if (r >= l && r < L) A(r0 + r, r0 + l) = dcol[r] - fma(v[r], wl, w[r] * vlv);
+      // (d) E = A[r0 + 8 .. r0 + 8 + L2 - 1][R] <- E H: lane = row l of E
+      {
+        const int L2 = min(SB_NB, k - r0 - SB_NB);
+        double e[SB_NB], u = 0.0;
+#pragma unroll
+        for (int c = 0; c < SB_NB; ++c) {
+          e[c] = (l < L2 && c < L) ? A(r0 + SB_NB + l, r0 + c) : 0.0;
+          u = fma(e[c], v[c], u);
+        }
+        u *= tau;
+        if (act && l < L2)
+#pragma unroll
+          for (int c = 0; c < SB_NB; ++c)
+            if (c < L) A(r0 + SB_NB + l, r0 + c) = fma(-u, v[c], e[c]);
+      }
+      __syncwarp();
+      fence_cta();
+      if (lane == 0) vsp[b] = j + 1;
+      ++nsup;
+    }
+  }
+  if (trace && (wid == 0 || wid == SB_NW - 1))
+    printf("[sbr chase k=%d warp %d] super-steps %lld, cycles %lld, waiting %lld\n", k, wid, nsup, clock64() - t_start,
+           t_wait);
+  __syncthreads();
+  // T: d = diagonal, e = first subdiagonal (raw) -> the tail
+  double dv[(GT_KMAX + SB_NT - 1) / SB_NT], ev[(GT_KMAX + SB_NT - 1) / SB_NT];
+#pragma unroll
+  for (int u = 0; u < (GT_KMAX + SB_NT - 1) / SB_NT; ++u) {
+    const int ii = t + u * SB_NT;
+    dv[u] = ii < k ? A(ii, ii) : 0.0;
+    ev[u] = ii + 1 < k ? A(ii + 1, ii) : 0.0;
+  }
+  __syncthreads();
+  double* d0 = AB;
+  double* e0 = AB + GT_KMAX;
+#pragma unroll
+  for (int u = 0; u < (GT_KMAX + SB_NT - 1) / SB_NT; ++u) {
+    const int ii = t + u * SB_NT;
+    if (ii < k) {
+      d0[ii] = dv[u];
+      e0[ii] = ev[u];
+    }
+  }
+  tri_tail(W, d0, e0, k, t, SB_NT);
+}
+
+// Z <- Q2 Z (stage-B reflectors, applied in reverse generation order): a CTA per SQ_COLS columns
+// of Z (k x 32 in shared memory, lane = column: each reflector is 8 loads, 16 FMAs and 8 stores per
+// lane, no shuffles).  Reflector (s, i) acts on rows [s+1+8i, s+8+8i]; of the reflectors generated
+// after it only (s+1, i-1) (row s+1+8i) overlaps it, and (s-1, i+1) is the next one down that
+// overlaps it.  So the application is a wavefront without CTA barriers: the warp owning step index
+// i applies (s, i) for s descending as soon as index i-1 has applied (s+1, i-1) (per-index
+// progress counters in shared memory); the reflectors of the next sweeps are prefetched.
+constexpr int SQ_NT = 1024;
+constexpr int SQ_NW = SQ_NT / 32;
+constexpr int SQ_COLS = 32;
+constexpr int SQ_NI = (GT_KMAX + SB_NB - 1) / SB_NB + 1;
+constexpr int SQ_RING = 4;  // per-warp cp.async ring of reflector slots
+constexpr size_t kSbrQSmem = (size_t)GT_KMAX * SQ_COLS * sizeof(double) + (GT_KMAX + 1 + SQ_NI) * sizeof(int) +
+                             (size_t)SQ_NW * SQ_RING * SB_NB * sizeof(double) + 64;
+
+__global__ void __launch_bounds__(SQ_NT, 1) k_sbr_q2(ProjArgs a) {
+  if (a.done && *a.done) return;
+  const GtrdDev& gt = a.gd.gt;
+  const int item = blockIdx.x;
+  const int g = find_item(gt.bt_pre, gt.ng, item);
+  if (gt.status[g] < 0) return;
+  const int k = a.ksz[gt.task[g]];
+  if (k < gt.sbr_min) return;
+  const int H = gt.hsel[g];
+  const GView W{gt.ws + gt.moff[g], k, H};
+  const int nsel = (int)W.hdr()[0];
+  // bt_pre counts CTAs of kGtrdBackCols columns: the even ones take SQ_COLS = 2 x 16 columns
+  const int local = item - gt.bt_pre[g];
+  if (local & 1) return;
+  const int col0 = local * kGtrdBackCols;
+  if (col0 >= nsel) return;
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31;
+  extern __shared__ double smq[];
+  double* Zs = smq;                                        // [i][c], k x 32
+  int* qoff = reinterpret_cast<int*>(Zs + GT_KMAX * SQ_COLS);
+  int* prog = qoff + (GT_KMAX + 1);                        // per step index: lowest sweep applied
+  double* ring = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(prog + SQ_NI) + 63) & ~uintptr_t(63)) +
+                 wid * SQ_RING * SB_NB;                    // this warp's prefetch slots
+  double* Z = W.Z();
+  const double* Q2 = W.Q2();
+  const int nsw = k - 2;
+  auto nsteps = [&](int s) { return (k - 1 - s + SB_NB - 1) / SB_NB; };
+  const int imax = nsw > 0 ? nsteps(0) : 0;
+  if (t == 0) {
+    int acc = 0;
+    for (int s = 0; s < nsw; ++s) {
+      qoff[s] = acc;
+      acc += nsteps(s);
+    }
+  }
+  for (int i = t; i < SQ_NI; i += SQ_NT) prog[i] = 1 << 30;
+  for (int e = t; e < k * SQ_COLS; e += SQ_NT) {
+    const int c = e / k, i = e % k;
+    Zs[i * SQ_COLS + c] = col0 + c < nsel ? Z[(int64_t)(col0 + c) * k + i] : 0.0;
+  }
+  __syncthreads();
+  volatile int* vprog = prog;
+  auto shi_of = [&](int i) { return min(nsw - 1, k - 2 - SB_NB * i); };  // last sweep with a step i
+  const bool trace = gt.debug == 3 && blockIdx.x == 0 && lane == 0 && (wid == 0 || wid == SQ_NW - 1);
+  long long t_wait = 0, t_start = clock64(), nstep = 0;
+  for (int i = wid; i < imax; i += SQ_NW) {
+    const int shi = shi_of(i);
+    const int shp = i > 0 ? shi_of(i - 1) : -1;
+    // reflector (tau, v_1 .. v_7) of sweeps shi, shi-1, ... staged SQ_RING - 1 ahead by cp.async
+    // (lanes 0..7, one element each; the fences below do not wait for them)
+    __syncwarp();
+    for (int u = 0; u < SQ_RING - 1; ++u) {
+      if (lane < SB_NB && shi - u >= 0)
+        cp_async8(ring + ((shi - u) & (SQ_RING - 1)) * SB_NB + lane, Q2 + (int64_t)(qoff[shi - u] + i) * SB_NB + lane);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    for (int s = shi; s >= 0; --s) {
+      if (lane < SB_NB && s - (SQ_RING - 1) >= 0)
+        cp_async8(ring + ((s - (SQ_RING - 1)) & (SQ_RING - 1)) * SB_NB + lane,
+                  Q2 + (int64_t)(qoff[s - (SQ_RING - 1)] + i) * SB_NB + lane);
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(SQ_RING - 1) : "memory");
+      if (i > 0 && s + 1 <= shp) {  // (s+1, i-1) must be applied first (every lane polls: no divergence)
+        const long long tw0 = trace ? clock64() : 0;
+        while (vprog[i - 1] > s + 1) __nanosleep(20);
+        if (trace) t_wait += clock64() - tw0;
+        fence_cta();
+      }
+      __syncwarp();
+      // tau, v_1 .. v_7 from the staged slot (broadcast loads); tau = 0 reflectors are applied as
+      // identities (their stored v is 0), so the step has no lane-dependent branch
+      const double2* rs = reinterpret_cast<const double2*>(ring + (s & (SQ_RING - 1)) * SB_NB);
+      double v[SB_NB];
+      double tau;
+      {
+        const double2 p0 = rs[0], p1 = rs[1], p2 = rs[2], p3 = rs[3];
+        tau = p0.x;
+        v[0] = 1.0;
+        v[1] = p0.y;
+        v[2] = p1.x;
+        v[3] = p1.y;
+        v[4] = p2.x;
+        v[5] = p2.y;
+        v[6] = p3.x;
+        v[7] = p3.y;
+      }
+      const int r0 = s + 1 + SB_NB * i;
+      const int L = min(SB_NB, k - r0);
+      double z[SB_NB], d = 0.0;
+#pragma unroll
+      for (int r = 0; r < SB_NB; ++r) {
+        z[r] = r < L ? Zs[(r0 + r) * SQ_COLS + lane] : 0.0;
+        d = fma(v[r], z[r], d);
+      }
+      d *= tau;
+#pragma unroll
+      for (int r = 0; r < SB_NB; ++r)
+        if (r < L) Zs[(r0 + r) * SQ_COLS + lane] = fma(-d, v[r], z[r]);
+      __syncwarp();
+      fence_cta();
+      if (lane == 0) vprog[i] = s;
+      ++nstep;
+    }
+  }
+  if (trace) printf("[sbr q2 k=%d warp %d] steps %lld, cycles %lld, waiting %lld\n", k, wid, nstep, clock64() - t_start, t_wait);
+  __syncthreads();
+  for (int e = t; e < k * SQ_COLS; e += SQ_NT) {
+    const int c = e / k, i = e % k;
+    if (col0 + c < nsel) Z[(int64_t)(col0 + c) * k + i] = Zs[i * SQ_COLS + c];
+  }
+}
+
 // ---------------------------------------------------------------- 3. back-transform V = Q Z
 // Q = H_0 H_1 ... H_{k-3}; the reflectors are applied in groups of GB_NR from the last one down,
 // each group in compact WY form H_lo ... H_hi = I - Y T Y^T (LAPACK dlarft, forward).
@@ -888,9 +1670,11 @@ __global__ void __launch_bounds__(GB_NT) k_gtrd_wy(ProjArgs a) {
   const int g = find_item(gt.wy_pre, gt.ng, blockIdx.x);
   if (gt.status[g] < 0) return;
   const int k = a.ksz[gt.task[g]];
-  const GView W{gt.ws + gt.moff[g], k, gt.hsel[g]};
+  const GView W{gt.ws + gt.moff[g], k, gt.hsel[g], k >= gt.sbr_min ? SB_NB : 1};
+  const int ro = W.ro;
   const int gi = blockIdx.x - gt.wy_pre[g];
-  const int jhi = k - 3 - gi * GB_NR;
+  if (gi >= W.nwy()) return;
+  const int jhi = W.nref() - 1 - gi * GB_NR;
   const int nr = min(GB_NR, jhi + 1);
   const int jlo = jhi - nr + 1;
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -902,7 +1686,7 @@ __global__ void __launch_bounds__(GB_NT) k_gtrd_wy(ProjArgs a) {
   for (int e = threadIdx.x; e < GB_NR * k; e += GB_NT) {  // v_j lives in column j: c fastest
     const int c = e % GB_NR, i = e / GB_NR;
     const int j = jlo + c;
-    vb[c * GT_KMAX + i] = (c >= nr || i < j + 1) ? 0.0 : (i == j + 1 ? 1.0 : M[(int64_t)i * LD + j]);
+    vb[c * GT_KMAX + i] = (c >= nr || i < j + ro) ? 0.0 : (i == j + ro ? 1.0 : M[(int64_t)i * LD + j]);
   }
   __syncthreads();
   for (int pr = wid; pr < GB_NR * (GB_NR - 1) / 2; pr += GB_NT / 32) {
@@ -914,7 +1698,7 @@ __global__ void __launch_bounds__(GB_NT) k_gtrd_wy(ProjArgs a) {
     const int bb = aa + 1 + rem;
     double sacc = 0.0;
     if (bb < nr)
-      for (int i = jlo + 1 + lane; i < k; i += 32) sacc = fma(vb[aa * GT_KMAX + i], vb[bb * GT_KMAX + i], sacc);
+      for (int i = jlo + ro + lane; i < k; i += 32) sacc = fma(vb[aa * GT_KMAX + i], vb[bb * GT_KMAX + i], sacc);
     sacc = warp_sum(sacc);
     if (lane == 0) Gm[aa * GB_NR + bb] = sacc;
   }
@@ -962,7 +1746,8 @@ __global__ void __launch_bounds__(BM_NT, 1) k_gtrd_back(ProjArgs a) {
   if (gt.status[g] < 0) return;
   const int k = a.ksz[gt.task[g]];
   const int H = gt.hsel[g];
-  const GView W{gt.ws + gt.moff[g], k, H};
+  const GView W{gt.ws + gt.moff[g], k, H, k >= gt.sbr_min ? SB_NB : 1};
+  const int ro = W.ro;
   const int nsel = (int)W.hdr()[0];
   const int col0 = (item - gt.bt_pre[g]) * kGtrdBackCols;
   if (col0 >= nsel) return;
@@ -984,16 +1769,16 @@ __global__ void __launch_bounds__(BM_NT, 1) k_gtrd_back(ProjArgs a) {
   }
   const int ngr = W.nwy();
   for (int gi = 0; gi < ngr; ++gi) {
-    const int jhi = k - 3 - gi * GB_NR;
+    const int jhi = W.nref() - 1 - gi * GB_NR;
     const int nr = min(GB_NR, jhi + 1);
     const int jlo = jhi - nr + 1;
     __syncthreads();  // previous group's Y / U no longer read
     for (int e = t; e < GB_NR * k; e += BM_NT) {  // v_j lives in column j of M: c fastest
       const int c = e % GB_NR, i = e / GB_NR;
       const int j = jlo + c;
-      if (c >= nr || i < j + 1)
+      if (c >= nr || i < j + ro)
         Ys[c * BM_YLD + i] = 0.0;
-      else if (i == j + 1)
+      else if (i == j + ro)
         Ys[c * BM_YLD + i] = 1.0;
       else
         cp_async8(Ys + c * BM_YLD + i, M + (int64_t)i * LD + j);
@@ -1009,7 +1794,7 @@ __global__ void __launch_bounds__(BM_NT, 1) k_gtrd_back(ProjArgs a) {
       for (int m = 0; m < 2; ++m)
 #pragma unroll
         for (int n = 0; n < 2; ++n) acc[m][n][0] = acc[m][n][1] = 0.0;
-      const int kb = max(rb, (jlo + 1) & ~3);  // rows <= jlo are zero in Y
+      const int kb = max(rb, (jlo + ro) & ~3);  // rows < jlo + ro are zero in Y
       for (int kk = kb; kk < rb + RS; kk += 4) {
         const double a0 = Ys[r4 * BM_YLD + kk + c4], a1 = Ys[(8 + r4) * BM_YLD + kk + c4];
         const double b0 = Zs[(kk + c4) * 16 + r4], b1 = Zs[(kk + c4) * 16 + 8 + r4];
@@ -1043,7 +1828,7 @@ __global__ void __launch_bounds__(BM_NT, 1) k_gtrd_back(ProjArgs a) {
     // Zs(rows of this warp) -= Y(rows) U
     const double* U = Sp + 256;
     for (int it = 0; it < RS; it += 8) {
-      if (rb + it + 7 <= jlo) continue;  // Y rows <= jlo are zero
+      if (rb + it + 7 < jlo + ro) continue;  // Y rows < jlo + ro are zero
       double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
@@ -1217,7 +2002,7 @@ constexpr size_t kBackSmem = (size_t)(16 * BM_YLD + BM_ZROWS * 16 + BM_NW * 256 
 template <int MODE>
 void launch_mode(const ProjArgs& a, cudaStream_t s) {
   const GtrdDev& gt = a.gd.gt;
-  {
+  if (gt.njob) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(gt.njob * TC_CS);
     cfg.blockDim = dim3(TC_NT);
@@ -1232,11 +2017,28 @@ void launch_mode(const ProjArgs& a, cudaStream_t s) {
     cfg.numAttrs = 1;
     cudaLaunchKernelEx(&cfg, k_gtrd_tridiag<MODE>, a);
   }
+  if (gt.njob2) {  // two-stage: dense -> band (clusters of SA_CS CTAs) -> tridiagonal (a CTA each)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(gt.njob2 * SA_CS);
+    cfg.blockDim = dim3(SA_NT);
+    cfg.dynamicSmemBytes = kSbrASmem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = SA_CS;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k_sbr_band<MODE>, a);
+    k_sbr_chase<<<gt.nsb, SB_NT, kSbrBSmem, s>>>(a);
+  }
   if (gt.tot_ev) {
     k_gtrd_bisect<<<gt.tot_ev, 32, (size_t)2 * gt.kmax * sizeof(double), s>>>(a);
     k_gtrd_cluster<<<gt.ng, 32, (size_t)gt.kmax * sizeof(double), s>>>(a);
     k_gtrd_vec<<<gt.tot_vg, VT, (size_t)kVecSmemDoubles * sizeof(double), s>>>(a);
   }
+  if (gt.nsb && gt.tot_bt) k_sbr_q2<<<gt.tot_bt, SQ_NT, kSbrQSmem, s>>>(a);
   if (gt.tot_wy) k_gtrd_wy<<<gt.tot_wy, GB_NT, kWySmem, s>>>(a);
   if (gt.tot_bt) k_gtrd_back<<<gt.tot_bt, BM_NT, kBackSmem, s>>>(a);
   if (gt.tot_rc) k_gtrd_recon<MODE><<<(gt.tot_rc + GR_NW - 1) / GR_NW, GR_NW * 32, GR_NW * sizeof(GrSmem), s>>>(a);
@@ -1246,6 +2048,7 @@ void launch_mode(const ProjArgs& a, cudaStream_t s) {
 template <int MODE>
 void set_attrs() {
   cudaFuncSetAttribute(k_gtrd_tridiag<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmem);
+  cudaFuncSetAttribute(k_sbr_band<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSbrASmem);
   cudaFuncSetAttribute(k_gtrd_recon<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(GR_NW * sizeof(GrSmem)));
 }
 
@@ -1259,6 +2062,8 @@ void psd_gtrd_init_attributes() {
   cudaFuncSetAttribute(k_gtrd_vec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kVecSmemDoubles * sizeof(double)));
   cudaFuncSetAttribute(k_gtrd_back, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBackSmem);
   cudaFuncSetAttribute(k_gtrd_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWySmem);
+  cudaFuncSetAttribute(k_sbr_chase, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSbrBSmem);
+  cudaFuncSetAttribute(k_sbr_q2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSbrQSmem);
 }
 
 int gtrd_max_order() { return GT_KMAX; }

@@ -448,13 +448,25 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs a) {
         for (int j = 0; j < 6; ++j) a.red[j] = v[j];
       return;
     }
+  } else if (a.n_fix2) {
+    // packed primal exchange: the shared-coordinate eps_d partials are computed identically on
+    // every rank after the all-reduce (k_shared_fixup, all shared coordinates) and added here
+    auto gather2 = [&](const double* src, int n) {
+      for (int i = threadIdx.x; i < n; i += 256) {
+        v[3] += src[2 * (int64_t)i];
+        v[4] += src[2 * (int64_t)i + 1];
+      }
+    };
+    gather2(a.fix_part, a.n_fix2);
+    block_sum<6, 256>(v, sm);
+    __syncthreads();
   }
   if (FORM == 1)
     for (int i = threadIdx.x; i < a.m; i += 256) w[0] += a.b[i] * a.y[i];
   block_sum<1, 256>(w, sm + 48);
   if (threadIdx.x == 0) {
     if (PHASE == 2)
-      for (int j = 0; j < 6; ++j) v[j] = a.red[j];
+      for (int j = 0; j < 6; ++j) v[j] += a.red[j];
     const double np = sqrt(v[0]);
     const double den_p = fmax(fmax(sqrt(v[1]), sqrt(v[2])), 1.0);
     const double eps_p = np / den_p;
@@ -490,11 +502,14 @@ __global__ void __launch_bounds__(256) k_finalize(FinalArgs a) {
 // ---------------------------------------------------------------- shared-coordinate fixup
 // After the all-reduce of the scatter partials of coordinates shared across
 // ranks: r1 -> rD, eps_d partials (counted by the owner only), reset buffer.
+// With prevall != NULL (packed primal exchange) the eps_d partials cover EVERY shared coordinate,
+// from a replicated copy of the previous sums, so that every rank computes the same values and no
+// further all-reduce is needed.
 __global__ void __launch_bounds__(256) k_shared_fixup(int nshared, const int32_t* __restrict__ shared_local,
                                                        double* __restrict__ xbuf, const double* __restrict__ Dinv,
                                                        const double* __restrict__ own, double* __restrict__ rD,
                                                        double* __restrict__ sprev, double* __restrict__ part,
-                                                       const int* done) {
+                                                       const int* done, double* __restrict__ prevall) {
   if (done && *done) return;
   __shared__ double sm[2 * 8];
   const int j = blockIdx.x * 256 + threadIdx.x;
@@ -509,10 +524,16 @@ __global__ void __launch_bounds__(256) k_shared_fixup(int nshared, const int32_t
       rD[t] = r1 * Dinv[t];
       const double d = sx - sprev[t];
       sprev[t] = sx;
-      if (own[t] != 0.0) {
+      if (!prevall && own[t] != 0.0) {
         acc[0] = d * d;
         acc[1] = sl * sl;
       }
+    }
+    if (prevall) {
+      const double d = sx - prevall[j];
+      prevall[j] = sx;
+      acc[0] = d * d;
+      acc[1] = sl * sl;
     }
   }
   block_sum<2, 256>(acc, sm);
@@ -765,10 +786,10 @@ int fixup_blocks(int nshared) { return (nshared + 255) / 256; }
 
 void launch_shared_fixup(int nshared, const int32_t* shared_local, double* xbuf, const double* Dinv,
                          const double* own, double* rD, double* sprev, double* part, const int* done,
-                         cudaStream_t s) {
+                         cudaStream_t s, double* prevall) {
   if (nshared <= 0) return;
   k_shared_fixup<<<fixup_blocks(nshared), 256, 0, s>>>(nshared, shared_local, xbuf, Dinv, own, rD, sprev, part,
-                                                       done);
+                                                       done, prevall);
 }
 
 void launch_syrk_dense(const double* A, int64_t lda, int m, const double* Dinv, double* S, cudaStream_t s) {

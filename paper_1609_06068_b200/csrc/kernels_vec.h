@@ -36,6 +36,7 @@ struct FinalArgs {
   int n_gT;
   const double* fix_part;
   int n_fix;
+  int n_fix2;         // PHASE 2 of the packed primal exchange: fix partials gathered here
   double* red;        // 6 partial sums (PHASE 1 out, PHASE 2 in)
   const double* b;
   const double* y;
@@ -85,7 +86,7 @@ void launch_finalize(int form, int phase, const FinalArgs& a, cudaStream_t s);
 int fixup_blocks(int nshared);
 void launch_shared_fixup(int nshared, const int32_t* shared_local, double* xbuf, const double* Dinv,
                          const double* own, double* rD, double* sprev, double* part, const int* done,
-                         cudaStream_t s);
+                         cudaStream_t s, double* prevall = nullptr);
 void launch_syrk_dense(const double* A, int64_t lda, int m, const double* Dinv, double* S, cudaStream_t s);
 void launch_mask_cols(double* A, int64_t lda, int m, const double* mask, cudaStream_t s);
 void launch_place_dense(const double* raw, int64_t npat, int m, const int64_t* map, const double* scale, double* A,

@@ -630,6 +630,34 @@ def test_gtrd_forced_fallback_subprocess():
     _giant_env_batch({"SDP_GTRD_FORCE_FALLBACK": "1"})
 
 
+@pytest.mark.parametrize("sbr_min", ["65", "200"])
+def test_gtrd_two_stage_and_mixed_subprocess(sbr_min):
+    """SDP_GTRD_SBR_MIN=65: every giant takes the two-stage reduction (dense -> band by blocked
+    QR panels, band -> tridiagonal by bulge chasing, back-transform Q1 Q2); =200: orders below 200
+    the one-stage reduction, the others the two-stage one, in the same call."""
+    _giant_env_batch({"SDP_GTRD_SBR_MIN": sbr_min})
+
+
+def test_gtrd_two_stage_admm_subprocess():
+    """The two-stage reduction inside the ADMM iteration (max-cut, giant cliques, both forms)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L, sdp_inputs as gen\n"
+        "from oracle import admm, decompose as dc\n"
+        "prob = gen.maxcut_er(700, 21); dec = dc.decompose(prob)\n"
+        "r = lambda g, o: float(np.max(np.abs(g - o)) / np.max(np.abs(o)))\n"
+        "for form, rho in (('primal', 0.1), ('dual', 10.0)):\n"
+        "    st = admm.step(dec, admm.zero_state(dec), rho, form, 30)\n"
+        "    s = L.Solver(prob, form=form, rho=rho); s.step(30)\n"
+        "    e = max(r(s.x(), st.x), r(s.y(), st.y), r(s.blocks('xk'), st.xk), r(s.blocks('lambda'), st.lam))\n"
+        "    print(form, e); assert e <= 1e-9, e\n" % ROOT)
+    env = dict(os.environ, SDP_GTRD_SBR_MIN="65")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
 def test_giant_block_jacobi_only_subprocess():
     """SDP_GIANT_METHOD=jacobi: the giant tier without the tridiagonal path."""
     _giant_env_batch({"SDP_GIANT_METHOD": "jacobi"})
