@@ -145,12 +145,13 @@ void sdp_default_options(sdp_options* opt);
 /* Build the decomposed problem and upload it (host setup, run once; timed
  * separately, "Setup: Chordal decomposition, KKT factorization").
  * Sharding (world > 1, collective: every rank calls it with the same full
- * problem): cliques are split into contiguous ranges balanced by k^3, each rank
- * runs the projections of its cliques and the affine step on the coordinates
- * they touch; per iteration three NCCL all-reduces cross ranks (partial sums of
- * shared coordinates, the m-vector A D^-1 r1 over owned columns, 6 residual
- * scalars).  Getters of a sharded handle are collective and return the full
- * (global) vectors.
+ * problem): cliques are assigned to ranks by LPT on k^3 (sdp_shard_plan), each
+ * rank runs the projections of its cliques and the affine step on the
+ * coordinates they touch; per iteration the ranks all-reduce the partial sums of
+ * shared coordinates (with the 6 residual scalars packed behind them in the
+ * primal form) and the m-vector A D^-1 r1 over owned columns (the dual form adds
+ * a third all-reduce for its residual scalars).  Getters of a sharded handle are
+ * collective and return the full (global) vectors.
  * prob, opt: host, read during the call.  out: receives the handle.
  * Errors: SDP_E_INVALID_ARG (index out of range, row > col, duplicate entry,
  * n <= 0, m <= 0, clique order > SDP_MAX_K), SDP_E_RANK_DEFICIENT, SDP_E_CUDA,
@@ -308,13 +309,13 @@ int sdp_loopback_create(int32_t world, int32_t device, void** out);
 int sdp_loopback_destroy(void* group);
 
 /* Host-only shard plan of the pattern (row, col) for `rank` of `world`:
- * clique_begin[world+1] (contiguous ranges in canonical clique order),
- * local_coords[n_local] (pattern coordinates the rank's cliques touch, sorted),
- * owned[n_local] (1 if the rank owns the coordinate: its first clique is local),
- * shared_coords[n_shared] (coordinates touched by >= 2 ranks).  cap = capacity of
- * the coordinate buffers. */
+ * clique_rank[p] (the rank of every clique, canonical clique order: LPT on k^3 + 16, most
+ * expensive clique first, each to the least-loaded rank), local_coords[n_local] (pattern
+ * coordinates the rank's cliques touch, sorted), owned[n_local] (1 if the rank owns the coordinate:
+ * the rank of its first clique), shared_coords[n_shared] (coordinates touched by >= 2 ranks).
+ * cap = capacity of every output buffer (p <= cap). */
 int sdp_shard_plan(int32_t n, int64_t nnz, const int32_t* row, const int32_t* col, int32_t world, int32_t rank,
-                   int64_t* clique_begin, int64_t* n_local, int32_t* local_coords, uint8_t* owned,
+                   int32_t* clique_rank, int64_t* n_local, int32_t* local_coords, uint8_t* owned,
                    int64_t* n_shared, int32_t* shared_coords, int64_t cap);
 
 const char* sdp_last_error(void);

@@ -189,21 +189,24 @@ def nccl_unique_id():
 
 
 def shard_plan(n, row, col, world, rank):
-    """sdp_shard_plan: dict(clique_begin, local_coords, owned, shared_coords)."""
+    """sdp_shard_plan: dict(clique_rank, cliques (this rank's, ascending), local_coords, owned,
+    shared_coords)."""
     row = _arr(row, np.int32)
     col = _arr(col, np.int32)
     cap = max(16, int(n) * int(n))
     cap = min(cap, 1 << 26)
-    cb = np.zeros(world + 1, np.int64)
+    crank = np.zeros(cap, np.int32)
     loc = np.zeros(cap, np.int32)
     own = np.zeros(cap, np.uint8)
     shr = np.zeros(cap, np.int32)
     nl = C.c_int64()
     ns = C.c_int64()
-    _check(lib.sdp_shard_plan(n, row.size, _ptr(row), _ptr(col), world, rank, _ptr(cb), C.byref(nl), _ptr(loc),
+    _check(lib.sdp_shard_plan(n, row.size, _ptr(row), _ptr(col), world, rank, _ptr(crank), C.byref(nl), _ptr(loc),
                               _ptr(own), C.byref(ns), _ptr(shr), cap))
-    return {"clique_begin": cb, "local_coords": loc[:nl.value].copy(), "owned": own[:nl.value].astype(bool),
-            "shared_coords": shr[:ns.value].copy()}
+    p = len(chordal_cliques(n, row, col)[0])
+    cr = crank[:p].copy()
+    return {"clique_rank": cr, "cliques": np.flatnonzero(cr == rank), "local_coords": loc[:nl.value].copy(),
+            "owned": own[:nl.value].astype(bool), "shared_coords": shr[:ns.value].copy()}
 
 
 class TorchAllocator:

@@ -343,7 +343,8 @@ struct sdp_handle_s {
   // sharding: this rank's local view
   int world = 1, rank = 0;
   Comm* comm = nullptr;         // NCCL or in-process loopback (comm.cu)
-  int64_t cb = 0, pl = 0, Nl = 0, stotl = 0;  // first clique, local cliques / coordinates / stacked length
+  int64_t pl = 0, Nl = 0, stotl = 0;  // local cliques / coordinates / stacked length
+  std::vector<int32_t> my_cliques;    // this rank's cliques (canonical ids, ascending)
   std::vector<int32_t> local_coords;
   bool coord_perm = false;      // world == 1 with a permuted local coordinate order (pipelined iteration)
   double* own = nullptr;        // 1.0 on owned local coordinates
@@ -1533,7 +1534,9 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   if (h->world > p) throw Error{SDP_E_INVALID_ARG, "more ranks than cliques"};
   ShardPlan sp;
   if (h->world == 1) {
-    sp.clique_begin = {0, p};
+    sp.clique_rank.assign(p, 0);
+    sp.my_cliques.resize(p);
+    std::iota(sp.my_cliques.begin(), sp.my_cliques.end(), 0);
     sp.local_coords.resize(N);
     std::iota(sp.local_coords.begin(), sp.local_coords.end(), 0);
     sp.owned.assign(N, 1);
@@ -1555,10 +1558,16 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   } else {
     sp = make_shard_plan(ksz, off, seg_ptr, seg_idx, h->world, h->rank);
   }
-  const int64_t cb = sp.clique_begin[h->rank], ce = sp.clique_begin[h->rank + 1];
-  const int64_t pl = ce - cb, Nl = (int64_t)sp.local_coords.size();
-  const int64_t stotl = off[ce] - off[cb];
-  h->cb = cb;
+  const int64_t pl = (int64_t)sp.my_cliques.size(), Nl = (int64_t)sp.local_coords.size();
+  std::vector<int64_t> offl(pl + 1, 0);  // local stacked layout: this rank's cliques, canonical order
+  std::vector<int32_t> kszl(pl);
+  for (int64_t q = 0; q < pl; ++q) {
+    const int32_t k = sp.my_cliques[q];
+    offl[q + 1] = offl[q] + (off[k + 1] - off[k]);
+    kszl[q] = ksz[k];
+  }
+  const int64_t stotl = offl[pl];
+  h->my_cliques = sp.my_cliques;
   h->pl = pl;
   h->Nl = Nl;
   h->stotl = stotl;
@@ -1567,12 +1576,11 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   h->nshared = (int)sp.shared_coords.size();
   std::vector<int32_t> g2l(N, -1);
   for (int64_t i = 0; i < Nl; ++i) g2l[sp.local_coords[i]] = (int32_t)i;
-  std::vector<int64_t> offl(pl + 1);
-  std::vector<int32_t> kszl(pl);
-  for (int64_t k = 0; k <= pl; ++k) offl[k] = off[cb + k] - off[cb];
-  for (int64_t k = 0; k < pl; ++k) kszl[k] = ksz[cb + k];
   std::vector<int32_t> Gl(stotl);
-  for (int64_t s = 0; s < stotl; ++s) Gl[s] = g2l[Gmap[off[cb] + s]];
+  for (int64_t q = 0; q < pl; ++q) {
+    const int32_t k = sp.my_cliques[q];
+    for (int64_t e = 0; e < off[k + 1] - off[k]; ++e) Gl[offl[q] + e] = g2l[Gmap[off[k] + e]];
+  }
   std::vector<int32_t> segl_ptr(Nl + 1, 0), segl_idx(stotl);
   {
     std::vector<int32_t> cnt(Nl + 1, 0);
@@ -1654,18 +1662,20 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
       double* raw = al.get<double>((size_t)std::min<int64_t>(rows_per, m) * npat);
       int64_t* dmap = al.upload(map);
       double* dscale = al.upload(scale);
+      int* dbad = al.zeros<int>(1);
       for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
         const int64_t nr = std::min<int64_t>(rows_per, m - r0);
-        for (int64_t i = 0; i < nr * npat; ++i)
-          if (!std::isfinite(P->a_val[r0 * npat + i])) throw Error{SDP_E_INVALID_ARG, "A value not finite"};
         SDP_CUDA_TRY(cudaMemcpy(raw, P->a_val + r0 * npat, nr * npat * sizeof(double), cudaMemcpyHostToDevice));
-        launch_place_dense(raw, npat, (int)nr, dmap, dscale, h->A + r0 * h->lda, h->lda, nullptr);
+        launch_place_dense(raw, npat, (int)nr, dmap, dscale, h->A + r0 * h->lda, h->lda, nullptr, dbad);
         SDP_CUDA_TRY(cudaGetLastError());
-        SDP_CUDA_TRY(cudaDeviceSynchronize());
       }
+      int bad = 0;
+      SDP_CUDA_TRY(cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost));
+      if (bad) throw Error{SDP_E_INVALID_ARG, "A value not finite"};
       al.release(raw);
       al.release(dmap);
       al.release(dscale);
+      al.release(dbad);
     }
     // A^T copy over every local coordinate (x is needed on all of them) ...
     smark("A upload + placement");
@@ -2151,10 +2161,15 @@ int sdp_get_blocks(sdp_handle h, int32_t which, double* out) {
     if (!src) throw Error{SDP_E_INVALID_ARG, "unknown block id"};
     if (h->world == 1) {
       SDP_CUDA_TRY(cudaMemcpy(out, src, h->stot * sizeof(double), cudaMemcpyDeviceToHost));
-    } else {  // collective: every rank places its clique range
-      std::vector<double> full(h->stot, 0.0);
-      SDP_CUDA_TRY(cudaMemcpy(full.data() + h->clique_off[h->cb], src, h->stotl * sizeof(double),
-                              cudaMemcpyDeviceToHost));
+    } else {  // collective: every rank places its cliques
+      std::vector<double> loc(h->stotl), full(h->stot, 0.0);
+      SDP_CUDA_TRY(cudaMemcpy(loc.data(), src, h->stotl * sizeof(double), cudaMemcpyDeviceToHost));
+      int64_t e = 0;
+      for (int32_t k : h->my_cliques) {
+        const int64_t len = h->clique_off[k + 1] - h->clique_off[k];
+        std::memcpy(full.data() + h->clique_off[k], loc.data() + e, len * sizeof(double));
+        e += len;
+      }
       allreduce_host(h, full);
       std::memcpy(out, full.data(), h->stot * sizeof(double));
     }
@@ -2246,7 +2261,7 @@ int64_t layout_hash(sdp_handle h) {
   };
   mix((uint64_t)h->Nl);
   for (int32_t t : h->local_coords) mix((uint64_t)(uint32_t)t);
-  mix((uint64_t)h->cb);
+  for (int32_t k : h->my_cliques) mix((uint64_t)(uint32_t)k);
   mix((uint64_t)h->pl);
   return (int64_t)(x & 0x7fffffffffffffffull);
 }
@@ -2579,12 +2594,12 @@ int sdp_nccl_unique_id(void* out128) {
 }
 
 int sdp_shard_plan(int32_t n, int64_t nnz, const int32_t* row, const int32_t* col, int32_t world, int32_t rank,
-                   int64_t* clique_begin, int64_t* n_local, int32_t* local_coords, uint8_t* owned,
+                   int32_t* clique_rank, int64_t* n_local, int32_t* local_coords, uint8_t* owned,
                    int64_t* n_shared, int32_t* shared_coords, int64_t cap) {
   return guarded([&] {
     if (n <= 0 || world < 1 || rank < 0 || rank >= world) throw Error{SDP_E_INVALID_ARG, "bad n/world/rank"};
     if (nnz > 0 && (!row || !col)) throw Error{SDP_E_INVALID_ARG, "NULL pattern"};
-    if (!clique_begin || !n_local || !local_coords || !owned || !n_shared || !shared_coords)
+    if (!clique_rank || !n_local || !local_coords || !owned || !n_shared || !shared_coords)
       throw Error{SDP_E_INVALID_ARG, "NULL output"};
     check_indices("pattern", nnz, row, col, n);
     std::vector<std::pair<int32_t, int32_t>> edges;
@@ -2612,7 +2627,8 @@ int sdp_shard_plan(int32_t n, int64_t nnz, const int32_t* row, const int32_t* co
     for (int64_t s2 = 0; s2 < off[p]; ++s2) seg_idx[fillp[Gmap[s2]]++] = (int32_t)s2;
     if (world > p) throw Error{SDP_E_INVALID_ARG, "more ranks than cliques"};
     ShardPlan sp = make_shard_plan(ksz, off, seg_ptr, seg_idx, world, rank);
-    for (int r = 0; r <= world; ++r) clique_begin[r] = sp.clique_begin[r];
+    if (p > cap) throw Error{SDP_E_INVALID_ARG, "output buffers too small"};
+    std::memcpy(clique_rank, sp.clique_rank.data(), p * sizeof(int32_t));
     *n_local = (int64_t)sp.local_coords.size();
     *n_shared = (int64_t)sp.shared_coords.size();
     if (*n_local > cap || *n_shared > cap) throw Error{SDP_E_INVALID_ARG, "output buffers too small"};

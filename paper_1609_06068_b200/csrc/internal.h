@@ -47,7 +47,8 @@ int64_t coord_index(const ChordalResult& cr, int32_t i, int32_t j);  // -1 if ab
 // ---------------------------------------------------------------- sharding (shard.cpp)
 struct ShardPlan {
   int world = 1, rank = 0;
-  std::vector<int64_t> clique_begin;   // world + 1 boundaries of contiguous clique ranges
+  std::vector<int32_t> clique_rank;    // per clique (canonical order): its rank (LPT on k^3)
+  std::vector<int32_t> my_cliques;     // this rank's cliques, ascending
   std::vector<int32_t> local_coords;   // sorted global coordinates touched by this rank
   std::vector<uint8_t> owned;          // per local coordinate: 1 if this rank owns it
   std::vector<int32_t> shared_coords;  // sorted global coordinates touched by >= 2 ranks

@@ -9,6 +9,8 @@
 //   finalize  eps_p, eps_d, objective, stop flag   (reading G9)
 // All reductions are deterministic (fixed assignment and fixed tree order; no
 // floating-point atomics), so two runs give bit-identical iterates.
+#include <cstdlib>
+
 #include "kernels_vec.h"
 
 namespace sdp {
@@ -597,6 +599,95 @@ __global__ void __launch_bounds__(256) k_syrk_dense(const double* __restrict__ A
     }
 }
 
+// S = A D^-1 A^T for dense A (m x lda, row-major) on the FP64 tensor path: 128 x 128 output tiles
+// (upper tiles only: one wave of ~T(T+1)/2 CTAs for m = 2000, so A streams from DRAM about once),
+// 8 warps of 64 x 32 DMMA (mma.sync m8n8k4 f64) accumulators, K staged in chunks of 16 columns by
+// cp.async (double-buffered), D^-1 applied to the A fragments.  A diagonal tile writes only i <= j
+// (its mirror has a different rounding), so S is deterministic and exactly symmetric.
+constexpr int SY_T = 128, SY_K = 16, SY_LD = SY_K + 4, SY_NT = 256;
+constexpr size_t kSyrkSmem = (size_t)(2 * 2 * SY_T * SY_LD + 2 * SY_K) * sizeof(double);
+
+__device__ __forceinline__ void sy_cp16(double* sdst, const double* gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gsrc), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(SY_NT, 1) k_syrk_dmma(const double* __restrict__ A, int64_t lda, int m,
+                                                         const double* __restrict__ Dinv, double* __restrict__ S) {
+  const int nt = (m + SY_T - 1) / SY_T;
+  int bi = 0, rem = blockIdx.x;  // upper tile (bi <= bj) of this CTA, row by row
+  while (rem >= nt - bi) {
+    rem -= nt - bi;
+    ++bi;
+  }
+  const int bj = bi + rem;
+  const int i0 = bi * SY_T, j0 = bj * SY_T;
+  extern __shared__ double sy[];
+  double* As = sy;                          // [buf][r][kk], row stride SY_LD
+  double* Bs = As + 2 * SY_T * SY_LD;
+  double* Dv = Bs + 2 * SY_T * SY_LD;       // [buf][kk]
+  const int t = threadIdx.x, wid = t >> 5, lane = t & 31, r4 = lane >> 2, c4 = lane & 3;
+  const int wr = (wid >> 2) * 64, wc = (wid & 3) * 32;  // warp tile origin inside the CTA tile
+  auto load = [&](int buf, int64_t k0) {
+    for (int e = t; e < SY_T * (SY_K / 2); e += SY_NT) {
+      const int r = e / (SY_K / 2), q = (e % (SY_K / 2)) * 2;
+      sy_cp16(As + (buf * SY_T + r) * SY_LD + q, A + (int64_t)(i0 + r < m ? i0 + r : 0) * lda + k0 + q, i0 + r < m);
+      sy_cp16(Bs + (buf * SY_T + r) * SY_LD + q, A + (int64_t)(j0 + r < m ? j0 + r : 0) * lda + k0 + q, j0 + r < m);
+    }
+    if (t < SY_K / 2) sy_cp16(Dv + buf * SY_K + 2 * t, Dinv + k0 + 2 * t, true);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int64_t nk = lda / SY_K;  // lda is a multiple of 32
+  load(0, 0);
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    const int buf = (int)(kt & 1);
+    if (kt + 1 < nk) {
+      load(buf ^ 1, (kt + 1) * SY_K);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const double* as = As + (buf * SY_T + wr) * SY_LD;
+    const double* bs = Bs + (buf * SY_T + wc) * SY_LD;
+#pragma unroll
+    for (int ks = 0; ks < SY_K / 4; ++ks) {
+      const double dk = Dv[buf * SY_K + ks * 4 + c4];
+      double af[8], bf[4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) af[a] = as[(8 * a + r4) * SY_LD + ks * 4 + c4] * dk;
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bf[b] = bs[(8 * b + r4) * SY_LD + ks * 4 + c4];
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+              : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+              : "d"(af[a]), "d"(bf[b]));
+    }
+    __syncthreads();  // the next iteration's load overwrites this buffer
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = i0 + wr + 8 * a + r4, j = j0 + wc + 8 * b + 2 * c4 + h;
+        if (i < m && j < m && (bi != bj || i <= j)) {
+          S[(int64_t)i * m + j] = acc[a][b][h];
+          S[(int64_t)j * m + i] = acc[a][b][h];
+        }
+      }
+}
+
 // Zero the columns of A whose mask entry is 0 (non-owned coordinates of a rank).
 __global__ void k_mask_cols(double* __restrict__ A, int64_t lda, int m, const double* __restrict__ mask) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -605,12 +696,15 @@ __global__ void k_mask_cols(double* __restrict__ A, int64_t lda, int m, const do
 }
 
 // Column permutation + svec scaling of the user's dense-on-pattern A.
+// (sets *bad when an input value is not finite: the check runs on the device, not over the host array)
 __global__ void k_place_dense(const double* __restrict__ raw, int64_t npat, int m, const int64_t* __restrict__ map,
-                              const double* __restrict__ scale, double* __restrict__ A, int64_t lda) {
+                              const double* __restrict__ scale, double* __restrict__ A, int64_t lda, int* bad) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int i = blockIdx.y;
   if (e >= npat || i >= m) return;
-  if (map[e] >= 0) A[(int64_t)i * lda + map[e]] = raw[(int64_t)i * npat + e] * scale[e];
+  const double v = raw[(int64_t)i * npat + e];
+  if (!isfinite(v)) *bad = 1;
+  if (map[e] >= 0) A[(int64_t)i * lda + map[e]] = v * scale[e];
 }
 
 }  // namespace
@@ -793,6 +887,16 @@ void launch_shared_fixup(int nshared, const int32_t* shared_local, double* xbuf,
 }
 
 void launch_syrk_dense(const double* A, int64_t lda, int m, const double* Dinv, double* S, cudaStream_t s) {
+  if (lda % 32 == 0 && getenv("SDP_SYRK_SCALAR") == nullptr) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_syrk_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSyrkSmem);
+      attr = true;
+    }
+    const int nt = (m + SY_T - 1) / SY_T;
+    k_syrk_dmma<<<nt * (nt + 1) / 2, SY_NT, kSyrkSmem, s>>>(A, lda, m, Dinv, S);
+    return;
+  }
   const int nt = (m + 63) / 64;
   dim3 grid(nt, nt);
   k_syrk_dense<<<grid, 256, 0, s>>>(A, lda, m, Dinv, S);
@@ -803,9 +907,9 @@ void launch_mask_cols(double* A, int64_t lda, int m, const double* mask, cudaStr
 }
 
 void launch_place_dense(const double* raw, int64_t npat, int m, const int64_t* map, const double* scale, double* A,
-                        int64_t lda, cudaStream_t s) {
+                        int64_t lda, cudaStream_t s, int* bad) {
   dim3 grid((unsigned)((npat + 255) / 256), m);
-  k_place_dense<<<grid, 256, 0, s>>>(raw, npat, m, map, scale, A, lda);
+  k_place_dense<<<grid, 256, 0, s>>>(raw, npat, m, map, scale, A, lda, bad);
 }
 
 }  // namespace sdp

@@ -90,6 +90,6 @@ void launch_shared_fixup(int nshared, const int32_t* shared_local, double* xbuf,
 void launch_syrk_dense(const double* A, int64_t lda, int m, const double* Dinv, double* S, cudaStream_t s);
 void launch_mask_cols(double* A, int64_t lda, int m, const double* mask, cudaStream_t s);
 void launch_place_dense(const double* raw, int64_t npat, int m, const int64_t* map, const double* scale, double* A,
-                        int64_t lda, cudaStream_t s);
+                        int64_t lda, cudaStream_t s, int* bad);
 
 }  // namespace sdp

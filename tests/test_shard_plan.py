@@ -6,7 +6,8 @@
    CUDA path runs per rank (local scatter with c at the owner, all-reduce of the
    shared-coordinate partials, column-sharded A D^-1 r1 + all-reduce, replicated
    triangular solves, A^T y on the local coordinates, local projections,
-   all-reduce of the residual partials).  The assembled iterates must equal the
+   all-reduce of the residual partials), with the library's LPT clique assignment.  The assembled
+  iterates must equal the
    single-process oracle's to rounding: this checks that the plan's ownership
    and exchange sets are complete and that no partial is counted twice.
 """
@@ -38,14 +39,20 @@ def test_plan_invariants(gen, world):
         dec = dc.decompose(prob, factor=False)
         r, c = pattern_of(prob)
         plans = [L.shard_plan(prob.n, r, c, world, rk) for rk in range(world)]
-        cb = plans[0]["clique_begin"]
-        assert cb[0] == 0 and cb[-1] == dec.p and np.all(np.diff(cb) >= 0)
-        for pl in plans:
-            assert np.array_equal(pl["clique_begin"], cb)
+        crank = plans[0]["clique_rank"]
+        assert crank.shape == (dec.p,) and crank.min() >= 0 and crank.max() < world
+        assert len(np.unique(crank)) == world  # every rank has a clique
+        # LPT on k^3 + 16: the largest rank load is within the largest clique cost of the mean
+        cost = np.array([len(C) ** 3 + 16.0 for C in dec.cliques])
+        loads = np.array([cost[crank == rk].sum() for rk in range(world)])
+        assert loads.max() <= cost.sum() / world + cost.max() + 1e-9
+        for rk, pl in enumerate(plans):
+            assert np.array_equal(pl["clique_rank"], crank)
+            assert np.array_equal(pl["cliques"], np.flatnonzero(crank == rk))
             assert np.array_equal(pl["shared_coords"], plans[0]["shared_coords"])
         touch = np.zeros((world, dec.N), dtype=bool)
         for rk in range(world):
-            for k in range(cb[rk], cb[rk + 1]):
+            for k in np.flatnonzero(crank == rk):
                 touch[rk, dec.H[k]] = True
             want = np.flatnonzero(touch[rk])
             assert np.array_equal(plans[rk]["local_coords"], want)
@@ -60,7 +67,7 @@ def test_plan_invariants(gen, world):
         first = np.full(dec.N, -1)
         for k in range(dec.p):
             new = first[dec.H[k]] < 0
-            first[dec.H[k][new]] = np.searchsorted(cb, k, side="right") - 1
+            first[dec.H[k][new]] = crank[k]
         for rk in range(world):
             loc = plans[rk]["local_coords"]
             assert np.array_equal(plans[rk]["owned"], first[loc] == rk)
@@ -88,7 +95,6 @@ def _sharded_worker(rank, world, port, form, iters, out_dir):
     dec = dc.decompose(prob)
     r, c = pattern_of(prob)
     pl = L.shard_plan(prob.n, r, c, world, rank)
-    cb, ce = pl["clique_begin"][rank], pl["clique_begin"][rank + 1]
     loc, owned = pl["local_coords"], pl["owned"]
     own_mask = np.zeros(dec.N, dtype=bool)
     own_mask[loc[owned]] = True
@@ -97,7 +103,7 @@ def _sharded_worker(rank, world, port, form, iters, out_dir):
     A = dec.A.toarray() if hasattr(dec.A, "toarray") else dec.A
     c_own = np.where(own_mask, dec.c, 0.0)
     rho = 1.0
-    ks = range(cb, ce)
+    ks = [int(k) for k in pl["cliques"]]
     xk = {k: np.zeros(len(dec.H[k])) for k in ks}
     lam = {k: np.zeros(len(dec.H[k])) for k in ks}
     vk = {k: np.zeros(len(dec.H[k])) for k in ks}

@@ -1,0 +1,14 @@
+set -u
+OUT=gpurun_out/r2k
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+SDP_SETUP_TRACE=1 timeout 300 python -c "
+import sys; sys.path.insert(0,'.')
+import torch; torch.zeros(1).cuda()
+import paper_1609_06068_b200 as L, sdp_inputs as gen, time
+p = gen.config(2)
+t=time.time(); s = L.Solver(p, form='primal', rho=10.0); print('setup wall', time.time()-t)
+" > $OUT/setup_trace.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "iterates_after_50 or solve_objective or cfg2_full_size or cfg2_pipelined_path or affine" > $OUT/parity_sub.log 2>&1; echo "parity rc=$?" >> $OUT/rc.txt
+timeout 900 python -m pytest tests/test_gpu_boundary.py -q -m gpu -x -k "sharded" > $OUT/sharded.log 2>&1; echo "sharded rc=$?" >> $OUT/rc.txt
+timeout 900 python bench.py --also "" --no-cpu > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/rc.txt
