@@ -135,6 +135,9 @@ typedef struct {
   int32_t pipelined;         /* 1: the pipelined primal iteration is in use:
                               * sdp_step(n) overlaps the projections with the A passes of the
                               * neighbouring iterations; SDP_PIPELINE=0 at setup turns it off */
+  int32_t s_factor;          /* factorisation of S = A D^-1 A^T: 0 diagonal, 1 dense
+                              * Cholesky, 2 sparse Cholesky in a minimum-degree order */
+  int64_t nnz_l;             /* nonzeros of the Cholesky factor (0 when S is diagonal) */
 } sdp_info;
 
 typedef struct sdp_handle_s* sdp_handle;
@@ -317,6 +320,15 @@ int sdp_loopback_destroy(void* group);
 int sdp_shard_plan(int32_t n, int64_t nnz, const int32_t* row, const int32_t* col, int32_t world, int32_t rank,
                    int32_t* clique_rank, int64_t* n_local, int32_t* local_coords, uint8_t* owned,
                    int64_t* n_shared, int32_t* shared_coords, int64_t cap);
+
+/* ---- sparse Cholesky of S (host only) ------------------------------------
+ * The factorisation sdp_setup uses when S = A D^-1 A^T is sparse: minimum-degree order (the
+ * chordal analysis of S's graph), left-looking S = L L^T, G = L^-1 along elimination-tree paths.
+ * S given as CSR with both triangles (ptr[m+1], idx, val; host).  sinv (host, m*m row-major)
+ * receives G^T G = S^-1.  Returns SDP_E_RANK_DEFICIENT for a pivot <= 1e-12 S_ii, SDP_E_STATE
+ * if the factor is denser than m^2 / 8 and force_sparse == 0.  For tests and diagnostics. */
+int sdp_schur_inverse_host(int32_t m, const int64_t* ptr, const int32_t* idx, const double* val, int32_t force_sparse,
+                           double* sinv, int64_t* nnz_l);
 
 const char* sdp_last_error(void);
 

@@ -82,7 +82,7 @@ class sdp_info(C.Structure):
                 ("kmin", C.c_int64), ("kmax", C.c_int64), ("stot", C.c_int64), ("form", C.c_int32),
                 ("s_diagonal", C.c_int32), ("jacobi_capped", C.c_int64),
                 ("launches_per_iter", C.c_int32), ("jacobi_sweeps", C.c_int64), ("rho", C.c_double),
-                ("pipelined", C.c_int32)]
+                ("pipelined", C.c_int32), ("s_factor", C.c_int32), ("nnz_l", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -124,6 +124,7 @@ _sig = {
     "sdp_nccl_unique_id": (_i32, [_vp]),
     "sdp_shard_plan": (_i32, [_i32, _i64, _vp, _vp, _i32, _i32, _vp, C.POINTER(_i64), _vp, _vp, C.POINTER(_i64), _vp,
                               _i64]),
+    "sdp_schur_inverse_host": (_i32, [_i32, _vp, _vp, _vp, _i32, _vp, C.POINTER(_i64)]),
     "sdp_last_error": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _sig.items():
@@ -179,6 +180,23 @@ def chordal_cliques(n, row, col):
         out.append(verts[e:e + k].copy())
         e += k
     return out, int(fill.value)
+
+
+def schur_inverse_host(S, force_sparse=True):
+    """sdp_schur_inverse_host: S^-1 of a sparse SPD matrix (scipy sparse or dense) through the
+    library's sparse Cholesky; returns (S^-1 dense, nnz of the factor)."""
+    import scipy.sparse as sp
+    A = sp.csr_matrix(S)
+    A.sort_indices()
+    m = A.shape[0]
+    ptr = _arr(A.indptr, np.int64)
+    idx = _arr(A.indices, np.int32)
+    val = _arr(A.data, np.float64)
+    out = np.empty((m, m))
+    nnz = C.c_int64()
+    _check(lib.sdp_schur_inverse_host(m, _ptr(ptr), _ptr(idx), _ptr(val), int(bool(force_sparse)), _ptr(out),
+                                      C.byref(nnz)))
+    return out, int(nnz.value)
 
 
 def nccl_unique_id():

@@ -322,6 +322,8 @@ struct sdp_handle_s {
   int32_t *a_rp = nullptr, *a_ci = nullptr, *at_cp = nullptr, *at_ri = nullptr;
   double *a_val = nullptr, *at_val = nullptr;
   int s_diag = 0;
+  int s_factor = 0;      // 0: S diagonal, 1: dense Cholesky (host), 2: sparse Cholesky (sparse_chol.cpp)
+  int64_t nnz_l = 0;     // nonzeros of the sparse factor
   double* sdiag = nullptr;
   double *W = nullptr, *WT = nullptr, *Sinv = nullptr;
   double* gemv_part = nullptr;
@@ -1773,15 +1775,71 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
         gri[pos[en.t]] = en.con;
         gval[pos[en.t]++] = en.v;
       }
-      S.assign((size_t)m * m, 0.0);
+      // sparse S (both triangles, CSR by row): one entry per pair of constraints sharing a coordinate
+      struct Trip {
+        int32_t a, b;
+        double v;
+      };
+      std::vector<Trip> trip;
       for (int64_t t = 0; t < N; ++t)
         for (int e1 = gcp[t]; e1 < gcp[t + 1]; ++e1)
           for (int e2 = gcp[t]; e2 < gcp[t + 1]; ++e2)
-            S[(size_t)gri[e1] * m + gri[e2]] += gval[e1] * gval[e2] * Dinv_g[t];
+            trip.push_back({gri[e1], gri[e2], gval[e1] * gval[e2] * Dinv_g[t]});
+      std::stable_sort(trip.begin(), trip.end(),
+                       [](const Trip& x, const Trip& y) { return x.a != y.a ? x.a < y.a : x.b < y.b; });
+      std::vector<int64_t> sptr(m + 1, 0);
+      std::vector<int32_t> sidx;
+      std::vector<double> sval;
+      for (size_t q = 0; q < trip.size();) {
+        size_t r = q;
+        double acc = 0.0;
+        for (; r < trip.size() && trip[r].a == trip[q].a && trip[r].b == trip[q].b; ++r) acc += trip[r].v;
+        sidx.push_back(trip[q].b);
+        sval.push_back(acc);
+        sptr[trip[q].a + 1]++;
+        q = r;
+      }
+      for (int i = 0; i < m; ++i) sptr[i + 1] += sptr[i];
+      trip.clear();
+      trip.shrink_to_fit();
+      // sparse Cholesky of S (fill-reducing minimum degree) when its factor is sparse;
+      // SDP_SPARSE_S=0 never, =1 always (tests); default for m >= 256 and nnz(L) <= m^2 / 8
+      const char* ss = getenv("SDP_SPARSE_S");
+      const bool force = ss && *ss == '1', never = ss && *ss == '0';
+      bool done_sparse = false;
+      if (!never && (force || m >= 256)) {
+        const int64_t ldg = (m + 31) / 32 * 32;
+        std::vector<double> GT;
+        std::string why;
+        int64_t nnzl = 0;
+        if (sparse_inverse_factor(m, sptr, sidx, sval, ldg, GT, &nnzl, 0.125, force, &why)) {
+          double* dGT = al.upload(GT);
+          std::vector<double> ones(ldg, 1.0);
+          double* d1 = al.upload(ones);
+          h->Sinv = al.get<double>((size_t)m * m);
+          launch_syrk_dense(dGT, ldg, m, d1, h->Sinv, nullptr);  // S^-1 = G^T G
+          SDP_CUDA_TRY(cudaGetLastError());
+          SDP_CUDA_TRY(cudaDeviceSynchronize());
+          al.release(dGT);
+          al.release(d1);
+          symv_init_attributes(m);
+          h->s_factor = 2;
+          h->nnz_l = nnzl;
+          done_sparse = true;
+        } else if (why != "factor too dense") {
+          throw Error{SDP_E_RANK_DEFICIENT, why};
+        }
+      }
+      if (!done_sparse) {
+        S.assign((size_t)m * m, 0.0);
+        for (int i = 0; i < m; ++i)
+          for (int64_t e = sptr[i]; e < sptr[i + 1]; ++e) S[(size_t)i * m + sidx[e]] = sval[e];
+      }
     }
   }
   smark("S = A D^-1 A^T (+ D2H)");
-  if (!h->s_diag) {
+  if (!h->s_diag && h->s_factor != 2) {
+    h->s_factor = 1;
     if (!cholesky_host(S, m)) throw Error{SDP_E_RANK_DEFICIENT, "S = A D^-1 A^T is not positive definite"};
     smark("Cholesky (host)");
     std::vector<double> Wt;
@@ -1884,6 +1942,8 @@ void fill_info(sdp_handle h, sdp_info* info) {
   info->jacobi_sweeps = (int64_t)sw;
   info->rho = h->rho;
   info->pipelined = h->pipe.on ? 1 : 0;
+  info->s_factor = h->s_factor;
+  info->nnz_l = h->s_factor == 2 ? h->nnz_l : (h->s_factor == 1 ? (int64_t)h->m * (h->m + 1) / 2 : 0);
 }
 
 void launch_iterations(sdp_handle h, int32_t iters, bool for_solve = false) {
@@ -2635,6 +2695,35 @@ int sdp_shard_plan(int32_t n, int64_t nnz, const int32_t* row, const int32_t* co
     std::memcpy(local_coords, sp.local_coords.data(), sp.local_coords.size() * sizeof(int32_t));
     std::memcpy(owned, sp.owned.data(), sp.owned.size());
     std::memcpy(shared_coords, sp.shared_coords.data(), sp.shared_coords.size() * sizeof(int32_t));
+    return SDP_OK;
+  });
+}
+
+int sdp_schur_inverse_host(int32_t m, const int64_t* ptr, const int32_t* idx, const double* val, int32_t force_sparse,
+                           double* sinv, int64_t* nnz_l) {
+  return guarded([&] {
+    if (m <= 0 || !ptr || !idx || !val || !sinv) throw Error{SDP_E_INVALID_ARG, "bad argument"};
+    std::vector<int64_t> sp(ptr, ptr + m + 1);
+    std::vector<int32_t> si(idx, idx + sp[m]);
+    std::vector<double> sv(val, val + sp[m]);
+    for (int64_t e = 0; e < sp[m]; ++e)
+      if (si[e] < 0 || si[e] >= m) throw Error{SDP_E_INVALID_ARG, "column index out of range"};
+    const int64_t ldg = (m + 31) / 32 * 32;
+    std::vector<double> GT;
+    std::string why;
+    int64_t nnz = 0;
+    if (!sparse_inverse_factor(m, sp, si, sv, ldg, GT, &nnz, 0.125, force_sparse != 0, &why))
+      throw Error{why == "factor too dense" ? SDP_E_STATE : SDP_E_RANK_DEFICIENT, why};
+    if (nnz_l) *nnz_l = nnz;
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int a = 0; a < m; ++a)
+      for (int b = 0; b < m; ++b) {
+        const double* ga = GT.data() + (size_t)a * ldg;
+        const double* gb = GT.data() + (size_t)b * ldg;
+        double acc = 0.0;
+        for (int k = 0; k < m; ++k) acc += ga[k] * gb[k];
+        sinv[(size_t)a * m + b] = acc;
+      }
     return SDP_OK;
   });
 }

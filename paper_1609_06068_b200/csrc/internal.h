@@ -44,6 +44,14 @@ void complete_psd_host(int32_t n, const ChordalResult& cr, const std::vector<uin
 ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges);
 int64_t coord_index(const ChordalResult& cr, int32_t i, int32_t j);  // -1 if absent
 
+// Sparse Cholesky of S (sparse_chol.cpp): S given as CSR (both triangles); on success GT (m x ldg,
+// row-major) holds G^T with G = L^-1 (S = L L^T in a minimum-degree order), so S^-1 = G^T G.
+// Returns false with *why = "factor too dense" (nnz(L) > max_fill_frac m^2 and !force) or the
+// rank-deficiency message.
+bool sparse_inverse_factor(int m, const std::vector<int64_t>& sp, const std::vector<int32_t>& si,
+                           const std::vector<double>& sv, int64_t ldg, std::vector<double>& GT, int64_t* nnz_l,
+                           double max_fill_frac, bool force, std::string* why);
+
 // ---------------------------------------------------------------- sharding (shard.cpp)
 struct ShardPlan {
   int world = 1, rank = 0;

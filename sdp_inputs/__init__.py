@@ -195,6 +195,43 @@ def lovasz_theta_cycle(n: int = 5) -> Problem:
     )
 
 
+def sensor_network(n: int, radius: float, seed: int, name: str = "") -> Problem:
+    """Distance-constraint SDP on a random geometric graph (the sparse SDP class of sensor network
+    localisation, SDPA-type input with a sparse Schur complement; SURVEY 8(f) #3 stand-in for the
+    SDPLIB theta / qp instances of P:509-532, whose files are not available).
+
+    Draw order: P ~ U[0,1]^(n x 2) (vertex positions; edges = pairs closer than `radius`),
+    G ~ N(0,1)^(n x n), Coff ~ U(-1,1)^(#edges).  X0 = G G^T / n (strictly positive definite).
+    Constraint per edge (i, j): X_ii + X_jj - 2 X_ij = b_ij := the same of X0.
+    C = diagonally dominant on the graph: C_ij = Coff_ij / 2 on edges,
+    C_ii = 1 + sum_j |C_ij| (C > 0, so y = 0 is strictly dual feasible)."""
+    from scipy.spatial import cKDTree
+    rng = np.random.default_rng(seed)
+    P = rng.random((n, 2))
+    G = rng.standard_normal((n, n))
+    E = np.array(sorted(cKDTree(P).query_pairs(radius)), dtype=np.int64).reshape(-1, 2)
+    m = E.shape[0]
+    coff = 0.5 * rng.uniform(-1.0, 1.0, m)
+    i, j = E[:, 0], E[:, 1]
+    gi = np.einsum("ij,ij->i", G, G) / n                      # X0_ii
+    xij = np.einsum("ij,ij->i", G[i], G[j]) / n               # X0_ij on the edges
+    b = gi[i] + gi[j] - 2.0 * xij
+    cdiag = np.ones(n)
+    np.add.at(cdiag, i, np.abs(coff))
+    np.add.at(cdiag, j, np.abs(coff))
+    c_row = np.concatenate([np.arange(n), i]).astype(np.int32)
+    c_col = np.concatenate([np.arange(n), j]).astype(np.int32)
+    c_val = np.concatenate([cdiag, coff])
+    k = np.arange(m)
+    a_con = np.concatenate([k, k, k]).astype(np.int32)
+    a_row = np.concatenate([i, j, i]).astype(np.int32)
+    a_col = np.concatenate([i, j, j]).astype(np.int32)
+    a_val = np.concatenate([np.ones(m), np.ones(m), -np.ones(m)])
+    return Problem(name=name or f"sensor_n{n}_r{radius}_s{seed}", n=n, m=m, c_row=c_row, c_col=c_col,
+                   c_val=c_val, b=b, a_fmt="coo", a_con=a_con, a_row=a_row, a_col=a_col, a_val=a_val,
+                   meta={"kind": "sensor", "seed": seed, "edges": m})
+
+
 def scalar_primal() -> Problem:
     """n=1, min x s.t. x = 2, x >= 0 (objective 2)."""
     z = np.zeros(1, dtype=np.int32)

@@ -287,3 +287,61 @@ def test_sharded_loopback_solve_stops_together(lib, gen):
         gstatus, info = res[r]
         assert gstatus == status and info["iters"] == st.it
         assert abs(info["objective"] - st.objective) <= 1e-6 * abs(st.objective)
+
+
+# ------------------------------------------------------------------ sparse S
+
+@pytest.mark.parametrize("form", ["primal", "dual"])
+def test_sensor_network_sparse_schur(lib, gen, tmp_path, form):
+    """An SDPA instance with m >= 5000 (distance constraints on a random geometric graph, written
+    and read back through the SDPA reader): S = A D^-1 A^T is factorised by the sparse Cholesky
+    (s_factor 2, nnz(L) << m^2), and 30 iterations match the oracle (dense KKT) element by element."""
+    from paper_1609_06068_b200 import sdpa
+    prob = gen.sensor_network(2000, 0.032, seed=7)
+    assert prob.m >= 5000
+    path = tmp_path / "sensor.dat-s"
+    sdpa.write_sdpa(prob, str(path))
+    data = sdpa.read_sdpa(str(path))
+    dec = dc.decompose(data)
+    st = admm.step(dec, admm.zero_state(dec), 1.0, form, 30, record=True)
+    s = lib.Solver(data, form=form, rho=1.0)
+    info = s.info()
+    assert info["s_factor"] == 2 and info["nnz_l"] < prob.m * prob.m / 16
+    s.step(30)
+    for g, o in ((s.x(), st.x), (s.y(), st.y), (s.blocks("xk"), st.xk), (s.blocks("lambda"), st.lam)):
+        assert rel(g, o) <= 1e-9 and rel_inf(g, o) <= 1e-9
+    h = s.history()
+    o = np.array(st.history)
+    assert np.allclose(h[:, 2], o[:, 3], rtol=1e-9, atol=1e-12)
+    s.close()
+
+
+def test_forced_sparse_schur_subprocess():
+    """SDP_SPARSE_S=1 forces the sparse factorisation on small problems (dense-ish S included):
+    iterates still match the oracle."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L, sdp_inputs as gen\n"
+        "from oracle import admm, decompose as dc\n"
+        "r = lambda g, o: float(np.max(np.abs(g - o)) / np.max(np.abs(o)))\n"
+        "def coo(p):\n"
+        "    m, npat = p.a_val.shape\n"
+        "    p.a_con = np.repeat(np.arange(m, dtype=np.int32), npat)\n"
+        "    p.a_row = np.tile(p.a_row, m); p.a_col = np.tile(p.a_col, m); p.a_val = p.a_val.reshape(-1)\n"
+        "    p.a_fmt = 'coo'; return p\n"
+        "for prob in (coo(gen.block_arrow(4, 3, 2, 9, seed=2)), gen.sensor_network(60, 0.3, 2),\n"
+        "             gen.sensor_network(200, 0.12, 1)):\n"
+        "    dec = dc.decompose(prob)\n"
+        "    for form in ('primal', 'dual'):\n"
+        "        st = admm.step(dec, admm.zero_state(dec), 1.0, form, 40)\n"
+        "        s = L.Solver(prob, form=form, rho=1.0); assert s.info()['s_factor'] == 2, s.info()\n"
+        "        s.step(40)\n"
+        "        e = max(r(s.x(), st.x), r(s.y(), st.y), r(s.blocks('xk'), st.xk), r(s.blocks('lambda'), st.lam))\n"
+        "        print(prob.name, form, e); assert e <= 1e-9, e\n" % root)
+    env = dict(os.environ, SDP_SPARSE_S="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
