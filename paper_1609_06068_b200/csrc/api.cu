@@ -479,9 +479,10 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
     std::vector<int32_t>& jg = two ? job2_g : job_g;
     std::vector<int32_t>& jc = two ? job2_coop : job_coop;
     if (two) sb_g.push_back(g);
+    const int cs = two ? 8 : GTRD_CLUSTER;  // stage-A jobs use 8-CTA clusters
     if (kk >= coop_min) {
       jc.push_back(1);
-      for (int r = 0; r < 8; ++r) jg.push_back(r == 0 ? g : -1);
+      for (int r = 0; r < cs; ++r) jg.push_back(r == 0 ? g : -1);
     } else {
       (two ? solo2 : solo).push_back(g);
     }
@@ -490,9 +491,10 @@ void build_gtrd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<in
     std::vector<int>& so = pass ? solo2 : solo;
     std::vector<int32_t>& jg = pass ? job2_g : job_g;
     std::vector<int32_t>& jc = pass ? job2_coop : job_coop;
-    for (size_t i = 0; i < so.size(); i += 8) {
+    const size_t cs = pass ? 8 : GTRD_CLUSTER;
+    for (size_t i = 0; i < so.size(); i += cs) {
       jc.push_back(0);
-      for (size_t r = 0; r < 8; ++r) jg.push_back(i + r < so.size() ? so[i + r] : -1);
+      for (size_t r = 0; r < cs; ++r) jg.push_back(i + r < so.size() ? so[i + r] : -1);
     }
   }
   gt.njob = (int)job_coop.size();

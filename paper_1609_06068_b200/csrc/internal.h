@@ -215,6 +215,10 @@ void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_rv(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_giant(int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_gtrd(int mode, const ProjArgs& a, cudaStream_t s);
+// CTAs per thread-block cluster of the giant one-stage tridiagonalization (k_gtrd_tridiag jobs)
+#ifndef GTRD_CLUSTER
+#define GTRD_CLUSTER 8
+#endif
 // columns per back-transform CTA of the giant tridiagonal path (one warp each)
 constexpr int kGtrdBackCols = 16;
 // vector-kernel group capacity of the giant tridiagonal path for order k (shared-memory bound)

@@ -185,7 +185,7 @@ __device__ void tri_tail(const GView& W, double* d, double* e, int k, int t, int
 namespace cg = cooperative_groups;
 constexpr int TC_NT = 512;
 constexpr int TC_NB = 6;
-constexpr int TC_CS = 8;
+constexpr int TC_CS = GTRD_CLUSTER;  // CTAs per tridiagonalization cluster (16: non-portable size)
 constexpr int TC_NR = 1 + 2 * TC_NB;  // block-reduced values per column: |x|^2, W^T x, V^T x
 constexpr int TC_PS = GT_KMAX > TC_NT ? GT_KMAX : TC_NT;
 constexpr size_t kTriSmem =
@@ -2048,6 +2048,7 @@ void launch_mode(const ProjArgs& a, cudaStream_t s) {
 template <int MODE>
 void set_attrs() {
   cudaFuncSetAttribute(k_gtrd_tridiag<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTriSmem);
+  if (TC_CS > 8) cudaFuncSetAttribute(k_gtrd_tridiag<MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaFuncSetAttribute(k_sbr_band<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSbrASmem);
   cudaFuncSetAttribute(k_gtrd_recon<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(GR_NW * sizeof(GrSmem)));
 }
