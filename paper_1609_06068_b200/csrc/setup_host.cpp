@@ -11,8 +11,9 @@
 //  * cliques sorted ascending inside and lexicographically as a list
 //    (reading G14); coordinates of E' in column-major upper order.
 //
-// Adjacency is a dense bitset (n^2/8 bytes): n <= 46340 in this build.
+// Adjacency is a dense bitset (n^2/8 bytes) for n <= 46340, sorted adjacency lists beyond.
 #include <algorithm>
+#include <cstdlib>
 #include <set>
 #include <stdexcept>
 
@@ -24,8 +25,10 @@ namespace {
 inline int popc(uint64_t x) { return __builtin_popcountll(x); }
 }  // namespace
 
-ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges) {
-  if (n > 46340) throw Error{SDP_E_INVALID_ARG, "n > 46340 not supported by the bitset chordal analysis"};
+// Exact minimum degree on a dense bitset (fast for n up to ~5e4: one word op per 64 vertices).
+// Fills later[v] (v's not-yet-eliminated neighbours when it is eliminated) and pos[v].
+int64_t eliminate_bitset(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges,
+                         std::vector<std::vector<int32_t>>& later, std::vector<int32_t>& pos) {
   const int64_t W = (n + 63) / 64;
   std::vector<uint64_t> adj((size_t)n * W, 0ull);
   auto row = [&](int v) { return adj.data() + (size_t)v * W; };
@@ -42,7 +45,7 @@ ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, i
   }
   std::vector<uint64_t> alive(W, ~0ull);
   if (n % 64) alive[W - 1] = (1ull << (n % 64)) - 1ull;
-  std::vector<int32_t> deg(n), pos(n);
+  std::vector<int32_t> deg(n);
   std::set<std::pair<int32_t, int32_t>> queue;
   for (int v = 0; v < n; ++v) {
     int d = 0;
@@ -51,7 +54,6 @@ ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, i
     deg[v] = d;
     queue.insert({d, v});
   }
-  std::vector<std::vector<int32_t>> later(n);
   std::vector<uint64_t> nbmask(W);
   for (int step = 0; step < n; ++step) {
     auto it = queue.begin();  // smallest degree, then smallest index
@@ -87,6 +89,72 @@ ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, i
       }
     }
   }
+  return e0;
+}
+
+// The same elimination on sorted adjacency lists of the alive vertices (O(n + fill) memory; no
+// order limit): eliminating v replaces adj(u) by (adj(u) U N(v)) \ {u, v} for every u in N(v).
+int64_t eliminate_sparse(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges,
+                         std::vector<std::vector<int32_t>>& later, std::vector<int32_t>& pos) {
+  std::vector<std::vector<int32_t>> adj(n);
+  for (auto& e : edges) {
+    if (e.first == e.second) continue;
+    adj[e.first].push_back(e.second);
+    adj[e.second].push_back(e.first);
+  }
+  int64_t e0 = 0;
+  for (int v = 0; v < n; ++v) {
+    std::sort(adj[v].begin(), adj[v].end());
+    adj[v].erase(std::unique(adj[v].begin(), adj[v].end()), adj[v].end());
+    e0 += (int64_t)adj[v].size();
+  }
+  e0 /= 2;
+  std::set<std::pair<int32_t, int32_t>> queue;
+  for (int v = 0; v < n; ++v) queue.insert({(int32_t)adj[v].size(), v});
+  std::vector<int32_t> merged;
+  for (int step = 0; step < n; ++step) {
+    auto it = queue.begin();
+    const int v = it->second;
+    queue.erase(it);
+    pos[v] = step;
+    std::vector<int32_t>& nb = later[v];
+    nb = std::move(adj[v]);  // alive neighbours only (eliminated vertices are removed below)
+    adj[v].clear();
+    for (int u : nb) {
+      const std::vector<int32_t>& au = adj[u];
+      merged.clear();
+      size_t a = 0, b = 0;
+      while (a < au.size() || b < nb.size()) {
+        int32_t x;
+        if (b == nb.size() || (a < au.size() && au[a] < nb[b]))
+          x = au[a++];
+        else if (a == au.size() || nb[b] < au[a])
+          x = nb[b++];
+        else {
+          x = au[a++];
+          ++b;
+        }
+        if (x != u && x != v) merged.push_back(x);
+      }
+      const int32_t d0 = (int32_t)au.size();
+      adj[u].swap(merged);
+      if ((int32_t)adj[u].size() != d0) {
+        queue.erase({d0, u});
+        queue.insert({(int32_t)adj[u].size(), u});
+      }
+    }
+  }
+  return e0;
+}
+
+ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, int32_t>>& edges) {
+  // bitset for n <= 46340 (n^2 / 8 bytes), sorted lists beyond (or SDP_CHORDAL_SPARSE=1);
+  // both give the same elimination (exact minimum degree, lowest index on ties)
+  const char* sp = getenv("SDP_CHORDAL_SPARSE");
+  const bool sparse = n > 46340 || (sp && *sp == '1');
+  std::vector<std::vector<int32_t>> later(n);
+  std::vector<int32_t> pos(n);
+  const int64_t e0 = sparse ? eliminate_sparse(n, edges, later, pos) : eliminate_bitset(n, edges, later, pos);
   ChordalResult cr;
   cr.order.resize(n);
   for (int v = 0; v < n; ++v) cr.order[pos[v]] = v;
@@ -115,27 +183,29 @@ ChordalResult chordal_analysis(int32_t n, const std::vector<std::pair<int32_t, i
     cr.cliques.push_back(std::move(K));
   }
   std::sort(cr.cliques.begin(), cr.cliques.end());
-  // extended pattern E' (+ diagonal) in canonical order
-  int64_t e1 = 0;
+  // extended pattern E' (+ diagonal) in canonical order: every edge of the filled graph joins a
+  // vertex to one of its later neighbours
+  std::vector<int64_t> cnt(n + 1, 0);
+  for (int v = 0; v < n; ++v)
+    for (int u : later[v]) cnt[std::max(u, v) + 1]++;
+  for (int j = 0; j < n; ++j) cnt[j + 1] += cnt[j] + 1;  // + the diagonal entry of each column
+  const int64_t tot = cnt[n];
+  cr.coord_row.assign(tot, 0);
+  cr.coord_col.assign(tot, 0);
+  std::vector<int64_t> fillp(cnt.begin(), cnt.end() - 1);
+  for (int v = 0; v < n; ++v)
+    for (int u : later[v]) {
+      const int j = std::max(u, v);
+      cr.coord_row[fillp[j]++] = std::min(u, v);
+    }
   cr.col_ptr.assign(n + 1, 0);
   for (int j = 0; j < n; ++j) {
-    const uint64_t* rj = row(j);
-    for (int64_t w = 0; w <= (j >> 6); ++w) {
-      uint64_t m = rj[w];
-      if (w == (j >> 6)) m &= (j & 63) ? ((1ull << (j & 63)) - 1ull) : 0ull;
-      while (m) {
-        int b = __builtin_ctzll(m);
-        cr.coord_row.push_back((int32_t)(w * 64 + b));
-        cr.coord_col.push_back(j);
-        ++e1;
-        m &= m - 1;
-      }
-    }
-    cr.coord_row.push_back(j);
-    cr.coord_col.push_back(j);
-    cr.col_ptr[j + 1] = (int64_t)cr.coord_row.size();
+    std::sort(cr.coord_row.begin() + cnt[j], cr.coord_row.begin() + fillp[j]);
+    cr.coord_row[fillp[j]] = j;  // diagonal last (rows < j first)
+    for (int64_t e = cnt[j]; e <= fillp[j]; ++e) cr.coord_col[e] = j;
+    cr.col_ptr[j + 1] = cnt[j + 1];
   }
-  cr.fill_edges = e1 - e0;
+  cr.fill_edges = (tot - n) - e0;
   return cr;
 }
 

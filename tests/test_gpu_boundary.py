@@ -366,3 +366,26 @@ def test_sensor_network_solve_to_tolerance(lib, gen):
     assert info["iters"] == st.it
     assert abs(info["objective"] - st.objective) <= 1e-6 * abs(st.objective)
     s.close()
+
+
+@pytest.mark.parametrize("delta", [1e-2, 1e-3])
+def test_ill_conditioned_schur(lib, gen, delta):
+    """The iteration applies the cached S^-1 = G^T G (one mat-vec) while the oracle solves with the
+    Cholesky factor; both are accurate to O(cond(S) eps).  Block-arrow with two nearly dependent
+    constraints (A_m = A_{m-1} + delta R): cond(S) ~ 1e4 .. 1e6, and 50 iterations still match the
+    oracle to 1e-9."""
+    prob = gen.block_arrow(7, 3, 3, 11, seed=5)
+    rng = np.random.default_rng(9)
+    prob.a_val = prob.a_val.copy()
+    prob.a_val[-1] = prob.a_val[-2] + delta * rng.uniform(-1, 1, prob.a_val.shape[1])
+    dec = dc.decompose(prob)
+    S = (dec.A / dec.D) @ dec.A.T
+    cond = np.linalg.cond(S)
+    assert cond > 1e3
+    for form in ("primal", "dual"):
+        st = admm.step(dec, admm.zero_state(dec), 1.0, form, 50)
+        s = lib.Solver(prob, form=form, rho=1.0)
+        s.step(50)
+        for g, o in ((s.x(), st.x), (s.y(), st.y), (s.blocks("xk"), st.xk), (s.blocks("lambda"), st.lam)):
+            assert rel(g, o) <= 1e-9, (form, cond, rel(g, o))
+        s.close()

@@ -2,6 +2,7 @@
 in include/chordal_sdp.h, and its host-side chordal analysis (C++) produces the
 same cliques as the oracle (Python) -- two independent implementations of the
 rules in DESIGN.md reading G13/G14.  No GPU compute is called."""
+import os
 import re
 import subprocess
 
@@ -94,3 +95,28 @@ def test_sharded_setup_option_validation(gen):
         lib_mod.Solver(prob, world=2, rank=0)
     with pytest.raises(lib_mod.SdpError, match="rank"):
         lib_mod.Solver(prob, world=2, rank=2, nccl_id=b"\0" * 128)
+
+
+def test_sparse_elimination_equals_bitset(gen):
+    """The sorted-adjacency-list minimum-degree elimination (used for n > 46340, or with
+    SDP_CHORDAL_SPARSE=1) gives exactly the bitset elimination's cliques and fill (reading G13)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, json, numpy as np; sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L, sdp_inputs as gen\n"
+        "out = []\n"
+        "for prob in (gen.maxcut_er(3000, 1003), gen.config(1), gen.maxcut_er(500, 7), gen.sensor_network(400, 0.08, 2)):\n"
+        "    r = np.concatenate([prob.c_row, prob.a_row]); c = np.concatenate([prob.c_col, prob.a_col])\n"
+        "    cl, fill = L.chordal_cliques(prob.n, r, c)\n"
+        "    out.append([[x.tolist() for x in cl], fill])\n"
+        "print(json.dumps(out))\n" % root)
+    res = []
+    for env in ({}, {"SDP_CHORDAL_SPARSE": "1"}):
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **env), capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr
+        res.append(json.loads(r.stdout.strip().splitlines()[-1]))
+    assert res[0] == res[1]
