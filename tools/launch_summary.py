@@ -4,7 +4,7 @@ import collections
 import csv
 import sys
 
-SETUP = ("k_syrk_dense", "k_place_dense", "k_transpose", "k_mask_cols")
+SETUP = ("k_syrk_dmma", "k_syrk_dense", "k_place_dense", "k_transpose", "k_mask_cols")
 
 
 def main(path):
