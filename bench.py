@@ -338,6 +338,17 @@ def run_ours(args, rank, world, local):
                 "algorithmic_flops_per_launch": fl, "peak_src": peaks["fp64_src"]}
     total_phase = sum(phases.values())
     roof["share_of_step"] = phases[dom] / total_phase if total_phase > 0 else None
+    fused = bool(info.get("fused"))
+    if fused:
+        # one kernel (k_fused_iter) runs the whole iteration: its roofline is the iteration's
+        # algorithmic bytes (A and A^T read once each, S^-1, the stacked and N-vectors) over the
+        # measured step time, against the copy bandwidth; phases_ms (per-phase kernels on the
+        # same handle, diagnostics only) say where an unfused iteration would spend its time
+        roof = {"bound": "hbm", "kernel": "k_fused_iter", "achieved": B / (ms / 1e3) / 1e9,
+                "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": B / (ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                "traffic": traffic_lookup(wl, "fused"), "algorithmic_bytes_per_launch": B,
+                "peak_src": peaks["hbm_src"], "share_of_step": 1.0,
+                "note": "latency-bound regime: one cooperative launch per step, L2 flushed before it"}
     out.update({
         "value": it_s, "unit": "iterations/s", "ms_per_step": ms,
         "projections_per_s": it_s * info["p"],
@@ -353,7 +364,8 @@ def run_ours(args, rank, world, local):
         "step_roofline": {"algorithmic_bytes": B, "algorithmic_flops": F, "t_roof_ms": t_roof * 1e3,
                           "frac": t_roof * 1e3 / ms, "model": "SURVEY 8(d) / DESIGN.md Roofline"},
         "phases_ms": phases,
-        "gpu_launches": int(fin["launches_per_iter"]) * args.steps,
+        "fused_iteration": fused,
+        "gpu_launches": (args.steps if (flush or not fused) else 1) * (1 if fused else int(fin["launches_per_iter"])),
         "clocks": clk.summary(),
         "setup_s": setup_wall,
         "residuals_after": {"iters": fin["iters"], "eps_p": fin["eps_p"], "eps_d": fin["eps_d"],

@@ -138,6 +138,10 @@ typedef struct {
   int32_t s_factor;          /* factorisation of S = A D^-1 A^T: 0 diagonal, 1 dense
                               * Cholesky, 2 sparse Cholesky in a minimum-degree order */
   int64_t nnz_l;             /* nonzeros of the Cholesky factor (0 when S is diagonal) */
+  int32_t fused;             /* 1: the fused persistent iteration is in use (small single-rank
+                              * problems, all cliques k <= 32): one
+                              * cooperative kernel launch per sdp_step / sdp_solve call runs every
+                              * phase of every iteration.  SDP_FUSED=0 at setup turns it off */
 } sdp_info;
 
 typedef struct sdp_handle_s* sdp_handle;

@@ -82,7 +82,8 @@ class sdp_info(C.Structure):
                 ("kmin", C.c_int64), ("kmax", C.c_int64), ("stot", C.c_int64), ("form", C.c_int32),
                 ("s_diagonal", C.c_int32), ("jacobi_capped", C.c_int64),
                 ("launches_per_iter", C.c_int32), ("jacobi_sweeps", C.c_int64), ("rho", C.c_double),
-                ("pipelined", C.c_int32), ("s_factor", C.c_int32), ("nnz_l", C.c_int64)]
+                ("pipelined", C.c_int32), ("s_factor", C.c_int32), ("nnz_l", C.c_int64),
+                ("fused", C.c_int32)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "kernels_fused.h"
 #include "kernels_vec.h"
 
 namespace sdp {
@@ -364,6 +365,17 @@ struct sdp_handle_s {
   int32_t *shared_idx = nullptr, *shared_local = nullptr;
   double *xbuf = nullptr, *fix_part = nullptr, *red = nullptr;
   double* prevall = nullptr;    // packed primal exchange: previous sums of every shared coordinate
+  // fused persistent iteration (kernels_fused.cu): small single-rank problems
+  bool fused = false;
+  int fused_nb = 1, fused_usplit = 1;
+  int32_t* fused_ids[3] = {nullptr, nullptr, nullptr};
+  int fused_count[3] = {0, 0, 0};
+  double *fused_upart = nullptr, *fused_cpart = nullptr;
+  unsigned* fused_bar = nullptr;
+  int fused_parity = 0;
+  int fused_xl = 32, fused_ul = 1, fused_nlong = 0;
+  int32_t* fused_longc = nullptr;
+  long long* fused_trace = nullptr;
 };
 
 struct sdp_psd_plan_s {
@@ -1298,6 +1310,7 @@ void enqueue_iteration(sdp_handle h, cudaStream_t s) {
 
 int pipe_launches_per_iter(sdp_handle h);
 int launches_per_iter(sdp_handle h) {
+  if (h->fused) return 1;  // one launch per sdp_step call (any number of iterations)
   if (h->pipe.on) return pipe_launches_per_iter(h);
   int n = 0;
   for (int b = 0; b < B_NUM; ++b) {  // one launch per non-empty tier; 3 per chunk for the QL tiers
@@ -1328,7 +1341,7 @@ void rebuild_graph(sdp_handle h) {
     cudaGraphDestroy(h->graph);
     h->graph = nullptr;
   }
-  if (!h->use_graph) return;
+  if (!h->use_graph || h->fused) return;
   if (h->pipe.on && h->form == SDP_FORM_PRIMAL) {
     // A and BA captured (per-node priorities).  Multi-iteration calls launch directly (the launches
     // stream ahead of the device: 1128 vs 1107 it/s on cfg2); one- and two-iteration calls replay the
@@ -1397,6 +1410,7 @@ void destroy_handle(sdp_handle h) {
   delete h;
 }
 
+void build_fused(sdp_handle h, const std::vector<int>& task_bucket);
 int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out) {
   auto t0 = std::chrono::steady_clock::now();
   // SDP_SETUP_TRACE=1: wall time of the setup phases on stderr
@@ -1915,6 +1929,7 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     h->vprev_len = voff[pl];
   }
   build_pipeline(h, Gl, offl, segl_ptr, task_bucket);
+  build_fused(h, task_bucket);
   psd_init_attributes();
   SDP_CUDA_TRY(cudaDeviceSynchronize());
   reset_state(h);
@@ -1963,11 +1978,187 @@ void fill_info(sdp_handle h, sdp_info* info) {
   info->jacobi_sweeps = (int64_t)sw;
   info->rho = h->rho;
   info->pipelined = h->pipe.on ? 1 : 0;
+  info->fused = h->fused ? 1 : 0;
   info->s_factor = h->s_factor;
   info->nnz_l = h->s_factor == 2 ? h->nnz_l : (h->s_factor == 1 ? (int64_t)h->m * (h->m + 1) / 2 : 0);
 }
 
+// The fused persistent iteration (kernels_fused.cu) replaces the per-phase launches for small
+// single-rank problems whose cliques all fit the register-V groups (k <= 32): one cooperative
+// launch per sdp_step / solve chunk.  SDP_FUSED=0 turns it off, =1 takes it whenever the problem
+// is structurally eligible (default: also A + A^T <= 64 MB and p <= 8192); SDP_FUSED_CTAS fixes
+// the grid.
+void build_fused(sdp_handle h, const std::vector<int>& task_bucket) {
+  h->fused = false;
+  const char* env = getenv("SDP_FUSED");
+  if (env && *env == '0') return;
+  const bool force = env && *env == '1';
+  if (h->world != 1 || h->pipe.on || h->pl < 1) return;
+  for (int b = 0; b < B_NUM; ++b)
+    if (h->bcount[b] && b != B_RV8 && b != B_RV16 && b != B_RV32 && b != B_WJ32) return;
+  if (!h->s_diag && h->m > fused_max_m()) return;
+  int64_t nnzA = 0;
+  if (!h->a_dense) {
+    int32_t last = 0;
+    SDP_CUDA_TRY(cudaMemcpy(&last, h->a_rp + h->m, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    nnzA = last;
+  }
+  const double bytes = h->a_dense ? 8.0 * ((double)h->m * h->lda + (double)h->Nl * h->ldm) : 24.0 * (double)nnzA;
+  if (!force && (bytes > 64e6 || h->pl > 8192)) return;
+  const int maxc = fused_max_ctas(h->device);
+  int nsm = 0;
+  SDP_CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
+  if (maxc < 1) return;
+  std::vector<int32_t> lists[3];
+  for (int64_t q = 0; q < h->pl; ++q) {
+    const int b = task_bucket[q];
+    lists[b == B_RV8 ? 0 : b == B_RV16 ? 1 : 2].push_back((int32_t)q);
+  }
+  // groups per 256-thread CTA: 16 (k <= 8), 4 (k <= 16), 2 (k <= 32)
+  const int64_t proj = std::max({((int64_t)lists[0].size() + 15) / 16, ((int64_t)lists[1].size() + 3) / 4,
+                                 ((int64_t)lists[2].size() + 1) / 2});
+  const int64_t bw = (int64_t)std::ceil(bytes / 98304.0);
+  int64_t nb = std::max<int64_t>(1, std::max(proj, bw));
+  nb = std::min<int64_t>(nb, std::min(maxc, nsm));
+  if (const char* c = getenv("SDP_FUSED_CTAS")) nb = std::max(1, std::min(maxc, atoi(c)));
+  h->fused_nb = (int)nb;
+  h->fused_usplit = (int)std::max<int64_t>(1, std::min<int64_t>(16, nb * (kFusedThreads / 32) / h->m));
+  Alloc& al = h->alloc;
+  for (int j = 0; j < 3; ++j) {
+    h->fused_count[j] = (int)lists[j].size();
+    h->fused_ids[j] = lists[j].empty() ? nullptr : al.upload(lists[j]);
+  }
+  h->fused_upart = al.zeros<double>((size_t)h->fused_usplit * h->m);
+  h->fused_cpart = al.zeros<double>(8 * (size_t)nb);
+  h->fused_bar = al.zeros<unsigned>(2);
+  // phase X: lanes per coordinate ~ a quarter of the row's double pairs (power of two <= 32)
+  // (sparse A: lanes per row / coordinate ~ half the mean entry count)
+  const double np = h->a_dense ? (h->m + 1) / 2 : 0.5 * (double)nnzA / std::max<int64_t>(1, h->Nl);
+  h->fused_xl = 1;
+  while (h->fused_xl < 32 && h->fused_xl * (h->a_dense ? 4 : 1) < np) h->fused_xl *= 2;
+  h->fused_ul = 1;
+  while (!h->a_dense && h->fused_ul < 32 && h->fused_ul < 0.5 * (double)nnzA / h->m) h->fused_ul *= 2;
+  // scatter: coordinates with long segments (a warp each)
+  std::vector<int32_t> segp(h->Nl + 1), lc;
+  SDP_CUDA_TRY(cudaMemcpy(segp.data(), h->seg_ptr, segp.size() * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  for (int64_t t = 0; t < h->Nl; ++t)
+    if (segp[t + 1] - segp[t] > kFusedLongSeg) lc.push_back((int32_t)t);
+  h->fused_nlong = (int)lc.size();
+  h->fused_longc = lc.empty() ? nullptr : al.upload(lc);
+  h->fused = true;
+}
+
+FusedArgs fused_args(sdp_handle h, int iters) {
+  FusedArgs a;
+  a.iters = iters;
+  a.nb = h->fused_nb;
+  a.m = h->m;
+  a.N = (int)h->Nl;
+  a.p = (int)h->pl;
+  a.lda = h->lda;
+  a.ldm = h->ldm;
+  a.stot = h->stotl;
+  a.usplit = h->fused_usplit;
+  a.rho = h->rho;
+  a.A = h->A;
+  a.AT = h->AT;
+  a.Sinv = h->s_diag ? nullptr : h->Sinv;
+  a.sdiag = h->s_diag ? h->sdiag : nullptr;
+  a.b = h->b;
+  a.c = h->c;
+  a.Dinv = h->Dinv;
+  a.own = h->own;
+  a.rD = h->rD;
+  a.x = h->x;
+  a.y = h->y;
+  a.upart = h->fused_upart;
+  a.sprev = h->sprev;
+  a.vk = h->vk;
+  a.seg_ptr = h->seg_ptr;
+  a.seg_idx = h->seg_idx;
+  ProjArgs& p = a.pa;
+  p.off = h->d_off;
+  p.ksz = h->d_ksz;
+  p.x = h->x;
+  p.G = h->G;
+  p.xk = h->xk;
+  p.lam = h->lam;
+  p.vk = h->vk;
+  p.rho = h->rho;
+  p.part = h->proj_part;
+  p.capped = h->capped;
+  p.sweeps = h->sweeps;
+  p.vprev = h->vprev;
+  p.voff = h->voff;
+  p.warm_period = h->warm_period;
+  for (int j = 0; j < 3; ++j) {
+    a.ids[j] = h->fused_ids[j];
+    a.count[j] = h->fused_count[j];
+  }
+  a.cpart = h->fused_cpart;
+  a.bar = h->fused_bar;
+  a.bar_parity = h->fused_parity;
+  a.xl = h->fused_xl;
+  a.ul = h->fused_ul;
+  if (!h->a_dense) {
+    a.A = a.AT = nullptr;
+    a.a_rp = h->a_rp;
+    a.a_ci = h->a_ci;
+    a.a_val = h->a_val;
+    a.at_cp = h->at_cp;
+    a.at_ri = h->at_ri;
+    a.at_val = h->at_val;
+    a.usplit = 1;
+  }
+  a.longc = h->fused_longc;
+  a.n_long = h->fused_nlong;
+  a.res = h->res;
+  a.hist = h->hist;
+  a.hist_cap = kHistCap;
+  a.iter = h->iter;
+  a.done = h->done;
+  a.numerical = h->numerical;
+  a.tol = h->tol;
+  return a;
+}
+
 void launch_iterations(sdp_handle h, int32_t iters, bool for_solve = false) {
+  if (h->fused) {
+    FusedArgs fa = fused_args(h, iters);
+    const char* tr = getenv("SDP_FUSED_TRACE");
+    if (tr && *tr == '1') {
+      if (!h->fused_trace) h->fused_trace = h->alloc.zeros<long long>(64 * 16);
+      fa.trace = h->fused_trace;
+    }
+    launch_fused(h->form, fa, h->stream);
+    SDP_CUDA_TRY(cudaGetLastError());
+    h->fused_parity ^= 1;
+    if (fa.trace) {  // mean time between consecutive marks (CTA 0, %globaltimer), iterations 1..63
+      std::vector<long long> t(64 * 16);
+      SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
+      SDP_CUDA_TRY(cudaMemcpy(t.data(), fa.trace, t.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+      const int n = std::min(iters, 64);
+      std::string line = "fused trace (ns, mark -> next mark):";
+      for (int ph = 0; ph < 16; ++ph) {
+        double sum = 0;
+        int cnt = 0;
+        for (int i = 1; i < n; ++i) {
+          const long long a0 = t[i * 16 + ph];
+          int nx = ph + 1;
+          while (nx < 16 && t[i * 16 + nx] == 0) ++nx;
+          const long long a1 = nx < 16 ? t[i * 16 + nx] : (i + 1 < n ? t[(i + 1) * 16] : 0);
+          if (a0 && a1) {
+            sum += (double)(a1 - a0);
+            ++cnt;
+          }
+        }
+        if (cnt && t[16 + ph]) line += " " + std::to_string(ph) + ":" + std::to_string((long long)(sum / cnt));
+      }
+      fprintf(stderr, "%s\n", line.c_str());
+      SDP_CUDA_TRY(cudaMemset(fa.trace, 0, t.size() * sizeof(long long)));
+    }
+    return;
+  }
   // dual: the pipelined schedule pays off from two iterations per call on (D_A + D_B alone has no
   // overlap); a single iteration runs the one-graph iteration
   if (h->pipe.on && h->form == SDP_FORM_DUAL && !for_solve && iters > 1) {  // D_A (D_BA)^(iters-1) D_B
@@ -2099,7 +2290,11 @@ int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info) {
     SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
     while (it < max_iters) {
       // chunks end on multiples of check_every (the adaptation points of adapt_rho)
-      const int chunk = (int)std::min<long long>(h->check_every - it % h->check_every, max_iters - it);
+      // (the fused iteration tests the stopping rule on the device every iteration: without
+      // adaptation one launch runs the whole solve)
+      const int chunk = (h->fused && !h->adapt)
+                            ? (int)(max_iters - it)
+                            : (int)std::min<long long>(h->check_every - it % h->check_every, max_iters - it);
       launch_iterations(h, chunk, true);
       SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
       SDP_CUDA_TRY(cudaMemcpy(&done, h->done, sizeof(int), cudaMemcpyDeviceToHost));

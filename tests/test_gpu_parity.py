@@ -510,7 +510,10 @@ def test_psd_completion_matches_oracle(lib, gen, name):
     want = completion.complete_psd(X, known, order, later, rtol=1e-8)
     got = s.complete_x(rtol=1e-8)
     assert np.allclose(got[known], X[known], rtol=0, atol=0)
-    assert np.linalg.norm(got - want) <= 1e-9 * np.linalg.norm(want)
+    # an eigenvalue of a conditional block lying at the 1e-8 cutoff can be dropped on one side and
+    # kept on the other (the two eigensolvers round differently): each such flip moves the
+    # completion by at most the cutoff, rtol * |lambda_max|, so agreement is asserted to 5 * rtol
+    assert np.linalg.norm(got - want) <= 5e-8 * np.linalg.norm(want)
     assert np.linalg.eigvalsh(got).min() >= -1e-5 * np.linalg.norm(got)
     s.close()
 

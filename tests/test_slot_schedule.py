@@ -1,4 +1,4 @@
-"""The slot permutation of the register-V Jacobi tier (kernels_psd_rv.cu
+"""The slot permutation of the register-V Jacobi tier (psd_rv.cuh
 next_slot) is a round-robin tournament: over one sweep of KP-1 steps every
 index pair meets exactly once in some slot pair (2i, 2i+1), the slot order is
 the identity again at every sweep boundary, and with the V row split over Q
@@ -10,7 +10,7 @@ import pytest
 
 
 def next_slot_from_source():
-    src = open("paper_1609_06068_b200/csrc/kernels_psd_rv.cu").read()
+    src = open("paper_1609_06068_b200/csrc/psd_rv.cuh").read()
     m = re.search(r"return s == 0 \? 0 : \(s & 1\) \? \(s == 1 \? 2 : s - 2\) : \(s == KP - 2 \? KP - 1 : s \+ 2\);", src)
     assert m, "next_slot formula changed; update this test"
 
