@@ -206,7 +206,11 @@ struct TierFork {
   static constexpr int kMaxSide = 4;
   int nside = 0;  // SDP_TIER_STREAMS (default 1: measured no gain from more on cfg3 / cfg4)
   cudaStream_t side[kMaxSide] = {};
-  cudaEvent_t fork = nullptr, join[kMaxSide] = {};
+  // the lead tier (the giant chain, else the largest tier) runs on a stream of the highest
+  // priority, so its kernels take the SMs first and the other tiers fill what its low-occupancy
+  // phases (QL, inverse iteration, cluster reductions) leave idle; SDP_TIER_PRIO=0: off
+  cudaStream_t hi = nullptr;
+  cudaEvent_t fork = nullptr, join[kMaxSide] = {}, join_hi = nullptr;
   void create() {
     const char* e = getenv("SDP_TIER_STREAMS");
     nside = e ? std::max(1, std::min(kMaxSide, atoi(e))) : 1;
@@ -214,6 +218,13 @@ struct TierFork {
     for (int i = 0; i < nside; ++i) {
       SDP_CUDA_TRY(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
       SDP_CUDA_TRY(cudaEventCreateWithFlags(&join[i], cudaEventDisableTiming));
+    }
+    const char* pr = getenv("SDP_TIER_PRIO");
+    if (!(pr && *pr == '0')) {
+      int least = 0, greatest = 0;
+      SDP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+      SDP_CUDA_TRY(cudaStreamCreateWithPriority(&hi, cudaStreamNonBlocking, greatest));
+      SDP_CUDA_TRY(cudaEventCreateWithFlags(&join_hi, cudaEventDisableTiming));
     }
   }
   void destroy() {
@@ -223,19 +234,15 @@ struct TierFork {
       side[i] = nullptr;
       join[i] = nullptr;
     }
+    if (hi) cudaStreamDestroy(hi);
+    if (join_hi) cudaEventDestroy(join_hi);
+    hi = nullptr;
+    join_hi = nullptr;
     if (fork) cudaEventDestroy(fork);
     fork = nullptr;
     nside = 0;
   }
 };
-
-// Pipelined primal iteration (dense A, one rank, no giant tier; DESIGN.md §7 "Pipelined iteration"):
-// the cliques are split in two halves H1 = [0, p1), H2 = [p1, p); coordinates are classed by the
-// halves that touch them.  One iteration = A: u = A D^-1 r1 (all column pieces), y = S^-1 u,
-// x on the coordinates H1 touches; B: x on the H2-only coordinates || P_+ of H1 and the scatter
-// of the H1-only coordinates, then P_+ of H2, the rest of the scatter, finalize.  sdp_step(n)
-// launches A (BA)^(n-1) B, and inside BA the next iteration's A-pass over the H1-only columns
-// runs concurrently with P_+ of H2: the projections hide under the two A passes.
 struct BucketSet {
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
@@ -675,20 +682,31 @@ void launch_tiers(ProjArgs a, int mode, int32_t* const d_ids[B_NUM], const int b
   const bool giant = bcount[B_GLOBAL] > 0;
   const bool fork = tf.nside > 0 && nt + (giant ? 1 : 0) >= 2;
   bool used[TierFork::kMaxSide] = {};
+  const bool lead_hi = fork && tf.hi != nullptr;
   if (fork) SDP_CUDA_TRY(cudaEventRecord(tf.fork, s));
+  if (lead_hi) SDP_CUDA_TRY(cudaStreamWaitEvent(tf.hi, tf.fork, 0));
   if (giant) {
     a.ids = d_ids[B_GLOBAL];
     a.count = bcount[B_GLOBAL];
-    launch_projection(B_GLOBAL, mode, a, s);
+    launch_projection(B_GLOBAL, mode, a, lead_hi ? tf.hi : s);
   }
   for (int q = 0; q < nt; ++q) {
     const int b = tiers[q];
     cudaStream_t so = s;
-    if (fork && (giant || q > 0)) {
+    if (lead_hi && !giant && q == 0) {
+      so = tf.hi;
+    } else if (fork && !lead_hi && (giant || q > 0)) {
       const int k = (giant ? q : q - 1) % tf.nside;
       so = tf.side[k];
       if (!used[k]) SDP_CUDA_TRY(cudaStreamWaitEvent(so, tf.fork, 0));
       used[k] = true;
+    } else if (lead_hi && tf.nside > 1) {  // the remaining tiers: the caller's stream + side streams
+      const int r = (giant ? q : q - 1) % tf.nside;
+      if (r > 0) {
+        so = tf.side[r - 1];
+        if (!used[r - 1]) SDP_CUDA_TRY(cudaStreamWaitEvent(so, tf.fork, 0));
+        used[r - 1] = true;
+      }
     }
     a.ids = d_ids[b];
     a.count = bcount[b];
@@ -700,6 +718,10 @@ void launch_tiers(ProjArgs a, int mode, int32_t* const d_ids[B_NUM], const int b
       SDP_CUDA_TRY(cudaEventRecord(tf.join[k], tf.side[k]));
       SDP_CUDA_TRY(cudaStreamWaitEvent(s, tf.join[k], 0));
     }
+  if (lead_hi) {
+    SDP_CUDA_TRY(cudaEventRecord(tf.join_hi, tf.hi));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, tf.join_hi, 0));
+  }
 }
 
 void enqueue_projection(sdp_handle h, int mode, cudaStream_t s) {
