@@ -41,14 +41,17 @@ __device__ __forceinline__ JRot jacobi_rotation(double app, double aqq, double a
   }
   const float df = (float)ds, af = (float)as;
   // fp32 smaller root: t = 2 apq sign(d) / (|d| + sqrt(d^2 + 4 apq^2))
-  const float rf = sqrtf(df * df + 4.0f * af * af);
+  // (approximate fp32 square root and divisions: the estimate only seeds the fp64 Newton step, and
+  // the scaled operands keep every intermediate in [2^-60, 8], far from the approximations' limits)
+  const float q = df * df + 4.0f * af * af;  // > 0: |as| >= 2^-53 |ds| or |ds| in [1, 2)
+  const float rf = q * rsqrtf(q);
   const float den = fabsf(df) + rf;
-  float tf = (df >= 0.0f ? 2.0f : -2.0f) * af / den;
+  float tf = __fdividef((df >= 0.0f ? 2.0f : -2.0f) * af, den);
   double t = (double)tf;
   // one fp64 Newton step on g(t) = apq t^2 + d t - apq (scaled coefficients)
   const double g = fma(fma(as, t, ds), t, -as);
   const float gp = 2.0f * af * tf + df;  // g'(t) in fp32
-  if (gp != 0.0f) t -= g * (double)(1.0f / gp);
+  if (gp != 0.0f) t -= g * (double)__fdividef(1.0f, gp);
   const double c = rsqrt(fma(t, t, 1.0));
   r.c = c;
   r.s = t * c;

@@ -166,6 +166,38 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
   }
   fro2 = g.sum(fro2);
   const double thr = kJacTol * kJacTol * fro2;
+  // this thread's 2x2 blocks of the pair triangle (the same in every step: the slot permutation is
+  // applied physically), with their source and destination offsets: A_next = (J^T A J) permuted by
+  // ns(), upper triangle only; every block (i <= j, row-major over the pair triangle so that a
+  // warp's lanes touch consecutive columns) writes each entry once, at (min, max) of its slots
+  constexpr int NBU = (Lay::NBLK + G - 1) / G;
+  int b_src[NBU], b_i[NBU], b_j[NBU], b_d[NBU][4];
+#pragma unroll
+  for (int u = 0; u < NBU; ++u) {
+    const int b = g.tid + u * G;
+    b_src[u] = -1;
+    b_i[u] = b_j[u] = 0;
+    b_d[u][0] = b_d[u][1] = b_d[u][2] = b_d[u][3] = 0;
+    if (b < Lay::NBLK) {
+      const int ij = tab[b];
+      const int i = ij >> 16, j = ij & 0xffff;
+      const int pi = next_slot<KP>(2 * i), qi = next_slot<KP>(2 * i + 1);
+      b_src[u] = 2 * i * LD + 2 * j;
+      b_i[u] = i;
+      b_j[u] = j;
+      if (i == j) {
+        b_d[u][0] = pi * LD + pi;
+        b_d[u][1] = qi * LD + qi;
+        b_d[u][2] = min(pi, qi) * LD + max(pi, qi);
+      } else {
+        const int pj = next_slot<KP>(2 * j), qj = next_slot<KP>(2 * j + 1);
+        b_d[u][0] = min(pi, pj) * LD + max(pi, pj);
+        b_d[u][1] = min(pi, qj) * LD + max(pi, qj);
+        b_d[u][2] = min(qi, pj) * LD + max(qi, pj);
+        b_d[u][3] = min(qi, qj) * LD + max(qi, qj);
+      }
+    }
+  }
   int sweep = 0;
   for (; sweep < kMaxSweeps; ++sweep) {
     double off2 = 0.0;
@@ -185,21 +217,16 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
         const double app = Ac[2 * i * LD + 2 * i], aqq = Ac[(2 * i + 1) * LD + 2 * i + 1];
         const double apq = Ac[2 * i * LD + 2 * i + 1];
         const JRot jr = jacobi_rotation(app, aqq, apq);
-        const double cs = jr.c, sn = jr.s, t = 0.0;
-        rc[i] = cs;
-        rs[i] = sn;
-        rt[i] = t;
+        rc[i] = jr.c;
+        rs[i] = jr.s;
       }
       g.sync();
-      // A_next = (J^T A J) permuted by ns(), upper triangle only: every 2x2 block
-      // (i <= j, row-major over the pair triangle so that a warp's lanes touch
-      // consecutive columns) writes each entry once, at (min, max) of its slots
-      for (int b = g.tid; b < Lay::NBLK; b += G) {
-        const int ij = tab[b];
-        const int i = ij >> 16, j = ij & 0xffff;
-        const double2 top = *reinterpret_cast<const double2*>(Ac + 2 * i * LD + 2 * j);
-        const double2 bot = *reinterpret_cast<const double2*>(Ac + (2 * i + 1) * LD + 2 * j);
-        const int pi = next_slot<KP>(2 * i), qi = next_slot<KP>(2 * i + 1);
+#pragma unroll
+      for (int u = 0; u < NBU; ++u) {
+        if (b_src[u] < 0) continue;
+        const int i = b_i[u], j = b_j[u];
+        const double2 top = *reinterpret_cast<const double2*>(Ac + b_src[u]);
+        const double2 bot = *reinterpret_cast<const double2*>(Ac + b_src[u] + LD);
         const double c1 = rc[i], s1 = rs[i];
         if (i == j) {
           // full J^T B J (the rotation annihilates a_pq only to ~1e-14 relative)
@@ -207,18 +234,17 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
           const double r00 = c1 * app - s1 * apq, r01 = c1 * apq - s1 * aqq;
           const double r10 = s1 * app + c1 * apq, r11 = s1 * apq + c1 * aqq;
           const double n01 = 0.5 * ((s1 * r00 + c1 * r01) + (c1 * r10 - s1 * r11));
-          An[pi * LD + pi] = c1 * r00 - s1 * r01;
-          An[qi * LD + qi] = s1 * r10 + c1 * r11;
-          An[min(pi, qi) * LD + max(pi, qi)] = n01;
+          An[b_d[u][0]] = c1 * r00 - s1 * r01;
+          An[b_d[u][1]] = s1 * r10 + c1 * r11;
+          An[b_d[u][2]] = n01;
         } else {
-          const int pj = next_slot<KP>(2 * j), qj = next_slot<KP>(2 * j + 1);
           const double c2 = rc[j], s2 = rs[j];
           const double r00 = c1 * top.x - s1 * bot.x, r01 = c1 * top.y - s1 * bot.y;
           const double r10 = s1 * top.x + c1 * bot.x, r11 = s1 * top.y + c1 * bot.y;
-          An[min(pi, pj) * LD + max(pi, pj)] = c2 * r00 - s2 * r01;
-          An[min(pi, qj) * LD + max(pi, qj)] = s2 * r00 + c2 * r01;
-          An[min(qi, pj) * LD + max(qi, pj)] = c2 * r10 - s2 * r11;
-          An[min(qi, qj) * LD + max(qi, qj)] = s2 * r10 + c2 * r11;
+          An[b_d[u][0]] = c2 * r00 - s2 * r01;
+          An[b_d[u][1]] = s2 * r00 + c2 * r01;
+          An[b_d[u][2]] = c2 * r10 - s2 * r11;
+          An[b_d[u][3]] = s2 * r10 + c2 * r11;
         }
       }
       // V <- V J in registers (this lane's S/2 pairs), then the slot permutation:
