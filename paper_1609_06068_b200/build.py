@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libchordal_sdp.so")
 BUILD = os.path.join(HERE, "_build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-SOURCES = ["api.cu", "kernels_psd.cu", "kernels_psd_rv.cu", "kernels_psd_giant.cu", "kernels_psd_trd.cu", "kernels_psd_wj.cu", "kernels_psd_gtrd.cu", "kernels_vec.cu", "kernels_fused.cu", "setup_host.cpp", "completion.cpp", "shard.cpp",
+SOURCES = ["api.cu", "kernels_psd.cu", "kernels_psd_rv.cu", "kernels_psd_giant.cu", "kernels_psd_trd.cu", "kernels_psd_wj.cu", "kernels_psd_gtrd.cu", "kernels_vec.cu", "kernels_fused.cu", "kernels_schur.cu", "setup_host.cpp", "completion.cpp", "shard.cpp",
            "nccl_dl.cpp", "comm.cu", "sparse_chol.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-fopenmp,-O3", "--expt-relaxed-constexpr"]

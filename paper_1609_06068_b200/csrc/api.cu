@@ -8,6 +8,7 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "internal.h"
@@ -1432,6 +1433,31 @@ void destroy_handle(sdp_handle h) {
   delete h;
 }
 
+// A host-to-device copy on a helper thread (its own non-blocking stream, so pageable sources work
+// and no legacy-stream ordering couples it to the caller's work); joined by finish() or on unwind.
+struct AsyncUpload {
+  double* dst = nullptr;
+  std::thread th;
+  cudaError_t err = cudaSuccess;
+  void start(const double* src, size_t bytes, int device) {
+    th = std::thread([this, src, bytes, device] {
+      cudaStream_t st = nullptr;
+      err = cudaSetDevice(device);
+      if (err == cudaSuccess) err = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+      if (err == cudaSuccess) err = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+      if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+      if (st) cudaStreamDestroy(st);
+    });
+  }
+  void finish() {
+    if (th.joinable()) th.join();
+    if (err != cudaSuccess) throw Error{SDP_E_CUDA, std::string("A upload: ") + cudaGetErrorString(err)};
+  }
+  ~AsyncUpload() {
+    if (th.joinable()) th.join();
+  }
+};
+
 void build_fused(sdp_handle h, const std::vector<int>& task_bucket);
 int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out) {
   auto t0 = std::chrono::steady_clock::now();
@@ -1485,6 +1511,27 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   DeviceGuard dg(opt.device);
 
   smark("validation");
+  sdp_handle h = new sdp_handle_s();
+  *out = h;  // so the caller-side cleanup path below can destroy it
+  h->n = n;
+  h->m = m;
+  h->form = opt.form;
+  h->rho = opt.rho;
+  h->device = opt.device;
+  h->check_every = opt.check_every > 0 ? opt.check_every : 10;
+  h->use_graph = opt.use_graph;
+  h->adapt = opt.adapt_rho ? 1 : 0;
+  h->adapt_mu = opt.adapt_mu > 1.0 ? opt.adapt_mu : 10.0;
+  h->adapt_tau = opt.adapt_tau > 1.0 ? opt.adapt_tau : 2.0;
+  // The raw dense A values (the bulk of the input) go to the device on a helper thread while the
+  // host runs the chordal analysis below; the placement onto the pattern waits for them (step 5).
+  h->alloc.set_hook(opt.allocator, opt.device);
+  AsyncUpload a_up;
+  if (P->a_fmt == SDP_A_DENSE_ON_PATTERN && P->a_nnz > 0 &&
+      (double)m * (double)P->a_nnz * 8.0 <= 16e9) {
+    a_up.dst = h->alloc.get<double>((size_t)m * P->a_nnz);
+    a_up.start(P->a_val, (size_t)m * P->a_nnz * sizeof(double), opt.device);
+  }
   // ---- 1. aggregate pattern and chordal analysis
   std::vector<std::pair<int32_t, int32_t>> edges;
   edges.reserve((size_t)(P->c_nnz + P->a_nnz + P->e_nnz));
@@ -1499,24 +1546,11 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   edges.clear();
   edges.shrink_to_fit();
 
-  sdp_handle h = new sdp_handle_s();
-  *out = h;  // so the caller-side cleanup path below can destroy it
-  h->n = n;
-  h->m = m;
-  h->form = opt.form;
-  h->rho = opt.rho;
-  h->device = opt.device;
-  h->check_every = opt.check_every > 0 ? opt.check_every : 10;
-  h->use_graph = opt.use_graph;
-  h->adapt = opt.adapt_rho ? 1 : 0;
-  h->adapt_mu = opt.adapt_mu > 1.0 ? opt.adapt_mu : 10.0;
-  h->adapt_tau = opt.adapt_tau > 1.0 ? opt.adapt_tau : 2.0;
   h->fill_edges = cr.fill_edges;
   h->stream = (cudaStream_t)opt.stream;  // NULL = the legacy default stream, as in the CUDA runtime
   h->own_stream = false;
   h->world = opt.world;
   h->rank = opt.rank;
-  h->alloc.set_hook(opt.allocator, opt.device);
   if (h->world > 1)  // collective
     h->comm = opt.comm ? make_loop_comm(opt.comm, h->world, h->rank) : make_nccl_comm(opt.nccl_id, h->world, h->rank);
   if (h->comm && h->comm->loopback()) h->use_graph = 0;  // capture cannot cross the ranks' streams
@@ -1701,6 +1735,10 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
   smark("uploads, tiers");
   // ---- 5. A (svec rows) and S = A D^-1 A^T, factor cached once
   std::vector<double> S;
+  // S^-1 of a dense S: device Gauss-Jordan (default) or host Cholesky + L^-1 (SDP_SCHUR_HOST=1)
+  const char* shost = getenv("SDP_SCHUR_HOST");
+  const bool schur_host = shost && *shost == '1';
+  double* dS_keep = nullptr;
   if (P->a_fmt == SDP_A_DENSE_ON_PATTERN) {
     h->a_dense = 1;
     const int64_t npat = P->a_nnz;
@@ -1716,22 +1754,29 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     }
     h->A = al.zeros<double>((size_t)m * h->lda);
     if (npat > 0) {
-      // stream the raw values in row slabs of <= 256 MB through a staging buffer
-      const int64_t rows_per = std::max<int64_t>(1, (256ll << 20) / (8 * npat));
-      double* raw = al.get<double>((size_t)std::min<int64_t>(rows_per, m) * npat);
+      // the raw values: already on the device (uploaded during the chordal analysis), else streamed
+      // in row slabs of <= 256 MB through a staging buffer
+      const bool pre = a_up.dst != nullptr;
+      if (pre) a_up.finish();
+      const int64_t rows_per =
+          pre ? std::min<int64_t>(m, 65535) : std::max<int64_t>(1, (256ll << 20) / (8 * npat));
+      double* raw = pre ? a_up.dst : al.get<double>((size_t)std::min<int64_t>(rows_per, m) * npat);
       int64_t* dmap = al.upload(map);
       double* dscale = al.upload(scale);
       int* dbad = al.zeros<int>(1);
       for (int64_t r0 = 0; r0 < m; r0 += rows_per) {
         const int64_t nr = std::min<int64_t>(rows_per, m - r0);
-        SDP_CUDA_TRY(cudaMemcpy(raw, P->a_val + r0 * npat, nr * npat * sizeof(double), cudaMemcpyHostToDevice));
-        launch_place_dense(raw, npat, (int)nr, dmap, dscale, h->A + r0 * h->lda, h->lda, nullptr, dbad);
+        if (!pre)
+          SDP_CUDA_TRY(cudaMemcpy(raw, P->a_val + r0 * npat, nr * npat * sizeof(double), cudaMemcpyHostToDevice));
+        launch_place_dense(pre ? raw + r0 * npat : raw, npat, (int)nr, dmap, dscale, h->A + r0 * h->lda, h->lda,
+                           nullptr, dbad);
         SDP_CUDA_TRY(cudaGetLastError());
       }
       int bad = 0;
       SDP_CUDA_TRY(cudaMemcpy(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost));
       if (bad) throw Error{SDP_E_INVALID_ARG, "A value not finite"};
       al.release(raw);
+      a_up.dst = nullptr;
       al.release(dmap);
       al.release(dscale);
       al.release(dbad);
@@ -1754,9 +1799,13 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     launch_syrk_dense(h->A, h->lda, m, h->Dinv, dS, nullptr);
     SDP_CUDA_TRY(cudaGetLastError());
     if (h->world > 1) h->comm->allreduce_sum(dS, (size_t)m * m, nullptr);  // S = sum of owned-column parts
-    S.resize((size_t)m * m);
-    SDP_CUDA_TRY(cudaMemcpy(S.data(), dS, S.size() * sizeof(double), cudaMemcpyDeviceToHost));
-    al.release(dS);
+    if (schur_host) {
+      S.resize((size_t)m * m);
+      SDP_CUDA_TRY(cudaMemcpy(S.data(), dS, S.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      al.release(dS);
+    } else {
+      dS_keep = dS;  // inverted on the device below
+    }
   } else {
     h->a_dense = 0;
     struct Ent {
@@ -1895,18 +1944,35 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     }
   }
   smark("S = A D^-1 A^T (+ D2H)");
-  if (!h->s_diag && h->s_factor != 2) {
+  if (!h->s_diag && h->s_factor != 2 && !schur_host) {
+    // S^-1 on the device: blocked Gauss-Jordan sweep of the SPD S (kernels_schur.cu)
+    h->s_factor = 1;
+    double* dS = dS_keep ? dS_keep : al.upload(S);
+    dS_keep = nullptr;
+    S.clear();
+    S.shrink_to_fit();
+    h->Sinv = al.get<double>((size_t)m * m);
+    double* work = al.get<double>((size_t)m * m);
+    double* d0 = al.get<double>((size_t)m + 1024);
+    int* dbad = al.zeros<int>(1);
+    smark("S^-1 buffers");
+    const bool ok = spd_inverse_gpu(dS, m, h->Sinv, work, d0, dbad, nullptr);
+    smark("S^-1 (device Gauss-Jordan)");
+    al.release(work);
+    al.release(d0);
+    al.release(dbad);
+    al.release(dS);
+    if (!ok) throw Error{SDP_E_RANK_DEFICIENT, "S = A D^-1 A^T is not positive definite"};
+    symv_init_attributes(m);
+    smark("S^-1 release");
+  } else if (!h->s_diag && h->s_factor != 2) {
+    if (dS_keep) al.release(dS_keep);
     h->s_factor = 1;
     if (!cholesky_host(S, m)) throw Error{SDP_E_RANK_DEFICIENT, "S = A D^-1 A^T is not positive definite"};
     smark("Cholesky (host)");
     std::vector<double> Wt;
     tri_inverse_T(S, m, Wt);
     smark("L^-1 (host)");
-    std::vector<double> Wl((size_t)m * m);
-#pragma omp parallel for
-    for (int i = 0; i < m; ++i)
-      for (int j = 0; j < m; ++j) Wl[(size_t)i * m + j] = Wt[(size_t)j * m + i];
-    h->W = al.upload(Wl);
     h->WT = al.upload(Wt);
     // cached S^-1 = W^T W (one dense mat-vec per iteration instead of two dependent
     // triangular ones; cond(S) ~ 2 on the block-arrow configs), formed by the SYRK kernel
@@ -1917,7 +1983,6 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
     SDP_CUDA_TRY(cudaGetLastError());
     SDP_CUDA_TRY(cudaDeviceSynchronize());
     al.release(d1);
-    al.release(h->W);
     al.release(h->WT);
     h->W = h->WT = nullptr;
     symv_init_attributes(m);

@@ -48,6 +48,9 @@ int64_t coord_index(const ChordalResult& cr, int32_t i, int32_t j);  // -1 if ab
 // row-major) holds G^T with G = L^-1 (S = L L^T in a minimum-degree order), so S^-1 = G^T G.
 // Returns false with *why = "factor too dense" (nnz(L) > max_fill_frac m^2 and !force) or the
 // rank-deficiency message.
+// S^-1 of a symmetric positive definite S (device, m x m; clobbered) by a blocked Gauss-Jordan sweep
+// (kernels_schur.cu); false if a pivot fails the 1e-12 relative test
+bool spd_inverse_gpu(double* S, int m, double* Sinv, double* work, double* diag0, int* bad, cudaStream_t s);
 bool sparse_inverse_factor(int m, const std::vector<int64_t>& sp, const std::vector<int32_t>& si,
                            const std::vector<double>& sv, int64_t ldg, std::vector<double>& GT, int64_t* nnz_l,
                            double max_fill_frac, bool force, std::string* why);

@@ -23,6 +23,30 @@ namespace sdp {
 
 namespace {
 inline int popc(uint64_t x) { return __builtin_popcountll(x); }
+
+// Minimum-degree queue, smallest degree then smallest index (reading G13), as a binary heap with
+// lazy deletion: an update pushes the new key, stale entries are skipped when they surface (no
+// per-update allocation, unlike an ordered set).
+struct MinDegQueue {
+  std::vector<std::pair<int32_t, int32_t>> heap;  // (degree, vertex), min-heap
+  const std::vector<int32_t>* deg = nullptr;
+  const std::vector<char>* dead = nullptr;
+  static bool later_first(const std::pair<int32_t, int32_t>& a, const std::pair<int32_t, int32_t>& b) {
+    return a > b;  // std heap is a max-heap: invert for the smallest (degree, index)
+  }
+  void push(int32_t d, int32_t v) {
+    heap.push_back({d, v});
+    std::push_heap(heap.begin(), heap.end(), later_first);
+  }
+  int32_t pop() {
+    for (;;) {
+      std::pop_heap(heap.begin(), heap.end(), later_first);
+      const auto e = heap.back();
+      heap.pop_back();
+      if (!(*dead)[e.second] && (*deg)[e.second] == e.first) return e.second;
+    }
+  }
+};
 }  // namespace
 
 // Exact minimum degree on a dense bitset (fast for n up to ~5e4: one word op per 64 vertices).
@@ -46,48 +70,58 @@ int64_t eliminate_bitset(int32_t n, const std::vector<std::pair<int32_t, int32_t
   std::vector<uint64_t> alive(W, ~0ull);
   if (n % 64) alive[W - 1] = (1ull << (n % 64)) - 1ull;
   std::vector<int32_t> deg(n);
-  std::set<std::pair<int32_t, int32_t>> queue;
+  std::vector<char> dead(n, 0);
+  MinDegQueue queue;
+  queue.deg = &deg;
+  queue.dead = &dead;
+  queue.heap.reserve((size_t)4 * n);
   for (int v = 0; v < n; ++v) {
     int d = 0;
     const uint64_t* r = row(v);
     for (int64_t w = 0; w < W; ++w) d += popc(r[w]);
     deg[v] = d;
-    queue.insert({d, v});
+    queue.push(d, v);
   }
-  std::vector<uint64_t> nbmask(W);
+  std::vector<uint64_t> nbmask(W, 0ull);
+  std::vector<int32_t> nzw;  // words of nbmask with bits set
   for (int step = 0; step < n; ++step) {
-    auto it = queue.begin();  // smallest degree, then smallest index
-    const int v = it->second;
-    queue.erase(it);
+    const int v = queue.pop();
+    dead[v] = 1;
     pos[v] = step;
     alive[v >> 6] &= ~(1ull << (v & 63));
     const uint64_t* rv = row(v);
     std::vector<int32_t>& nb = later[v];
+    nzw.clear();
     for (int64_t w = 0; w < W; ++w) {
       uint64_t m = rv[w] & alive[w];
+      if (!m) continue;
       nbmask[w] = m;
+      nzw.push_back((int32_t)w);
       while (m) {
         int b = __builtin_ctzll(m);
         nb.push_back((int32_t)(w * 64 + b));
         m &= m - 1;
       }
     }
-    // eliminate v: its remaining neighbourhood becomes a clique (fill edges)
+    // eliminate v: its remaining neighbourhood becomes a clique (fill edges).  Only the words of
+    // N(v) change in a neighbour's row, so its alive degree is updated from them: -1 for v, + the
+    // members of N(v) \ {u} it was not adjacent to
     for (int u : nb) {
       uint64_t* ru = row(u);
-      for (int64_t w = 0; w < W; ++w) ru[w] |= nbmask[w];
-      ru[u >> 6] &= ~(1ull << (u & 63));
-    }
-    for (int u : nb) {
-      const uint64_t* ru = row(u);
-      int d = 0;
-      for (int64_t w = 0; w < W; ++w) d += popc(ru[w] & alive[w]);
+      int added = 0;
+      for (int32_t w : nzw) {
+        uint64_t fresh = nbmask[w] & ~ru[w];
+        if (w == (u >> 6)) fresh &= ~(1ull << (u & 63));
+        added += popc(fresh);
+        ru[w] |= fresh;
+      }
+      const int d = deg[u] - 1 + added;
       if (d != deg[u]) {
-        queue.erase({deg[u], u});
         deg[u] = d;
-        queue.insert({d, u});
+        queue.push(d, u);
       }
     }
+    for (int32_t w : nzw) nbmask[w] = 0ull;
   }
   return e0;
 }
@@ -109,13 +143,20 @@ int64_t eliminate_sparse(int32_t n, const std::vector<std::pair<int32_t, int32_t
     e0 += (int64_t)adj[v].size();
   }
   e0 /= 2;
-  std::set<std::pair<int32_t, int32_t>> queue;
-  for (int v = 0; v < n; ++v) queue.insert({(int32_t)adj[v].size(), v});
+  std::vector<int32_t> deg(n);
+  std::vector<char> dead(n, 0);
+  MinDegQueue queue;
+  queue.deg = &deg;
+  queue.dead = &dead;
+  queue.heap.reserve((size_t)4 * n);
+  for (int v = 0; v < n; ++v) {
+    deg[v] = (int32_t)adj[v].size();
+    queue.push(deg[v], v);
+  }
   std::vector<int32_t> merged;
   for (int step = 0; step < n; ++step) {
-    auto it = queue.begin();
-    const int v = it->second;
-    queue.erase(it);
+    const int v = queue.pop();
+    dead[v] = 1;
     pos[v] = step;
     std::vector<int32_t>& nb = later[v];
     nb = std::move(adj[v]);  // alive neighbours only (eliminated vertices are removed below)
@@ -136,11 +177,10 @@ int64_t eliminate_sparse(int32_t n, const std::vector<std::pair<int32_t, int32_t
         }
         if (x != u && x != v) merged.push_back(x);
       }
-      const int32_t d0 = (int32_t)au.size();
       adj[u].swap(merged);
-      if ((int32_t)adj[u].size() != d0) {
-        queue.erase({d0, u});
-        queue.insert({(int32_t)adj[u].size(), u});
+      if ((int32_t)adj[u].size() != deg[u]) {
+        deg[u] = (int32_t)adj[u].size();
+        queue.push(deg[u], u);
       }
     }
   }
