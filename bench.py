@@ -565,7 +565,7 @@ def main():
         a2.workload, a2.no_cpu, a2.e2e_cap, a2.paper_row = wl, True, 0, False
         # cfg3's per-iteration cost depends on the iterate (its giant cliques' spectra): a window
         # after 20 warm-up iterations, 100 long (~1 s); cfg4 is iterate-independent
-        a2.steps = {"cfg3": 100, "cfg4": 10}.get(wl, 200)
+        a2.steps = {"cfg3": 300, "cfg4": 10}.get(wl, 200)
         a2.warmup = {"cfg3": 20}.get(wl, 5)
         try:
             r2 = run_ours(a2, rank, world, local)

@@ -184,3 +184,25 @@ def test_fused_long_run_no_capped_sweeps(lib, gen):
     assert info["iters"] == 500 and info["jacobi_capped"] == 0
     assert np.isfinite(info["eps_p"]) and np.isfinite(info["eps_d"])
     s.close()
+
+
+@pytest.mark.parametrize("name", ["scalar", "cyc5", "cyc9", "trace", "theta7", "sensor60"])
+@pytest.mark.parametrize("form", ["primal", "dual"])
+def test_fused_small_generators(lib, gen, name, form):
+    """Degenerate and sparse-A shapes through the fused path: one 1 x 1 clique (n = m = 1), cliques of
+    2 / 3 / 7, a diagonal S (max-cut), a sparse S (distance constraints on a geometric graph with
+    cliques of 3..16); 40 iterations against the oracle element by element."""
+    prob = {"scalar": lambda: gen.scalar_primal(), "cyc5": lambda: gen.cycle_maxcut(5),
+            "cyc9": lambda: gen.cycle_maxcut(9), "trace": lambda: gen.trace_one_tridiagonal(12),
+            "theta7": lambda: gen.lovasz_theta_cycle(7), "sensor60": lambda: gen.sensor_network(60, 0.3, 2)}[name]()
+    dec = dc.decompose(prob)
+    st = admm.step(dec, admm.zero_state(dec), 1.0, form, 40, record=True)
+    with env(SDP_FUSED=1):
+        s = lib.Solver(prob, form=form, rho=1.0)
+    assert s.info()["fused"] == 1
+    s.step(40)
+    compare(st, s, form)
+    h = s.history()
+    o = np.array(st.history)
+    assert np.allclose(h[:, 2], o[:, 3], rtol=1e-9, atol=1e-12)
+    s.close()
