@@ -379,8 +379,13 @@ def run_ours(args, rank, world, local):
     # iterations/s = iterations / total wall time (paper P:464 / Table II report total time
     # including pre-processing).  Plus the paper's own settings (tol 1e-3, 2000-iteration cap).
     if args.e2e_cap > 0:
-        out["e2e"] = time_to_solution(L, prob, args.form, rho, 1e-4, args.e2e_cap, local, stream, rank, world,
-                                      nccl_id)
+        # median of --e2e-reps independent runs (each from host data, fresh handle): the setup's host
+        # part (page faults of the pinned buffers, allocation) varies from run to run
+        runs = [time_to_solution(L, prob, args.form, rho, 1e-4, args.e2e_cap, local, stream, rank, world, nccl_id)
+                for _ in range(max(1, args.e2e_reps))]
+        runs.sort(key=lambda r: r["time_to_solution_s"])
+        out["e2e"] = dict(runs[len(runs) // 2])
+        out["e2e"]["runs_time_to_solution_s"] = [r["time_to_solution_s"] for r in runs]
     if args.paper_row:
         out["paper_settings"] = time_to_solution(L, prob, args.form, rho, 1e-3, 2000, local, stream, rank, world,
                                                  nccl_id)
@@ -531,6 +536,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-cap", type=int, default=3000, help="iteration cap of the e2e time-to-solution run")
+    ap.add_argument("--e2e-reps", type=int, default=3, help="e2e runs; the median is reported")
     ap.add_argument("--paper-row", action="store_true", default=None,
                     help="also solve at the paper's settings (1e-3, 2000 it); default on for the cfg2 headline")
     ap.add_argument("--no-paper-row", dest="paper_row", action="store_false")
