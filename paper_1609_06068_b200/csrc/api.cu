@@ -404,6 +404,14 @@ struct sdp_psd_plan_s {
   // threads while the DMA of the other chunk is in flight
   double* stage[2] = {nullptr, nullptr};
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // pinned host buffers: the batch in contiguous sub-plans whose H2D copy, projection and D2H copy
+  // overlap (copy engines in both directions beside the compute)
+  std::vector<int32_t> h_sizes;
+  std::vector<sdp_psd_plan_s*> sub;
+  std::vector<int64_t> sub_v0, sub_nv;
+  cudaStream_t cp_in = nullptr, cp_out = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_comp;
+  cudaEvent_t ev_end = nullptr;
   void free_stage() {
     for (int b = 0; b < 2; ++b) {
       if (stage[b]) cudaFreeHost(stage[b]);
@@ -2122,7 +2130,7 @@ void build_fused(sdp_handle h, const std::vector<int>& task_bucket) {
   // (sparse A: lanes per row / coordinate ~ half the mean entry count)
   const double np = h->a_dense ? (h->m + 1) / 2 : 0.5 * (double)nnzA / std::max<int64_t>(1, h->Nl);
   h->fused_xl = 1;
-  while (h->fused_xl < 32 && h->fused_xl * (h->a_dense ? 4 : 1) < np) h->fused_xl *= 2;
+  while (h->fused_xl < 32 && h->fused_xl * (h->a_dense ? 8 : 1) < np) h->fused_xl *= 2;
   h->fused_ul = 1;
   while (!h->a_dense && h->fused_ul < 32 && h->fused_ul < 0.5 * (double)nnzA / h->m) h->fused_ul *= 2;
   // scatter: coordinates with long segments (a warp each)
@@ -2214,14 +2222,15 @@ void launch_iterations(sdp_handle h, int32_t iters, bool for_solve = false) {
     FusedArgs fa = fused_args(h, iters);
     const char* tr = getenv("SDP_FUSED_TRACE");
     if (tr && *tr == '1') {
-      if (!h->fused_trace) h->fused_trace = h->alloc.zeros<long long>(64 * 16);
+      if (!h->fused_trace) h->fused_trace = h->alloc.zeros<long long>(64 * 16 + 8);
       fa.trace = h->fused_trace;
     }
+    if (iters <= 0) return;
     launch_fused(h->form, fa, h->stream);
     SDP_CUDA_TRY(cudaGetLastError());
-    h->fused_parity ^= 1;
+    h->fused_parity ^= 1;  // the next launch uses the other barrier counter (zeroed by this one)
     if (fa.trace) {  // mean time between consecutive marks (CTA 0, %globaltimer), iterations 1..63
-      std::vector<long long> t(64 * 16);
+      std::vector<long long> t(64 * 16 + 8);
       SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
       SDP_CUDA_TRY(cudaMemcpy(t.data(), fa.trace, t.size() * sizeof(long long), cudaMemcpyDeviceToHost));
       const int n = std::min(iters, 64);
@@ -2242,6 +2251,13 @@ void launch_iterations(sdp_handle h, int32_t iters, bool for_solve = false) {
         if (cnt && t[16 + ph]) line += " " + std::to_string(ph) + ":" + std::to_string((long long)(sum / cnt));
       }
       fprintf(stderr, "%s\n", line.c_str());
+      const long long* rv = t.data() + 64 * 16;  // register-V Jacobi clocks (CTA 0, group 0)
+      if (rv[0] > 0)
+        fprintf(stderr,
+                "  rv projection (cycles per call): load %.0f, warm start %.0f, sweeps %.0f (%.2f sweeps, %.0f per "
+                "step), recon+epilogue %.0f\n",
+                (double)rv[1] / rv[0], (double)rv[2] / rv[0], (double)rv[3] / rv[0], (double)rv[5] / rv[0],
+                rv[4] ? (double)rv[3] / rv[4] : 0.0, (double)rv[6] / rv[0]);
       SDP_CUDA_TRY(cudaMemset(fa.trace, 0, t.size() * sizeof(long long)));
     }
     return;
@@ -2827,6 +2843,7 @@ int sdp_psd_plan_create_ex(int64_t count, const int32_t* h_sizes, int32_t device
       off[i + 1] = off[i] + (int64_t)k * (k + 1) / 2;
     }
     pl->values = off[count];
+    pl->h_sizes = ksz;
     pl->d_off = pl->alloc.upload(off);
     pl->d_ksz = pl->alloc.upload(ksz);
     build_buckets(pl->alloc, ksz, pl->d_ids, pl->bcount, pl->gd, pl->td);
@@ -2866,6 +2883,85 @@ int sdp_project_psd_batch(sdp_psd_plan pl, const double* d_in, double* d_out, vo
   });
 }
 
+}  // extern "C"
+
+namespace {
+constexpr int64_t kPipeMinCount = 4096;  // matrices per sub-plan of the pinned pipeline (at least)
+constexpr int kPipeChunks = 4;
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// Pinned host buffers: kPipeChunks contiguous sub-plans (equal value counts); chunk i's H2D copy
+// (stream cp_in), projection (the caller's stream) and D2H copy (stream cp_out) are ordered by
+// events only, so copies in both directions run beside the projections of other chunks.
+void project_pipelined(sdp_psd_plan pl, const double* h_in, double* h_out, cudaStream_t s) {
+  if (!pl->h_in_dev) {
+    pl->h_in_dev = pl->alloc.get<double>(pl->values);
+    pl->h_out_dev = pl->alloc.get<double>(pl->values);
+  }
+  if (pl->sub.empty()) {
+    const int64_t n = pl->count;
+    int64_t start = 0, v = 0;
+    for (int c = 0; c < kPipeChunks && start < n; ++c) {
+      const int64_t target = pl->values * (c + 1) / kPipeChunks;
+      int64_t end = start, nvc = 0;
+      while (end < n && (c == kPipeChunks - 1 || v + nvc < target)) {
+        const int64_t k = pl->h_sizes[end];
+        nvc += k * (k + 1) / 2;
+        ++end;
+      }
+      sdp_psd_plan q = nullptr;
+      const int rc = sdp_psd_plan_create_ex(end - start, pl->h_sizes.data() + start, pl->device,
+                                            pl->alloc.has_hook ? &pl->alloc.hook : nullptr, &q);
+      if (rc != SDP_OK) throw Error{rc, std::string("sub-plan: ") + sdp_last_error()};
+      pl->sub.push_back(q);
+      pl->sub_v0.push_back(v);
+      pl->sub_nv.push_back(nvc);
+      v += nvc;
+      start = end;
+    }
+    SDP_CUDA_TRY(cudaStreamCreateWithFlags(&pl->cp_in, cudaStreamNonBlocking));
+    SDP_CUDA_TRY(cudaStreamCreateWithFlags(&pl->cp_out, cudaStreamNonBlocking));
+    pl->ev_in.assign(pl->sub.size(), nullptr);
+    pl->ev_comp.assign(pl->sub.size(), nullptr);
+    for (size_t i = 0; i < pl->sub.size(); ++i) {
+      SDP_CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_in[i], cudaEventDisableTiming));
+      SDP_CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_comp[i], cudaEventDisableTiming));
+    }
+    SDP_CUDA_TRY(cudaEventCreateWithFlags(&pl->ev_end, cudaEventDisableTiming));
+  }
+  // the copies start after the caller's earlier work on s (event ordering only)
+  SDP_CUDA_TRY(cudaEventRecord(pl->ev_end, s));
+  SDP_CUDA_TRY(cudaStreamWaitEvent(pl->cp_in, pl->ev_end, 0));
+  for (size_t i = 0; i < pl->sub.size(); ++i) {
+    SDP_CUDA_TRY(cudaMemcpyAsync(pl->h_in_dev + pl->sub_v0[i], h_in + pl->sub_v0[i],
+                                 pl->sub_nv[i] * sizeof(double), cudaMemcpyHostToDevice, pl->cp_in));
+    SDP_CUDA_TRY(cudaEventRecord(pl->ev_in[i], pl->cp_in));
+  }
+  for (size_t i = 0; i < pl->sub.size(); ++i) {
+    SDP_CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_in[i], 0));
+    const int rc = sdp_project_psd_batch(pl->sub[i], pl->h_in_dev + pl->sub_v0[i], pl->h_out_dev + pl->sub_v0[i], s);
+    if (rc != SDP_OK) throw Error{rc, std::string("sub-plan: ") + sdp_last_error()};
+    SDP_CUDA_TRY(cudaEventRecord(pl->ev_comp[i], s));
+    SDP_CUDA_TRY(cudaStreamWaitEvent(pl->cp_out, pl->ev_comp[i], 0));
+    SDP_CUDA_TRY(cudaMemcpyAsync(h_out + pl->sub_v0[i], pl->h_out_dev + pl->sub_v0[i], pl->sub_nv[i] * sizeof(double),
+                                 cudaMemcpyDeviceToHost, pl->cp_out));
+  }
+  SDP_CUDA_TRY(cudaEventRecord(pl->ev_end, pl->cp_out));
+  SDP_CUDA_TRY(cudaStreamWaitEvent(s, pl->ev_end, 0));
+  SDP_CUDA_TRY(cudaStreamSynchronize(s));
+}
+}  // namespace
+
+extern "C" {
+
 int sdp_project_psd_batch_host(sdp_psd_plan pl, const double* h_in, double* h_out, void* stream) {
   return guarded([&] {
     if (!pl) throw Error{SDP_E_INVALID_ARG, "plan is NULL"};
@@ -2883,6 +2979,10 @@ int sdp_project_psd_batch_host(sdp_psd_plan pl, const double* h_in, double* h_ou
       }
     }
     const int64_t nv = pl->values;
+    if (host_pinned(h_in) && host_pinned(h_out) && pl->count >= 4 * kPipeMinCount) {
+      project_pipelined(pl, h_in, h_out, s);
+      return SDP_OK;
+    }
     // H2D: host -> pinned chunk (all host threads) -> async DMA, two chunks in flight
     for (int64_t c0 = 0, it = 0; c0 < nv; c0 += kStageDoubles, ++it) {
       const int b = (int)(it & 1);
@@ -2939,6 +3039,13 @@ int sdp_psd_plan_destroy(sdp_psd_plan pl) {
     cudaGetDevice(&cur);
     cudaSetDevice(pl->device);
     cudaDeviceSynchronize();
+    for (auto* q : pl->sub) sdp_psd_plan_destroy(q);
+    pl->sub.clear();
+    if (pl->cp_in) cudaStreamDestroy(pl->cp_in);
+    if (pl->cp_out) cudaStreamDestroy(pl->cp_out);
+    for (auto e : pl->ev_in) cudaEventDestroy(e);
+    for (auto e : pl->ev_comp) cudaEventDestroy(e);
+    if (pl->ev_end) cudaEventDestroy(pl->ev_end);
     pl->alloc.free_all();
     pl->tiers.destroy();
     pl->free_stage();

@@ -212,6 +212,7 @@ struct ProjArgs {
   const int64_t* voff;
   const long long* iter;  // iteration counter; cold start when iter % warm_period == 0
   int32_t warm_period;    // 0 = never warm start
+  long long* rvtrace = nullptr;  // diagnostics (SDP_FUSED_TRACE): register-V Jacobi phase clocks
 };
 
 void launch_projection(int bucket, int mode, const ProjArgs& a, cudaStream_t s);

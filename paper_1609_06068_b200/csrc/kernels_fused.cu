@@ -32,6 +32,7 @@ namespace {
 
 constexpr int FT = kFusedThreads;  // threads per CTA
 constexpr int kLongSegF = kFusedLongSeg;
+constexpr int FU = 8;              // phases U / X: 16-byte loads in flight per lane
 constexpr int FW = FT / 32;        // warps per CTA
 
 __device__ __forceinline__ double fwarp_sum(double v) {
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(FT, 1) k_fused_iter(FusedArgs a) {
   ProjArgs pa = a.pa;
   pa.iter = &s_iter;  // the warm-start decision reads the CTA's copy of the iteration index
   pa.done = nullptr;
+  pa.rvtrace = a.trace ? a.trace + 64 * 16 : nullptr;
   const double2* rD2 = reinterpret_cast<const double2*>(a.rD);
   const double2* y2 = reinterpret_cast<const double2*>(a.y);
   long long* trace = (a.trace && blockIdx.x == 0) ? a.trace : nullptr;
@@ -278,16 +280,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_iter(FusedArgs a) {
         const int64_t j0 = part * per, j1 = min(np, j0 + per);
         const double2* Ar = reinterpret_cast<const double2*>(a.A + (int64_t)row * a.lda);
         double s0 = 0.0, s1 = 0.0;
-        for (int64_t j = j0 + lane; j < j1; j += 32 * 4) {
-          double2 av[4], rv[4];
+        for (int64_t j = j0 + lane; j < j1; j += 32 * FU) {
+          double2 av[FU], rv[FU];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < FU; ++q) {
             const int64_t jj = j + 32 * q;
             av[q] = jj < j1 ? __ldg(Ar + jj) : make_double2(0.0, 0.0);
             rv[q] = jj < j1 ? rD2[jj] : make_double2(0.0, 0.0);
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < FU; ++q) {
             s0 = fma(av[q].x, rv[q].x, s0);
             s1 = fma(av[q].y, rv[q].y, s1);
           }
@@ -357,16 +359,16 @@ __global__ void __launch_bounds__(FT, 1) k_fused_iter(FusedArgs a) {
         const bool ok = t < a.N;
         const double2* row = reinterpret_cast<const double2*>(a.AT + (int64_t)(ok ? t : 0) * a.ldm);
         double w0 = 0.0, w1 = 0.0;
-        for (int j = sl; j < np; j += L * 4) {
-          double2 av[4], yv[4];
+        for (int j = sl; j < np; j += L * FU) {
+          double2 av[FU], yv[FU];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < FU; ++q) {
             const int jj = j + L * q;
             av[q] = (ok && jj < np) ? __ldg(row + jj) : make_double2(0.0, 0.0);
             yv[q] = (ok && jj < np) ? y2[jj] : make_double2(0.0, 0.0);
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 0; q < FU; ++q) {
             w0 = fma(av[q].x, yv[q].x, w0);
             w1 = fma(av[q].y, yv[q].y, w1);
           }

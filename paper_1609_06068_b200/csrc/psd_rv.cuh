@@ -104,6 +104,10 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
   const int r = g.tid / Q;           // V row owned by this lane group
   const int q = g.tid - r * Q;       // part: slots [q*S, q*S + S)
   const unsigned qmask = Q == 1 ? 0u : (((1u << Q) - 1u) << ((threadIdx.x & 31) / Q * Q));
+  // diagnostics: clock64 per phase of the first group of CTA 0 (slots: calls, load, warm start,
+  // sweep loop, steps, sweeps, reconstruction + epilogue)
+  long long* rtr = (a.rvtrace && blockIdx.x == 0 && threadIdx.x == 0) ? a.rvtrace : nullptr;
+  long long rt0 = rtr ? clock64() : 0;
   // ---- load: zero padding, then the packed entries (gather H_k x)
   for (int e = g.tid; e < KP * KP; e += G) {
     const int rr = e / KP, cc = e - rr * KP;
@@ -125,6 +129,12 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
     }
     Ac[rr * LD + cc] = v;
     Ac[cc * LD + rr] = v;
+  }
+  if (rtr) {
+    const long long now = clock64();
+    rtr[0] += 1;
+    rtr[1] += now - rt0;
+    rt0 = now;
   }
   double v[S];
   const bool warm = (MODE != PM_BATCH) && T != nullptr && a.vprev != nullptr && a.warm_period > 0 &&
@@ -165,6 +175,11 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
     }
   }
   fro2 = g.sum(fro2);
+  if (rtr) {
+    const long long now = clock64();
+    rtr[2] += now - rt0;
+    rt0 = now;
+  }
   const double thr = kJacTol * kJacTol * fro2;
   // this thread's 2x2 blocks of the pair triangle (the same in every step: the slot permutation is
   // applied physically), with their source and destination offsets: A_next = (J^T A J) permuted by
@@ -284,6 +299,13 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
       An = tmp;
     }
   }
+  if (rtr) {
+    const long long now = clock64();
+    rtr[3] += now - rt0;
+    rtr[4] += (long long)sweep * (KP - 1);
+    rtr[5] += sweep;
+    rt0 = now;
+  }
   if (sweep == kMaxSweeps && g.tid == 0 && a.capped) atomicAdd(a.capped, 1ull);
   if (g.tid == 0 && a.sweeps) atomicAdd(a.sweeps, (unsigned long long)sweep);
   // sweep boundary: slot order == natural order.  V rows -> shared memory (An).
@@ -334,6 +356,7 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
     }
   }
   g.sync();
+  if (rtr) rtr[6] += clock64() - rt0;
 }
 
 }  // namespace

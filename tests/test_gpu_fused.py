@@ -129,8 +129,10 @@ def test_fused_deterministic_and_call_split(lib, gen):
     s.step(30)
     a = (s.x(), s.y(), s.blocks("xk"), s.blocks("lambda"), s.history())
     s.reset()
-    for _ in range(30):
+    for i in range(30):
         s.step(1)
+        if i % 7 == 3:
+            s.step(0)  # an empty call must not disturb the launches' barrier counters
     b = (s.x(), s.y(), s.blocks("xk"), s.blocks("lambda"), s.history())
     for u, v in zip(a, b):
         assert np.array_equal(u, v)

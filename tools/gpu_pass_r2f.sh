@@ -36,4 +36,15 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_t
   -o "$OUT/full_cfg4" python bench.py --workload cfg4 --steps 1 --warmup 3 --no-cpu > "$OUT/ncu_f4.log" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fused_iter" -s 10 -c 2 \
   -o "$OUT/full_cfg1" python bench.py --workload cfg1 --steps 20 --warmup 3 --no-cpu --also "" --e2e-cap 0 > "$OUT/ncu_f1.log" 2>&1
+python tools/fused_probe2.py trace > "$OUT/fused_trace.log" 2>&1
+# the reports are large (gpurun copies back <= 64 MiB): keep the raw-page CSV and the top SASS lines
+for r in full_cfg1 full_cfg2 full_cfg3 full_cfg4; do
+  if [ -f "$OUT/$r.ncu-rep" ]; then
+    ncu -i "$OUT/$r.ncu-rep" --page raw --csv > "$OUT/${r}_raw.csv" 2>/dev/null
+    ncu -i "$OUT/$r.ncu-rep" --page source --csv --print-source sass > "$OUT/${r}_sass.csv" 2>/dev/null
+    gzip -f "$OUT/${r}_sass.csv"
+    rm -f "$OUT/$r.ncu-rep"
+  fi
+done
+du -sh "$OUT" >> "$OUT/rc.txt"
 echo done >> "$OUT/rc.txt"
