@@ -290,7 +290,13 @@ int sdp_psd_plan_create_ex(int64_t count, const int32_t* h_sizes, int32_t device
 /* out_i = argmin_{P PSD} ||P - in_i||_F for every i.  d_in, d_out: device,
  * may alias (in place).  Asynchronous on `stream` (cudaStream_t, NULL = default). */
 int sdp_project_psd_batch(sdp_psd_plan plan, const double* d_in, double* d_out, void* stream);
-/* Same, from/to HOST buffers (copies inside the call; synchronous). */
+/* Same, from/to HOST buffers (copies inside the call; synchronous).  h_in, h_out: host, owned by
+ * the caller, `values` doubles each, must not alias.  Pageable buffers are staged through two
+ * pinned chunks (host copies overlapping the DMA).  When BOTH buffers are pinned (cudaHostAlloc /
+ * torch pin_memory) and the plan holds >= 16384 matrices, the batch is streamed as four contiguous
+ * sub-plans (created on the first such call, from the plan's allocator) whose H2D copy, projection
+ * and D2H copy overlap; each matrix may then take a different tier than in the whole-batch plan
+ * (tier choice depends on the count per size range), so results agree to rounding, not bitwise. */
 int sdp_project_psd_batch_host(sdp_psd_plan plan, const double* h_in, double* h_out, void* stream);
 int64_t sdp_psd_plan_values(sdp_psd_plan plan);   /* total doubles of in/out */
 /* Kernel launches one sdp_project_psd_batch call makes (diagnostics; -1 if plan is NULL). */
