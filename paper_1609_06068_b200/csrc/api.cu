@@ -2887,7 +2887,10 @@ int sdp_project_psd_batch(sdp_psd_plan pl, const double* d_in, double* d_out, vo
 
 namespace {
 constexpr int64_t kPipeMinCount = 4096;  // matrices per sub-plan of the pinned pipeline (at least)
-constexpr int kPipeChunks = 4;
+int pipe_chunks() {  // SDP_PSD_PIPE_CHUNKS (default 4)
+  const char* e = getenv("SDP_PSD_PIPE_CHUNKS");
+  return e ? std::max(2, std::min(16, atoi(e))) : 4;
+}
 
 bool host_pinned(const void* p) {
   cudaPointerAttributes at{};
@@ -2898,7 +2901,7 @@ bool host_pinned(const void* p) {
   return at.type == cudaMemoryTypeHost;
 }
 
-// Pinned host buffers: kPipeChunks contiguous sub-plans (equal value counts); chunk i's H2D copy
+// Pinned host buffers: pipe_chunks() contiguous sub-plans (equal value counts); chunk i's H2D copy
 // (stream cp_in), projection (the caller's stream) and D2H copy (stream cp_out) are ordered by
 // events only, so copies in both directions run beside the projections of other chunks.
 void project_pipelined(sdp_psd_plan pl, const double* h_in, double* h_out, cudaStream_t s) {
@@ -2909,10 +2912,11 @@ void project_pipelined(sdp_psd_plan pl, const double* h_in, double* h_out, cudaS
   if (pl->sub.empty()) {
     const int64_t n = pl->count;
     int64_t start = 0, v = 0;
-    for (int c = 0; c < kPipeChunks && start < n; ++c) {
-      const int64_t target = pl->values * (c + 1) / kPipeChunks;
+    const int nch = pipe_chunks();
+    for (int c = 0; c < nch && start < n; ++c) {
+      const int64_t target = pl->values * (c + 1) / nch;
       int64_t end = start, nvc = 0;
-      while (end < n && (c == kPipeChunks - 1 || v + nvc < target)) {
+      while (end < n && (c == nch - 1 || v + nvc < target)) {
         const int64_t k = pl->h_sizes[end];
         nvc += k * (k + 1) / 2;
         ++end;
