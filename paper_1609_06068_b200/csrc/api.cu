@@ -2222,7 +2222,7 @@ void launch_iterations(sdp_handle h, int32_t iters, bool for_solve = false) {
     FusedArgs fa = fused_args(h, iters);
     const char* tr = getenv("SDP_FUSED_TRACE");
     if (tr && *tr == '1') {
-      if (!h->fused_trace) h->fused_trace = h->alloc.zeros<long long>(64 * 16 + 8);
+      if (!h->fused_trace) h->fused_trace = h->alloc.zeros<long long>(64 * 16 + 16);
       fa.trace = h->fused_trace;
     }
     if (iters <= 0) return;
@@ -2230,7 +2230,7 @@ void launch_iterations(sdp_handle h, int32_t iters, bool for_solve = false) {
     SDP_CUDA_TRY(cudaGetLastError());
     h->fused_parity ^= 1;  // the next launch uses the other barrier counter (zeroed by this one)
     if (fa.trace) {  // mean time between consecutive marks (CTA 0, %globaltimer), iterations 1..63
-      std::vector<long long> t(64 * 16 + 8);
+      std::vector<long long> t(64 * 16 + 16);
       SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
       SDP_CUDA_TRY(cudaMemcpy(t.data(), fa.trace, t.size() * sizeof(long long), cudaMemcpyDeviceToHost));
       const int n = std::min(iters, 64);

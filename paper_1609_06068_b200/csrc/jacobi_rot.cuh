@@ -20,41 +20,36 @@ struct JRot {
 };
 
 __device__ __forceinline__ JRot jacobi_rotation(double app, double aqq, double apq) {
-  JRot r{1.0, 0.0};
-  if (apq == 0.0) return r;
+  // Branch-free (the rotation is on the critical chain of every Jacobi step).  Any orthogonal J is
+  // a valid similarity, so the accuracy of t only affects how fast off(A) falls: the power-of-two
+  // scaling is clamped instead of special-cased (mx outside [2^-1000, 2^1000] only slows the
+  // estimate down), and apq == 0 selects the identity at the end.
   const double d = aqq - app;
-  // power-of-two scale so that max(|d|, |apq|) is in [1, 2)
   const double mx = fmax(fabs(d), fabs(apq));
-  // 2^-e with e = ilogb(mx), from the exponent bits (exact power of two, so
-  // multiplying by it equals scalbn(., -e)); libm ilogb/scalbn only for
-  // subnormal / extreme mx
-  const int ex = ((__double2hiint(mx) >> 20) & 0x7ff) - 1023;
-  double ds, as;
-  if (ex > -1022 && ex < 1022) {
-    const double sc = __hiloint2double((1023 - ex) << 20, 0);
-    ds = d * sc;
-    as = apq * sc;
-  } else {
-    const int e = ilogb(mx);
-    ds = scalbn(d, -e);
-    as = scalbn(apq, -e);
-  }
+  // 2^-e with e = ilogb(mx) from the exponent bits, clamped so that 2^-e stays a normal number
+  int ex = ((__double2hiint(mx) >> 20) & 0x7ff) - 1023;
+  ex = min(max(ex, -1000), 1000);
+  const double sc = __hiloint2double((1023 - ex) << 20, 0);
+  const double ds = d * sc, as = apq * sc;
   const float df = (float)ds, af = (float)as;
-  // fp32 smaller root: t = 2 apq sign(d) / (|d| + sqrt(d^2 + 4 apq^2))
-  // (approximate fp32 square root and divisions: the estimate only seeds the fp64 Newton step, and
-  // the scaled operands keep every intermediate in [2^-60, 8], far from the approximations' limits)
-  const float q = df * df + 4.0f * af * af;  // > 0: |as| >= 2^-53 |ds| or |ds| in [1, 2)
+  // fp32 smaller root: t = 2 apq sign(d) / (|d| + sqrt(d^2 + 4 apq^2)).  Approximate fp32 square
+  // root and divisions: the estimate only seeds the fp64 Newton step (q >= 1e-30 keeps rsqrtf finite;
+  // q = 0 means apq = 0, selected away below)
+  const float q = fmaxf(df * df + 4.0f * af * af, 1e-30f);
   const float rf = q * rsqrtf(q);
   const float den = fabsf(df) + rf;
-  float tf = __fdividef((df >= 0.0f ? 2.0f : -2.0f) * af, den);
+  const float tf = __fdividef((df >= 0.0f ? 2.0f : -2.0f) * af, den);
   double t = (double)tf;
-  // one fp64 Newton step on g(t) = apq t^2 + d t - apq (scaled coefficients)
+  // one fp64 Newton step on g(t) = apq t^2 + d t - apq (scaled coefficients); g'(t) in fp32 is
+  // +-sqrt(d^2 + 4 apq^2) at the root, nonzero whenever apq != 0
   const double g = fma(fma(as, t, ds), t, -as);
-  const float gp = 2.0f * af * tf + df;  // g'(t) in fp32
-  if (gp != 0.0f) t -= g * (double)__fdividef(1.0f, gp);
+  const float gp = 2.0f * af * tf + df;
+  t -= g * (double)__fdividef(1.0f, gp);
   const double c = rsqrt(fma(t, t, 1.0));
-  r.c = c;
-  r.s = t * c;
+  JRot r;
+  const bool zero = apq == 0.0;
+  r.c = zero ? 1.0 : c;
+  r.s = zero ? 0.0 : t * c;
   return r;
 }
 

@@ -236,32 +236,6 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
         rs[i] = jr.s;
       }
       g.sync();
-#pragma unroll
-      for (int u = 0; u < NBU; ++u) {
-        if (b_src[u] < 0) continue;
-        const int i = b_i[u], j = b_j[u];
-        const double2 top = *reinterpret_cast<const double2*>(Ac + b_src[u]);
-        const double2 bot = *reinterpret_cast<const double2*>(Ac + b_src[u] + LD);
-        const double c1 = rc[i], s1 = rs[i];
-        if (i == j) {
-          // full J^T B J (the rotation annihilates a_pq only to ~1e-14 relative)
-          const double app = top.x, apq = top.y, aqq = bot.y;
-          const double r00 = c1 * app - s1 * apq, r01 = c1 * apq - s1 * aqq;
-          const double r10 = s1 * app + c1 * apq, r11 = s1 * apq + c1 * aqq;
-          const double n01 = 0.5 * ((s1 * r00 + c1 * r01) + (c1 * r10 - s1 * r11));
-          An[b_d[u][0]] = c1 * r00 - s1 * r01;
-          An[b_d[u][1]] = s1 * r10 + c1 * r11;
-          An[b_d[u][2]] = n01;
-        } else {
-          const double c2 = rc[j], s2 = rs[j];
-          const double r00 = c1 * top.x - s1 * bot.x, r01 = c1 * top.y - s1 * bot.y;
-          const double r10 = s1 * top.x + c1 * bot.x, r11 = s1 * top.y + c1 * bot.y;
-          An[b_d[u][0]] = c2 * r00 - s2 * r01;
-          An[b_d[u][1]] = s2 * r00 + c2 * r01;
-          An[b_d[u][2]] = c2 * r10 - s2 * r11;
-          An[b_d[u][3]] = s2 * r10 + c2 * r11;
-        }
-      }
       // V <- V J in registers (this lane's S/2 pairs), then the slot permutation:
       // even slots move +2, odd slots -2; one element crosses to each neighbour lane
 #pragma unroll
@@ -292,6 +266,32 @@ __device__ void project_rv(const RvGroup<KP * Q>& g, const int k, const int64_t 
         if (q == Q - 1) nv[S - 1] = v[S - 2];  // slot KP-2 -> KP-1
 #pragma unroll
         for (int l = 0; l < S; ++l) v[l] = nv[l];
+      }
+#pragma unroll
+      for (int u = 0; u < NBU; ++u) {
+        if (b_src[u] < 0) continue;
+        const int i = b_i[u], j = b_j[u];
+        const double2 top = *reinterpret_cast<const double2*>(Ac + b_src[u]);
+        const double2 bot = *reinterpret_cast<const double2*>(Ac + b_src[u] + LD);
+        const double c1 = rc[i], s1 = rs[i];
+        if (i == j) {
+          // full J^T B J (the rotation annihilates a_pq only to ~1e-14 relative)
+          const double app = top.x, apq = top.y, aqq = bot.y;
+          const double r00 = c1 * app - s1 * apq, r01 = c1 * apq - s1 * aqq;
+          const double r10 = s1 * app + c1 * apq, r11 = s1 * apq + c1 * aqq;
+          const double n01 = 0.5 * ((s1 * r00 + c1 * r01) + (c1 * r10 - s1 * r11));
+          An[b_d[u][0]] = c1 * r00 - s1 * r01;
+          An[b_d[u][1]] = s1 * r10 + c1 * r11;
+          An[b_d[u][2]] = n01;
+        } else {
+          const double c2 = rc[j], s2 = rs[j];
+          const double r00 = c1 * top.x - s1 * bot.x, r01 = c1 * top.y - s1 * bot.y;
+          const double r10 = s1 * top.x + c1 * bot.x, r11 = s1 * top.y + c1 * bot.y;
+          An[b_d[u][0]] = c2 * r00 - s2 * r01;
+          An[b_d[u][1]] = s2 * r00 + c2 * r01;
+          An[b_d[u][2]] = c2 * r10 - s2 * r11;
+          An[b_d[u][3]] = s2 * r10 + c2 * r11;
+        }
       }
       g.sync();
       double* tmp = Ac;
