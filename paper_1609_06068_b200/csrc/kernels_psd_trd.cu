@@ -296,8 +296,8 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
       for (int l = L0; l < KP; l += 2) {
         const double2 w2 = *reinterpret_cast<const double2*>(ws + l);
         const double2 v2 = *reinterpret_cast<const double2*>(vs + l);
-        A[l] -= fma(vi, w2.x, wi * v2.x);
-        A[l + 1] -= fma(vi, w2.y, wi * v2.y);
+        A[l] = fma(-vi, w2.x, fma(-wi, v2.x, A[l]));  // two DFMA (no DMUL + DADD)
+        A[l + 1] = fma(-vi, w2.y, fma(-wi, v2.y, A[l + 1]));
       }
       // (the next column writes vs / ws only after the barriers of its g.sum)
     }
@@ -471,6 +471,7 @@ __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& 
   return ok;
 }
 
+
 template <int KP, bool RSQ = false>
 __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
@@ -527,28 +528,47 @@ __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslo
   a.td.rcount[slot] = ok ? 0 : -1;
 }
 
-// ---------------------------------------------------------------- 3. inverse iteration
-// One thread per cluster of selected eigenvalues (LAPACK dstein): for each
-// eigenvalue in the cluster, the partial-pivoting LU of T - lam I (dlagtf;
-// pivots below tol replaced by +-tol, stored inverted), then kTrdInvIters = 2 solves
-// (dlagts) from a deterministic pseudo-random start, each followed by modified
-// Gram-Schmidt against the cluster's previous vectors and normalisation.  The
-// per-thread factors live in shared memory, thread-minor.  A vector whose
-// residual ||T z - lam z||_inf exceeds 1e-9 ||T|| marks the matrix (rcount = -1)
-// and the apply kernel redoes it by QL with eigenvector accumulation.
+// ---------------------------------------------------------------- 3. eigenvectors of T
+// One thread per cluster of selected eigenvalues (gap <= 1e-3 ||T||, LAPACK dstein's ORTOL).
+// A singleton (the usual case) takes the twisted factorization of T - lam I (Dhillon & Parlett's
+// getvec, here on T itself: lam is accurate to eps ||T|| and its gap is > 1e-3 ||T||): the
+// top-down T - lam I = L+ D+ L+^T and bottom-up U- D- U-^T pivots, the twist index
+// r = argmin |gamma_i|, gamma_i = D+_i - e_i^2 / D-_{i+1}, then z_r = 1,
+// z_i = -(e_i / D+_i) z_{i+1} below r and z_i = -(e_{i-1} / D-_i) z_{i-1} above r, for which
+// (T - lam I) z = gamma_r e_r.  That is two pivot chains and one product pass, against the LU
+// chain and two forward / back substitution pairs of inverse iteration, and two per-thread
+// arrays (the reciprocal pivots) instead of three, so more threads are resident.  A cluster is
+// handled by inverse iteration (dstein: partial-pivoting LU of T - lam I (dlagtf; pivots below
+// tol replaced by +-tol, stored inverted), kTrdInvIters = 2 solves (dlagts) from a
+// deterministic pseudo-random start, each followed by modified Gram-Schmidt against the
+// cluster's previous vectors and normalisation), its iterate in the output column.  Every
+// vector is then checked: ||T z - lam z||_inf > 1e-9 ||T|| ||z||_inf (NaN included) marks the
+// matrix (rcount = -1) and the apply kernel redoes it by QL with eigenvector accumulation.
 constexpr int IV_T = 32;  // threads per CTA
 constexpr int kTrdInvIters = 2;  // solves per vector (eigenvalues from QL are accurate to eps ||T||)
 template <int KP>
 struct InvLayout {
   static constexpr int HALF = KP / 2;        // selected eigenvalues per matrix <= k / 2
   static constexpr int NMAT = IV_T / HALF;   // matrices per CTA
-  static constexpr size_t bytes() { return (size_t)(3 * KP * IV_T + NMAT * 2 * KP) * sizeof(double); }
+  static constexpr size_t bytes() { return (size_t)(2 * KP * IV_T + NMAT * 2 * KP) * sizeof(double); }
 };
+
+// 1 / x to full fp64 precision: hardware approximation + two Newton steps (no IEEE-division
+// slow path on the pivot chains)
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double t = fma(-x, r, 1.0);
+  r = fma(r, t, r);
+  t = fma(-x, r, 1.0);
+  return fma(r, t, r);
+}
 
 template <int KP>
 __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = InvLayout<KP>;
+  constexpr int ZL = KP / 2;  // row length of the output block
   extern __shared__ double smem[];
   const int t = threadIdx.x;
   const int sl = blockIdx.x * Lay::NMAT + t / Lay::HALF;
@@ -560,7 +580,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   const int k = a.ksz[a.ids[slot]];
   // T (d, e) into shared memory: the recurrences below read it element by element, and the
   // workspace is far larger than L2 / L1, so global reads would each pay a DRAM round trip
-  double* d = smem + 3 * KP * IV_T + (t / Lay::HALF) * 2 * KP;
+  double* d = smem + 2 * KP * IV_T + (t / Lay::HALF) * 2 * KP;
   double* e = d + KP;
   for (int i = j0; i < k; i += Lay::HALF) {
     d[i] = H.d()[i];
@@ -570,102 +590,175 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   if (j0 >= nsel || (int)H.clst()[j0] != j0) return;
   const double tnorm = H.hdr()[2];
   const double tol = 2.220446049250313e-16 * fmax(tnorm, 1e-300);
-  double* ui = smem + t;  // inverse pivots, element i at [i * IV_T]
-  double* mu = ui + KP * IV_T;
-  double* x = mu + KP * IV_T;
-  // the first superdiagonal of U is recomputed in the back substitution (3 instead of 4
-  // per-thread arrays: 33 % more resident threads): u2_i = d_{i+1} - lam where row i
-  // pivoted, else the carried r1 = e_0 (i = 0), -mu_{i-1} e_i (row i-1 pivoted) or e_i;
-  // the second superdiagonal is e_{i+1} where row i pivoted, else 0
+  double* A0 = smem + t;  // per-thread arrays, element i at [i * IV_T]
+  double* A1 = A0 + KP * IV_T;
   double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [i][j], row length KP/2
+  const bool single = j0 + 1 >= nsel || (int)H.clst()[j0 + 1] != j0;
   bool fail = false;
-  for (int j = j0; j < nsel && (int)H.clst()[j] == j0; ++j) {
-    const double lam = H.lsel()[j];
-    unsigned long long pv = 0ull;  // pivot flags (k <= 64)
-    double r0 = d[0] - lam, r1 = k > 1 ? e[0] : 0.0;
-    for (int i = 0; i + 1 < k; ++i) {
-      const double ci = e[i], ai = d[i + 1] - lam, bi = (i + 2 < k) ? e[i + 1] : 0.0;
-      double p1, p2, m;
-      if (fabs(ci) > fabs(r0)) {
-        pv |= 1ull << i;
-        p1 = ci;
-        p2 = ai;
-        m = r0 / ci;
-        r0 = r1 - m * ai;
-        r1 = -m * bi;
+  if (single) {
+    const double lam = H.lsel()[j0];
+    double* rm = A0;  // 1 / D-_i
+    double* rp = A1;  // 1 / D+_i
+    double dm = d[k - 1] - lam;
+    if (fabs(dm) < tol) dm = dm < 0.0 ? -tol : tol;
+    rm[(k - 1) * IV_T] = rcp_nr(dm);
+    for (int i = k - 2; i >= 1; --i) {
+      const double ei = e[i];
+      dm = fma(-ei * ei, rm[(i + 1) * IV_T], d[i] - lam);
+      if (fabs(dm) < tol) dm = dm < 0.0 ? -tol : tol;
+      rm[i * IV_T] = rcp_nr(dm);
+    }
+    double dp = 0.0, best = 0.0;
+    int r = 0;
+    for (int i = 0; i < k; ++i) {
+      const double ai = d[i] - lam;
+      if (i == 0) {
+        dp = ai;
       } else {
-        p1 = r0;
-        p2 = r1;
-        m = r0 != 0.0 ? ci / r0 : 0.0;
-        r0 = ai - m * r1;
-        r1 = bi;
+        const double em = e[i - 1];
+        dp = fma(-em * em, rp[(i - 1) * IV_T], ai);
       }
-      if (fabs(p1) < tol) p1 = p1 < 0.0 ? -tol : tol;
-      ui[i * IV_T] = 1.0 / p1;
-      mu[i * IV_T] = m;
-      (void)p2;
+      if (fabs(dp) < tol) dp = dp < 0.0 ? -tol : tol;
+      rp[i * IV_T] = rcp_nr(dp);
+      const double gam = i + 1 < k ? fma(-e[i] * e[i], rm[(i + 1) * IV_T], dp) : dp;
+      if (i == 0 || fabs(gam) < best) {
+        best = fabs(gam);
+        r = i;
+      }
     }
-    if (fabs(r0) < tol) r0 = r0 < 0.0 ? -tol : tol;
-    ui[(k - 1) * IV_T] = 1.0 / r0;
-    for (int i = 0; i < k; ++i) {
-      unsigned long long h = (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull ^
-                             (unsigned long long)(j + 7) * 0xD1B54A32D192ED03ull;
-      h ^= h >> 31;
-      h *= 0xBF58476D1CE4E5B9ull;
-      h ^= h >> 29;
-      x[i * IV_T] = (double)(h >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+    // z is written unnormalised; its residual rows and its norm are formed on the way, and the
+    // reconstruction weight takes the 1 / ||z||^2 (w z z^T / ||z||^2 = w v v^T)
+    double* zj = Zo + j0;
+    zj[r * ZL] = 1.0;
+    double u1 = 1.0, u2 = 0.0, w1 = 1.0, w2 = 0.0;  // z at the last two rows of each chain
+    double zr_up = 0.0, zr_dn = 0.0, nrm = 1.0, mx = 1.0, res = 0.0;
+    for (int s = 1; s < k; ++s) {  // the two product chains run side by side
+      const int iu = r + s, id = r - s;
+      if (iu < k) {
+        const double z = u1 * (-e[iu - 1] * rm[iu * IV_T]);
+        zj[iu * ZL] = z;
+        if (s >= 2) res = fmax(res, fabs(fma(e[iu - 2], u2, fma(d[iu - 1] - lam, u1, e[iu - 1] * z))));
+        else zr_up = z;
+        u2 = u1;
+        u1 = z;
+        nrm = fma(z, z, nrm);
+        mx = fmax(mx, fabs(z));
+      }
+      if (id >= 0) {
+        const double z = w1 * (-e[id] * rp[id * IV_T]);
+        zj[id * ZL] = z;
+        if (s >= 2) res = fmax(res, fabs(fma(e[id], z, fma(d[id + 1] - lam, w1, e[id + 1] * w2))));
+        else zr_dn = z;
+        w2 = w1;
+        w1 = z;
+        nrm = fma(z, z, nrm);
+        mx = fmax(mx, fabs(z));
+      }
     }
-    for (int it = 0; it < kTrdInvIters; ++it) {
-      double ry = x[0];
+    // rows r, k - 1 (above r) and 0 (below r)
+    res = fmax(res, fabs((d[r] - lam) + (r >= 1 ? e[r - 1] * zr_dn : 0.0) + (r + 1 < k ? e[r] * zr_up : 0.0)));
+    if (r + 1 < k) res = fmax(res, fabs(fma(e[k - 2], u2, (d[k - 1] - lam) * u1)));
+    if (r >= 1) res = fmax(res, fabs(fma(e[0], w2, (d[0] - lam) * w1)));
+    if (!(res <= 1e-9 * fmax(tnorm, 1e-300) * mx) || !(nrm < 1e300)) fail = true;  // NaN / Inf too
+    else H.lw()[j0] /= nrm;
+  } else {
+    double* ui = A0;  // inverse pivots
+    double* mu = A1;  // multipliers
+    // the first superdiagonal of U is recomputed in the back substitution: u2_i = d_{i+1} - lam
+    // where row i pivoted, else the carried r1 = e_0 (i = 0), -mu_{i-1} e_i (row i-1 pivoted) or
+    // e_i; the second superdiagonal is e_{i+1} where row i pivoted, else 0
+    for (int j = j0; j < nsel && (int)H.clst()[j] == j0; ++j) {
+      const double lam = H.lsel()[j];
+      double* x = Zo + j;  // the iterate lives in its output column (row stride KP/2)
+      unsigned long long pv = 0ull;  // pivot flags (k <= 64)
+      double r0 = d[0] - lam, r1 = k > 1 ? e[0] : 0.0;
       for (int i = 0; i + 1 < k; ++i) {
-        const double yn = x[(i + 1) * IV_T];
-        const double m = mu[i * IV_T];
-        if ((pv >> i) & 1ull) {
-          x[i * IV_T] = yn;
-          ry = fma(-m, yn, ry);
+        const double ci = e[i], ai = d[i + 1] - lam, bi = (i + 2 < k) ? e[i + 1] : 0.0;
+        double p1, m;
+        if (fabs(ci) > fabs(r0)) {
+          pv |= 1ull << i;
+          p1 = ci;
+          m = r0 / ci;
+          r0 = r1 - m * ai;
+          r1 = -m * bi;
         } else {
-          x[i * IV_T] = ry;
-          ry = fma(-m, ry, yn);
+          p1 = r0;
+          m = r0 != 0.0 ? ci / r0 : 0.0;
+          r0 = ai - m * r1;
+          r1 = bi;
         }
+        if (fabs(p1) < tol) p1 = p1 < 0.0 ? -tol : tol;
+        ui[i * IV_T] = 1.0 / p1;
+        mu[i * IV_T] = m;
       }
-      double xn = ry * ui[(k - 1) * IV_T], xn1 = 0.0;
-      x[(k - 1) * IV_T] = xn;
-      double mx = fabs(xn);
-      for (int i = k - 2; i >= 0; --i) {
-        const bool piv = (pv >> i) & 1ull;
-        const double u3 = piv ? e[i + 1] : 0.0;  // i + 2 < k here
-        const double u2 = piv ? d[i + 1] - lam
-                              : (i == 0 ? e[0] : (((pv >> (i - 1)) & 1ull) ? -mu[(i - 1) * IV_T] * e[i] : e[i]));
-        const double xi = (x[i * IV_T] - u2 * xn - u3 * xn1) * ui[i * IV_T];
-        x[i * IV_T] = xi;
-        mx = fmax(mx, fabs(xi));
-        xn1 = xn;
-        xn = xi;
+      if (fabs(r0) < tol) r0 = r0 < 0.0 ? -tol : tol;
+      ui[(k - 1) * IV_T] = 1.0 / r0;
+      for (int i = 0; i < k; ++i) {
+        unsigned long long h = (unsigned long long)(i + 1) * 0x9E3779B97F4A7C15ull ^
+                               (unsigned long long)(j + 7) * 0xD1B54A32D192ED03ull;
+        h ^= h >> 31;
+        h *= 0xBF58476D1CE4E5B9ull;
+        h ^= h >> 29;
+        x[i * ZL] = (double)(h >> 11) * (2.0 / 9007199254740992.0) - 1.0;
       }
-      const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
-      for (int i = 0; i < k; ++i) x[i * IV_T] *= inv;
-      for (int p = j0; p < j; ++p) {
-        const double* zp = Zo + p;  // column p of the [i][j] block (row length KP/2)
-        double dot = 0.0;
-        for (int i = 0; i < k; ++i) dot = fma(zp[i * (KP / 2)], x[i * IV_T], dot);
-        for (int i = 0; i < k; ++i) x[i * IV_T] = fma(-dot, zp[i * (KP / 2)], x[i * IV_T]);
+      for (int it = 0; it < kTrdInvIters; ++it) {
+        double ry = x[0];
+        for (int i = 0; i + 1 < k; ++i) {
+          const double yn = x[(i + 1) * ZL];
+          const double m = mu[i * IV_T];
+          if ((pv >> i) & 1ull) {
+            x[i * ZL] = yn;
+            ry = fma(-m, yn, ry);
+          } else {
+            x[i * ZL] = ry;
+            ry = fma(-m, ry, yn);
+          }
+        }
+        double xn = ry * ui[(k - 1) * IV_T], xn1 = 0.0;
+        x[(k - 1) * ZL] = xn;
+        double mx = fabs(xn);
+        for (int i = k - 2; i >= 0; --i) {
+          const bool piv = (pv >> i) & 1ull;
+          const double u3 = piv ? e[i + 1] : 0.0;  // i + 2 < k here
+          const double u2 = piv ? d[i + 1] - lam
+                                : (i == 0 ? e[0] : (((pv >> (i - 1)) & 1ull) ? -mu[(i - 1) * IV_T] * e[i] : e[i]));
+          const double xi = (x[i * ZL] - u2 * xn - u3 * xn1) * ui[i * IV_T];
+          x[i * ZL] = xi;
+          mx = fmax(mx, fabs(xi));
+          xn1 = xn;
+          xn = xi;
+        }
+        const double inv = mx > 0.0 ? 1.0 / mx : 1.0;
+        for (int i = 0; i < k; ++i) x[i * ZL] *= inv;
+        for (int p = j0; p < j; ++p) {
+          const double* zp = Zo + p;  // column p of the [i][j] block
+          double dot = 0.0;
+          for (int i = 0; i < k; ++i) dot = fma(zp[i * ZL], x[i * ZL], dot);
+          for (int i = 0; i < k; ++i) x[i * ZL] = fma(-dot, zp[i * ZL], x[i * ZL]);
+        }
+        double nrm = 0.0;
+        for (int i = 0; i < k; ++i) nrm = fma(x[i * ZL], x[i * ZL], nrm);
+        const double in2 = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+        for (int i = 0; i < k; ++i) x[i * ZL] *= in2;
       }
-      double nrm = 0.0;
-      for (int i = 0; i < k; ++i) nrm = fma(x[i * IV_T], x[i * IV_T], nrm);
-      const double in2 = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
-      for (int i = 0; i < k; ++i) x[i * IV_T] *= in2;
     }
-    double res = 0.0;
+  }
+  // check every vector of the cluster against T
+  for (int j = j0; !single && j < nsel && (int)H.clst()[j] == j0; ++j) {
+    const double lam = H.lsel()[j];
     double* zj = Zo + j;
+    double res = 0.0, mx = 0.0, zprev = 0.0, zi = zj[0];
     for (int i = 0; i < k; ++i) {
-      const double xi = x[i * IV_T];
-      double tz = (d[i] - lam) * xi;
-      if (i > 0) tz = fma(e[i - 1], x[(i - 1) * IV_T], tz);
-      if (i + 1 < k) tz = fma(e[i], x[(i + 1) * IV_T], tz);
+      const double znext = i + 1 < k ? zj[(i + 1) * ZL] : 0.0;
+      double tz = (d[i] - lam) * zi;
+      if (i > 0) tz = fma(e[i - 1], zprev, tz);
+      if (i + 1 < k) tz = fma(e[i], znext, tz);
       res = fmax(res, fabs(tz));
-      zj[i * (KP / 2)] = xi;  // [i][j]: the threads of a matrix write consecutive j
+      mx = fmax(mx, fabs(zi));
+      zprev = zi;
+      zi = znext;
     }
-    if (!(res <= 1e-9 * fmax(tnorm, 1e-300))) fail = true;  // includes NaN
+    if (!(res <= 1e-9 * fmax(tnorm, 1e-300) * mx)) fail = true;  // includes NaN / Inf
   }
   if (fail) a.td.rcount[slot] = -1;
 }

@@ -6,7 +6,7 @@ import paper_1609_06068_b200 as L
 import sdp_inputs as gen
 
 res = {}
-for k in (8, 16, 32, 64):
+for k in ([int(x) for x in sys.argv[1].split(',')] if len(sys.argv) > 1 else (8, 16, 32, 64)):
     for count in (50000,):
         ks = np.full(count, k, np.int32)
         rng = np.random.default_rng(k)
