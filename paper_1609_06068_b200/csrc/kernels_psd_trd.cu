@@ -380,6 +380,7 @@ __global__ void __launch_bounds__(128, 3) k_trd_tridiag_reg(ProjArgs a, int slot
 
 static int g_trd_reg = 1;    // SDP_TRD_REG=0: the shared-memory tridiagonalization
 static int g_ql_rsqrt = 1;  // SDP_TRD_QLRSQ=0: QL rotations with sqrt + reciprocal
+__constant__ int g_ql_fused = 1;  // SDP_TRD_QLFUSED=0: tql's scan loop in the QL kernel
 
 // ---------------------------------------------------------------- 2. implicit QL
 // One tqli chain on T (d, e; e[i] couples i and i+1).  T is first scaled by a
@@ -472,6 +473,120 @@ __device__ __forceinline__ bool tql(int k, double* d, double* e, int st, Emit&& 
 }
 
 
+// tql without eigenvectors, the same shifts, rotations and deflation tests (the same eigenvalues
+// up to where the compiler contracts a multiply-add), with the chain shortened for the
+// one-chain-per-lane QL kernel (k = 64 bucket of cfg4: 3.28 -> 2.48 ms):
+//  * no separate scan for m: after the rotation at i, d[i+1], e[i+1] and d[i+2] hold their
+//    final values for this sweep, so the test of position i+1 that tql's next scan makes is
+//    made there (d[i+2] carried in a register), position l when the sweep ends, and the lowest
+//    negligible position found is the next m (a full scan runs only when l passes m, i.e. at
+//    the start of an unreduced block, and after the q == 0 early deflation);
+//  * the next rotation's operands e[i-1], d[i-1] are loaded one rotation ahead (no rotation
+//    writes them), so the shared-memory latency leaves the dependent chain.
+template <bool RSQ = false>
+__device__ __forceinline__ bool tql_vals(int k, double* d, double* e, int st) {
+  double mx = 0.0;
+  for (int i = 0; i < k; ++i) mx = fmax(mx, fmax(fabs(d[i * st]), fabs(e[i * st])));
+  if (mx == 0.0) return true;
+  const int ex = ilogb(mx);
+  const double sc = scalbn(1.0, -ex), usc = scalbn(1.0, ex);
+  double tn = 0.0;
+  for (int i = 0; i < k; ++i) {
+    d[i * st] *= sc;
+    e[i * st] *= sc;
+  }
+  for (int i = 0; i < k; ++i)
+    tn = fmax(tn, fabs(d[i * st]) + fabs(e[i * st]) + (i > 0 ? fabs(e[(i - 1) * st]) : 0.0));
+  const double gtol = 2.220446049250313e-16 * tn;
+  auto negl = [gtol](double dj, double dj1, double ej) {
+    const double dd = fabs(dj) + fabs(dj1), em = fabs(ej);
+    return em + dd == dd || em <= gtol;
+  };
+  auto scan = [&](int j) {
+    while (j < k - 1 && !negl(d[j * st], d[(j + 1) * st], e[j * st])) ++j;
+    return j;
+  };
+  bool ok = true;
+  int m = scan(0);
+  for (int l = 0; l < k && ok; ++l) {
+    if (m < l) m = scan(l);
+    int iter = 0, mnext = -1;
+    while (m != l) {
+      if (iter++ == kQlMaxIter) {
+        ok = false;
+        break;
+      }
+      double di = d[l * st];
+      const double el = e[l * st];
+      double g = (d[(l + 1) * st] - di) / (2.0 * el);
+      double r = fabs(g) > 1e150 ? fabs(g) : sqrt(fma(g, g, 1.0));
+      g = d[m * st] - di + el / (g + copysign(r, g));
+      double s = 1.0, c = 1.0, p = 0.0, dprev = 0.0;
+      int i = m - 1, mlo = m;
+      double ei = e[i * st], di1 = d[m * st];
+      di = d[i * st];
+      bool early = false;
+      for (;; --i) {
+        double ein = 0.0, din = 0.0;
+        if (i > l) {
+          ein = e[(i - 1) * st];
+          din = d[(i - 1) * st];
+        }
+        const double f = s * ei, b = c * ei;
+        const double q = fma(f, f, g * g);
+        if (q == 0.0) {
+          e[(i + 1) * st] = 0.0;
+          d[(i + 1) * st] = di1 - p;
+          e[m * st] = 0.0;
+          early = true;
+          break;
+        }
+        double ri;
+        if constexpr (RSQ) {
+          ri = rsqrt(q);
+          r = q * ri;
+        } else {
+          r = sqrt(q);
+          ri = 1.0 / r;
+        }
+        const double en = r;
+        e[(i + 1) * st] = en;
+        s = f * ri;
+        c = g * ri;
+        g = di1 - p;
+        r = (di - g) * s + 2.0 * c * b;
+        p = s * r;
+        const double dn = g + p;
+        d[(i + 1) * st] = dn;
+        g = c * r - b;
+        if (i + 1 < m && negl(dn, dprev, en)) mlo = i + 1;
+        dprev = dn;
+        if (i == l) break;
+        ei = ein;
+        di1 = di;
+        di = din;
+      }
+      if (early) {  // tql's r == 0 branch: rescan from l
+        m = scan(l);
+        continue;
+      }
+      const double dl = di - p;  // i == l: di = d[l]
+      d[l * st] = dl;
+      e[l * st] = g;
+      e[m * st] = 0.0;
+      if (negl(dl, dprev, g)) {
+        mnext = mlo;  // first negligible position >= l + 1
+        m = l;
+      } else {
+        m = mlo;
+      }
+    }
+    if (mnext >= 0) m = mnext;
+  }
+  for (int j = 0; j < k; ++j) d[j * st] *= usc;
+  return ok;
+}
+
 template <int KP, bool RSQ = false>
 __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
@@ -488,7 +603,7 @@ __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslo
     d[i * QL_T] = H.d()[i];
     e[i * QL_T] = H.e()[i];
   }
-  const bool ok = tql<RSQ>(k, d, e, QL_T, [](int, double, double) {});
+  const bool ok = g_ql_fused ? tql_vals<RSQ>(k, d, e, QL_T) : tql<RSQ>(k, d, e, QL_T, [](int, double, double) {});
   // the side of 0 with fewer eigenvectors: P_+ = sum_{l>0} l v v^T (side 0) or
   // A + sum_{l<0} |l| v v^T (side 1); selected eigenvalues sorted ascending,
   // clusters (gap <= 1e-3 ||T||, LAPACK dstein's ORTOL) and distinct shifts
@@ -1056,6 +1171,9 @@ void psd_trd_init_attributes() {
   g_trd_reg = (ev && ev[0] == '0') ? 0 : 1;
   const char* eq = std::getenv("SDP_TRD_QLRSQ");
   g_ql_rsqrt = (eq && eq[0] == '0') ? 0 : 1;
+  const char* eqf = std::getenv("SDP_TRD_QLFUSED");
+  const int qf = (eqf && eqf[0] == '0') ? 0 : 1;
+  cudaMemcpyToSymbol(g_ql_fused, &qf, sizeof(int));
   set_attrs<32, PM_BATCH>();
   set_attrs<32, PM_PRIMAL>();
   set_attrs<32, PM_DUAL>();
