@@ -247,7 +247,7 @@ struct TierFork {
 struct BucketSet {
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
-  TrdDev td[2];
+  TrdDev td[kTrdTiers];
 };
 struct Pipe {
   bool on = false;
@@ -330,7 +330,7 @@ struct sdp_handle_s {
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
   GiantDev gd;
-  TrdDev td[2];  // B_TRD32, B_TRD64
+  TrdDev td[kTrdTiers];  // B_TRD16, B_TRD32, B_TRD64
   TierFork tiers;
   Pipe pipe;
   // A
@@ -395,7 +395,7 @@ struct sdp_psd_plan_s {
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
   GiantDev gd;
-  TrdDev td[2];
+  TrdDev td[kTrdTiers];
   TierFork tiers;
   unsigned long long* capped = nullptr;
   unsigned long long* sweeps = nullptr;
@@ -661,7 +661,7 @@ void build_trd(Alloc& al, const std::vector<int32_t>& ksz, const std::vector<int
 }
 
 void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_NUM], int bcount[B_NUM],
-                   GiantDev& gd, TrdDev td[2], std::vector<int>* bucket_out = nullptr) {
+                   GiantDev& gd, TrdDev td[kTrdTiers], std::vector<int>* bucket_out = nullptr) {
   std::vector<std::vector<int32_t>> lists(B_NUM);
   int64_t in_range[6] = {0, 0, 0, 0, 0, 0};
   for (size_t i = 0; i < ksz.size(); ++i) in_range[size_range(ksz[i])]++;
@@ -675,15 +675,14 @@ void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_
     d_ids[b] = bcount[b] ? al.upload(lists[b]) : nullptr;
   }
   build_giant(al, ksz, lists[B_GLOBAL], gd);
-  build_trd(al, ksz, lists[B_TRD32], 32, td[0]);
-  build_trd(al, ksz, lists[B_TRD64], 64, td[1]);
+  for (int t = 0; t < kTrdTiers; ++t) build_trd(al, ksz, lists[B_TRD16 + t], trd_kp(B_TRD16 + t), td[t]);
 }
 
 // The tiers are independent: the giant tier (a chain of kernels whose tail leaves most SMs idle)
 // runs on the calling stream, every other tier on a side stream of its own (round-robin over
 // TierFork::nside), so the low-occupancy kernels of one tier (QL, inverse iteration) overlap the
 // others; captured into the iteration graph as parallel branches.
-void launch_tiers(ProjArgs a, int mode, int32_t* const d_ids[B_NUM], const int bcount[B_NUM], const TrdDev td[2],
+void launch_tiers(ProjArgs a, int mode, int32_t* const d_ids[B_NUM], const int bcount[B_NUM], const TrdDev td[kTrdTiers],
                   const TierFork& tf, cudaStream_t s) {
   int tiers[B_NUM], nt = 0;
   for (int b = B_NUM - 1; b >= 0; --b)  // larger first
@@ -719,7 +718,7 @@ void launch_tiers(ProjArgs a, int mode, int32_t* const d_ids[B_NUM], const int b
     }
     a.ids = d_ids[b];
     a.count = bcount[b];
-    if (is_trd(b)) a.td = td[b - B_TRD32];
+    if (is_trd(b)) a.td = td[b - B_TRD16];
     launch_projection(b, mode, a, so);
   }
   for (int k = 0; k < TierFork::kMaxSide; ++k)
@@ -1018,8 +1017,7 @@ void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vect
     }
     std::vector<int32_t> ksz(p);
     SDP_CUDA_TRY(cudaMemcpy(ksz.data(), h->d_ksz, p * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    build_trd(al, ksz, lists[B_TRD32], 32, B.td[0]);
-    build_trd(al, ksz, lists[B_TRD64], 64, B.td[1]);
+    for (int t = 0; t < kTrdTiers; ++t) build_trd(al, ksz, lists[B_TRD16 + t], trd_kp(B_TRD16 + t), B.td[t]);
   }
   int lo = 0, hi = 0;
   SDP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1283,7 +1281,7 @@ int pipe_launches_per_iter(sdp_handle h) {
     for (int b = 0; b < B_NUM; ++b) {
       if (!P.half[hf].bcount[b]) continue;
       if (is_trd(b)) {
-        const TrdDev& t = P.half[hf].td[b - B_TRD32];
+        const TrdDev& t = P.half[hf].td[b - B_TRD16];
         n += 4 * ((t.count + t.chunk - 1) / t.chunk);
       } else {
         n += 1;
@@ -1347,7 +1345,7 @@ int launches_per_iter(sdp_handle h) {
   for (int b = 0; b < B_NUM; ++b) {  // one launch per non-empty tier; 3 per chunk for the QL tiers
     if (!h->bcount[b]) continue;
     if (is_trd(b)) {
-      const TrdDev& t = h->td[b - B_TRD32];
+      const TrdDev& t = h->td[b - B_TRD16];
       n += 4 * ((t.count + t.chunk - 1) / t.chunk);
     } else {
       n += 1;
@@ -3027,7 +3025,7 @@ int32_t sdp_psd_plan_launches(sdp_psd_plan pl) {
   for (int b = 0; b < B_NUM; ++b) {
     if (!pl->bcount[b]) continue;
     if (is_trd(b)) {
-      const TrdDev& t = pl->td[b - B_TRD32];
+      const TrdDev& t = pl->td[b - B_TRD16];
       n += 4 * ((t.count + t.chunk - 1) / t.chunk);
     } else {
       n += 1;

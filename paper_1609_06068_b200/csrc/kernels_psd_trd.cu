@@ -87,19 +87,34 @@ struct HView {
 };
 
 // A group of G = KP threads (one matrix row each); G = 64 spans two warps and
-// synchronises on a named barrier.  Sums are fixed-order (deterministic).
+// synchronises on a named barrier, G = 16 is half a warp (its own lane mask: the two halves run
+// independent matrices).  Sums are fixed-order (deterministic).
 template <int G>
 struct Grp {
   int tid;
   int bar;      // named barrier id (G > 32)
   double* red;  // 2 doubles of scratch (G > 32)
+  __device__ __forceinline__ unsigned mask() const {
+    if constexpr (G >= 32)
+      return 0xffffffffu;
+    else
+      return ((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1));
+  }
   __device__ __forceinline__ void sync() const {
-    if constexpr (G <= 32)
+    if constexpr (G < 32)
+      __syncwarp(mask());
+    else if constexpr (G == 32)
       __syncwarp();
     else
       asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(G) : "memory");
   }
   __device__ __forceinline__ double sum(double v) const {
+    if constexpr (G < 32) {
+      const unsigned m = mask();
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(m, v, o);
+      return v;
+    }
     v = warp_sum(v);
     if constexpr (G > 32) {
       sync();
@@ -251,7 +266,9 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
     const bool below = i >= j + 2 && i < k;
     if (i == j) H.d()[j] = xi;  // row j is final: d_j = A(j, j)
     double alpha;
-    if constexpr (G <= 32) {
+    if constexpr (G < 32) {
+      alpha = __shfl_sync(g.mask(), xi, j + 1, G);
+    } else if constexpr (G == 32) {
       alpha = __shfl_sync(0xffffffffu, xi, (j + 1) & 31);
     } else {
       xs[i] = xi;  // published by the barriers inside g.sum
@@ -324,7 +341,7 @@ __device__ __forceinline__ void reg_blocks(double (&A)[KP], int i, int k, const 
 }
 
 template <int KP, int MODE>
-__global__ void __launch_bounds__(128, 3) k_trd_tridiag_reg(ProjArgs a, int slot0, int nslots) {
+__global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = RegLayout<KP>;
   extern __shared__ double smem[];
@@ -701,7 +718,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
     d[i] = H.d()[i];
     e[i] = H.e()[i];
   }
-  __syncwarp(Lay::HALF == 32 ? 0xffffffffu : (0xffffu << (16 * ((t / Lay::HALF) & 1))));
+  __syncwarp(Lay::HALF == 32 ? 0xffffffffu : (((1u << Lay::HALF) - 1u) << (Lay::HALF * ((t / Lay::HALF) % (32 / Lay::HALF)))));
   if (j0 >= nsel || (int)H.clst()[j0] != j0) return;
   const double tnorm = H.hdr()[2];
   const double tol = 2.220446049250313e-16 * fmax(tnorm, 1e-300);
@@ -887,11 +904,12 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
 // the Y / T block is shared (2 CTA barriers per block instead of 3 per reflector).
 template <int KP>
 struct ApplyLayout {
+  static constexpr int AT = KP < 32 ? 32 : KP;  // threads (a full warp for the DMMA fragments)
   static constexpr int LD = KP / 2 + 4;
   static constexpr int YLD = 12;  // Y block row stride (8 reflectors + pad)
-  static constexpr int NW = KP / 32;
+  static constexpr int NW = AT / 32;
   static constexpr size_t bytes() {
-    return (size_t)(KP * LD + KP * YLD + 128 + NW * 128 + KP + 12) * sizeof(double);
+    return (size_t)(KP * LD + AT * YLD + 128 + NW * 128 + KP + 12) * sizeof(double);
   }
 };
 
@@ -902,22 +920,22 @@ __device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
 }
 
 template <int KP, int MODE>
-__global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nslots) {
+__global__ void __launch_bounds__(ApplyLayout<KP>::AT) k_trd_apply(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = ApplyLayout<KP>;
   constexpr int LD = Lay::LD;
   extern __shared__ double smem[];
   const int sl = blockIdx.x;
   if (sl >= nslots) return;
-  constexpr int YLD = Lay::YLD, NW = Lay::NW;
+  constexpr int YLD = Lay::YLD, NW = Lay::NW, AT = Lay::AT;
   double* Z = smem;  // selected eigenvectors (columns), then back-transformed
   double* Ys = Z + KP * LD;     // Y block [row][8]
-  double* Gs = Ys + KP * YLD;   // Y^T Y (8 x 8)
+  double* Gs = Ys + AT * YLD;   // Y^T Y (8 x 8)
   double* Ts = Gs + 64;         // T (8 x 8, upper)
   double* Wsm = Ts + 64;        // per warp: W = Y^T Z tile, then T W
   double* lw = Wsm + NW * 128;
   double* red = lw + KP;
-  Grp<KP> g{(int)threadIdx.x, 1, red};
+  Grp<AT> g{(int)threadIdx.x, 1, red};
   const int tid = g.tid;
   const int slot = slot0 + sl;
   const int task = a.ids[slot];
@@ -927,11 +945,11 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
   int nsel = (int)H.hdr()[0];
   int side = (int)H.hdr()[1];
   const bool fallback = a.td.rcount[slot] < 0 || a.td.force_fallback;
-  for (int e = tid; e < KP * LD; e += KP) Z[e] = 0.0;  // rows >= k, columns >= nsel stay 0 (DMMA tiles)
+  for (int e = tid; e < KP * LD; e += AT) Z[e] = 0.0;  // rows >= k, columns >= nsel stay 0 (DMMA tiles)
   g.sync();
   if (!fallback) {
     const double* Zo = a.td.zbuf + a.td.zoff[slot];  // [i][j], row length KP/2
-    for (int e = tid; e < k * (KP / 2); e += KP) {
+    for (int e = tid; e < k * (KP / 2); e += AT) {
       const int i = e / (KP / 2), j = e - i * (KP / 2);
       if (j < nsel) Z[i * LD + j] = Zo[e];
     }
@@ -944,7 +962,8 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     const int row = tid;
     double* Zg = a.td.zbuf + a.td.zoff[slot];
     double* Zr = Zg + (size_t)row * KP;
-    for (int j = 0; j < KP; ++j) Zr[j] = (j == row) ? 1.0 : 0.0;
+    if (row < KP)
+      for (int j = 0; j < KP; ++j) Zr[j] = (j == row) ? 1.0 : 0.0;
     double dl[KP], el[KP];
     for (int i = 0; i < k; ++i) {
       dl[i] = H.d()[i];
@@ -1077,7 +1096,7 @@ __global__ void __launch_bounds__(KP) k_trd_apply(ProjArgs a, int slot0, int nsl
     const int r4 = lane >> 2, c4 = lane & 3;
     const int nt = (k + 7) / 8;
     const int ntile = nt * (nt + 1) / 2;
-    for (int tl = warp; tl < ntile; tl += KP / 32) {
+    for (int tl = warp; tl < ntile; tl += NW) {
       int rt, ct;
       packed_rc(tl, rt, ct);
       double acc[2] = {0.0, 0.0};
@@ -1140,7 +1159,7 @@ void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
   else
     k_trd_ql<KP><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
   k_trd_invit<KP><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
-  k_trd_apply<KP, MODE><<<n, KP, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
+  k_trd_apply<KP, MODE><<<n, ApplyLayout<KP>::AT, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
 }
 
 template <int KP, int MODE>
@@ -1174,6 +1193,9 @@ void psd_trd_init_attributes() {
   const char* eqf = std::getenv("SDP_TRD_QLFUSED");
   const int qf = (eqf && eqf[0] == '0') ? 0 : 1;
   cudaMemcpyToSymbol(g_ql_fused, &qf, sizeof(int));
+  set_attrs<16, PM_BATCH>();
+  set_attrs<16, PM_PRIMAL>();
+  set_attrs<16, PM_DUAL>();
   set_attrs<32, PM_BATCH>();
   set_attrs<32, PM_PRIMAL>();
   set_attrs<32, PM_DUAL>();
@@ -1192,7 +1214,11 @@ void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t
   if (count <= 0) return;
   for (int c0 = 0; c0 < count; c0 += a.td.chunk) {
     const int n = std::min(a.td.chunk, count - c0);
-    if (bucket == B_TRD32) {
+    if (bucket == B_TRD16) {
+      if (mode == PM_BATCH) launch_chunk<16, PM_BATCH>(a, c0, n, s);
+      else if (mode == PM_PRIMAL) launch_chunk<16, PM_PRIMAL>(a, c0, n, s);
+      else launch_chunk<16, PM_DUAL>(a, c0, n, s);
+    } else if (bucket == B_TRD32) {
       if (mode == PM_BATCH) launch_chunk<32, PM_BATCH>(a, c0, n, s);
       else if (mode == PM_PRIMAL) launch_chunk<32, PM_PRIMAL>(a, c0, n, s);
       else launch_chunk<32, PM_DUAL>(a, c0, n, s);

@@ -697,6 +697,21 @@ def test_trd_tier_batch_many(lib, gen):
     check_batch(lib, ks, vals, tol=1e-12)
 
 
+def test_trd16_tier_batch_many(lib, gen):
+    """>= 2048 matrices of order 9..16 select the KP = 16 tridiagonal-QL tier (half-warp groups in
+    the tridiagonalization, eight selected eigenvectors per matrix, one warp per apply); random
+    orders plus the degenerate structured inputs, against the oracle."""
+    rng = np.random.default_rng(16)
+    mats = []
+    for k in (9, 12, 15, 16):
+        mats += _structured(k, rng)
+    ks = list(rng.integers(9, 17, 4400))
+    vals = [rng.standard_normal(k * (k + 1) // 2) for k in ks]
+    ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)
+    vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)
+    check_batch(lib, ks, vals, tol=1e-12)
+
+
 def test_trd_tier_admm_subprocess():
     """SDP_PSD_TIERS=trd: every clique of order 17..64 takes the QL tier inside
     the ADMM iteration (primal and dual), iterates match the oracle."""
@@ -730,13 +745,13 @@ def test_trd_tier_inline_ql_fallback_subprocess():
         "import paper_1609_06068_b200 as L\n"
         "from oracle import psd as opsd\n"
         "rng = np.random.default_rng(4)\n"
-        "ks = rng.integers(17, 65, 2200).astype(np.int32)\n"
+        "ks = rng.integers(9, 65, 3000).astype(np.int32)\n"
         "vals = np.concatenate([rng.standard_normal(k*(k+1)//2) for k in ks])\n"
         "out = L.PsdPlan(ks).project_host(vals)\n"
         "want = opsd.project_psd_packed_batch(ks, vals)\n"
         "e = np.linalg.norm(out - want) / np.linalg.norm(want)\n"
         "print(e); assert e <= 1e-12, e\n" % ROOT)
-    env = dict(os.environ, SDP_TRD_FORCE_FALLBACK="1")
+    env = dict(os.environ, SDP_TRD_FORCE_FALLBACK="1", SDP_PSD_TIERS="trd")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
 
@@ -754,8 +769,8 @@ def test_trd_tier_variants_subprocess(variant):
         "from oracle import psd as opsd\n"
         "from test_gpu_parity import _structured\n"
         "rng = np.random.default_rng(5)\n"
-        "mats = [M for k in (17, 32, 33, 64) for M in _structured(k, rng)]\n"
-        "ks = list(rng.integers(17, 65, 2200))\n"
+        "mats = [M for k in (9, 16, 17, 32, 33, 64) for M in _structured(k, rng)]\n"
+        "ks = list(rng.integers(9, 65, 3000))\n"
         "vals = [rng.standard_normal(k*(k+1)//2) for k in ks]\n"
         "ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)\n"
         "vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)\n"
@@ -763,7 +778,7 @@ def test_trd_tier_variants_subprocess(variant):
         "want = opsd.project_psd_packed_batch(ks, vals)\n"
         "e = np.linalg.norm(out - want) / np.linalg.norm(want)\n"
         "print(e); assert e <= 1e-12, e\n" % (ROOT, os.path.dirname(os.path.abspath(__file__))))
-    env = dict(os.environ, **variant)
+    env = dict(os.environ, SDP_PSD_TIERS="trd", **variant)
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
 
@@ -784,8 +799,8 @@ def test_trd_ql_fused_matches_tql_subprocess():
         "from oracle import psd as opsd\n"
         "from test_gpu_parity import _structured\n"
         "rng = np.random.default_rng(11)\n"
-        "mats = [M for k in (17, 24, 32, 33, 48, 64) for M in _structured(k, rng)]\n"
-        "ks = list(rng.integers(17, 65, 3000))\n"
+        "mats = [M for k in (9, 16, 17, 24, 32, 33, 48, 64) for M in _structured(k, rng)]\n"
+        "ks = list(rng.integers(9, 65, 3000))\n"
         "vals = [rng.standard_normal(k*(k+1)//2) for k in ks]\n"
         "ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)\n"
         "vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)\n"
