@@ -1037,11 +1037,19 @@ __global__ void __launch_bounds__(ApplyLayout<KP>::AT) k_trd_apply(ProjArgs a, i
       g.sync();
       const int kb = (j0 + 1) & ~3;  // first row (multiple of 4) where the block is nonzero
       if (warp == 0) {
-        double gacc[2] = {0.0, 0.0};  // G = Y^T Y
-        for (int k0 = kb; k0 < k; k0 += 4) {
+        double gacc[2] = {0.0, 0.0}, gacc2[2] = {0.0, 0.0};  // G = Y^T Y (two accumulator chains)
+        int k0 = kb;
+        for (; k0 + 4 < k; k0 += 8) {
+          const double y = Ys[(k0 + c4) * YLD + r4], y2 = Ys[(k0 + 4 + c4) * YLD + r4];
+          dmma8(gacc, y, y);
+          dmma8(gacc2, y2, y2);
+        }
+        if (k0 < k) {
           const double y = Ys[(k0 + c4) * YLD + r4];
           dmma8(gacc, y, y);
         }
+        gacc[0] += gacc2[0];
+        gacc[1] += gacc2[1];
         Gs[r4 * 8 + 2 * c4] = gacc[0];
         Gs[r4 * 8 + 2 * c4 + 1] = gacc[1];
         __syncwarp();
@@ -1064,8 +1072,15 @@ __global__ void __launch_bounds__(ApplyLayout<KP>::AT) k_trd_apply(ProjArgs a, i
       g.sync();
       for (int nt = warp; nt < ntile; nt += NW) {
         const int n0 = 8 * nt;
-        double w[2] = {0.0, 0.0};  // W = Y^T Z (8 reflectors x 8 columns)
-        for (int k0 = kb; k0 < k; k0 += 4) dmma8(w, Ys[(k0 + c4) * YLD + r4], Z[(k0 + c4) * LD + n0 + r4]);
+        double w[2] = {0.0, 0.0}, wb[2] = {0.0, 0.0};  // W = Y^T Z (8 reflectors x 8 columns), two chains
+        int k0 = kb;
+        for (; k0 + 4 < k; k0 += 8) {
+          dmma8(w, Ys[(k0 + c4) * YLD + r4], Z[(k0 + c4) * LD + n0 + r4]);
+          dmma8(wb, Ys[(k0 + 4 + c4) * YLD + r4], Z[(k0 + 4 + c4) * LD + n0 + r4]);
+        }
+        if (k0 < k) dmma8(w, Ys[(k0 + c4) * YLD + r4], Z[(k0 + c4) * LD + n0 + r4]);
+        w[0] += wb[0];
+        w[1] += wb[1];
         Wt[r4 * 8 + 2 * c4] = w[0];
         Wt[r4 * 8 + 2 * c4 + 1] = w[1];
         __syncwarp();
@@ -1099,6 +1114,19 @@ __global__ void __launch_bounds__(ApplyLayout<KP>::AT) k_trd_apply(ProjArgs a, i
     for (int tl = warp; tl < ntile; tl += NW) {
       int rt, ct;
       packed_rc(tl, rt, ct);
+      // the epilogue's global operands are loaded before the K loop (their latency then overlaps it)
+      double pin[2] = {0.0, 0.0}, phx[2] = {0.0, 0.0}, plam[2] = {0.0, 0.0};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * rt + r4, c = 8 * ct + 2 * c4 + h;
+        if (r > c || c >= k) continue;
+        const int64_t pe = off + (int64_t)c * (c + 1) / 2 + r;
+        if (side == 1) pin[h] = input_value<MODE>(a, pe, r, c);
+        if constexpr (MODE == PM_PRIMAL) {
+          phx[h] = __ldg(a.x + a.G[pe]);
+          plam[h] = a.lam[pe];
+        }
+      }
       double acc[2] = {0.0, 0.0};
       for (int u0 = 0; u0 < nsel; u0 += 4) {
         const int u = u0 + c4;
@@ -1115,15 +1143,15 @@ __global__ void __launch_bounds__(ApplyLayout<KP>::AT) k_trd_apply(ProjArgs a, i
         if (r > c || c >= k) continue;
         double v = acc[h];
         const int64_t pe = off + (int64_t)c * (c + 1) / 2 + r;
-        if (side == 1) v += input_value<MODE>(a, pe, r, c);
+        if (side == 1) v += pin[h];
         if constexpr (MODE == PM_BATCH) {
           a.out[pe] = v;
         } else if constexpr (MODE == PM_PRIMAL) {
           const double xkv = (r == c) ? v : v * kSqrt2;
-          const double hx = __ldg(a.x + a.G[pe]);
+          const double hx = phx[h];
           const double dd = xkv - hx;
           a.xk[pe] = xkv;
-          a.lam[pe] = a.lam[pe] + a.rho * dd;  // E:LambdakUpdate
+          a.lam[pe] = plam[h] + a.rho * dd;  // E:LambdakUpdate
           p0 += dd * dd;
           p1 += xkv * xkv;
           p2 += hx * hx;
