@@ -682,7 +682,11 @@ template <int KP>
 struct InvLayout {
   static constexpr int HALF = KP / 2;        // selected eigenvalues per matrix <= k / 2
   static constexpr int NMAT = IV_T / HALF;   // matrices per CTA
-  static constexpr size_t bytes() { return (size_t)(2 * KP * IV_T + NMAT * 2 * KP) * sizeof(double); }
+  // KP = 64: the second per-thread array (reciprocal D+ pivots / LU multipliers) lives in the
+  // slot's global scratch, so twice as many CTAs are resident (k = 64 bucket 2.04 -> 1.88 ms);
+  // smaller orders keep it in shared memory (measured faster there)
+  static constexpr bool GLOBAL2 = KP >= 64;
+  static constexpr size_t bytes() { return (size_t)((GLOBAL2 ? 1 : 2) * KP * IV_T + NMAT * 2 * KP) * sizeof(double); }
 };
 
 // 1 / x to full fp64 precision: hardware approximation + two Newton steps (no IEEE-division
@@ -712,7 +716,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   const int k = a.ksz[a.ids[slot]];
   // T (d, e) into shared memory: the recurrences below read it element by element, and the
   // workspace is far larger than L2 / L1, so global reads would each pay a DRAM round trip
-  double* d = smem + 2 * KP * IV_T + (t / Lay::HALF) * 2 * KP;
+  double* d = smem + (Lay::GLOBAL2 ? 1 : 2) * KP * IV_T + (t / Lay::HALF) * 2 * KP;
   double* e = d + KP;
   for (int i = j0; i < k; i += Lay::HALF) {
     d[i] = H.d()[i];
@@ -722,25 +726,33 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   if (j0 >= nsel || (int)H.clst()[j0] != j0) return;
   const double tnorm = H.hdr()[2];
   const double tol = 2.220446049250313e-16 * fmax(tnorm, 1e-300);
-  double* A0 = smem + t;  // per-thread arrays, element i at [i * IV_T]
-  double* A1 = A0 + KP * IV_T;
+  double* A0 = smem + t;  // per-thread array, element i at [i * IV_T]
+  double* Zo0 = a.td.zbuf + a.td.zoff[slot];
+  // the second per-thread array: shared memory [i * IV_T], or the unused half of the slot's
+  // scratch [i * ZL] (GLOBAL2)
+  double* A1 = Lay::GLOBAL2 ? Zo0 + ZL * KP + j0 : A0 + KP * IV_T;
+  constexpr int S1 = Lay::GLOBAL2 ? ZL : IV_T;
   double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [i][j], row length KP/2
   const bool single = j0 + 1 >= nsel || (int)H.clst()[j0 + 1] != j0;
   bool fail = false;
   if (single) {
     const double lam = H.lsel()[j0];
-    double* rm = A0;  // 1 / D-_i
-    double* rp = A1;  // 1 / D+_i
+    double* rm = A0;  // 1 / D-_i (shared memory)
+    double* zj = Zo + j0;  // the output column (z_i)
+    double* rp = Lay::GLOBAL2 ? zj : A0 + KP * IV_T;  // 1 / D+_i: the output column (z_i overwrites
+    constexpr int SP = Lay::GLOBAL2 ? ZL : IV_T;       // it), or shared memory
     double dm = d[k - 1] - lam;
     if (fabs(dm) < tol) dm = dm < 0.0 ? -tol : tol;
-    rm[(k - 1) * IV_T] = rcp_nr(dm);
+    double rmi = rcp_nr(dm);
+    rm[(k - 1) * IV_T] = rmi;
     for (int i = k - 2; i >= 1; --i) {
       const double ei = e[i];
-      dm = fma(-ei * ei, rm[(i + 1) * IV_T], d[i] - lam);
+      dm = fma(-ei * ei, rmi, d[i] - lam);
       if (fabs(dm) < tol) dm = dm < 0.0 ? -tol : tol;
-      rm[i * IV_T] = rcp_nr(dm);
+      rmi = rcp_nr(dm);
+      rm[i * IV_T] = rmi;
     }
-    double dp = 0.0, best = 0.0;
+    double dp = 0.0, best = 0.0, rpi = 0.0;
     int r = 0;
     for (int i = 0; i < k; ++i) {
       const double ai = d[i] - lam;
@@ -748,10 +760,11 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
         dp = ai;
       } else {
         const double em = e[i - 1];
-        dp = fma(-em * em, rp[(i - 1) * IV_T], ai);
+        dp = fma(-em * em, rpi, ai);
       }
       if (fabs(dp) < tol) dp = dp < 0.0 ? -tol : tol;
-      rp[i * IV_T] = rcp_nr(dp);
+      rpi = rcp_nr(dp);
+      rp[i * SP] = rpi;
       const double gam = i + 1 < k ? fma(-e[i] * e[i], rm[(i + 1) * IV_T], dp) : dp;
       if (i == 0 || fabs(gam) < best) {
         best = fabs(gam);
@@ -760,37 +773,44 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
     }
     // z is written unnormalised; its residual rows and its norm are formed on the way, and the
     // reconstruction weight takes the 1 / ||z||^2 (w z z^T / ||z||^2 = w v v^T)
-    double* zj = Zo + j0;
-    zj[r * ZL] = 1.0;
-    double u1 = 1.0, u2 = 0.0, w1 = 1.0, w2 = 0.0;  // z at the last two rows of each chain
-    double zr_up = 0.0, zr_dn = 0.0, nrm = 1.0, mx = 1.0, res = 0.0;
-    for (int s = 1; s < k; ++s) {  // the two product chains run side by side
-      const int iu = r + s, id = r - s;
-      if (iu < k) {
-        const double z = u1 * (-e[iu - 1] * rm[iu * IV_T]);
-        zj[iu * ZL] = z;
-        if (s >= 2) res = fmax(res, fabs(fma(e[iu - 2], u2, fma(d[iu - 1] - lam, u1, e[iu - 1] * z))));
-        else zr_up = z;
-        u2 = u1;
-        u1 = z;
-        nrm = fma(z, z, nrm);
-        mx = fmax(mx, fabs(z));
-      }
-      if (id >= 0) {
-        const double z = w1 * (-e[id] * rp[id * IV_T]);
-        zj[id * ZL] = z;
-        if (s >= 2) res = fmax(res, fabs(fma(e[id], z, fma(d[id + 1] - lam, w1, e[id + 1] * w2))));
+    double nrm = 1.0, mx = 1.0, res = 0.0, zr_up = 0.0, zr_dn = 0.0;
+    double z1 = 1.0, z2 = 0.0;  // z at the last two rows of a chain
+    for (int i = r + 1; i < k; ++i) {  // above r: z_i = -(e_{i-1} / D-_i) z_{i-1}
+      const double z = z1 * (-e[i - 1] * rm[i * IV_T]);
+      zj[i * ZL] = z;
+      if (i >= r + 2) res = fmax(res, fabs(fma(e[i - 2], z2, fma(d[i - 1] - lam, z1, e[i - 1] * z))));
+      else zr_up = z;
+      z2 = z1;
+      z1 = z;
+      nrm = fma(z, z, nrm);
+      mx = fmax(mx, fabs(z));
+    }
+    if (r + 1 < k) res = fmax(res, fabs(fma(e[k - 2], z2, (d[k - 1] - lam) * z1)));  // row k - 1
+    z1 = 1.0;
+    z2 = 0.0;
+    // below r: z_i = -(e_i / D+_i) z_{i+1}, the reciprocal pivots read back from the column eight
+    // at a time (the loads of a block are independent of the chain)
+    for (int i0 = r - 1; i0 >= 0; i0 -= 8) {
+      double rpb[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) rpb[q] = i0 - q >= 0 ? rp[(i0 - q) * SP] : 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = i0 - q;
+        if (i < 0) break;
+        const double z = z1 * (-e[i] * rpb[q]);
+        zj[i * ZL] = z;
+        if (i <= r - 2) res = fmax(res, fabs(fma(e[i], z, fma(d[i + 1] - lam, z1, e[i + 1] * z2))));
         else zr_dn = z;
-        w2 = w1;
-        w1 = z;
+        z2 = z1;
+        z1 = z;
         nrm = fma(z, z, nrm);
         mx = fmax(mx, fabs(z));
       }
     }
-    // rows r, k - 1 (above r) and 0 (below r)
+    if (r >= 1) res = fmax(res, fabs(fma(e[0], z2, (d[0] - lam) * z1)));  // row 0
+    zj[r * ZL] = 1.0;
     res = fmax(res, fabs((d[r] - lam) + (r >= 1 ? e[r - 1] * zr_dn : 0.0) + (r + 1 < k ? e[r] * zr_up : 0.0)));
-    if (r + 1 < k) res = fmax(res, fabs(fma(e[k - 2], u2, (d[k - 1] - lam) * u1)));
-    if (r >= 1) res = fmax(res, fabs(fma(e[0], w2, (d[0] - lam) * w1)));
     if (!(res <= 1e-9 * fmax(tnorm, 1e-300) * mx) || !(nrm < 1e300)) fail = true;  // NaN / Inf too
     else H.lw()[j0] /= nrm;
   } else {
@@ -821,7 +841,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
         }
         if (fabs(p1) < tol) p1 = p1 < 0.0 ? -tol : tol;
         ui[i * IV_T] = 1.0 / p1;
-        mu[i * IV_T] = m;
+        mu[i * S1] = m;
       }
       if (fabs(r0) < tol) r0 = r0 < 0.0 ? -tol : tol;
       ui[(k - 1) * IV_T] = 1.0 / r0;
@@ -837,7 +857,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
         double ry = x[0];
         for (int i = 0; i + 1 < k; ++i) {
           const double yn = x[(i + 1) * ZL];
-          const double m = mu[i * IV_T];
+          const double m = mu[i * S1];
           if ((pv >> i) & 1ull) {
             x[i * ZL] = yn;
             ry = fma(-m, yn, ry);
@@ -853,7 +873,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
           const bool piv = (pv >> i) & 1ull;
           const double u3 = piv ? e[i + 1] : 0.0;  // i + 2 < k here
           const double u2 = piv ? d[i + 1] - lam
-                                : (i == 0 ? e[0] : (((pv >> (i - 1)) & 1ull) ? -mu[(i - 1) * IV_T] * e[i] : e[i]));
+                                : (i == 0 ? e[0] : (((pv >> (i - 1)) & 1ull) ? -mu[(i - 1) * S1] * e[i] : e[i]));
           const double xi = (x[i * ZL] - u2 * xn - u3 * xn1) * ui[i * IV_T];
           x[i * ZL] = xi;
           mx = fmax(mx, fabs(xi));
