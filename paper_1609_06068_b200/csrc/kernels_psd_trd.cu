@@ -116,13 +116,26 @@ struct Grp {
       return v;
     }
     v = warp_sum(v);
-    if constexpr (G > 32) {
+    if constexpr (G > 32) {  // (the leading barrier: red may still be read by the previous sum)
       sync();
       if ((tid & 31) == 0) red[tid >> 5] = v;
       sync();
       v = red[0] + red[1];
     }
     return v;
+  }
+  // sum() for call sites that alternate between two scratch slots (red[0..1], red[2..3]): a slot
+  // is rewritten only after the other slot's sum and the caller's barriers in between, so the
+  // leading WAR barrier is not needed (G = 64: 2 of the 6 barriers per tridiagonalization step)
+  __device__ __forceinline__ double sum_slot(double v, int slot) const {
+    if constexpr (G <= 32) {
+      return sum(v);
+    } else {
+      v = warp_sum(v);
+      if ((tid & 31) == 0) red[2 * slot + (tid >> 5)] = v;
+      sync();
+      return red[2 * slot] + red[2 * slot + 1];
+    }
   }
 };
 
@@ -273,7 +286,7 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
     } else {
       xs[i] = xi;  // published by the barriers inside g.sum
     }
-    const double sig = g.sum(below ? xi * xi : 0.0);
+    const double sig = g.sum_slot(below ? xi * xi : 0.0, 0);
     if constexpr (G > 32) alpha = xs[j + 1];
     double tau = 0.0, beta = alpha, scl = 0.0;
     if (sig > 0.0) {
@@ -305,7 +318,7 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
         a3 = fma(A[l + 3], v23.y, a3);
       }
       const double pi = tau * ((a0 + a1) + (a2 + a3));
-      const double K = 0.5 * tau * g.sum(pi * vi);
+      const double K = 0.5 * tau * g.sum_slot(pi * vi, 1);
       const double wi = in ? pi - K * vi : 0.0;
       ws[i] = wi;
       g.sync();
