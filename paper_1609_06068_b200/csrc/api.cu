@@ -1282,7 +1282,7 @@ int pipe_launches_per_iter(sdp_handle h) {
       if (!P.half[hf].bcount[b]) continue;
       if (is_trd(b)) {
         const TrdDev& t = P.half[hf].td[b - B_TRD16];
-        n += 4 * ((t.count + t.chunk - 1) / t.chunk);
+        n += trd_launches_per_chunk(b) * ((t.count + t.chunk - 1) / t.chunk);
       } else {
         n += 1;
       }
@@ -1342,11 +1342,11 @@ int launches_per_iter(sdp_handle h) {
   if (h->fused) return 1;  // one launch per sdp_step call (any number of iterations)
   if (h->pipe.on) return pipe_launches_per_iter(h);
   int n = 0;
-  for (int b = 0; b < B_NUM; ++b) {  // one launch per non-empty tier; 3 per chunk for the QL tiers
+  for (int b = 0; b < B_NUM; ++b) {  // one launch per non-empty tier; 4-5 per chunk for the QL tiers
     if (!h->bcount[b]) continue;
     if (is_trd(b)) {
       const TrdDev& t = h->td[b - B_TRD16];
-      n += 4 * ((t.count + t.chunk - 1) / t.chunk);
+      n += trd_launches_per_chunk(b) * ((t.count + t.chunk - 1) / t.chunk);
     } else {
       n += 1;
     }
@@ -3026,7 +3026,7 @@ int32_t sdp_psd_plan_launches(sdp_psd_plan pl) {
     if (!pl->bcount[b]) continue;
     if (is_trd(b)) {
       const TrdDev& t = pl->td[b - B_TRD16];
-      n += 4 * ((t.count + t.chunk - 1) / t.chunk);
+      n += trd_launches_per_chunk(b) * ((t.count + t.chunk - 1) / t.chunk);
     } else {
       n += 1;
     }

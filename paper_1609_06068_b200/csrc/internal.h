@@ -237,6 +237,7 @@ int64_t gtrd_ws_doubles(int k);  // workspace of one matrix of order k
 void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t s);
 void launch_projection_wj(int mode, const ProjArgs& a, cudaStream_t s);
 int64_t trd_hsize(int kp, int k);  // doubles of per-slot Householder workspace
+int trd_launches_per_chunk(int bucket);  // kernels per chunk of a QL tier (5 for the split k = 64 form)
 int giant_grid();        // CTAs of the persistent giant kernel on the current device
 int giant_min_order();   // smallest order routed to the giant tier (SDP_GIANT_MIN, default 65)
 int rv_kp(int bucket);

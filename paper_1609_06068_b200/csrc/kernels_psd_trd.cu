@@ -121,6 +121,8 @@ struct Grp {
       if ((tid & 31) == 0) red[tid >> 5] = v;
       sync();
       v = red[0] + red[1];
+#pragma unroll
+      for (int w = 2; w < G / 32; ++w) v += red[w];  // (fixed order)
     }
     return v;
   }
@@ -131,6 +133,7 @@ struct Grp {
     if constexpr (G <= 32) {
       return sum(v);
     } else {
+      static_assert(G == 64, "two warps per group");
       v = warp_sum(v);
       if ((tid & 31) == 0) red[2 * slot + (tid >> 5)] = v;
       sync();
@@ -264,9 +267,11 @@ struct RegLayout {
   static constexpr int PER = ((TRI + 1) & ~1) + 3 * KP + 4;  // staging (packed), xs, vs, ws, red
 };
 
-template <int KP, int JB, int G>
+// (HKP, JO: the slot layout and the index of local step 0 in it -- the trailing-block kernel of the
+// split k = 64 reduction runs KP = 32 registers on a KP = 64 slot from step 32)
+template <int KP, int JB, int G, int HKP = KP, int JO = 0>
 __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const Grp<G>& g, double* xs, double* vs,
-                                          double* ws, const HView<KP>& H, int64_t& vpos) {
+                                          double* ws, const HView<HKP>& H, int64_t& vpos) {
   constexpr int L0 = 8 * JB;
   constexpr int UNR = KP <= 32 ? 8 : 1;  // KP = 32: steps unrolled too (all register indices static)
 #pragma unroll UNR
@@ -277,7 +282,7 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
     for (int s = 1; s < 8; ++s)
       if (j == L0 + s) xi = A[L0 + s];
     const bool below = i >= j + 2 && i < k;
-    if (i == j) H.d()[j] = xi;  // row j is final: d_j = A(j, j)
+    if (i == j) H.d()[JO + j] = xi;  // row j is final: d_j = A(j, j)
     double alpha;
     if constexpr (G < 32) {
       alpha = __shfl_sync(g.mask(), xi, j + 1, G);
@@ -300,8 +305,8 @@ __device__ __forceinline__ void reg_block(double (&A)[KP], int i, int k, const G
     vs[i] = vi;
     if (below) H.v()[vpos + (i - j - 2)] = vi;
     if (i == KP - 1) {  // (row KP-1 takes part in every block)
-      H.e()[j] = beta;
-      H.tau()[j] = tau;
+      H.e()[JO + j] = beta;
+      H.tau()[JO + j] = tau;
     }
     vpos += k - j - 2;
     g.sync();  // vs visible; every thread has read alpha
@@ -353,7 +358,24 @@ __device__ __forceinline__ void reg_blocks(double (&A)[KP], int i, int k, const 
   (reg_block_any<KP, JB>(A, i, k, g, xs, vs, ws, H, vpos), ...);
 }
 
-template <int KP, int MODE>
+// Split k = 64 reduction (SDP_TRD_SPLIT, default on).  Steps j >= 32 of the one-kernel form run on
+// the second warp alone while the first waits with its registers held, so half of the SM's
+// tridiagonalization warps idle for a third of the kernel.  Here phase 1 (PH = 1: steps 0..31,
+// both warps) stores the trailing block A(32:k, 32:k) column-major into the slot's eigenvector
+// scratch (free until the eigenvector kernel) and exits; the trailing-block kernel (PH = 2: KP = 32
+// registers, one warp per matrix, four matrices per CTA) reduces it, writing d, e, tau and the
+// Householder vectors at their places in the KP = 64 slot (the vectors of steps >= 32 follow those
+// of steps < 32 in the packed order, and their entries are relative to the step, so only the step
+// index is offset).  Orders k <= 34 finish in phase 1.
+template <int... JB>
+__device__ __forceinline__ void reg_blocks_tail(double (&A)[32], int i, int k, const Grp<32>& g, double* xs,
+                                                double* vs, double* ws, const HView<64>& H, int64_t vpos,
+                                                std::integer_sequence<int, JB...>) {
+  (reg_block<32, JB, 32, 64, 32>(A, i, k, g, xs, vs, ws, H, vpos), ...);
+}
+static int g_trd_split = 1;
+
+template <int KP, int MODE, int PH = 0>
 __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = RegLayout<KP>;
@@ -369,6 +391,32 @@ __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjA
   const int i = g.tid;
   const int slot = slot0 + sl;
   const int task = a.ids[slot];
+  if constexpr (PH == 2) {  // trailing block of a split k = 64 reduction (KP = 32 registers)
+    static_assert(KP == 32, "trailing block of a KP = 64 slot");
+    const int kf = a.ksz[task];
+    if (kf <= 34) return;  // finished in phase 1 (whole warps leave together)
+    const int k = kf - 32;
+    const HView<64> H{a.td.hbuf + a.td.hoff[slot]};
+    const double* zb = a.td.zbuf + a.td.zoff[slot];
+    double A[32];
+#pragma unroll
+    for (int l = 0; l < 32; ++l) A[l] = (i < k && l < k) ? zb[l * 32 + i] : 0.0;
+    reg_blocks_tail(A, i, k, g, xs, vs, ws, H, (int64_t)32 * (kf - 2) - 496, std::make_integer_sequence<int, 4>{});
+    g.sync();
+    if (i == k - 1 || i == k - 2) {
+      double* row = st + (i == k - 1 ? 32 : 0);
+#pragma unroll
+      for (int l = 0; l < 32; ++l) row[l] = A[l];
+    }
+    g.sync();
+    if (i == 0) {
+      H.d()[32 + k - 2] = st[k - 2];
+      H.d()[32 + k - 1] = st[32 + k - 1];
+      H.e()[32 + k - 2] = st[32 + k - 2];
+      H.e()[32 + k - 1] = 0.0;
+    }
+    return;
+  } else {
   const int k = a.ksz[task];
   const int64_t off = a.off[task];
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
@@ -382,7 +430,20 @@ __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjA
   double A[KP];
 #pragma unroll
   for (int l = 0; l < KP; ++l) A[l] = (i < k && l < k) ? st[l >= i ? tri(l) + i : tri(i) + l] : 0.0;
-  reg_blocks<KP>(A, i, k, g, xs, vs, ws, H, std::make_integer_sequence<int, KP / 8>{});
+  if constexpr (PH == 1) {
+    static_assert(KP == 64, "phase 1 of the split k = 64 reduction");
+    reg_blocks<KP>(A, i, k, g, xs, vs, ws, H, std::make_integer_sequence<int, 4>{});
+    if (k > 34) {  // steps 32.. remain: the trailing block, column-major, for the KP = 32 kernel
+      if (i >= 32) {
+        double* zb = a.td.zbuf + a.td.zoff[slot];
+#pragma unroll
+        for (int l = 32; l < 64; ++l) zb[(l - 32) * 32 + (i - 32)] = A[l];
+      }
+      return;
+    }
+  } else {
+    reg_blocks<KP>(A, i, k, g, xs, vs, ws, H, std::make_integer_sequence<int, KP / 8>{});
+  }
   // d_j (j < k - 2) was stored at step j; the last 2 x 2 block of T from rows k-2, k-1 through the
   // (free) staging area, so that no register is indexed dynamically
   static_assert(Lay::TRI >= 2 * KP, "staging holds two rows");
@@ -406,6 +467,7 @@ __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjA
     }
   }
   if (i == 0) H.e()[k - 1] = 0.0;
+  }
 }
 
 static int g_trd_reg = 1;    // SDP_TRD_REG=0: the shared-memory tridiagonalization
@@ -937,7 +999,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
 // the Y / T block is shared (2 CTA barriers per block instead of 3 per reflector).
 template <int KP>
 struct ApplyLayout {
-  static constexpr int AT = KP < 32 ? 32 : KP;  // threads (a full warp for the DMMA fragments)
+  static constexpr int AT = KP < 32 ? 32 : KP;  // threads (a full warp for the DMMA fragments; 2 KP measured: no gain)
   static constexpr int LD = KP / 2 + 4;
   static constexpr int YLD = 12;  // Y block row stride (8 reflectors + pad)
   static constexpr int NW = AT / 32;
@@ -1211,7 +1273,18 @@ void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
   using TL = TridiagLayout<KP>;
   using IL = InvLayout<KP>;
   using RL = RegLayout<KP>;
-  if (g_trd_reg)
+  bool split = false;
+  if constexpr (KP == 64) {
+    if (g_trd_reg && g_trd_split) {
+      using RL32 = RegLayout<32>;
+      k_trd_tridiag_reg<KP, MODE, 1><<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
+      k_trd_tridiag_reg<32, PM_BATCH, 2>
+          <<<(n + RL32::NMAT - 1) / RL32::NMAT, 128, RL32::NMAT * RL32::PER * sizeof(double), s>>>(a, c0, n);
+      split = true;
+    }
+  }
+  if (split) {
+  } else if (g_trd_reg)
     k_trd_tridiag_reg<KP, MODE><<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
   else
     k_trd_tridiag<KP, MODE><<<(n + TL::NMAT - 1) / TL::NMAT, 128, TL::NMAT * TL::PER * sizeof(double), s>>>(a, c0, n);
@@ -1229,6 +1302,12 @@ void set_attrs() {
   cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
+  if constexpr (KP == 64) {
+    cudaFuncSetAttribute(k_trd_tridiag_reg<64, MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(RegLayout<64>::NMAT * RegLayout<64>::PER * sizeof(double)));
+    cudaFuncSetAttribute(k_trd_tridiag_reg<32, PM_BATCH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(RegLayout<32>::NMAT * RegLayout<32>::PER * sizeof(double)));
+  }
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1251,6 +1330,8 @@ void psd_trd_init_attributes() {
   g_trd_reg = (ev && ev[0] == '0') ? 0 : 1;
   const char* eq = std::getenv("SDP_TRD_QLRSQ");
   g_ql_rsqrt = (eq && eq[0] == '0') ? 0 : 1;
+  const char* esp = std::getenv("SDP_TRD_SPLIT");
+  g_trd_split = (esp && esp[0] == '0') ? 0 : 1;
   const char* eqf = std::getenv("SDP_TRD_QLFUSED");
   const int qf = (eqf && eqf[0] == '0') ? 0 : 1;
   cudaMemcpyToSymbol(g_ql_fused, &qf, sizeof(int));
@@ -1264,6 +1345,8 @@ void psd_trd_init_attributes() {
   set_attrs<64, PM_PRIMAL>();
   set_attrs<64, PM_DUAL>();
 }
+
+int trd_launches_per_chunk(int bucket) { return (bucket == B_TRD64 && g_trd_reg && g_trd_split) ? 5 : 4; }
 
 int64_t trd_hsize(int kp, int k) {
   const int64_t v = k >= 2 ? (int64_t)(k - 1) * (k - 2) / 2 : 0;

@@ -756,7 +756,7 @@ def test_trd_tier_inline_ql_fallback_subprocess():
     assert r.returncode == 0, r.stdout + r.stderr
 
 
-@pytest.mark.parametrize("variant", [{"SDP_TRD_REG": "0"}, {"SDP_TRD_QLRSQ": "0"}])
+@pytest.mark.parametrize("variant", [{"SDP_TRD_REG": "0"}, {"SDP_TRD_QLRSQ": "0"}, {"SDP_TRD_SPLIT": "0"}])
 def test_trd_tier_variants_subprocess(variant):
     """The A/B variants of the QL tier kept for measurement (shared-memory
     tridiagonalization; sqrt + reciprocal QL rotations) stay correct: random orders
