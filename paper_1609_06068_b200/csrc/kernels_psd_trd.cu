@@ -351,31 +351,31 @@ __device__ __forceinline__ void reg_block_any(double (&A)[KP], int i, int k, con
   }
 }
 
-template <int KP, int... JB>
+template <int KP, int HKP, int JO, int... JB>
 __device__ __forceinline__ void reg_blocks(double (&A)[KP], int i, int k, const Grp<KP>& g, double* xs, double* vs,
-                                           double* ws, const HView<KP>& H, std::integer_sequence<int, JB...>) {
-  int64_t vpos = 0;
-  (reg_block_any<KP, JB>(A, i, k, g, xs, vs, ws, H, vpos), ...);
+                                           double* ws, const HView<HKP>& H, int64_t vpos,
+                                           std::integer_sequence<int, JB...>) {
+  if constexpr (HKP == KP && JO == 0)
+    (reg_block_any<KP, JB>(A, i, k, g, xs, vs, ws, H, vpos), ...);
+  else
+    (reg_block<KP, JB, KP, HKP, JO>(A, i, k, g, xs, vs, ws, H, vpos), ...);
 }
 
-// Split k = 64 reduction (SDP_TRD_SPLIT, default on).  Steps j >= 32 of the one-kernel form run on
-// the second warp alone while the first waits with its registers held, so half of the SM's
-// tridiagonalization warps idle for a third of the kernel.  Here phase 1 (PH = 1: steps 0..31,
-// both warps) stores the trailing block A(32:k, 32:k) column-major into the slot's eigenvector
-// scratch (free until the eigenvector kernel) and exits; the trailing-block kernel (PH = 2: KP = 32
-// registers, one warp per matrix, four matrices per CTA) reduces it, writing d, e, tau and the
-// Householder vectors at their places in the KP = 64 slot (the vectors of steps >= 32 follow those
-// of steps < 32 in the packed order, and their entries are relative to the step, so only the step
-// index is offset).  Orders k <= 34 finish in phase 1.
-template <int... JB>
-__device__ __forceinline__ void reg_blocks_tail(double (&A)[32], int i, int k, const Grp<32>& g, double* xs,
-                                                double* vs, double* ws, const HView<64>& H, int64_t vpos,
-                                                std::integer_sequence<int, JB...>) {
-  (reg_block<32, JB, 32, 64, 32>(A, i, k, g, xs, vs, ws, H, vpos), ...);
-}
+// Split reduction (SDP_TRD_SPLIT, default on).  Once half of a group's steps are done, the rows of
+// its first half are final: in the one-kernel form their threads (KP = 64: a whole warp waiting at
+// the closing barrier; KP = 32: half of the warp's lanes) keep their registers without doing work.
+// So a stage with STOP runs steps 0 .. KP/2 - 1 of its block, stores the trailing block
+// A(KP/2:k, KP/2:k) column-major into the slot's eigenvector scratch (free until the eigenvector
+// kernel) and exits, and a stage of half the width (KP = 32: one warp per matrix; KP = 16: two
+// matrices per warp) reduces the trailing block, writing d, e, tau and the Householder vectors at
+// their places in the slot (the vectors of later steps follow the earlier ones in the packed order
+// and their entries are relative to the step, so only the step index JO is offset).
+// k = 64 bucket: 64 -> 32 -> 16 (steps 0..31, 32..47, 48..); k = 32 bucket: 32 -> 16.  A matrix whose
+// remaining order is <= 2 at a stage boundary finishes in the stage that reaches it.
 static int g_trd_split = 1;
+__host__ __device__ constexpr int split_zoff(int jo) { return jo == 48 ? 1024 : 0; }  // doubles
 
-template <int KP, int MODE, int PH = 0>
+template <int KP, int MODE, int HKP = KP, int JO = 0, bool STOP = false>
 __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = RegLayout<KP>;
@@ -391,58 +391,40 @@ __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjA
   const int i = g.tid;
   const int slot = slot0 + sl;
   const int task = a.ids[slot];
-  if constexpr (PH == 2) {  // trailing block of a split k = 64 reduction (KP = 32 registers)
-    static_assert(KP == 32, "trailing block of a KP = 64 slot");
-    const int kf = a.ksz[task];
-    if (kf <= 34) return;  // finished in phase 1 (whole warps leave together)
-    const int k = kf - 32;
-    const HView<64> H{a.td.hbuf + a.td.hoff[slot]};
-    const double* zb = a.td.zbuf + a.td.zoff[slot];
-    double A[32];
-#pragma unroll
-    for (int l = 0; l < 32; ++l) A[l] = (i < k && l < k) ? zb[l * 32 + i] : 0.0;
-    reg_blocks_tail(A, i, k, g, xs, vs, ws, H, (int64_t)32 * (kf - 2) - 496, std::make_integer_sequence<int, 4>{});
-    g.sync();
-    if (i == k - 1 || i == k - 2) {
-      double* row = st + (i == k - 1 ? 32 : 0);
-#pragma unroll
-      for (int l = 0; l < 32; ++l) row[l] = A[l];
-    }
-    g.sync();
-    if (i == 0) {
-      H.d()[32 + k - 2] = st[k - 2];
-      H.d()[32 + k - 1] = st[32 + k - 1];
-      H.e()[32 + k - 2] = st[32 + k - 2];
-      H.e()[32 + k - 1] = 0.0;
-    }
-    return;
-  } else {
-  const int k = a.ksz[task];
-  const int64_t off = a.off[task];
-  const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
-  const int ns = k * (k + 1) / 2;
-  for (int e = i; e < ns; e += KP) {
-    int r, c;
-    packed_rc(e, r, c);
-    st[e] = input_value<MODE>(a, off + e, r, c);  // (r, c), r <= c at c(c+1)/2 + r
-  }
-  g.sync();
+  const int kf = a.ksz[task];
+  if (JO > 0 && kf <= JO + 2) return;  // finished by an earlier stage (whole groups leave together)
+  const int k = kf - JO;               // order of this stage's block
+  const HView<HKP> H{a.td.hbuf + a.td.hoff[slot]};
   double A[KP];
+  if constexpr (JO == 0) {
+    const int64_t off = a.off[task];
+    const int ns = k * (k + 1) / 2;
+    for (int e = i; e < ns; e += KP) {
+      int r, c;
+      packed_rc(e, r, c);
+      st[e] = input_value<MODE>(a, off + e, r, c);  // (r, c), r <= c at c(c+1)/2 + r
+    }
+    g.sync();
 #pragma unroll
-  for (int l = 0; l < KP; ++l) A[l] = (i < k && l < k) ? st[l >= i ? tri(l) + i : tri(i) + l] : 0.0;
-  if constexpr (PH == 1) {
-    static_assert(KP == 64, "phase 1 of the split k = 64 reduction");
-    reg_blocks<KP>(A, i, k, g, xs, vs, ws, H, std::make_integer_sequence<int, 4>{});
-    if (k > 34) {  // steps 32.. remain: the trailing block, column-major, for the KP = 32 kernel
-      if (i >= 32) {
-        double* zb = a.td.zbuf + a.td.zoff[slot];
+    for (int l = 0; l < KP; ++l) A[l] = (i < k && l < k) ? st[l >= i ? tri(l) + i : tri(i) + l] : 0.0;
+  } else {
+    const double* zb = a.td.zbuf + a.td.zoff[slot] + split_zoff(JO);
 #pragma unroll
-        for (int l = 32; l < 64; ++l) zb[(l - 32) * 32 + (i - 32)] = A[l];
+    for (int l = 0; l < KP; ++l) A[l] = (i < k && l < k) ? zb[l * KP + i] : 0.0;
+  }
+  const int64_t vpos0 = (int64_t)JO * (kf - 2) - (int64_t)JO * (JO - 1) / 2;  // sum_{j < JO} (kf - j - 2)
+  if constexpr (STOP) {
+    reg_blocks<KP, HKP, JO>(A, i, k, g, xs, vs, ws, H, vpos0, std::make_integer_sequence<int, KP / 16>{});
+    if (k > KP / 2 + 2) {  // steps remain: the trailing block for the next stage
+      if (i >= KP / 2) {
+        double* zb = a.td.zbuf + a.td.zoff[slot] + split_zoff(JO + KP / 2);
+#pragma unroll
+        for (int l = KP / 2; l < KP; ++l) zb[(l - KP / 2) * (KP / 2) + (i - KP / 2)] = A[l];
       }
       return;
     }
   } else {
-    reg_blocks<KP>(A, i, k, g, xs, vs, ws, H, std::make_integer_sequence<int, KP / 8>{});
+    reg_blocks<KP, HKP, JO>(A, i, k, g, xs, vs, ws, H, vpos0, std::make_integer_sequence<int, KP / 8>{});
   }
   // d_j (j < k - 2) was stored at step j; the last 2 x 2 block of T from rows k-2, k-1 through the
   // (free) staging area, so that no register is indexed dynamically
@@ -459,14 +441,13 @@ __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjA
   g.sync();
   if (i == 0) {
     if (k >= 2) {
-      H.d()[k - 2] = st[k - 2];
-      H.d()[k - 1] = st[KP + k - 1];
-      H.e()[k - 2] = st[KP + k - 2];
+      H.d()[JO + k - 2] = st[k - 2];
+      H.d()[JO + k - 1] = st[KP + k - 1];
+      H.e()[JO + k - 2] = st[KP + k - 2];
     } else {
-      H.d()[0] = st[0];
+      H.d()[JO] = st[0];
     }
-  }
-  if (i == 0) H.e()[k - 1] = 0.0;
+    H.e()[JO + k - 1] = 0.0;
   }
 }
 
@@ -1274,12 +1255,17 @@ void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
   using IL = InvLayout<KP>;
   using RL = RegLayout<KP>;
   bool split = false;
-  if constexpr (KP == 64) {
+  if constexpr (KP >= 32) {
     if (g_trd_reg && g_trd_split) {
-      using RL32 = RegLayout<32>;
-      k_trd_tridiag_reg<KP, MODE, 1><<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
-      k_trd_tridiag_reg<32, PM_BATCH, 2>
-          <<<(n + RL32::NMAT - 1) / RL32::NMAT, 128, RL32::NMAT * RL32::PER * sizeof(double), s>>>(a, c0, n);
+      using R32 = RegLayout<32>;
+      using R16 = RegLayout<16>;
+      k_trd_tridiag_reg<KP, MODE, KP, 0, true>
+          <<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
+      if constexpr (KP == 64)
+        k_trd_tridiag_reg<32, PM_BATCH, 64, 32, true>
+            <<<(n + R32::NMAT - 1) / R32::NMAT, 128, R32::NMAT * R32::PER * sizeof(double), s>>>(a, c0, n);
+      k_trd_tridiag_reg<16, PM_BATCH, KP, KP - 16, false>
+          <<<(n + R16::NMAT - 1) / R16::NMAT, 128, R16::NMAT * R16::PER * sizeof(double), s>>>(a, c0, n);
       split = true;
     }
   }
@@ -1302,11 +1288,15 @@ void set_attrs() {
   cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
-  if constexpr (KP == 64) {
-    cudaFuncSetAttribute(k_trd_tridiag_reg<64, MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(RegLayout<64>::NMAT * RegLayout<64>::PER * sizeof(double)));
-    cudaFuncSetAttribute(k_trd_tridiag_reg<32, PM_BATCH, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(RegLayout<32>::NMAT * RegLayout<32>::PER * sizeof(double)));
+  if constexpr (KP >= 32) {
+    cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE, KP, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
+    if constexpr (KP == 64)
+      cudaFuncSetAttribute(k_trd_tridiag_reg<32, PM_BATCH, 64, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(RegLayout<32>::NMAT * RegLayout<32>::PER * sizeof(double)));
+    cudaFuncSetAttribute(k_trd_tridiag_reg<16, PM_BATCH, KP, KP - 16, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(RegLayout<16>::NMAT * RegLayout<16>::PER * sizeof(double)));
   }
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1346,7 +1336,10 @@ void psd_trd_init_attributes() {
   set_attrs<64, PM_DUAL>();
 }
 
-int trd_launches_per_chunk(int bucket) { return (bucket == B_TRD64 && g_trd_reg && g_trd_split) ? 5 : 4; }
+int trd_launches_per_chunk(int bucket) {
+  if (!(g_trd_reg && g_trd_split)) return 4;
+  return bucket == B_TRD64 ? 6 : bucket == B_TRD32 ? 5 : 4;
+}
 
 int64_t trd_hsize(int kp, int k) {
   const int64_t v = k >= 2 ? (int64_t)(k - 1) * (k - 2) / 2 : 0;
