@@ -370,10 +370,15 @@ __device__ __forceinline__ void reg_blocks(double (&A)[KP], int i, int k, const 
 // matrices per warp) reduces the trailing block, writing d, e, tau and the Householder vectors at
 // their places in the slot (the vectors of later steps follow the earlier ones in the packed order
 // and their entries are relative to the step, so only the step index JO is offset).
-// k = 64 bucket: 64 -> 32 -> 16 (steps 0..31, 32..47, 48..); k = 32 bucket: 32 -> 16.  A matrix whose
+// k = 64 bucket: 64 -> 32 -> 16 -> 8 (steps 0..31, 32..47, 48..55, 56..); k = 32: 32 -> 16 -> 8;
+// k = 16: 16 -> 8.  A matrix whose
 // remaining order is <= 2 at a stage boundary finishes in the stage that reaches it.
 static int g_trd_split = 1;
-__host__ __device__ constexpr int split_zoff(int jo) { return jo == 48 ? 1024 : 0; }  // doubles
+// scratch offset (doubles) of the block a stage starting at step jo reads: 64 | 32 | 16 | 8 wide
+// blocks of one slot never overlap the block the same stage writes
+__host__ __device__ constexpr int split_zoff(int jo) {
+  return jo == 48 ? 1024 : jo == 56 ? 1280 : jo == 24 ? 256 : 0;
+}
 
 template <int KP, int MODE, int HKP = KP, int JO = 0, bool STOP = false>
 __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjArgs a, int slot0, int nslots) {
@@ -1255,19 +1260,21 @@ void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
   using IL = InvLayout<KP>;
   using RL = RegLayout<KP>;
   bool split = false;
-  if constexpr (KP >= 32) {
-    if (g_trd_reg && g_trd_split) {
-      using R32 = RegLayout<32>;
-      using R16 = RegLayout<16>;
-      k_trd_tridiag_reg<KP, MODE, KP, 0, true>
-          <<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
-      if constexpr (KP == 64)
-        k_trd_tridiag_reg<32, PM_BATCH, 64, 32, true>
-            <<<(n + R32::NMAT - 1) / R32::NMAT, 128, R32::NMAT * R32::PER * sizeof(double), s>>>(a, c0, n);
-      k_trd_tridiag_reg<16, PM_BATCH, KP, KP - 16, false>
+  if (g_trd_reg && g_trd_split) {
+    using R32 = RegLayout<32>;
+    using R16 = RegLayout<16>;
+    using R8 = RegLayout<8>;
+    k_trd_tridiag_reg<KP, MODE, KP, 0, true>
+        <<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
+    if constexpr (KP == 64)
+      k_trd_tridiag_reg<32, PM_BATCH, 64, 32, true>
+          <<<(n + R32::NMAT - 1) / R32::NMAT, 128, R32::NMAT * R32::PER * sizeof(double), s>>>(a, c0, n);
+    if constexpr (KP >= 32)
+      k_trd_tridiag_reg<16, PM_BATCH, KP, KP - 16, true>
           <<<(n + R16::NMAT - 1) / R16::NMAT, 128, R16::NMAT * R16::PER * sizeof(double), s>>>(a, c0, n);
-      split = true;
-    }
+    k_trd_tridiag_reg<8, PM_BATCH, KP, KP - 8, false>
+        <<<(n + R8::NMAT - 1) / R8::NMAT, 128, R8::NMAT * R8::PER * sizeof(double), s>>>(a, c0, n);
+    split = true;
   }
   if (split) {
   } else if (g_trd_reg)
@@ -1288,16 +1295,17 @@ void set_attrs() {
   cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
-  if constexpr (KP >= 32) {
-    cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE, KP, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
-    if constexpr (KP == 64)
-      cudaFuncSetAttribute(k_trd_tridiag_reg<32, PM_BATCH, 64, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(RegLayout<32>::NMAT * RegLayout<32>::PER * sizeof(double)));
-    cudaFuncSetAttribute(k_trd_tridiag_reg<16, PM_BATCH, KP, KP - 16, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE, KP, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
+  if constexpr (KP == 64)
+    cudaFuncSetAttribute(k_trd_tridiag_reg<32, PM_BATCH, 64, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(RegLayout<32>::NMAT * RegLayout<32>::PER * sizeof(double)));
+  if constexpr (KP >= 32)
+    cudaFuncSetAttribute(k_trd_tridiag_reg<16, PM_BATCH, KP, KP - 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(RegLayout<16>::NMAT * RegLayout<16>::PER * sizeof(double)));
-  }
+  cudaFuncSetAttribute(k_trd_tridiag_reg<8, PM_BATCH, KP, KP - 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(RegLayout<8>::NMAT * RegLayout<8>::PER * sizeof(double)));
+
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1338,7 +1346,7 @@ void psd_trd_init_attributes() {
 
 int trd_launches_per_chunk(int bucket) {
   if (!(g_trd_reg && g_trd_split)) return 4;
-  return bucket == B_TRD64 ? 6 : bucket == B_TRD32 ? 5 : 4;
+  return bucket == B_TRD64 ? 7 : bucket == B_TRD32 ? 6 : 5;
 }
 
 int64_t trd_hsize(int kp, int k) {
