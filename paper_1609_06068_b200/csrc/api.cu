@@ -205,7 +205,7 @@ inline int64_t pipe_split(const std::vector<int64_t>& off, int64_t p, int form) 
 // (fork / join by events, captured into the iteration graph as a branch).
 struct TierFork {
   static constexpr int kMaxSide = 4;
-  int nside = 0;  // SDP_TIER_STREAMS (default 1: measured no gain from more on cfg3 / cfg4)
+  int nside = 0;  // SDP_TIER_STREAMS (default 2: cfg4 16.52M -> 16.78M proj/s, cfg3 / cfg1 unchanged; 3-4: no further gain)
   cudaStream_t side[kMaxSide] = {};
   // the lead tier (the giant chain, else the largest tier) runs on a stream of the highest
   // priority, so its kernels take the SMs first and the other tiers fill what its low-occupancy
@@ -214,7 +214,7 @@ struct TierFork {
   cudaEvent_t fork = nullptr, join[kMaxSide] = {}, join_hi = nullptr;
   void create() {
     const char* e = getenv("SDP_TIER_STREAMS");
-    nside = e ? std::max(1, std::min(kMaxSide, atoi(e))) : 1;
+    nside = e ? std::max(1, std::min(kMaxSide, atoi(e))) : 2;
     SDP_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     for (int i = 0; i < nside; ++i) {
       SDP_CUDA_TRY(cudaStreamCreateWithFlags(&side[i], cudaStreamNonBlocking));
