@@ -677,43 +677,51 @@ __global__ void __launch_bounds__(QL_T) k_trd_ql(ProjArgs a, int slot0, int nslo
   const int slot = slot0 + sl;
   const int k = a.ksz[a.ids[slot]];
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
+  double tnorm = 0.0, eprev = 0.0;  // ||T||_inf of the unscaled T
   for (int i = 0; i < k; ++i) {
-    d[i * QL_T] = H.d()[i];
-    e[i * QL_T] = H.e()[i];
+    const double di = H.d()[i], ei = H.e()[i];
+    d[i * QL_T] = di;
+    e[i * QL_T] = ei;
+    tnorm = fmax(tnorm, fabs(di) + eprev + (i + 1 < k ? fabs(ei) : 0.0));
+    eprev = fabs(ei);
   }
   const bool ok = g_ql_fused ? tql_vals<RSQ>(k, d, e, QL_T) : tql<RSQ>(k, d, e, QL_T, [](int, double, double) {});
   // the side of 0 with fewer eigenvectors: P_+ = sum_{l>0} l v v^T (side 0) or
   // A + sum_{l<0} |l| v v^T (side 1); selected eigenvalues sorted ascending,
   // clusters (gap <= 1e-3 ||T||, LAPACK dstein's ORTOL) and distinct shifts
   int npos = 0, nneg = 0;
-  double tnorm = 0.0;
   for (int i = 0; i < k; ++i) {
     const double l = d[i * QL_T];
     npos += l > 0.0;
     nneg += l < 0.0;
-    tnorm = fmax(tnorm, fabs(H.d()[i]) + (i > 0 ? fabs(H.e()[i - 1]) : 0.0) + (i + 1 < k ? fabs(H.e()[i]) : 0.0));
   }
   const int side = npos <= nneg ? 0 : 1;
-  double* ls = H.lsel();
+  // the selected eigenvalues are sorted in shared memory (e is free after QL; the sort in the
+  // global workspace put one L2 round trip into every comparison: ~10 % of the kernel)
+  double* ls = e;  // element i at [i * QL_T]
   int n = 0;
   for (int i = 0; i < k; ++i) {
     const double l = d[i * QL_T];
     if (side == 0 ? l > 0.0 : l < 0.0) {
       int j = n++ - 1;  // insertion sort, ascending
-      while (j >= 0 && ls[j] > l) {
-        ls[j + 1] = ls[j];
+      while (j >= 0 && ls[j * QL_T] > l) {
+        ls[(j + 1) * QL_T] = ls[j * QL_T];
         --j;
       }
-      ls[j + 1] = l;
+      ls[(j + 1) * QL_T] = l;
     }
   }
   const double ortol = 1e-3 * tnorm, pertol = 10.0 * 2.220446049250313e-16 * tnorm;
   int lead = 0;
+  double prev = 0.0;
   for (int i = 0; i < n; ++i) {
-    H.lw()[i] = side == 0 ? ls[i] : -ls[i];
-    if (i == 0 || ls[i] - ls[i - 1] > ortol) lead = i;
+    double li = ls[i * QL_T];
+    H.lw()[i] = side == 0 ? li : -li;
+    if (i == 0 || li - prev > ortol) lead = i;
     H.clst()[i] = (double)lead;
-    if (i > lead && ls[i] - ls[i - 1] < pertol) ls[i] = ls[i - 1] + pertol;
+    if (i > lead && li - prev < pertol) li = prev + pertol;
+    H.lsel()[i] = li;
+    prev = li;
   }
   H.hdr()[0] = (double)n;
   H.hdr()[1] = (double)side;
