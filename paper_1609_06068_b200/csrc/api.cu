@@ -60,17 +60,24 @@ struct Alloc {
   T* get(size_t n) {
     return (T*)raw(std::max<size_t>(n, 1) * sizeof(T));
   }
+  // cudaMemset and cudaMemcpy from pageable host memory run on the legacy default stream and may
+  // return before they land; the kernels that read the buffers run on non-blocking streams, so
+  // both wait for the legacy stream before returning the buffer
   template <class T>
   T* zeros(size_t n) {
     T* p = get<T>(n);
     SDP_CUDA_TRY(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+    SDP_CUDA_TRY(cudaStreamSynchronize(cudaStreamLegacy));
     return p;
   }
   template <class T>
   T* upload(const std::vector<T>& v, size_t n_alloc = 0) {
     size_t n = std::max(v.size(), n_alloc);
-    T* p = zeros<T>(n);
+    T* p = get<T>(n);
+    if (v.size() < std::max<size_t>(n, 1))
+      SDP_CUDA_TRY(cudaMemset(p, 0, std::max<size_t>(n, 1) * sizeof(T)));
     if (!v.empty()) SDP_CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    SDP_CUDA_TRY(cudaStreamSynchronize(cudaStreamLegacy));
     return p;
   }
   void free_one(void* p) {
@@ -2035,7 +2042,9 @@ int setup_impl(const sdp_problem* P, const sdp_options* opt_in, sdp_handle* out)
 // Sum a host vector over the ranks (getters of a sharded handle; collective).
 void allreduce_host(sdp_handle h, std::vector<double>& v) {
   double* d = h->alloc.get<double>(v.size());
-  SDP_CUDA_TRY(cudaMemcpy(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+  // on the handle's stream: a legacy-stream cudaMemcpy from pageable memory can return before the
+  // data lands, and the loopback sum (ordered after this stream's ready event) would read it early
+  SDP_CUDA_TRY(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   h->comm->allreduce_sum(d, v.size(), h->stream);
   SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
   SDP_CUDA_TRY(cudaMemcpy(v.data(), d, v.size() * sizeof(double), cudaMemcpyDeviceToHost));
@@ -2371,8 +2380,8 @@ void apply_rho(sdp_handle h, double rho) {
     SDP_CUDA_TRY(cudaMemcpy(&saved, h->done, sizeof(int), cudaMemcpyDeviceToHost));
     SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
     enqueue_scatter(h, h->stream);
+    SDP_CUDA_TRY(cudaMemcpyAsync(h->done, &saved, sizeof(int), cudaMemcpyHostToDevice, h->stream));
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    SDP_CUDA_TRY(cudaMemcpy(h->done, &saved, sizeof(int), cudaMemcpyHostToDevice));
   }
   rebuild_graph(h);
 }
@@ -2383,9 +2392,9 @@ int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info) {
     if (!h) throw Error{SDP_E_INVALID_ARG, "handle is NULL"};
     if (!(tol > 0)) throw Error{SDP_E_INVALID_ARG, "tol must be positive"};
     DeviceGuard dg(h->device);
+    SDP_CUDA_TRY(cudaMemcpyAsync(h->tol, &tol, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    SDP_CUDA_TRY(cudaMemcpy(h->tol, &tol, sizeof(double), cudaMemcpyHostToDevice));
-    SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
     long long it = 0;
     int done = 0, num = 0;
     SDP_CUDA_TRY(cudaMemcpy(&it, h->iter, sizeof(it), cudaMemcpyDeviceToHost));
@@ -2417,8 +2426,9 @@ int sdp_solve(sdp_handle h, int32_t max_iters, double tol, sdp_info* info) {
     // a stop skips the pending next-iteration A: put the finished iteration's x / y back
     settle(h);
     const double neg = -1.0;
-    SDP_CUDA_TRY(cudaMemcpy(h->tol, &neg, sizeof(double), cudaMemcpyHostToDevice));
-    SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
+    SDP_CUDA_TRY(cudaMemcpyAsync(h->tol, &neg, sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
     if (info) fill_info(h, info);
     if (num) throw Error{SDP_E_NUMERICAL, "non-finite residuals (NaN/Inf in the iterates)"};
     return done ? SDP_OK : SDP_MAX_ITER;
@@ -2591,8 +2601,8 @@ int sdp_profile_phases(sdp_handle h, int32_t iters, double* out_ms) {
     if (!h || !out_ms || iters <= 0) throw Error{SDP_E_INVALID_ARG, "bad argument"};
     DeviceGuard dg(h->device);
     settle(h);
+    SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
     SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));
-    SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
     std::vector<cudaEvent_t> ev(16 * (size_t)iters);
     for (auto& e : ev) SDP_CUDA_TRY(cudaEventCreate(&e));
     std::vector<int> ids;
@@ -2741,7 +2751,7 @@ int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes) {
     if (bytes < 8 * L.words()) throw Error{SDP_E_INVALID_ARG, "state blob truncated"};
     const double* w = reinterpret_cast<const double*>(hd + kStateHeader);
     auto put = [&](double* dev, int64_t n) {
-      if (n) SDP_CUDA_TRY(cudaMemcpy(dev, w, n * sizeof(double), cudaMemcpyHostToDevice));
+      if (n) SDP_CUDA_TRY(cudaMemcpyAsync(dev, w, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
       w += n;
     };
     put(h->xk, L.stot);
@@ -2757,11 +2767,12 @@ int sdp_load_state(sdp_handle h, const void* host_in, int64_t bytes) {
     put(h->prevall, L.nprev);
     const long long it = hd[9];
     const unsigned long long cap = (unsigned long long)hd[10], sw = (unsigned long long)hd[11];
-    SDP_CUDA_TRY(cudaMemcpy(h->iter, &it, sizeof(it), cudaMemcpyHostToDevice));
-    SDP_CUDA_TRY(cudaMemcpy(h->capped, &cap, sizeof(cap), cudaMemcpyHostToDevice));
-    SDP_CUDA_TRY(cudaMemcpy(h->sweeps, &sw, sizeof(sw), cudaMemcpyHostToDevice));
-    SDP_CUDA_TRY(cudaMemset(h->done, 0, sizeof(int)));
-    SDP_CUDA_TRY(cudaMemset(h->numerical, 0, sizeof(int)));
+    SDP_CUDA_TRY(cudaMemcpyAsync(h->iter, &it, sizeof(it), cudaMemcpyHostToDevice, h->stream));
+    SDP_CUDA_TRY(cudaMemcpyAsync(h->capped, &cap, sizeof(cap), cudaMemcpyHostToDevice, h->stream));
+    SDP_CUDA_TRY(cudaMemcpyAsync(h->sweeps, &sw, sizeof(sw), cudaMemcpyHostToDevice, h->stream));
+    SDP_CUDA_TRY(cudaMemsetAsync(h->done, 0, sizeof(int), h->stream));
+    SDP_CUDA_TRY(cudaMemsetAsync(h->numerical, 0, sizeof(int), h->stream));
+    SDP_CUDA_TRY(cudaStreamSynchronize(h->stream));  // (it, cap, sw are locals)
     double rho;
     std::memcpy(&rho, &hd[12], 8);
     h->rho = rho;  // r1 / D was restored as saved: no rebuild from x_k, lambda_k
