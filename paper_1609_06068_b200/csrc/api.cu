@@ -337,7 +337,7 @@ struct sdp_handle_s {
   int32_t* d_ids[B_NUM] = {};
   int bcount[B_NUM] = {};
   GiantDev gd;
-  TrdDev td[kTrdTiers];  // B_TRD16, B_TRD32, B_TRD64
+  TrdDev td[kTrdTiers];  // B_TRD8 .. B_TRD64
   TierFork tiers;
   Pipe pipe;
   // A
@@ -682,7 +682,7 @@ void build_buckets(Alloc& al, const std::vector<int32_t>& ksz, int32_t* d_ids[B_
     d_ids[b] = bcount[b] ? al.upload(lists[b]) : nullptr;
   }
   build_giant(al, ksz, lists[B_GLOBAL], gd);
-  for (int t = 0; t < kTrdTiers; ++t) build_trd(al, ksz, lists[B_TRD16 + t], trd_kp(B_TRD16 + t), td[t]);
+  for (int t = 0; t < kTrdTiers; ++t) build_trd(al, ksz, lists[B_TRD8 + t], trd_kp(B_TRD8 + t), td[t]);
 }
 
 // The tiers are independent: the giant tier (a chain of kernels whose tail leaves most SMs idle)
@@ -725,7 +725,7 @@ void launch_tiers(ProjArgs a, int mode, int32_t* const d_ids[B_NUM], const int b
     }
     a.ids = d_ids[b];
     a.count = bcount[b];
-    if (is_trd(b)) a.td = td[b - B_TRD16];
+    if (is_trd(b)) a.td = td[b - B_TRD8];
     launch_projection(b, mode, a, so);
   }
   for (int k = 0; k < TierFork::kMaxSide; ++k)
@@ -1024,7 +1024,7 @@ void build_pipeline(sdp_handle h, const std::vector<int32_t>& G, const std::vect
     }
     std::vector<int32_t> ksz(p);
     SDP_CUDA_TRY(cudaMemcpy(ksz.data(), h->d_ksz, p * sizeof(int32_t), cudaMemcpyDeviceToHost));
-    for (int t = 0; t < kTrdTiers; ++t) build_trd(al, ksz, lists[B_TRD16 + t], trd_kp(B_TRD16 + t), B.td[t]);
+    for (int t = 0; t < kTrdTiers; ++t) build_trd(al, ksz, lists[B_TRD8 + t], trd_kp(B_TRD8 + t), B.td[t]);
   }
   int lo = 0, hi = 0;
   SDP_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1288,7 +1288,7 @@ int pipe_launches_per_iter(sdp_handle h) {
     for (int b = 0; b < B_NUM; ++b) {
       if (!P.half[hf].bcount[b]) continue;
       if (is_trd(b)) {
-        const TrdDev& t = P.half[hf].td[b - B_TRD16];
+        const TrdDev& t = P.half[hf].td[b - B_TRD8];
         n += trd_launches_per_chunk(b) * ((t.count + t.chunk - 1) / t.chunk);
       } else {
         n += 1;
@@ -1352,7 +1352,7 @@ int launches_per_iter(sdp_handle h) {
   for (int b = 0; b < B_NUM; ++b) {  // one launch per non-empty tier; 4-5 per chunk for the QL tiers
     if (!h->bcount[b]) continue;
     if (is_trd(b)) {
-      const TrdDev& t = h->td[b - B_TRD16];
+      const TrdDev& t = h->td[b - B_TRD8];
       n += trd_launches_per_chunk(b) * ((t.count + t.chunk - 1) / t.chunk);
     } else {
       n += 1;
@@ -3036,7 +3036,7 @@ int32_t sdp_psd_plan_launches(sdp_psd_plan pl) {
   for (int b = 0; b < B_NUM; ++b) {
     if (!pl->bcount[b]) continue;
     if (is_trd(b)) {
-      const TrdDev& t = pl->td[b - B_TRD16];
+      const TrdDev& t = pl->td[b - B_TRD8];
       n += trd_launches_per_chunk(b) * ((t.count + t.chunk - 1) / t.chunk);
     } else {
       n += 1;

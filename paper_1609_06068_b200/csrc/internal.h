@@ -89,12 +89,12 @@ Comm* make_loop_comm(void* group, int world, int rank);
 // ---------------------------------------------------------------- projection buckets
 // Kernel tiers for the batched eigen-projection (kernels_psd.cu).
 enum BucketKind {
-  B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_RV8, B_RV16, B_RV32, B_RV64, B_TRD16, B_TRD32, B_TRD64, B_WJ32, B_NUM
+  B_G8 = 0, B_G16, B_G32, B_CTA32, B_CTA64, B_CTA96, B_GLOBAL, B_RV8, B_RV16, B_RV32, B_RV64, B_TRD8, B_TRD16, B_TRD32, B_TRD64, B_WJ32, B_NUM
 };
 inline bool is_rv(int b) { return b >= B_RV8 && b <= B_RV64; }
-inline bool is_trd(int b) { return b == B_TRD16 || b == B_TRD32 || b == B_TRD64; }
-inline int trd_kp(int b) { return b == B_TRD16 ? 16 : b == B_TRD32 ? 32 : 64; }
-constexpr int kTrdTiers = 3;  // B_TRD16, B_TRD32, B_TRD64 (TrdDev arrays indexed by b - B_TRD16)
+inline bool is_trd(int b) { return b >= B_TRD8 && b <= B_TRD64; }
+inline int trd_kp(int b) { return b == B_TRD8 ? 8 : b == B_TRD16 ? 16 : b == B_TRD32 ? 32 : 64; }
+constexpr int kTrdTiers = 4;  // B_TRD8 .. B_TRD64 (TrdDev arrays indexed by b - B_TRD8)
 // Size ranges (k <= 8, 16, 32, 64, 96, larger) with fewer than kFewMatrices
 // members use one CTA per matrix so that a small batch still fills the GPU.
 constexpr int64_t kFewMatrices = 2048;

@@ -483,13 +483,14 @@ static int tier_mode() {  // 0 default, 1 smem Jacobi, 2 Jacobi (register V), 3 
   return v;
 }
 static int use_smem_tiers() { return tier_mode() == 1; }
-// orders above this take the QL tier when there are many of them: 8 (8 < k <= 16 in the KP = 16
-// QL tier); SDP_TRD16=0 keeps 8 < k <= 16 on register-V Jacobi (order 16)
+// orders above this take the QL tier when there are many of them: 4 (KP = 8 and 16 QL tiers);
+// SDP_TRD8=0 keeps k <= 8 on register-V Jacobi (order 8), SDP_TRD16=0 every k <= 16 (order 16)
 static int trd_min_order() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("SDP_TRD16");
-    v = (e && e[0] == '0') ? 16 : 8;
+    const char* e16 = getenv("SDP_TRD16");
+    const char* e8 = getenv("SDP_TRD8");
+    v = (e16 && e16[0] == '0') ? 16 : (e8 && e8[0] == '0') ? 8 : 4;
   }
   return v;
 }
@@ -500,7 +501,7 @@ int bucket_of(int k, int64_t count_in_range) {
   // many mid-size matrices: tridiagonal-QL (throughput); a few (e.g. 400 cliques of
   // 30): one CTA each with warm-started Jacobi is the lower-latency choice
   if (k > trd_min_order() && k <= 64 && (tier_mode() == 3 || (tier_mode() == 0 && count_in_range >= kFewMatrices)))
-    return k <= 16 ? B_TRD16 : k <= 32 ? B_TRD32 : B_TRD64;
+    return k <= 8 ? B_TRD8 : k <= 16 ? B_TRD16 : k <= 32 ? B_TRD32 : B_TRD64;
   if (!use_smem_tiers() && k <= 64) {
     // few mid-size matrices (e.g. 400 cliques of 30): one 128-thread CTA each is
     // the lower-latency choice; otherwise the register-V tiers

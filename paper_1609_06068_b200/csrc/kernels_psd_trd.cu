@@ -1268,20 +1268,22 @@ void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
   using IL = InvLayout<KP>;
   using RL = RegLayout<KP>;
   bool split = false;
-  if (g_trd_reg && g_trd_split) {
+  if (KP >= 16 && g_trd_reg && g_trd_split) {
     using R32 = RegLayout<32>;
     using R16 = RegLayout<16>;
     using R8 = RegLayout<8>;
-    k_trd_tridiag_reg<KP, MODE, KP, 0, true>
-        <<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
+    if constexpr (KP >= 16)
+      k_trd_tridiag_reg<KP, MODE, KP, 0, true>
+          <<<(n + RL::NMAT - 1) / RL::NMAT, 128, RL::NMAT * RL::PER * sizeof(double), s>>>(a, c0, n);
     if constexpr (KP == 64)
       k_trd_tridiag_reg<32, PM_BATCH, 64, 32, true>
           <<<(n + R32::NMAT - 1) / R32::NMAT, 128, R32::NMAT * R32::PER * sizeof(double), s>>>(a, c0, n);
     if constexpr (KP >= 32)
       k_trd_tridiag_reg<16, PM_BATCH, KP, KP - 16, true>
           <<<(n + R16::NMAT - 1) / R16::NMAT, 128, R16::NMAT * R16::PER * sizeof(double), s>>>(a, c0, n);
-    k_trd_tridiag_reg<8, PM_BATCH, KP, KP - 8, false>
-        <<<(n + R8::NMAT - 1) / R8::NMAT, 128, R8::NMAT * R8::PER * sizeof(double), s>>>(a, c0, n);
+    if constexpr (KP >= 16)
+      k_trd_tridiag_reg<8, PM_BATCH, KP, KP - 8, false>
+          <<<(n + R8::NMAT - 1) / R8::NMAT, 128, R8::NMAT * R8::PER * sizeof(double), s>>>(a, c0, n);
     split = true;
   }
   if (split) {
@@ -1303,16 +1305,18 @@ void set_attrs() {
   cudaFuncSetAttribute(k_trd_tridiag<KP, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
-  cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE, KP, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
+  if constexpr (KP >= 16)
+    cudaFuncSetAttribute(k_trd_tridiag_reg<KP, MODE, KP, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(RegLayout<KP>::NMAT * RegLayout<KP>::PER * sizeof(double)));
   if constexpr (KP == 64)
     cudaFuncSetAttribute(k_trd_tridiag_reg<32, PM_BATCH, 64, 32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(RegLayout<32>::NMAT * RegLayout<32>::PER * sizeof(double)));
   if constexpr (KP >= 32)
     cudaFuncSetAttribute(k_trd_tridiag_reg<16, PM_BATCH, KP, KP - 16, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(RegLayout<16>::NMAT * RegLayout<16>::PER * sizeof(double)));
-  cudaFuncSetAttribute(k_trd_tridiag_reg<8, PM_BATCH, KP, KP - 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)(RegLayout<8>::NMAT * RegLayout<8>::PER * sizeof(double)));
+  if constexpr (KP >= 16)
+    cudaFuncSetAttribute(k_trd_tridiag_reg<8, PM_BATCH, KP, KP - 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(RegLayout<8>::NMAT * RegLayout<8>::PER * sizeof(double)));
 
   cudaFuncSetAttribute(k_trd_ql<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1341,6 +1345,9 @@ void psd_trd_init_attributes() {
   const char* eqf = std::getenv("SDP_TRD_QLFUSED");
   const int qf = (eqf && eqf[0] == '0') ? 0 : 1;
   cudaMemcpyToSymbol(g_ql_fused, &qf, sizeof(int));
+  set_attrs<8, PM_BATCH>();
+  set_attrs<8, PM_PRIMAL>();
+  set_attrs<8, PM_DUAL>();
   set_attrs<16, PM_BATCH>();
   set_attrs<16, PM_PRIMAL>();
   set_attrs<16, PM_DUAL>();
@@ -1354,7 +1361,7 @@ void psd_trd_init_attributes() {
 
 int trd_launches_per_chunk(int bucket) {
   if (!(g_trd_reg && g_trd_split)) return 4;
-  return bucket == B_TRD64 ? 7 : bucket == B_TRD32 ? 6 : 5;
+  return bucket == B_TRD64 ? 7 : bucket == B_TRD32 ? 6 : bucket == B_TRD16 ? 5 : 4;
 }
 
 int64_t trd_hsize(int kp, int k) {
@@ -1367,7 +1374,11 @@ void launch_projection_trd(int bucket, int mode, const ProjArgs& a, cudaStream_t
   if (count <= 0) return;
   for (int c0 = 0; c0 < count; c0 += a.td.chunk) {
     const int n = std::min(a.td.chunk, count - c0);
-    if (bucket == B_TRD16) {
+    if (bucket == B_TRD8) {
+      if (mode == PM_BATCH) launch_chunk<8, PM_BATCH>(a, c0, n, s);
+      else if (mode == PM_PRIMAL) launch_chunk<8, PM_PRIMAL>(a, c0, n, s);
+      else launch_chunk<8, PM_DUAL>(a, c0, n, s);
+    } else if (bucket == B_TRD16) {
       if (mode == PM_BATCH) launch_chunk<16, PM_BATCH>(a, c0, n, s);
       else if (mode == PM_PRIMAL) launch_chunk<16, PM_PRIMAL>(a, c0, n, s);
       else launch_chunk<16, PM_DUAL>(a, c0, n, s);

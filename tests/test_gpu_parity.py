@@ -712,6 +712,21 @@ def test_trd16_tier_batch_many(lib, gen):
     check_batch(lib, ks, vals, tol=1e-12)
 
 
+def test_trd8_tier_batch_many(lib, gen):
+    """>= 2048 matrices of order 5..8 select the KP = 8 tridiagonal-QL tier (four matrices per warp in
+    the tridiagonalization, at most four selected eigenvectors, one warp per apply); random orders
+    plus the degenerate structured inputs, against the oracle."""
+    rng = np.random.default_rng(8)
+    mats = []
+    for k in (5, 6, 7, 8):
+        mats += _structured(k, rng)
+    ks = list(rng.integers(5, 9, 4400))
+    vals = [rng.standard_normal(k * (k + 1) // 2) for k in ks]
+    ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)
+    vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)
+    check_batch(lib, ks, vals, tol=1e-12)
+
+
 def test_trd_tier_admm_subprocess():
     """SDP_PSD_TIERS=trd: every clique of order 17..64 takes the QL tier inside
     the ADMM iteration (primal and dual), iterates match the oracle."""
@@ -745,7 +760,7 @@ def test_trd_tier_inline_ql_fallback_subprocess():
         "import paper_1609_06068_b200 as L\n"
         "from oracle import psd as opsd\n"
         "rng = np.random.default_rng(4)\n"
-        "ks = rng.integers(9, 65, 3000).astype(np.int32)\n"
+        "ks = rng.integers(5, 65, 3000).astype(np.int32)\n"
         "vals = np.concatenate([rng.standard_normal(k*(k+1)//2) for k in ks])\n"
         "out = L.PsdPlan(ks).project_host(vals)\n"
         "want = opsd.project_psd_packed_batch(ks, vals)\n"
@@ -769,8 +784,8 @@ def test_trd_tier_variants_subprocess(variant):
         "from oracle import psd as opsd\n"
         "from test_gpu_parity import _structured\n"
         "rng = np.random.default_rng(5)\n"
-        "mats = [M for k in (9, 16, 17, 32, 33, 64) for M in _structured(k, rng)]\n"
-        "ks = list(rng.integers(9, 65, 3000))\n"
+        "mats = [M for k in (5, 8, 9, 16, 17, 32, 33, 64) for M in _structured(k, rng)]\n"
+        "ks = list(rng.integers(5, 65, 3000))\n"
         "vals = [rng.standard_normal(k*(k+1)//2) for k in ks]\n"
         "ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)\n"
         "vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)\n"
