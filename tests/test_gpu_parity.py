@@ -727,6 +727,35 @@ def test_trd8_tier_batch_many(lib, gen):
     check_batch(lib, ks, vals, tol=1e-12)
 
 
+def test_trd_tiers_inplace_and_deterministic(lib, gen):
+    """Every QL tier (KP = 8, 16, 32, 64: >= 2048 matrices per size range, the halving
+    tridiagonalization cascade, twisted eigenvectors): a projection in place (d_in == d_out, the
+    apply epilogue reads the side-1 input where it writes) equals the out-of-place one bit for bit,
+    two plans agree bit for bit, and the result matches the oracle."""
+    import torch
+    rng = np.random.default_rng(21)
+    ks = np.concatenate([rng.integers(lo, hi + 1, 2100) for lo, hi in ((5, 8), (9, 16), (17, 32), (33, 64))])
+    rng.shuffle(ks)
+    ks = ks.astype(np.int32)
+    vals = np.concatenate([rng.standard_normal(k * (k + 1) // 2) for k in ks])
+    pa, pb = lib.PsdPlan(ks), lib.PsdPlan(ks)
+    d_in = torch.from_numpy(vals).cuda()
+    out_a = torch.empty_like(d_in)
+    pa.project(d_in, out_a)
+    out_b = torch.empty_like(d_in)
+    pb.project(d_in, out_b)
+    d_ip = d_in.clone()
+    pa.project(d_ip, d_ip)
+    torch.cuda.synchronize()
+    a_, b_, ip = out_a.cpu().numpy(), out_b.cpu().numpy(), d_ip.cpu().numpy()
+    assert np.array_equal(a_, b_)
+    assert np.array_equal(a_, ip)
+    want = opsd.project_psd_packed_batch(ks, vals)
+    assert np.linalg.norm(a_ - want) <= 1e-12 * np.linalg.norm(want)
+    pa.close()
+    pb.close()
+
+
 def test_trd_tier_admm_subprocess():
     """SDP_PSD_TIERS=trd: every clique of order 17..64 takes the QL tier inside
     the ADMM iteration (primal and dual), iterates match the oracle."""
