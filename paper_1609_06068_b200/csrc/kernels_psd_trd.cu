@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjA
 
 static int g_trd_reg = 1;    // SDP_TRD_REG=0: the shared-memory tridiagonalization
 static int g_ql_rsqrt = 1;  // SDP_TRD_QLRSQ=0: QL rotations with sqrt + reciprocal
+static int g_trd_fusevec = 0;  // SDP_TRD_FUSEVEC=1: singleton eigenvectors in the apply kernel (measured slower)
 __constant__ int g_ql_fused = 1;  // SDP_TRD_QLFUSED=0: tql's scan loop in the QL kernel
 
 // ---------------------------------------------------------------- 2. implicit QL
@@ -769,7 +770,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, t, r);
 }
 
-template <int KP>
+// SKIP_SINGLE: the apply kernel forms the singleton vectors itself (twisted_vec below); only
+// clusters are handled here
+template <int KP, bool SKIP_SINGLE = false>
 __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = InvLayout<KP>;
@@ -783,6 +786,10 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
   const int nsel = (int)H.hdr()[0];
   const int k = a.ksz[a.ids[slot]];
+  if constexpr (SKIP_SINGLE) {  // a warp whose matrices have no cluster has nothing to do
+    const bool need = j0 + 1 < nsel && (int)H.clst()[j0] == j0 && (int)H.clst()[j0 + 1] == j0;
+    if (!__any_sync(__activemask(), need)) return;
+  }
   // T (d, e) into shared memory: the recurrences below read it element by element, and the
   // workspace is far larger than L2 / L1, so global reads would each pay a DRAM round trip
   double* d = smem + (Lay::GLOBAL2 ? 1 : 2) * KP * IV_T + (t / Lay::HALF) * 2 * KP;
@@ -803,6 +810,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   constexpr int S1 = Lay::GLOBAL2 ? ZL : IV_T;
   double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [i][j], row length KP/2
   const bool single = j0 + 1 >= nsel || (int)H.clst()[j0 + 1] != j0;
+  if (SKIP_SINGLE && single) return;
   bool fail = false;
   if (single) {
     const double lam = H.lsel()[j0];
@@ -997,10 +1005,95 @@ struct ApplyLayout {
   static constexpr int LD = KP / 2 + 4;
   static constexpr int YLD = 12;  // Y block row stride (8 reflectors + pad)
   static constexpr int NW = AT / 32;
+  // ... + d, e of T and the per-column cluster flags (fused eigenvector stage)
   static constexpr size_t bytes() {
-    return (size_t)(KP * LD + AT * YLD + 128 + NW * 128 + KP + 12) * sizeof(double);
+    return (size_t)(KP * LD + AT * YLD + 128 + NW * 128 + KP + 12 + 3 * KP) * sizeof(double);
   }
 };
+
+// The singleton eigenvector of k_trd_invit (same twisted factorization, same operations in the
+// same order, so the vector and its weight are bit-identical) formed in the apply kernel's shared
+// Z column zc (row stride LDZ), so Z never goes through DRAM.  No per-thread pivot arrays: the
+// bottom-up reciprocal pivots 1 / D-_i go into the column, the twist index r is found by a first
+// top-down pass, and a second top-down pass up to r overwrites rows 0..r-1 with 1 / D+_i (rows
+// below r need only D+, rows above r only D-).  Returns false where k_trd_invit sets rcount = -1.
+template <int LDZ>
+__device__ bool twisted_vec(int k, const double* d, const double* e, double lam, double tnorm, double* zc,
+                            double& nrm_out) {
+  const double tol = 2.220446049250313e-16 * fmax(tnorm, 1e-300);
+  double dm = d[k - 1] - lam;
+  if (fabs(dm) < tol) dm = dm < 0.0 ? -tol : tol;
+  double rmi = rcp_nr(dm);
+  zc[(k - 1) * LDZ] = rmi;
+  for (int i = k - 2; i >= 1; --i) {
+    const double ei = e[i];
+    dm = fma(-ei * ei, rmi, d[i] - lam);
+    if (fabs(dm) < tol) dm = dm < 0.0 ? -tol : tol;
+    rmi = rcp_nr(dm);
+    zc[i * LDZ] = rmi;
+  }
+  double dp = 0.0, best = 0.0, rpi = 0.0;
+  int r = 0;
+  for (int i = 0; i < k; ++i) {
+    const double ai = d[i] - lam;
+    if (i == 0) {
+      dp = ai;
+    } else {
+      const double em = e[i - 1];
+      dp = fma(-em * em, rpi, ai);
+    }
+    if (fabs(dp) < tol) dp = dp < 0.0 ? -tol : tol;
+    rpi = rcp_nr(dp);
+    const double gam = i + 1 < k ? fma(-e[i] * e[i], zc[(i + 1) * LDZ], dp) : dp;
+    if (i == 0 || fabs(gam) < best) {
+      best = fabs(gam);
+      r = i;
+    }
+  }
+  rpi = 0.0;
+  for (int i = 0; i < r; ++i) {  // 1 / D+_i below the twist (the same recurrence again)
+    const double ai = d[i] - lam;
+    if (i == 0) {
+      dp = ai;
+    } else {
+      const double em = e[i - 1];
+      dp = fma(-em * em, rpi, ai);
+    }
+    if (fabs(dp) < tol) dp = dp < 0.0 ? -tol : tol;
+    rpi = rcp_nr(dp);
+    zc[i * LDZ] = rpi;
+  }
+  double nrm = 1.0, mx = 1.0, res = 0.0, zr_up = 0.0, zr_dn = 0.0;
+  double z1 = 1.0, z2 = 0.0;
+  for (int i = r + 1; i < k; ++i) {  // above r: z_i = -(e_{i-1} / D-_i) z_{i-1}
+    const double z = z1 * (-e[i - 1] * zc[i * LDZ]);
+    zc[i * LDZ] = z;
+    if (i >= r + 2) res = fmax(res, fabs(fma(e[i - 2], z2, fma(d[i - 1] - lam, z1, e[i - 1] * z))));
+    else zr_up = z;
+    z2 = z1;
+    z1 = z;
+    nrm = fma(z, z, nrm);
+    mx = fmax(mx, fabs(z));
+  }
+  if (r + 1 < k) res = fmax(res, fabs(fma(e[k - 2], z2, (d[k - 1] - lam) * z1)));
+  z1 = 1.0;
+  z2 = 0.0;
+  for (int i = r - 1; i >= 0; --i) {  // below r: z_i = -(e_i / D+_i) z_{i+1}
+    const double z = z1 * (-e[i] * zc[i * LDZ]);
+    zc[i * LDZ] = z;
+    if (i <= r - 2) res = fmax(res, fabs(fma(e[i], z, fma(d[i + 1] - lam, z1, e[i + 1] * z2))));
+    else zr_dn = z;
+    z2 = z1;
+    z1 = z;
+    nrm = fma(z, z, nrm);
+    mx = fmax(mx, fabs(z));
+  }
+  if (r >= 1) res = fmax(res, fabs(fma(e[0], z2, (d[0] - lam) * z1)));
+  zc[r * LDZ] = 1.0;
+  res = fmax(res, fabs((d[r] - lam) + (r >= 1 ? e[r - 1] * zr_dn : 0.0) + (r + 1 < k ? e[r] * zr_up : 0.0)));
+  nrm_out = nrm;
+  return (res <= 1e-9 * fmax(tnorm, 1e-300) * mx) && (nrm < 1e300);
+}
 
 __device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -1008,7 +1101,7 @@ __device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <int KP, int MODE>
+template <int KP, int MODE, bool FV = false>
 __global__ void __launch_bounds__(ApplyLayout<KP>::AT) k_trd_apply(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = ApplyLayout<KP>;
@@ -1033,17 +1126,54 @@ __global__ void __launch_bounds__(ApplyLayout<KP>::AT) k_trd_apply(ProjArgs a, i
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
   int nsel = (int)H.hdr()[0];
   int side = (int)H.hdr()[1];
-  const bool fallback = a.td.rcount[slot] < 0 || a.td.force_fallback;
+  bool fallback = a.td.rcount[slot] < 0 || a.td.force_fallback;
   for (int e = tid; e < KP * LD; e += AT) Z[e] = 0.0;  // rows >= k, columns >= nsel stay 0 (DMMA tiles)
+  if constexpr (FV) {
+    // fused eigenvector stage: thread j forms singleton vector j in Z's column j; cluster columns
+    // (k_trd_invit<KP, true>) are read from the workspace
+    double* dsm = red + 12;
+    double* esm = dsm + KP;
+    double* cfl = esm + KP;
+    if (!fallback) {
+      for (int i = tid; i < k; i += AT) {
+        dsm[i] = H.d()[i];
+        esm[i] = H.e()[i];
+      }
+      if (tid < nsel) {
+        const bool single = (int)H.clst()[tid] == tid && (tid + 1 >= nsel || (int)H.clst()[tid + 1] != tid);
+        cfl[tid] = single ? 0.0 : 1.0;
+        lw[tid] = H.lw()[tid];
+      }
+    }
+    g.sync();
+    bool fail = false;
+    if (!fallback) {
+      const double* Zo = a.td.zbuf + a.td.zoff[slot];
+      for (int e = tid; e < k * (KP / 2); e += AT) {
+        const int i = e / (KP / 2), j = e - i * (KP / 2);
+        if (j < nsel && cfl[j] != 0.0) Z[i * LD + j] = Zo[e];
+      }
+      if (tid < nsel && cfl[tid] == 0.0) {
+        double nrm;
+        if (twisted_vec<LD>(k, dsm, esm, H.lsel()[tid], H.hdr()[2], Z + tid, nrm)) lw[tid] /= nrm;
+        else fail = true;
+      }
+    }
+    if (__syncthreads_or(fail) && !fallback) {
+      fallback = true;
+      for (int e = tid; e < KP * LD; e += AT) Z[e] = 0.0;
+    }
+  }
   g.sync();
-  if (!fallback) {
+  if (!FV && !fallback) {
     const double* Zo = a.td.zbuf + a.td.zoff[slot];  // [i][j], row length KP/2
     for (int e = tid; e < k * (KP / 2); e += AT) {
       const int i = e / (KP / 2), j = e - i * (KP / 2);
       if (j < nsel) Z[i * LD + j] = Zo[e];
     }
     if (tid < nsel) lw[tid] = H.lw()[tid];
-  } else {
+  }
+  if (fallback) {
     // QL with eigenvectors in the slot's global scratch (KP x KP), every thread
     // running the same chain on a private copy of (d, e) (identical arithmetic,
     // identical rotations) and rotating its own row; then the side of 0 with
@@ -1295,8 +1425,13 @@ void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
     k_trd_ql<KP, true><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
   else
     k_trd_ql<KP><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
-  k_trd_invit<KP><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
-  k_trd_apply<KP, MODE><<<n, ApplyLayout<KP>::AT, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
+  if (g_trd_fusevec) {
+    k_trd_invit<KP, true><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
+    k_trd_apply<KP, MODE, true><<<n, ApplyLayout<KP>::AT, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
+  } else {
+    k_trd_invit<KP><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
+    k_trd_apply<KP, MODE><<<n, ApplyLayout<KP>::AT, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
+  }
 }
 
 template <int KP, int MODE>
@@ -1331,6 +1466,11 @@ void set_attrs() {
   cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)InvLayout<KP>::bytes());
   cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)ApplyLayout<KP>::bytes());
+  cudaFuncSetAttribute(k_trd_invit<KP, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_invit<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)InvLayout<KP>::bytes());
+  cudaFuncSetAttribute(k_trd_apply<KP, MODE, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_apply<KP, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)ApplyLayout<KP>::bytes());
 }
 
 }  // namespace
@@ -1340,6 +1480,8 @@ void psd_trd_init_attributes() {
   g_trd_reg = (ev && ev[0] == '0') ? 0 : 1;
   const char* eq = std::getenv("SDP_TRD_QLRSQ");
   g_ql_rsqrt = (eq && eq[0] == '0') ? 0 : 1;
+  const char* efv = std::getenv("SDP_TRD_FUSEVEC");
+  g_trd_fusevec = (efv && efv[0] == '1') ? 1 : 0;
   const char* esp = std::getenv("SDP_TRD_SPLIT");
   g_trd_split = (esp && esp[0] == '0') ? 0 : 1;
   const char* eqf = std::getenv("SDP_TRD_QLFUSED");

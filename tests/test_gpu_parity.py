@@ -863,6 +863,41 @@ def test_trd_ql_fused_matches_tql_subprocess():
     assert np.linalg.norm(outs[0] - outs[1]) <= 1e-13 * np.linalg.norm(outs[1])
 
 
+def test_trd_fused_eigenvectors_bit_identical_subprocess():
+    """Singleton eigenvectors formed in the apply kernel's shared memory (SDP_TRD_FUSEVEC=1) are the same
+    twisted factorization as k_trd_invit's (default, vectors through the workspace),
+    so the projections agree bit for bit on every QL tier (orders 5..64, >= 2048 matrices per size
+    range) plus the structured spectra whose clusters still go through inverse iteration; both
+    match the oracle."""
+    import subprocess
+    import sys
+    import tempfile
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import paper_1609_06068_b200 as L\n"
+        "from oracle import psd as opsd\n"
+        "from test_gpu_parity import _structured\n"
+        "rng = np.random.default_rng(23)\n"
+        "mats = [M for k in (5, 8, 9, 16, 17, 24, 32, 33, 48, 64) for M in _structured(k, rng)]\n"
+        "ks = list(np.concatenate([rng.integers(lo, hi + 1, 2100) for lo, hi in ((5, 8), (9, 16), (17, 32), (33, 64))]))\n"
+        "vals = [rng.standard_normal(k*(k+1)//2) for k in ks]\n"
+        "ks = np.array([M.shape[0] for M in mats] + ks, dtype=np.int32)\n"
+        "vals = np.concatenate([opsd.pack_upper(M) for M in mats] + vals)\n"
+        "out = L.PsdPlan(ks).project_host(vals)\n"
+        "want = opsd.project_psd_packed_batch(ks, vals)\n"
+        "assert np.linalg.norm(out - want) <= 1e-12 * np.linalg.norm(want)\n"
+        "np.save(sys.argv[1], out)\n" % (ROOT, os.path.dirname(os.path.abspath(__file__))))
+    outs = []
+    with tempfile.TemporaryDirectory() as td:
+        for flag in ("1", "0"):
+            f = os.path.join(td, f"o{flag}.npy")
+            env = dict(os.environ, SDP_TRD_FUSEVEC=flag)
+            r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=900)
+            assert r.returncode == 0, r.stdout + r.stderr
+            outs.append(np.load(f))
+    assert np.array_equal(outs[0], outs[1])
+
+
 # ------------------------------------------------------------------ adaptive rho (SURVEY 8(f) #2)
 
 @pytest.mark.parametrize("form,rho", [("primal", 1.0), ("dual", 1.0), ("primal", 50.0)])
