@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(128, KP <= 16 ? 6 : 3) k_trd_tridiag_reg(ProjA
 
 static int g_trd_reg = 1;    // SDP_TRD_REG=0: the shared-memory tridiagonalization
 static int g_ql_rsqrt = 1;  // SDP_TRD_QLRSQ=0: QL rotations with sqrt + reciprocal
+static int g_trd_invit_order = 0;  // SDP_TRD_INVIT_ORDER=1: cluster eigenvectors scheduled first
 static int g_trd_fusevec = 0;  // SDP_TRD_FUSEVEC=1: singleton eigenvectors in the apply kernel (measured slower)
 __constant__ int g_ql_fused = 1;  // SDP_TRD_QLFUSED=0: tql's scan loop in the QL kernel
 
@@ -770,23 +771,32 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, t, r);
 }
 
-// SKIP_SINGLE: the apply kernel forms the singleton vectors itself (twisted_vec below); only
-// clusters are handled here
-template <int KP, bool SKIP_SINGLE = false>
+// ROLE 0: every selected eigenvector.  ROLE 1: clusters only (the apply kernel forms the singleton
+// vectors itself, twisted_vec below).  ROLE 2: a grid of two halves, the first for the clusters (so
+// their long inverse-iteration chains start first and overlap the rest), the second for the
+// singletons (SDP_TRD_INVIT_ORDER=1; same vectors bit for bit)
+template <int KP, int ROLE = 0>
 __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int nslots) {
   if (a.done && *a.done) return;
   using Lay = InvLayout<KP>;
   constexpr int ZL = KP / 2;  // row length of the output block
   extern __shared__ double smem[];
   const int t = threadIdx.x;
-  const int sl = blockIdx.x * Lay::NMAT + t / Lay::HALF;
+  int bid = blockIdx.x;
+  bool cl_role = ROLE == 1;
+  if constexpr (ROLE == 2) {
+    const int nb = (nslots + Lay::NMAT - 1) / Lay::NMAT;
+    cl_role = bid < nb;
+    if (!cl_role) bid -= nb;
+  }
+  const int sl = bid * Lay::NMAT + t / Lay::HALF;
   const int j0 = t % Lay::HALF;  // cluster leader this thread may own
   if (sl >= nslots) return;
   const int slot = slot0 + sl;
   const HView<KP> H{a.td.hbuf + a.td.hoff[slot]};
   const int nsel = (int)H.hdr()[0];
   const int k = a.ksz[a.ids[slot]];
-  if constexpr (SKIP_SINGLE) {  // a warp whose matrices have no cluster has nothing to do
+  if (cl_role) {  // a warp whose matrices have no cluster has nothing to do
     const bool need = j0 + 1 < nsel && (int)H.clst()[j0] == j0 && (int)H.clst()[j0 + 1] == j0;
     if (!__any_sync(__activemask(), need)) return;
   }
@@ -810,7 +820,7 @@ __global__ void __launch_bounds__(IV_T) k_trd_invit(ProjArgs a, int slot0, int n
   constexpr int S1 = Lay::GLOBAL2 ? ZL : IV_T;
   double* Zo = a.td.zbuf + a.td.zoff[slot];  // selected eigenvectors of T, [i][j], row length KP/2
   const bool single = j0 + 1 >= nsel || (int)H.clst()[j0 + 1] != j0;
-  if (SKIP_SINGLE && single) return;
+  if (ROLE != 0 && single == cl_role) return;
   bool fail = false;
   if (single) {
     const double lam = H.lsel()[j0];
@@ -1130,7 +1140,7 @@ __global__ void __launch_bounds__(ApplyLayout<KP>::AT) k_trd_apply(ProjArgs a, i
   for (int e = tid; e < KP * LD; e += AT) Z[e] = 0.0;  // rows >= k, columns >= nsel stay 0 (DMMA tiles)
   if constexpr (FV) {
     // fused eigenvector stage: thread j forms singleton vector j in Z's column j; cluster columns
-    // (k_trd_invit<KP, true>) are read from the workspace
+    // (k_trd_invit<KP, 1>) are read from the workspace
     double* dsm = red + 12;
     double* esm = dsm + KP;
     double* cfl = esm + KP;
@@ -1426,10 +1436,13 @@ void launch_chunk(const ProjArgs& a, int c0, int n, cudaStream_t s) {
   else
     k_trd_ql<KP><<<(n + QL_T - 1) / QL_T, QL_T, 2 * KP * QL_T * sizeof(double), s>>>(a, c0, n);
   if (g_trd_fusevec) {
-    k_trd_invit<KP, true><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
+    k_trd_invit<KP, 1><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
     k_trd_apply<KP, MODE, true><<<n, ApplyLayout<KP>::AT, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
   } else {
-    k_trd_invit<KP><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
+    if (g_trd_invit_order)
+      k_trd_invit<KP, 2><<<2 * ((n + IL::NMAT - 1) / IL::NMAT), IV_T, IL::bytes(), s>>>(a, c0, n);
+    else
+      k_trd_invit<KP><<<(n + IL::NMAT - 1) / IL::NMAT, IV_T, IL::bytes(), s>>>(a, c0, n);
     k_trd_apply<KP, MODE><<<n, ApplyLayout<KP>::AT, ApplyLayout<KP>::bytes(), s>>>(a, c0, n);
   }
 }
@@ -1466,8 +1479,10 @@ void set_attrs() {
   cudaFuncSetAttribute(k_trd_invit<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)InvLayout<KP>::bytes());
   cudaFuncSetAttribute(k_trd_apply<KP, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)ApplyLayout<KP>::bytes());
-  cudaFuncSetAttribute(k_trd_invit<KP, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaFuncSetAttribute(k_trd_invit<KP, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)InvLayout<KP>::bytes());
+  cudaFuncSetAttribute(k_trd_invit<KP, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_invit<KP, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)InvLayout<KP>::bytes());
+  cudaFuncSetAttribute(k_trd_invit<KP, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaFuncSetAttribute(k_trd_invit<KP, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)InvLayout<KP>::bytes());
   cudaFuncSetAttribute(k_trd_apply<KP, MODE, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   cudaFuncSetAttribute(k_trd_apply<KP, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)ApplyLayout<KP>::bytes());
@@ -1480,6 +1495,8 @@ void psd_trd_init_attributes() {
   g_trd_reg = (ev && ev[0] == '0') ? 0 : 1;
   const char* eq = std::getenv("SDP_TRD_QLRSQ");
   g_ql_rsqrt = (eq && eq[0] == '0') ? 0 : 1;
+  const char* eio = std::getenv("SDP_TRD_INVIT_ORDER");
+  g_trd_invit_order = (eio && eio[0] == '1') ? 1 : 0;
   const char* efv = std::getenv("SDP_TRD_FUSEVEC");
   g_trd_fusevec = (efv && efv[0] == '1') ? 1 : 0;
   const char* esp = std::getenv("SDP_TRD_SPLIT");

@@ -889,13 +889,15 @@ def test_trd_fused_eigenvectors_bit_identical_subprocess():
         "np.save(sys.argv[1], out)\n" % (ROOT, os.path.dirname(os.path.abspath(__file__))))
     outs = []
     with tempfile.TemporaryDirectory() as td:
-        for flag in ("1", "0"):
-            f = os.path.join(td, f"o{flag}.npy")
-            env = dict(os.environ, SDP_TRD_FUSEVEC=flag)
+        # default; singletons in the apply kernel; clusters scheduled first (SDP_TRD_INVIT_ORDER=1)
+        for i, extra in enumerate(({}, {"SDP_TRD_FUSEVEC": "1"}, {"SDP_TRD_INVIT_ORDER": "1"})):
+            f = os.path.join(td, f"o{i}.npy")
+            env = dict(os.environ, **extra)
             r = subprocess.run([sys.executable, "-c", code, f], env=env, capture_output=True, text=True, timeout=900)
             assert r.returncode == 0, r.stdout + r.stderr
             outs.append(np.load(f))
     assert np.array_equal(outs[0], outs[1])
+    assert np.array_equal(outs[0], outs[2])
 
 
 # ------------------------------------------------------------------ adaptive rho
